@@ -1,0 +1,236 @@
+"""CPU oracle for the LASNet dynamic residual block -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and bench.py's ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product package
+``paper_2210_06223_b200`` never imports it and shares no code with it.
+
+This module is a thin ctypes binding over ``lasnet_oracle.c`` (fp64, plain loops,
+each function citing the PAPER.md passage it follows).  All tensors cross the
+boundary as C-contiguous float64 numpy arrays holding the *exact* values of the
+bf16/fp32 tensors the GPU sees (bf16 -> fp64 is exact).
+
+Parity status per function:
+  masker_2ch, masker, upsample, compact, static_block, dyn_block_def,
+  dyn_block_literal, block_pixel, round_bf16 -- all pinned by tests in
+  tests/test_oracle_pins.py (library conv2d in fp64, exact rationals, closed
+  forms, brute force, textbook routines).  No function is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "lasnet_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+ROUND_NONE, ROUND_F32, ROUND_BF16 = 0, 1, 2
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle shared library with gcc (-O2, OpenMP over patches)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-std=c99", "-fopenmp", "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"]
+        subprocess.run(cmd, check=True)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        _lib = ctypes.CDLL(_LIB)
+        D = ctypes.POINTER(ctypes.c_double)
+        U8 = ctypes.POINTER(ctypes.c_uint8)
+        I32 = ctypes.POINTER(ctypes.c_int32)
+        i = ctypes.c_int
+        _lib.oracle_round_bf16.restype = ctypes.c_double
+        _lib.oracle_round_bf16.argtypes = [ctypes.c_double]
+        _lib.oracle_round_f32.restype = ctypes.c_double
+        _lib.oracle_round_f32.argtypes = [ctypes.c_double]
+        _lib.oracle_masker_2ch.argtypes = [D, i, i, i, i, i, D, D, U8, D, D]
+        _lib.oracle_masker.argtypes = [D, i, i, i, i, i, D, ctypes.c_double, U8, D]
+        _lib.oracle_upsample.argtypes = [U8, i, i, i, i, U8]
+        _lib.oracle_compact.restype = ctypes.c_int
+        _lib.oracle_compact.argtypes = [U8, i, I32]
+        _lib.oracle_static_block.argtypes = [D, i, i, i, i, i, i, D, D, D, D, D, D, i, D, D, D]
+        _lib.oracle_dyn_block_def.argtypes = [D, i, i, i, i, i, i, D, D, D, D, D, D, U8, i, i, D]
+        _lib.oracle_dyn_block_literal.argtypes = [D, i, i, i, i, i, i, D, D, D, D, D, D, I32, i, i, i, D]
+        _lib.oracle_block_pixel.restype = ctypes.c_int
+        _lib.oracle_block_pixel.argtypes = [D, i, i, i, i, i, D, D, D, D, D, D, U8, i, i, i, i, i, D]
+        _lib.oracle_num_threads.restype = ctypes.c_int
+        _lib.oracle_set_threads.argtypes = [i]
+    return _lib
+
+
+def _d(a):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _u8(a):
+    a = np.ascontiguousarray(a, dtype=np.uint8)
+    return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))
+
+
+def _i32(a):
+    a = np.ascontiguousarray(a, dtype=np.int32)
+    return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+def grid(h: int, w: int, s: int):
+    """Cell grid of the coarse mask (R7: ceil, clipped edge patches)."""
+    return -(-h // s), -(-w // s)
+
+
+def round_bf16(v: float) -> float:
+    return _load().oracle_round_bf16(float(v))
+
+
+def round_f32(v: float) -> float:
+    return _load().oracle_round_f32(float(v))
+
+
+def masker_2ch(x, Wm, bm, s):
+    """Paper-form masker: avgpool -> 1x1 conv (2 ch) -> argmax."""
+    lib = _load()
+    x, xp = _d(x)
+    n, h, w, c = x.shape
+    gh, gw = grid(h, w, s)
+    Wm, wp = _d(Wm)
+    bm, bp = _d(bm)
+    mask = np.zeros((n, gh, gw), np.uint8)
+    z0 = np.zeros((n, gh, gw))
+    z1 = np.zeros((n, gh, gw))
+    _, mp = _u8(mask)
+    _, z0p = _d(z0)
+    _, z1p = _d(z1)
+    lib.oracle_masker_2ch(xp, n, h, w, c, s, wp, bp, mp, z0p, z1p)
+    return mask, z0, z1
+
+
+def masker(x, wm, bm, s):
+    """Reduced masker (App. B): logit = w . avgpool(x) + b, mask = logit > 0."""
+    lib = _load()
+    x, xp = _d(x)
+    n, h, w, c = x.shape
+    gh, gw = grid(h, w, s)
+    wm, wp = _d(wm)
+    mask = np.zeros((n, gh, gw), np.uint8)
+    logit = np.zeros((n, gh, gw))
+    _, mp = _u8(mask)
+    _, lp = _d(logit)
+    lib.oracle_masker(xp, n, h, w, c, s, wp, float(bm), mp, lp)
+    return mask, logit
+
+
+def upsample(mask_cells, h, w, s):
+    lib = _load()
+    mc, mcp = _u8(mask_cells)
+    n = mc.shape[0]
+    m = np.zeros((n, h, w), np.uint8)
+    _, mp = _u8(m)
+    lib.oracle_upsample(mcp, n, h, w, s, mp)
+    return m
+
+
+def compact(mask_cells):
+    lib = _load()
+    m, mp = _u8(np.asarray(mask_cells).reshape(-1))
+    idx = np.zeros(max(m.size, 1), np.int32)
+    _, ip = _i32(idx)
+    count = lib.oracle_compact(mp, m.size, ip)
+    return idx[:count].copy(), count
+
+
+def _weights(wts):
+    out = []
+    keep = []
+    for k in ("w1", "b1", "w2", "b2", "w3", "b3"):
+        a, p = _d(wts[k])
+        keep.append(a)
+        out.append(p)
+    return keep, out
+
+
+def static_block(x, wts, rmode=ROUND_BF16, return_intermediates=False):
+    """Dense bottleneck: h1, h2 with zero padding, y = ReLU(x + conv3(h2))."""
+    lib = _load()
+    x, xp = _d(x)
+    n, h, w, c_in = x.shape
+    c_mid = wts["w1"].shape[0]
+    c_out = wts["w3"].shape[0]
+    keep, wp = _weights(wts)
+    y = np.zeros((n, h, w, c_out))
+    h1 = np.zeros((n, h, w, c_mid))
+    h2 = np.zeros((n, h, w, c_mid))
+    _, yp = _d(y)
+    _, h1p = _d(h1)
+    _, h2p = _d(h2)
+    lib.oracle_static_block(xp, n, h, w, c_in, c_mid, c_out, *wp, rmode, yp, h1p, h2p)
+    if return_intermediates:
+        return y, h1, h2
+    return y
+
+
+def dyn_block_def(x, wts, mask_cells, s, rmode=ROUND_BF16):
+    """Definition mode: y = M ? static_block(x) : x."""
+    lib = _load()
+    x, xp = _d(x)
+    n, h, w, c_in = x.shape
+    c_mid = wts["w1"].shape[0]
+    c_out = wts["w3"].shape[0]
+    keep, wp = _weights(wts)
+    mc, mcp = _u8(mask_cells)
+    y = np.zeros((n, h, w, c_out))
+    _, yp = _d(y)
+    lib.oracle_dyn_block_def(xp, n, h, w, c_in, c_mid, c_out, *wp, mcp, s, rmode, yp)
+    return y
+
+
+def dyn_block_literal(x, wts, idx, s, rmode=ROUND_BF16, threads: int | None = None):
+    """Literal mode: gather halo -> conv1 -> conv2 -> conv3 + residual -> scatter."""
+    lib = _load()
+    if threads is not None:
+        lib.oracle_set_threads(int(threads))
+    x, xp = _d(x)
+    n, h, w, c_in = x.shape
+    c_mid = wts["w1"].shape[0]
+    c_out = wts["w3"].shape[0]
+    keep, wp = _weights(wts)
+    idx = np.asarray(idx, dtype=np.int32).reshape(-1)
+    count = int(idx.size)
+    idx, ip = _i32(idx if count else np.zeros(1, np.int32))
+    y = np.zeros((n, h, w, c_out))
+    _, yp = _d(y)
+    lib.oracle_dyn_block_literal(xp, n, h, w, c_in, c_mid, c_out, *wp, ip, count, s, rmode, yp)
+    return y
+
+
+def block_pixel(x, wts, mask_cells, s, n, yy, xx, rmode=ROUND_BF16):
+    """One output pixel of the block computed on its own (sampled full-size checks)."""
+    lib = _load()
+    x, xp = _d(x)
+    _, h, w, c_in = x.shape
+    c_mid = wts["w1"].shape[0]
+    c_out = wts["w3"].shape[0]
+    keep, wp = _weights(wts)
+    mc, mcp = _u8(mask_cells)
+    out = np.zeros(c_out)
+    _, op = _d(out)
+    active = lib.oracle_block_pixel(xp, h, w, c_in, c_mid, c_out, *wp, mcp, s, rmode,
+                                    int(n), int(yy), int(xx), op)
+    return out, bool(active)
+
+
+def num_threads() -> int:
+    return _load().oracle_num_threads()
+
+
+def set_threads(t: int) -> None:
+    _load().oracle_set_threads(int(t))

@@ -1,0 +1,109 @@
+"""Seeded synthetic inputs shared by the oracle side and the CUDA side.
+
+This module holds NONE of the method's arithmetic: it only draws random
+tensors and random cell masks.  Both the tests
+(oracle vs CUDA parity) and bench.py draw their inputs from here, so the two
+sides see the same bytes.
+
+Recipe (SURVEY.md 8(d) / DESIGN.md):
+  x      = ReLU(N(0,1)) stored NHWC, bf16 (or fp32 for config 1)   -- post-ReLU block input
+  W1, W2 = He-normal (std sqrt(2/fan_in)); W3 = He-normal * 0.1 (gamma = 0.1)
+  b1..b3 = N(0, 0.05^2), fp32 (BN folded)
+  wm     = N(0, 1/c_in) fp32  -- reduced masker weight W_0 - W_1
+  cell masks: exactly k = floor(r*G + 0.5) active cells per image from a seeded
+  permutation (uniform family) or the top-k of 3x3-box-smoothed noise
+  (clustered family; real masks follow objects).
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+
+def _gen(seed: int) -> torch.Generator:
+    g = torch.Generator(device="cpu")
+    g.manual_seed(int(seed))
+    return g
+
+
+def _dt(dtype: str):
+    return {"bf16": torch.bfloat16, "f32": torch.float32}[dtype]
+
+
+def make_x(n: int, h: int, w: int, c: int, seed: int = 0, dtype: str = "bf16",
+           relu: bool = True) -> torch.Tensor:
+    """Block input, NHWC, on the CPU. relu=False gives signed inputs (R5 pin)."""
+    t = torch.randn((n, h, w, c), generator=_gen(seed), dtype=torch.float32)
+    if relu:
+        t = torch.clamp_min(t, 0.0)
+    return t.to(_dt(dtype)).contiguous()
+
+
+def make_block_weights(c_in: int, c_mid: int, c_out: int, seed: int = 1,
+                       dtype: str = "bf16", w3_gamma: float = 0.1,
+                       bias_std: float = 0.05) -> dict:
+    """BN-folded bottleneck weights: w1 [c_mid][c_in], w2 [c_mid][3][3][c_mid] (OHWI),
+    w3 [c_out][c_mid]; biases fp32."""
+    g = _gen(seed)
+    w1 = torch.randn((c_mid, c_in), generator=g) * (2.0 / c_in) ** 0.5
+    w2 = torch.randn((c_mid, 3, 3, c_mid), generator=g) * (2.0 / (9 * c_mid)) ** 0.5
+    w3 = torch.randn((c_out, c_mid), generator=g) * (2.0 / c_mid) ** 0.5 * w3_gamma
+    b1 = torch.randn((c_mid,), generator=g) * bias_std
+    b2 = torch.randn((c_mid,), generator=g) * bias_std
+    b3 = torch.randn((c_out,), generator=g) * bias_std
+    dt = _dt(dtype)
+    return {
+        "w1": w1.to(dt).contiguous(), "b1": b1.float().contiguous(),
+        "w2": w2.to(dt).contiguous(), "b2": b2.float().contiguous(),
+        "w3": w3.to(dt).contiguous(), "b3": b3.float().contiguous(),
+    }
+
+
+def make_masker_weights(c_in: int, seed: int = 3) -> torch.Tensor:
+    """Reduced masker weight w = W_0 - W_1, fp32 [c_in]."""
+    return (torch.randn((c_in,), generator=_gen(seed)) * (1.0 / c_in) ** 0.5).float().contiguous()
+
+
+def make_masker_weights_2ch(c_in: int, seed: int = 3):
+    """Two-channel masker weights W [2][c_in] and bias [2] (paper form)."""
+    g = _gen(seed)
+    W = (torch.randn((2, c_in), generator=g) * (1.0 / c_in) ** 0.5).float()
+    b = (torch.randn((2,), generator=g) * 0.05).float()
+    return W.contiguous(), b.contiguous()
+
+
+def active_cells(r: float, cells: int) -> int:
+    """k = floor(r*G + 0.5) (R16)."""
+    return int(np.floor(r * cells + 0.5))
+
+
+def make_cell_mask(n: int, gh: int, gw: int, r: float, seed: int = 2,
+                   family: str = "uniform") -> np.ndarray:
+    """uint8 [n][gh][gw] with exactly active_cells(r, gh*gw) ones per image."""
+    rng = np.random.default_rng(int(seed))
+    G = gh * gw
+    k = active_cells(r, G)
+    m = np.zeros((n, G), np.uint8)
+    for i in range(n):
+        if family == "uniform":
+            sel = rng.permutation(G)[:k]
+        elif family == "clustered":
+            noise = rng.standard_normal((gh + 2, gw + 2))
+            sm = np.zeros((gh, gw))
+            for dy in range(3):
+                for dx in range(3):
+                    sm += noise[dy:dy + gh, dx:dx + gw]
+            sel = np.argsort(-sm.reshape(-1), kind="stable")[:k]
+        else:
+            raise ValueError(family)
+        m[i, sel] = 1
+    return m.reshape(n, gh, gw)
+
+
+def to_f64(t: torch.Tensor) -> np.ndarray:
+    """Exact float64 copy of a bf16/fp32 tensor (for the oracle)."""
+    return t.detach().to("cpu").to(torch.float64).numpy()
+
+
+def weights_f64(wts: dict) -> dict:
+    return {k: to_f64(v) for k, v in wts.items()}

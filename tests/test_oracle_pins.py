@@ -1,0 +1,347 @@
+"""Pins for the CPU oracle against things other than itself (-m "not gpu").
+
+Each test names what fixes the expected value: a library routine
+(torch.nn.functional.conv2d in float64, numpy.flatnonzero, numpy.kron),
+exact rational arithmetic (fractions.Fraction), closed forms, a bit-level
+second implementation of bf16 rounding pinned by torch's fp32->bf16 cast,
+or brute force written here in plain Python loops.
+"""
+from fractions import Fraction
+import itertools
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+import synth
+
+
+# ---------------------------------------------------------------- helpers ----
+
+def bf16_rne_bits(a: np.ndarray) -> np.ndarray:
+    """Second, bit-level implementation of fp64 -> bf16 round-to-nearest-even
+    (keep 7 of the 52 fp64 fraction bits; ties to even), normal range only."""
+    a = np.asarray(a, np.float64)
+    bits = a.view(np.uint64).copy()
+    drop = np.uint64(52 - 7)
+    lsb = (bits >> drop) & np.uint64(1)
+    half = np.uint64(1) << (drop - np.uint64(1))
+    bits = bits + half - np.uint64(1) + lsb
+    bits &= ~((np.uint64(1) << drop) - np.uint64(1))
+    out = bits.view(np.float64)
+    return np.where(a == 0, a, out)
+
+
+def torch_static_block(x, wts, rnd=None):
+    """Static bottleneck with torch float64 conv2d (library routine)."""
+    r = (lambda t: t) if rnd is None else rnd
+    xt = torch.from_numpy(x).permute(0, 3, 1, 2)  # NCHW
+    w1 = torch.from_numpy(wts["w1"])[:, :, None, None]
+    w2 = torch.from_numpy(wts["w2"]).permute(0, 3, 1, 2)  # OHWI -> OIHW
+    w3 = torch.from_numpy(wts["w3"])[:, :, None, None]
+    h1 = r(torch.relu(F.conv2d(xt, w1, torch.from_numpy(wts["b1"]))))
+    h2 = r(torch.relu(F.conv2d(h1, w2, torch.from_numpy(wts["b2"]), padding=1)))
+    y = r(torch.relu(xt + F.conv2d(h2, w3, torch.from_numpy(wts["b3"]))))
+    return y.permute(0, 2, 3, 1).contiguous().numpy(), h1.permute(0, 2, 3, 1).numpy(), h2.permute(0, 2, 3, 1).numpy()
+
+
+def tiny_case(n, h, w, c_in, c_mid, seed, dtype="bf16", relu=True):
+    x = synth.to_f64(synth.make_x(n, h, w, c_in, seed=seed, dtype=dtype, relu=relu))
+    wts = synth.weights_f64(synth.make_block_weights(c_in, c_mid, c_in, seed=seed + 100, dtype=dtype))
+    return x, wts
+
+
+# ------------------------------------------------------------ rounding -------
+
+def test_round_bf16_matches_torch_cast_on_fp32_values(oracle_mod):
+    g = torch.Generator().manual_seed(0)
+    v = torch.randn(4000, generator=g) * torch.exp2(torch.randint(-30, 30, (4000,), generator=g).float())
+    want = v.to(torch.bfloat16).to(torch.float64).numpy()
+    got = np.array([oracle_mod.round_bf16(float(t)) for t in v.to(torch.float64)])
+    assert np.array_equal(got, want)
+
+
+def test_round_bf16_ties_and_subnormals(oracle_mod):
+    r = oracle_mod.round_bf16
+    assert r(1 + 2 ** -8) == 1.0                      # tie -> even (down)
+    assert r(1 + 3 * 2 ** -8) == 1 + 2 ** -6           # tie -> even (up)
+    assert r(-(1 + 3 * 2 ** -8)) == -(1 + 2 ** -6)
+    assert r(2 ** -134) == 0.0                         # subnormal tie -> even (0)
+    assert r(3 * 2 ** -134) == 2 ** -132               # subnormal tie -> even
+    assert r(1e-300) == 0.0
+    assert r(3.0e38) == 226 * 2.0 ** 120          # finite: 1.765625 * 2^127
+    assert r(3.4e38) == float("inf")            # above the RNE overflow threshold
+    assert oracle_mod.round_f32(1 + 2 ** -30) == 1.0
+
+
+def test_bitlevel_rne_helper_agrees_with_torch():
+    g = torch.Generator().manual_seed(1)
+    v = torch.randn(5000, generator=g, dtype=torch.float32)
+    assert np.array_equal(bf16_rne_bits(v.double().numpy()), v.to(torch.bfloat16).double().numpy())
+
+
+# --------------------------------------------------------------- masker ------
+
+@pytest.mark.parametrize("h,w,s", [(4, 4, 2), (5, 5, 2), (7, 5, 3), (4, 6, 1), (5, 7, 4)])
+def test_masker_exact_rational_sign(oracle_mod, h, w, s):
+    """logit = sum_c w_c * mean_{p in Omega} x_pc + b computed exactly with Fractions
+    (P:109 pooling + 1x1 conv; R1 average; R7 clipped Omega; R3 strict >)."""
+    c = 8
+    x = synth.to_f64(synth.make_x(2, h, w, c, seed=h * 31 + w, relu=False))
+    wm = synth.make_masker_weights(c, seed=7).double().numpy()
+    b = 0.01
+    mask, logit = oracle_mod.masker(x, wm, b, s)
+    gh, gw = -(-h // s), -(-w // s)
+    for n in range(2):
+        for gy in range(gh):
+            for gx in range(gw):
+                pix = [(yy, xx) for yy in range(gy * s, min(gy * s + s, h)) for xx in range(gx * s, min(gx * s + s, w))]
+                exact = Fraction(b)
+                for ci in range(c):
+                    tot = sum(Fraction(x[n, yy, xx, ci]) for yy, xx in pix)
+                    exact += Fraction(wm[ci]) * tot / len(pix)
+                assert mask[n, gy, gx] == (1 if exact > 0 else 0)
+                assert abs(Fraction(logit[n, gy, gx]) - exact) <= Fraction(1, 10 ** 12) * (1 + abs(exact))
+
+
+def test_masker_two_channel_argmax_equals_reduced_sign(oracle_mod):
+    """App. B eq.: [x*W]_0 > [x*W]_1  <=>  x*(W_0-W_1) > 0, at >= 1000 cells."""
+    c = 32
+    x = synth.to_f64(synth.make_x(4, 16, 16, c, seed=11))
+    W, bb = synth.make_masker_weights_2ch(c, seed=12)
+    W = W.double().numpy()
+    bb = bb.double().numpy()
+    m2, z0, z1 = oracle_mod.masker_2ch(x, W, bb, 1)
+    m1, l1 = oracle_mod.masker(x, W[0] - W[1], bb[0] - bb[1], 1)
+    assert m2.size >= 1000
+    sure = np.abs(z0 - z1) > 1e-12
+    assert sure.sum() >= 1000
+    assert np.array_equal(m2[sure], m1[sure])
+    np.testing.assert_allclose(l1, z0 - z1, rtol=0, atol=1e-12)
+
+
+def test_masker_s1_is_per_pixel_matvec(oracle_mod):
+    """S = 1: pooling is the identity, logit = x . w + b (numpy matmul)."""
+    c = 16
+    x = synth.to_f64(synth.make_x(2, 5, 6, c, seed=5, relu=False))
+    wm = synth.make_masker_weights(c, seed=6).double().numpy()
+    mask, logit = oracle_mod.masker(x, wm, -0.02, 1)
+    np.testing.assert_allclose(logit, x @ wm - 0.02, rtol=0, atol=1e-13)
+    assert np.array_equal(mask, (x @ wm - 0.02 > 0).astype(np.uint8))
+
+
+def test_masker_constant_input_closed_form(oracle_mod):
+    """x == a everywhere: logit = a * sum(w) + b for every cell, clipped or not."""
+    c = 16
+    a = 0.75
+    x = np.full((1, 7, 9, c), a)
+    wm = synth.make_masker_weights(c, seed=9).double().numpy()
+    mask, logit = oracle_mod.masker(x, wm, 0.125, 4)
+    np.testing.assert_allclose(logit, a * wm.sum() + 0.125, rtol=1e-14, atol=1e-15)
+    assert logit.shape == (1, 2, 3)
+
+
+def test_masker_tie_is_inactive(oracle_mod):
+    """R3: logit exactly 0 -> not selected (strict >)."""
+    x = np.zeros((1, 4, 4, 16))
+    mask, logit = oracle_mod.masker(x, np.ones(16), 0.0, 2)
+    assert np.all(logit == 0) and np.all(mask == 0)
+
+
+# ----------------------------------------------------- compaction, upsample --
+
+@pytest.mark.parametrize("r", [0.0, 0.1, 0.5, 1.0])
+def test_compact_equals_flatnonzero(oracle_mod, r):
+    m = synth.make_cell_mask(3, 7, 9, r, seed=4)
+    idx, count = oracle_mod.compact(m)
+    ref = np.flatnonzero(m.reshape(-1))
+    assert count == int(m.sum()) == len(ref)
+    assert np.array_equal(idx, ref)
+    assert np.all(np.diff(idx) > 0)
+
+
+def test_upsample_matches_kron_and_preserves_rate(oracle_mod):
+    m = synth.make_cell_mask(2, 7, 7, 0.5, seed=8)
+    for s in (1, 2, 4):
+        up = oracle_mod.upsample(m, 7 * s, 7 * s, s)
+        ref = np.stack([np.kron(m[i], np.ones((s, s), np.uint8)) for i in range(2)])
+        assert np.array_equal(up, ref)
+        assert Fraction(int(up.sum()), up.size) == Fraction(int(m.sum()), m.size)
+
+
+# ---------------------------------------------------------- static block -----
+
+@pytest.mark.parametrize("n,h,w,c_in,c_mid", [(1, 5, 7, 32, 16), (2, 8, 8, 64, 16), (1, 4, 4, 16, 8)])
+def test_static_block_matches_torch_conv2d_fp64(oracle_mod, n, h, w, c_in, c_mid):
+    x, wts = tiny_case(n, h, w, c_in, c_mid, seed=h + w)
+    y, h1, h2 = oracle_mod.static_block(x, wts, rmode=oracle_mod.ROUND_NONE, return_intermediates=True)
+    yt, h1t, h2t = torch_static_block(x, wts)
+    np.testing.assert_allclose(h1, h1t, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(h2, h2t, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(y, yt, rtol=0, atol=1e-12)
+
+
+def test_static_block_bf16_storage_rounding(oracle_mod):
+    """bf16 RNE at h1/h2/y (R13) vs torch fp64 conv2d + bit-level RNE."""
+    x, wts = tiny_case(2, 6, 7, 32, 16, seed=21)
+    y = oracle_mod.static_block(x, wts, rmode=oracle_mod.ROUND_BF16)
+    rnd = lambda t: torch.from_numpy(bf16_rne_bits(t.numpy()))
+    yt, _, _ = torch_static_block(x, wts, rnd=rnd)
+    assert np.mean(y == yt) > 0.999
+    ulp = np.abs(yt) * 2.0 ** -7 + 1e-30
+    assert np.all(np.abs(y - yt) <= ulp)
+
+
+def test_static_block_fp32_storage_rounding(oracle_mod):
+    x, wts = tiny_case(1, 5, 5, 16, 16, seed=22, dtype="f32")
+    y = oracle_mod.static_block(x, wts, rmode=oracle_mod.ROUND_F32)
+    rnd = lambda t: t.float().double()
+    yt, _, _ = torch_static_block(x, wts, rnd=rnd)
+    np.testing.assert_allclose(y, yt, rtol=1e-7, atol=1e-12)
+
+
+# ------------------------------------------------------------- dyn block -----
+
+SHAPES = [(1, 4, 4, 32, 16, 2), (2, 5, 5, 32, 16, 2), (1, 7, 7, 32, 16, 4), (1, 8, 8, 64, 32, 3),
+          (2, 7, 5, 32, 16, 1), (1, 8, 8, 32, 16, 8), (1, 5, 8, 16, 16, 7)]
+
+
+@pytest.mark.parametrize("n,h,w,c_in,c_mid,s", SHAPES)
+def test_literal_equals_definition(oracle_mod, n, h, w, c_in, c_mid, s):
+    """Gather/compute/scatter reaches the definition y = M ? static : x exactly."""
+    x, wts = tiny_case(n, h, w, c_in, c_mid, seed=s * 7 + h)
+    gh, gw = -(-h // s), -(-w // s)
+    for r in (0.3, 0.7):
+        mc = synth.make_cell_mask(n, gh, gw, r, seed=3)
+        idx, _ = oracle_mod.compact(mc)
+        y_lit = oracle_mod.dyn_block_literal(x, wts, idx, s)
+        y_def = oracle_mod.dyn_block_def(x, wts, mc, s)
+        assert np.array_equal(y_lit, y_def)
+
+
+@pytest.mark.parametrize("n,h,w,c_in,c_mid,s", SHAPES[:4])
+def test_all_zero_mask_is_identity_and_all_one_is_static(oracle_mod, n, h, w, c_in, c_mid, s):
+    x, wts = tiny_case(n, h, w, c_in, c_mid, seed=5)
+    gh, gw = -(-h // s), -(-w // s)
+    zeros = np.zeros((n, gh, gw), np.uint8)
+    ones = np.ones((n, gh, gw), np.uint8)
+    assert np.array_equal(oracle_mod.dyn_block_literal(x, wts, [], s), x)
+    idx, _ = oracle_mod.compact(ones)
+    assert np.array_equal(oracle_mod.dyn_block_literal(x, wts, idx, s),
+                          oracle_mod.static_block(x, wts))
+    assert np.array_equal(oracle_mod.dyn_block_def(x, wts, zeros, s), x)
+
+
+@pytest.mark.parametrize("s", [2, 3, 4])
+def test_granularity_equivalence_to_pixel_level(oracle_mod, s):
+    """dyn(x, Mc, S) == dyn(x, upsample(Mc, S), 1): S = 1 is pixel-level DynConv."""
+    n, h, w = 2, 8, 7
+    x, wts = tiny_case(n, h, w, 32, 16, seed=40 + s)
+    gh, gw = -(-h // s), -(-w // s)
+    mc = synth.make_cell_mask(n, gh, gw, 0.5, seed=s)
+    idx, _ = oracle_mod.compact(mc)
+    up = oracle_mod.upsample(mc, h, w, s)
+    idx1, _ = oracle_mod.compact(up)
+    assert np.array_equal(oracle_mod.dyn_block_literal(x, wts, idx, s),
+                          oracle_mod.dyn_block_literal(x, wts, idx1, 1))
+
+
+def test_closed_form_w3_zero(oracle_mod):
+    """W3 = 0, b3 = 0 -> y = ReLU(x) on active pixels, x elsewhere."""
+    x, wts = tiny_case(1, 6, 6, 32, 16, seed=50, relu=False)
+    wts["w3"][:] = 0
+    wts["b3"][:] = 0
+    mc = synth.make_cell_mask(1, 3, 3, 0.5, seed=1)
+    y = oracle_mod.dyn_block_literal(x, wts, oracle_mod.compact(mc)[0], 2)
+    up = np.kron(mc[0], np.ones((2, 2), np.uint8)).astype(bool)
+    assert np.array_equal(y[0][up], np.maximum(x[0][up], 0))
+    assert np.array_equal(y[0][~up], x[0][~up])
+
+
+def test_closed_form_w1_zero(oracle_mod):
+    """W1 = 0, b1 = 0 -> h1 = 0, h2 = round(ReLU(b2)), y = round(ReLU(x + W3 h2 + b3))."""
+    x, wts = tiny_case(1, 5, 5, 32, 16, seed=51)
+    wts["w1"][:] = 0
+    wts["b1"][:] = 0
+    h2 = bf16_rne_bits(np.maximum(wts["b2"], 0))
+    z = wts["w3"] @ h2 + wts["b3"]
+    y = oracle_mod.static_block(x, wts)
+    want = bf16_rne_bits(np.maximum(x + z, 0))
+    assert np.array_equal(y, want)
+
+
+def test_single_cell_covering_image_is_static_block(oracle_mod):
+    """S = H = W, the single cell active -> the whole-image static block (P:109 extreme)."""
+    x, wts = tiny_case(1, 6, 6, 32, 16, seed=52)
+    y = oracle_mod.dyn_block_literal(x, wts, [0], 6)
+    assert np.array_equal(y, oracle_mod.static_block(x, wts))
+
+
+def test_block_pixel_matches_definition(oracle_mod):
+    x, wts = tiny_case(2, 7, 9, 32, 16, seed=53)
+    mc = synth.make_cell_mask(2, 4, 5, 0.5, seed=9)
+    y = oracle_mod.dyn_block_def(x, wts, mc, 2)
+    rng = np.random.default_rng(0)
+    for _ in range(25):
+        n, yy, xx = rng.integers(2), rng.integers(7), rng.integers(9)
+        out, act = oracle_mod.block_pixel(x, wts, mc, 2, n, yy, xx)
+        assert np.array_equal(out, y[n, yy, xx])
+        assert act == bool(mc[n, yy // 2, xx // 2])
+
+
+# ----------------------------------------------------------- brute force -----
+
+def _brute_block(x, wts, mc, s):
+    """Whole block in plain Python loops straight from P:86/P:89 (tiny sizes only)."""
+    n_img, h, w, c_in = x.shape
+    c_mid = wts["w1"].shape[0]
+    W1, b1, W2, b2, W3, b3 = (wts[k] for k in ("w1", "b1", "w2", "b2", "w3", "b3"))
+    rnd = lambda v: float(bf16_rne_bits(np.array([v]))[0])
+    h1 = {}
+    for n in range(n_img):
+        for yy in range(h):
+            for xx in range(w):
+                for c in range(c_mid):
+                    a = float(b1[c])
+                    for ci in range(c_in):
+                        a += float(W1[c, ci]) * float(x[n, yy, xx, ci])
+                    h1[n, yy, xx, c] = rnd(max(a, 0.0))
+    y = x.copy()
+    for n in range(n_img):
+        for yy in range(h):
+            for xx in range(w):
+                if not mc[n, yy // s, xx // s]:
+                    continue
+                h2 = []
+                for c in range(c_mid):
+                    a = float(b2[c])
+                    for dy in range(3):
+                        for dx in range(3):
+                            sy, sx = yy + dy - 1, xx + dx - 1
+                            if 0 <= sy < h and 0 <= sx < w:
+                                for ci in range(c_mid):
+                                    a += float(W2[c, dy, dx, ci]) * h1[n, sy, sx, ci]
+                    h2.append(rnd(max(a, 0.0)))
+                for co in range(c_in):
+                    a = float(b3[co])
+                    for c in range(c_mid):
+                        a += float(W3[co, c]) * h2[c]
+                    y[n, yy, xx, co] = rnd(max(float(x[n, yy, xx, co]) + a, 0.0))
+    return y
+
+
+@pytest.mark.parametrize("h,w,s", [(4, 4, 2), (5, 4, 3)])
+def test_brute_force_exhaustive_masks(oracle_mod, h, w, s):
+    """Every coarse mask of a G <= 4 grid, compared with plain-Python loops."""
+    x, wts = tiny_case(1, h, w, 8, 4, seed=60 + h)
+    gh, gw = -(-h // s), -(-w // s)
+    G = gh * gw
+    assert G <= 4
+    for bits in itertools.product([0, 1], repeat=G):
+        mc = np.array(bits, np.uint8).reshape(1, gh, gw)
+        idx, _ = oracle_mod.compact(mc)
+        got = oracle_mod.dyn_block_literal(x, wts, idx, s)
+        want = _brute_block(x, wts, mc, s)
+        assert np.allclose(got, want, rtol=0, atol=np.abs(want).max() * 2 ** -7)
+        assert np.mean(got == want) > 0.99
