@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""bench.py -- LASNet coarse-grained spatially-dynamic residual block on B200.
+
+Workload (BASELINE.json configs[1]): ResNet-50 stage-3
+identity bottleneck (He et al. conv3_x; LASNet stage 2), N = 128 images per GPU,
+28x28x512 NHWC bf16, c_mid = 128, granularity S = 4, activation rate r ~ 0.5
+(masker bias calibrated on a separate batch), synthetic seeded inputs, random-
+init weights.  A step = one pass of the whole hot path (masker -> compaction ->
+gather+conv1 -> conv2 -> conv3+scatter-add) over the batch, in place.
+
+Timing: W warm-up steps, then exactly K timed steps bracketed by barrier +
+synchronize; CUDA events on the launching stream around every step; before
+each step (untimed) the input is restored and L2 is flushed by writing a
+256 MiB buffer (x is 103 MB < 126 MB L2).  Multi-GPU (torchrun): weak scaling,
+each rank its own 128 images, no data-path collective; max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lasnet|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "LASNet-R101 images/s & dyn-block latency vs activation rate (1/2/4/8 B200)"
+WORKLOAD = dict(n=128, h=28, w=28, c_in=512, c_mid=128, s=4, r=0.5)
+WORKLOAD_NAME = "resnet50-stage3 identity dyn-block (BASELINE configs[1]) N=128/GPU 28x28x512 c_mid=128 S=4 r=0.5"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="lasnet", choices=["lasnet", "reference"])
+    ap.add_argument("--s", type=int, default=WORKLOAD["s"])
+    ap.add_argument("--r", type=float, default=WORKLOAD["r"])
+    ap.add_argument("--n", type=int, default=WORKLOAD["n"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
+    ap.add_argument("--detail", default=None, help="write per-kernel detail JSON here")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# --------------------------------------------------------------- clocks ----
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,utilization.gpu,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 10:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        load = [r for r in rows if r[4] not in ("0", "[N/A]")] or rows
+        sm = [float(r[1]) for r in load if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in load:
+            for nm, v in zip(names, r[6:10]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": sorted(reasons), "samples": len(rows), "samples_under_load": len(load)}
+
+
+# ------------------------------------------------------ algorithmic work ----
+
+def algorithmic_work(mask_cells: np.ndarray, n, h, w, c_in, c_mid, c_out, s):
+    """Per-kernel algorithmic bytes and FLOPs for the concrete mask (DESIGN.md
+    "Roofline accounting"; SURVEY 8(d) per-unit figures)."""
+    gh, gw = -(-h // s), -(-w // s)
+    ids = np.flatnonzero(mask_cells.reshape(-1))
+    P = len(ids)
+    g = ids % (gh * gw)
+    gy, gx = g // gw, g % gw
+    # in-image halo pixels of each active patch: (S+2)^2 window at (gy*S-1, gx*S-1)
+    y0, x0 = gy * s - 1, gx * s - 1
+    hy = np.minimum(y0 + s + 2, h) - np.maximum(y0, 0)
+    hx = np.minimum(x0 + s + 2, w) - np.maximum(x0, 0)
+    halo_px = int(np.sum(hy * hx))
+    oy = np.minimum(gy * s + s, h) - gy * s
+    ox = np.minimum(gx * s + s, w) - gx * s
+    out_px = int(np.sum(oy * ox))
+    e = 2
+    hs2, ss = (s + 2) ** 2, s * s
+    W1, W2, W3 = c_mid * c_in * e, 9 * c_mid * c_mid * e, c_out * c_mid * e
+    k = {
+        "mask_compact": dict(bytes=n * h * w * c_in * e + n * gh * gw + 4 * P + 4, flops=2 * n * h * w * c_in),
+        "conv1": dict(bytes=halo_px * c_in * e + P * hs2 * c_mid * e + W1, flops=2 * halo_px * c_in * c_mid),
+        "conv2": dict(bytes=P * hs2 * c_mid * e + P * ss * c_mid * e + W2, flops=2 * out_px * 9 * c_mid * c_mid),
+        "conv3": dict(bytes=P * ss * c_mid * e + 2 * out_px * c_out * e + W3, flops=2 * out_px * c_mid * c_out),
+    }
+    block = dict(
+        bytes=n * h * w * c_in * e + n * gh * gw + 4 * P + halo_px * c_in * e + 2 * out_px * c_out * e + W1 + W2 + W3,
+        flops=k["conv1"]["flops"] + k["conv2"]["flops"] + k["conv3"]["flops"])
+    dense = dict(bytes=2 * n * h * w * c_in * e + W1 + W2 + W3,
+                 flops=2 * n * h * w * (c_in * c_mid + 9 * c_mid * c_mid + c_mid * c_out))
+    return k, block, dense, dict(P=P, halo_px=halo_px, out_px=out_px, r_patch=P / (n * gh * gw),
+                                 r_pixel=out_px / (n * h * w))
+
+
+def roofline_entry(work, ms, hbm, tfl):
+    t_hbm = work["bytes"] / (hbm * 1e9)
+    t_tc = work["flops"] / (tfl * 1e12)
+    if t_hbm >= t_tc:
+        ach = work["bytes"] / (ms * 1e-3) / 1e9
+        return {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4)}
+    ach = work["flops"] / (ms * 1e-3) / 1e12
+    return {"bound": "tensor", "achieved": round(ach, 1), "peak": tfl, "unit": "TFLOP/s", "frac": round(ach / tfl, 4)}
+
+
+# ------------------------------------------------------------ cpu oracle ----
+
+def oracle_sample(x_cpu, wts_cpu, wm_cpu, bm, s, k_images, threads):
+    """The oracle as it stands, run on the first k images: masker -> compact ->
+    literal gather/conv/scatter block.  Returns seconds."""
+    import oracle
+    import synth
+
+    oracle.set_threads(threads)
+    xd = synth.to_f64(x_cpu[:k_images])
+    wd = synth.weights_f64(wts_cpu)
+    t0 = time.perf_counter()
+    m, _ = oracle.masker(xd, synth.to_f64(wm_cpu), bm, s)
+    idx, _ = oracle.compact(m)
+    oracle.dyn_block_literal(xd, wd, idx, s)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(x_cpu, wts_cpu, wm_cpu, bm, s, budget_s, n_total):
+    import oracle
+
+    oracle.build()
+    threads = os.cpu_count() or 1
+    t1 = oracle_sample(x_cpu, wts_cpu, wm_cpu, bm, s, 2, threads)
+    k = int(max(2, min(n_total, budget_s / max(t1 / 2, 1e-6))))
+    t = oracle_sample(x_cpu, wts_cpu, wm_cpu, bm, s, k, threads) if k > 2 else t1
+    return {"value": round(k / t, 2), "unit": "images/s", "cores": threads, "kind": "oracle",
+            "sample": f"first {k} of the {n_total} images, same S/weights/masker bias, fp64 literal mode "
+                      f"(masker+compact+gather/conv/scatter), OpenMP over patches; {t:.2f} s"}
+
+
+# ------------------------------------------------------------- reference ----
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands on the host cores (this tier's
+    reference arm), each step a bounded sample of the same workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    import synth
+
+    oracle.build()
+    wl = dict(WORKLOAD, n=args.n, s=args.s, r=args.r)
+    x = synth.make_x(wl["n"], wl["h"], wl["w"], wl["c_in"], seed=0)
+    wts = synth.make_block_weights(wl["c_in"], wl["c_mid"], wl["c_in"], seed=1)
+    wm = synth.make_masker_weights(wl["c_in"], seed=2)
+    xc = synth.make_x(wl["n"], wl["h"], wl["w"], wl["c_in"], seed=1000)
+    _, l0 = oracle.masker(synth.to_f64(xc), synth.to_f64(wm), 0.0, wl["s"])
+    lg = np.sort(l0.reshape(-1))
+    kk = int(round(wl["r"] * lg.size))
+    bm = float(np.float32(-0.5 * (lg[lg.size - kk - 1] + lg[lg.size - kk])))
+    threads = os.cpu_count() or 1
+    t1 = oracle_sample(x, wts, wm, bm, wl["s"], 2, threads)
+    k_img = int(max(2, min(wl["n"], 3.0 / max(t1 / 2, 1e-6))))
+    for _ in range(args.warmup):
+        oracle_sample(x, wts, wm, bm, wl["s"], k_img, threads)
+    ts = [oracle_sample(x, wts, wm, bm, wl["s"], k_img, threads) for _ in range(args.steps)]
+    tot = sum(ts)
+    val = k_img * args.steps / tot
+    line = {"metric": METRIC, "value": round(val, 3), "unit": "images/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * tot / args.steps, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD_NAME, "global_batch": wl["n"], "sample_images_per_step": k_img,
+                       "S": wl["s"], "r_target": wl["r"]},
+            "cpu_baseline": {"value": round(val, 3), "unit": "images/s", "cores": threads, "kind": "oracle",
+                             "sample": f"first {k_img} of {wl['n']} images per step"},
+            "e2e": {"value": round(val, 3), "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- lasnet ----
+
+def run_lasnet(args):
+    import torch.distributed as dist
+
+    import synth
+    import paper_2210_06223_b200 as L
+    from paper_2210_06223_b200 import _lib, build
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (there is no CPU fallback)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if rank == 0 or not os.path.exists(_lib.LIB_PATH):
+        build.build()
+    if world > 1:
+        dist.barrier()
+    lib = _lib.load()
+
+    wl = dict(WORKLOAD, n=args.n, s=args.s, r=args.r)
+    n, h, w, c_in, c_mid, s = (wl[k] for k in ("n", "h", "w", "c_in", "c_mid", "s"))
+    x_cpu = synth.make_x(n, h, w, c_in, seed=0 + 7919 * rank)
+    wts_cpu = synth.make_block_weights(c_in, c_mid, c_in, seed=1)
+    wm_cpu = synth.make_masker_weights(c_in, seed=2)
+    blk = L.DynBlock(L.BlockShape(n, h, w, c_in, c_mid, s), wts_cpu, wm_cpu, 0.0)
+    # masker bias calibrated on a separate batch of the same distribution
+    blk.calibrate_bias(synth.make_x(n, h, w, c_in, seed=1000 + rank).cuda(), wl["r"])
+    x = x_cpu.cuda()
+    y = torch.empty_like(x)
+    y2 = torch.empty_like(x)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def prep():
+        y.copy_(x)
+        flush.zero_()
+
+    for _ in range(max(args.warmup, 3)):
+        prep()
+        blk.forward(y)
+    torch.cuda.synchronize()
+    mask_cells = blk.mask_buf.cpu().numpy()
+    kwork, bwork, dwork, stats = algorithmic_work(mask_cells, n, h, w, c_in, c_mid, c_in, s)
+
+    K = args.steps
+    names = ["mask_compact", "conv1", "conv2", "conv3"]
+    ev_step = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    ev_k = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * len(names))] for _ in range(K)]
+    for row in ev_k:
+        for e in row:
+            e.record(stream)  # materialise the cudaEvent_t handles
+    handles = [ctypes_array(row) for row in ev_k]
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = blk.launches
+    for k in range(K):
+        prep()
+        lib.lasnet_set_kernel_events(handles[k], len(names))
+        ev_step[k][0].record(stream)
+        blk.forward(y)
+        ev_step[k][1].record(stream)
+    lib.lasnet_set_kernel_events(None, 0)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = blk.launches - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev_step]
+    kern_ms = {nm: statistics.fmean(ev_k[k][2 * i].elapsed_time(ev_k[k][2 * i + 1]) for k in range(K))
+               for i, nm in enumerate(names)}
+    tot_ms = sum(step_ms)
+
+    # dense comparator: the same kernels on every pixel (lasnet_dense_block)
+    for _ in range(3):
+        flush.zero_()
+        blk.dense(x, y2)
+    dense_ms = []
+    for k in range(K):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        blk.dense(x, y2)
+        b.record(stream)
+        dense_ms.append((a, b))
+    torch.cuda.synchronize()
+    dense_ms = [a.elapsed_time(b) for a, b in dense_ms]
+
+    # end to end through the public API with pinned HOST buffers
+    x_host = x_cpu.pin_memory()
+    y_host = torch.empty_like(x_cpu).pin_memory()
+    for _ in range(2):
+        blk.forward_host(x_host, y_host, y)
+    e2e_ev = []
+    for k in range(K):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        blk.forward_host(x_host, y_host, y)
+        b.record(stream)
+        e2e_ev.append((a, b))
+    torch.cuda.synchronize()
+    e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev)
+    clocks = sampler.stop()
+
+    t = torch.tensor([tot_ms, e2e_ms, statistics.fmean(dense_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot_max, e2e_max, dense_max = (float(v) for v in t.tolist())
+    value = world * n * K / (tot_max / 1e3)
+    e2e_val = world * n * K / (e2e_max / 1e3)
+
+    if rank == 0:
+        hbm, tfl, tfl_sus, src = peaks()
+        dom = max(names, key=lambda nm: kern_ms[nm])
+        roof = roofline_entry(kwork[dom], kern_ms[dom], hbm, tfl)
+        roof.update({"kernel": dom, "traffic": None, "peak_source": src,
+                     "algorithmic": {"bytes": kwork[dom]["bytes"], "flops": kwork[dom]["flops"]},
+                     "share_of_step": round(kern_ms[dom] / statistics.fmean(step_ms), 3)})
+        blk_roof = roofline_entry(bwork, statistics.fmean(step_ms), hbm, tfl)
+        t_roof = max(bwork["bytes"] / (hbm * 1e9), bwork["flops"] / (tfl * 1e12)) * 1e3
+        blk_roof.update({"t_roof_ms": round(t_roof, 4), "frac_time": round(t_roof / statistics.fmean(step_ms), 4),
+                         "definition": "headline: masker read of x + idx + halo gather + residual + y + weights; "
+                                       "halo-method FLOPs (SURVEY 8(d))"})
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "images/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": round(tot_max / K, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": WORKLOAD_NAME, "global_batch": world * n, "per_gpu_batch": n,
+                       "H": h, "W": w, "c_in": c_in, "c_mid": c_mid, "S": s, "r_target": wl["r"],
+                       "r_patch": round(stats["r_patch"], 4), "r_pixel": round(stats["r_pixel"], 4),
+                       "parallelism": f"dp{world}", "l2": "flushed (256 MiB write) before every timed step"},
+            "latency_ms": {"p10": round(float(np.percentile(step_ms, 10)), 4),
+                           "p50": round(float(np.percentile(step_ms, 50)), 4),
+                           "p90": round(float(np.percentile(step_ms, 90)), 4)},
+            "kernels_ms": {k2: round(v, 4) for k2, v in kern_ms.items()},
+            "dense_ms_per_step": round(dense_max, 4),
+            "speedup_vs_dense": round(dense_max / (tot_max / K), 3),
+            "roofline": roof,
+            "block_roofline": blk_roof,
+            "e2e": {"value": round(e2e_val, 1), "unit": "images/s", "h2d_bytes_per_step": x.numel() * 2,
+                    "d2h_bytes_per_step": x.numel() * 2},
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(x_cpu, wts_cpu, wm_cpu, blk.bm, s, args.cpu_budget, n)
+        if args.detail:
+            with open(args.detail, "w") as f:
+                json.dump({"line": line, "step_ms": step_ms, "dense_ms": dense_ms, "work": kwork,
+                           "block": bwork, "dense": dwork, "stats": stats}, f, indent=1)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def ctypes_array(events):
+    import ctypes
+
+    arr = (ctypes.c_void_p * len(events))()
+    for i, e in enumerate(events):
+        arr[i] = e.cuda_event
+    return arr
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_lasnet(args)
+
+
+if __name__ == "__main__":
+    main()

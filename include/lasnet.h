@@ -1,0 +1,176 @@
+/*
+ * lasnet.h -- C ABI of the B200-native LASNet coarse-grained spatially-dynamic
+ * residual block (arXiv 2210.06223, "Latency-aware Spatial-wise Dynamic
+ * Networks").  Citations: P:n = PAPER.md line n.
+ *
+ * The block (sec. 3.1, sec. 3.2 / Fig. 2, sec. 3.4,
+ * P:556-577 App. B) runs as five steps:
+ *   1 masker      lasnet_mask      pooled 1x1 conv + hard threshold -> S x S patch mask
+ *   2 compaction  lasnet_compact   ascending index list of activated patches + count
+ *   (1+2 fused:   lasnet_mask_compact, one launch)
+ *   3 gather+conv1                 \
+ *   4 conv2 (3x3)                   > lasnet_dyn_block
+ *   5 conv3+scatter-add            /
+ * and lasnet_dense_block runs the same convolutions on every pixel (the static
+ * counterpart) as the comparator.
+ *
+ * Conventions for every entry point
+ *  - Pointers are DEVICE pointers unless stated otherwise.  The caller owns and
+ *    frees every buffer, including the workspace; the library never allocates
+ *    device memory and keeps no per-call state.
+ *  - Every call only enqueues work on `stream` (a cudaStream_t; NULL = legacy
+ *    default stream).  Results are valid once the stream has synchronised.
+ *    The active-patch count never leaves the device: kernels read it from
+ *    device memory, so the sequence mask -> compact -> dyn_block needs no host
+ *    synchronisation and is CUDA-graph capturable.
+ *  - Arguments are validated on the host before anything is launched.  On any
+ *    error status nothing is launched and no output is touched.  No C++
+ *    exception crosses this ABI.  Launch failures are reported as
+ *    LASNET_ERR_CUDA (from cudaGetLastError()).
+ *  - Layouts: activations NHWC, channels innermost; a pixel row is c*elt bytes.
+ *    bf16 tensors are IEEE bfloat16 bit patterns (uint16).  Device pointers must
+ *    be 16-byte aligned.
+ *  - The bf16 path (dtype LASNET_BF16) runs tcgen05 tensor-core kernels fed by
+ *    TMA: c_in a multiple of 64, c_mid and c_out equal to 64 or multiples of 128
+ *    (at most 2048), s <= 11, w <= 128.  The fp32 path (LASNET_F32) runs fp32
+ *    CUDA-core kernels: all channels multiples of 64.  Other valid shapes return
+ *    LASNET_ERR_UNSUPPORTED.  lasnet_mask alone only needs c_in % 8 (bf16) or
+ *    % 4 (fp32).
+ */
+#ifndef LASNET_H
+#define LASNET_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LASNET_ABI_VERSION 1
+
+typedef enum {
+    LASNET_OK = 0,
+    LASNET_ERR_NULL = 1,        /* a required pointer is NULL                            */
+    LASNET_ERR_SHAPE = 2,       /* non-positive or inconsistent sizes                    */
+    LASNET_ERR_DOMAIN = 3,      /* S < 1, stride not in {1,2}, unknown dtype             */
+    LASNET_ERR_UNSUPPORTED = 4, /* valid but not built: channel multiples, stride 2      */
+    LASNET_ERR_ALIAS = 5,       /* y partially overlaps x (only y == x is allowed)       */
+    LASNET_ERR_WORKSPACE = 6,   /* workspace NULL or smaller than the *_workspace_bytes  */
+    LASNET_ERR_CUDA = 7         /* a CUDA launch or runtime call failed                  */
+} lasnet_status;
+
+typedef enum { LASNET_F32 = 0, LASNET_BF16 = 1 } lasnet_dtype;
+
+/* cudaStream_t without pulling in the CUDA headers. */
+typedef struct CUstream_st *lasnet_stream_t;
+
+/* Shape of one bottleneck block.  h, w are the OUTPUT spatial dims; the mask
+ * lives on the output grid ("the corresponding location of the output
+ * feature").  The coarse grid is gh = ceil(h/s) x gw = ceil(w/s); edge patches
+ * are clipped when s does not divide h or w (reading R7). */
+typedef struct {
+    int32_t n, h, w;              /* batch, output height, output width              */
+    int32_t c_in, c_mid, c_out;   /* bottleneck widths; identity block: c_in == c_out */
+    int32_t stride;               /* 1 (stride-2 first blocks: not built, ERR_UNSUPPORTED) */
+    int32_t s;                    /* spatial granularity S >= 1               */
+    int32_t dtype;                /* lasnet_dtype of x, y and w1..w3                  */
+} lasnet_block_desc;
+
+/* BN-folded weights.  Biases are fp32; w1..w3 have the block dtype.
+ *   w1 [c_mid][c_in]            conv1 1x1, K-major
+ *   w2 [c_mid][3][3][c_mid]     conv2 3x3, OHWI (K = 9*c_mid, tap-major)
+ *   w3 [c_out][c_mid]           conv3 1x1
+ *   wd, bd                      downsample projection; must be NULL (stride 1) */
+typedef struct {
+    const void *w1; const float *b1;
+    const void *w2; const float *b2;
+    const void *w3; const float *b3;
+    const void *wd; const float *bd;
+} lasnet_block_weights;
+
+/* Step 1 -- masker ("a pooling layer followed by a 1x1 convolution";
+ * App. B: the 2-channel argmax reduces to x*(W_0 - W_1) > 0).
+ *   x      [n][h][w][c_in] (block dtype)
+ *   wm     [c_in] fp32, the reduced weight W_0 - W_1
+ *   bm     reduced bias b_0 - b_1 (host scalar)
+ *   mask   [n][gh][gw] uint8 out: 1 iff logit > 0 (ties inactive, R3)
+ *   logits [n][gh][gw] fp64 out, nullable: logit = sum_c wm_c * avgpool_c(x) + bm,
+ *          average over the in-image pixels of the cell (R1, R7).
+ * Accumulation is fp64 so the 1-bit decision is reproducible. */
+lasnet_status lasnet_mask(const lasnet_block_desc *desc, const void *x, const float *wm,
+                          float bm, uint8_t *mask, double *logits, lasnet_stream_t stream);
+
+/* Steps 1+2 fused in one launch (App. B: "the masker generates the
+ * indices of activated patches"): the same logits and decisions as lasnet_mask,
+ * and the same idx/count as lasnet_compact on that mask.
+ *   mask, logits  nullable outputs as in lasnet_mask
+ *   idx [n*gh*gw], count   as in lasnet_compact
+ *   ws     lasnet_mask_compact_workspace_bytes(desc) bytes that must be ALL ZERO
+ *          before the first call; every call leaves them all zero again.
+ *          Concurrent calls must not share a workspace. */
+lasnet_status lasnet_mask_compact(const lasnet_block_desc *desc, const void *x, const float *wm, float bm,
+                                  uint8_t *mask, double *logits, int32_t *idx, int32_t *count, void *ws,
+                                  size_t ws_bytes, lasnet_stream_t stream);
+size_t lasnet_mask_compact_workspace_bytes(const lasnet_block_desc *desc);
+
+/* Step 2 -- compaction (App. B P:568-569 "the masker generates the indices of
+ * activated patches instead of sparse mask").
+ *   mask   [ncells] uint8 (ncells = n*gh*gw), nonzero = active
+ *   idx    [ncells] int32 out: ascending linear cell ids n*gh*gw + gy*gw + gx of
+ *          the active cells in idx[0 .. count-1]; the rest is untouched
+ *   count  int32 device scalar out
+ *   ws     device workspace of lasnet_compact_workspace_bytes(ncells) bytes
+ * ncells == 0 is valid (count = 0). */
+lasnet_status lasnet_compact(const uint8_t *mask, int32_t ncells, int32_t *idx,
+                             int32_t *count, void *ws, size_t ws_bytes,
+                             lasnet_stream_t stream);
+size_t lasnet_compact_workspace_bytes(int32_t ncells);
+
+/* Steps 3-5 -- the dynamic bottleneck on the activated patches
+ * (P:89 gather -> compute -> scatter; P:162-166 gather fused into the dynamic
+ * conv; P:168-170, P:574-577 scatter fused with the residual add).
+ * For every active cell idx[t], t < *count:
+ *   h1 = ReLU(conv1(x) + b1) on the (s+2)x(s+2) halo window, 0 outside the image (R6)
+ *   h2 = ReLU(conv3x3_valid(h1, w2) + b2)                  -> s x s
+ *   y  = ReLU(x + conv1x1(h2, w3) + b3) on the in-image pixels of the patch (R5, R7)
+ * Pixels of inactive cells keep y = x (input fill, R4).
+ *   x, y   [n][h][w][c_in]; y == x runs in place (inactive pixels cost nothing);
+ *          y != x copies x to y first; any partial overlap -> LASNET_ERR_ALIAS
+ *   idx, count  output of lasnet_compact (device); cap = capacity of idx (>= *count)
+ *   ws     device workspace of lasnet_dyn_workspace_bytes(desc, cap) bytes
+ * Intermediates h1/h2 are stored in the block dtype (bf16 RNE or fp32). */
+lasnet_status lasnet_dyn_block(const lasnet_block_desc *desc, const lasnet_block_weights *wts,
+                               const void *x, void *y, const int32_t *idx,
+                               const int32_t *count, int32_t cap, void *ws,
+                               size_t ws_bytes, lasnet_stream_t stream);
+size_t lasnet_dyn_workspace_bytes(const lasnet_block_desc *desc, int32_t cap);
+
+/* The same convolutions on every pixel (static block): y = ReLU(x +
+ * conv3(ReLU(conv3x3(ReLU(conv1(x)))))), zero padding 1 for the 3x3.
+ *   x, y   [n][h][w][c_in]; y == x allowed (in place); partial overlap -> ERR_ALIAS
+ *   ws     lasnet_dense_workspace_bytes(desc) bytes */
+lasnet_status lasnet_dense_block(const lasnet_block_desc *desc, const lasnet_block_weights *wts,
+                                 const void *x, void *y, void *ws, size_t ws_bytes,
+                                 lasnet_stream_t stream);
+size_t lasnet_dense_workspace_bytes(const lasnet_block_desc *desc);
+
+/* Benchmark instrumentation.  The next n_pairs kernels this host thread
+ * launches through the ABI are bracketed by cudaEventRecord(events[2i]) and
+ * cudaEventRecord(events[2i+1]) on their launch stream (i counts launches from
+ * this call).  events are cudaEvent_t handles owned by the caller and must stay
+ * valid until recorded; n_pairs = 0 disables.  Host-side, launches nothing. */
+lasnet_status lasnet_set_kernel_events(void *const *events, int32_t n_pairs);
+
+/* Host-side, pure helpers. */
+const char *lasnet_status_str(lasnet_status st);
+int32_t lasnet_abi_version(void);
+/* Number of kernels the last successful call on this host thread enqueued
+ * (bench bookkeeping for "gpu_launches"; memsets/copies are not counted). */
+int32_t lasnet_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LASNET_H */

@@ -1,0 +1,11 @@
+"""B200-native LASNet coarse-grained spatially-dynamic residual block (arXiv 2210.06223).
+
+Product path: include/lasnet.h C ABI implemented by liblasnet.so (sm_100a
+kernels in csrc/), bound by ctypes in _lib.py, with the Python API in block.py.
+There is no CPU fallback: calls raise if the CUDA library is missing.
+"""
+from .block import (BlockShape, DynBlock, compact, dense_block, dyn_block, grid, last_launch_count,
+                    make_desc, make_weights, mask)
+
+__all__ = ["BlockShape", "DynBlock", "compact", "dense_block", "dyn_block", "grid", "last_launch_count",
+           "make_desc", "make_weights", "mask"]

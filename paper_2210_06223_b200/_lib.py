@@ -1,0 +1,89 @@
+"""ctypes binding of liblasnet.so (include/lasnet.h).  Argument marshalling only.
+
+There is no fallback: if the CUDA library is missing or fails to load, every
+entry point raises.  Tensors are passed as raw device pointers; torch only
+supplies memory and the current stream.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liblasnet.so")
+
+LASNET_F32, LASNET_BF16 = 0, 1
+STATUS = {
+    0: "LASNET_OK", 1: "LASNET_ERR_NULL", 2: "LASNET_ERR_SHAPE", 3: "LASNET_ERR_DOMAIN",
+    4: "LASNET_ERR_UNSUPPORTED", 5: "LASNET_ERR_ALIAS", 6: "LASNET_ERR_WORKSPACE", 7: "LASNET_ERR_CUDA",
+}
+
+# every symbol include/lasnet.h declares
+EXPORTS = [
+    "lasnet_mask", "lasnet_mask_compact", "lasnet_mask_compact_workspace_bytes", "lasnet_compact", "lasnet_compact_workspace_bytes", "lasnet_dyn_block",
+    "lasnet_dyn_workspace_bytes", "lasnet_dense_block", "lasnet_dense_workspace_bytes",
+    "lasnet_status_str", "lasnet_abi_version", "lasnet_last_launch_count", "lasnet_set_kernel_events",
+]
+
+
+class BlockDesc(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_int32) for k in ("n", "h", "w", "c_in", "c_mid", "c_out", "stride", "s", "dtype")]
+
+
+class BlockWeights(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_void_p) for k in ("w1", "b1", "w2", "b2", "w3", "b3", "wd", "bd")]
+
+
+class LasnetError(RuntimeError):
+    def __init__(self, fn: str, code: int):
+        super().__init__(f"{fn} -> {STATUS.get(code, code)}")
+        self.code = code
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load liblasnet.so.  Raises (never falls back) when it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"liblasnet.so not found at {path}; build it with `python -m paper_2210_06223_b200.build` "
+            "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    vp, i32, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_size_t
+    D = ctypes.POINTER(BlockDesc)
+    Wt = ctypes.POINTER(BlockWeights)
+    lib.lasnet_mask.argtypes = [D, vp, vp, ctypes.c_float, vp, vp, vp]
+    lib.lasnet_mask.restype = ctypes.c_int
+    lib.lasnet_mask_compact.argtypes = [D, vp, vp, ctypes.c_float, vp, vp, vp, vp, vp, sz, vp]
+    lib.lasnet_mask_compact.restype = ctypes.c_int
+    lib.lasnet_mask_compact_workspace_bytes.argtypes = [D]
+    lib.lasnet_mask_compact_workspace_bytes.restype = sz
+    lib.lasnet_compact.argtypes = [vp, i32, vp, vp, vp, sz, vp]
+    lib.lasnet_compact.restype = ctypes.c_int
+    lib.lasnet_compact_workspace_bytes.argtypes = [i32]
+    lib.lasnet_compact_workspace_bytes.restype = sz
+    lib.lasnet_dyn_block.argtypes = [D, Wt, vp, vp, vp, vp, i32, vp, sz, vp]
+    lib.lasnet_dyn_block.restype = ctypes.c_int
+    lib.lasnet_dyn_workspace_bytes.argtypes = [D, i32]
+    lib.lasnet_dyn_workspace_bytes.restype = sz
+    lib.lasnet_dense_block.argtypes = [D, Wt, vp, vp, vp, sz, vp]
+    lib.lasnet_dense_block.restype = ctypes.c_int
+    lib.lasnet_dense_workspace_bytes.argtypes = [D]
+    lib.lasnet_dense_workspace_bytes.restype = sz
+    lib.lasnet_status_str.argtypes = [ctypes.c_int]
+    lib.lasnet_status_str.restype = ctypes.c_char_p
+    lib.lasnet_abi_version.restype = i32
+    lib.lasnet_last_launch_count.restype = i32
+    lib.lasnet_set_kernel_events.argtypes = [ctypes.POINTER(ctypes.c_void_p), i32]
+    lib.lasnet_set_kernel_events.restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def check(fn: str, code: int) -> None:
+    if code != 0:
+        raise LasnetError(fn, code)

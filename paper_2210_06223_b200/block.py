@@ -1,0 +1,251 @@
+"""Python API of the LASNet dynamic residual block (thin marshalling over the C ABI).
+
+Every step of the block runs in liblasnet.so kernels; this module only creates
+descriptor structs, allocates caller-owned buffers with torch and passes raw
+device pointers plus the current CUDA stream.  Functions mirror the C-ABI
+names: ``mask``, ``compact``, ``dyn_block``, ``dense_block``.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+
+_DT = {torch.bfloat16: _lib.LASNET_BF16, torch.float32: _lib.LASNET_F32}
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def grid(h: int, w: int, s: int):
+    return -(-h // s), -(-w // s)
+
+
+def make_desc(n, h, w, c_in, c_mid, c_out, s, dtype) -> _lib.BlockDesc:
+    return _lib.BlockDesc(n, h, w, c_in, c_mid, c_out, 1, s, _DT[dtype])
+
+
+def make_weights(wts: dict) -> _lib.BlockWeights:
+    return _lib.BlockWeights(*(wts[k].data_ptr() for k in ("w1", "b1", "w2", "b2", "w3", "b3")), None, None)
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if t is not None and (not t.is_cuda or not t.is_contiguous()):
+            raise ValueError("lasnet: tensors must be contiguous CUDA tensors")
+
+
+# ------------------------------------------------------------- functional --
+
+def mask(x: torch.Tensor, wm: torch.Tensor, bm: float, s: int, logits: bool = False,
+         out: torch.Tensor | None = None, logits_out: torch.Tensor | None = None):
+    """Step 1: uint8 [n, gh, gw] mask and optional fp64 logits."""
+    _require_cuda(x, wm)
+    n, h, w, c = x.shape
+    gh, gw = grid(h, w, s)
+    m = out if out is not None else torch.empty((n, gh, gw), dtype=torch.uint8, device=x.device)
+    lg = logits_out if logits_out is not None else (
+        torch.empty((n, gh, gw), dtype=torch.float64, device=x.device) if logits else None)
+    d = make_desc(n, h, w, c, c, c, s, x.dtype)
+    lib = _lib.load()
+    _lib.check("lasnet_mask", lib.lasnet_mask(ctypes.byref(d), _p(x), _p(wm), float(bm), _p(m), _p(lg), _stream()))
+    return (m, lg) if logits else m
+
+
+def compact(m: torch.Tensor, idx: torch.Tensor | None = None, count: torch.Tensor | None = None,
+            ws: torch.Tensor | None = None):
+    """Step 2: ascending active cell ids + device count."""
+    _require_cuda(m)
+    lib = _lib.load()
+    ncells = m.numel()
+    idx = idx if idx is not None else torch.empty(max(ncells, 1), dtype=torch.int32, device=m.device)
+    count = count if count is not None else torch.empty(1, dtype=torch.int32, device=m.device)
+    wsb = lib.lasnet_compact_workspace_bytes(ncells)
+    ws = ws if ws is not None else torch.empty(wsb, dtype=torch.uint8, device=m.device)
+    _lib.check("lasnet_compact", lib.lasnet_compact(_p(m), ncells, _p(idx), _p(count), _p(ws), ws.numel(), _stream()))
+    return idx, count
+
+
+def dyn_block(x: torch.Tensor, wts: dict, idx: torch.Tensor, count: torch.Tensor, s: int,
+              y: torch.Tensor | None = None, ws: torch.Tensor | None = None, cap: int | None = None):
+    """Steps 3-5.  y=None runs in place on x."""
+    _require_cuda(x, idx, count)
+    lib = _lib.load()
+    n, h, w, c_in = x.shape
+    c_mid, c_out = wts["w1"].shape[0], wts["w3"].shape[0]
+    gh, gw = grid(h, w, s)
+    cap = cap if cap is not None else n * gh * gw
+    d = make_desc(n, h, w, c_in, c_mid, c_out, s, x.dtype)
+    wsb = lib.lasnet_dyn_workspace_bytes(ctypes.byref(d), cap)
+    ws = ws if ws is not None else torch.empty(max(wsb, 1), dtype=torch.uint8, device=x.device)
+    y = x if y is None else y
+    wt = make_weights(wts)
+    _lib.check("lasnet_dyn_block", lib.lasnet_dyn_block(ctypes.byref(d), ctypes.byref(wt), _p(x), _p(y), _p(idx),
+                                                        _p(count), cap, _p(ws), ws.numel(), _stream()))
+    return y
+
+
+def dense_block(x: torch.Tensor, wts: dict, y: torch.Tensor | None = None, ws: torch.Tensor | None = None):
+    """Static comparator: the same kernels on every pixel."""
+    _require_cuda(x)
+    lib = _lib.load()
+    n, h, w, c_in = x.shape
+    c_mid, c_out = wts["w1"].shape[0], wts["w3"].shape[0]
+    d = make_desc(n, h, w, c_in, c_mid, c_out, 1, x.dtype)
+    wsb = lib.lasnet_dense_workspace_bytes(ctypes.byref(d))
+    ws = ws if ws is not None else torch.empty(max(wsb, 1), dtype=torch.uint8, device=x.device)
+    y = torch.empty_like(x) if y is None else y
+    wt = make_weights(wts)
+    _lib.check("lasnet_dense_block", lib.lasnet_dense_block(ctypes.byref(d), ctypes.byref(wt), _p(x), _p(y), _p(ws),
+                                                            ws.numel(), _stream()))
+    return y
+
+
+def last_launch_count() -> int:
+    return int(_lib.load().lasnet_last_launch_count())
+
+
+# ------------------------------------------------------------------ block --
+
+@dataclass
+class BlockShape:
+    n: int
+    h: int
+    w: int
+    c_in: int
+    c_mid: int
+    s: int
+    dtype: torch.dtype = torch.bfloat16
+
+    @property
+    def gh(self):
+        return -(-self.h // self.s)
+
+    @property
+    def gw(self):
+        return -(-self.w // self.s)
+
+    @property
+    def ncells(self):
+        return self.n * self.gh * self.gw
+
+
+class DynBlock:
+    """One LASNet bottleneck block with device-resident weights and caller-owned
+    buffers preallocated once (mask, idx, count, workspaces), so a forward is
+    exactly the kernel launches: mask -> compact -> conv1 -> conv2 -> conv3."""
+
+    def __init__(self, shape: BlockShape, wts: dict, wm: torch.Tensor, bm: float, device="cuda"):
+        self.shape = shape
+        self.wts = {k: v.to(device).contiguous() for k, v in wts.items()}
+        self.wm = wm.to(device).float().contiguous()
+        self.bm = float(bm)
+        sh = shape
+        self.c_out = self.wts["w3"].shape[0]
+        lib = _lib.load()
+        self.desc = make_desc(sh.n, sh.h, sh.w, sh.c_in, sh.c_mid, self.c_out, sh.s, sh.dtype)
+        self.wt = make_weights(self.wts)
+        self.mask_buf = torch.empty((sh.n, sh.gh, sh.gw), dtype=torch.uint8, device=device)
+        self.logits = torch.empty((sh.n, sh.gh, sh.gw), dtype=torch.float64, device=device)
+        self.idx = torch.empty(max(sh.ncells, 1), dtype=torch.int32, device=device)
+        self.count = torch.zeros(1, dtype=torch.int32, device=device)
+        self.cws = torch.empty(max(lib.lasnet_compact_workspace_bytes(sh.ncells), 1), dtype=torch.uint8, device=device)
+        # fused masker+compaction workspace: zero before first use, left zero by every call
+        self.mcws = torch.zeros(max(lib.lasnet_mask_compact_workspace_bytes(ctypes.byref(self.desc)), 16),
+                                dtype=torch.uint8, device=device)
+        self.cap = sh.ncells
+        self.dws = torch.empty(max(lib.lasnet_dyn_workspace_bytes(ctypes.byref(self.desc), self.cap), 1),
+                               dtype=torch.uint8, device=device)
+        dd = make_desc(sh.n, sh.h, sh.w, sh.c_in, sh.c_mid, self.c_out, 1, sh.dtype)
+        self.dense_desc = dd
+        self._dense_ws = None
+        self.launches = 0
+
+    def mask(self, x: torch.Tensor, want_logits: bool = False):
+        lib = _lib.load()
+        _lib.check("lasnet_mask", lib.lasnet_mask(ctypes.byref(self.desc), _p(x), _p(self.wm), self.bm,
+                                                  _p(self.mask_buf), _p(self.logits) if want_logits else None,
+                                                  _stream()))
+        self.launches += lib.lasnet_last_launch_count()
+        return self.mask_buf
+
+    def compact(self):
+        lib = _lib.load()
+        _lib.check("lasnet_compact", lib.lasnet_compact(_p(self.mask_buf), self.shape.ncells, _p(self.idx),
+                                                        _p(self.count), _p(self.cws), self.cws.numel(), _stream()))
+        self.launches += lib.lasnet_last_launch_count()
+        return self.idx, self.count
+
+    def mask_compact(self, x: torch.Tensor, want_logits: bool = False):
+        """Steps 1+2 in one launch (lasnet_mask_compact)."""
+        lib = _lib.load()
+        _lib.check("lasnet_mask_compact", lib.lasnet_mask_compact(
+            ctypes.byref(self.desc), _p(x), _p(self.wm), self.bm, _p(self.mask_buf),
+            _p(self.logits) if want_logits else None, _p(self.idx), _p(self.count), _p(self.mcws),
+            self.mcws.numel(), _stream()))
+        self.launches += lib.lasnet_last_launch_count()
+        return self.idx, self.count
+
+    def convs(self, x: torch.Tensor, y: torch.Tensor | None = None):
+        lib = _lib.load()
+        y = x if y is None else y
+        _lib.check("lasnet_dyn_block", lib.lasnet_dyn_block(ctypes.byref(self.desc), ctypes.byref(self.wt), _p(x),
+                                                            _p(y), _p(self.idx), _p(self.count), self.cap,
+                                                            _p(self.dws), self.dws.numel(), _stream()))
+        self.launches += lib.lasnet_last_launch_count()
+        return y
+
+    def forward(self, x: torch.Tensor, y: torch.Tensor | None = None):
+        """Five steps, in place on x when y is None.  No host synchronisation.
+        Steps 1+2 run as one fused launch, steps 3-5 as three."""
+        self.mask_compact(x)
+        return self.convs(x, y)
+
+    __call__ = forward
+
+    def dense(self, x: torch.Tensor, y: torch.Tensor):
+        lib = _lib.load()
+        if self._dense_ws is None:
+            self._dense_ws = torch.empty(max(lib.lasnet_dense_workspace_bytes(ctypes.byref(self.dense_desc)), 1),
+                                         dtype=torch.uint8, device=x.device)
+        _lib.check("lasnet_dense_block", lib.lasnet_dense_block(ctypes.byref(self.dense_desc), ctypes.byref(self.wt),
+                                                                _p(x), _p(y), _p(self._dense_ws),
+                                                                self._dense_ws.numel(), _stream()))
+        self.launches += lib.lasnet_last_launch_count()
+        return y
+
+    def forward_host(self, x_host: torch.Tensor, y_host: torch.Tensor, x_dev: torch.Tensor):
+        """End-to-end call with HOST buffers: H2D copy of x (pinned) into x_dev,
+        the five steps in place, D2H copy of the result into y_host (pinned)."""
+        x_dev.copy_(x_host, non_blocking=True)
+        self.forward(x_dev)
+        y_host.copy_(x_dev, non_blocking=True)
+        return y_host
+
+    def calibrate_bias(self, x: torch.Tensor, r: float) -> float:
+        """Pick the masker bias so that ~r of the cells are active on x, from the
+        product masker's own logits (b = 0): bm = -(the (1-r) quantile), placed
+        midway between two neighbouring logits so no cell sits on the threshold."""
+        saved = self.bm
+        self.bm = 0.0
+        self.mask(x, want_logits=True)
+        lg = self.logits.flatten().double().sort().values.cpu()
+        self.bm = saved
+        G = lg.numel()
+        k = int(round(r * G))
+        if k <= 0:
+            b = -(float(lg[-1]) + 1.0)
+        elif k >= G:
+            b = -(float(lg[0]) - 1.0)
+        else:
+            b = -0.5 * (float(lg[G - k - 1]) + float(lg[G - k]))
+        self.bm = float(torch.tensor(b, dtype=torch.float32))
+        return self.bm

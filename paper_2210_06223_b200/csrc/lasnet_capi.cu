@@ -1,0 +1,454 @@
+// lasnet_capi.cu -- the C ABI declared in include/lasnet.h.  Host-side
+// validation, workspace carving and kernel launches; no device memory is
+// allocated here and no per-call state is kept (the only globals are the
+// cached SM count and a thread-local launch counter for bench bookkeeping).
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include "../../include/lasnet.h"
+#include "rowmap.cuh"
+
+namespace lasnet {
+cudaError_t launch_masker(int dtype_bf16, const void *x, const float *wm, float bm, int n_img, int H, int W,
+                          int C, int S, uint8_t *mask, double *logits, cudaStream_t st);
+int launch_compact(const uint8_t *mask, int ncells, int32_t *idx, int32_t *count, void *ws, cudaStream_t st,
+                   cudaError_t *err);
+size_t compact_workspace_bytes(int ncells);
+size_t mask_compact_workspace_bytes(long ncells);
+cudaError_t launch_mask_compact(int dtype_bf16, const void *x, const float *wm, float bm, int n_img, int H, int W,
+                                int C, int S, uint8_t *mask, double *logits, int32_t *idx, int32_t *count, void *ws,
+                                cudaStream_t st);
+cudaError_t launch_conv_tc(int mode, const ConvArgs &a, int max_tiles_m, int num_sms, cudaStream_t st);
+cudaError_t launch_conv_simt(int mode, const ConvArgs &a, int max_rows, cudaStream_t st);
+}  // namespace lasnet
+
+using namespace lasnet;
+
+namespace {
+
+thread_local int32_t g_last_launches = 0;
+thread_local void *const *g_events = nullptr;
+thread_local int32_t g_event_pairs = 0, g_event_next = 0;
+
+// Brackets one kernel launch with the caller's benchmark events, if armed.
+struct KernelEvents {
+    cudaStream_t st;
+    bool on;
+    explicit KernelEvents(cudaStream_t s) : st(s), on(g_events && g_event_next < g_event_pairs) {
+        if (on) cudaEventRecord(static_cast<cudaEvent_t>(g_events[2 * g_event_next]), st);
+    }
+    ~KernelEvents() {
+        if (on) {
+            cudaEventRecord(static_cast<cudaEvent_t>(g_events[2 * g_event_next + 1]), st);
+            ++g_event_next;
+        }
+    }
+};
+
+int num_sms() {
+    static int cached = 0;
+    if (!cached) {
+        int dev = 0, n = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cached = n > 0 ? n : 148;
+    }
+    return cached;
+}
+
+size_t elt_size(int dtype) { return dtype == LASNET_BF16 ? 2 : 4; }
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+bool misaligned(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) != 0; }
+
+lasnet_status check_desc(const lasnet_block_desc *d) {
+    if (!d) return LASNET_ERR_NULL;
+    if (d->n < 0 || d->h <= 0 || d->w <= 0 || d->c_in <= 0 || d->c_mid <= 0 || d->c_out <= 0)
+        return LASNET_ERR_SHAPE;
+    if (d->s < 1 || (d->stride != 1 && d->stride != 2)) return LASNET_ERR_DOMAIN;
+    if (d->dtype != LASNET_F32 && d->dtype != LASNET_BF16) return LASNET_ERR_DOMAIN;
+    if ((long)d->n * d->h * d->w * (long)(d->c_in > d->c_out ? d->c_in : d->c_out) > 0x7fffffffL)
+        return LASNET_ERR_UNSUPPORTED;  // 32-bit element offsets in the row maps
+    return LASNET_OK;
+}
+
+// Channel constraints of the convolution kernels (tcgen05: K-blocks of 64,
+// N tiles of 64/128; SIMT: N tiles of 64, K chunks of 32).
+lasnet_status check_channels(const lasnet_block_desc *d) {
+    if (d->c_in % 64 || d->c_mid % 64 || d->c_out % 64) return LASNET_ERR_UNSUPPORTED;
+    // tcgen05 N tiles are 64 (N == 64) or 128 wide
+    if ((d->c_mid != 64 && d->c_mid % 128) || (d->c_out != 64 && d->c_out % 128)) return LASNET_ERR_UNSUPPORTED;
+    if (d->c_out > 2048 || d->c_mid > 2048) return LASNET_ERR_UNSUPPORTED;  // bias staged in smem
+    if (d->dtype == LASNET_BF16 && (d->s > 11 || d->w > 128)) return LASNET_ERR_UNSUPPORTED;  // TMA box limits
+    if (d->stride != 1) return LASNET_ERR_UNSUPPORTED;  // stride-2 first blocks: NEXT-f1
+    if (d->c_in != d->c_out) return LASNET_ERR_UNSUPPORTED;  // identity residual only
+    return LASNET_OK;
+}
+
+lasnet_status check_weights(const lasnet_block_weights *w) {
+    if (!w || !w->w1 || !w->b1 || !w->w2 || !w->b2 || !w->w3 || !w->b3) return LASNET_ERR_NULL;
+    if (w->wd || w->bd) return LASNET_ERR_UNSUPPORTED;
+    return LASNET_OK;
+}
+
+lasnet_status check_alias(const void *x, const void *y, size_t bytes) {
+    if (x == y) return LASNET_OK;
+    const uint8_t *a = static_cast<const uint8_t *>(x), *b = static_cast<const uint8_t *>(y);
+    if (a < b + bytes && b < a + bytes) return LASNET_ERR_ALIAS;
+    return LASNET_OK;
+}
+
+struct Carve {
+    uint8_t *p;
+    size_t used = 0;
+    void *take(size_t bytes) {
+        void *r = p + used;
+        used += align_up(bytes, 256);
+        return r;
+    }
+};
+
+size_t dyn_ws_bytes(const lasnet_block_desc *d, int32_t cap) {
+    const size_t e = elt_size(d->dtype);
+    const size_t hs = (size_t)(d->s + 2) * (d->s + 2), ss = (size_t)d->s * d->s;
+    return align_up((size_t)cap * hs * d->c_mid * e, 256) + align_up((size_t)cap * ss * d->c_mid * e, 256);
+}
+
+size_t dense_ws_bytes(const lasnet_block_desc *d) {
+    const size_t px = (size_t)d->n * d->h * d->w;
+    return 2 * align_up(px * d->c_mid * elt_size(d->dtype), 256);
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (the only
+// process-wide state: a once-initialised function pointer).
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// bf16 tensor map, innermost dimension first, 128-B swizzle, OOB elements zero.
+bool tmap(CUtensorMap *m, const void *base, int rank, const uint64_t *dims, const uint32_t *box) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t gd[5], gs[4];
+    cuuint32_t bx[5], es[5];
+    uint64_t stride = 2;
+    for (int i = 0; i < rank; ++i) {
+        gd[i] = dims[i];
+        bx[i] = box[i];
+        es[i] = 1;
+        if (i > 0) gs[i - 1] = stride;
+        stride *= dims[i];
+    }
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void *>(base), gd, gs, bx, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool tmap2(CUtensorMap *m, const void *base, uint64_t cols, uint64_t rows, uint32_t box_cols, uint32_t box_rows) {
+    const uint64_t d[2] = {cols, rows};
+    const uint32_t b[2] = {box_cols, box_rows};
+    return tmap(m, base, 2, d, b);
+}
+
+bool tmap4(CUtensorMap *m, const void *base, uint64_t c, uint64_t w, uint64_t h, uint64_t n, uint32_t bc, uint32_t bw,
+           uint32_t bh, uint32_t bn) {
+    const uint64_t d[4] = {c, w, h, n};
+    const uint32_t b[4] = {bc, bw, bh, bn};
+    return tmap(m, base, 4, d, b);
+}
+
+int bn_of(int n) { return n == 64 ? 64 : 128; }
+
+// Fills the TMA descriptors and tile geometry of one tcgen05 convolution and
+// returns the capacity bound on its M tiles (grid sizing), or -1 on failure.
+// x/y: block input/output; h1/h2: workspace intermediates; cap: patch capacity.
+int prepare_tc(int mode, ConvArgs &a, const lasnet_block_desc *d, const void *x, const void *y, const void *h1,
+               const void *h2, int cap) {
+    const int S = d->s, hs = S + 2, C = d->c_mid;
+    const uint64_t px = (uint64_t)d->n * d->h * d->w;
+    bool ok = tmap2(&a.tmap_b, a.w, a.K, a.N, 64, bn_of(a.N));
+    switch (mode) {
+        case CONV1_DYN: {
+            const bool whole = hs * hs <= 128 && (128 / (hs * hs)) * hs * hs >= 96;
+            a.units_per_patch = whole ? 1 : hs;
+            a.unit_rows = whole ? hs * hs : hs;
+            a.unit_halo_rows = whole ? hs : 1;
+            a.units_per_tile = 128 / a.unit_rows;
+            ok = ok && tmap4(&a.tmap_a, x, d->c_in, d->w, d->h, d->n, 64, hs, a.unit_halo_rows, 1);
+            ok = ok && tmap2(&a.tmap_out, h1, C, (uint64_t)cap * hs * hs, 64, a.units_per_tile * a.unit_rows);
+            const long units = (long)cap * a.units_per_patch;
+            return ok ? (int)((units + a.units_per_tile - 1) / a.units_per_tile) : -1;
+        }
+        case CONV2_DYN: {
+            a.units_per_tile = 128 / (S * S);
+            a.box_rows = a.units_per_tile * S * S;
+            ok = ok && tmap4(&a.tmap_a, h1, C, hs, hs, cap, 64, S, S, a.units_per_tile);
+            ok = ok && tmap2(&a.tmap_out, h2, C, (uint64_t)cap * S * S, 64, a.box_rows);
+            return ok ? (cap + a.units_per_tile - 1) / a.units_per_tile : -1;
+        }
+        case CONV3_DYN: {
+            a.units_per_tile = 128 / (S * S);
+            a.box_rows = a.units_per_tile * S * S;
+            ok = ok && tmap2(&a.tmap_a, h2, C, (uint64_t)cap * S * S, 64, a.box_rows);
+            ok = ok && tmap4(&a.tmap_res, x, d->c_out, d->w, d->h, d->n, 64, S, S, 1);
+            ok = ok && tmap4(&a.tmap_out, y, d->c_out, d->w, d->h, d->n, 64, S, S, 1);
+            return ok ? (cap + a.units_per_tile - 1) / a.units_per_tile : -1;
+        }
+        case CONV1_DENSE: {
+            ok = ok && tmap2(&a.tmap_a, x, d->c_in, px, 64, 128);
+            ok = ok && tmap2(&a.tmap_out, h1, C, px, 64, 128);
+            return ok ? (int)((px + 127) / 128) : -1;
+        }
+        case CONV2_DENSE: {
+            if (d->h * d->w <= 128) {
+                a.rows_h = d->h;
+                a.imgs_box = 128 / (d->h * d->w);
+                a.dense_tiles = (d->n + a.imgs_box - 1) / a.imgs_box;
+            } else {
+                a.rows_h = 128 / d->w;
+                a.imgs_box = 1;
+                a.dense_tiles = d->n * ((d->h + a.rows_h - 1) / a.rows_h);
+            }
+            a.box_rows = d->w * a.rows_h * a.imgs_box;
+            ok = ok && tmap4(&a.tmap_a, h1, C, d->w, d->h, d->n, 64, d->w, a.rows_h, a.imgs_box);
+            ok = ok && tmap4(&a.tmap_out, h2, C, d->w, d->h, d->n, 64, d->w, a.rows_h, a.imgs_box);
+            return ok ? a.dense_tiles : -1;
+        }
+        case CONV3_DENSE: {
+            ok = ok && tmap2(&a.tmap_a, h2, C, px, 64, 128);
+            ok = ok && tmap2(&a.tmap_res, x, d->c_out, px, 64, 128);
+            ok = ok && tmap2(&a.tmap_out, y, d->c_out, px, 64, 128);
+            return ok ? (int)((px + 127) / 128) : -1;
+        }
+    }
+    return -1;
+}
+
+// One convolution: tcgen05 kernel (bf16) or fp32 CUDA-core kernel.
+cudaError_t run_conv(const lasnet_block_desc *d, int mode, ConvArgs &a, int max_rows, const void *x, const void *y,
+                     const void *h1, const void *h2, int cap, cudaStream_t st) {
+    if (d->dtype == LASNET_BF16) {
+        const int tiles = prepare_tc(mode, a, d, x, y, h1, h2, cap);
+        if (tiles < 0) return cudaErrorInvalidValue;
+        KernelEvents ev(st);
+        return launch_conv_tc(mode, a, tiles, num_sms(), st);
+    }
+    KernelEvents ev(st);
+    return launch_conv_simt(mode, a, max_rows, st);
+}
+
+ConvArgs base_args(const lasnet_block_desc *d) {
+    ConvArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.n_img = d->n;
+    a.H = d->h;
+    a.W = d->w;
+    a.S = d->s;
+    a.Gh = (d->h + d->s - 1) / d->s;
+    a.Gw = (d->w + d->s - 1) / d->s;
+    return a;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *lasnet_status_str(lasnet_status st) {
+    switch (st) {
+        case LASNET_OK: return "LASNET_OK";
+        case LASNET_ERR_NULL: return "LASNET_ERR_NULL: a required pointer is NULL";
+        case LASNET_ERR_SHAPE: return "LASNET_ERR_SHAPE: non-positive or inconsistent sizes";
+        case LASNET_ERR_DOMAIN: return "LASNET_ERR_DOMAIN: S < 1, stride not in {1,2} or unknown dtype";
+        case LASNET_ERR_UNSUPPORTED: return "LASNET_ERR_UNSUPPORTED: configuration not built";
+        case LASNET_ERR_ALIAS: return "LASNET_ERR_ALIAS: y partially overlaps x";
+        case LASNET_ERR_WORKSPACE: return "LASNET_ERR_WORKSPACE: workspace missing or too small";
+        case LASNET_ERR_CUDA: return "LASNET_ERR_CUDA: a CUDA call failed";
+    }
+    return "LASNET_ERR_UNKNOWN";
+}
+
+int32_t lasnet_abi_version(void) { return LASNET_ABI_VERSION; }
+
+int32_t lasnet_last_launch_count(void) { return g_last_launches; }
+
+lasnet_status lasnet_set_kernel_events(void *const *events, int32_t n_pairs) {
+    if (n_pairs < 0) return LASNET_ERR_SHAPE;
+    if (n_pairs > 0 && !events) return LASNET_ERR_NULL;
+    g_events = n_pairs > 0 ? events : nullptr;
+    g_event_pairs = n_pairs;
+    g_event_next = 0;
+    return LASNET_OK;
+}
+
+size_t lasnet_compact_workspace_bytes(int32_t ncells) { return compact_workspace_bytes(ncells < 0 ? 0 : ncells); }
+
+size_t lasnet_dyn_workspace_bytes(const lasnet_block_desc *d, int32_t cap) {
+    if (check_desc(d) != LASNET_OK || cap < 0) return 0;
+    return dyn_ws_bytes(d, cap);
+}
+
+size_t lasnet_dense_workspace_bytes(const lasnet_block_desc *d) {
+    if (check_desc(d) != LASNET_OK) return 0;
+    return dense_ws_bytes(d);
+}
+
+lasnet_status lasnet_mask(const lasnet_block_desc *d, const void *x, const float *wm, float bm, uint8_t *mask,
+                          double *logits, lasnet_stream_t stream) {
+    lasnet_status s = check_desc(d);
+    if (s != LASNET_OK) return s;
+    if (!x || !wm || !mask) return LASNET_ERR_NULL;
+    if (d->stride != 1) return LASNET_ERR_UNSUPPORTED;
+    const int vec = d->dtype == LASNET_BF16 ? 8 : 4;
+    if (d->c_in % vec || misaligned(x)) return LASNET_ERR_UNSUPPORTED;
+    g_last_launches = 0;
+    if (d->n == 0) return LASNET_OK;
+    KernelEvents ev(reinterpret_cast<cudaStream_t>(stream));
+    cudaError_t e = launch_masker(d->dtype == LASNET_BF16, x, wm, bm, d->n, d->h, d->w, d->c_in, d->s, mask,
+                                  logits, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return LASNET_ERR_CUDA;
+    g_last_launches = 1;
+    return LASNET_OK;
+}
+
+size_t lasnet_mask_compact_workspace_bytes(const lasnet_block_desc *d) {
+    if (check_desc(d) != LASNET_OK) return 0;
+    return mask_compact_workspace_bytes((long)d->n * ((d->h + d->s - 1) / d->s) * ((d->w + d->s - 1) / d->s));
+}
+
+lasnet_status lasnet_mask_compact(const lasnet_block_desc *d, const void *x, const float *wm, float bm,
+                                  uint8_t *mask, double *logits, int32_t *idx, int32_t *count, void *ws,
+                                  size_t ws_bytes, lasnet_stream_t stream) {
+    lasnet_status s = check_desc(d);
+    if (s != LASNET_OK) return s;
+    if (!x || !wm || !idx || !count) return LASNET_ERR_NULL;
+    if (d->stride != 1) return LASNET_ERR_UNSUPPORTED;
+    const int vec = d->dtype == LASNET_BF16 ? 8 : 4;
+    if (d->c_in % vec || misaligned(x)) return LASNET_ERR_UNSUPPORTED;
+    if (!ws || ws_bytes < lasnet_mask_compact_workspace_bytes(d)) return LASNET_ERR_WORKSPACE;
+    g_last_launches = 0;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    KernelEvents ev(st);
+    cudaError_t e = launch_mask_compact(d->dtype == LASNET_BF16, x, wm, bm, d->n, d->h, d->w, d->c_in, d->s, mask,
+                                        logits, idx, count, ws, st);
+    if (e != cudaSuccess) return LASNET_ERR_CUDA;
+    g_last_launches = d->n > 0 ? 1 : 0;
+    return LASNET_OK;
+}
+
+lasnet_status lasnet_compact(const uint8_t *mask, int32_t ncells, int32_t *idx, int32_t *count, void *ws,
+                             size_t ws_bytes, lasnet_stream_t stream) {
+    if (ncells < 0) return LASNET_ERR_SHAPE;
+    if (!count || (ncells > 0 && (!mask || !idx))) return LASNET_ERR_NULL;
+    if (ncells > 0 && (!ws || ws_bytes < compact_workspace_bytes(ncells))) return LASNET_ERR_WORKSPACE;
+    cudaError_t e = cudaSuccess;
+    g_last_launches = 0;
+    KernelEvents ev(reinterpret_cast<cudaStream_t>(stream));
+    const int k = launch_compact(mask, ncells, idx, count, ws, reinterpret_cast<cudaStream_t>(stream), &e);
+    if (e != cudaSuccess) return LASNET_ERR_CUDA;
+    g_last_launches = k;
+    return LASNET_OK;
+}
+
+lasnet_status lasnet_dyn_block(const lasnet_block_desc *d, const lasnet_block_weights *w, const void *x, void *y,
+                               const int32_t *idx, const int32_t *count, int32_t cap, void *ws, size_t ws_bytes,
+                               lasnet_stream_t stream) {
+    lasnet_status s = check_desc(d);
+    if (s != LASNET_OK) return s;
+    if ((s = check_weights(w)) != LASNET_OK) return s;
+    if (!x || !y || !count || (cap > 0 && !idx)) return LASNET_ERR_NULL;
+    if (cap < 0) return LASNET_ERR_SHAPE;
+    const long ncells = (long)d->n * ((d->h + d->s - 1) / d->s) * ((d->w + d->s - 1) / d->s);
+    if (cap > ncells) return LASNET_ERR_SHAPE;
+    if ((s = check_channels(d)) != LASNET_OK) return s;
+    if (misaligned(x) || misaligned(y)) return LASNET_ERR_UNSUPPORTED;
+    const size_t e = elt_size(d->dtype);
+    const size_t xbytes = (size_t)d->n * d->h * d->w * d->c_in * e;
+    if ((s = check_alias(x, y, xbytes)) != LASNET_OK) return s;
+    const size_t need = dyn_ws_bytes(d, cap);
+    if (need > 0 && (!ws || ws_bytes < need)) return LASNET_ERR_WORKSPACE;
+
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    g_last_launches = 0;
+    if (x != y && xbytes) {
+        if (cudaMemcpyAsync(y, x, xbytes, cudaMemcpyDeviceToDevice, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    }
+    if (cap == 0 || d->n == 0) return LASNET_OK;
+
+    Carve cv{static_cast<uint8_t *>(ws)};
+    const int hs2 = (d->s + 2) * (d->s + 2), ss = d->s * d->s;
+    void *h1 = cv.take((size_t)cap * hs2 * d->c_mid * e);
+    void *h2 = cv.take((size_t)cap * ss * d->c_mid * e);
+
+    ConvArgs a = base_args(d);
+    a.idx = idx;
+    a.count = count;
+
+    // step 3: gather + conv1 over the halo rows of every active patch
+    a.a_src = x; a.w = w->w1; a.bias = w->b1; a.out = h1; a.resid = nullptr;
+    a.K = d->c_in; a.N = d->c_mid; a.a_ld = d->c_in; a.out_ld = d->c_mid;
+    if (run_conv(d, CONV1_DYN, a, cap * hs2, x, y, h1, h2, cap, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    // step 4: 3x3 conv on the gathered patch batch
+    a.a_src = h1; a.w = w->w2; a.bias = w->b2; a.out = h2;
+    a.K = 9 * d->c_mid; a.N = d->c_mid; a.a_ld = d->c_mid; a.out_ld = d->c_mid;
+    if (run_conv(d, CONV2_DYN, a, cap * ss, x, y, h1, h2, cap, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    // step 5: conv3 + residual add + scatter into y (reads the residual from x;
+    // when y == x every read of x by steps 3/5 precedes the write of its pixel)
+    a.a_src = h2; a.w = w->w3; a.bias = w->b3; a.out = y; a.resid = x;
+    a.K = d->c_mid; a.N = d->c_out; a.a_ld = d->c_mid; a.out_ld = d->c_out;
+    if (run_conv(d, CONV3_DYN, a, cap * ss, x, y, h1, h2, cap, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    g_last_launches = 3;
+    return LASNET_OK;
+}
+
+lasnet_status lasnet_dense_block(const lasnet_block_desc *d, const lasnet_block_weights *w, const void *x, void *y,
+                                 void *ws, size_t ws_bytes, lasnet_stream_t stream) {
+    lasnet_status s = check_desc(d);
+    if (s != LASNET_OK) return s;
+    if ((s = check_weights(w)) != LASNET_OK) return s;
+    if (!x || !y) return LASNET_ERR_NULL;
+    if ((s = check_channels(d)) != LASNET_OK) return s;
+    if (misaligned(x) || misaligned(y)) return LASNET_ERR_UNSUPPORTED;
+    const size_t e = elt_size(d->dtype);
+    const size_t xbytes = (size_t)d->n * d->h * d->w * d->c_in * e;
+    if ((s = check_alias(x, y, xbytes)) != LASNET_OK) return s;
+    const size_t need = dense_ws_bytes(d);
+    if (need > 0 && (!ws || ws_bytes < need)) return LASNET_ERR_WORKSPACE;
+    g_last_launches = 0;
+    if (d->n == 0) return LASNET_OK;
+
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    Carve cv{static_cast<uint8_t *>(ws)};
+    const int px = d->n * d->h * d->w;
+    void *h1 = cv.take((size_t)px * d->c_mid * e);
+    void *h2 = cv.take((size_t)px * d->c_mid * e);
+    ConvArgs a = base_args(d);
+    a.m_dense = px;
+
+    a.a_src = x; a.w = w->w1; a.bias = w->b1; a.out = h1;
+    a.K = d->c_in; a.N = d->c_mid; a.a_ld = d->c_in; a.out_ld = d->c_mid;
+    if (run_conv(d, CONV1_DENSE, a, px, x, y, h1, h2, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    a.a_src = h1; a.w = w->w2; a.bias = w->b2; a.out = h2;
+    a.K = 9 * d->c_mid; a.N = d->c_mid; a.a_ld = d->c_mid; a.out_ld = d->c_mid;
+    if (run_conv(d, CONV2_DENSE, a, px, x, y, h1, h2, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    a.a_src = h2; a.w = w->w3; a.bias = w->b3; a.out = y; a.resid = x;
+    a.K = d->c_mid; a.N = d->c_out; a.a_ld = d->c_mid; a.out_ld = d->c_out;
+    if (run_conv(d, CONV3_DENSE, a, px, x, y, h1, h2, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    g_last_launches = 3;
+    return LASNET_OK;
+}
+
+}  // extern "C"

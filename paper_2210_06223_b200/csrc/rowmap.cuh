@@ -1,0 +1,108 @@
+// rowmap.cuh -- how GEMM rows of the three convolutions map onto pixels.
+//
+// The dynamic block is run as three implicit GEMMs:
+//   conv1  rows = (active patch t, halo pixel j), j < (S+2)^2   K = c_in
+//   conv2  rows = (active patch t, output pixel j), j < S^2     K = 9*c_mid (3x3 taps on h1)
+//   conv3  rows = (active patch t, output pixel j)              K = c_mid, scatter-add epilogue
+// and the dense comparator uses rows = pixels for all three.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+
+namespace lasnet {
+
+enum ConvMode : int {
+    CONV1_DYN = 0,    // A = gathered halo rows of x, out = h1 [P][(S+2)^2][c_mid]
+    CONV2_DYN = 1,    // A = im2col of h1 patch windows, out = h2 [P][S^2][c_mid]
+    CONV3_DYN = 2,    // A = h2 rows, out = y pixels (residual add, ReLU, scatter)
+    CONV1_DENSE = 3,  // A = x pixel rows, out = h1 [n*h*w][c_mid]
+    CONV2_DENSE = 4,  // A = im2col of h1 with zero padding, out = h2 [n*h*w][c_mid]
+    CONV3_DENSE = 5,  // A = h2 rows, out = y (residual add, ReLU)
+};
+
+struct ConvArgs {
+    // TMA descriptors (tcgen05 path only; see conv_tc.cu for the box shapes)
+    CUtensorMap tmap_a;     // activation operand A (x, h1 or h2)
+    CUtensorMap tmap_b;     // weight matrix [N][K]
+    CUtensorMap tmap_out;   // output (h1, h2 or y)
+    CUtensorMap tmap_res;   // residual x (conv3)
+    const void *a_src;      // x (conv1), h1 (conv2), h2 (conv3)
+    const void *w;          // [N][K] row-major (K-major)
+    const float *bias;      // [N]
+    void *out;              // h1, h2 or y
+    const void *resid;      // x (conv3 epilogue)
+    const int32_t *idx;     // active cell ids (dynamic modes)
+    const int32_t *count;   // device count (dynamic modes)
+    int32_t m_dense;        // rows for dense modes
+    int32_t K, N;           // GEMM sizes
+    int32_t a_ld;           // elements per A source row (c_in for conv1, c_mid otherwise)
+    int32_t out_ld;         // elements per output row
+    int32_t n_img, H, W, S, Gh, Gw;
+    // tcgen05 tile geometry (host-computed)
+    int32_t units_per_tile;   // dynamic: TMA boxes (conv1) / patches (conv2, conv3) per 128-row tile
+    int32_t units_per_patch;  // conv1: 1 (whole halo box) or S+2 (one box per halo row)
+    int32_t unit_rows;        // conv1: GEMM rows per box
+    int32_t unit_halo_rows;   // conv1: halo rows per box
+    int32_t box_rows;         // rows one A box delivers (conv2 dyn/dense, conv3 dyn)
+    int32_t rows_h, imgs_box; // conv2 dense: image rows / images per box
+    int32_t dense_tiles;      // conv2 dense: M tiles
+};
+
+__host__ __device__ __forceinline__ int rows_per_patch(int mode, int S) {
+    return mode == CONV1_DYN ? (S + 2) * (S + 2) : S * S;
+}
+
+// Total GEMM rows; dynamic modes read the device-resident active count.
+__device__ __forceinline__ int gemm_rows(int mode, const ConvArgs &a) {
+    if (mode <= CONV3_DYN) return (*a.count) * rows_per_patch(mode, a.S);
+    return a.m_dense;
+}
+
+// Active cell t -> (image n, cell row gy, cell col gx).
+__device__ __forceinline__ void cell_coords(const ConvArgs &a, int t, int &n, int &gy, int &gx) {
+    int cell = a.idx[t];
+    int G = a.Gh * a.Gw;
+    n = cell / G;
+    int g = cell - n * G;
+    gy = g / a.Gw;
+    gx = g - gy * a.Gw;
+}
+
+// conv1 (dynamic): GEMM row -> source pixel of x, or -1 for a halo pixel outside
+// the image / a row past the end (zero row; the epilogue also writes 0, R6).
+__device__ __forceinline__ int halo_pixel(const ConvArgs &a, int r, int M) {
+    if (r >= M) return -1;
+    int hs = a.S + 2, hs2 = hs * hs;
+    int t = r / hs2, j = r - t * hs2;
+    int n, gy, gx;
+    cell_coords(a, t, n, gy, gx);
+    int jy = j / hs;
+    int hy = gy * a.S - 1 + jy, hx = gx * a.S - 1 + (j - jy * hs);
+    if (hy < 0 || hy >= a.H || hx < 0 || hx >= a.W) return -1;
+    return (n * a.H + hy) * a.W + hx;
+}
+
+// conv2 (dynamic): GEMM row -> h1 row of the window centre of output pixel j of patch t.
+__device__ __forceinline__ int conv2_center_row(const ConvArgs &a, int r, int M) {
+    if (r >= M) return -1;
+    int ss = a.S * a.S, hs = a.S + 2;
+    int t = r / ss, j = r - t * ss;
+    int py = j / a.S, px = j - py * a.S;
+    return t * hs * hs + (py + 1) * hs + (px + 1);
+}
+
+// conv3 (dynamic): GEMM row -> output pixel, or -1 when the patch is clipped at
+// the image border (R7) or the row is past the end.
+__device__ __forceinline__ int out_pixel(const ConvArgs &a, int r, int M) {
+    if (r >= M) return -1;
+    int ss = a.S * a.S;
+    int t = r / ss, j = r - t * ss;
+    int n, gy, gx;
+    cell_coords(a, t, n, gy, gx);
+    int py = j / a.S;
+    int yy = gy * a.S + py, xx = gx * a.S + (j - py * a.S);
+    if (yy >= a.H || xx >= a.W) return -1;
+    return (n * a.H + yy) * a.W + xx;
+}
+
+}  // namespace lasnet

@@ -1,0 +1,255 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle (-m gpu).
+
+Masks and indices: bit-exact.  Activations: max-abs-rel <= 2e-2 (bf16, fp32
+accumulation) or 1e-5 (fp32 path), per tensor; inactive pixels: bitwise x.
+Sizes span several 128-row tiles with ragged tails; the full-size config-2
+launch (the one bench.py times) is checked on sampled pixels.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from parity_util import (BF16_TOL, F32_TOL, make_case, margin_bias, max_abs_rel, rmode, tol, to_dev)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2210_06223_b200 import build, _lib
+    build.build()
+    _lib.load()
+    oracle.build()
+
+
+import paper_2210_06223_b200 as L  # noqa: E402
+
+
+# ------------------------------------------------------------------ step 1 --
+
+MASK_CASES = [
+    (1, 14, 14, 256, 2, "f32"),     # config 1
+    (2, 13, 11, 64, 4, "bf16"),     # ragged: clipped edge cells
+    (3, 9, 10, 128, 5, "bf16"),
+    (128, 28, 28, 512, 1, "bf16"),  # config 2, every S
+    (128, 28, 28, 512, 2, "bf16"),
+    (128, 28, 28, 512, 4, "bf16"),
+    (128, 28, 28, 512, 7, "bf16"),
+]
+
+
+@pytest.mark.parametrize("n,h,w,c,s,dtype", MASK_CASES)
+def test_mask_bit_exact(n, h, w, c, s, dtype):
+    x = synth.make_x(n, h, w, c, seed=s, dtype=dtype)
+    wm = synth.make_masker_weights(c, seed=s + 10)
+    xd = synth.to_f64(x)
+    _, l0 = oracle.masker(xd, synth.to_f64(wm), 0.0, s)
+    bm = margin_bias(l0, 0.5)
+    m_or, l_or = oracle.masker(xd, synth.to_f64(wm), bm, s)
+    m, lg = L.mask(x.cuda(), wm.cuda(), bm, s, logits=True)
+    m = m.cpu().numpy()
+    assert np.array_equal(m, m_or)
+    np.testing.assert_allclose(lg.cpu().numpy(), l_or, rtol=1e-12, atol=1e-12 * np.abs(l_or).max())
+    margin = np.abs(l_or).min()
+    assert margin > 1e-9 * np.abs(l_or).max()  # no cell inside the rounding band
+
+
+def test_mask_all_on_all_off():
+    x = synth.make_x(2, 8, 8, 64, seed=1)
+    wm = synth.make_masker_weights(64, seed=2)
+    assert L.mask(x.cuda(), wm.cuda(), 1e6, 2).sum().item() == 2 * 16
+    assert L.mask(x.cuda(), wm.cuda(), -1e6, 2).sum().item() == 0
+
+
+@pytest.mark.parametrize("n,h,w,c,s,dtype", MASK_CASES)
+def test_fused_mask_compact_bit_exact(n, h, w, c, s, dtype):
+    """Steps 1+2 in one launch: same mask, logits, idx and count as the oracle;
+    repeated calls reuse the self-resetting workspace."""
+    x = synth.make_x(n, h, w, c, seed=s + 1, dtype=dtype)
+    wm = synth.make_masker_weights(c, seed=s + 11)
+    xd = synth.to_f64(x)
+    _, l0 = oracle.masker(xd, synth.to_f64(wm), 0.0, s)
+    blk = L.DynBlock(L.BlockShape(n, h, w, c, 64, s, torch.float32 if dtype == "f32" else torch.bfloat16),
+                     synth.make_block_weights(c, 64, c, seed=1, dtype=dtype), wm, 0.0)
+    xg = x.cuda()
+    for r in (0.5, 0.2, 0.9):
+        blk.bm = margin_bias(l0, r)
+        blk.mask_compact(xg, want_logits=True)
+        m_or, l_or = oracle.masker(xd, synth.to_f64(wm), blk.bm, s)
+        idx_or, cnt = oracle.compact(m_or)
+        assert np.array_equal(blk.mask_buf.cpu().numpy(), m_or)
+        assert int(blk.count.item()) == cnt
+        assert np.array_equal(blk.idx[:cnt].cpu().numpy(), idx_or)
+        np.testing.assert_allclose(blk.logits.cpu().numpy(), l_or, rtol=1e-12, atol=1e-12 * np.abs(l_or).max())
+    assert int(blk.mcws.count_nonzero().item()) == 0  # workspace left zeroed
+
+
+# ------------------------------------------------------------------ step 2 --
+
+@pytest.mark.parametrize("ncells,r", [(1, 1.0), (7, 0.5), (4095, 0.3), (4096, 0.5), (4097, 0.9),
+                                      (100352, 0.5), (100352, 0.0), (100352, 1.0), (250001, 0.1)])
+def test_compact_bit_exact(ncells, r):
+    rng = np.random.default_rng(ncells)
+    m = (rng.random(ncells) < r).astype(np.uint8)
+    idx, count = L.compact(torch.from_numpy(m).cuda())
+    want, wc = oracle.compact(m)
+    c = int(count.item())
+    assert c == wc
+    assert np.array_equal(idx[:c].cpu().numpy(), want)
+
+
+def test_compact_empty():
+    m = torch.zeros(0, dtype=torch.uint8, device="cuda")
+    idx, count = L.compact(m)
+    assert int(count.item()) == 0
+
+
+# ---------------------------------------------------------------- steps 3-5 --
+
+def run_dyn(x, wts, mc, s, inplace=True):
+    xd = x.cuda()
+    idx, count = L.compact(torch.from_numpy(mc).cuda())
+    if inplace:
+        y = xd.clone()
+        L.dyn_block(y, to_dev(wts), idx, count, s)
+    else:
+        y = torch.empty_like(xd)
+        L.dyn_block(xd, to_dev(wts), idx, count, s, y=y)
+    return y
+
+
+DYN_CASES = [
+    # n, h, w, c_in, c_mid, s, r, dtype
+    (2, 14, 14, 256, 64, 2, 0.5, "bf16"),
+    (2, 14, 14, 256, 64, 1, 0.3, "bf16"),
+    (2, 14, 14, 256, 64, 4, 0.6, "bf16"),
+    (2, 14, 14, 256, 64, 7, 0.5, "bf16"),
+    (3, 13, 11, 128, 128, 3, 0.5, "bf16"),   # S not dividing H or W: clipped patches
+    (2, 10, 10, 128, 64, 4, 1.0, "bf16"),
+    (1, 7, 7, 512, 256, 1, 0.5, "bf16"),     # stage-4-like widths, N tile 256
+    (4, 28, 28, 512, 128, 4, 0.5, "bf16"),   # config-2 shape, reduced batch
+    (1, 14, 14, 256, 64, 2, 25 / 49, "f32"),  # config 1
+    (2, 9, 9, 128, 64, 2, 0.5, "f32"),
+]
+
+
+@pytest.mark.parametrize("n,h,w,c_in,c_mid,s,r,dtype", DYN_CASES)
+def test_dyn_block_matches_oracle(n, h, w, c_in, c_mid, s, r, dtype):
+    x, wts, _ = make_case(n, h, w, c_in, c_mid, s, seed=n * 100 + s, dtype=dtype)
+    gh, gw = L.grid(h, w, s)
+    mc = synth.make_cell_mask(n, gh, gw, r, seed=s)
+    y = run_dyn(x, wts, mc, s).cpu()
+    idx, _ = oracle.compact(mc)
+    want = oracle.dyn_block_literal(synth.to_f64(x), synth.weights_f64(wts), idx, s, rmode=rmode(dtype))
+    got = synth.to_f64(y)
+    up = oracle.upsample(mc, h, w, s).astype(bool)
+    assert max_abs_rel(got[up], want[up]) <= tol(dtype)
+    assert np.array_equal(got[~up], synth.to_f64(x)[~up])  # input fill, bitwise
+
+
+def test_dyn_block_clustered_mask():
+    n, h, w, s = 4, 28, 28, 4
+    x, wts, _ = make_case(n, h, w, 256, 64, s, seed=7)
+    mc = synth.make_cell_mask(n, 7, 7, 0.4, seed=3, family="clustered")
+    y = run_dyn(x, wts, mc, s).cpu()
+    want = oracle.dyn_block_def(synth.to_f64(x), synth.weights_f64(wts), mc, s)
+    assert max_abs_rel(synth.to_f64(y), want) <= BF16_TOL
+
+
+def test_in_place_equals_out_of_place():
+    x, wts, _ = make_case(2, 14, 14, 256, 64, 2, seed=3)
+    mc = synth.make_cell_mask(2, 7, 7, 0.5, seed=4)
+    a = run_dyn(x, wts, mc, 2, inplace=True)
+    b = run_dyn(x, wts, mc, 2, inplace=False)
+    assert torch.equal(a, b)
+
+
+def test_zero_mask_is_identity_bitwise():
+    x, wts, _ = make_case(2, 14, 14, 256, 64, 2, seed=5)
+    mc = np.zeros((2, 7, 7), np.uint8)
+    y = run_dyn(x, wts, mc, 2)
+    assert torch.equal(y.cpu(), x)
+
+
+def test_all_ones_equals_dense_comparator():
+    x, wts, _ = make_case(2, 14, 14, 256, 64, 2, seed=6)
+    mc = np.ones((2, 7, 7), np.uint8)
+    y = run_dyn(x, wts, mc, 2)
+    yd = L.dense_block(x.cuda(), to_dev(wts))
+    assert max_abs_rel(synth.to_f64(y.cpu()), synth.to_f64(yd.cpu())) <= 1e-2
+
+
+def test_granularity_equivalence_on_gpu():
+    """dyn(x, Mc, S) vs dyn(x, upsample(Mc, S), 1)."""
+    n, h, w, s = 2, 16, 16, 4
+    x, wts, _ = make_case(n, h, w, 128, 64, s, seed=8)
+    mc = synth.make_cell_mask(n, 4, 4, 0.5, seed=8)
+    up = oracle.upsample(mc, h, w, s)
+    a = run_dyn(x, wts, mc, s)
+    b = run_dyn(x, wts, up, 1)
+    assert max_abs_rel(synth.to_f64(a.cpu()), synth.to_f64(b.cpu())) <= 1e-2
+
+
+@pytest.mark.parametrize("n,h,w,c_in,c_mid,dtype", [(2, 14, 14, 256, 64, "bf16"), (3, 9, 7, 128, 128, "bf16"),
+                                                     (1, 14, 14, 256, 64, "f32")])
+def test_dense_block_matches_oracle(n, h, w, c_in, c_mid, dtype):
+    x, wts, _ = make_case(n, h, w, c_in, c_mid, 1, seed=9, dtype=dtype)
+    y = L.dense_block(x.cuda(), to_dev(wts)).cpu()
+    want = oracle.static_block(synth.to_f64(x), synth.weights_f64(wts), rmode=rmode(dtype))
+    assert max_abs_rel(synth.to_f64(y), want) <= tol(dtype)
+
+
+def test_five_steps_end_to_end_masker_driven():
+    """Full path with the masker deciding: mask -> compact -> dyn block."""
+    n, h, w, c, s = 4, 28, 28, 256, 4
+    x, wts, wm = make_case(n, h, w, c, 64, s, seed=11)
+    xd = synth.to_f64(x)
+    _, l0 = oracle.masker(xd, synth.to_f64(wm), 0.0, s)
+    bm = margin_bias(l0, 0.5)
+    blk = L.DynBlock(L.BlockShape(n, h, w, c, 64, s), wts, wm, bm)
+    y = x.cuda().clone()
+    blk.forward(y)
+    m_or, _ = oracle.masker(xd, synth.to_f64(wm), bm, s)
+    assert np.array_equal(blk.mask_buf.cpu().numpy(), m_or)
+    idx_or, cnt = oracle.compact(m_or)
+    assert int(blk.count.item()) == cnt
+    assert np.array_equal(blk.idx[:cnt].cpu().numpy(), idx_or)
+    want = oracle.dyn_block_literal(xd, synth.weights_f64(wts), idx_or, s)
+    assert max_abs_rel(synth.to_f64(y.cpu()), want) <= BF16_TOL
+
+
+@pytest.mark.parametrize("s", [1, 2, 4, 7])
+def test_full_size_config2_sampled(s):
+    """Config 2 at full size (N=128, 28x28x512, C=128) in the launch configuration
+    bench.py times; checked on sampled output pixels the oracle computes one by one."""
+    n, h, w, c_in, c_mid = 128, 28, 28, 512, 128
+    x, wts, wm = make_case(n, h, w, c_in, c_mid, s, seed=20 + s)
+    blk = L.DynBlock(L.BlockShape(n, h, w, c_in, c_mid, s), wts, wm, 0.0)
+    xg = x.cuda()
+    blk.calibrate_bias(xg, 0.5)
+    y = xg.clone()
+    blk.forward(y)
+    torch.cuda.synchronize()
+    mc = blk.mask_buf.cpu().numpy()
+    xd = synth.to_f64(x)
+    m_or, l_or = oracle.masker(xd, synth.to_f64(wm), blk.bm, s)
+    assert np.array_equal(mc, m_or)
+    wd = synth.weights_f64(wts)
+    yc = synth.to_f64(y.cpu())
+    rng = np.random.default_rng(s)
+    worst = 0.0
+    active = 0
+    for _ in range(96):
+        i, yy, xx = int(rng.integers(n)), int(rng.integers(h)), int(rng.integers(w))
+        want, act = oracle.block_pixel(xd, wd, mc, s, i, yy, xx)
+        if act:
+            active += 1
+            worst = max(worst, float(np.abs(yc[i, yy, xx] - want).max() / max(np.abs(want).max(), 1e-30)))
+        else:
+            assert np.array_equal(yc[i, yy, xx], xd[i, yy, xx])
+    assert active > 20
+    assert worst <= BF16_TOL
