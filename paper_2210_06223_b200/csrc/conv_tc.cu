@@ -2,27 +2,29 @@
 // LASNet bottleneck, bf16 x bf16 -> fp32 (TMEM) -> bf16, all operands moved by TMA.
 //
 // One persistent, warp-specialised kernel template serves the six modes of
-// rowmap.cuh.  Per CTA (1 per SM, 192 threads):
+// rowmap.cuh.  Per CTA (1 per SM):
 //   warps 0-3  epilogue: tcgen05.ld the fp32 accumulator (thread = GEMM row =
 //              TMEM lane), + bias [+ residual], ReLU, bf16 RNE into a 128-B-
-//              swizzled smem staging tile, then one thread TMA-stores it
-//   warp 4     producer: one thread issues every TMA load -- the weight tile B
-//              (2-D box) and the activation tile A, whose box shape does the
-//              gather/im2col:
-//                conv1 dyn   one 4-D box {64, S+2, S+2|1, 1} of x per patch
-//                            (or per halo row), OOB halo pixels zero-filled
-//                conv2 dyn   one 4-D box {64, S, S, patches} of h1 per tap
-//                conv2 dense one 4-D box {64, W, rows, imgs} of h1 per tap,
-//                            the zero padding is TMA's OOB fill
-//                others      one 2-D box {64, 128} of a contiguous row matrix
-//              and, for conv3, the residual tile of x into the staging buffer
-//              (per-patch 4-D boxes in dynamic mode: the scatter is the store)
+//              swizzled smem staging tile.  conv1/conv2: one thread TMA-stores
+//              the tile (contiguous h1/h2 rows).  conv3: each warp prefetches
+//              the residual rows of x for the NEXT tile with cp.async, and
+//              writes its 32 output pixels with coalesced 16-B stores -- the
+//              scatter-add is this epilogue
+//   warp 4     TMA producer: the weight tile B (2-D box) every K-block and the
+//              activation tile A where a box does the job:
+//                conv2 dyn   one 4-D box {64, S, S, patches} of h1 per tap (im2col)
+//                conv2 dense one 4-D box {64, W, rows, imgs} of h1 per tap, the
+//                            zero padding is TMA's out-of-bounds fill
+//                conv1 dense, conv3   one 2-D box {64, 128} of contiguous rows
+//   warps 6-9  (conv1 dyn only) cp.async gather of the halo rows of x: small
+//              scattered rows are where TMA's per-box cost dominates, 16-B
+//              LDGSTS keep the HBM pipe full
 //   warp 5     TMEM allocator + single-thread tcgen05.mma issuer
 // Pipelines: ST smem stages (full/empty mbarriers), two TMEM accumulators
-// (tmem_full/tmem_empty) and two staging buffers (stage_full/stage_empty), so
-// loads, MMAs, epilogue math and TMA stores of consecutive tiles overlap.
-// Dynamic modes derive their tile count from the device-resident active count:
-// no host synchronisation (the index list spreads work evenly).
+// (tmem_full/tmem_empty) and two staging buffers, so loads, MMAs, epilogue math
+// and stores of consecutive tiles overlap.  Dynamic modes derive their tile
+// count from the device-resident active count: no host synchronisation
+// (the index list spreads work evenly over the SMs).
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -35,29 +37,61 @@ namespace lasnet {
 
 using namespace ptx;
 
+#ifdef LASNET_TRACE
+// Debug timeline of CTA 0 (trace builds only): per local tile, globaltimer ns at
+// [0] producer tile start [1] producer K loads issued [2] MMA acc free
+// [3] MMA last commit [4] epilogue acc ready [5] epilogue staged [6] store issued
+__device__ unsigned long long g_trace[64 * 8];
+__device__ unsigned long long g_ktrace[128 * 4];  // per K-block: gather issue, TMA issue, MMA full, MMA commit
+__device__ int g_trace_mode = -1;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define KTRACE(it, k) \
+    do { if (blockIdx.x == 0 && (it) < 128 && MODE == g_trace_mode) g_ktrace[(it) * 4 + (k)] = gtimer(); } while (0)
+#define TRACE(lt, k) \
+    do { if (blockIdx.x == 0 && (lt) < 64 && MODE == g_trace_mode) g_trace[(lt) * 8 + (k)] = gtimer(); } while (0)
+#else
+#define TRACE(lt, k) do { } while (0)
+#define KTRACE(it, k) do { } while (0)
+#endif
+
 constexpr int kBM = 128;       // UMMA M (rows per tile = TMEM lanes)
 constexpr int kBK = 64;        // K elements per stage = one 128-B swizzle row
-constexpr int kThreads = 192;  // 4 epilogue + 1 producer + 1 MMA warps
 constexpr int kABytes = kBM * kBK * 2;
 constexpr int kChunkBytes = kBM * 128;  // one 64-column bf16 chunk of a 128-row tile
 
-template <int BN> struct TileCfg {
-    static constexpr int kStages = BN == 128 ? 4 : 6;
+// Per-mode configuration.  Warp roles: [0, E) epilogue, E TMA producer,
+// E+1 MMA issuer, E+2 .. E+9 cp.async gather (conv1 dyn only).
+template <int MODE, int BN> struct Cfg {
+    static constexpr bool kResid = MODE == CONV3_DYN || MODE == CONV3_DENSE;
+    static constexpr bool kGather = MODE == CONV1_DYN;
+    static constexpr int kEpiWarps = kResid ? 8 : 4;
+    static constexpr int kProdWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1, kGatherWarp0 = kEpiWarps + 2;
+    static constexpr int kGatherThreads = 256;
+    static constexpr int kThreads = 32 * (kEpiWarps + 2) + (kGather ? kGatherThreads : 0);
     static constexpr int kBBytes = BN * kBK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kStagingBytes = (BN / 64) * kChunkBytes;
+    // conv1 dyn: HBM gather -> deep pipeline, 1 staging buffer (TMA store drains fast)
+    // conv3: short K (2-8 blocks) -> 3 stages, 3 staging buffers (residual prefetched 2 tiles ahead)
+    static constexpr int kStaging = kGather ? 1 : (kResid ? 3 : 2);
+    static constexpr int kStages = kGather ? (BN == 128 ? 6 : 8) : (kResid ? 3 : (BN == 128 ? 4 : 6));
     static constexpr int kTmemCols = 2 * BN;
     static constexpr int kStagingOff = kStages * kStageBytes;
-    static constexpr int kBarOff = kStagingOff + 2 * kStagingBytes;
+    static constexpr int kBarOff = kStagingOff + kStaging * kStagingBytes;
     static constexpr int kBiasOff = kBarOff + 256;
     static constexpr int smem_bytes(int n) { return 1024 + kBiasOff + n * 4; }
 };
 
+template <int MODE, int BN> __host__ __device__ constexpr int threads_of() { return Cfg<MODE, BN>::kThreads; }
+
 // Tile geometry shared by all roles.
 struct TileGeo {
-    int num_tiles;    // total tiles (M tiles x N tiles)
-    int n_tiles_n;    // N / BN
-    int units_total;  // dynamic modes: units (boxes) overall
+    int num_tiles;  // total tiles (M tiles x N tiles)
+    int n_tiles_n;  // N / BN
 };
 
 template <int MODE>
@@ -65,18 +99,12 @@ __device__ __forceinline__ TileGeo tile_geo(const ConvArgs &a, int BN) {
     TileGeo g;
     g.n_tiles_n = a.N / BN;
     int mt;
-    if (MODE == CONV1_DYN) {
-        g.units_total = (*a.count) * a.units_per_patch;
-        mt = (g.units_total + a.units_per_tile - 1) / a.units_per_tile;
-    } else if (MODE == CONV2_DYN || MODE == CONV3_DYN) {
-        g.units_total = *a.count;  // units = patches
-        mt = (g.units_total + a.units_per_tile - 1) / a.units_per_tile;
+    if (MODE == CONV2_DYN) {
+        mt = (*a.count + a.units_per_tile - 1) / a.units_per_tile;  // patch-aligned tiles
     } else if (MODE == CONV2_DENSE) {
-        g.units_total = 0;
         mt = a.dense_tiles;
     } else {
-        g.units_total = 0;
-        mt = (a.m_dense + kBM - 1) / kBM;
+        mt = (gemm_rows(MODE, a) + kBM - 1) / kBM;
     }
     g.num_tiles = mt * g.n_tiles_n;
     return g;
@@ -95,49 +123,47 @@ __device__ __forceinline__ void dense2_tile(const ConvArgs &a, int mt, int &n0, 
 }
 
 template <int MODE, int BN>
-__global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_constant__ ConvArgs args) {
-    using Cfg = TileCfg<BN>;
-    constexpr int ST = Cfg::kStages;
-    constexpr bool kResid = (MODE == CONV3_DYN || MODE == CONV3_DENSE);
+__global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(const __grid_constant__ ConvArgs args) {
+    using C = Cfg<MODE, BN>;
+    constexpr int ST = C::kStages, NSTG = C::kStaging, EPI = C::kEpiWarps * 32;
+    constexpr bool kResid = C::kResid;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_u32 = smem_u32(smem_raw);
     const uint32_t sbase = (raw_u32 + 1023u) & ~1023u;
     uint8_t *sgen = smem_raw + (sbase - raw_u32);
 
-    const uint32_t staging = sbase + Cfg::kStagingOff;      // 2 x kStagingBytes
-    const uint32_t bar_full = sbase + Cfg::kBarOff;         // ST
-    const uint32_t bar_empty = bar_full + ST * 8;           // ST
-    const uint32_t bar_tfull = bar_empty + ST * 8;          // 2
-    const uint32_t bar_tempty = bar_tfull + 16;             // 2
-    const uint32_t bar_sfull = bar_tempty + 16;             // 2 (conv3: residual landed)
-    const uint32_t bar_sempty = bar_sfull + 16;             // 2 (staging free again)
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sgen + Cfg::kBarOff + ST * 16 + 64);
-    float *bias_s = reinterpret_cast<float *>(sgen + Cfg::kBiasOff);
+    const uint32_t staging = sbase + C::kStagingOff;  // NSTG x kStagingBytes
+    const uint32_t bar_full = sbase + C::kBarOff;     // ST
+    const uint32_t bar_empty = bar_full + ST * 8;     // ST
+    const uint32_t bar_tfull = bar_empty + ST * 8;    // 2
+    const uint32_t bar_tempty = bar_tfull + 16;       // 2
+    const uint32_t bar_sempty = bar_tempty + 16;      // 2 (TMA-store modes: staging free again)
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sgen + C::kBarOff + ST * 16 + 64);
+    float *bias_s = reinterpret_cast<float *>(sgen + C::kBiasOff);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
 
-    for (int i = tid; i < args.N; i += kThreads) bias_s[i] = args.bias[i];
+    for (int i = tid; i < args.N; i += C::kThreads) bias_s[i] = args.bias[i];
     if (tid == 0) {
         for (int s = 0; s < ST; ++s) {
-            mbar_init(bar_full + 8 * s, 1);   // producer arrive.expect_tx
+            // TMA producer's arrive.expect_tx (+ one noinc arrival per gather thread for conv1 dyn)
+            mbar_init(bar_full + 8 * s, C::kGather ? C::kGatherThreads + 1 : 1);
             mbar_init(bar_empty + 8 * s, 1);  // tcgen05.commit
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(bar_tfull + 8 * a, 1);     // tcgen05.commit
-            mbar_init(bar_tempty + 8 * a, 128);  // every epilogue thread
-            mbar_init(bar_sfull + 8 * a, 1);     // producer arrive.expect_tx (residual)
+            mbar_init(bar_tempty + 8 * a, EPI);  // every epilogue thread
             mbar_init(bar_sempty + 8 * a, 1);    // store thread, after the TMA store read smem
         }
         fence_mbar_init();
     }
-    if (warp == 4 && lane == 0) {
-        tma_prefetch_desc(&args.tmap_a);
+    if (warp == C::kProdWarp && lane == 0) {
+        if (!C::kGather) tma_prefetch_desc(&args.tmap_a);
         tma_prefetch_desc(&args.tmap_b);
-        tma_prefetch_desc(&args.tmap_out);
-        if (kResid) tma_prefetch_desc(&args.tmap_res);
+        if (!kResid) tma_prefetch_desc(&args.tmap_out);
     }
-    if (warp == 5) tmem_alloc<Cfg::kTmemCols>(smem_u32(tmem_slot));
+    if (warp == C::kMmaWarp) tmem_alloc<C::kTmemCols>(smem_u32(tmem_slot));
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -147,87 +173,108 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     const int num_kb = args.K / kBK;
     const int kpt = args.a_ld / kBK;  // K-blocks per 3x3 tap (conv2)
 
-    if (warp == 4) {
-        // ------------------------------------------------------- producer --
+    if (warp == C::kProdWarp) {
+        // --------------------------------------------------- TMA producer --
         if (lane == 0) {
             int it = 0, lt = 0;
             for (int tile = blockIdx.x; tile < geo.num_tiles; tile += gridDim.x, ++lt) {
                 const int mt = tile / geo.n_tiles_n;
                 const int n0 = (tile - mt * geo.n_tiles_n) * BN;
-                int u0 = 0, nu = 0;  // first unit and unit count of this tile (dynamic modes)
-                if (MODE == CONV1_DYN || MODE == CONV2_DYN || MODE == CONV3_DYN) {
-                    u0 = mt * args.units_per_tile;
-                    nu = min(args.units_per_tile, geo.units_total - u0);
-                }
+                const int u0 = MODE == CONV2_DYN ? mt * args.units_per_tile : 0;  // first patch (conv2 dyn)
                 int d2n = 0, d2y = 0;
                 if (MODE == CONV2_DENSE) dense2_tile(args, mt, d2n, d2y);
+                TRACE(lt, 0);
                 for (int kb = 0; kb < num_kb; ++kb, ++it) {
                     const int stage = it % ST;
                     mbar_wait(bar_empty + 8 * stage, ((it / ST) & 1) ^ 1);
-                    const uint32_t sa = sbase + stage * Cfg::kStageBytes;
+                    const uint32_t sa = sbase + stage * C::kStageBytes;
                     const uint32_t sb = sa + kABytes;
                     const uint32_t fb = bar_full + 8 * stage;
-                    int a_bytes;
-                    if (MODE == CONV1_DYN) {
-                        a_bytes = nu * args.unit_rows * 128;
-                    } else if (MODE == CONV2_DYN || MODE == CONV3_DYN) {
-                        a_bytes = args.box_rows * 128;  // one box (garbage rows past count are never stored)
-                    } else if (MODE == CONV2_DENSE) {
-                        a_bytes = args.box_rows * 128;
-                    } else {
-                        a_bytes = kABytes;
-                    }
-                    mbar_arrive_expect_tx(fb, a_bytes + Cfg::kBBytes);
+                    int a_bytes = kABytes;  // conv1 dyn: A arrives by cp.async (not counted here)
+                    if (C::kGather) a_bytes = 0;
+                    else if (MODE == CONV2_DYN || MODE == CONV2_DENSE) a_bytes = args.box_rows * 128;
+                    mbar_arrive_expect_tx(fb, a_bytes + C::kBBytes);
                     tma_load_2d(sb, &args.tmap_b, fb, kb * kBK, n0);
-                    if (MODE == CONV1_DYN) {
-                        const int c0 = kb * kBK;
-                        for (int u = 0; u < nu; ++u) {
-                            const int unit = u0 + u;
-                            const int t = unit / args.units_per_patch;
-                            const int jy = (unit - t * args.units_per_patch) * args.unit_halo_rows;
-                            int n, gy, gx;
-                            cell_coords(args, t, n, gy, gx);
-                            tma_load_4d(sa + u * args.unit_rows * 128, &args.tmap_a, fb, c0, gx * args.S - 1,
-                                        gy * args.S - 1 + jy, n);
-                        }
-                    } else if (MODE == CONV2_DYN) {
+                    KTRACE(it, 1);
+                    if (MODE == CONV2_DYN) {
                         const int tap = kb / kpt, dy = tap / 3, dx = tap - dy * 3;
                         tma_load_4d(sa, &args.tmap_a, fb, (kb - tap * kpt) * kBK, dx, dy, u0);
                     } else if (MODE == CONV2_DENSE) {
                         const int tap = kb / kpt, dy = tap / 3, dx = tap - dy * 3;
                         tma_load_4d(sa, &args.tmap_a, fb, (kb - tap * kpt) * kBK, dx - 1, d2y + dy - 1, d2n);
-                    } else if (MODE == CONV3_DYN) {
-                        tma_load_2d(sa, &args.tmap_a, fb, kb * kBK, u0 * args.S * args.S);
-                    } else {
+                    } else if (!C::kGather) {
                         tma_load_2d(sa, &args.tmap_a, fb, kb * kBK, mt * kBM);
                     }
                 }
-                if (kResid) {
-                    // residual tile of x -> staging buffer lt&1 (the epilogue adds it in place);
-                    // issued after the K loads so MMA(lt) overlaps the epilogue of lt-1
-                    const int b = lt & 1;
-                    mbar_wait(bar_sempty + 8 * b, ((lt >> 1) & 1) ^ 1);
-                    const uint32_t sdst = staging + b * Cfg::kStagingBytes;
-                    if (MODE == CONV3_DYN) {
-                        const int box_bytes = args.S * args.S * 128;
-                        mbar_arrive_expect_tx(bar_sfull + 8 * b, nu * (BN / 64) * box_bytes);
-                        for (int p = 0; p < nu; ++p) {
-                            int n, gy, gx;
-                            cell_coords(args, u0 + p, n, gy, gx);
-                            for (int c = 0; c < BN / 64; ++c)
-                                tma_load_4d(sdst + c * kChunkBytes + p * box_bytes, &args.tmap_res, bar_sfull + 8 * b,
-                                            n0 + c * 64, gx * args.S, gy * args.S, n);
-                        }
-                    } else {
-                        mbar_arrive_expect_tx(bar_sfull + 8 * b, (BN / 64) * kChunkBytes);
-                        for (int c = 0; c < BN / 64; ++c)
-                            tma_load_2d(sdst + c * kChunkBytes, &args.tmap_res, bar_sfull + 8 * b, n0 + c * 64,
-                                        mt * kBM);
-                    }
-                }
+                TRACE(lt, 1);
             }
         }
-    } else if (warp == 5) {
+    } else if (C::kGather && warp >= C::kGatherWarp0) {
+        // ------------------------------------------ cp.async halo gather --
+        // thread -> (row group prow, 16-B chunk pch); rows prow + 32 i, i < 4.
+        // The idx loads of tile t+1 are issued before the K-loop of tile t and
+        // decoded after it, so row mapping never sits on the critical path.
+        constexpr int RPT = 128 * 8 / C::kGatherThreads;  // rows per thread
+        constexpr int RSTEP = 128 / RPT;
+        const int pt = tid - 32 * C::kGatherWarp0;
+        const int prow = pt >> 3, pch = pt & 7;
+        const __nv_bfloat16 *X = static_cast<const __nv_bfloat16 *>(args.a_src);
+        const int M = gemm_rows(MODE, args);
+        const int hs = args.S + 2, hs2 = hs * hs;
+        auto load_cells = [&](int tile, int (&cell)[RPT], int (&jj)[RPT]) {
+            const int r0 = (tile / geo.n_tiles_n) * kBM + prow;
+            int t = args.fd_hs2.div(r0), j = r0 - t * hs2;
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const int r = r0 + RSTEP * i;
+                cell[i] = -1;
+                if (tile < geo.num_tiles && r < M) cell[i] = ld_nc_volatile(args.idx + t);  // stays before the K-loop
+                jj[i] = j;
+                j += RSTEP;
+                while (j >= hs2) {
+                    j -= hs2;
+                    ++t;
+                }
+            }
+        };
+        auto decode = [&](const int (&cell)[RPT], const int (&jj)[RPT], int (&src)[RPT]) {
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                src[i] = -1;
+                if (cell[i] >= 0) {
+                    int n, gy, gx;
+                    cell_decode(args, cell[i], n, gy, gx);
+                    const int jy = args.fd_hs.div(jj[i]);
+                    const int hy = gy * args.S - 1 + jy, hx = gx * args.S - 1 + (jj[i] - jy * hs);
+                    if (hy >= 0 && hy < args.H && hx >= 0 && hx < args.W) src[i] = (n * args.H + hy) * args.W + hx;
+                }
+            }
+        };
+        int cell[RPT], jj[RPT], src[RPT], src_next[RPT];
+        load_cells(blockIdx.x, cell, jj);
+        decode(cell, jj, src);
+        int it = 0;
+        for (int tile = blockIdx.x; tile < geo.num_tiles; tile += gridDim.x) {
+            load_cells(tile + gridDim.x, cell, jj);  // next tile: loads in flight during this K-loop
+            for (int kb = 0; kb < num_kb; ++kb, ++it) {
+                const int stage = it % ST;
+                mbar_wait(bar_empty + 8 * stage, ((it / ST) & 1) ^ 1);
+                const uint32_t sa = sbase + stage * C::kStageBytes;
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                    const int row = prow + RSTEP * i;
+                    const bool ok = src[i] >= 0;
+                    const __nv_bfloat16 *g = ok ? X + (size_t)src[i] * args.a_ld + kb * kBK + pch * 8 : X;
+                    cp_async_16(sa + row * 128 + ((pch ^ (row & 7)) << 4), g, ok ? 16u : 0u);
+                }
+                cp_async_arrive_noinc(bar_full + 8 * stage);
+                if (pt == 0) KTRACE(it, 0);
+                if (kb == (num_kb >> 1)) decode(cell, jj, src_next);  // mid-loop: off the tile boundary
+            }
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) src[i] = src_next[i];
+        }
+    } else if (warp == C::kMmaWarp) {
         // ---------------------------------------------------- MMA issuer --
         if (lane == 0) {
             constexpr uint32_t idesc = idesc_bf16_f32(kBM, BN);
@@ -236,12 +283,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                 const int acc = lt & 1;
                 mbar_wait(bar_tempty + 8 * acc, ((lt >> 1) & 1) ^ 1);
                 tc_fence_after();
+                TRACE(lt, 2);
                 const uint32_t d_tmem = tmem_base + acc * BN;
                 for (int kb = 0; kb < num_kb; ++kb, ++it) {
                     const int stage = it % ST;
                     mbar_wait(bar_full + 8 * stage, (it / ST) & 1);
+                    KTRACE(it, 2);
+                    if (C::kGather) fence_proxy_async_smem();  // cp.async (generic) -> tcgen05 (async)
                     tc_fence_after();
-                    const uint32_t sa = sbase + stage * Cfg::kStageBytes;
+                    const uint32_t sa = sbase + stage * C::kStageBytes;
                     const uint64_t adesc = smem_desc_sw128(sa);
                     const uint64_t bdesc = smem_desc_sw128(sa + kABytes);
 #pragma unroll
@@ -250,43 +300,77 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                     mma_commit(bar_empty + 8 * stage);
                 }
                 mma_commit(bar_tfull + 8 * acc);
+                TRACE(lt, 3);
             }
         }
         __syncwarp();
-    } else {
+    } else if (warp < C::kEpiWarps) {
         // ------------------------------------------------------- epilogue --
-        const int r = tid;  // tile row == TMEM lane
-        const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+        // warp -> TMEM lane quarter (warp % 4) and column range [c_lo, c_hi)
+        const int quarter = warp & 3;
+        const int r = quarter * 32 + lane;  // tile row == TMEM lane
+        constexpr int kCols = BN / (C::kEpiWarps / 4);
+        const int c_lo = (warp >> 2) * kCols;
+        const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+        const int M = gemm_rows(MODE, args);
+        const __nv_bfloat16 *X = static_cast<const __nv_bfloat16 *>(args.resid);
+        __nv_bfloat16 *Y = static_cast<__nv_bfloat16 *>(args.out);
+        // conv3: output pixel of GEMM row m (or -1: past the end / clipped patch, R7)
+        auto pixel_of = [&](int m) -> int {
+            if (MODE == CONV3_DYN) return out_pixel(args, m, M);
+            return m < M ? m : -1;
+        };
+        // conv3: rows x 16-B chunks of this warp's [32 rows] x [kCols columns] block
+        constexpr int kChunks = kCols / 8;
+        constexpr int kRowsPerIt = 32 / kChunks;
+        auto chunk_addr = [&](uint32_t buf, int rl, int c16) -> uint32_t {
+            const int row = quarter * 32 + rl;
+            const int col = c_lo + c16 * 8;  // column within the tile
+            return buf + (col >> 6) * kChunkBytes + row * 128 + ((((col & 63) >> 3) ^ (row & 7)) << 4);
+        };
+        auto prefetch_resid = [&](int tl, uint32_t buf) {
+            const int m0 = (tl / geo.n_tiles_n) * kBM, n0 = (tl % geo.n_tiles_n) * BN;
+            const int mypix = pixel_of(m0 + r);
+#pragma unroll
+            for (int i = 0; i < 32 / kRowsPerIt; ++i) {
+                const int rl = i * kRowsPerIt + lane / kChunks, c16 = lane % kChunks;
+                const int pix = __shfl_sync(0xffffffffu, mypix, rl);
+                const __nv_bfloat16 *g = pix >= 0 ? X + (size_t)pix * args.out_ld + n0 + c_lo + c16 * 8 : X;
+                cp_async_16(chunk_addr(buf, rl, c16), g, pix >= 0 ? 16u : 0u);
+            }
+            cp_async_commit();
+        };
         int lt = 0;
+        if (kResid) {  // residual of the first two tiles
+            for (int k = 0; k < NSTG - 1; ++k) {
+                const int tl = blockIdx.x + k * gridDim.x;
+                if (tl < geo.num_tiles) prefetch_resid(tl, staging + k * C::kStagingBytes);
+                else cp_async_commit();
+            }
+        }
         for (int tile = blockIdx.x; tile < geo.num_tiles; tile += gridDim.x, ++lt) {
             const int mt = tile / geo.n_tiles_n;
             const int n0 = (tile - mt * geo.n_tiles_n) * BN;
-            const int acc = lt & 1, b = lt & 1;
-            const uint32_t sbuf = staging + b * Cfg::kStagingBytes;
+            const int acc = lt & 1, b = lt % NSTG;
+            const uint32_t sbuf = staging + b * C::kStagingBytes;
             bool zero = false;  // conv1: halo pixel outside the image stores 0 (R6)
-            if (MODE == CONV1_DYN) {
-                const int u = r / args.unit_rows, q = r - u * args.unit_rows;
-                const int unit = mt * args.units_per_tile + u;
-                if (u < args.units_per_tile && unit < geo.units_total) {
-                    const int t = unit / args.units_per_patch;
-                    const int hs = args.S + 2;
-                    const int j = (unit - t * args.units_per_patch) * args.unit_rows + q;  // halo index
-                    const int jy = j / hs, jx = j - jy * hs;
-                    int n, gy, gx;
-                    cell_coords(args, t, n, gy, gx);
-                    const int hy = gy * args.S - 1 + jy, hx = gx * args.S - 1 + jx;
-                    zero = hy < 0 || hy >= args.H || hx < 0 || hx >= args.W;
-                }
-            }
+            if (MODE == CONV1_DYN) zero = mt * kBM + r < M && halo_pixel(args, mt * kBM + r, M) < 0;
             if (kResid) {
-                mbar_wait(bar_sfull + 8 * b, (lt >> 1) & 1);
+                // prefetch tile lt+NSTG-1 into the buffer tile lt-1 used, then wait for tile lt's group
+                const int nxt = tile + (NSTG - 1) * gridDim.x;
+                if (nxt < geo.num_tiles) prefetch_resid(nxt, staging + ((lt + NSTG - 1) % NSTG) * C::kStagingBytes);
+                else cp_async_commit();
+                cp_async_wait<NSTG - 1>();
+                __syncwarp();
             } else {
-                mbar_wait(bar_sempty + 8 * b, ((lt >> 1) & 1) ^ 1);
+                // staging buffer b is free once the store of tile lt - NSTG has read it
+                mbar_wait(bar_sempty + 8 * b, ((lt / NSTG) & 1) ^ 1);
             }
             mbar_wait(bar_tfull + 8 * acc, (lt >> 1) & 1);
             tc_fence_after();
+            if (tid == 0) TRACE(lt, 4);
 #pragma unroll 1
-            for (int c = 0; c < BN; c += 32) {
+            for (int c = c_lo; c < c_lo + kCols; c += 32) {
                 uint32_t v[32];
                 tmem_ld32(tmem_base + lane_base + acc * BN + c, v);
                 tmem_ld_wait();
@@ -323,47 +407,60 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             }
             tc_fence_before();
             mbar_arrive(bar_tempty + 8 * acc);
+            if (kResid) {
+                // scatter-add store: the warp's 32 rows x kCols columns, 16-B chunks,
+                // kRowsPerIt rows per instruction (full 128-B lines)
+                __syncwarp();
+                const int mypix = pixel_of(mt * kBM + r);
+#pragma unroll
+                for (int i = 0; i < 32 / kRowsPerIt; ++i) {
+                    const int rl = i * kRowsPerIt + lane / kChunks, c16 = lane % kChunks;
+                    const int pix = __shfl_sync(0xffffffffu, mypix, rl);
+                    uint32_t o[4];
+                    asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3])
+                                 : "r"(chunk_addr(sbuf, rl, c16)));
+                    if (pix >= 0)
+                        *reinterpret_cast<uint4 *>(Y + (size_t)pix * args.out_ld + n0 + c_lo + c16 * 8) =
+                            make_uint4(o[0], o[1], o[2], o[3]);
+                }
+                __syncwarp();
+                if (tid == 0) TRACE(lt, 6);
+                continue;
+            }
             fence_proxy_async_smem();  // staging writes -> visible to the TMA store
-            named_bar_sync(1, 128);
-            if (r == 0) {
-                if (MODE == CONV3_DYN) {
-                    const int u0 = mt * args.units_per_tile;
-                    const int nu = min(args.units_per_tile, geo.units_total - u0);
-                    const int box_bytes = args.S * args.S * 128;
-                    for (int p = 0; p < nu; ++p) {
-                        int n, gy, gx;
-                        cell_coords(args, u0 + p, n, gy, gx);
-                        for (int c = 0; c < BN / 64; ++c)
-                            tma_store_4d(&args.tmap_out, sbuf + c * kChunkBytes + p * box_bytes, n0 + c * 64,
-                                         gx * args.S, gy * args.S, n);
-                    }
-                } else if (MODE == CONV2_DENSE) {
+            named_bar_sync(1, EPI);
+            if (tid == 0) TRACE(lt, 5);
+            if (tid == 0) {
+                if (MODE == CONV2_DENSE) {
                     int d2n, d2y;
                     dense2_tile(args, mt, d2n, d2y);
                     for (int c = 0; c < BN / 64; ++c)
                         tma_store_4d(&args.tmap_out, sbuf + c * kChunkBytes, n0 + c * 64, 0, d2y, d2n);
                 } else {
-                    int row0;
-                    if (MODE == CONV1_DYN) row0 = mt * args.units_per_tile * args.unit_rows;
-                    else if (MODE == CONV2_DYN) row0 = mt * args.units_per_tile * args.S * args.S;
-                    else row0 = mt * kBM;
+                    const int row0 = MODE == CONV2_DYN ? mt * args.units_per_tile * args.S * args.S : mt * kBM;
                     for (int c = 0; c < BN / 64; ++c)
                         tma_store_2d(&args.tmap_out, sbuf + c * kChunkBytes, n0 + c * 64, row0);
                 }
                 bulk_commit();
-                // the previous tile's store has finished reading its staging buffer
-                bulk_wait_read<1>();
-                if (lt >= 1) mbar_arrive(bar_sempty + 8 * (b ^ 1));
+                TRACE(lt, 6);
+                if (NSTG == 1) {
+                    bulk_wait_read<0>();  // single buffer: free it as soon as this store has read it
+                    mbar_arrive(bar_sempty);
+                } else {
+                    bulk_wait_read<1>();  // the previous tile's store has read its buffer
+                    if (lt >= 1) mbar_arrive(bar_sempty + 8 * ((lt - 1) % NSTG));
+                }
             }
         }
-        if (r == 0) bulk_wait_all<0>();
+        if (tid == 0 && !kResid) bulk_wait_all<0>();
     }
 
     tc_fence_before();
     __syncthreads();
-    if (warp == 5) {
+    if (warp == C::kMmaWarp) {
         tc_fence_after();
-        tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+        tmem_dealloc<C::kTmemCols>(tmem_base);
     }
 }
 
@@ -372,7 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
 template <int MODE, int BN>
 static cudaError_t launch_mode_bn(const ConvArgs &a, int max_tiles_m, int num_sms, cudaStream_t st) {
     auto kern = conv_tc_kernel<MODE, BN>;
-    const int smem = TileCfg<BN>::smem_bytes(a.N);
+    const int smem = Cfg<MODE, BN>::smem_bytes(a.N);
     static int configured = 0;  // per instantiation: largest dynamic smem enabled so far
     if (smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -381,7 +478,7 @@ static cudaError_t launch_mode_bn(const ConvArgs &a, int max_tiles_m, int num_sm
     }
     const long tiles = (long)max_tiles_m * (a.N / BN);
     const int grid = (int)(tiles < num_sms ? (tiles > 0 ? tiles : 1) : num_sms);
-    kern<<<grid, kThreads, smem, st>>>(a);
+    kern<<<grid, threads_of<MODE, BN>(), smem, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -408,3 +505,18 @@ cudaError_t launch_conv_tc(int mode, const ConvArgs &a, int max_tiles_m, int num
 }
 
 }  // namespace lasnet
+
+#ifdef LASNET_TRACE
+extern "C" int lasnet_trace_read(unsigned long long *host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, lasnet::g_trace, sizeof(unsigned long long) * (n < 512 ? n : 512));
+}
+extern "C" int lasnet_trace_clear(int mode) {
+    static unsigned long long z[512];
+    cudaMemcpyToSymbol(lasnet::g_trace_mode, &mode, sizeof(int));
+    cudaMemcpyToSymbol(lasnet::g_ktrace, z, sizeof(z));
+    return (int)cudaMemcpyToSymbol(lasnet::g_trace, z, sizeof(z));
+}
+extern "C" int lasnet_ktrace_read(unsigned long long *host) {
+    return (int)cudaMemcpyFromSymbol(host, lasnet::g_ktrace, sizeof(unsigned long long) * 512);
+}
+#endif

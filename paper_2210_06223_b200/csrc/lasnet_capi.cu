@@ -60,6 +60,14 @@ int num_sms() {
     return cached;
 }
 
+// masker: 16-B channel vectors; a pixel of >= 32 vectors must be 1, 2, 4 or 8
+// slots of 32 vectors (lanes own whole vector slots).
+bool masker_channels_ok(int c, int vec) {
+    if (c % vec) return false;
+    const int nvec = c / vec;
+    return nvec < 32 || nvec == 32 || nvec == 64 || nvec == 128 || nvec == 256;  // 1, 2, 4, 8 slots
+}
+
 size_t elt_size(int dtype) { return dtype == LASNET_BF16 ? 2 : 4; }
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -183,15 +191,9 @@ int prepare_tc(int mode, ConvArgs &a, const lasnet_block_desc *d, const void *x,
     bool ok = tmap2(&a.tmap_b, a.w, a.K, a.N, 64, bn_of(a.N));
     switch (mode) {
         case CONV1_DYN: {
-            const bool whole = hs * hs <= 128 && (128 / (hs * hs)) * hs * hs >= 96;
-            a.units_per_patch = whole ? 1 : hs;
-            a.unit_rows = whole ? hs * hs : hs;
-            a.unit_halo_rows = whole ? hs : 1;
-            a.units_per_tile = 128 / a.unit_rows;
-            ok = ok && tmap4(&a.tmap_a, x, d->c_in, d->w, d->h, d->n, 64, hs, a.unit_halo_rows, 1);
-            ok = ok && tmap2(&a.tmap_out, h1, C, (uint64_t)cap * hs * hs, 64, a.units_per_tile * a.unit_rows);
-            const long units = (long)cap * a.units_per_patch;
-            return ok ? (int)((units + a.units_per_tile - 1) / a.units_per_tile) : -1;
+            // A = halo rows gathered by cp.async; h1 rows stored by 2-D TMA boxes
+            ok = ok && tmap2(&a.tmap_out, h1, C, (uint64_t)cap * hs * hs, 64, 128);
+            return ok ? (int)(((long)cap * hs * hs + 127) / 128) : -1;
         }
         case CONV2_DYN: {
             a.units_per_tile = 128 / (S * S);
@@ -201,12 +203,9 @@ int prepare_tc(int mode, ConvArgs &a, const lasnet_block_desc *d, const void *x,
             return ok ? (cap + a.units_per_tile - 1) / a.units_per_tile : -1;
         }
         case CONV3_DYN: {
-            a.units_per_tile = 128 / (S * S);
-            a.box_rows = a.units_per_tile * S * S;
-            ok = ok && tmap2(&a.tmap_a, h2, C, (uint64_t)cap * S * S, 64, a.box_rows);
-            ok = ok && tmap4(&a.tmap_res, x, d->c_out, d->w, d->h, d->n, 64, S, S, 1);
-            ok = ok && tmap4(&a.tmap_out, y, d->c_out, d->w, d->h, d->n, 64, S, S, 1);
-            return ok ? (cap + a.units_per_tile - 1) / a.units_per_tile : -1;
+            // A = h2 rows (2-D TMA); residual and scatter by the epilogue warps
+            ok = ok && tmap2(&a.tmap_a, h2, C, (uint64_t)cap * S * S, 64, 128);
+            return ok ? (int)(((long)cap * S * S + 127) / 128) : -1;
         }
         case CONV1_DENSE: {
             ok = ok && tmap2(&a.tmap_a, x, d->c_in, px, 64, 128);
@@ -230,8 +229,6 @@ int prepare_tc(int mode, ConvArgs &a, const lasnet_block_desc *d, const void *x,
         }
         case CONV3_DENSE: {
             ok = ok && tmap2(&a.tmap_a, h2, C, px, 64, 128);
-            ok = ok && tmap2(&a.tmap_res, x, d->c_out, px, 64, 128);
-            ok = ok && tmap2(&a.tmap_out, y, d->c_out, px, 64, 128);
             return ok ? (int)((px + 127) / 128) : -1;
         }
     }
@@ -260,6 +257,12 @@ ConvArgs base_args(const lasnet_block_desc *d) {
     a.S = d->s;
     a.Gh = (d->h + d->s - 1) / d->s;
     a.Gw = (d->w + d->s - 1) / d->s;
+    a.fd_G = FastDiv((uint32_t)(a.Gh * a.Gw));
+    a.fd_Gw = FastDiv((uint32_t)a.Gw);
+    a.fd_hs = FastDiv((uint32_t)(d->s + 2));
+    a.fd_hs2 = FastDiv((uint32_t)((d->s + 2) * (d->s + 2)));
+    a.fd_S = FastDiv((uint32_t)d->s);
+    a.fd_SS = FastDiv((uint32_t)(d->s * d->s));
     return a;
 }
 
@@ -313,7 +316,7 @@ lasnet_status lasnet_mask(const lasnet_block_desc *d, const void *x, const float
     if (!x || !wm || !mask) return LASNET_ERR_NULL;
     if (d->stride != 1) return LASNET_ERR_UNSUPPORTED;
     const int vec = d->dtype == LASNET_BF16 ? 8 : 4;
-    if (d->c_in % vec || misaligned(x)) return LASNET_ERR_UNSUPPORTED;
+    if (!masker_channels_ok(d->c_in, vec) || misaligned(x)) return LASNET_ERR_UNSUPPORTED;
     g_last_launches = 0;
     if (d->n == 0) return LASNET_OK;
     KernelEvents ev(reinterpret_cast<cudaStream_t>(stream));
@@ -337,7 +340,7 @@ lasnet_status lasnet_mask_compact(const lasnet_block_desc *d, const void *x, con
     if (!x || !wm || !idx || !count) return LASNET_ERR_NULL;
     if (d->stride != 1) return LASNET_ERR_UNSUPPORTED;
     const int vec = d->dtype == LASNET_BF16 ? 8 : 4;
-    if (d->c_in % vec || misaligned(x)) return LASNET_ERR_UNSUPPORTED;
+    if (!masker_channels_ok(d->c_in, vec) || misaligned(x)) return LASNET_ERR_UNSUPPORTED;
     if (!ws || ws_bytes < lasnet_mask_compact_workspace_bytes(d)) return LASNET_ERR_WORKSPACE;
     g_last_launches = 0;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);

@@ -42,15 +42,15 @@ template <> struct Elem<__nv_bfloat16> {
             acc = fma((double)w[2 * i + 1], bf16_to_f64(q[i] >> 16), acc);
         }
     }
-    __device__ static void ffma8(const uint4 &v, const float *w, const float *wa, float &acc, float &mag) {
+    __device__ static void ffma8(const uint4 &v, const float *w, float &acc, float &mag) {
         const uint32_t q[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const float lo = __uint_as_float(q[i] << 16), hi = __uint_as_float(q[i] & 0xFFFF0000u);
             acc = fmaf(w[2 * i], lo, acc);
             acc = fmaf(w[2 * i + 1], hi, acc);
-            mag = fmaf(wa[2 * i], fabsf(lo), mag);
-            mag = fmaf(wa[2 * i + 1], fabsf(hi), mag);
+            mag = fmaf(fabsf(w[2 * i]), fabsf(lo), mag);  // |.| are free operand modifiers
+            mag = fmaf(fabsf(w[2 * i + 1]), fabsf(hi), mag);
         }
     }
 };
@@ -62,134 +62,235 @@ template <> struct Elem<float> {
         acc = fma((double)w[2], (double)__uint_as_float(v.z), acc);
         acc = fma((double)w[3], (double)__uint_as_float(v.w), acc);
     }
-    __device__ static void ffma8(const uint4 &v, const float *w, const float *wa, float &acc, float &mag) {
+    __device__ static void ffma8(const uint4 &v, const float *w, float &acc, float &mag) {
         const float f[4] = {__uint_as_float(v.x), __uint_as_float(v.y), __uint_as_float(v.z), __uint_as_float(v.w)};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             acc = fmaf(w[i], f[i], acc);
-            mag = fmaf(wa[i], fabsf(f[i]), mag);
+            mag = fmaf(fabsf(w[i]), fabsf(f[i]), mag);
         }
     }
 };
 
-// One warp computes the masker logit of one coarse cell:
-//   logit = (1/|Omega|) * sum_{p in Omega} sum_c w_c x[p,c] + b
-// EXACT = true: fp64 accumulation of exact products (bf16 x fp32 fits a double).
-// EXACT = false: fp32 FFMA accumulation of the same sum together with
-//   sum |w_c x[p,c]|; returns a bound on the fp32 rounding error through *err
-//   (Higham: |fl(s) - s| <= gamma_n * sum|terms|, n = longest addition chain).
-// Lanes own 16-byte channel vectors; when a pixel has fewer than 32 vectors
-// the warp covers several pixels per step.  8 loads per lane are in flight.
-template <typename T, bool EXACT>
-__device__ __forceinline__ double cell_sum(const T *__restrict__ x, const float *__restrict__ wm, int H, int W, int C,
-                                           int S, int n, int gy, int gx, int lane, int &npix_out, double *err) {
+// Masker geometry (host-computed).  A cell's work is split into "items": one
+// 16-byte channel vector per lane for one pixel (nvec >= 32 vectors per pixel:
+// item = (pixel, vector slot), lane l reads vector 32*slot + l), or, for narrow
+// pixels (nvec < 32), one vector of each of ppw = 32/nvec pixels.  A group of
+// wpc warps shares one cell and each warp issues all of its <= 16 loads at
+// once, so every warp needs a single memory round trip; cpb = 8/wpc cells per
+// 256-thread CTA.  <= 64 registers keep 4 CTAs (32 warps) per SM resident.
+struct MaskGeo {
+    int nvec;  // 16-B vectors per pixel
+    int ppw;   // pixels per item (nvec < 32), else 1
+    int nvl;   // vector slots per pixel (nvec >= 32), else 1
+    int wpc;   // warps per cell (1, 2, 4, 8)
+    int cpb;   // cells per CTA = 8 / wpc
+};
+
+constexpr int kMaskThreads = 256;
+constexpr int kMaxItems = 8;  // loads in flight per lane
+
+// Partial sum of this warp's pixels of cell (n, gy, gx).  EXACT: fp64 with exact
+// products (bf16 x fp32 fits a double).  Otherwise fp32 FFMA plus sum|w x| and
+// the longest addition chain for the error bound (Higham: |fl(s)-s| <= gamma_n sum|terms|).
+// Warp k of the cell's group takes pixels p0, p0 + pstride, ...; each pixel is
+// SLOTS 16-B vectors per lane (wide pixels) or one vector (narrow pixels).  The
+// pixel walk is incremental (no integer division in the loop) and every lane
+// issues up to 8 loads before consuming any.
+template <typename T, bool EXACT, int SLOTS>
+__device__ __forceinline__ void warp_items_s(const T *__restrict__ x, const float *__restrict__ wm, const MaskGeo &mg,
+                                             int H, int W, int C, int S, int n, int gy, int gx, int k, int lane,
+                                             double &dacc, float &facc, float &fmag, int &nterms) {
     constexpr int PV = Elem<T>::kPerVec;
+    constexpr int PPC = kMaxItems / SLOTS;  // pixels per chunk
     const int y0 = gy * S, x0 = gx * S;
     const int cw = min(x0 + S, W) - x0;
     const int npix = (min(y0 + S, H) - y0) * cw;
-    npix_out = npix;
-    const int nvec = C / PV;
+    const bool wide = mg.nvec >= 32;
+    const int vlane = wide ? lane : lane % mg.nvec;
+    const int psub = wide ? 0 : lane / mg.nvec;
+    if (!wide && psub >= mg.ppw) return;  // idle lane (zeros join the shuffles)
+    const int p0 = wide ? k : k * mg.ppw + psub;
+    const int pstride = wide ? mg.wpc : mg.wpc * mg.ppw;
     const uint4 *xv = reinterpret_cast<const uint4 *>(x);
-    const long img = (long)n * H * W;
-    double acc = 0.0;
-    float facc = 0.f, fmag = 0.f;
-    int nterms = 0;
-    const int ppw = nvec <= 32 ? 32 / nvec : 1;         // pixels per warp step
-    const int v0 = nvec <= 32 ? lane % nvec : lane;     // first vector of this lane
-    const int psub = nvec <= 32 ? lane / nvec : 0;
-    const int vstep = nvec <= 32 ? nvec : 32;
-    if (psub < ppw) {
-        for (int v = v0; v < nvec; v += vstep) {
-            float w[PV], wa[PV];
+    const long rowpitch = (long)W * (C / PV);  // uint4 per image row
+    const uint4 *base = xv + ((long)n * H + y0) * rowpitch + (long)x0 * (C / PV) + vlane;
+    int p = p0, py = p0 / cw, px = p0 - (p0 / cw) * cw;
+    while (p < npix) {
+        uint4 q[kMaxItems];
+        int np = 0;
+        {
+            int qy = py, qx = px, qp = p;
 #pragma unroll
-            for (int k = 0; k < PV; ++k) {
-                w[k] = __ldg(wm + v * PV + k);
-                wa[k] = fabsf(w[k]);
-            }
-            for (int p0 = psub; p0 < npix; p0 += 8 * ppw) {
-                uint4 q[8];
+            for (int i = 0; i < PPC; ++i) {
+                if (qp < npix) {
+                    const uint4 *pix = base + qy * rowpitch + (long)qx * (C / PV);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int p = p0 + u * ppw;
-                    if (p < npix) {
-                        const int yy = y0 + p / cw, xx = x0 + p % cw;
-                        q[u] = __ldg(xv + ((img + (long)yy * W + xx) * C) / PV + v);
-                    }
+                    for (int sl = 0; sl < SLOTS; ++sl) q[i * SLOTS + sl] = __ldg(pix + sl * 32);
+                    ++np;
                 }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    if (p0 + u * ppw < npix) {
-                        if constexpr (EXACT) {
-                            Elem<T>::fma8(q[u], w, acc);
-                        } else {
-                            Elem<T>::ffma8(q[u], w, wa, facc, fmag);
-                            nterms += PV;
-                        }
-                    }
+                qp += pstride;
+                qx += pstride;
+                while (qx >= cw) {
+                    qx -= cw;
+                    ++qy;
                 }
             }
-            if (nvec <= 32) break;
+            p = qp;
+            py = qy;
+            px = qx;
+        }
+#pragma unroll
+        for (int i = 0; i < PPC; ++i) {
+            if (i >= np) break;
+#pragma unroll
+            for (int sl = 0; sl < SLOTS; ++sl) {
+                const float4 *wp = reinterpret_cast<const float4 *>(wm + (sl * 32 + vlane) * PV);
+                float w[PV];
+#pragma unroll
+                for (int e = 0; e < PV / 4; ++e) {
+                    const float4 f = __ldg(wp + e);  // L1-resident
+                    w[4 * e] = f.x;
+                    w[4 * e + 1] = f.y;
+                    w[4 * e + 2] = f.z;
+                    w[4 * e + 3] = f.w;
+                }
+                if constexpr (EXACT) {
+                    Elem<T>::fma8(q[i * SLOTS + sl], w, dacc);
+                } else {
+                    Elem<T>::ffma8(q[i * SLOTS + sl], w, facc, fmag);
+                    nterms += PV;
+                }
+            }
         }
     }
-    if constexpr (EXACT) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-        return acc;
-    }
+}
+
+template <typename T, bool EXACT, int SLOTS>
+__device__ __forceinline__ void warp_items(const T *__restrict__ x, const float *__restrict__ w_s, const MaskGeo &mg,
+                                           int H, int W, int C, int S, int n, int gy, int gx, int k, int lane,
+                                           double &dacc, float &facc, float &fmag, int &nterms) {
+    warp_items_s<T, EXACT, SLOTS>(x, w_s, mg, H, W, C, S, n, gy, gx, k, lane, dacc, facc, fmag, nterms);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
-        facc += __shfl_xor_sync(0xffffffffu, facc, off);
-        fmag += __shfl_xor_sync(0xffffffffu, fmag, off);
-        nterms = max(nterms, __shfl_xor_sync(0xffffffffu, nterms, off));
-    }
-    // chain length: per-lane sequential terms + 5 shuffle levels (+1 for the FFMA product)
-    const double n_chain = (double)nterms + 6.0;
-    const double u = 5.9604644775390625e-8;  // 2^-24
-    *err = (double)fmag * (n_chain * u / (1.0 - n_chain * u)) * 1.0001 + 1e-37;
-    return (double)facc;
-}
-
-// Decision and logit of one cell.  want_logit: exact fp64 logit.  Otherwise the
-// decision is taken from the fp32 sum when its error bound separates it from 0
-// (so it equals the decision of exact arithmetic) and recomputed in fp64 when not.
-template <typename T>
-__device__ __forceinline__ bool cell_decide(const T *__restrict__ x, const float *__restrict__ wm, float bm, int H,
-                                            int W, int C, int S, int n, int gy, int gx, int lane, bool want_logit,
-                                            double &logit) {
-    int npix;
-    if (!want_logit) {
-        double err;
-        const double s32 = cell_sum<T, false>(x, wm, H, W, C, S, n, gy, gx, lane, npix, &err);
-        const double z = s32 + (double)bm * (double)npix;  // scaled logit, fp64
-        if (fabs(z) > err * 1.0001 + 1e-300) {
-            logit = z / (double)npix;
-            return z > 0.0;
+        if constexpr (EXACT) {
+            dacc += __shfl_xor_sync(0xffffffffu, dacc, off);
+        } else {
+            facc += __shfl_xor_sync(0xffffffffu, facc, off);
+            fmag += __shfl_xor_sync(0xffffffffu, fmag, off);
+            nterms = max(nterms, __shfl_xor_sync(0xffffffffu, nterms, off));
         }
     }
-    const double s64 = cell_sum<T, true>(x, wm, H, W, C, S, n, gy, gx, lane, npix, nullptr);
-    logit = s64 / (double)npix + (double)bm;
-    return logit > 0.0;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(256) masker_kernel(const T *__restrict__ x, const float *__restrict__ wm,
-                                                     float bm, int n_img, int H, int W, int C, int S,
-                                                     int Gh, int Gw, uint8_t *__restrict__ mask,
-                                                     double *__restrict__ logits) {
-    const int lane = threadIdx.x & 31;
-    const long cell = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const long ncells = (long)n_img * Gh * Gw;
-    if (cell >= ncells) return;
+// The exact fp64 pass, kept out of line: it runs for logits requests and for the
+// rare cells the fp32 bound cannot decide, and must not cost the fast path registers.
+template <typename T, int SLOTS>
+__device__ __noinline__ double warp_items_exact(const T *__restrict__ x, const float *__restrict__ w_s,
+                                                const MaskGeo mg, int H, int W, int C, int S, int n, int gy, int gx,
+                                                int k, int lane) {
+    double d = 0.0;
+    float fa = 0.f, fm = 0.f;
+    int nt = 0;
+    warp_items<T, true, SLOTS>(x, w_s, mg, H, W, C, S, n, gy, gx, k, lane, d, fa, fm, nt);
+    return d;
+}
+
+__device__ __forceinline__ int cell_npix(int H, int W, int S, int gy, int gx) {
+    return (min(gy * S + S, H) - gy * S) * (min(gx * S + S, W) - gx * S);
+}
+
+// All 256 threads of the CTA call this together: decides the CTA's cpb cells
+// [cell0, cell0 + cpb).  want_logits: exact fp64 everywhere.  Otherwise each cell
+// is decided from the fp32 sum when the error bound separates it from 0 (so the
+// decision equals exact arithmetic), and re-summed in fp64 when it does not.
+// Returns, in thread 0 of each group's leading warp, the decision (and logit).
+template <typename T, int SLOTS>
+__device__ __forceinline__ void cta_decide(const T *__restrict__ x, const float *__restrict__ w_s, const MaskGeo &mg, float bm,
+                                           int H, int W, int C, int S, int Gh, int Gw, long ncells, long cell0,
+                                           bool want_logits, uint8_t *dec, double *logits) {
+    __shared__ float r_f[8], r_m[8];
+    __shared__ int r_n[8];
+    __shared__ double r_d[8];
+    __shared__ int s_need[8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int grp = warp / mg.wpc, k = warp - grp * mg.wpc;
+    const long cell = cell0 + grp;
+    const bool valid = grp < mg.cpb && cell < ncells;
     const int G = Gh * Gw;
-    const int n = (int)(cell / G);
-    const int g = (int)(cell - (long)n * G);
-    const int gy = g / Gw, gx = g - gy * Gw;
-    double logit;
-    const bool act = cell_decide<T>(x, wm, bm, H, W, C, S, n, gy, gx, lane, logits != nullptr, logit);
-    if (lane == 0) {
-        mask[cell] = act ? 1 : 0;
+    int n = 0, gy = 0, gx = 0;
+    if (valid) {
+        n = (int)(cell / G);
+        const int g = (int)(cell - (long)n * G);
+        gy = g / Gw;
+        gx = g - gy * Gw;
+    }
+    bool need_exact = want_logits;
+    if (!want_logits) {
+        double d = 0.0;
+        float fa = 0.f, fm = 0.f;
+        int nt = 0;
+        if (valid) warp_items<T, false, SLOTS>(x, w_s, mg, H, W, C, S, n, gy, gx, k, lane, d, fa, fm, nt);
+        if (lane == 0) {
+            r_f[warp] = fa;
+            r_m[warp] = fm;
+            r_n[warp] = nt;
+        }
+        __syncthreads();
+        if (valid && k == 0 && lane == 0) {
+            float sa = 0.f, sm = 0.f;
+            int chain = 0;
+            for (int j = 0; j < mg.wpc; ++j) {  // fixed order
+                sa += r_f[warp + j];
+                sm += r_m[warp + j];
+                chain = max(chain, r_n[warp + j]);
+            }
+            const double n_chain = (double)chain + 6.0 + mg.wpc;  // lane chain + shuffles + group adds
+            const double u = 5.9604644775390625e-8;               // 2^-24
+            const double err = (double)sm * (n_chain * u / (1.0 - n_chain * u)) * 1.0001 + 1e-37;
+            const int npix = cell_npix(H, W, S, gy, gx);
+            const double z = (double)sa + (double)bm * (double)npix;  // scaled logit
+            const bool sure = fabs(z) > err * 1.0001 + 1e-300;
+            s_need[grp] = !sure;
+            if (sure) dec[cell] = z > 0.0 ? 1 : 0;
+        }
+        __syncthreads();
+        need_exact = valid && s_need[grp];
+        if (!__syncthreads_or(need_exact)) return;
+    }
+    double d = 0.0;
+    if (need_exact) d = warp_items_exact<T, SLOTS>(x, w_s, mg, H, W, C, S, n, gy, gx, k, lane);
+    if (lane == 0) r_d[warp] = d;
+    __syncthreads();
+    if (need_exact && k == 0 && lane == 0) {
+        double sd = 0.0;
+        for (int j = 0; j < mg.wpc; ++j) sd += r_d[warp + j];
+        const double logit = sd / (double)cell_npix(H, W, S, gy, gx) + (double)bm;
+        dec[cell] = logit > 0.0 ? 1 : 0;
         if (logits) logits[cell] = logit;
     }
+}
+
+template <typename T, int SLOTS>
+__global__ void __launch_bounds__(kMaskThreads, 3) masker_kernel(const T *__restrict__ x, const float *__restrict__ wm,
+                                                              float bm, int n_img, int H, int W, int C, int S, int Gh,
+                                                              int Gw, MaskGeo mg, uint8_t *__restrict__ mask,
+                                                              double *__restrict__ logits) {
+    const long ncells = (long)n_img * Gh * Gw;
+    cta_decide<T, SLOTS>(x, wm, mg, bm, H, W, C, S, Gh, Gw, ncells, (long)blockIdx.x * mg.cpb, logits != nullptr,
+                         mask, logits);
+}
+
+MaskGeo mask_geo(int C, int PV, int S) {
+    MaskGeo g;
+    g.nvec = C / PV;
+    g.ppw = g.nvec < 32 ? 32 / g.nvec : 1;
+    g.nvl = g.nvec >= 32 ? g.nvec / 32 : 1;
+    const int items = g.nvec >= 32 ? S * S * g.nvl : (S * S + g.ppw - 1) / g.ppw;  // loads per lane per cell
+    g.wpc = 1;
+    while (g.wpc < 8 && (items + g.wpc - 1) / g.wpc > kMaxItems) g.wpc *= 2;
+    g.cpb = 8 / g.wpc;
+    return g;
 }
 
 cudaError_t launch_masker(int dtype_bf16, const void *x, const float *wm, float bm, int n_img, int H,
@@ -197,14 +298,24 @@ cudaError_t launch_masker(int dtype_bf16, const void *x, const float *wm, float 
     const int Gh = (H + S - 1) / S, Gw = (W + S - 1) / S;
     const long ncells = (long)n_img * Gh * Gw;
     if (ncells == 0) return cudaSuccess;
-    const int warps = 8;
-    const long grid = (ncells + warps - 1) / warps;
-    if (dtype_bf16)
-        masker_kernel<__nv_bfloat16><<<(unsigned)grid, warps * 32, 0, st>>>(
-            static_cast<const __nv_bfloat16 *>(x), wm, bm, n_img, H, W, C, S, Gh, Gw, mask, logits);
-    else
-        masker_kernel<float><<<(unsigned)grid, warps * 32, 0, st>>>(static_cast<const float *>(x), wm, bm,
-                                                                    n_img, H, W, C, S, Gh, Gw, mask, logits);
+    const MaskGeo mg = mask_geo(C, dtype_bf16 ? 8 : 4, S);
+    const long grid = (ncells + mg.cpb - 1) / mg.cpb;
+    const int slots = mg.nvec >= 32 ? mg.nvl : 1;
+#define LASNET_MASKER(TT, SL)                                                                                  \
+    masker_kernel<TT, SL><<<(unsigned)grid, kMaskThreads, 0, st>>>(static_cast<const TT *>(x), wm, bm, n_img, H, \
+                                                                   W, C, S, Gh, Gw, mg, mask, logits)
+    if (dtype_bf16) {
+        if (slots == 1) LASNET_MASKER(__nv_bfloat16, 1);
+        else if (slots == 2) LASNET_MASKER(__nv_bfloat16, 2);
+        else if (slots == 4) LASNET_MASKER(__nv_bfloat16, 4);
+        else LASNET_MASKER(__nv_bfloat16, 8);
+    } else {
+        if (slots == 1) LASNET_MASKER(float, 1);
+        else if (slots == 2) LASNET_MASKER(float, 2);
+        else if (slots == 4) LASNET_MASKER(float, 4);
+        else LASNET_MASKER(float, 8);
+    }
+#undef LASNET_MASKER
     return cudaGetLastError();
 }
 
@@ -341,12 +452,38 @@ int launch_compact(const uint8_t *mask, int ncells, int32_t *idx, int32_t *count
 // count and resets the counter -- the workspace is left zeroed, so no per-call
 // memset.  (A decoupled look-back is slower here: all CTAs finish together and
 // the prefix chain becomes serial.)
-constexpr int kFusedWarps = 16;
+constexpr int kFusedWarps = 8;
+
+#ifdef LASNET_TRACE
+// [0] earliest CTA start, [1] latest cell decision, [2] last CTA begins compaction, [3] compaction done
+__device__ unsigned long long g_mtrace[4];
+__device__ __forceinline__ unsigned long long mtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define MTRACE_MIN(k) atomicMin(&g_mtrace[k], mtimer())
+#define MTRACE_MAX(k) atomicMax(&g_mtrace[k], mtimer())
+extern "C" int lasnet_mtrace_read(unsigned long long *h) { return (int)cudaMemcpyFromSymbol(h, g_mtrace, 32); }
+extern "C" int lasnet_mtrace_clear(void) {
+    unsigned long long z[4] = {~0ull, 0, 0, 0};
+    return (int)cudaMemcpyToSymbol(g_mtrace, z, 32);
+}
+#else
+#define MTRACE_MIN(k) do { } while (0)
+#define MTRACE_MAX(k) do { } while (0)
+#endif
 
 struct FusedWs {
     unsigned int done, pad[3];
     uint8_t decisions[16];  // used when the caller passes no mask buffer (ncells bytes)
 };
+
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned *p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
 
 __device__ __forceinline__ uint4 ld_cg_u4(const void *p) {
     uint4 v;
@@ -354,39 +491,30 @@ __device__ __forceinline__ uint4 ld_cg_u4(const void *p) {
     return v;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(32 * kFusedWarps) masker_compact_kernel(
+template <typename T, int SLOTS>
+__global__ void __launch_bounds__(kMaskThreads, 3) masker_compact_kernel(
     const T *__restrict__ x, const float *__restrict__ wm, float bm, int n_img, int H, int W, int C, int S, int Gh,
-    int Gw, uint8_t *mask, double *__restrict__ logits, int32_t *__restrict__ idx, int32_t *__restrict__ count,
-    FusedWs *ws) {
+    int Gw, MaskGeo mg, uint8_t *mask, double *__restrict__ logits, int32_t *__restrict__ idx,
+    int32_t *__restrict__ count, FusedWs *ws) {
     __shared__ int s_last;
     __shared__ int s_warp[kFusedWarps];
     __shared__ int s_base;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const long ncells = (long)n_img * Gh * Gw;
-    const long cell = (long)blockIdx.x * kFusedWarps + warp;
     uint8_t *dec = mask ? mask : ws->decisions;
-    if (cell < ncells) {
-        const int G = Gh * Gw;
-        const int n = (int)(cell / G);
-        const int g = (int)(cell - (long)n * G);
-        const int gy = g / Gw, gx = g - gy * Gw;
-        double logit;
-        const bool act = cell_decide<T>(x, wm, bm, H, W, C, S, n, gy, gx, lane, logits != nullptr, logit);
-        if (lane == 0) {
-            dec[cell] = act ? 1 : 0;
-            if (logits) logits[cell] = logit;
-            __threadfence();  // publish before the done-counter increment
-        }
-    }
+    if (threadIdx.x == 0) MTRACE_MIN(0);
+    cta_decide<T, SLOTS>(x, wm, mg, bm, H, W, C, S, Gh, Gw, ncells, (long)blockIdx.x * mg.cpb, logits != nullptr,
+                         dec, logits);
+    if (threadIdx.x == 0) MTRACE_MAX(1);
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
-        s_last = atomicAdd(&ws->done, 1u) == gridDim.x - 1;
+        // release: this CTA's decisions (ordered before by bar.sync) become visible
+        // before the counter moves; acquire: the last CTA then sees everyone's
+        s_last = atom_add_acq_rel_gpu(&ws->done, 1u) == gridDim.x - 1;
     }
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
+    if (threadIdx.x == 0) MTRACE_MAX(2);
     // ---- last CTA: compaction of all ncells decisions (16 per thread per pass)
     if (threadIdx.x == 0) s_base = 0;
     __syncthreads();
@@ -437,8 +565,8 @@ __global__ void __launch_bounds__(32 * kFusedWarps) masker_compact_kernel(
     }
     if (threadIdx.x == 0) {
         *count = s_base;
-        ws->done = 0u;
-        __threadfence();
+        ws->done = 0u;  // kernel completion orders this before the next launch
+        MTRACE_MAX(3);
     }
 }
 
@@ -452,14 +580,26 @@ cudaError_t launch_mask_compact(int dtype_bf16, const void *x, const float *wm, 
     const int Gh = (H + S - 1) / S, Gw = (W + S - 1) / S;
     const long ncells = (long)n_img * Gh * Gw;
     if (ncells == 0) return cudaMemsetAsync(count, 0, sizeof(int32_t), st);
-    const long grid = (ncells + kFusedWarps - 1) / kFusedWarps;
+    const MaskGeo mg = mask_geo(C, dtype_bf16 ? 8 : 4, S);
+    const long grid = (ncells + mg.cpb - 1) / mg.cpb;
     FusedWs *w = static_cast<FusedWs *>(ws);
-    if (dtype_bf16)
-        masker_compact_kernel<__nv_bfloat16><<<(unsigned)grid, 32 * kFusedWarps, 0, st>>>(
-            static_cast<const __nv_bfloat16 *>(x), wm, bm, n_img, H, W, C, S, Gh, Gw, mask, logits, idx, count, w);
-    else
-        masker_compact_kernel<float><<<(unsigned)grid, 32 * kFusedWarps, 0, st>>>(
-            static_cast<const float *>(x), wm, bm, n_img, H, W, C, S, Gh, Gw, mask, logits, idx, count, w);
+    const int slots = mg.nvec >= 32 ? mg.nvl : 1;
+#define LASNET_FUSED(TT, SL)                                                                                      \
+    masker_compact_kernel<TT, SL><<<(unsigned)grid, kMaskThreads, 0, st>>>(static_cast<const TT *>(x), wm, bm, n_img, \
+                                                                           H, W, C, S, Gh, Gw, mg, mask, logits, idx, \
+                                                                           count, w)
+    if (dtype_bf16) {
+        if (slots == 1) LASNET_FUSED(__nv_bfloat16, 1);
+        else if (slots == 2) LASNET_FUSED(__nv_bfloat16, 2);
+        else if (slots == 4) LASNET_FUSED(__nv_bfloat16, 4);
+        else LASNET_FUSED(__nv_bfloat16, 8);
+    } else {
+        if (slots == 1) LASNET_FUSED(float, 1);
+        else if (slots == 2) LASNET_FUSED(float, 2);
+        else if (slots == 4) LASNET_FUSED(float, 4);
+        else LASNET_FUSED(float, 8);
+    }
+#undef LASNET_FUSED
     return cudaGetLastError();
 }
 

@@ -11,6 +11,25 @@
 
 namespace lasnet {
 
+// Division by a runtime constant via multiply-high (valid for 0 <= n < 2^31):
+// p = 31 + ceil(log2 d), mul = ceil(2^p / d), q = umulhi(n, mul) >> (p - 32).
+struct FastDiv {
+    uint32_t d, mul, shr;
+    __host__ __device__ FastDiv() : d(1), mul(0), shr(0) {}
+    __host__ FastDiv(uint32_t div) : d(div), mul(0), shr(0) {
+        if (d > 1) {
+            int l = 0;
+            while ((1u << l) < d) ++l;  // ceil(log2 d)
+            const int p = 31 + l;
+            mul = (uint32_t)(((1ull << p) + d - 1) / d);
+            shr = (uint32_t)(p - 32);
+        }
+    }
+    __device__ __forceinline__ int div(int n) const {
+        return d == 1 ? n : (int)(__umulhi((uint32_t)n, mul) >> shr);
+    }
+};
+
 enum ConvMode : int {
     CONV1_DYN = 0,    // A = gathered halo rows of x, out = h1 [P][(S+2)^2][c_mid]
     CONV2_DYN = 1,    // A = im2col of h1 patch windows, out = h2 [P][S^2][c_mid]
@@ -38,6 +57,7 @@ struct ConvArgs {
     int32_t a_ld;           // elements per A source row (c_in for conv1, c_mid otherwise)
     int32_t out_ld;         // elements per output row
     int32_t n_img, H, W, S, Gh, Gw;
+    FastDiv fd_G, fd_Gw, fd_hs, fd_hs2, fd_S, fd_SS;  // G = Gh*Gw, hs = S+2, SS = S*S
     // tcgen05 tile geometry (host-computed)
     int32_t units_per_tile;   // dynamic: TMA boxes (conv1) / patches (conv2, conv3) per 128-row tile
     int32_t units_per_patch;  // conv1: 1 (whole halo box) or S+2 (one box per halo row)
@@ -59,25 +79,26 @@ __device__ __forceinline__ int gemm_rows(int mode, const ConvArgs &a) {
 }
 
 // Active cell t -> (image n, cell row gy, cell col gx).
-__device__ __forceinline__ void cell_coords(const ConvArgs &a, int t, int &n, int &gy, int &gx) {
-    int cell = a.idx[t];
-    int G = a.Gh * a.Gw;
-    n = cell / G;
-    int g = cell - n * G;
-    gy = g / a.Gw;
+__device__ __forceinline__ void cell_decode(const ConvArgs &a, int cell, int &n, int &gy, int &gx) {
+    n = a.fd_G.div(cell);
+    const int g = cell - n * (int)a.fd_G.d;
+    gy = a.fd_Gw.div(g);
     gx = g - gy * a.Gw;
+}
+__device__ __forceinline__ void cell_coords(const ConvArgs &a, int t, int &n, int &gy, int &gx) {
+    cell_decode(a, a.idx[t], n, gy, gx);
 }
 
 // conv1 (dynamic): GEMM row -> source pixel of x, or -1 for a halo pixel outside
 // the image / a row past the end (zero row; the epilogue also writes 0, R6).
 __device__ __forceinline__ int halo_pixel(const ConvArgs &a, int r, int M) {
     if (r >= M) return -1;
-    int hs = a.S + 2, hs2 = hs * hs;
-    int t = r / hs2, j = r - t * hs2;
+    const int hs = a.S + 2, hs2 = hs * hs;
+    const int t = a.fd_hs2.div(r), j = r - t * hs2;
     int n, gy, gx;
     cell_coords(a, t, n, gy, gx);
-    int jy = j / hs;
-    int hy = gy * a.S - 1 + jy, hx = gx * a.S - 1 + (j - jy * hs);
+    const int jy = a.fd_hs.div(j);
+    const int hy = gy * a.S - 1 + jy, hx = gx * a.S - 1 + (j - jy * hs);
     if (hy < 0 || hy >= a.H || hx < 0 || hx >= a.W) return -1;
     return (n * a.H + hy) * a.W + hx;
 }
@@ -85,9 +106,9 @@ __device__ __forceinline__ int halo_pixel(const ConvArgs &a, int r, int M) {
 // conv2 (dynamic): GEMM row -> h1 row of the window centre of output pixel j of patch t.
 __device__ __forceinline__ int conv2_center_row(const ConvArgs &a, int r, int M) {
     if (r >= M) return -1;
-    int ss = a.S * a.S, hs = a.S + 2;
-    int t = r / ss, j = r - t * ss;
-    int py = j / a.S, px = j - py * a.S;
+    const int ss = a.S * a.S, hs = a.S + 2;
+    const int t = a.fd_SS.div(r), j = r - t * ss;
+    const int py = a.fd_S.div(j), px = j - py * a.S;
     return t * hs * hs + (py + 1) * hs + (px + 1);
 }
 
@@ -95,12 +116,12 @@ __device__ __forceinline__ int conv2_center_row(const ConvArgs &a, int r, int M)
 // the image border (R7) or the row is past the end.
 __device__ __forceinline__ int out_pixel(const ConvArgs &a, int r, int M) {
     if (r >= M) return -1;
-    int ss = a.S * a.S;
-    int t = r / ss, j = r - t * ss;
+    const int ss = a.S * a.S;
+    const int t = a.fd_SS.div(r), j = r - t * ss;
     int n, gy, gx;
     cell_coords(a, t, n, gy, gx);
-    int py = j / a.S;
-    int yy = gy * a.S + py, xx = gx * a.S + (j - py * a.S);
+    const int py = a.fd_S.div(j);
+    const int yy = gy * a.S + py, xx = gx * a.S + (j - py * a.S);
     if (yy >= a.H || xx >= a.W) return -1;
     return (n * a.H + yy) * a.W + xx;
 }
