@@ -315,10 +315,25 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
         const int M = gemm_rows(MODE, args);
         const __nv_bfloat16 *X = static_cast<const __nv_bfloat16 *>(args.resid);
         __nv_bfloat16 *Y = static_cast<__nv_bfloat16 *>(args.out);
-        // conv3: output pixel of GEMM row m (or -1: past the end / clipped patch, R7)
-        auto pixel_of = [&](int m) -> int {
-            if (MODE == CONV3_DYN) return out_pixel(args, m, M);
-            return m < M ? m : -1;
+        // conv3: output pixel of a GEMM row, in two halves so the idx load can be
+        // issued early: row_cell (volatile load of idx[patch]) then cell_pixel.
+        auto row_cell = [&](int tl) -> int {
+            if (tl >= geo.num_tiles) return -2;
+            const int m = (tl / geo.n_tiles_n) * kBM + r;
+            if (m >= M) return -2;
+            if (MODE != CONV3_DYN) return -1;
+            return ld_nc_volatile(args.idx + args.fd_SS.div(m));
+        };
+        auto cell_pixel = [&](int tl, int cell) -> int {
+            if (cell == -2) return -1;
+            const int m = (tl / geo.n_tiles_n) * kBM + r;
+            if (MODE != CONV3_DYN) return m;
+            int n, gy, gx;
+            cell_decode(args, cell, n, gy, gx);
+            const int j = m - args.fd_SS.div(m) * args.S * args.S;
+            const int py = args.fd_S.div(j);
+            const int yy = gy * args.S + py, xx = gx * args.S + (j - py * args.S);
+            return (yy < args.H && xx < args.W) ? (n * args.H + yy) * args.W + xx : -1;  // R7 clip
         };
         // conv3: rows x 16-B chunks of this warp's [32 rows] x [kCols columns] block
         constexpr int kChunks = kCols / 8;
@@ -328,24 +343,29 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             const int col = c_lo + c16 * 8;  // column within the tile
             return buf + (col >> 6) * kChunkBytes + row * 128 + ((((col & 63) >> 3) ^ (row & 7)) << 4);
         };
-        auto prefetch_resid = [&](int tl, uint32_t buf) {
-            const int m0 = (tl / geo.n_tiles_n) * kBM, n0 = (tl % geo.n_tiles_n) * BN;
-            const int mypix = pixel_of(m0 + r);
+        auto prefetch_resid = [&](int tl, int mypix, uint32_t buf) {
+            if (tl < geo.num_tiles) {
+                const int n0 = (tl % geo.n_tiles_n) * BN;
 #pragma unroll
-            for (int i = 0; i < 32 / kRowsPerIt; ++i) {
-                const int rl = i * kRowsPerIt + lane / kChunks, c16 = lane % kChunks;
-                const int pix = __shfl_sync(0xffffffffu, mypix, rl);
-                const __nv_bfloat16 *g = pix >= 0 ? X + (size_t)pix * args.out_ld + n0 + c_lo + c16 * 8 : X;
-                cp_async_16(chunk_addr(buf, rl, c16), g, pix >= 0 ? 16u : 0u);
+                for (int i = 0; i < 32 / kRowsPerIt; ++i) {
+                    const int rl = i * kRowsPerIt + lane / kChunks, c16 = lane % kChunks;
+                    const int pix = __shfl_sync(0xffffffffu, mypix, rl);
+                    const __nv_bfloat16 *g = pix >= 0 ? X + (size_t)pix * args.out_ld + n0 + c_lo + c16 * 8 : X;
+                    cp_async_16(chunk_addr(buf, rl, c16), g, pix >= 0 ? 16u : 0u);
+                }
             }
             cp_async_commit();
         };
         int lt = 0;
-        if (kResid) {  // residual of the first two tiles
+        int pix_ring[NSTG];  // output pixel of this thread's row for tiles lt .. lt+NSTG-2 (rotated)
+#pragma unroll
+        for (int k = 0; k < NSTG; ++k) pix_ring[k] = -1;
+        if (kResid) {  // residual of the first NSTG-1 tiles
+#pragma unroll
             for (int k = 0; k < NSTG - 1; ++k) {
                 const int tl = blockIdx.x + k * gridDim.x;
-                if (tl < geo.num_tiles) prefetch_resid(tl, staging + k * C::kStagingBytes);
-                else cp_async_commit();
+                pix_ring[k] = cell_pixel(tl, row_cell(tl));
+                prefetch_resid(tl, pix_ring[k], staging + k * C::kStagingBytes);
             }
         }
         for (int tile = blockIdx.x; tile < geo.num_tiles; tile += gridDim.x, ++lt) {
@@ -355,12 +375,10 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             const uint32_t sbuf = staging + b * C::kStagingBytes;
             bool zero = false;  // conv1: halo pixel outside the image stores 0 (R6)
             if (MODE == CONV1_DYN) zero = mt * kBM + r < M && halo_pixel(args, mt * kBM + r, M) < 0;
+            int cell_ahead = -2;
             if (kResid) {
-                // prefetch tile lt+NSTG-1 into the buffer tile lt-1 used, then wait for tile lt's group
-                const int nxt = tile + (NSTG - 1) * gridDim.x;
-                if (nxt < geo.num_tiles) prefetch_resid(nxt, staging + ((lt + NSTG - 1) % NSTG) * C::kStagingBytes);
-                else cp_async_commit();
-                cp_async_wait<NSTG - 1>();
+                cell_ahead = row_cell(tile + (NSTG - 1) * gridDim.x);  // idx load in flight during this tile
+                cp_async_wait<NSTG - 2>();  // this tile's residual has landed
                 __syncwarp();
             } else {
                 // staging buffer b is free once the store of tile lt - NSTG has read it
@@ -411,7 +429,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                 // scatter-add store: the warp's 32 rows x kCols columns, 16-B chunks,
                 // kRowsPerIt rows per instruction (full 128-B lines)
                 __syncwarp();
-                const int mypix = pixel_of(mt * kBM + r);
+                const int mypix = pix_ring[0];
 #pragma unroll
                 for (int i = 0; i < 32 / kRowsPerIt; ++i) {
                     const int rl = i * kRowsPerIt + lane / kChunks, c16 = lane % kChunks;
@@ -425,6 +443,13 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                             make_uint4(o[0], o[1], o[2], o[3]);
                 }
                 __syncwarp();
+                // residual prefetch for tile lt+NSTG-1 into the buffer tile lt-1 used
+                const int ahead = tile + (NSTG - 1) * gridDim.x;
+                const int slot = (lt + NSTG - 1) % NSTG;
+#pragma unroll
+                for (int k = 0; k + 1 < NSTG - 1; ++k) pix_ring[k] = pix_ring[k + 1];
+                pix_ring[NSTG - 2] = cell_pixel(ahead, cell_ahead);
+                prefetch_resid(ahead, pix_ring[NSTG - 2], staging + slot * C::kStagingBytes);
                 if (tid == 0) TRACE(lt, 6);
                 continue;
             }
