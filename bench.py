@@ -147,6 +147,21 @@ def algorithmic_work(mask_cells: np.ndarray, n, h, w, c_in, c_mid, c_out, s):
                                  r_pixel=out_px / (n * h * w))
 
 
+def ncu_traffic(kernel: str):
+    """DRAM bytes (read + write) per launch of `kernel` from the latest committed
+    ncu --set full capture (profiles/ncu_full_<tag>.json), or (None, None)."""
+    import glob
+
+    names = {"mask_compact": "mask_compact", "conv1": "conv1_dyn", "conv2": "conv2_dyn", "conv3": "conv3_dyn"}
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_full_*.json")), key=os.path.getmtime)
+    for f in reversed(files):
+        d = json.load(open(f))
+        for e in d.get("full", []):
+            if e.get("kernel") == names.get(kernel):
+                return int(e.get("dram_read", 0) + e.get("dram_write", 0)), os.path.relpath(f, ROOT)
+    return None, None
+
+
 def roofline_entry(work, ms, hbm, tfl):
     t_hbm = work["bytes"] / (hbm * 1e9)
     t_tc = work["flops"] / (tfl * 1e12)
@@ -345,18 +360,18 @@ def run_lasnet(args):
     e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev)
     clocks = sampler.stop()
 
-    t = torch.tensor([tot_ms, e2e_ms, statistics.fmean(dense_ms)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    tot_max, e2e_max, dense_max = (float(v) for v in t.tolist())
-    value = world * n * K / (tot_max / 1e3)
-    e2e_val = world * n * K / (e2e_max / 1e3)
+    from paper_2210_06223_b200 import dist as ldist
+
+    tot_max, e2e_max, dense_max = ldist.max_over_ranks([tot_ms, e2e_ms, statistics.fmean(dense_ms)], device="cuda")
+    value = ldist.throughput(n, world, K, tot_max)
+    e2e_val = ldist.throughput(n, world, K, e2e_max)
 
     if rank == 0:
         hbm, tfl, tfl_sus, src = peaks()
         dom = max(names, key=lambda nm: kern_ms[nm])
         roof = roofline_entry(kwork[dom], kern_ms[dom], hbm, tfl)
-        roof.update({"kernel": dom, "traffic": None, "peak_source": src,
+        traffic, tsrc = ncu_traffic(dom)
+        roof.update({"kernel": dom, "traffic": traffic, "traffic_source": tsrc, "peak_source": src,
                      "algorithmic": {"bytes": kwork[dom]["bytes"], "flops": kwork[dom]["flops"]},
                      "share_of_step": round(kern_ms[dom] / statistics.fmean(step_ms), 3)})
         blk_roof = roofline_entry(bwork, statistics.fmean(step_ms), hbm, tfl)

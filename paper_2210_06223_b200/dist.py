@@ -1,0 +1,52 @@
+"""Multi-GPU host logic (one process per GPU, torch.distributed).
+
+The dynamic block shards by image with no exchange step (masks, indices and
+blocks are per image): each rank runs its own images and the only
+collectives are bookkeeping -- the max-over-ranks step time and summed
+statistics.  Backend "nccl" on GPUs; the same functions run on "gloo" (CPU) in
+the tests.
+"""
+from __future__ import annotations
+
+import os
+
+import torch
+import torch.distributed as dist
+
+
+def env_ranks():
+    """(rank, world_size, local_rank) from the torchrun environment (defaults: single process)."""
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def shard(n_total: int, rank: int, world: int):
+    """Contiguous image range [start, stop) of `rank` when n_total images are split
+    over `world` ranks (strong scaling of a global batch); sizes differ by <= 1."""
+    if world <= 0 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    base, extra = divmod(n_total, world)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
+
+
+def _reduce(values, op, device):
+    t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=op)
+    return [float(v) for v in t.tolist()]
+
+
+def max_over_ranks(values, device="cpu"):
+    """Element-wise max over ranks (timings: the job is as slow as its slowest rank)."""
+    return _reduce(values, dist.ReduceOp.MAX, device)
+
+
+def sum_over_ranks(values, device="cpu"):
+    """Element-wise sum over ranks (active-cell counts, images processed)."""
+    return _reduce(values, dist.ReduceOp.SUM, device)
+
+
+def throughput(images_per_rank: int, world: int, steps: int, max_total_ms: float) -> float:
+    """Whole-job images/s of a weak-scaling run: all ranks' images over the slowest rank's time."""
+    return images_per_rank * world * steps / (max_total_ms / 1e3)

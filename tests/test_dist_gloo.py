@@ -1,0 +1,67 @@
+"""Multi-process host logic on CPU: world_size-2 gloo process group (no GPU)."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2210_06223_b200 import dist as L
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        r, w, lr = L.env_ranks()
+        mx = L.max_over_ranks([rank * 10.0 + 1.0, -rank])
+        sm = L.sum_over_ranks([1.0, rank])
+        start, stop = L.shard(256, r, w)
+        n_local = torch.tensor([stop - start])
+        dist.all_reduce(n_local)
+        q.put((rank, r, w, lr, mx, sm, (start, stop), int(n_local.item())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_two_ranks():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, r, w, lr, mx, sm, rng, n_all in out:
+        assert (r, w, lr) == (rank, 2, rank)
+        assert mx == [11.0, 0.0]          # max over ranks
+        assert sm == [2.0, 1.0]           # sum over ranks
+        assert n_all == 256               # shards cover the global batch
+    assert out[0][6] == (0, 128) and out[1][6] == (128, 256)
+
+
+@pytest.mark.parametrize("n,world", [(256, 1), (256, 8), (10, 3), (3, 8), (0, 4)])
+def test_shard_partitions(n, world):
+    ranges = [L.shard(n, r, world) for r in range(world)]
+    assert ranges[0][0] == 0 and ranges[-1][1] == n
+    assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+    sizes = [b - a for a, b in ranges]
+    assert max(sizes) - min(sizes) <= 1
+
+
+def test_single_process_reductions_are_identity():
+    assert L.max_over_ranks([3.0, 4.0]) == [3.0, 4.0]
+    assert L.throughput(128, 8, 10, 1000.0) == 128 * 8 * 10
