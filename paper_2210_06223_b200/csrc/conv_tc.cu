@@ -259,6 +259,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             for (int kb = 0; kb < num_kb; ++kb, ++it) {
                 const int stage = it % ST;
                 mbar_wait(bar_empty + 8 * stage, ((it / ST) & 1) ^ 1);
+                if (pt == 0) KTRACE(it, 3);
                 const uint32_t sa = sbase + stage * C::kStageBytes;
 #pragma unroll
                 for (int i = 0; i < RPT; ++i) {

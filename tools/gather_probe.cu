@@ -4,6 +4,7 @@
 // smem stages.  Variants: cp.async (k-major: one 128-B chunk of each row per
 // stage, like the GEMM), cp.async with more threads, and plain LDG + st.shared.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/gather_probe tools/gather_probe.cu
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <cstdint>
@@ -96,6 +97,70 @@ __global__ void __launch_bounds__(THREADS + 32) gather(const uint8_t *x, int til
     }
 }
 
+// TMA tile::gather4 variant: ISSUERS threads each issue 32/ISSUERS gather4 ops per K-block
+// (4 rows x 128 B each) into an mbarrier-tracked ring.
+template <int STAGES, int ISSUERS>
+__global__ void __launch_bounds__(64) gather_tma(const __grid_constant__ CUtensorMap tm, int tiles, unsigned *out) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ __align__(8) uint64_t full[16], empty[16];
+    const uint32_t base = (su32(smem) + 1023) & ~1023u;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&full[s])), "r"(ISSUERS));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&empty[s])));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    __syncthreads();
+    const int H = 28, W = 28;
+    if (tid < ISSUERS) {
+        constexpr int OPS = 32 / ISSUERS;
+        int it = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            int rows[OPS * 4];
+#pragma unroll
+            for (int i = 0; i < OPS * 4; ++i) {
+                const int row = (tid * OPS * 4 + i);
+                const int patch = t * 3 + min(row / 36, 2), j = row % 36;
+                unsigned h = (unsigned)patch * 2654435761u;
+                const int n = h % 128, gy = (h >> 8) % 7, gx = (h >> 16) % 7;
+                const int yy = min(max(gy * 4 - 1 + j / 6, 0), H - 1), xx = min(max(gx * 4 - 1 + j % 6, 0), W - 1);
+                rows[i] = (n * H + yy) * W + xx;
+            }
+            for (int kb = 0; kb < 8; ++kb, ++it) {
+                const int s = it % STAGES;
+                uint32_t done = 0;
+                while (!done)
+                    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p; }"
+                                 : "=r"(done) : "r"(su32(&empty[s])), "r"(((it / STAGES) & 1) ^ 1));
+                const uint32_t bar = su32(&full[s]);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(OPS * 512));
+#pragma unroll
+                for (int o = 0; o < OPS; ++o) {
+                    const uint32_t dst = base + s * 16384 + (tid * OPS + o) * 512;
+                    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                                 " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];"
+                                 ::"r"(dst), "l"((uint64_t)&tm), "r"(bar), "r"(kb * 64), "r"(rows[4 * o]),
+                                 "r"(rows[4 * o + 1]), "r"(rows[4 * o + 2]), "r"(rows[4 * o + 3]) : "memory");
+                }
+            }
+        }
+    } else if (tid == 32) {
+        int it = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x)
+            for (int kb = 0; kb < 8; ++kb, ++it) {
+                const int s = it % STAGES;
+                uint32_t done = 0;
+                while (!done)
+                    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p; }"
+                                 : "=r"(done) : "r"(su32(&full[s])), "r"((it / STAGES) & 1));
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[s])) : "memory");
+            }
+        out[blockIdx.x] = it;
+    }
+}
+
 int main() {
     const size_t bytes = (size_t)128 * 28 * 28 * 512 * 2;
     uint8_t *x;
@@ -136,5 +201,36 @@ int main() {
     run("cp.async 256 thr", gather<256, 6, 0>, 6, 256);
     run("cp.async 256 thr", gather<256, 8, 0>, 8, 256);
     run("cp.async 512 thr", gather<512, 6, 0>, 6, 512);
+    {
+        CUtensorMap tm;
+        cuuint64_t gd[2] = {512, 128ull * 28 * 28}, gs[1] = {1024};
+        cuuint32_t bx[2] = {64, 1}, es[2] = {1, 1};
+        CUresult e = cuTensorMapEncodeTiled(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x, gd, gs, bx, es,
+                                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        printf("gather4 tensor map: %d\n", (int)e);
+        auto run4 = [&](const char *name, auto kern, int stages) {
+            const int smem = stages * 16384 + 1024;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            float best = 1e9;
+            for (int rep = 0; rep < 4; ++rep) {
+                rd<<<148 * 4, 512>>>(fl, (256 << 20) / 16, o);
+                cudaEventRecord(a);
+                kern<<<148, 64, smem>>>(tm, tiles, o);
+                cudaEventRecord(b);
+                cudaEventSynchronize(b);
+                float ms;
+                cudaEventElapsedTime(&ms, a, b);
+                best = ms < best ? ms : best;
+            }
+            const double moved = (double)tiles * 8 * 16384;
+            printf("%-34s stages=%2d : %7.2f us  %7.1f GB/s gathered  (%s)\n", name, stages, best * 1e3, moved / best / 1e6,
+                   cudaGetErrorString(cudaGetLastError()));
+        };
+        run4("TMA gather4, 1 issuer", gather_tma<6, 1>, 6);
+        run4("TMA gather4, 4 issuers", gather_tma<6, 4>, 6);
+        run4("TMA gather4, 4 issuers", gather_tma<10, 4>, 10);
+        run4("TMA gather4, 32 issuers", gather_tma<10, 32>, 10);
+    }
     return 0;
 }

@@ -61,10 +61,10 @@ for mode in range(6):
         kb = (ctypes.c_ulonglong * 512)()
         lib.lasnet_ktrace_read(kb)
         k = np.array(kb, dtype=np.int64).reshape(128, 4)
-        print("   kblk  gather   tma   mmaFull  (us rel.)  lat(full-issue)")
+        print("   kblk  gather   tma   mmaFull  gthrWaitDone (us rel.)  lat(full-issue)")
         for i in range(0, 48):
             if k[i, 1] == 0:
                 continue
             iss = max(k[i, 0], k[i, 1]) if k[i, 0] else k[i, 1]
-            print(f"   {i:4d} " + " ".join(f"{(v - t0) / 1e3:7.2f}" if v else "    nan" for v in k[i, :3])
+            print(f"   {i:4d} " + " ".join(f"{(v - t0) / 1e3:7.2f}" if v else "    nan" for v in k[i, :4])
                   + f"   {(k[i, 2] - iss) / 1e3:6.2f}")
