@@ -134,6 +134,9 @@ def algorithmic_work(mask_cells: np.ndarray, n, h, w, c_in, c_mid, c_out, s):
     W1, W2, W3 = c_mid * c_in * e, 9 * c_mid * c_mid * e, c_out * c_mid * e
     k = {
         "mask_compact": dict(bytes=n * h * w * c_in * e + n * gh * gw + 4 * P + 4, flops=2 * n * h * w * c_in),
+        # fused steps 4+5: h1 read once per tap-row window, residual + y, both weights
+        "conv23": dict(bytes=P * hs2 * c_mid * e + 2 * out_px * c_out * e + 9 * c_mid * c_mid * e + c_out * c_mid * e,
+                       flops=2 * out_px * 9 * c_mid * c_mid + 2 * out_px * c_mid * c_out),
         "conv1": dict(bytes=halo_px * c_in * e + P * hs2 * c_mid * e + W1, flops=2 * halo_px * c_in * c_mid),
         "conv2": dict(bytes=P * hs2 * c_mid * e + P * ss * c_mid * e + W2, flops=2 * out_px * 9 * c_mid * c_mid),
         "conv3": dict(bytes=P * ss * c_mid * e + 2 * out_px * c_out * e + W3, flops=2 * out_px * c_mid * c_out),
@@ -152,7 +155,8 @@ def ncu_traffic(kernel: str):
     ncu --set full capture (profiles/ncu_full_<tag>.json), or (None, None)."""
     import glob
 
-    names = {"mask_compact": "mask_compact", "conv1": "conv1_dyn", "conv2": "conv2_dyn", "conv3": "conv3_dyn"}
+    names = {"mask_compact": "mask_compact", "conv1": "conv1_dyn", "conv2": "conv2_dyn", "conv3": "conv3_dyn",
+             "conv23": "conv23_dyn"}
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_full_*.json")), key=os.path.getmtime)
     for f in reversed(files):
         d = json.load(open(f))
@@ -298,7 +302,8 @@ def run_lasnet(args):
     kwork, bwork, dwork, stats = algorithmic_work(mask_cells, n, h, w, c_in, c_mid, c_in, s)
 
     K = args.steps
-    names = ["mask_compact", "conv1", "conv2", "conv3"]
+    fused23 = os.environ.get("LASNET_NO_FUSE", "0") != "1" and c_mid in (64, 128) and c_in % 128 == 0
+    names = ["mask_compact", "conv1", "conv23"] if fused23 else ["mask_compact", "conv1", "conv2", "conv3"]
     ev_step = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     ev_k = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * len(names))] for _ in range(K)]
     for row in ev_k:

@@ -198,10 +198,10 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     KTRACE(it, 1);
                     if (MODE == CONV2_DYN) {
                         const int tap = kb / kpt, dy = tap / 3, dx = tap - dy * 3;
-                        tma_load_4d(sa, &args.tmap_a, fb, (kb - tap * kpt) * kBK, dx, dy, u0);
+                        tma_load_5d(sa, &args.tmap_a, fb, 0, dx, dy, u0, kb - tap * kpt);  // h1 [c/64][P][S+2][S+2][64]
                     } else if (MODE == CONV2_DENSE) {
                         const int tap = kb / kpt, dy = tap / 3, dx = tap - dy * 3;
-                        tma_load_4d(sa, &args.tmap_a, fb, (kb - tap * kpt) * kBK, dx - 1, d2y + dy - 1, d2n);
+                        tma_load_5d(sa, &args.tmap_a, fb, 0, dx - 1, d2y + dy - 1, d2n, kb - tap * kpt);  // [c/64][N][H][W][64]
                     } else if (!C::kGather) {
                         tma_load_2d(sa, &args.tmap_a, fb, kb * kBK, mt * kBM);
                     }
@@ -463,6 +463,9 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     dense2_tile(args, mt, d2n, d2y);
                     for (int c = 0; c < BN / 64; ++c)
                         tma_store_4d(&args.tmap_out, sbuf + c * kChunkBytes, n0 + c * 64, 0, d2y, d2n);
+                } else if (MODE == CONV1_DYN || MODE == CONV1_DENSE) {  // h1: [c_mid/64][rows][64]
+                    for (int c = 0; c < BN / 64; ++c)
+                        tma_store_3d(&args.tmap_out, sbuf + c * kChunkBytes, 0, mt * kBM, (n0 >> 6) + c);
                 } else {
                     const int row0 = MODE == CONV2_DYN ? mt * args.units_per_tile * args.S * args.S : mt * kBM;
                     for (int c = 0; c < BN / 64; ++c)

@@ -3,6 +3,7 @@
 // allocated here and no per-call state is kept (the only globals are the
 // cached SM count and a thread-local launch counter for bench bookkeeping).
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <cuda.h>
@@ -24,6 +25,7 @@ cudaError_t launch_mask_compact(int dtype_bf16, const void *x, const float *wm, 
                                 cudaStream_t st);
 cudaError_t launch_conv_tc(int mode, const ConvArgs &a, int max_tiles_m, int num_sms, cudaStream_t st);
 cudaError_t launch_conv_simt(int mode, const ConvArgs &a, int max_rows, cudaStream_t st);
+cudaError_t launch_conv23(bool dense, const ConvArgs &a, int max_tiles, int num_sms, cudaStream_t st);
 }  // namespace lasnet
 
 using namespace lasnet;
@@ -179,6 +181,17 @@ bool tmap4(CUtensorMap *m, const void *base, uint64_t c, uint64_t w, uint64_t h,
     return tmap(m, base, 4, d, b);
 }
 
+bool tmap3(CUtensorMap *m, const void *base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1,
+           uint32_t b2) {
+    const uint64_t d[3] = {d0, d1, d2};
+    const uint32_t b[3] = {b0, b1, b2};
+    return tmap(m, base, 3, d, b);
+}
+
+bool tmap5(CUtensorMap *m, const void *base, const uint64_t (&d)[5], const uint32_t (&b)[5]) {
+    return tmap(m, base, 5, d, b);
+}
+
 int bn_of(int n) { return n == 64 ? 64 : 128; }
 
 // Fills the TMA descriptors and tile geometry of one tcgen05 convolution and
@@ -191,14 +204,16 @@ int prepare_tc(int mode, ConvArgs &a, const lasnet_block_desc *d, const void *x,
     bool ok = tmap2(&a.tmap_b, a.w, a.K, a.N, 64, bn_of(a.N));
     switch (mode) {
         case CONV1_DYN: {
-            // A = halo rows gathered by cp.async; h1 rows stored by 2-D TMA boxes
-            ok = ok && tmap2(&a.tmap_out, h1, C, (uint64_t)cap * hs * hs, 64, 128);
+            // A = halo rows gathered by cp.async; h1 stored channel-chunk-major
+            // [c_mid/64][rows][64] by 3-D TMA boxes {64, 128, 1}
+            ok = ok && tmap3(&a.tmap_out, h1, 64, (uint64_t)cap * hs * hs, C / 64, 64, 128, 1);
             return ok ? (int)(((long)cap * hs * hs + 127) / 128) : -1;
         }
         case CONV2_DYN: {
             a.units_per_tile = 128 / (S * S);
             a.box_rows = a.units_per_tile * S * S;
-            ok = ok && tmap4(&a.tmap_a, h1, C, hs, hs, cap, 64, S, S, a.units_per_tile);
+            ok = ok && tmap5(&a.tmap_a, h1, {64, (uint64_t)hs, (uint64_t)hs, (uint64_t)cap, (uint64_t)(C / 64)},
+                             {64, (uint32_t)S, (uint32_t)S, (uint32_t)a.units_per_tile, 1});
             ok = ok && tmap2(&a.tmap_out, h2, C, (uint64_t)cap * S * S, 64, a.box_rows);
             return ok ? (cap + a.units_per_tile - 1) / a.units_per_tile : -1;
         }
@@ -209,7 +224,7 @@ int prepare_tc(int mode, ConvArgs &a, const lasnet_block_desc *d, const void *x,
         }
         case CONV1_DENSE: {
             ok = ok && tmap2(&a.tmap_a, x, d->c_in, px, 64, 128);
-            ok = ok && tmap2(&a.tmap_out, h1, C, px, 64, 128);
+            ok = ok && tmap3(&a.tmap_out, h1, 64, px, C / 64, 64, 128, 1);
             return ok ? (int)((px + 127) / 128) : -1;
         }
         case CONV2_DENSE: {
@@ -223,7 +238,8 @@ int prepare_tc(int mode, ConvArgs &a, const lasnet_block_desc *d, const void *x,
                 a.dense_tiles = d->n * ((d->h + a.rows_h - 1) / a.rows_h);
             }
             a.box_rows = d->w * a.rows_h * a.imgs_box;
-            ok = ok && tmap4(&a.tmap_a, h1, C, d->w, d->h, d->n, 64, d->w, a.rows_h, a.imgs_box);
+            ok = ok && tmap5(&a.tmap_a, h1, {64, (uint64_t)d->w, (uint64_t)d->h, (uint64_t)d->n, (uint64_t)(C / 64)},
+                             {64, (uint32_t)d->w, (uint32_t)a.rows_h, (uint32_t)a.imgs_box, 1});
             ok = ok && tmap4(&a.tmap_out, h2, C, d->w, d->h, d->n, 64, d->w, a.rows_h, a.imgs_box);
             return ok ? a.dense_tiles : -1;
         }
@@ -233,6 +249,51 @@ int prepare_tc(int mode, ConvArgs &a, const lasnet_block_desc *d, const void *x,
         }
     }
     return -1;
+}
+
+// Steps 4+5 fused in one tcgen05 kernel (conv23_tc.cu): bf16, c_mid in {64, 128},
+// c_out a multiple of 128.  LASNET_NO_FUSE=1 in the environment selects the
+// separate conv2 / conv3 kernels (A/B measurements).
+bool use_fused23(const lasnet_block_desc *d) {
+    static const bool off = [] {
+        const char *e = getenv("LASNET_NO_FUSE");
+        return e && e[0] == '1';
+    }();
+    return !off && d->dtype == LASNET_BF16 && (d->c_mid == 64 || d->c_mid == 128) && d->c_out % 64 == 0;
+}
+
+cudaError_t run_conv23(const lasnet_block_desc *d, bool dense, ConvArgs a, const lasnet_block_weights *w,
+                       const void *x, void *y, const void *h1, int cap, cudaStream_t st) {
+    const int S = d->s, hs = S + 2, C = d->c_mid;
+    a.a_src = h1; a.w = w->w2; a.bias = w->b2; a.out = y; a.resid = x;
+    a.K = 9 * C; a.N = C; a.a_ld = C; a.out_ld = d->c_out;
+    a.w3 = w->w3; a.bias3 = w->b3; a.n3 = d->c_out;
+    bool ok = tmap2(&a.tmap_b, a.w, a.K, a.N, 64, C) && tmap2(&a.tmap_b3, w->w3, C, d->c_out, 64, d->c_out % 128 == 0 ? 128 : 64);  // conv3 MMA N
+    int tiles;
+    if (dense) {
+        if (d->h * d->w <= 128) {
+            a.rows_h = d->h;
+            a.imgs_box = 128 / (d->h * d->w);
+            a.dense_tiles = (d->n + a.imgs_box - 1) / a.imgs_box;
+        } else {
+            a.rows_h = 128 / d->w;
+            a.imgs_box = 1;
+            a.dense_tiles = d->n * ((d->h + a.rows_h - 1) / a.rows_h);
+        }
+        a.box_rows = d->w * a.rows_h * a.imgs_box;
+        ok = ok && tmap5(&a.tmap_a, h1, {64, (uint64_t)d->w, (uint64_t)d->h, (uint64_t)d->n, (uint64_t)(C / 64)},
+                         {64, (uint32_t)d->w, (uint32_t)a.rows_h, (uint32_t)a.imgs_box, 1});
+        tiles = a.dense_tiles;
+    } else {
+        a.units_per_tile = 128 / (S * S);
+        a.box_rows = a.units_per_tile * S * S;
+        ok = ok && tmap5(&a.tmap_a, h1, {64, (uint64_t)hs, (uint64_t)hs, (uint64_t)cap, (uint64_t)(C / 64)},
+                         {64, (uint32_t)S, (uint32_t)S, (uint32_t)a.units_per_tile, 1});
+        tiles = (cap + a.units_per_tile - 1) / a.units_per_tile;
+    }
+    if (!ok) return cudaErrorInvalidValue;
+    KernelEvents ev(st);
+    return launch_conv23(dense, a, tiles, num_sms(), st);
 }
 
 // One convolution: tcgen05 kernel (bf16) or fp32 CUDA-core kernel.
@@ -404,6 +465,11 @@ lasnet_status lasnet_dyn_block(const lasnet_block_desc *d, const lasnet_block_we
     a.a_src = x; a.w = w->w1; a.bias = w->b1; a.out = h1; a.resid = nullptr;
     a.K = d->c_in; a.N = d->c_mid; a.a_ld = d->c_in; a.out_ld = d->c_mid;
     if (run_conv(d, CONV1_DYN, a, cap * hs2, x, y, h1, h2, cap, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    if (use_fused23(d)) {  // steps 4+5 in one kernel: h2 never leaves shared memory
+        if (run_conv23(d, false, a, w, x, y, h1, cap, st) != cudaSuccess) return LASNET_ERR_CUDA;
+        g_last_launches = 2;
+        return LASNET_OK;
+    }
     // step 4: 3x3 conv on the gathered patch batch
     a.a_src = h1; a.w = w->w2; a.bias = w->b2; a.out = h2;
     a.K = 9 * d->c_mid; a.N = d->c_mid; a.a_ld = d->c_mid; a.out_ld = d->c_mid;
@@ -444,6 +510,11 @@ lasnet_status lasnet_dense_block(const lasnet_block_desc *d, const lasnet_block_
     a.a_src = x; a.w = w->w1; a.bias = w->b1; a.out = h1;
     a.K = d->c_in; a.N = d->c_mid; a.a_ld = d->c_in; a.out_ld = d->c_mid;
     if (run_conv(d, CONV1_DENSE, a, px, x, y, h1, h2, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    if (use_fused23(d)) {
+        if (run_conv23(d, true, a, w, x, y, h1, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
+        g_last_launches = 2;
+        return LASNET_OK;
+    }
     a.a_src = h1; a.w = w->w2; a.bias = w->b2; a.out = h2;
     a.K = 9 * d->c_mid; a.N = d->c_mid; a.a_ld = d->c_mid; a.out_ld = d->c_mid;
     if (run_conv(d, CONV2_DENSE, a, px, x, y, h1, h2, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;

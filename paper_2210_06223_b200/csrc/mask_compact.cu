@@ -14,6 +14,7 @@
 // aggregate, looks back over predecessors 32 at a time, and writes ascending
 // cell ids.  The last tile writes the device count.
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -287,8 +288,14 @@ MaskGeo mask_geo(int C, int PV, int S) {
     g.ppw = g.nvec < 32 ? 32 / g.nvec : 1;
     g.nvl = g.nvec >= 32 ? g.nvec / 32 : 1;
     const int items = g.nvec >= 32 ? S * S * g.nvl : (S * S + g.ppw - 1) / g.ppw;  // loads per lane per cell
+    // warps per cell: LASNET_MASK_MAXITEMS (default 8 = loads per lane per round
+    // trip) bounds a warp's share; 1 warp per cell walks the cell in several round trips
+    static const int max_items = [] {
+        const char *e = getenv("LASNET_MASK_MAXITEMS");
+        return e ? atoi(e) : 2 * kMaxItems;
+    }();
     g.wpc = 1;
-    while (g.wpc < 8 && (items + g.wpc - 1) / g.wpc > kMaxItems) g.wpc *= 2;
+    while (g.wpc < 8 && (items + g.wpc - 1) / g.wpc > max_items) g.wpc *= 2;
     g.cpb = 8 / g.wpc;
     return g;
 }

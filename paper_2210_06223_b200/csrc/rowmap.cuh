@@ -45,6 +45,10 @@ struct ConvArgs {
     CUtensorMap tmap_b;     // weight matrix [N][K]
     CUtensorMap tmap_out;   // output (h1, h2 or y)
     CUtensorMap tmap_res;   // residual x (conv3)
+    CUtensorMap tmap_b3;    // conv3 weights [c_out][c_mid] (fused conv2+conv3 kernel)
+    const void *w3;         // fused kernel: conv3 weights
+    const float *bias3;     // fused kernel: conv3 bias [c_out]
+    int32_t n3;             // fused kernel: c_out
     const void *a_src;      // x (conv1), h1 (conv2), h2 (conv3)
     const void *w;          // [N][K] row-major (K-major)
     const float *bias;      // [N]

@@ -65,6 +65,10 @@ __global__ void tma_stream(const __grid_constant__ CUtensorMap tm, int mode, int
                 if (mode == 1) {
                     asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];"
                                  ::"r"(dst), "l"((uint64_t)&tm), "r"(bar), "r"(kc), "r"(gx * 4 + 1 - d - d), "r"(gy * 4 + 1 - d - d), "r"(n) : "memory");
+                } else if (mode == 3) {  // h1-like [P][6][6][128]: box {64,4,4,8}
+                    const int p0 = (int)((sd >> 33) % 3000u);
+                    asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];"
+                                 ::"r"(dst), "l"((uint64_t)&tm), "r"(bar), "r"((it & 1) * 64), "r"(it % 3), "r"((it / 3) % 3), "r"(p0) : "memory");
                 } else {  // mode 2: 3-D box {64, 6, 6} over [N*H][W][C]
                     asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
                                  ::"r"(dst), "l"((uint64_t)&tm), "r"(bar), "r"(kc), "r"(gx * 4 + 1 - d - d), "r"(n * H + gy * 4 + 1 - d - d) : "memory");
@@ -137,7 +141,10 @@ int main() {
     const cuuint64_t gs4[3] = {(cuuint64_t)C * 2, (cuuint64_t)C * 2 * W, (cuuint64_t)C * 2 * W * H};
     const cuuint64_t gd3[3] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H * N};
     const cuuint64_t gs3[2] = {(cuuint64_t)C * 2, (cuuint64_t)C * 2 * W};
-    CUtensorMap t2_128, t2_36, t4_66, t4_66_np, t4_66_128, t3_66, t4_28x4;
+    CUtensorMap t2_128, t2_36, t4_66, t4_66_np, t4_66_128, t3_66, t4_28x4, th1;
+    const cuuint64_t gdh[4] = {128, 6, 6, 3200}, gsh[3] = {256, 256 * 6, 256 * 36};
+    const cuuint32_t bh[4] = {64, 4, 4, 8};
+    enc(&th1, 4, gdh, gsh, bh, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
     const cuuint32_t b2_128[2] = {64, 128}, b2_36[2] = {64, 36}, b4_66[4] = {64, 6, 6, 1}, b3_66[3] = {64, 6, 6},
                      b4_28[4] = {64, 28, 4, 1};
     enc(&t2_128, 2, gd2, gs2, b2_128, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
@@ -160,6 +167,8 @@ int main() {
         {&t4_66_128, 1, 8, 3, 4608, 2, "4D {64,6,6,1} promo128 k-sweep, 8 stg"},
         {&t3_66, 2, 8, 3, 4608, 2, "3D {64,6,6} k-sweep, 8 stg"},
         {&t4_28x4, 1, 8, 1, 14336, 2, "4D {64,28,4,1} k-sweep, 8 stg"},
+        {&th1, 3, 4, 1, 16384, 0, "h1 im2col 4D {64,4,4,8} (L2-resident), 4 stg"},
+        {&th1, 3, 8, 1, 16384, 0, "h1 im2col 4D {64,4,4,8} (L2-resident), 8 stg"},
     };
     for (auto &c : cfgs) {
         const int iters = 256;

@@ -33,6 +33,33 @@ for _ in range(3):
     lib.lasnet_mtrace_read(mt)
     print(f"== mask_compact: last decision {(mt[1] - mt[0]) / 1e3:.2f} us, compaction start {(mt[2] - mt[0]) / 1e3:.2f}, "
           f"done {(mt[3] - mt[0]) / 1e3:.2f} us after the first CTA started")
+if hasattr(lib, "lasnet_trace23_read"):
+    lib.lasnet_trace23_read.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
+    for _ in range(2):
+        y.copy_(x)
+        blk.forward(y)
+    torch.cuda.synchronize()
+    lib.lasnet_trace23_clear()
+    y.copy_(x)
+    blk.forward(y)
+    torch.cuda.synchronize()
+    b23 = (ctypes.c_ulonglong * 512)()
+    lib.lasnet_trace23_read(b23)
+    t = np.array(b23, dtype=np.int64).reshape(64, 8)
+    t0 = t[t[:, 0] > 0][:, 0].min()
+    print("== conv23 (fused conv2+conv3), CTA0; us: conv2 start | acc2 ready | H2 staged | conv3 MMAs done | stored")
+    for i in range(64):
+        if t[i, 0]:
+            print(f"   {i:4d} " + " ".join(f"{(v - t0) / 1e3:7.2f}" if v else "    nan" for v in t[i, :5]))
+    if hasattr(lib, "lasnet_trace23c_read"):
+        lib.lasnet_trace23c_read.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
+        bc = (ctypes.c_ulonglong * 1024)()
+        lib.lasnet_trace23c_read(bc)
+        tc = np.array(bc, dtype=np.int64).reshape(64, 16)
+        print("   chunk  W3issue accFree W3land  commit | resLand accRdy stored  tmemLd  mathDn  ldsDn")
+        for c in range(64):
+            if tc[c, 0]:
+                print(f"   {c:5d} " + " ".join(f"{(v - t0) / 1e3:7.2f}" if v else "    nan" for v in tc[c, :10]))
 names = {0: "conv1_dyn", 1: "conv2_dyn", 2: "conv3_dyn", 3: "conv1_dense", 4: "conv2_dense", 5: "conv3_dense"}
 for mode in range(6):
     for _ in range(2):
