@@ -157,7 +157,7 @@ def ncu_traffic(kernel: str):
 
     names = {"mask_compact": "mask_compact", "conv1": "conv1_dyn", "conv2": "conv2_dyn", "conv3": "conv3_dyn",
              "conv23": "conv23_dyn"}
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_full_*.json")), key=os.path.getmtime)
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_full_*.json")))  # by round tag
     for f in reversed(files):
         d = json.load(open(f))
         for e in d.get("full", []):

@@ -20,6 +20,9 @@ def short(name):
     name = name.replace("lasnet::", "").replace("(lasnet::ConvArgs)", "")
     table = {"conv_tc_kernel<0,": "conv1_dyn", "conv_tc_kernel<1,": "conv2_dyn", "conv_tc_kernel<2,": "conv3_dyn",
              "conv_tc_kernel<3,": "conv1_dense", "conv_tc_kernel<4,": "conv2_dense", "conv_tc_kernel<5,": "conv3_dense",
+             "conv23_kernel<(bool)0>": "conv23_dyn", "conv23_kernel<(bool)1>": "conv23_dense",
+             "conv23_kernel<0>": "conv23_dyn", "conv23_kernel<1>": "conv23_dense",
+             "conv23_kernel<false>": "conv23_dyn", "conv23_kernel<true>": "conv23_dense",
              "masker_compact_kernel": "mask_compact", "masker_kernel": "mask", "compact_kernel": "compact"}
     flat = name.replace(" ", "").replace("(int)", "")
     for k, v in table.items():
@@ -41,10 +44,22 @@ launches = [dict(id=int(k), kernel=short(v["name"]), grid=v["grid"], block=v["bl
                  dram_write=v.get("dram__bytes_write.sum")) for k, v in per.items()]
 launches.sort(key=lambda d: d["id"])
 # the last dynamic step: last mask_compact and the three convs after it
+DYN = ("conv1_dyn", "conv2_dyn", "conv3_dyn", "conv23_dyn")
+DENSE = ("conv2_dense", "conv3_dense", "conv23_dense")
 idx_mc = max(i for i, d in enumerate(launches) if d["kernel"] == "mask_compact")
-step = [d for d in launches[idx_mc:idx_mc + 4]]
+step = [launches[idx_mc]]
+for d in launches[idx_mc + 1:]:
+    if d["kernel"] not in DYN:
+        break
+    step.append(d)
 dense_ids = [i for i, d in enumerate(launches) if d["kernel"] == "conv1_dense"]
-dense = launches[dense_ids[-1]:dense_ids[-1] + 3] if dense_ids else []
+dense = []
+if dense_ids:
+    dense = [launches[dense_ids[-1]]]
+    for d in launches[dense_ids[-1] + 1:]:
+        if d["kernel"] not in DENSE:
+            break
+        dense.append(d)
 with open(os.path.join(out_dir, f"ncu_launches_{tag}.csv"), "w") as f:
     w = csv.writer(f)
     w.writerow(["id", "kernel", "grid", "block", "time_ns", "dram_read_bytes", "dram_write_bytes"])
