@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
     ap.add_argument("--detail", default=None, help="write per-kernel detail JSON here")
+    ap.add_argument("--schedule", default="auto", choices=["auto", "separate", "fused"],
+                    help="separate: north-star branch (masker, then gather+conv1 on halos); fused: the paper's "
+                         "Table-1 schedule (masker fused into a static conv1); auto: lasnet_choose_schedule(r)")
     return ap.parse_args()
 
 
@@ -140,14 +143,25 @@ def algorithmic_work(mask_cells: np.ndarray, n, h, w, c_in, c_mid, c_out, s):
         "conv1": dict(bytes=halo_px * c_in * e + P * hs2 * c_mid * e + W1, flops=2 * halo_px * c_in * c_mid),
         "conv2": dict(bytes=P * hs2 * c_mid * e + P * ss * c_mid * e + W2, flops=2 * out_px * 9 * c_mid * c_mid),
         "conv3": dict(bytes=P * ss * c_mid * e + 2 * out_px * c_out * e + W3, flops=2 * out_px * c_mid * c_out),
+        # masker-fused schedule: dense conv1 + masker partials; decision + compaction + h1 halo gather
+        "conv1_mask": dict(bytes=n * h * w * (c_in * e + c_mid * e + 16) + W1,
+                           flops=2 * n * h * w * c_in * (c_mid + 1)),
+        "decide_gather": dict(bytes=n * h * w * 16 + n * gh * gw + 4 * P + halo_px * c_mid * e + P * hs2 * c_mid * e,
+                              flops=0),
     }
     block = dict(
         bytes=n * h * w * c_in * e + n * gh * gw + 4 * P + halo_px * c_in * e + 2 * out_px * c_out * e + W1 + W2 + W3,
         flops=k["conv1"]["flops"] + k["conv2"]["flops"] + k["conv3"]["flops"])
+    # the masker-fused schedule's own minimum: x once, h1 written once and its halos
+    # read back, residual + y of active pixels, weights; dense conv1 FLOPs
+    block_fused = dict(
+        bytes=n * h * w * (c_in + c_mid) * e + n * gh * gw + 4 * P + halo_px * c_mid * e + 2 * out_px * c_out * e
+        + W1 + W2 + W3,
+        flops=2 * n * h * w * c_in * c_mid + k["conv2"]["flops"] + k["conv3"]["flops"])
     dense = dict(bytes=2 * n * h * w * c_in * e + W1 + W2 + W3,
                  flops=2 * n * h * w * (c_in * c_mid + 9 * c_mid * c_mid + c_mid * c_out))
     return k, block, dense, dict(P=P, halo_px=halo_px, out_px=out_px, r_patch=P / (n * gh * gw),
-                                 r_pixel=out_px / (n * h * w))
+                                 r_pixel=out_px / (n * h * w), block_fused=block_fused)
 
 
 def ncu_traffic(kernel: str):
@@ -156,7 +170,7 @@ def ncu_traffic(kernel: str):
     import glob
 
     names = {"mask_compact": "mask_compact", "conv1": "conv1_dyn", "conv2": "conv2_dyn", "conv3": "conv3_dyn",
-             "conv23": "conv23_dyn"}
+             "conv23": "conv23_dyn", "conv1_mask": "conv1_mask", "decide_gather": "decide_gather"}
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_full_*.json")))  # by round tag
     for f in reversed(files):
         d = json.load(open(f))
@@ -276,7 +290,14 @@ def run_lasnet(args):
     x_cpu = synth.make_x(n, h, w, c_in, seed=0 + 7919 * rank)
     wts_cpu = synth.make_block_weights(c_in, c_mid, c_in, seed=1)
     wm_cpu = synth.make_masker_weights(c_in, seed=2)
-    blk = L.DynBlock(L.BlockShape(n, h, w, c_in, c_mid, s), wts_cpu, wm_cpu, 0.0)
+    if args.schedule == "auto":
+        sched = L.choose_schedule(n, h, w, c_in, c_mid, c_in, s, wl["r"])
+    else:
+        sched = L.SCHED_FUSED if args.schedule == "fused" else L.SCHED_SEPARATE
+    sched_name = "fused" if sched == L.SCHED_FUSED else "separate"
+    # separate: the step-by-step north-star calls (mask_compact + dyn_block); fused: lasnet_block_forward
+    blk = L.DynBlock(L.BlockShape(n, h, w, c_in, c_mid, s), wts_cpu, wm_cpu, 0.0,
+                     schedule=L.SCHED_FUSED if sched == L.SCHED_FUSED else None)
     # masker bias calibrated on a separate batch of the same distribution
     blk.calibrate_bias(synth.make_x(n, h, w, c_in, seed=1000 + rank).cuda(), wl["r"])
     x = x_cpu.cuda()
@@ -303,7 +324,8 @@ def run_lasnet(args):
 
     K = args.steps
     fused23 = os.environ.get("LASNET_NO_FUSE", "0") != "1" and c_mid in (64, 128) and c_in % 128 == 0
-    names = ["mask_compact", "conv1", "conv23"] if fused23 else ["mask_compact", "conv1", "conv2", "conv3"]
+    head = ["conv1_mask", "decide_gather"] if sched == L.SCHED_FUSED else ["mask_compact", "conv1"]
+    names = head + (["conv23"] if fused23 else ["conv2", "conv3"])
     ev_step = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     ev_k = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * len(names))] for _ in range(K)]
     for row in ev_k:
@@ -384,6 +406,13 @@ def run_lasnet(args):
         blk_roof.update({"t_roof_ms": round(t_roof, 4), "frac_time": round(t_roof / statistics.fmean(step_ms), 4),
                          "definition": "headline: masker read of x + idx + halo gather + residual + y + weights; "
                                        "halo-method FLOPs (SURVEY 8(d))"})
+        if sched == L.SCHED_FUSED:
+            bf = stats["block_fused"]
+            t_f = max(bf["bytes"] / (hbm * 1e9), bf["flops"] / (tfl * 1e12)) * 1e3
+            blk_roof["schedule_roofline"] = {
+                "t_roof_ms": round(t_f, 4), "frac_time": round(t_f / statistics.fmean(step_ms), 4),
+                "definition": "masker-fused schedule minimum: x once + h1 write + h1 halo reads + residual + y + "
+                              "weights; dense-conv1 FLOPs"}
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "images/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": round(tot_max / K, 4), "higher_is_better": True,
@@ -391,7 +420,8 @@ def run_lasnet(args):
             "config": {"workload": WORKLOAD_NAME, "global_batch": world * n, "per_gpu_batch": n,
                        "H": h, "W": w, "c_in": c_in, "c_mid": c_mid, "S": s, "r_target": wl["r"],
                        "r_patch": round(stats["r_patch"], 4), "r_pixel": round(stats["r_pixel"], 4),
-                       "parallelism": f"dp{world}", "l2": "flushed (256 MiB read) before every timed step"},
+                       "parallelism": f"dp{world}", "l2": "flushed (256 MiB read) before every timed step",
+                       "schedule": sched_name},
             "latency_ms": {"p10": round(float(np.percentile(step_ms, 10)), 4),
                            "p50": round(float(np.percentile(step_ms, 50)), 4),
                            "p90": round(float(np.percentile(step_ms, 90)), 4)},

@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define LASNET_ABI_VERSION 1
+#define LASNET_ABI_VERSION 2
 
 typedef enum {
     LASNET_OK = 0,
@@ -154,6 +154,42 @@ lasnet_status lasnet_dense_block(const lasnet_block_desc *desc, const lasnet_blo
                                  const void *x, void *y, void *ws, size_t ws_bytes,
                                  lasnet_stream_t stream);
 size_t lasnet_dense_workspace_bytes(const lasnet_block_desc *desc);
+
+/* The whole block, steps 1-5, in one call, under one of two schedules.
+ *
+ * LASNET_SCHED_MASKER_SEPARATE -- the north-star branch: masker + compaction in
+ *   one launch (lasnet_mask_compact), then lasnet_dyn_block (gather + conv1 on
+ *   the (s+2)^2 halo of each active patch, conv2, conv3 + scatter-add).  The
+ *   masker reads all of x once and conv1 reads the halos again.
+ * LASNET_SCHED_MASKER_FUSED -- the paper's best schedule (Table 1 last row,
+ *   P:336-342; sec. 3.4; App. B): the masker is fused into a
+ *   STATIC conv1 that reads x once and computes h1 on every pixel together with
+ *   the masker's per-pixel partial logits; one launch then decides every cell,
+ *   compacts the indices and gathers the h1 halos of the active patches (the
+ *   "gather fused into the 3x3 conv" of Table 1 feeds conv2 from them); conv2 +
+ *   conv3 + scatter-add as in lasnet_dyn_block.  bf16 only.
+ * Both produce bit-identical mask / idx / count (the decision rule is the one
+ * of lasnet_mask: certified fp32 with an exact fp64 re-sum when the bound does
+ * not separate the logit from 0) and the same y up to fp32 accumulation order.
+ *   x, y     [n][h][w][c_in]; y == x in place, else x is copied to y first;
+ *            partial overlap -> LASNET_ERR_ALIAS
+ *   wm, bm   masker as in lasnet_mask
+ *   schedule lasnet_schedule value, else LASNET_ERR_DOMAIN
+ *   mask     [n][gh][gw] uint8 out, nullable
+ *   idx      [n*gh*gw] int32 out (capacity = all cells), count int32 device out
+ *   ws       lasnet_block_forward_workspace_bytes(desc, schedule) bytes, ALL ZERO
+ *            before the first call (its leading control words are left zero by
+ *            every call; the rest is scratch).  Concurrent calls must not share it. */
+typedef enum { LASNET_SCHED_MASKER_SEPARATE = 0, LASNET_SCHED_MASKER_FUSED = 1 } lasnet_schedule;
+lasnet_status lasnet_block_forward(const lasnet_block_desc *desc, const lasnet_block_weights *wts,
+                                   const void *x, void *y, const float *wm, float bm, int32_t schedule,
+                                   uint8_t *mask, int32_t *idx, int32_t *count, void *ws, size_t ws_bytes,
+                                   lasnet_stream_t stream);
+size_t lasnet_block_forward_workspace_bytes(const lasnet_block_desc *desc, int32_t schedule);
+/* Host-side schedule choice for an expected activation rate r (the paper's
+ * threshold r_th, from a B200 HBM-bytes model): returns the
+ * lasnet_schedule that moves fewer bytes.  Pure, launches nothing. */
+int32_t lasnet_choose_schedule(const lasnet_block_desc *desc, double r);
 
 /* Benchmark instrumentation.  The next n_pairs kernels this host thread
  * launches through the ABI are bracketed by cudaEventRecord(events[2i]) and

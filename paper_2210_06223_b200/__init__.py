@@ -4,8 +4,9 @@ Product path: include/lasnet.h C ABI implemented by liblasnet.so (sm_100a
 kernels in csrc/), bound by ctypes in _lib.py, with the Python API in block.py.
 There is no CPU fallback: calls raise if the CUDA library is missing.
 """
-from .block import (BlockShape, DynBlock, compact, dense_block, dyn_block, grid, last_launch_count,
-                    make_desc, make_weights, mask)
+from ._lib import SCHED_FUSED, SCHED_SEPARATE
+from .block import (BlockShape, DynBlock, block_forward, choose_schedule, compact, dense_block, dyn_block, grid,
+                    last_launch_count, make_desc, make_weights, mask)
 
-__all__ = ["BlockShape", "DynBlock", "compact", "dense_block", "dyn_block", "grid", "last_launch_count",
-           "make_desc", "make_weights", "mask"]
+__all__ = ["BlockShape", "DynBlock", "SCHED_FUSED", "SCHED_SEPARATE", "block_forward", "choose_schedule", "compact",
+           "dense_block", "dyn_block", "grid", "last_launch_count", "make_desc", "make_weights", "mask"]

@@ -23,7 +23,11 @@ EXPORTS = [
     "lasnet_mask", "lasnet_mask_compact", "lasnet_mask_compact_workspace_bytes", "lasnet_compact", "lasnet_compact_workspace_bytes", "lasnet_dyn_block",
     "lasnet_dyn_workspace_bytes", "lasnet_dense_block", "lasnet_dense_workspace_bytes",
     "lasnet_status_str", "lasnet_abi_version", "lasnet_last_launch_count", "lasnet_set_kernel_events",
+    "lasnet_block_forward", "lasnet_block_forward_workspace_bytes", "lasnet_choose_schedule",
 ]
+
+# lasnet_schedule
+SCHED_SEPARATE, SCHED_FUSED = 0, 1
 
 
 class BlockDesc(ctypes.Structure):
@@ -74,6 +78,12 @@ def load(path: str = LIB_PATH):
     lib.lasnet_dense_block.restype = ctypes.c_int
     lib.lasnet_dense_workspace_bytes.argtypes = [D]
     lib.lasnet_dense_workspace_bytes.restype = sz
+    lib.lasnet_block_forward.argtypes = [D, Wt, vp, vp, vp, ctypes.c_float, i32, vp, vp, vp, vp, sz, vp]
+    lib.lasnet_block_forward.restype = ctypes.c_int
+    lib.lasnet_block_forward_workspace_bytes.argtypes = [D, i32]
+    lib.lasnet_block_forward_workspace_bytes.restype = sz
+    lib.lasnet_choose_schedule.argtypes = [D, ctypes.c_double]
+    lib.lasnet_choose_schedule.restype = i32
     lib.lasnet_status_str.argtypes = [ctypes.c_int]
     lib.lasnet_status_str.restype = ctypes.c_char_p
     lib.lasnet_abi_version.restype = i32

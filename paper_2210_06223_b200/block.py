@@ -109,6 +109,36 @@ def dense_block(x: torch.Tensor, wts: dict, y: torch.Tensor | None = None, ws: t
     return y
 
 
+def block_forward(x: torch.Tensor, wts: dict, wm: torch.Tensor, bm: float, s: int, schedule: int,
+                  y: torch.Tensor | None = None, ws: torch.Tensor | None = None, mask_out: bool = True):
+    """Steps 1-5 in one C-ABI call (lasnet_block_forward) under `schedule`
+    (SCHED_SEPARATE: the north-star branch; SCHED_FUSED: the paper's Table-1
+    schedule, masker fused into a static conv1).  Returns (y, mask, idx, count).
+    y=None runs in place on x."""
+    _require_cuda(x, wm)
+    lib = _lib.load()
+    n, h, w, c_in = x.shape
+    c_mid, c_out = wts["w1"].shape[0], wts["w3"].shape[0]
+    gh, gw = grid(h, w, s)
+    d = make_desc(n, h, w, c_in, c_mid, c_out, s, x.dtype)
+    wsb = lib.lasnet_block_forward_workspace_bytes(ctypes.byref(d), schedule)
+    ws = ws if ws is not None else torch.zeros(max(wsb, 1), dtype=torch.uint8, device=x.device)
+    y = x if y is None else y
+    m = torch.empty((n, gh, gw), dtype=torch.uint8, device=x.device) if mask_out else None
+    idx = torch.empty(max(n * gh * gw, 1), dtype=torch.int32, device=x.device)
+    count = torch.empty(1, dtype=torch.int32, device=x.device)
+    wt = make_weights(wts)
+    _lib.check("lasnet_block_forward", lib.lasnet_block_forward(
+        ctypes.byref(d), ctypes.byref(wt), _p(x), _p(y), _p(wm), float(bm), int(schedule), _p(m), _p(idx),
+        _p(count), _p(ws), ws.numel(), _stream()))
+    return y, m, idx, count
+
+
+def choose_schedule(n, h, w, c_in, c_mid, c_out, s, r, dtype=torch.bfloat16) -> int:
+    d = make_desc(n, h, w, c_in, c_mid, c_out, s, dtype)
+    return int(_lib.load().lasnet_choose_schedule(ctypes.byref(d), float(r)))
+
+
 def last_launch_count() -> int:
     return int(_lib.load().lasnet_last_launch_count())
 
@@ -143,7 +173,8 @@ class DynBlock:
     buffers preallocated once (mask, idx, count, workspaces), so a forward is
     exactly the kernel launches: mask -> compact -> conv1 -> conv2 -> conv3."""
 
-    def __init__(self, shape: BlockShape, wts: dict, wm: torch.Tensor, bm: float, device="cuda"):
+    def __init__(self, shape: BlockShape, wts: dict, wm: torch.Tensor, bm: float, device="cuda",
+                 schedule: int | None = None):
         self.shape = shape
         self.wts = {k: v.to(device).contiguous() for k, v in wts.items()}
         self.wm = wm.to(device).float().contiguous()
@@ -164,6 +195,13 @@ class DynBlock:
         self.cap = sh.ncells
         self.dws = torch.empty(max(lib.lasnet_dyn_workspace_bytes(ctypes.byref(self.desc), self.cap), 1),
                                dtype=torch.uint8, device=device)
+        # schedule: None = the north-star step-by-step calls (mask_compact + dyn_block);
+        # SCHED_SEPARATE / SCHED_FUSED = one lasnet_block_forward call
+        self.schedule = schedule
+        self.fws = None
+        if schedule is not None:
+            self.fws = torch.zeros(max(lib.lasnet_block_forward_workspace_bytes(ctypes.byref(self.desc), schedule), 1),
+                                   dtype=torch.uint8, device=device)
         dd = make_desc(sh.n, sh.h, sh.w, sh.c_in, sh.c_mid, self.c_out, 1, sh.dtype)
         self.dense_desc = dd
         self._dense_ws = None
@@ -205,9 +243,18 @@ class DynBlock:
 
     def forward(self, x: torch.Tensor, y: torch.Tensor | None = None):
         """Five steps, in place on x when y is None.  No host synchronisation.
-        Steps 1+2 run as one fused launch, steps 3-5 as three."""
-        self.mask_compact(x)
-        return self.convs(x, y)
+        schedule None: steps 1+2 as one fused launch, then lasnet_dyn_block;
+        otherwise one lasnet_block_forward call under self.schedule."""
+        if self.schedule is None:
+            self.mask_compact(x)
+            return self.convs(x, y)
+        lib = _lib.load()
+        y = x if y is None else y
+        _lib.check("lasnet_block_forward", lib.lasnet_block_forward(
+            ctypes.byref(self.desc), ctypes.byref(self.wt), _p(x), _p(y), _p(self.wm), self.bm, self.schedule,
+            _p(self.mask_buf), _p(self.idx), _p(self.count), _p(self.fws), self.fws.numel(), _stream()))
+        self.launches += lib.lasnet_last_launch_count()
+        return y
 
     __call__ = forward
 

@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "liblasnet.so")
-SOURCES = ["lasnet_capi.cu", "mask_compact.cu", "conv_tc.cu", "conv23_tc.cu", "conv_simt.cu"]
+SOURCES = ["lasnet_capi.cu", "mask_compact.cu", "conv_tc.cu", "conv23_tc.cu", "conv_simt.cu", "decide_gather.cu"]
 HEADERS = ["rowmap.cuh", "sm100_ptx.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

@@ -19,6 +19,10 @@
 //   warps 6-9  (conv1 dyn only) cp.async gather of the halo rows of x: small
 //              scattered rows are where TMA's per-box cost dominates, 16-B
 //              LDGSTS keep the HBM pipe full
+//   warps 6-9  (conv1 dense + masker, the paper's masker-conv1 fusion P:153-160)
+//              read each A stage of x from smem (thread = pixel row) and
+//              accumulate the fp32 masker partial sum_c wm_c x[p,c] and its
+//              magnitude sum_c |wm_c x[p,c]| (error bound of the decision)
 //   warp 5     TMEM allocator + single-thread tcgen05.mma issuer
 // Pipelines: ST smem stages (full/empty mbarriers), two TMEM accumulators
 // (tmem_full/tmem_empty) and two staging buffers, so loads, MMAs, epilogue math
@@ -68,10 +72,13 @@ constexpr int kChunkBytes = kBM * 128;  // one 64-column bf16 chunk of a 128-row
 template <int MODE, int BN> struct Cfg {
     static constexpr bool kResid = MODE == CONV3_DYN || MODE == CONV3_DENSE;
     static constexpr bool kGather = MODE == CONV1_DYN;
+    static constexpr bool kMasker = MODE == CONV1_DENSE_MASK;
     static constexpr int kEpiWarps = kResid ? 8 : 4;
     static constexpr int kProdWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1, kGatherWarp0 = kEpiWarps + 2;
     static constexpr int kGatherThreads = 256;
-    static constexpr int kThreads = 32 * (kEpiWarps + 2) + (kGather ? kGatherThreads : 0);
+    static constexpr int kMaskerWarp0 = kEpiWarps + 2, kMaskerThreads = 128;
+    static constexpr int kThreads =
+        32 * (kEpiWarps + 2) + (kGather ? kGatherThreads : 0) + (kMasker ? kMaskerThreads : 0);
     static constexpr int kBBytes = BN * kBK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kStagingBytes = (BN / 64) * kChunkBytes;
@@ -83,7 +90,8 @@ template <int MODE, int BN> struct Cfg {
     static constexpr int kStagingOff = kStages * kStageBytes;
     static constexpr int kBarOff = kStagingOff + kStaging * kStagingBytes;
     static constexpr int kBiasOff = kBarOff + 256;
-    static constexpr int smem_bytes(int n) { return 1024 + kBiasOff + n * 4; }
+    // bias [n] then (masker) wm [k]
+    static constexpr int smem_bytes(int n, int k) { return 1024 + kBiasOff + n * 4 + (kMasker ? k * 4 : 0); }
 };
 
 template <int MODE, int BN> __host__ __device__ constexpr int threads_of() { return Cfg<MODE, BN>::kThreads; }
@@ -145,11 +153,14 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
     const int warp = tid >> 5, lane = tid & 31;
 
     for (int i = tid; i < args.N; i += C::kThreads) bias_s[i] = args.bias[i];
+    float *wm_s = bias_s + args.N;  // masker weight (CONV1_DENSE_MASK); N % 64 == 0 keeps it 16-B aligned
+    if (C::kMasker)
+        for (int i = tid; i < args.K; i += C::kThreads) wm_s[i] = args.wm[i];
     if (tid == 0) {
         for (int s = 0; s < ST; ++s) {
             // TMA producer's arrive.expect_tx (+ one noinc arrival per gather thread for conv1 dyn)
             mbar_init(bar_full + 8 * s, C::kGather ? C::kGatherThreads + 1 : 1);
-            mbar_init(bar_empty + 8 * s, 1);  // tcgen05.commit
+            mbar_init(bar_empty + 8 * s, C::kMasker ? 1 + C::kMaskerThreads / 32 : 1);  // tcgen05.commit (+ masker warps)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(bar_tfull + 8 * a, 1);     // tcgen05.commit
@@ -274,6 +285,52 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             }
 #pragma unroll
             for (int i = 0; i < RPT; ++i) src[i] = src_next[i];
+        }
+    } else if (C::kMasker && warp >= C::kMaskerWarp0) {
+        // -------------------------------------- masker partials (fused) --
+        // thread = A row = pixel; reads the 8 16-B chunks of its 128-B swizzled
+        // row of every K-block (conflict-free: 8 consecutive rows cover all 32
+        // banks) while the MMA consumes the same stage.  Per 16-B chunk (8
+        // channels) an fp32 FFMA chain, added to an fp64 accumulator: the partial
+        // sum_c wm_c x[p,c] is within gamma_8 (fp32) of exact per chunk, and
+        // sum_c |wm_c x| (fp32) bounds it.  Fixed channel order; the certified
+        // decision happens in decide_gather.cu.
+        const int r = tid - 32 * C::kMaskerWarp0;
+        int it = 0;
+        for (int tile = blockIdx.x; tile < geo.num_tiles; tile += gridDim.x) {
+            double acc = 0.0;
+            float mag = 0.f;
+            for (int kb = 0; kb < num_kb; ++kb, ++it) {
+                const int stage = it % ST;
+                mbar_wait(bar_full + 8 * stage, (it / ST) & 1);
+                const uint32_t row = sbase + stage * C::kStageBytes + r * 128;
+                uint32_t q[8][4];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(q[j][0]), "=r"(q[j][1]), "=r"(q[j][2]), "=r"(q[j][3])
+                                 : "r"(row + ((j ^ (r & 7)) << 4)));
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar_empty + 8 * stage);  // this warp's reads are done
+                const float4 *w4 = reinterpret_cast<const float4 *>(wm_s + kb * kBK);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float4 wa = w4[2 * j], wb = w4[2 * j + 1];
+                    const float wv[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+                    float cs = 0.f;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float lo = bf16lo(q[j][e]), hi = bf16hi(q[j][e]);
+                        cs = fmaf(wv[2 * e], lo, cs);
+                        cs = fmaf(wv[2 * e + 1], hi, cs);
+                        mag = fmaf(fabsf(wv[2 * e]), fabsf(lo), mag);
+                        mag = fmaf(fabsf(wv[2 * e + 1]), fabsf(hi), mag);
+                    }
+                    acc += (double)cs;
+                }
+            }
+            const int m = (tile / geo.n_tiles_n) * kBM + r;
+            if (tile % geo.n_tiles_n == 0 && m < args.m_dense) args.mpart[m] = make_double2(acc, (double)mag);
         }
     } else if (warp == C::kMmaWarp) {
         // ---------------------------------------------------- MMA issuer --
@@ -463,7 +520,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     dense2_tile(args, mt, d2n, d2y);
                     for (int c = 0; c < BN / 64; ++c)
                         tma_store_4d(&args.tmap_out, sbuf + c * kChunkBytes, n0 + c * 64, 0, d2y, d2n);
-                } else if (MODE == CONV1_DYN || MODE == CONV1_DENSE) {  // h1: [c_mid/64][rows][64]
+                } else if (MODE == CONV1_DYN || MODE == CONV1_DENSE || MODE == CONV1_DENSE_MASK) {  // h1: [c_mid/64][rows][64]
                     for (int c = 0; c < BN / 64; ++c)
                         tma_store_3d(&args.tmap_out, sbuf + c * kChunkBytes, 0, mt * kBM, (n0 >> 6) + c);
                 } else {
@@ -498,7 +555,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
 template <int MODE, int BN>
 static cudaError_t launch_mode_bn(const ConvArgs &a, int max_tiles_m, int num_sms, cudaStream_t st) {
     auto kern = conv_tc_kernel<MODE, BN>;
-    const int smem = Cfg<MODE, BN>::smem_bytes(a.N);
+    const int smem = Cfg<MODE, BN>::smem_bytes(a.N, a.K);
     static int configured = 0;  // per instantiation: largest dynamic smem enabled so far
     if (smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -527,6 +584,7 @@ cudaError_t launch_conv_tc(int mode, const ConvArgs &a, int max_tiles_m, int num
         case CONV2_DYN: return launch_mode<CONV2_DYN>(a, max_tiles_m, num_sms, st);
         case CONV3_DYN: return launch_mode<CONV3_DYN>(a, max_tiles_m, num_sms, st);
         case CONV1_DENSE: return launch_mode<CONV1_DENSE>(a, max_tiles_m, num_sms, st);
+        case CONV1_DENSE_MASK: return launch_mode<CONV1_DENSE_MASK>(a, max_tiles_m, num_sms, st);
         case CONV2_DENSE: return launch_mode<CONV2_DENSE>(a, max_tiles_m, num_sms, st);
         case CONV3_DENSE: return launch_mode<CONV3_DENSE>(a, max_tiles_m, num_sms, st);
         default: return cudaErrorInvalidValue;

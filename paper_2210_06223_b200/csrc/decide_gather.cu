@@ -1,0 +1,313 @@
+// decide_gather.cu -- steps 1 (decision) and 2 of the masker-fused schedule,
+// plus the h1 halo gather that feeds the fused conv2+conv3 kernel.
+//
+// The paper's best schedule (Table 1; sec. 3.4; App. B
+// P:556-565) fuses the masker into a STATIC conv1: conv1 runs on every pixel and
+// the masker's pooled 1x1 conv rides along.  Here the dense conv1 kernel
+// (conv_tc.cu, CONV1_DENSE_MASK) leaves per pixel p the partial
+//   a_p = sum_c wm_c x[p,c]   (fp32 FFMA chains of 8 channels summed in fp64) and
+//   m_p = sum_c |wm_c x[p,c]| (its magnitude, fp32),
+// and two launches finish steps 1-2 and the gather:
+//   (a) decides each cell (P:109 avg-pool + 1x1 conv, P:562 sign form):
+//       z = sum_{p in Omega} a_p + bm*|Omega| in fp64.  With gamma_n = n u/(1-n u)
+//       (Higham): each 8-channel fp32 chain is within gamma_8(2^-24) of its exact
+//       value and the fp64 additions (c_in/8 + |Omega| + 4 on any path) within
+//       gamma_n(2^-53), so |z - z_exact| <= (gamma_8^32 + gamma_n^64) sum m_p.
+//       When |z| exceeds that bound the sign is the exact sign; otherwise (~1e-5
+//       of the cells) the cell is re-summed from x in fp64 (exact products) --
+//       the rule of the standalone masker (R20).
+//       decide_kernel, one thread per cell: writes the mask and the active count of
+//       every 32-cell group; the last CTA to finish (done counter) turns the
+//       group counts into exclusive prefixes and writes the total count.
+//   (b) compact_gather_kernel, one warp per (group, 64-channel chunk, halo row):
+//       the group's active cells get positions prefix + ballot rank (ascending
+//       cell ids, App. B: idx/count), and the warp copies that halo row
+//       of h1 of each of them from the dense h1 [c_mid/64][n][h][w][64] into the
+//       patch-major gathered layout [c_mid/64][cap][S+2][S+2][64] that conv23's
+//       im2col TMA box reads; pixels outside the image are 0 (R6: conv2's zero
+//       padding).  Thousands of independent warps keep the copy bandwidth-bound.
+// The done counter is zero on entry and reset by the last CTA (no memset).
+#include <cstdint>
+#include <cstdlib>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace lasnet {
+
+struct DecideArgs {
+    const double2 *mpart;       // [n*h*w] (a_p, m_p)
+    const __nv_bfloat16 *x;     // [n][h][w][c_in] (exact fallback)
+    const float *wm;            // [c_in]
+    float bm;
+    int n_img, H, W, c_in, S, Gh, Gw;
+    int ncells, ngroups;        // cells, 32-cell groups
+    uint8_t *dec;               // [ncells] decisions (caller's mask or workspace)
+    int32_t *gpre;              // [ngroups] group counts -> exclusive prefixes
+    int32_t *count;
+    unsigned *done;             // CTAs finished (zero on entry, reset by the last)
+};
+
+constexpr int kDecThreads = 256;
+
+__device__ __forceinline__ unsigned atom_add_acqrel(unsigned *p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
+// exact fp64 sum_{p in Omega} sum_c wm_c x[p,c] of one cell by one warp (bf16 x
+// fp32 products are exact in fp64; lanes own 16-B channel vectors, fixed order)
+__device__ double cell_exact(const DecideArgs &a, int n, int y0, int x0, int ch, int cw, int lane) {
+    double s = 0.0;
+    const int nvec = a.c_in / 8;  // 16-B vectors per pixel
+    for (int py = 0; py < ch; ++py)
+        for (int px = 0; px < cw; ++px) {
+            const uint4 *row = reinterpret_cast<const uint4 *>(a.x + ((size_t)((n * a.H + y0 + py) * a.W) + x0 + px) * a.c_in);
+            for (int v = lane; v < nvec; v += 32) {
+                const uint4 q = __ldg(row + v);
+                const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const uint32_t b = (e & 1) ? (qq[e >> 1] >> 16) : (qq[e >> 1] & 0xFFFFu);
+                    s = fma((double)a.wm[8 * v + e], (double)__uint_as_float(b << 16), s);
+                }
+            }
+        }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    return s;
+}
+
+__global__ void __launch_bounds__(kDecThreads) decide_kernel(const DecideArgs a) {
+    __shared__ int s_unc[kDecThreads], s_nunc;
+    __shared__ uint8_t s_dec[kDecThreads];
+    __shared__ int s_last;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = a.Gh * a.Gw;
+    const int cell0 = blockIdx.x * kDecThreads;
+    if (tid == 0) s_nunc = 0;
+    __syncthreads();
+
+    // certified decision per cell from the fused conv1's partials
+    const int cell = cell0 + tid;
+    const bool valid = cell < a.ncells;
+    int dec = 0;
+    if (valid) {
+        const int n = cell / G, g = cell - n * G, gy = g / a.Gw, gx = g - gy * a.Gw;
+        const int y0 = gy * a.S, x0 = gx * a.S;
+        const int ch = min(y0 + a.S, a.H) - y0, cw = min(x0 + a.S, a.W) - x0;
+        double z = 0.0, m = 0.0;
+        // all loads of a batch of 16 pixels in flight before the (fixed-order) sums
+        const double2 *base = a.mpart + (size_t)(n * a.H + y0) * a.W + x0;
+        const int npix = ch * cw;
+        int py = 0, px = 0;
+        for (int p0 = 0; p0 < npix; p0 += 16) {
+            double2 v[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                v[i] = make_double2(0.0, 0.0);
+                if (p0 + i < npix) {
+                    v[i] = __ldg(base + py * a.W + px);
+                    if (++px == cw) px = 0, ++py;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                z += v[i].x;
+                m += v[i].y;
+            }
+        }
+        const double u32 = 5.9604644775390625e-8, u64 = 1.1102230246251565e-16;  // 2^-24, 2^-53
+        const double n64 = (double)(a.c_in / 8 + ch * cw + 4);
+        const double gam = 8.0 * u32 / (1.0 - 8.0 * u32) + n64 * u64 / (1.0 - n64 * u64);
+        // m_p are fp32 sums (relative error <= c_in 2^-24 < 1e-3 for c_in < 16k): x1.01
+        const double err = m * 1.01 * gam + 1e-300;
+        z += (double)a.bm * (double)(ch * cw);
+        if (fabs(z) > err) {
+            dec = z > 0.0;
+        } else {
+            s_unc[atomicAdd(&s_nunc, 1)] = tid;
+        }
+    }
+    __syncthreads();
+    // exact re-sum of the undecided cells, one warp each (rare)
+    for (int k = warp; k < s_nunc; k += kDecThreads / 32) {
+        const int t = s_unc[k], c = cell0 + t;
+        const int n = c / G, g = c - n * G, gy = g / a.Gw, gx = g - gy * a.Gw;
+        const int y0 = gy * a.S, x0 = gx * a.S;
+        const int ch = min(y0 + a.S, a.H) - y0, cw = min(x0 + a.S, a.W) - x0;
+        const double sum = cell_exact(a, n, y0, x0, ch, cw, lane);
+        if (lane == 0) s_dec[t] = (sum / (double)(ch * cw) + (double)a.bm) > 0.0;
+    }
+    __syncthreads();
+    for (int k = 0; k < s_nunc; ++k)
+        if (s_unc[k] == tid) dec = s_dec[tid];
+    if (valid) a.dec[cell] = (uint8_t)dec;
+    const unsigned bal = __ballot_sync(0xffffffffu, dec);
+    if (lane == 0 && cell0 / 32 + warp < a.ngroups) a.gpre[cell0 / 32 + warp] = __popc(bal);
+
+    // the last CTA: exclusive prefix over the group counts, total count
+    __syncthreads();
+    if (tid == 0) s_last = atom_add_acqrel(a.done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __shared__ int s_wsum[kDecThreads / 32];
+    __shared__ int s_base;
+    if (tid == 0) s_base = 0;
+    __syncthreads();
+    for (int g0 = 0; g0 < a.ngroups; g0 += kDecThreads) {
+        const int g = g0 + tid;
+        int v = 0;
+        if (g < a.ngroups) asm volatile("ld.global.cg.b32 %0, [%1];" : "=r"(v) : "l"(a.gpre + g));
+        int incl = v;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += t;
+        }
+        if (lane == 31) s_wsum[warp] = incl;
+        __syncthreads();
+        int woff = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < kDecThreads / 32; ++w) {
+            woff += w < warp ? s_wsum[w] : 0;
+            tot += s_wsum[w];
+        }
+        if (g < a.ngroups) a.gpre[g] = s_base + woff + incl - v;
+        __syncthreads();
+        if (tid == 0) s_base += tot;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        *a.count = s_base;
+        *a.done = 0u;  // kernel completion orders this before the next launch
+    }
+}
+
+struct GatherArgs {
+    const uint8_t *dec;         // [ncells]
+    const int32_t *gpre;        // [ngroups] exclusive prefixes
+    int32_t *idx;
+    const __nv_bfloat16 *h1d;   // dense h1 [c_mid/64][n][h][w][64]
+    __nv_bfloat16 *h1g;         // gathered h1 [c_mid/64][cap][S+2][S+2][64]
+    int n_img, H, W, S, Gh, Gw, ncells, ngroups, nch, cap;
+};
+
+// One warp per task (32-cell group g, 64-channel chunk cc, halo row hr).  Lane
+// k first decodes the k-th active cell of the group into source/destination
+// row bases (no division in the copy loop); then lane l copies 16-B vector
+// w = l + 32 i (pixel w/8, part w%8) of that halo row for every active cell,
+// 8 loads in flight before the stores.
+__global__ void __launch_bounds__(256) compact_gather_kernel(const GatherArgs a) {
+    __shared__ long s_src[8][32], s_dst[8][32];
+    __shared__ int s_x0[8][32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int hs = a.S + 2;
+    const long task = (long)blockIdx.x * 8 + wib;
+    const long ntask = (long)a.ngroups * a.nch * hs;
+    if (task >= ntask) return;
+    const int g = (int)(task / (a.nch * hs));
+    const int rem = (int)(task - (long)g * a.nch * hs);
+    const int cc = rem / hs, hr = rem - cc * hs;
+    const int cell = g * 32 + lane;
+    const int d = cell < a.ncells ? a.dec[cell] : 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, d);
+    if (bal == 0u) return;
+    const int rank = __popc(bal & ((1u << lane) - 1u));
+    if (d) {
+        const int pos = a.gpre[g] + rank;
+        if (cc == 0 && hr == 0) a.idx[pos] = cell;
+        const int G = a.Gh * a.Gw;
+        const int n = cell / G, gg = cell - n * G, gy = gg / a.Gw, gx = gg - gy * a.Gw;
+        const int hy = gy * a.S - 1 + hr;
+        const long pix_all = (long)a.n_img * a.H * a.W;
+        // source: vector index of pixel (hy, gx*S) in chunk cc (halo pixel px is px - 1
+        // from it); a row outside the image gets an x origin no pixel can pass
+        const bool row_ok = hy >= 0 && hy < a.H;
+        s_src[wib][rank] = (cc * pix_all + ((long)n * a.H + (row_ok ? hy : 0)) * a.W + gx * a.S) * 8;
+        s_dst[wib][rank] = (((long)cc * a.cap + pos) * hs * hs + hr * hs) * 8;
+        s_x0[wib][rank] = row_ok ? gx * a.S - 1 : -(1 << 30);
+    }
+    __syncwarp();
+    const int nact = __popc(bal);
+    const int per = hs * 8;  // vectors of one halo row of one cell
+    const uint4 *src = reinterpret_cast<const uint4 *>(a.h1d);
+    uint4 *dst = reinterpret_cast<uint4 *>(a.h1g);
+    for (int w = lane; w < per; w += 32) {
+        const int px = w >> 3;
+        constexpr int kU = 8;
+        for (int k0 = 0; k0 < nact; k0 += kU) {
+            uint4 val[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                val[u] = make_uint4(0u, 0u, 0u, 0u);
+                const int k = k0 + u;
+                if (k < nact) {
+                    const int hx = s_x0[wib][k] + px;
+                    if (hx >= 0 && hx < a.W) val[u] = __ldg(src + s_src[wib][k] + w - 8);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u)
+                if (k0 + u < nact) dst[s_dst[wib][k0 + u] + w] = val[u];
+        }
+    }
+}
+
+size_t decide_sync_bytes(int ncells, int) {
+    // done counter (16 B) + decisions (ncells) + group prefixes (ngroups ints)
+    const long ngroups = ((long)ncells + 31) / 32;
+    return 16 + ((size_t)ncells + 15) / 16 * 16 + (size_t)ngroups * 4;
+}
+
+// sync: decide_sync_bytes() bytes whose first 16 are zero (left zero)
+cudaError_t launch_decide_gather(const double2 *mpart, const void *x, const float *wm, float bm, int n_img, int H,
+                                 int W, int c_in, int S, uint8_t *mask, int32_t *idx, int32_t *count, void *sync,
+                                 const void *h1d, void *h1g, int c_mid, int cap, int num_sms, cudaStream_t st) {
+    (void)num_sms;
+    DecideArgs a;
+    a.mpart = mpart;
+    a.x = static_cast<const __nv_bfloat16 *>(x);
+    a.wm = wm;
+    a.bm = bm;
+    a.n_img = n_img;
+    a.H = H;
+    a.W = W;
+    a.c_in = c_in;
+    a.S = S;
+    a.Gh = (H + S - 1) / S;
+    a.Gw = (W + S - 1) / S;
+    a.ncells = n_img * a.Gh * a.Gw;
+    if (a.ncells == 0) return cudaMemsetAsync(count, 0, sizeof(int32_t), st);
+    a.ngroups = (a.ncells + 31) / 32;
+    uint8_t *base = static_cast<uint8_t *>(sync);
+    a.done = reinterpret_cast<unsigned *>(base);
+    uint8_t *decs = base + 16;
+    a.dec = mask ? mask : decs;
+    a.gpre = reinterpret_cast<int32_t *>(decs + ((size_t)a.ncells + 15) / 16 * 16);
+    a.count = count;
+    decide_kernel<<<(a.ncells + kDecThreads - 1) / kDecThreads, kDecThreads, 0, st>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || h1d == nullptr) return e;
+    GatherArgs g;
+    g.dec = a.dec;
+    g.gpre = a.gpre;
+    g.idx = idx;
+    g.h1d = static_cast<const __nv_bfloat16 *>(h1d);
+    g.h1g = static_cast<__nv_bfloat16 *>(h1g);
+    g.n_img = n_img;
+    g.H = H;
+    g.W = W;
+    g.S = S;
+    g.Gh = a.Gh;
+    g.Gw = a.Gw;
+    g.ncells = a.ncells;
+    g.ngroups = a.ngroups;
+    g.nch = c_mid / 64;
+    g.cap = cap;
+    const long ntask = (long)a.ngroups * g.nch * (S + 2);
+    compact_gather_kernel<<<(unsigned)((ntask + 7) / 8), 256, 0, st>>>(g);
+    return cudaGetLastError();
+}
+
+}  // namespace lasnet

@@ -26,6 +26,10 @@ cudaError_t launch_mask_compact(int dtype_bf16, const void *x, const float *wm, 
 cudaError_t launch_conv_tc(int mode, const ConvArgs &a, int max_tiles_m, int num_sms, cudaStream_t st);
 cudaError_t launch_conv_simt(int mode, const ConvArgs &a, int max_rows, cudaStream_t st);
 cudaError_t launch_conv23(bool dense, const ConvArgs &a, int max_tiles, int num_sms, cudaStream_t st);
+size_t decide_sync_bytes(int ncells, int num_sms);
+cudaError_t launch_decide_gather(const double2 *mpart, const void *x, const float *wm, float bm, int n_img, int H,
+                                 int W, int c_in, int S, uint8_t *mask, int32_t *idx, int32_t *count, void *sync,
+                                 const void *h1d, void *h1g, int c_mid, int cap, int num_sms, cudaStream_t st);
 }  // namespace lasnet
 
 using namespace lasnet;
@@ -222,7 +226,8 @@ int prepare_tc(int mode, ConvArgs &a, const lasnet_block_desc *d, const void *x,
             ok = ok && tmap2(&a.tmap_a, h2, C, (uint64_t)cap * S * S, 64, 128);
             return ok ? (int)(((long)cap * S * S + 127) / 128) : -1;
         }
-        case CONV1_DENSE: {
+        case CONV1_DENSE:
+        case CONV1_DENSE_MASK: {
             ok = ok && tmap2(&a.tmap_a, x, d->c_in, px, 64, 128);
             ok = ok && tmap3(&a.tmap_out, h1, 64, px, C / 64, 64, 128, 1);
             return ok ? (int)((px + 127) / 128) : -1;
@@ -309,6 +314,26 @@ cudaError_t run_conv(const lasnet_block_desc *d, int mode, ConvArgs &a, int max_
     return launch_conv_simt(mode, a, max_rows, st);
 }
 
+// Steps 4+5 on the gathered h1 [c_mid/64][cap][S+2][S+2][64]: one fused kernel
+// (h2 stays in shared memory) or conv2 -> h2 -> conv3 + scatter-add.  When y == x
+// every read of x's pixel by step 5 precedes its write (same thread).
+cudaError_t run_steps45(const lasnet_block_desc *d, const lasnet_block_weights *w, ConvArgs a, const void *x,
+                        void *y, const void *h1, void *h2, int cap, cudaStream_t st, int *launches) {
+    const int ss = d->s * d->s;
+    if (use_fused23(d)) {
+        *launches = 1;
+        return run_conv23(d, false, a, w, x, y, h1, cap, st);
+    }
+    a.a_src = h1; a.w = w->w2; a.bias = w->b2; a.out = h2;
+    a.K = 9 * d->c_mid; a.N = d->c_mid; a.a_ld = d->c_mid; a.out_ld = d->c_mid;
+    cudaError_t e = run_conv(d, CONV2_DYN, a, cap * ss, x, y, h1, h2, cap, st);
+    if (e != cudaSuccess) return e;
+    a.a_src = h2; a.w = w->w3; a.bias = w->b3; a.out = y; a.resid = x;
+    a.K = d->c_mid; a.N = d->c_out; a.a_ld = d->c_mid; a.out_ld = d->c_out;
+    *launches = 2;
+    return run_conv(d, CONV3_DYN, a, cap * ss, x, y, h1, h2, cap, st);
+}
+
 ConvArgs base_args(const lasnet_block_desc *d) {
     ConvArgs a;
     std::memset(&a, 0, sizeof(a));
@@ -325,6 +350,30 @@ ConvArgs base_args(const lasnet_block_desc *d) {
     a.fd_S = FastDiv((uint32_t)d->s);
     a.fd_SS = FastDiv((uint32_t)(d->s * d->s));
     return a;
+}
+
+// Workspace of lasnet_block_forward: zero-contract control words first, then
+// scratch.  Returns the byte size; with base != NULL also the region pointers.
+struct FwdWs {
+    void *sync, *mpart, *h1d, *h1g, *h2, *sep_dyn;
+};
+size_t fwd_ws(const lasnet_block_desc *d, int schedule, uint8_t *base, FwdWs *o) {
+    const long ncells = (long)d->n * ((d->h + d->s - 1) / d->s) * ((d->w + d->s - 1) / d->s);
+    const size_t e = elt_size(d->dtype), px = (size_t)d->n * d->h * d->w;
+    Carve cv{base};
+    FwdWs r{};
+    if (schedule == LASNET_SCHED_MASKER_FUSED) {
+        r.sync = cv.take(decide_sync_bytes((int)ncells, num_sms()));
+        r.mpart = cv.take(px * 16);
+        r.h1d = cv.take(px * d->c_mid * e);
+        r.h1g = cv.take((size_t)ncells * (d->s + 2) * (d->s + 2) * d->c_mid * e);
+        r.h2 = use_fused23(d) ? nullptr : cv.take((size_t)ncells * d->s * d->s * d->c_mid * e);
+    } else {
+        r.sync = cv.take(mask_compact_workspace_bytes(ncells));
+        r.sep_dyn = cv.take(dyn_ws_bytes(d, (int32_t)ncells));
+    }
+    if (o) *o = r;
+    return cv.used;
 }
 
 }  // namespace
@@ -465,21 +514,9 @@ lasnet_status lasnet_dyn_block(const lasnet_block_desc *d, const lasnet_block_we
     a.a_src = x; a.w = w->w1; a.bias = w->b1; a.out = h1; a.resid = nullptr;
     a.K = d->c_in; a.N = d->c_mid; a.a_ld = d->c_in; a.out_ld = d->c_mid;
     if (run_conv(d, CONV1_DYN, a, cap * hs2, x, y, h1, h2, cap, st) != cudaSuccess) return LASNET_ERR_CUDA;
-    if (use_fused23(d)) {  // steps 4+5 in one kernel: h2 never leaves shared memory
-        if (run_conv23(d, false, a, w, x, y, h1, cap, st) != cudaSuccess) return LASNET_ERR_CUDA;
-        g_last_launches = 2;
-        return LASNET_OK;
-    }
-    // step 4: 3x3 conv on the gathered patch batch
-    a.a_src = h1; a.w = w->w2; a.bias = w->b2; a.out = h2;
-    a.K = 9 * d->c_mid; a.N = d->c_mid; a.a_ld = d->c_mid; a.out_ld = d->c_mid;
-    if (run_conv(d, CONV2_DYN, a, cap * ss, x, y, h1, h2, cap, st) != cudaSuccess) return LASNET_ERR_CUDA;
-    // step 5: conv3 + residual add + scatter into y (reads the residual from x;
-    // when y == x every read of x by steps 3/5 precedes the write of its pixel)
-    a.a_src = h2; a.w = w->w3; a.bias = w->b3; a.out = y; a.resid = x;
-    a.K = d->c_mid; a.N = d->c_out; a.a_ld = d->c_mid; a.out_ld = d->c_out;
-    if (run_conv(d, CONV3_DYN, a, cap * ss, x, y, h1, h2, cap, st) != cudaSuccess) return LASNET_ERR_CUDA;
-    g_last_launches = 3;
+    int k = 0;
+    if (run_steps45(d, w, a, x, y, h1, h2, cap, st, &k) != cudaSuccess) return LASNET_ERR_CUDA;
+    g_last_launches = 1 + k;
     return LASNET_OK;
 }
 
@@ -523,6 +560,96 @@ lasnet_status lasnet_dense_block(const lasnet_block_desc *d, const lasnet_block_
     if (run_conv(d, CONV3_DENSE, a, px, x, y, h1, h2, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
     g_last_launches = 3;
     return LASNET_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+size_t lasnet_block_forward_workspace_bytes(const lasnet_block_desc *d, int32_t schedule) {
+    if (check_desc(d) != LASNET_OK) return 0;
+    if (schedule != LASNET_SCHED_MASKER_SEPARATE && schedule != LASNET_SCHED_MASKER_FUSED) return 0;
+    return fwd_ws(d, schedule, nullptr, nullptr);
+}
+
+lasnet_status lasnet_block_forward(const lasnet_block_desc *d, const lasnet_block_weights *w, const void *x, void *y,
+                                   const float *wm, float bm, int32_t schedule, uint8_t *mask, int32_t *idx,
+                                   int32_t *count, void *ws, size_t ws_bytes, lasnet_stream_t stream) {
+    lasnet_status s = check_desc(d);
+    if (s != LASNET_OK) return s;
+    if (schedule != LASNET_SCHED_MASKER_SEPARATE && schedule != LASNET_SCHED_MASKER_FUSED) return LASNET_ERR_DOMAIN;
+    if ((s = check_weights(w)) != LASNET_OK) return s;
+    if (!x || !y || !wm || !idx || !count) return LASNET_ERR_NULL;
+    if ((s = check_channels(d)) != LASNET_OK) return s;
+    const int vec = d->dtype == LASNET_BF16 ? 8 : 4;
+    if (!masker_channels_ok(d->c_in, vec)) return LASNET_ERR_UNSUPPORTED;
+    if (schedule == LASNET_SCHED_MASKER_FUSED && d->dtype != LASNET_BF16) return LASNET_ERR_UNSUPPORTED;
+    if (misaligned(x) || misaligned(y)) return LASNET_ERR_UNSUPPORTED;
+    const size_t e = elt_size(d->dtype);
+    const size_t xbytes = (size_t)d->n * d->h * d->w * d->c_in * e;
+    if ((s = check_alias(x, y, xbytes)) != LASNET_OK) return s;
+    const size_t need = fwd_ws(d, schedule, nullptr, nullptr);
+    if (!ws || ws_bytes < need) return LASNET_ERR_WORKSPACE;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    g_last_launches = 0;
+    const int ncells = d->n * ((d->h + d->s - 1) / d->s) * ((d->w + d->s - 1) / d->s);
+    if (d->n == 0) return cudaMemsetAsync(count, 0, sizeof(int32_t), st) == cudaSuccess ? LASNET_OK : LASNET_ERR_CUDA;
+    FwdWs r;
+    fwd_ws(d, schedule, static_cast<uint8_t *>(ws), &r);
+
+    if (schedule == LASNET_SCHED_MASKER_SEPARATE) {
+        // north-star branch: masker+compaction (one launch), then gather+conv1 on the halos, conv2, conv3
+        {
+            KernelEvents ev(st);
+            if (launch_mask_compact(d->dtype == LASNET_BF16, x, wm, bm, d->n, d->h, d->w, d->c_in, d->s, mask, nullptr,
+                                    idx, count, r.sync, st) != cudaSuccess)
+                return LASNET_ERR_CUDA;
+        }
+        s = lasnet_dyn_block(d, w, x, y, idx, count, ncells, r.sep_dyn, dyn_ws_bytes(d, ncells), stream);
+        if (s != LASNET_OK) return s;
+        g_last_launches += 1;
+        return LASNET_OK;
+    }
+
+    // the paper's Table-1 schedule: masker fused into a static conv1
+    if (x != y && cudaMemcpyAsync(y, x, xbytes, cudaMemcpyDeviceToDevice, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    const int px = d->n * d->h * d->w;
+    ConvArgs a = base_args(d);
+    a.m_dense = px;
+    a.a_src = x; a.w = w->w1; a.bias = w->b1; a.out = r.h1d;
+    a.K = d->c_in; a.N = d->c_mid; a.a_ld = d->c_in; a.out_ld = d->c_mid;
+    a.wm = wm; a.mpart = static_cast<double2 *>(r.mpart);
+    if (run_conv(d, CONV1_DENSE_MASK, a, px, x, y, r.h1d, nullptr, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    {
+        KernelEvents ev(st);
+        if (launch_decide_gather(static_cast<const double2 *>(r.mpart), x, wm, bm, d->n, d->h, d->w, d->c_in, d->s,
+                                 mask, idx, count, r.sync, r.h1d, r.h1g, d->c_mid, ncells, num_sms(), st) !=
+            cudaSuccess)
+            return LASNET_ERR_CUDA;
+    }
+    ConvArgs b = base_args(d);
+    b.idx = idx;
+    b.count = count;
+    int k = 0;
+    if (run_steps45(d, w, b, x, y, r.h1g, r.h2, ncells, st, &k) != cudaSuccess) return LASNET_ERR_CUDA;
+    g_last_launches = 3 + k;  // conv1+masker, decide, compact+gather, steps 4-5
+    return LASNET_OK;
+}
+
+/* Roofline model of the two schedules on this GPU (the paper's latency
+ * predictor role, P:113-121 / P:158-160 r_th, retargeted to B200): bytes that
+ * must cross HBM at activation rate r.  Separate: masker read of x + halo
+ * gather of x for conv1 + residual/y; fused: x once + h1 write + gathered-h1
+ * read + residual/y.  Tensor time is below the HBM time at every shape the
+ * bf16 path supports, so bytes decide. */
+int32_t lasnet_choose_schedule(const lasnet_block_desc *d, double r) {
+    if (check_desc(d) != LASNET_OK || d->dtype != LASNET_BF16) return LASNET_SCHED_MASKER_SEPARATE;
+    const double S = d->s, hs2 = (S + 2) * (S + 2), px = (double)d->n * d->h * d->w;
+    const double xb = px * d->c_in * 2.0, h1b = px * d->c_mid * 2.0;
+    const double halo = hs2 / (S * S);
+    const double sep = xb + r * halo * xb;
+    const double fused = xb + h1b + r * halo * h1b * 2.0;
+    return fused < sep ? LASNET_SCHED_MASKER_FUSED : LASNET_SCHED_MASKER_SEPARATE;
 }
 
 }  // extern "C"

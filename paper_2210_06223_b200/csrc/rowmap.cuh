@@ -37,6 +37,7 @@ enum ConvMode : int {
     CONV1_DENSE = 3,  // A = x pixel rows, out = h1 [n*h*w][c_mid]
     CONV2_DENSE = 4,  // A = im2col of h1 with zero padding, out = h2 [n*h*w][c_mid]
     CONV3_DENSE = 5,  // A = h2 rows, out = y (residual add, ReLU)
+    CONV1_DENSE_MASK = 6,  // CONV1_DENSE + per-pixel masker partials (the paper's masker-conv1 fusion)
 };
 
 struct ConvArgs {
@@ -70,6 +71,10 @@ struct ConvArgs {
     int32_t box_rows;         // rows one A box delivers (conv2 dyn/dense, conv3 dyn)
     int32_t rows_h, imgs_box; // conv2 dense: image rows / images per box
     int32_t dense_tiles;      // conv2 dense: M tiles
+    // masker fused into the dense conv1 (CONV1_DENSE_MASK): per pixel p the fp64
+    // partial logit sum_c wm_c x[p,c] and its magnitude sum_c |wm_c x[p,c]|
+    const float *wm;          // [c_in] reduced masker weight W_0 - W_1
+    double2 *mpart;           // [n*h*w] (partial, magnitude)
 };
 
 __host__ __device__ __forceinline__ int rows_per_patch(int mode, int S) {

@@ -205,6 +205,16 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // RNE
     return *reinterpret_cast<uint32_t *>(&v);
 }
+// bf16 bit pattern (low 16 bits of b) -> the exact double, with integer ops for
+// normal numbers (keeps the F2F conversion pipe out of hot loops); zero and
+// subnormal inputs give +-0 / the fp32 path, inf/nan through the fp32 path.
+__device__ __forceinline__ double bf16_bits_to_f64(uint32_t b) {
+    const uint32_t e = b & 0x7F80u;
+    if (__builtin_expect(e == 0u || e == 0x7F80u, 0)) return (double)__uint_as_float(b << 16);
+    // double high word: sign | (exp8 + 896) << 20 | mant7 << 13; low word 0
+    const uint32_t hi = ((b & 0x8000u) << 16) | (((b & 0x7FFFu) << 13) + (896u << 20));
+    return __hiloint2double((int)hi, 0);
+}
 __device__ __forceinline__ float bf16lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
 

@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_status_strings_and_version(lib):
-    assert lib.lasnet_abi_version() == 1
+    assert lib.lasnet_abi_version() == 2
     for code, name in _lib.STATUS.items():
         assert lib.lasnet_status_str(code).decode().startswith(name)
 
@@ -109,6 +109,39 @@ def test_dense_block_validation(lib):
     assert lib.lasnet_dense_block(ctypes.byref(d), ctypes.byref(w), FAKE, ctypes.c_void_p(0x10010), FAKE,
                                   1 << 30, None) == 5
     assert lib.lasnet_dense_block(ctypes.byref(d), ctypes.byref(w), FAKE, FAKE, FAKE, 10, None) == 6
+
+
+def test_block_forward_validation(lib):
+    d = desc()
+    w = _lib.BlockWeights(0x10000, 0x10000, 0x10000, 0x10000, 0x10000, 0x10000, None, None)
+    big = 1 << 30
+    call = lambda dd, sched, x=FAKE, y=FAKE, wm=FAKE, ws=FAKE, wsb=big: lib.lasnet_block_forward(
+        ctypes.byref(dd), ctypes.byref(w), x, y, wm, 0.0, sched, None, FAKE, FAKE, ws, wsb, None)
+    for sched in (_lib.SCHED_SEPARATE, _lib.SCHED_FUSED):
+        assert call(d, sched, x=None) == 1
+        assert call(d, sched, wm=None) == 1
+        assert call(desc(s=0), sched) == 3
+        assert call(desc(c_out=128), sched) == 4
+        assert call(d, sched, y=ctypes.c_void_p(0x10000 + 4096)) == 5
+        assert call(d, sched, ws=None) == 6
+        assert call(d, sched, wsb=64) == 6
+    assert call(d, 2) == 3                                              # unknown schedule
+    assert call(desc(dtype=_lib.LASNET_F32), _lib.SCHED_FUSED) == 4    # fused masker: bf16 only
+
+
+def test_block_forward_workspace_and_schedule_choice(lib):
+    d = desc(n=128, h=28, w=28, c_in=512, c_mid=128, c_out=512, s=4)
+    px, cells = 128 * 28 * 28, 128 * 7 * 7
+    fused = lib.lasnet_block_forward_workspace_bytes(ctypes.byref(d), _lib.SCHED_FUSED)
+    # mpart + dense h1 + gathered h1 (every cell) dominate; control words are small
+    assert fused >= px * 16 + px * 128 * 2 + cells * 36 * 128 * 2
+    assert fused < px * 16 + px * 128 * 2 + cells * 36 * 128 * 2 + 64 * 1024
+    assert lib.lasnet_block_forward_workspace_bytes(ctypes.byref(d), 5) == 0
+    # bytes model (P:158-160 r_th): at r = 0.5 the fused masker moves fewer HBM bytes
+    assert lib.lasnet_choose_schedule(ctypes.byref(d), 0.5) == _lib.SCHED_FUSED
+    assert lib.lasnet_choose_schedule(ctypes.byref(d), 0.01) == _lib.SCHED_SEPARATE
+    f32 = desc(dtype=_lib.LASNET_F32)
+    assert lib.lasnet_choose_schedule(ctypes.byref(f32), 0.9) == _lib.SCHED_SEPARATE
 
 
 def test_missing_library_fails_loudly(tmp_path):

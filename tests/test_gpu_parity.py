@@ -253,3 +253,108 @@ def test_full_size_config2_sampled(s):
             assert np.array_equal(yc[i, yy, xx], xd[i, yy, xx])
     assert active > 20
     assert worst <= BF16_TOL
+
+
+# ------------------------------------------- lasnet_block_forward, both schedules --
+
+FWD_CASES = [
+    # n, h, w, c_in, c_mid, s, r
+    (2, 14, 14, 256, 64, 2, 0.5),
+    (2, 14, 14, 256, 64, 1, 0.3),
+    (3, 13, 11, 128, 128, 3, 0.5),   # clipped edge cells
+    (2, 14, 14, 256, 64, 7, 0.6),
+    (2, 10, 10, 128, 64, 4, 1.0),    # every cell active
+    (2, 10, 10, 128, 64, 4, 0.0),    # no cell active
+    (1, 7, 7, 512, 256, 1, 0.5),     # c_mid 256: unfused conv2 / conv3 kernels
+    (4, 28, 28, 512, 128, 4, 0.5),   # config-2 widths, reduced batch
+]
+
+
+@pytest.mark.parametrize("sched", [L.SCHED_SEPARATE, L.SCHED_FUSED])
+@pytest.mark.parametrize("n,h,w,c_in,c_mid,s,r", FWD_CASES)
+def test_block_forward_matches_oracle(sched, n, h, w, c_in, c_mid, s, r):
+    """Steps 1-5 in one call: mask/idx/count bit-exact, y within 2e-2, inactive
+    pixels bitwise x -- for the north-star schedule and the paper's Table-1
+    schedule (masker fused into a static conv1)."""
+    x, wts, wm = make_case(n, h, w, c_in, c_mid, s, seed=n * 31 + s)
+    xd = synth.to_f64(x)
+    _, l0 = oracle.masker(xd, synth.to_f64(wm), 0.0, s)
+    bm = margin_bias(l0, r)
+    m_or, _ = oracle.masker(xd, synth.to_f64(wm), bm, s)
+    idx_or, cnt = oracle.compact(m_or)
+    xg = x.cuda()
+    ws = None
+    for rep in range(2):  # second call: the self-resetting control words
+        y, m, idx, count = L.block_forward(xg.clone(), to_dev(wts), wm.cuda(), bm, s, sched, ws=ws)
+        assert np.array_equal(m.cpu().numpy(), m_or)
+        assert int(count.item()) == cnt
+        assert np.array_equal(idx[:cnt].cpu().numpy(), idx_or)
+    want = oracle.dyn_block_literal(xd, synth.weights_f64(wts), idx_or, s)
+    got = synth.to_f64(y.cpu())
+    up = oracle.upsample(m_or, h, w, s).astype(bool)
+    assert max_abs_rel(got[up], want[up]) <= BF16_TOL
+    assert np.array_equal(got[~up], xd[~up])
+
+
+def test_block_forward_fused_equals_separate_and_out_of_place():
+    n, h, w, c, s = 4, 28, 28, 256, 4
+    x, wts, wm = make_case(n, h, w, c, 64, s, seed=77)
+    _, l0 = oracle.masker(synth.to_f64(x), synth.to_f64(wm), 0.0, s)
+    bm = margin_bias(l0, 0.5)
+    xg, wd, wmg = x.cuda(), to_dev(wts), wm.cuda()
+    a = L.block_forward(xg.clone(), wd, wmg, bm, s, L.SCHED_SEPARATE)[0]
+    b = L.block_forward(xg.clone(), wd, wmg, bm, s, L.SCHED_FUSED)[0]
+    yo = torch.empty_like(xg)
+    c2 = L.block_forward(xg, wd, wmg, bm, s, L.SCHED_FUSED, y=yo)[0]
+    assert torch.equal(xg.cpu(), x)          # out of place leaves x untouched
+    assert torch.equal(b, c2)                # in place == out of place
+    assert max_abs_rel(synth.to_f64(a.cpu()), synth.to_f64(b.cpu())) <= 1e-2
+
+
+def test_block_forward_fused_uncertain_cells_fall_back_exactly():
+    """A masker bias placing logits right at the fp32 bound: the exact re-sum
+    path decides those cells; decisions still equal the fp64 oracle's."""
+    n, h, w, c, s = 2, 8, 8, 64, 2
+    x, wts, wm = make_case(n, h, w, c, 64, s, seed=5)
+    xd = synth.to_f64(x)
+    _, l0 = oracle.masker(xd, synth.to_f64(wm), 0.0, s)
+    # bias = -(one cell's logit) rounded to fp32: that cell sits within ~1e-8 of 0
+    bm = float(np.float32(-l0.reshape(-1)[3]))
+    m_or, l_or = oracle.masker(xd, synth.to_f64(wm), bm, s)
+    if np.abs(l_or).min() < 1e-12 * np.abs(l_or).max():
+        pytest.skip("exact tie at fp64 precision")
+    y, m, idx, count = L.block_forward(x.cuda(), to_dev(wts), wm.cuda(), bm, s, L.SCHED_FUSED)
+    assert np.array_equal(m.cpu().numpy(), m_or)
+
+
+@pytest.mark.parametrize("s", [1, 2, 4, 7])
+def test_full_size_config2_fused_sampled(s):
+    """Config 2 at full size through the paper's schedule (the bench launch)."""
+    n, h, w, c_in, c_mid = 128, 28, 28, 512, 128
+    x, wts, wm = make_case(n, h, w, c_in, c_mid, s, seed=40 + s)
+    blk = L.DynBlock(L.BlockShape(n, h, w, c_in, c_mid, s), wts, wm, 0.0, schedule=L.SCHED_FUSED)
+    xg = x.cuda()
+    blk.calibrate_bias(xg, 0.5)
+    y = xg.clone()
+    blk.forward(y)
+    torch.cuda.synchronize()
+    mc = blk.mask_buf.cpu().numpy()
+    xd = synth.to_f64(x)
+    m_or, _ = oracle.masker(xd, synth.to_f64(wm), blk.bm, s)
+    assert np.array_equal(mc, m_or)
+    idx_or, cnt = oracle.compact(m_or)
+    assert int(blk.count.item()) == cnt and np.array_equal(blk.idx[:cnt].cpu().numpy(), idx_or)
+    wd = synth.weights_f64(wts)
+    yc = synth.to_f64(y.cpu())
+    rng = np.random.default_rng(s + 100)
+    worst, active = 0.0, 0
+    for _ in range(96):
+        i, yy, xx = int(rng.integers(n)), int(rng.integers(h)), int(rng.integers(w))
+        want, act = oracle.block_pixel(xd, wd, mc, s, i, yy, xx)
+        if act:
+            active += 1
+            worst = max(worst, float(np.abs(yc[i, yy, xx] - want).max() / max(np.abs(want).max(), 1e-30)))
+        else:
+            assert np.array_equal(yc[i, yy, xx], xd[i, yy, xx])
+    assert active > 20
+    assert worst <= BF16_TOL
