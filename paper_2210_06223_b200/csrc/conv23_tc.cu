@@ -19,6 +19,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "launch.cuh"
 #include "rowmap.cuh"
 #include "sm100_ptx.cuh"
 
@@ -151,6 +152,8 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_wait();  // h1, idx and count of the previous kernels are complete from here on
+    pdl_trigger();
     // TMEM columns: acc2[2] at 0 / KC, acc3[kAcc3] at 256 + 64 k
     const uint32_t acc3_col = 256;
 
@@ -479,7 +482,7 @@ cudaError_t launch_conv23(bool dense, const ConvArgs &a, int max_tiles, int num_
             if (e != cudaSuccess) return e;
             cfg = smem;
         }
-        conv23_kernel<true><<<grid, c23::kThreads, smem, st>>>(a);
+        return launch_k(conv23_kernel<true>, dim3(grid), dim3(c23::kThreads), smem, st, a);
     } else {
         static int cfg = 0;
         if (smem > cfg) {
@@ -487,7 +490,7 @@ cudaError_t launch_conv23(bool dense, const ConvArgs &a, int max_tiles, int num_
             if (e != cudaSuccess) return e;
             cfg = smem;
         }
-        conv23_kernel<false><<<grid, c23::kThreads, smem, st>>>(a);
+        return launch_k(conv23_kernel<false>, dim3(grid), dim3(c23::kThreads), smem, st, a);
     }
     return cudaGetLastError();
 }

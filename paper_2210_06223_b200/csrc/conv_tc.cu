@@ -34,6 +34,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "launch.cuh"
 #include "rowmap.cuh"
 #include "sm100_ptx.cuh"
 
@@ -179,6 +180,8 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_wait();     // inputs of the previous kernel (x, h1, idx/count) are complete from here on
+    pdl_trigger();
 
     const TileGeo geo = tile_geo<MODE>(args, BN);
     const int num_kb = args.K / kBK;
@@ -564,8 +567,7 @@ static cudaError_t launch_mode_bn(const ConvArgs &a, int max_tiles_m, int num_sm
     }
     const long tiles = (long)max_tiles_m * (a.N / BN);
     const int grid = (int)(tiles < num_sms ? (tiles > 0 ? tiles : 1) : num_sms);
-    kern<<<grid, threads_of<MODE, BN>(), smem, st>>>(a);
-    return cudaGetLastError();
+    return launch_k(kern, dim3(grid), dim3(threads_of<MODE, BN>()), smem, st, a);
 }
 
 template <int MODE>

@@ -32,6 +32,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "launch.cuh"
+
 namespace lasnet {
 
 struct DecideArgs {
@@ -85,6 +87,8 @@ __global__ void __launch_bounds__(kDecThreads) decide_kernel(const DecideArgs a)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = a.Gh * a.Gw;
     const int cell0 = blockIdx.x * kDecThreads;
+    pdl_wait();
+    pdl_trigger();
     if (tid == 0) s_nunc = 0;
     __syncthreads();
 
@@ -203,6 +207,8 @@ __global__ void __launch_bounds__(256) compact_gather_kernel(const GatherArgs a)
     __shared__ int s_x0[8][32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int hs = a.S + 2;
+    pdl_wait();
+    pdl_trigger();
     const long task = (long)blockIdx.x * 8 + wib;
     const long ntask = (long)a.ngroups * a.nch * hs;
     if (task >= ntask) return;
@@ -286,8 +292,7 @@ cudaError_t launch_decide_gather(const double2 *mpart, const void *x, const floa
     a.dec = mask ? mask : decs;
     a.gpre = reinterpret_cast<int32_t *>(decs + ((size_t)a.ncells + 15) / 16 * 16);
     a.count = count;
-    decide_kernel<<<(a.ncells + kDecThreads - 1) / kDecThreads, kDecThreads, 0, st>>>(a);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_k(decide_kernel, dim3((a.ncells + kDecThreads - 1) / kDecThreads), dim3(kDecThreads), 0, st, a);
     if (e != cudaSuccess || h1d == nullptr) return e;
     GatherArgs g;
     g.dec = a.dec;
@@ -306,8 +311,7 @@ cudaError_t launch_decide_gather(const double2 *mpart, const void *x, const floa
     g.nch = c_mid / 64;
     g.cap = cap;
     const long ntask = (long)a.ngroups * g.nch * (S + 2);
-    compact_gather_kernel<<<(unsigned)((ntask + 7) / 8), 256, 0, st>>>(g);
-    return cudaGetLastError();
+    return launch_k(compact_gather_kernel, dim3((unsigned)((ntask + 7) / 8)), dim3(256), 0, st, g);
 }
 
 }  // namespace lasnet

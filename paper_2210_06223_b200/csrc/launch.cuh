@@ -1,0 +1,43 @@
+// launch.cuh -- every kernel of the library is launched through launch_k():
+// cudaLaunchKernelEx with Programmatic Dependent Launch (PDL) allowed, so the
+// next kernel of the block is scheduled while the previous one drains and its
+// prologue (mbarrier init, TMEM alloc, tensor-map prefetch, weight/bias
+// staging) overlaps that tail.  Every kernel calls pdl_wait() before its first
+// access to memory written by an earlier kernel (griddepcontrol.wait returns
+// once the prerequisite grid has completed and its writes are visible), and
+// pdl_trigger() once it no longer needs to delay its dependents.
+// LASNET_NO_PDL=1 launches without the attribute (A/B measurements).
+#pragma once
+#include <cstdlib>
+#include <utility>
+#include <cuda_runtime.h>
+
+namespace lasnet {
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("LASNET_NO_PDL");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+}  // namespace lasnet

@@ -18,6 +18,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "launch.cuh"
+
 namespace lasnet {
 
 // ---------------------------------------------------------------- masker ---
@@ -277,6 +279,8 @@ __global__ void __launch_bounds__(kMaskThreads, 3) masker_kernel(const T *__rest
                                                               float bm, int n_img, int H, int W, int C, int S, int Gh,
                                                               int Gw, MaskGeo mg, uint8_t *__restrict__ mask,
                                                               double *__restrict__ logits) {
+    pdl_wait();
+    pdl_trigger();
     const long ncells = (long)n_img * Gh * Gw;
     cta_decide<T, SLOTS>(x, wm, mg, bm, H, W, C, S, Gh, Gw, ncells, (long)blockIdx.x * mg.cpb, logits != nullptr,
                          mask, logits);
@@ -308,9 +312,10 @@ cudaError_t launch_masker(int dtype_bf16, const void *x, const float *wm, float 
     const MaskGeo mg = mask_geo(C, dtype_bf16 ? 8 : 4, S);
     const long grid = (ncells + mg.cpb - 1) / mg.cpb;
     const int slots = mg.nvec >= 32 ? mg.nvl : 1;
+    cudaError_t e = cudaSuccess;
 #define LASNET_MASKER(TT, SL)                                                                                  \
-    masker_kernel<TT, SL><<<(unsigned)grid, kMaskThreads, 0, st>>>(static_cast<const TT *>(x), wm, bm, n_img, H, \
-                                                                   W, C, S, Gh, Gw, mg, mask, logits)
+    e = launch_k(masker_kernel<TT, SL>, dim3((unsigned)grid), dim3(kMaskThreads), 0, st, static_cast<const TT *>(x), \
+                 wm, bm, n_img, H, W, C, S, Gh, Gw, mg, mask, logits)
     if (dtype_bf16) {
         if (slots == 1) LASNET_MASKER(__nv_bfloat16, 1);
         else if (slots == 2) LASNET_MASKER(__nv_bfloat16, 2);
@@ -323,7 +328,7 @@ cudaError_t launch_masker(int dtype_bf16, const void *x, const float *wm, float 
         else LASNET_MASKER(float, 8);
     }
 #undef LASNET_MASKER
-    return cudaGetLastError();
+    return e;
 }
 
 // ------------------------------------------------------------ compaction ---
@@ -345,6 +350,8 @@ __global__ void __launch_bounds__(kCompactThreads) compact_kernel(const uint8_t 
                                                                   unsigned long long *status) {
     __shared__ int warp_tot[kCompactThreads / 32];
     __shared__ int tile_prefix;
+    pdl_wait();
+    pdl_trigger();
     const int tile = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long base = (long)tile * kCellsPerTile + (long)tid * kCellsPerThread;
@@ -444,9 +451,8 @@ int launch_compact(const uint8_t *mask, int ncells, int32_t *idx, int32_t *count
         *err = e;
         return 0;
     }
-    compact_kernel<<<tiles, kCompactThreads, 0, st>>>(mask, ncells, idx, count,
-                                                      static_cast<unsigned long long *>(ws));
-    *err = cudaGetLastError();
+    *err = launch_k(compact_kernel, dim3(tiles), dim3(kCompactThreads), 0, st, mask, ncells, idx, count,
+                    static_cast<unsigned long long *>(ws));
     return 1;
 }
 
@@ -509,6 +515,8 @@ __global__ void __launch_bounds__(kMaskThreads, 3) masker_compact_kernel(
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const long ncells = (long)n_img * Gh * Gw;
     uint8_t *dec = mask ? mask : ws->decisions;
+    pdl_wait();
+    pdl_trigger();
     if (threadIdx.x == 0) MTRACE_MIN(0);
     cta_decide<T, SLOTS>(x, wm, mg, bm, H, W, C, S, Gh, Gw, ncells, (long)blockIdx.x * mg.cpb, logits != nullptr,
                          dec, logits);
@@ -591,10 +599,10 @@ cudaError_t launch_mask_compact(int dtype_bf16, const void *x, const float *wm, 
     const long grid = (ncells + mg.cpb - 1) / mg.cpb;
     FusedWs *w = static_cast<FusedWs *>(ws);
     const int slots = mg.nvec >= 32 ? mg.nvl : 1;
+    cudaError_t e = cudaSuccess;
 #define LASNET_FUSED(TT, SL)                                                                                      \
-    masker_compact_kernel<TT, SL><<<(unsigned)grid, kMaskThreads, 0, st>>>(static_cast<const TT *>(x), wm, bm, n_img, \
-                                                                           H, W, C, S, Gh, Gw, mg, mask, logits, idx, \
-                                                                           count, w)
+    e = launch_k(masker_compact_kernel<TT, SL>, dim3((unsigned)grid), dim3(kMaskThreads), 0, st,                      \
+                 static_cast<const TT *>(x), wm, bm, n_img, H, W, C, S, Gh, Gw, mg, mask, logits, idx, count, w)
     if (dtype_bf16) {
         if (slots == 1) LASNET_FUSED(__nv_bfloat16, 1);
         else if (slots == 2) LASNET_FUSED(__nv_bfloat16, 2);
@@ -607,7 +615,7 @@ cudaError_t launch_mask_compact(int dtype_bf16, const void *x, const float *wm, 
         else LASNET_FUSED(float, 8);
     }
 #undef LASNET_FUSED
-    return cudaGetLastError();
+    return e;
 }
 
 }  // namespace lasnet
