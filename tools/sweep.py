@@ -1,0 +1,151 @@
+#!/usr/bin/env python
+"""Block latency vs activation rate r and granularity S (BASELINE configs[1];
+north_star: "block ... latency versus activation rate and granularity S").
+
+For every S in --s and r in --r, on the bench workload shape (N=128, 28x28x512,
+c_mid=128, bf16, in place):
+  * the whole block (steps 1-5) under both schedules (masker-separate: the
+    north-star branch; masker-fused: the paper's Table-1 schedule), masker bias
+    calibrated on a separate batch to hit r (masker-driven masks);
+  * steps 3-5 alone (lasnet_dyn_block) on synthetic cell masks with exactly
+    floor(r*G+0.5) active cells per image, uniform and clustered families;
+  * the dense comparator (lasnet_dense_block: the same kernels on every pixel).
+Each point: W warm-ups, then K timed runs, L2 flushed (256 MiB read) before
+each, CUDA events on the launching stream; median and p10/p90 reported, with
+the SURVEY 8(d) headline roofline time of the same mask.
+
+  python tools/sweep.py [--s 1 2 4 7] [--r 0.1 ... 1.0] [--steps 20] [--out profiles/sweep_<tag>]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402  (algorithmic_work, peaks)
+import synth  # noqa: E402
+import paper_2210_06223_b200 as L  # noqa: E402
+from paper_2210_06223_b200 import block as B  # noqa: E402
+
+
+def timed(fn, prep, steps, warmup, stream):
+    for _ in range(warmup):
+        prep()
+        fn()
+    ev = []
+    for _ in range(steps):
+        prep()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        ev.append((a, b))
+    torch.cuda.synchronize()
+    ms = sorted(a.elapsed_time(b) for a, b in ev)
+    return {"p50": statistics.median(ms), "p10": float(np.percentile(ms, 10)), "p90": float(np.percentile(ms, 90))}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--s", type=int, nargs="+", default=[1, 2, 4, 7])
+    ap.add_argument("--r", type=float, nargs="+", default=[0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9, 1.0])
+    ap.add_argument("--n", type=int, default=128)
+    ap.add_argument("--hw", type=int, default=28)
+    ap.add_argument("--c-in", type=int, default=512)
+    ap.add_argument("--c-mid", type=int, default=128)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep"))
+    args = ap.parse_args()
+
+    from paper_2210_06223_b200 import build
+
+    build.build()
+    n, h, w, c_in, c_mid = args.n, args.hw, args.hw, args.c_in, args.c_mid
+    hbm, tfl, _, psrc = bench.peaks()
+    x = synth.make_x(n, h, w, c_in, seed=0).cuda()
+    xc = synth.make_x(n, h, w, c_in, seed=1000).cuda()
+    wts = synth.make_block_weights(c_in, c_mid, c_in, seed=1)
+    wm = synth.make_masker_weights(c_in, seed=2)
+    y = torch.empty_like(x)
+    flush = torch.ones(32 << 20, dtype=torch.int64, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def prep():
+        y.copy_(x)
+        flush.sum()
+
+    rows = []
+    dense_blk = L.DynBlock(L.BlockShape(n, h, w, c_in, c_mid, 1), wts, wm, 0.0)
+    y2 = torch.empty_like(x)
+    dense = timed(lambda: dense_blk.dense(x, y2), lambda: flush.sum(), args.steps, args.warmup, stream)
+    _, _, dwork, _ = bench.algorithmic_work(np.ones((n, h, w), np.uint8), n, h, w, c_in, c_mid, c_in, 1)
+    t_dense_roof = max(dwork["bytes"] / (hbm * 1e9), dwork["flops"] / (tfl * 1e12)) * 1e3
+    print(f"dense: {dense['p50']:.4f} ms (ideal {t_dense_roof:.4f} ms)", flush=True)
+    for s in args.s:
+        shape = L.BlockShape(n, h, w, c_in, c_mid, s)
+        blks = {"separate": L.DynBlock(shape, wts, wm, 0.0, schedule=L.SCHED_SEPARATE),
+                "fused": L.DynBlock(shape, wts, wm, 0.0, schedule=L.SCHED_FUSED)}
+        convs = L.DynBlock(shape, wts, wm, 0.0)
+        for r in args.r:
+            row = {"S": s, "r_target": r}
+            for name, blk in blks.items():
+                blk.calibrate_bias(xc, r)
+                row[name] = timed(lambda: blk.forward(y), prep, args.steps, args.warmup, stream)
+            # masker-driven mask of the timed input (same for both schedules)
+            blks["fused"].forward(y.copy_(x))
+            torch.cuda.synchronize()
+            m = blks["fused"].mask_buf.cpu().numpy()
+            kw, bw, _, st = bench.algorithmic_work(m, n, h, w, c_in, c_mid, c_in, s)
+            row["r_patch"], row["r_pixel"] = st["r_patch"], st["r_pixel"]
+            row["t_roof_ms"] = max(bw["bytes"] / (hbm * 1e9), bw["flops"] / (tfl * 1e12)) * 1e3
+            bf = st["block_fused"]
+            row["t_roof_fused_ms"] = max(bf["bytes"] / (hbm * 1e9), bf["flops"] / (tfl * 1e12)) * 1e3
+            # steps 3-5 alone on synthetic masks (uniform / clustered families)
+            for fam in ("uniform", "clustered"):
+                cm = synth.make_cell_mask(n, shape.gh, shape.gw, r, seed=2, family=fam)
+                mt = torch.from_numpy(cm).cuda()
+                B.compact(mt, convs.idx, convs.count)
+                row["convs_" + fam] = timed(lambda: convs.convs(y), prep, args.steps, args.warmup, stream)
+            row["dense"] = dense["p50"]
+            best = min(row["separate"]["p50"], row["fused"]["p50"])
+            row["speedup_vs_dense"] = dense["p50"] / best
+            row["roof_frac"] = row["t_roof_ms"] / best
+            rows.append(row)
+            print(f"S={s} r={r:.1f} (r_pix {row['r_pixel']:.3f}): separate {row['separate']['p50']:.4f} "
+                  f"fused {row['fused']['p50']:.4f} convs-uni {row['convs_uniform']['p50']:.4f} "
+                  f"convs-clu {row['convs_clustered']['p50']:.4f} dense {dense['p50']:.4f} "
+                  f"x{row['speedup_vs_dense']:.2f} roof {row['roof_frac']:.3f}", flush=True)
+    out = {"shape": dict(n=n, h=h, w=w, c_in=c_in, c_mid=c_mid), "peaks": dict(hbm_gbs=hbm, bf16_tflops=tfl, src=psrc),
+           "dense_ms": dense, "dense_ideal_ms": t_dense_roof, "rows": rows,
+           "device": torch.cuda.get_device_name(0), "steps": args.steps, "warmup": args.warmup}
+    os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
+    with open(args.out + ".json", "w") as f:
+        json.dump(out, f, indent=1)
+    with open(args.out + ".md", "w") as f:
+        f.write(f"# Block latency vs activation rate and S ({out['device']})\n\n")
+        f.write(f"Workload: N={n}, {h}x{w}x{c_in}, c_mid={c_mid}, bf16, in place, L2 flushed before every run; "
+                f"median of {args.steps} (p10-p90 in the JSON). Masker-driven rows: masker bias calibrated on a "
+                f"separate batch. convs-*: steps 3-5 only (lasnet_dyn_block) on synthetic masks. Dense comparator "
+                f"(same kernels on every pixel): {dense['p50'] * 1e3:.1f} us. T_roof: SURVEY 8(d) headline "
+                f"definition at {hbm:.0f} GB/s / {tfl:.0f} TFLOP/s ({psrc}).\n\n")
+        f.write("| S | r target | r pixel | separate (us) | fused (us) | convs uniform (us) | convs clustered (us) "
+                "| best vs dense | T_roof (us) | roofline frac |\n|---|---|---|---|---|---|---|---|---|---|\n")
+        for r in rows:
+            f.write(f"| {r['S']} | {r['r_target']:.1f} | {r['r_pixel']:.3f} | {r['separate']['p50'] * 1e3:.1f} | "
+                    f"{r['fused']['p50'] * 1e3:.1f} | {r['convs_uniform']['p50'] * 1e3:.1f} | "
+                    f"{r['convs_clustered']['p50'] * 1e3:.1f} | {r['speedup_vs_dense']:.2f}x | "
+                    f"{r['t_roof_ms'] * 1e3:.1f} | {r['roof_frac']:.3f} |\n")
+    print("wrote", args.out + ".json/.md")
+
+
+if __name__ == "__main__":
+    main()
