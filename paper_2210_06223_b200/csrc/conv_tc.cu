@@ -30,6 +30,7 @@
 // count from the device-resident active count: no host synchronisation
 // (the index list spreads work evenly over the SMs).
 #include <cstdint>
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -77,7 +78,7 @@ template <int MODE, int BN> struct Cfg {
     static constexpr int kEpiWarps = kResid ? 8 : 4;
     static constexpr int kProdWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1, kGatherWarp0 = kEpiWarps + 2;
     static constexpr int kGatherThreads = 256;
-    static constexpr int kMaskerWarp0 = kEpiWarps + 2, kMaskerThreads = 128;
+    static constexpr int kMaskerWarp0 = kEpiWarps + 2, kMaskerThreads = 256;
     static constexpr int kThreads =
         32 * (kEpiWarps + 2) + (kGather ? kGatherThreads : 0) + (kMasker ? kMaskerThreads : 0);
     static constexpr int kBBytes = BN * kBK * 2;
@@ -88,11 +89,13 @@ template <int MODE, int BN> struct Cfg {
     static constexpr int kStaging = kGather ? 1 : (kResid ? 3 : 2);
     static constexpr int kStages = kGather ? (BN == 128 ? 6 : 8) : (kResid ? 3 : (BN == 128 ? 4 : 6));
     static constexpr int kTmemCols = 2 * BN;
-    static constexpr int kStagingOff = kStages * kStageBytes;
+    static constexpr int kStageOff = 0;  // [stages][staging][barriers][bias (+wm)]
+    static constexpr int kStagingOff = kStageOff + kStages * kStageBytes;
     static constexpr int kBarOff = kStagingOff + kStaging * kStagingBytes;
     static constexpr int kBiasOff = kBarOff + 256;
     // bias [n] then (masker) wm [k]
-    static constexpr int smem_bytes(int n, int k) { return 1024 + kBiasOff + n * 4 + (kMasker ? k * 4 : 0); }
+    static constexpr bool kWmSmem = kMasker;
+    static constexpr int smem_bytes(int n, int k) { return 1024 + kBiasOff + n * 4 + (kWmSmem ? k * 4 : 0); }
 };
 
 template <int MODE, int BN> __host__ __device__ constexpr int threads_of() { return Cfg<MODE, BN>::kThreads; }
@@ -154,14 +157,15 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
     const int warp = tid >> 5, lane = tid & 31;
 
     for (int i = tid; i < args.N; i += C::kThreads) bias_s[i] = args.bias[i];
-    float *wm_s = bias_s + args.N;  // masker weight (CONV1_DENSE_MASK); N % 64 == 0 keeps it 16-B aligned
-    if (C::kMasker)
-        for (int i = tid; i < args.K; i += C::kThreads) wm_s[i] = args.wm[i];
+    // masker weight (CONV1_DENSE_MASK); N % 64 == 0 keeps it 16-B aligned
+    const float *wm_s = C::kWmSmem ? bias_s + args.N : args.wm;
+    if (C::kWmSmem)
+        for (int i = tid; i < args.K; i += C::kThreads) bias_s[args.N + i] = args.wm[i];
     if (tid == 0) {
         for (int s = 0; s < ST; ++s) {
             // TMA producer's arrive.expect_tx (+ one noinc arrival per gather thread for conv1 dyn)
             mbar_init(bar_full + 8 * s, C::kGather ? C::kGatherThreads + 1 : 1);
-            mbar_init(bar_empty + 8 * s, C::kMasker ? 1 + C::kMaskerThreads / 32 : 1);  // tcgen05.commit (+ masker warps)
+            mbar_init(bar_empty + 8 * s, C::kMasker ? 1 + 4 : 1);  // tcgen05.commit (+ the 4 masker warps of its K parity)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(bar_tfull + 8 * a, 1);     // tcgen05.commit
@@ -180,6 +184,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+
     pdl_wait();     // inputs of the previous kernel (x, h1, idx/count) are complete from here on
     pdl_trigger();
 
@@ -201,7 +206,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                 for (int kb = 0; kb < num_kb; ++kb, ++it) {
                     const int stage = it % ST;
                     mbar_wait(bar_empty + 8 * stage, ((it / ST) & 1) ^ 1);
-                    const uint32_t sa = sbase + stage * C::kStageBytes;
+                    const uint32_t sa = sbase + C::kStageOff + stage * C::kStageBytes;
                     const uint32_t sb = sa + kABytes;
                     const uint32_t fb = bar_full + 8 * stage;
                     int a_bytes = kABytes;  // conv1 dyn: A arrives by cp.async (not counted here)
@@ -274,7 +279,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                 const int stage = it % ST;
                 mbar_wait(bar_empty + 8 * stage, ((it / ST) & 1) ^ 1);
                 if (pt == 0) KTRACE(it, 3);
-                const uint32_t sa = sbase + stage * C::kStageBytes;
+                const uint32_t sa = sbase + C::kStageOff + stage * C::kStageBytes;
 #pragma unroll
                 for (int i = 0; i < RPT; ++i) {
                     const int row = prow + RSTEP * i;
@@ -291,22 +296,24 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
         }
     } else if (C::kMasker && warp >= C::kMaskerWarp0) {
         // -------------------------------------- masker partials (fused) --
-        // thread = A row = pixel; reads the 8 16-B chunks of its 128-B swizzled
-        // row of every K-block (conflict-free: 8 consecutive rows cover all 32
-        // banks) while the MMA consumes the same stage.  Per 16-B chunk (8
-        // channels) an fp32 FFMA chain, added to an fp64 accumulator: the partial
-        // sum_c wm_c x[p,c] is within gamma_8 (fp32) of exact per chunk, and
-        // sum_c |wm_c x| (fp32) bounds it.  Fixed channel order; the certified
-        // decision happens in decide_gather.cu.
-        const int r = tid - 32 * C::kMaskerWarp0;
-        int it = 0;
-        for (int tile = blockIdx.x; tile < geo.num_tiles; tile += gridDim.x) {
-            double acc = 0.0;
-            float mag = 0.f;
-            for (int kb = 0; kb < num_kb; ++kb, ++it) {
+        // 8 warps: warp w owns A rows (w & 3) * 32 + lane (thread = pixel) and the
+        // K-blocks of parity w >> 2.  It reads the 8 16-B chunks of its 128-B
+        // swizzled row of each of its K-blocks (conflict-free: 8 consecutive rows
+        // cover all 32 banks) while the MMA consumes the same stage, and keeps fp32
+        // FFMA sums: the partial a = sum_c wm_c x[p,c] over its channels and the
+        // magnitude m = sum_c |wm_c x[p,c]|, two independent chains each.  Every
+        // channel term passes through at most c_in/8 + 8 fp32 roundings, which
+        // decide_gather.cu's certified bound accounts for.  Fixed channel order.
+        const int mw = warp - C::kMaskerWarp0;
+        const int r = (mw & 3) * 32 + lane, par = mw >> 2;
+        int base = 0;
+        for (int tile = blockIdx.x; tile < geo.num_tiles; tile += gridDim.x, base += num_kb) {
+            float acc0 = 0.f, acc1 = 0.f, mag0 = 0.f, mag1 = 0.f;
+            for (int kb = par; kb < num_kb; kb += 2) {
+                const int it = base + kb;
                 const int stage = it % ST;
                 mbar_wait(bar_full + 8 * stage, (it / ST) & 1);
-                const uint32_t row = sbase + stage * C::kStageBytes + r * 128;
+                const uint32_t row = sbase + C::kStageOff + stage * C::kStageBytes + r * 128;
                 uint32_t q[8][4];
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
@@ -318,22 +325,24 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                 const float4 *w4 = reinterpret_cast<const float4 *>(wm_s + kb * kBK);
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    const float4 wa = w4[2 * j], wb = w4[2 * j + 1];
+                    const float4 wa = C::kWmSmem ? w4[2 * j] : __ldg(w4 + 2 * j);
+                    const float4 wb = C::kWmSmem ? w4[2 * j + 1] : __ldg(w4 + 2 * j + 1);
                     const float wv[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
-                    float cs = 0.f;
+                    float cs = 0.f, ms = 0.f;
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const float lo = bf16lo(q[j][e]), hi = bf16hi(q[j][e]);
                         cs = fmaf(wv[2 * e], lo, cs);
                         cs = fmaf(wv[2 * e + 1], hi, cs);
-                        mag = fmaf(fabsf(wv[2 * e]), fabsf(lo), mag);
-                        mag = fmaf(fabsf(wv[2 * e + 1]), fabsf(hi), mag);
+                        ms = fmaf(fabsf(wv[2 * e]), fabsf(lo), ms);
+                        ms = fmaf(fabsf(wv[2 * e + 1]), fabsf(hi), ms);
                     }
-                    acc += (double)cs;
+                    if (j & 1) { acc1 += cs; mag1 += ms; } else { acc0 += cs; mag0 += ms; }
                 }
             }
             const int m = (tile / geo.n_tiles_n) * kBM + r;
-            if (tile % geo.n_tiles_n == 0 && m < args.m_dense) args.mpart[m] = make_double2(acc, (double)mag);
+            if (tile % geo.n_tiles_n == 0 && m < args.m_dense)
+                reinterpret_cast<float2 *>(args.mpart)[2 * m + par] = make_float2(acc0 + acc1, mag0 + mag1);
         }
     } else if (warp == C::kMmaWarp) {
         // ---------------------------------------------------- MMA issuer --
@@ -352,7 +361,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     KTRACE(it, 2);
                     if (C::kGather) fence_proxy_async_smem();  // cp.async (generic) -> tcgen05 (async)
                     tc_fence_after();
-                    const uint32_t sa = sbase + stage * C::kStageBytes;
+                    const uint32_t sa = sbase + C::kStageOff + stage * C::kStageBytes;
                     const uint64_t adesc = smem_desc_sw128(sa);
                     const uint64_t bdesc = smem_desc_sw128(sa + kABytes);
 #pragma unroll

@@ -27,7 +27,7 @@ cudaError_t launch_conv_tc(int mode, const ConvArgs &a, int max_tiles_m, int num
 cudaError_t launch_conv_simt(int mode, const ConvArgs &a, int max_rows, cudaStream_t st);
 cudaError_t launch_conv23(bool dense, const ConvArgs &a, int max_tiles, int num_sms, cudaStream_t st);
 size_t decide_sync_bytes(int ncells, int num_sms);
-cudaError_t launch_decide_gather(const double2 *mpart, const void *x, const float *wm, float bm, int n_img, int H,
+cudaError_t launch_decide_gather(const float4 *mpart, const void *x, const float *wm, float bm, int n_img, int H,
                                  int W, int c_in, int S, uint8_t *mask, int32_t *idx, int32_t *count, void *sync,
                                  const void *h1d, void *h1g, int c_mid, int cap, int num_sms, cudaStream_t st);
 }  // namespace lasnet
@@ -618,11 +618,11 @@ lasnet_status lasnet_block_forward(const lasnet_block_desc *d, const lasnet_bloc
     a.m_dense = px;
     a.a_src = x; a.w = w->w1; a.bias = w->b1; a.out = r.h1d;
     a.K = d->c_in; a.N = d->c_mid; a.a_ld = d->c_in; a.out_ld = d->c_mid;
-    a.wm = wm; a.mpart = static_cast<double2 *>(r.mpart);
+    a.wm = wm; a.mpart = static_cast<float4 *>(r.mpart);
     if (run_conv(d, CONV1_DENSE_MASK, a, px, x, y, r.h1d, nullptr, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
     {
         KernelEvents ev(st);
-        if (launch_decide_gather(static_cast<const double2 *>(r.mpart), x, wm, bm, d->n, d->h, d->w, d->c_in, d->s,
+        if (launch_decide_gather(static_cast<const float4 *>(r.mpart), x, wm, bm, d->n, d->h, d->w, d->c_in, d->s,
                                  mask, idx, count, r.sync, r.h1d, r.h1g, d->c_mid, ncells, num_sms(), st) !=
             cudaSuccess)
             return LASNET_ERR_CUDA;

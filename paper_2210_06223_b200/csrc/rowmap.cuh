@@ -71,10 +71,11 @@ struct ConvArgs {
     int32_t box_rows;         // rows one A box delivers (conv2 dyn/dense, conv3 dyn)
     int32_t rows_h, imgs_box; // conv2 dense: image rows / images per box
     int32_t dense_tiles;      // conv2 dense: M tiles
-    // masker fused into the dense conv1 (CONV1_DENSE_MASK): per pixel p the fp64
-    // partial logit sum_c wm_c x[p,c] and its magnitude sum_c |wm_c x[p,c]|
+    // masker fused into the dense conv1 (CONV1_DENSE_MASK): per pixel p the fp32
+    // partial logits sum_c wm_c x[p,c] and magnitudes sum_c |wm_c x[p,c]| over the
+    // channels of the even and of the odd 64-channel K-blocks
     const float *wm;          // [c_in] reduced masker weight W_0 - W_1
-    double2 *mpart;           // [n*h*w] (partial, magnitude)
+    float4 *mpart;            // [n*h*w] (partial, magnitude) of the even and of the odd K-blocks
 };
 
 __host__ __device__ __forceinline__ int rows_per_patch(int mode, int S) {
