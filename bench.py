@@ -323,7 +323,7 @@ def run_lasnet(args):
     kwork, bwork, dwork, stats = algorithmic_work(mask_cells, n, h, w, c_in, c_mid, c_in, s)
 
     K = args.steps
-    fused23 = os.environ.get("LASNET_NO_FUSE", "0") != "1" and c_mid in (64, 128) and c_in % 128 == 0
+    fused23 = os.environ.get("LASNET_NO_FUSE", "0") != "1" and c_mid in (64, 128) and c_in % 64 == 0 and 192 <= c_in <= 512
     head = ["conv1_mask", "decide_gather"] if sched == L.SCHED_FUSED else ["mask_compact", "conv1"]
     names = head + (["conv23"] if fused23 else ["conv2", "conv3"])
     ev_step = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]

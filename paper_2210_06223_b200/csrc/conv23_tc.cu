@@ -14,6 +14,16 @@
 // warps, so the HBM-bound conv3 epilogue of tile i overlaps the L2-bound conv2
 // K-loop of tile i+1 instead of stalling it.  Warps: 0-3 epi2, 4-11 epi3,
 // 12 conv2 producer, 13 conv2 MMA + TMEM allocator, 14 conv3 MMA, 15 conv3 producer.
+//
+// Weight multicast (CL = 2 or 4 CTAs per cluster): the CTAs of a cluster run
+// their tiles in lockstep K-block by K-block; each loads 1/CL of every W2 / W3
+// K-block and multicasts it into the same stage of all CL CTAs, and each CTA's
+// MMA commit releases that stage in all of them.  Every 128-row tile otherwise
+// re-streams the whole W2 (288 KB at c_mid 128) and W3 through L2, and conv2's
+// K-loop is bound by L2 throughput (profiles/ncu_summary_r1c.md): multicast
+// cuts the weight share of that traffic by CL.  Tiles are dealt cluster-major
+// (tile = (cluster + i * clusters) * CL + rank); a CTA whose tile lies past the
+// end runs it anyway on zero-filled (out-of-bounds) operands and stores nothing.
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -51,7 +61,7 @@ __device__ unsigned long long g_trace23c[64 * 16];
 namespace c23 {
 constexpr int kBM = 128, kBK = 64;
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB
-constexpr int kStages = 3;
+constexpr int kStages = 3;  // conv2 ring depth
 constexpr int kH2Bufs = 1;  // H2 tiles (double-buffering lets epi2 of tile i+1 overlap conv3 of tile i)
 constexpr int kStageBytes = 2 * kABytes;  // A 16 KB + B (<= 128 rows) 16 KB
 constexpr int kNC3 = 128;                 // max conv3 output channels per MMA chunk (64 when c_out % 128 != 0)
@@ -59,18 +69,18 @@ constexpr int kAcc3 = 2;                  // conv3 accumulator buffers (128 TMEM
 constexpr int kChunkBytes = kBM * 128;    // one 64-column bf16 chunk of a 128-row tile
 constexpr int kThreads = 16 * 32;
 constexpr int kEpi2Warp0 = 0, kEpi3Warp0 = 4, kProdWarp = 12, kMmaWarp = 13, kMma3Warp = 14, kProd3Warp = 15;
-constexpr int kResBufs = 2;  // residual prefetched kResBufs-1 chunks ahead
-constexpr int kStages3 = 3;                // conv3 weight ring (<= 16 KB stages: kNC3 rows x 64 K)
+constexpr int kStages3 = 2;                // conv3 weight ring (<= 16 KB stages: kNC3 rows x 64 K)
 constexpr int kB3Bytes = kNC3 * 128;
 // smem layout (offsets from the 1024-aligned base); biases are read through L1
 constexpr int kStagesOff = 0;
 constexpr int kH2Off = kStages * kStageBytes;                 // 2 x up to 32 KB (c_mid <= 128), double-buffered
+constexpr int kResBufs = 4;  // residual prefetched kResBufs-1 64-column chunks ahead (epi3 waits on its HBM latency)
 constexpr int kResOff = kH2Off + kH2Bufs * 2 * kChunkBytes;   // kResBufs x 16 KB (one 64-col chunk)
 constexpr int kRing3Off = kResOff + kResBufs * kChunkBytes;
 constexpr int kBiasOff = kRing3Off + kStages3 * kB3Bytes;     // b2 (<= 128 floats), b3 (<= 2048 floats)
-constexpr int kMaxCout = 2048;
+constexpr int kMaxCout = 512;
 constexpr int kBarOff = kBiasOff + (128 + kMaxCout) * 4;      // barriers
-constexpr int smem_bytes(int, int) { return 1024 + kBarOff + 256; }
+constexpr int smem_bytes(int, int) { return kBarOff + 256; }  // dynamic smem base is 1024-aligned (checked)
 }  // namespace c23
 
 // output pixel of row r of a conv23 tile (or -1): patch rows in dynamic mode, image rows dense
@@ -95,13 +105,13 @@ __device__ __forceinline__ int tile_pixel(const ConvArgs &args, int tile, int r,
     return out_pixel(args, tile * rows_per_tile + r, M);
 }
 
-template <bool DENSE>
+template <bool DENSE, int CL>
 __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_constant__ ConvArgs args) {
     using namespace c23;
-    extern __shared__ uint8_t smem_raw[];
-    const uint32_t raw_u32 = smem_u32(smem_raw);
-    const uint32_t sbase = (raw_u32 + 1023u) & ~1023u;
-    uint8_t *sgen = smem_raw + (sbase - raw_u32);
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t sbase = smem_u32(smem_raw);
+    if (sbase & 1023u) __trap();  // the 128-B swizzle atoms need a 1024-B aligned base
+    uint8_t *sgen = smem_raw;
     const uint32_t h2s = sbase + kH2Off;
     const uint32_t bar = sbase + kBarOff;
     const uint32_t bar_full = bar, bar_empty = bar + 8 * kStages;
@@ -117,14 +127,16 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
     float *b3_s = b2_s + 128;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int rank = CL > 1 ? (int)cluster_ctarank() : 0;
+    constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(bar_full + 8 * s, 1);
-            mbar_init(bar_empty + 8 * s, 1);
+            mbar_init(bar_empty + 8 * s, CL);  // the MMA commits of all CL CTAs
         }
         for (int s = 0; s < kStages3; ++s) {
             mbar_init(bar_full3 + 8 * s, 1);
-            mbar_init(bar_empty3 + 8 * s, 1);
+            mbar_init(bar_empty3 + 8 * s, CL);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(bar_t2full + 8 * a, 1);
@@ -149,7 +161,8 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
     for (int c = tid; c < args.N; c += kThreads) b2_s[c] = args.bias[c];
     for (int c = tid; c < args.n3; c += kThreads) b3_s[c] = args.bias3[c];
     tc_fence_before();
-    __syncthreads();
+    if (CL > 1) cluster_sync();  // every CTA's barriers are initialised before any multicast lands
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     pdl_wait();  // h1, idx and count of the previous kernels are complete from here on
@@ -173,14 +186,18 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
     const int NC3 = CO % kNC3 == 0 ? kNC3 : 64;                   // conv3 MMA N
     const int nch = CO / NC3;                                     // conv3 MMA chunks
     const int nsub = CO / 64;                                     // 64-column epilogue sub-chunks
-    int ntl = 0;                                                  // tiles of this CTA
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) ++ntl;
+    // tiles dealt cluster-major: local tile i of this CTA is ((cl + i * ncl) * CL + rank);
+    // every CTA of a cluster runs the same ntl (lockstep multicast)
+    const int cl = blockIdx.x / CL, ncl = gridDim.x / CL;
+    int ntl = 0;
+    for (int t = cl * CL; t < num_tiles; t += ncl * CL) ++ntl;
+    auto tile_of = [&](int i) { return (cl + i * ncl) * CL + rank; };
 
     if (warp == kProdWarp) {
         // ------------------------------------------ conv2 TMA producer --
         int it = 0;
         for (int i = 0; i < ntl; ++i) {
-            const int tile = blockIdx.x + i * gridDim.x;
+            const int tile = tile_of(i);
             if (lane == 0) {
                 int n0 = 0, y0 = 0;
                 if (DENSE) {
@@ -198,7 +215,11 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
                     mbar_wait(bar_empty + 8 * st, ((it / kStages) & 1) ^ 1);
                     const uint32_t sa = sbase + st * kStageBytes, fb = bar_full + 8 * st;
                     mbar_arrive_expect_tx(fb, args.box_rows * 128 + KC * 128);
-                    tma_load_2d(sa + kABytes, &args.tmap_b, fb, kb * kBK, 0);
+                    if (CL > 1)  // this CTA's 1/CL of the W2 K-block, into every CTA of the cluster
+                        tma_load_2d_mc(sa + kABytes + rank * (KC / CL) * 128, &args.tmap_b, fb, kb * kBK,
+                                       rank * (KC / CL), kMask);
+                    else
+                        tma_load_2d(sa + kABytes, &args.tmap_b, fb, kb * kBK, 0);
                     const int tap = kb / kpt, dy = tap / 3, dx = tap - dy * 3, c0 = (kb - tap * kpt) * kBK;
                     // h1 is channel-chunk-major: [c_mid/64][P][S+2][S+2][64] (dense: [c_mid/64][N][H][W][64])
                     if (DENSE) tma_load_5d(sa, &args.tmap_a, fb, 0, dx - 1, y0 + dy - 1, n0, c0 >> 6);
@@ -219,7 +240,11 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
                         if (kb == 0) T23C(i * nch + nc, 0);
                         const uint32_t fb = bar_full3 + 8 * st;
                         mbar_arrive_expect_tx(fb, NC3 * 128);
-                        tma_load_2d(sbase + kRing3Off + st * kB3Bytes, &args.tmap_b3, fb, kb * kBK, nc * NC3);
+                        if (CL > 1)
+                            tma_load_2d_mc(sbase + kRing3Off + st * kB3Bytes + rank * (NC3 / CL) * 128, &args.tmap_b3,
+                                           fb, kb * kBK, nc * NC3 + rank * (NC3 / CL), kMask);
+                        else
+                            tma_load_2d(sbase + kRing3Off + st * kB3Bytes, &args.tmap_b3, fb, kb * kBK, nc * NC3);
                     }
         }
     } else if (warp == kMmaWarp) {
@@ -240,7 +265,8 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
                     const uint64_t ad = smem_desc_sw128(sa), bd = smem_desc_sw128(sa + kABytes);
 #pragma unroll
                     for (int kk = 0; kk < kBK / 16; ++kk) mma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc2, (kb | kk) != 0);
-                    mma_commit(bar_empty + 8 * st);
+                    if (CL > 1) mma_commit_mc(bar_empty + 8 * st, kMask);
+                    else mma_commit(bar_empty + 8 * st);
                 }
                 mma_commit(bar_t2full + 8 * acc);
             }
@@ -272,7 +298,8 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
 #pragma unroll
                         for (int kk = 0; kk < kBK / 16; ++kk)
                             mma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc3, (kb | kk) != 0);
-                        mma_commit(bar_empty3 + 8 * st);
+                        if (CL > 1) mma_commit_mc(bar_empty3 + 8 * st, kMask);
+                        else mma_commit(bar_empty3 + 8 * st);
                     }
                     mma_commit(bar_t3full + 8 * buf);
                     T23C(c3, 3);
@@ -330,7 +357,7 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
         __nv_bfloat16 *Y = static_cast<__nv_bfloat16 *>(args.out);
         // output pixel of tile-row r of local tile i (or -1)
         auto pixel_of = [&](int i) -> int {
-            return tile_pixel<DENSE>(args, blockIdx.x + i * gridDim.x, r, rows_per_tile, M);
+            return tile_pixel<DENSE>(args, tile_of(i), r, rows_per_tile, M);
         };
         constexpr int kChunks = 32 / 8;           // 16-B chunks of this warp's 32 columns
         constexpr int kRowsPerIt = 32 / kChunks;  // 8 rows (64 B each) per instruction
@@ -359,7 +386,7 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
         };
         const uint32_t res0 = sbase + kResOff;
         constexpr int D = kResBufs - 1;  // prefetch distance in chunks (D <= nch: at most one tile ahead)
-        static_assert(D == 1, "prefetch may run at most one tile ahead");
+        // the prefetch runs at most one tile ahead (cur / nxt row offsets): D <= nsub
         long long cur[kIt], nxt[kIt];
         row_offsets(0, cur);
         row_offsets(1, nxt);
@@ -450,7 +477,9 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
     }
 
     tc_fence_before();
-    __syncthreads();
+    // no CTA leaves while a peer may still multicast into its smem or arrive on its barriers
+    if (CL > 1) cluster_sync();
+    else __syncthreads();
     if (warp == kMmaWarp) {
         tc_fence_after();
         tmem_dealloc<512>(tmem_base);
@@ -471,28 +500,33 @@ extern "C" int lasnet_trace23c_read(unsigned long long *h) {
 }
 #endif
 
-cudaError_t launch_conv23(bool dense, const ConvArgs &a, int max_tiles, int num_sms, cudaStream_t st) {
-    if (!(a.N == 64 || a.N == 128) || a.n3 % 64 != 0 || a.n3 > c23::kMaxCout) return cudaErrorInvalidValue;
+template <bool DENSE, int CL>
+static cudaError_t launch23(const ConvArgs &a, int max_tiles, int num_sms, cudaStream_t st) {
     const int smem = c23::smem_bytes(a.N, a.n3);
-    const int grid = max_tiles < num_sms ? (max_tiles > 0 ? max_tiles : 1) : num_sms;
-    if (dense) {
-        static int cfg = 0;
-        if (smem > cfg) {
-            cudaError_t e = cudaFuncSetAttribute(conv23_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            if (e != cudaSuccess) return e;
-            cfg = smem;
-        }
-        return launch_k(conv23_kernel<true>, dim3(grid), dim3(c23::kThreads), smem, st, a);
-    } else {
-        static int cfg = 0;
-        if (smem > cfg) {
-            cudaError_t e = cudaFuncSetAttribute(conv23_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            if (e != cudaSuccess) return e;
-            cfg = smem;
-        }
-        return launch_k(conv23_kernel<false>, dim3(grid), dim3(c23::kThreads), smem, st, a);
+    static int cfg = 0;
+    if (smem > cfg) {
+        cudaError_t e = cudaFuncSetAttribute(conv23_kernel<DENSE, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        cfg = smem;
     }
-    return cudaGetLastError();
+    // whole clusters, at most one CTA per SM
+    const int want = (max_tiles + CL - 1) / CL * CL;
+    const int cap = num_sms / CL * CL;
+    const int grid = want < cap ? (want > 0 ? want : CL) : cap;
+    return launch_k_cluster(conv23_kernel<DENSE, CL>, dim3(grid), dim3(c23::kThreads), smem, st, CL, a);
+}
+
+// a.cluster: CTAs per cluster sharing the weight loads (1, 2 or 4; the tensor maps'
+// weight boxes were encoded with KC / cluster and NC3 / cluster rows).
+cudaError_t launch_conv23(bool dense, const ConvArgs &a, int max_tiles, int num_sms, cudaStream_t st) {
+    if (!(a.N == 64 || a.N == 128) || a.n3 % 64 != 0 || a.n3 > c23::kMaxCout || a.n3 < 64 * (c23::kResBufs - 1))
+        return cudaErrorInvalidValue;
+    switch (a.cluster) {
+        case 1: return dense ? launch23<true, 1>(a, max_tiles, num_sms, st) : launch23<false, 1>(a, max_tiles, num_sms, st);
+        case 2: return dense ? launch23<true, 2>(a, max_tiles, num_sms, st) : launch23<false, 2>(a, max_tiles, num_sms, st);
+        case 4: return dense ? launch23<true, 4>(a, max_tiles, num_sms, st) : launch23<false, 4>(a, max_tiles, num_sms, st);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 }  // namespace lasnet

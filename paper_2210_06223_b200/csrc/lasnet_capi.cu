@@ -264,7 +264,8 @@ bool use_fused23(const lasnet_block_desc *d) {
         const char *e = getenv("LASNET_NO_FUSE");
         return e && e[0] == '1';
     }();
-    return !off && d->dtype == LASNET_BF16 && (d->c_mid == 64 || d->c_mid == 128) && d->c_out % 64 == 0;
+    return !off && d->dtype == LASNET_BF16 && (d->c_mid == 64 || d->c_mid == 128) && d->c_out % 64 == 0 &&
+           d->c_out <= 512 && d->c_out >= 192;
 }
 
 cudaError_t run_conv23(const lasnet_block_desc *d, bool dense, ConvArgs a, const lasnet_block_weights *w,
@@ -273,7 +274,15 @@ cudaError_t run_conv23(const lasnet_block_desc *d, bool dense, ConvArgs a, const
     a.a_src = h1; a.w = w->w2; a.bias = w->b2; a.out = y; a.resid = x;
     a.K = 9 * C; a.N = C; a.a_ld = C; a.out_ld = d->c_out;
     a.w3 = w->w3; a.bias3 = w->b3; a.n3 = d->c_out;
-    bool ok = tmap2(&a.tmap_b, a.w, a.K, a.N, 64, C) && tmap2(&a.tmap_b3, w->w3, C, d->c_out, 64, d->c_out % 128 == 0 ? 128 : 64);  // conv3 MMA N
+    // CTAs per cluster multicasting the weight K-blocks (LASNET_C23_CLUSTER = 1, 2, 4)
+    static const int cl_env = [] {
+        const char *e = getenv("LASNET_C23_CLUSTER");
+        const int v = e ? atoi(e) : 1;
+        return (v == 1 || v == 2 || v == 4) ? v : 1;
+    }();
+    const int nc3 = d->c_out % 128 == 0 ? 128 : 64;  // conv3 MMA N
+    a.cluster = (C / cl_env >= 8 && nc3 / cl_env >= 8) ? cl_env : 1;
+    bool ok = tmap2(&a.tmap_b, a.w, a.K, a.N, 64, C / a.cluster) && tmap2(&a.tmap_b3, w->w3, C, d->c_out, 64, nc3 / a.cluster);
     int tiles;
     if (dense) {
         if (d->h * d->w <= 128) {

@@ -71,6 +71,7 @@ struct ConvArgs {
     int32_t box_rows;         // rows one A box delivers (conv2 dyn/dense, conv3 dyn)
     int32_t rows_h, imgs_box; // conv2 dense: image rows / images per box
     int32_t dense_tiles;      // conv2 dense: M tiles
+    int32_t cluster;          // fused conv2+conv3: CTAs per cluster sharing (multicasting) the weight loads
     // masker fused into the dense conv1 (CONV1_DENSE_MASK): per pixel p the fp32
     // partial logits sum_c wm_c x[p,c] and magnitudes sum_c |wm_c x[p,c]| over the
     // channels of the even and of the odd 64-channel K-blocks
