@@ -397,6 +397,9 @@ def run_lasnet(args):
     from paper_2210_06223_b200 import dist as ldist
 
     tot_max, e2e_max, dense_max = ldist.max_over_ranks([tot_ms, e2e_ms, statistics.fmean(dense_ms)], device="cuda")
+    # the exchange step of SURVEY 8(e): summed active-cell statistics and per-rank step times
+    act_all, cells_all = ldist.sum_over_ranks([stats["P"], mask_cells.size], device="cuda")
+    rank_ms = [t / K for t in ldist.gather_over_ranks(tot_ms, device="cuda")]
     value = ldist.throughput(n, world, K, tot_max)
     e2e_val = ldist.throughput(n, world, K, e2e_max)
 
@@ -440,6 +443,10 @@ def run_lasnet(args):
             "block_roofline": blk_roof,
             "e2e": {"value": round(e2e_val, 1), "unit": "images/s", "h2d_bytes_per_step": x.numel() * 2,
                     "d2h_bytes_per_step": x.numel() * 2},
+            "stats": {"active_cells_all_ranks": int(act_all), "cells_all_ranks": int(cells_all),
+                      "r_patch_all_ranks": round(act_all / max(cells_all, 1), 4),
+                      "rank_ms_per_step": {"min": round(min(rank_ms), 4), "max": round(max(rank_ms), 4),
+                                           "mean": round(statistics.fmean(rank_ms), 4)}},
             "gpu_launches": launches,
             "clocks": clocks,
         }

@@ -95,7 +95,8 @@ template <int MODE, int BN> struct Cfg {
     static constexpr int kBiasOff = kBarOff + 256;
     // bias [n] then (masker) wm [k]
     static constexpr bool kWmSmem = kMasker;
-    static constexpr int smem_bytes(int n, int k) { return 1024 + kBiasOff + n * 4 + (kWmSmem ? k * 4 : 0); }
+    // the dynamic smem base is 1024-B aligned (checked in the kernel): no alignment slack
+    static constexpr int smem_bytes(int n, int k) { return kBiasOff + n * 4 + (kWmSmem ? k * 4 : 0); }
 };
 
 template <int MODE, int BN> __host__ __device__ constexpr int threads_of() { return Cfg<MODE, BN>::kThreads; }
@@ -139,10 +140,10 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
     using C = Cfg<MODE, BN>;
     constexpr int ST = C::kStages, NSTG = C::kStaging, EPI = C::kEpiWarps * 32;
     constexpr bool kResid = C::kResid;
-    extern __shared__ uint8_t smem_raw[];
-    const uint32_t raw_u32 = smem_u32(smem_raw);
-    const uint32_t sbase = (raw_u32 + 1023u) & ~1023u;
-    uint8_t *sgen = smem_raw + (sbase - raw_u32);
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t sbase = smem_u32(smem_raw);
+    if (sbase & 1023u) __trap();  // the 128-B swizzle atoms need a 1024-B aligned base
+    uint8_t *sgen = smem_raw;
 
     const uint32_t staging = sbase + C::kStagingOff;  // NSTG x kStagingBytes
     const uint32_t bar_full = sbase + C::kBarOff;     // ST

@@ -52,7 +52,7 @@ struct DecideArgs {
     unsigned *done;             // CTAs finished (zero on entry, reset by the last)
 };
 
-constexpr int kDecThreads = 64;  // small CTAs: one thread per cell, spread over the SMs
+constexpr int kDecThreads = 256;
 
 __device__ __forceinline__ unsigned atom_add_acqrel(unsigned *p, unsigned v) {
     unsigned old;

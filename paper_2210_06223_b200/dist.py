@@ -47,6 +47,17 @@ def sum_over_ranks(values, device="cpu"):
     return _reduce(values, dist.ReduceOp.SUM, device)
 
 
+def gather_over_ranks(value: float, device="cpu"):
+    """[value of rank 0, value of rank 1, ...] on every rank (per-rank step times:
+    per-image activation rates vary, so ranks finish at different times)."""
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        out = [torch.zeros_like(t) for _ in range(dist.get_world_size())]
+        dist.all_gather(out, t)
+        return [float(o.item()) for o in out]
+    return [float(t.item())]
+
+
 def throughput(images_per_rank: int, world: int, steps: int, max_total_ms: float) -> float:
     """Whole-job images/s of a weak-scaling run: all ranks' images over the slowest rank's time."""
     return images_per_rank * world * steps / (max_total_ms / 1e3)

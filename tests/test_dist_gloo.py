@@ -26,10 +26,11 @@ def _worker(rank, world, port, q):
         r, w, lr = L.env_ranks()
         mx = L.max_over_ranks([rank * 10.0 + 1.0, -rank])
         sm = L.sum_over_ranks([1.0, rank])
+        ga = L.gather_over_ranks(100.0 + rank)
         start, stop = L.shard(256, r, w)
         n_local = torch.tensor([stop - start])
         dist.all_reduce(n_local)
-        q.put((rank, r, w, lr, mx, sm, (start, stop), int(n_local.item())))
+        q.put((rank, r, w, lr, mx, sm, (start, stop), int(n_local.item()), ga))
     finally:
         dist.destroy_process_group()
 
@@ -45,11 +46,12 @@ def test_gloo_two_ranks():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, r, w, lr, mx, sm, rng, n_all in out:
+    for rank, r, w, lr, mx, sm, rng, n_all, ga in out:
         assert (r, w, lr) == (rank, 2, rank)
         assert mx == [11.0, 0.0]          # max over ranks
         assert sm == [2.0, 1.0]           # sum over ranks
         assert n_all == 256               # shards cover the global batch
+        assert ga == [100.0, 101.0]       # per-rank values, rank order
     assert out[0][6] == (0, 128) and out[1][6] == (128, 256)
 
 
@@ -64,4 +66,5 @@ def test_shard_partitions(n, world):
 
 def test_single_process_reductions_are_identity():
     assert L.max_over_ranks([3.0, 4.0]) == [3.0, 4.0]
+    assert L.gather_over_ranks(5.0) == [5.0]
     assert L.throughput(128, 8, 10, 1000.0) == 128 * 8 * 10

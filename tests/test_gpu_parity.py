@@ -88,6 +88,53 @@ def test_fused_mask_compact_bit_exact(n, h, w, c, s, dtype):
     assert int(blk.mcws.count_nonzero().item()) == 0  # workspace left zeroed
 
 
+STREAM_CASES = MASK_CASES + [
+    (2, 13, 11, 256, 4, "bf16"),     # ragged, 1 slot per pixel
+    (1, 9, 7, 2048, 3, "bf16"),      # 8 slots per pixel
+    (3, 10, 12, 1024, 2, "f32"),     # fp32, 8 slots
+]
+
+
+@pytest.mark.parametrize("n,h,w,c,s,dtype", STREAM_CASES)
+def test_mask_decisions_only_bit_exact(n, h, w, c, s, dtype):
+    """Decisions without logits (the certified fp32 fast path): mask, and with
+    step 2 fused idx/count, equal the fp64 oracle's bit for bit; the workspace
+    is left zeroed."""
+    x = synth.make_x(n, h, w, c, seed=s + 3, dtype=dtype)
+    wm = synth.make_masker_weights(c, seed=s + 13)
+    xd = synth.to_f64(x)
+    _, l0 = oracle.masker(xd, synth.to_f64(wm), 0.0, s)
+    xg, wg = x.cuda(), wm.cuda()
+    for r in (0.5, 0.1, 0.9):
+        bm = margin_bias(l0, r)
+        m_or, _ = oracle.masker(xd, synth.to_f64(wm), bm, s)
+        idx_or, cnt = oracle.compact(m_or)
+        assert np.array_equal(L.mask(xg, wg, bm, s).cpu().numpy(), m_or)
+        blk = L.DynBlock(L.BlockShape(n, h, w, c, 64, s, torch.float32 if dtype == "f32" else torch.bfloat16),
+                         synth.make_block_weights(c, 64, c, seed=1, dtype=dtype), wm, bm)
+        blk.mask_compact(xg)
+        assert np.array_equal(blk.mask_buf.cpu().numpy(), m_or)
+        assert int(blk.count.item()) == cnt
+        assert np.array_equal(blk.idx[:cnt].cpu().numpy(), idx_or)
+        assert int(blk.mcws.count_nonzero().item()) == 0
+
+
+def test_mask_decisions_only_uncertain_cells_fall_back_exactly():
+    """Biases placing one cell's logit within fp32 rounding of 0: the masker's
+    exact fp64 re-sum decides it as the oracle does."""
+    n, h, w, c, s = 4, 12, 12, 512, 3
+    x = synth.make_x(n, h, w, c, seed=21)
+    wm = synth.make_masker_weights(c, seed=22)
+    xd = synth.to_f64(x)
+    _, l0 = oracle.masker(xd, synth.to_f64(wm), 0.0, s)
+    for k in (0, 5, 17):
+        bm = float(np.float32(-l0.reshape(-1)[k]))
+        m_or, l_or = oracle.masker(xd, synth.to_f64(wm), bm, s)
+        if np.abs(l_or).min() < 1e-12 * np.abs(l_or).max():
+            continue  # exact tie at fp64 precision
+        assert np.array_equal(L.mask(x.cuda(), wm.cuda(), bm, s).cpu().numpy(), m_or)
+
+
 # ------------------------------------------------------------------ step 2 --
 
 @pytest.mark.parametrize("ncells,r", [(1, 1.0), (7, 0.5), (4095, 0.3), (4096, 0.5), (4097, 0.9),
@@ -267,6 +314,9 @@ FWD_CASES = [
     (2, 10, 10, 128, 64, 4, 0.0),    # no cell active
     (1, 7, 7, 512, 256, 1, 0.5),     # c_mid 256: unfused conv2 / conv3 kernels
     (4, 28, 28, 512, 128, 4, 0.5),   # config-2 widths, reduced batch
+    (2, 56, 56, 256, 64, 4, 0.5),    # LAS-R101 stage 1 identity block (config 3), reduced batch
+    (2, 14, 14, 1024, 256, 2, 0.5),  # stage 3
+    (2, 7, 7, 2048, 512, 1, 0.5),    # stage 4
 ]
 
 
