@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--s", type=int, default=WORKLOAD["s"])
     ap.add_argument("--r", type=float, default=WORKLOAD["r"])
     ap.add_argument("--n", type=int, default=WORKLOAD["n"])
+    ap.add_argument("--hw", type=int, default=WORKLOAD["h"], help="(experiments) spatial size of the block")
+    ap.add_argument("--c-in", type=int, default=WORKLOAD["c_in"], help="(experiments) block width")
+    ap.add_argument("--c-mid", type=int, default=WORKLOAD["c_mid"], help="(experiments) bottleneck width")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
     ap.add_argument("--detail", default=None, help="write per-kernel detail JSON here")
@@ -285,7 +288,7 @@ def run_lasnet(args):
         dist.barrier()
     lib = _lib.load()
 
-    wl = dict(WORKLOAD, n=args.n, s=args.s, r=args.r)
+    wl = dict(WORKLOAD, n=args.n, s=args.s, r=args.r, h=args.hw, w=args.hw, c_in=args.c_in, c_mid=args.c_mid)
     n, h, w, c_in, c_mid, s = (wl[k] for k in ("n", "h", "w", "c_in", "c_mid", "s"))
     x_cpu = synth.make_x(n, h, w, c_in, seed=0 + 7919 * rank)
     wts_cpu = synth.make_block_weights(c_in, c_mid, c_in, seed=1)
@@ -428,7 +431,9 @@ def run_lasnet(args):
             "metric": METRIC, "value": round(value, 1), "unit": "images/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": round(tot_max / K, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": WORKLOAD_NAME, "global_batch": world * n, "per_gpu_batch": n,
+            "config": {"workload": WORKLOAD_NAME if (h, c_in, c_mid) == (28, 512, 128) else
+                       f"experiment: identity dyn-block {h}x{w}x{c_in} c_mid={c_mid}", "global_batch": world * n,
+                       "per_gpu_batch": n,
                        "H": h, "W": w, "c_in": c_in, "c_mid": c_mid, "S": s, "r_target": wl["r"],
                        "r_patch": round(stats["r_patch"], 4), "r_pixel": round(stats["r_pixel"], 4),
                        "parallelism": f"dp{world}", "l2": "flushed (256 MiB read) before every timed step",

@@ -86,8 +86,13 @@ template <int MODE, int BN> struct Cfg {
     static constexpr int kStagingBytes = (BN / 64) * kChunkBytes;
     // conv1 dyn: HBM gather -> deep pipeline, 1 staging buffer (TMA store drains fast)
     // conv3: short K (2-8 blocks) -> 3 stages, 3 staging buffers (residual prefetched 2 tiles ahead)
-    static constexpr int kStaging = kGather ? 1 : (kResid ? 3 : 2);
-    static constexpr int kStages = kGather ? (BN == 128 ? 6 : 8) : (kResid ? 3 : (BN == 128 ? 4 : 6));
+    // BN = 256 (conv1 at c_mid >= 256): A is read once per M tile instead
+    // of once per 128-column N tile, and each UMMA moves 96 instead of 128 smem bytes
+    // per clock; 3 stages of 48 KB + one 64 KB staging tile
+    static_assert(BN != 256 || !kResid, "BN = 256 only without the residual epilogue");
+    static constexpr int kStaging = BN == 256 ? 1 : (kGather ? 1 : (kResid ? 3 : 2));
+    static constexpr int kStages =
+        BN == 256 ? 3 : (kGather ? (BN == 128 ? 6 : 8) : (kResid ? 3 : (BN == 128 ? 4 : 6)));
     static constexpr int kTmemCols = 2 * BN;
     static constexpr int kStageOff = 0;  // [stages][staging][barriers][bias (+wm)]
     static constexpr int kStagingOff = kStageOff + kStages * kStageBytes;
@@ -583,6 +588,9 @@ static cudaError_t launch_mode_bn(const ConvArgs &a, int max_tiles_m, int num_sm
 template <int MODE>
 static cudaError_t launch_mode(const ConvArgs &a, int max_tiles_m, int num_sms, cudaStream_t st) {
     if (a.N == 64) return launch_mode_bn<MODE, 64>(a, max_tiles_m, num_sms, st);
+    if constexpr (MODE == CONV1_DYN || MODE == CONV1_DENSE || MODE == CONV1_DENSE_MASK) {
+        if (a.N % 256 == 0) return launch_mode_bn<MODE, 256>(a, max_tiles_m, num_sms, st);
+    }
     if (a.N % 128 == 0) return launch_mode_bn<MODE, 128>(a, max_tiles_m, num_sms, st);
     return cudaErrorInvalidValue;
 }

@@ -196,7 +196,12 @@ bool tmap5(CUtensorMap *m, const void *base, const uint64_t (&d)[5], const uint3
     return tmap(m, base, 5, d, b);
 }
 
-int bn_of(int n) { return n == 64 ? 64 : 128; }
+// N tile of conv_tc's launch for `mode` (must match launch_mode in conv_tc.cu)
+int bn_of(int n, int mode) {
+    if (n == 64) return 64;
+    if (n % 256 == 0 && (mode == CONV1_DYN || mode == CONV1_DENSE || mode == CONV1_DENSE_MASK)) return 256;
+    return 128;
+}
 
 // Fills the TMA descriptors and tile geometry of one tcgen05 convolution and
 // returns the capacity bound on its M tiles (grid sizing), or -1 on failure.
@@ -205,7 +210,7 @@ int prepare_tc(int mode, ConvArgs &a, const lasnet_block_desc *d, const void *x,
                const void *h2, int cap) {
     const int S = d->s, hs = S + 2, C = d->c_mid;
     const uint64_t px = (uint64_t)d->n * d->h * d->w;
-    bool ok = tmap2(&a.tmap_b, a.w, a.K, a.N, 64, bn_of(a.N));
+    bool ok = tmap2(&a.tmap_b, a.w, a.K, a.N, 64, bn_of(a.N, mode));
     switch (mode) {
         case CONV1_DYN: {
             // A = halo rows gathered by cp.async; h1 stored channel-chunk-major
