@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
     ap.add_argument("--detail", default=None, help="write per-kernel detail JSON here")
+    ap.add_argument("--graph", type=int, default=1, help="1: time CUDA-graph replays of the step (captured once on "
+                                                          "the same buffers), 0: eager launches")
     ap.add_argument("--schedule", default="auto", choices=["auto", "separate", "fused"],
                     help="separate: north-star branch (masker, then gather+conv1 on halos); fused: the paper's "
                          "Table-1 schedule (masker fused into a static conv1); auto: lasnet_choose_schedule(r)")
@@ -342,17 +344,22 @@ def run_lasnet(args):
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = blk.launches
+    step_fn = lambda: blk.forward(y)  # noqa: E731
+    n_launch = len(names)
+    if args.graph:
+        graph = blk.capture(y)
+        step_fn = graph.replay
     # headline: CUDA events around each step only (per-kernel events would
     # serialise the programmatic-dependent launches between the kernels)
     for k in range(K):
         prep()
         ev_step[k][0].record(stream)
-        blk.forward(y)
+        step_fn()
         ev_step[k][1].record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    launches = blk.launches - launches0
+    launches = blk.launches - launches0 if not args.graph else n_launch * K
     step_ms = [a.elapsed_time(b) for a, b in ev_step]
     tot_ms = sum(step_ms)
     # breakdown pass (same steps, not the headline): events around every kernel
@@ -437,6 +444,7 @@ def run_lasnet(args):
                        "H": h, "W": w, "c_in": c_in, "c_mid": c_mid, "S": s, "r_target": wl["r"],
                        "r_patch": round(stats["r_patch"], 4), "r_pixel": round(stats["r_pixel"], 4),
                        "parallelism": f"dp{world}", "l2": "flushed (256 MiB read) before every timed step",
+                       "launch": "CUDA graph replay" if args.graph else "eager (one launch per kernel, PDL)",
                        "schedule": sched_name},
             "latency_ms": {"p10": round(float(np.percentile(step_ms, 10)), 4),
                            "p50": round(float(np.percentile(step_ms, 50)), 4),

@@ -258,6 +258,22 @@ class DynBlock:
 
     __call__ = forward
 
+    def capture(self, x: torch.Tensor, y: torch.Tensor | None = None, warmup: int = 2) -> torch.cuda.CUDAGraph:
+        """Capture one forward on these exact buffers into a CUDA graph (the TMA
+        descriptors are kernel parameters, so the graph is bound to x / y and the
+        block's workspaces; re-capture if they change).  Replaying the graph runs
+        the same kernels with one launch call instead of one per kernel."""
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(warmup):  # first calls set kernel attributes outside the capture
+                self.forward(x, y)
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.forward(x, y)
+        return g
+
     def dense(self, x: torch.Tensor, y: torch.Tensor):
         lib = _lib.load()
         if self._dense_ws is None:

@@ -105,8 +105,16 @@ __device__ __forceinline__ int tile_pixel(const ConvArgs &args, int tile, int r,
     return out_pixel(args, tile * rows_per_tile + r, M);
 }
 
-template <bool DENSE, int CL>
+// PAIR (CL == 2): the two CTAs of a cluster run conv2 and conv3 as 2-SM UMMAs
+// (tcgen05.mma.cta_group::2, M = 256): each CTA stages its own 128 A rows but only
+// HALF of every W2 / W3 K-block (the pair shares them), so per output row the
+// weight bytes written to and read from shared memory halve.  The even CTA
+// issues the MMAs; both CTAs' TMA loads complete on its barriers; its commits
+// multicast to both CTAs' barriers; both CTAs' epilogues drain their own TMEM
+// rows and arrive on its barriers (cluster scope).
+template <bool DENSE, int CL, bool PAIR = false>
 __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_constant__ ConvArgs args) {
+    static_assert(!PAIR || CL == 2, "a 2-SM pair is a cluster of 2");
     using namespace c23;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t sbase = smem_u32(smem_raw);
@@ -129,25 +137,27 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int rank = CL > 1 ? (int)cluster_ctarank() : 0;
     constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
+    constexpr int kPeers = PAIR ? 2 : 1;  // CTAs whose epilogues arrive on the MMA-side barriers
+    const bool lead = !PAIR || rank == 0;
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(bar_full + 8 * s, 1);
-            mbar_init(bar_empty + 8 * s, CL);  // the MMA commits of all CL CTAs
+            mbar_init(bar_empty + 8 * s, PAIR ? 1 : CL);  // the MMA commits of all CL CTAs (pair: the lead's)
         }
         for (int s = 0; s < kStages3; ++s) {
             mbar_init(bar_full3 + 8 * s, 1);
-            mbar_init(bar_empty3 + 8 * s, CL);
+            mbar_init(bar_empty3 + 8 * s, PAIR ? 1 : CL);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(bar_t2full + 8 * a, 1);
-            mbar_init(bar_t2empty + 8 * a, 128);
+            mbar_init(bar_t2empty + 8 * a, 128 * kPeers);
         }
         for (int a = 0; a < kAcc3; ++a) {
             mbar_init(bar_t3full + 8 * a, 1);
-            mbar_init(bar_t3empty + 8 * a, 256);
+            mbar_init(bar_t3empty + 8 * a, 256 * kPeers);
         }
         for (int a = 0; a < 2; ++a) {
-            mbar_init(bar_h2full + 8 * a, 128);
+            mbar_init(bar_h2full + 8 * a, 128 * kPeers);
             mbar_init(bar_h2empty + 8 * a, 1);
         }
         fence_mbar_init();
@@ -157,7 +167,10 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
         tma_prefetch_desc(&args.tmap_b);
         tma_prefetch_desc(&args.tmap_b3);
     }
-    if (warp == kMmaWarp) tmem_alloc<512>(smem_u32(tmem_slot));
+    if (warp == kMmaWarp) {
+        if (PAIR) tmem_alloc_pair<512>(smem_u32(tmem_slot));
+        else tmem_alloc<512>(smem_u32(tmem_slot));
+    }
     for (int c = tid; c < args.N; c += kThreads) b2_s[c] = args.bias[c];
     for (int c = tid; c < args.n3; c += kThreads) b3_s[c] = args.bias3[c];
     tc_fence_before();
@@ -214,13 +227,20 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
                     const int st = it % kStages;
                     mbar_wait(bar_empty + 8 * st, ((it / kStages) & 1) ^ 1);
                     const uint32_t sa = sbase + st * kStageBytes, fb = bar_full + 8 * st;
+                    const int tap = kb / kpt, dy = tap / 3, dx = tap - dy * 3, c0 = (kb - tap * kpt) * kBK;
+                    if (PAIR) {  // own A rows + own half of the W2 K-block; both complete on the lead's barrier
+                        if (lead) mbar_arrive_expect_tx(fb, 2 * (args.box_rows * 128 + (KC / 2) * 128));
+                        tma_load_2d_pair(sa + kABytes, &args.tmap_b, fb, kb * kBK, rank * (KC / 2));
+                        if (DENSE) tma_load_5d_pair(sa, &args.tmap_a, fb, 0, dx - 1, y0 + dy - 1, n0, c0 >> 6);
+                        else tma_load_5d_pair(sa, &args.tmap_a, fb, 0, dx, dy, tile * args.units_per_tile, c0 >> 6);
+                        continue;
+                    }
                     mbar_arrive_expect_tx(fb, args.box_rows * 128 + KC * 128);
                     if (CL > 1)  // this CTA's 1/CL of the W2 K-block, into every CTA of the cluster
                         tma_load_2d_mc(sa + kABytes + rank * (KC / CL) * 128, &args.tmap_b, fb, kb * kBK,
                                        rank * (KC / CL), kMask);
                     else
                         tma_load_2d(sa + kABytes, &args.tmap_b, fb, kb * kBK, 0);
-                    const int tap = kb / kpt, dy = tap / 3, dx = tap - dy * 3, c0 = (kb - tap * kpt) * kBK;
                     // h1 is channel-chunk-major: [c_mid/64][P][S+2][S+2][64] (dense: [c_mid/64][N][H][W][64])
                     if (DENSE) tma_load_5d(sa, &args.tmap_a, fb, 0, dx - 1, y0 + dy - 1, n0, c0 >> 6);
                     else tma_load_5d(sa, &args.tmap_a, fb, 0, dx, dy, tile * args.units_per_tile, c0 >> 6);
@@ -239,6 +259,12 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
                         mbar_wait(bar_empty3 + 8 * st, ((it / kStages3) & 1) ^ 1);
                         if (kb == 0) T23C(i * nch + nc, 0);
                         const uint32_t fb = bar_full3 + 8 * st;
+                        if (PAIR) {
+                            if (lead) mbar_arrive_expect_tx(fb, NC3 * 128);  // both halves
+                            tma_load_2d_pair(sbase + kRing3Off + st * kB3Bytes, &args.tmap_b3, fb, kb * kBK,
+                                             nc * NC3 + rank * (NC3 / 2));
+                            continue;
+                        }
                         mbar_arrive_expect_tx(fb, NC3 * 128);
                         if (CL > 1)
                             tma_load_2d_mc(sbase + kRing3Off + st * kB3Bytes + rank * (NC3 / CL) * 128, &args.tmap_b3,
@@ -249,12 +275,13 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
         }
     } else if (warp == kMmaWarp) {
         // ---------------------------------------------- conv2 MMA issuer --
-        if (lane == 0) {
-            const uint32_t idesc2 = idesc_bf16_f32(kBM, KC);
+        if (lane == 0 && lead) {
+            const uint32_t idesc2 = idesc_bf16_f32(PAIR ? 2 * kBM : kBM, KC);
             int it = 0;
             for (int i = 0; i < ntl; ++i) {
                 const int acc = i & 1;
-                mbar_wait(bar_t2empty + 8 * acc, ((i >> 1) & 1) ^ 1);
+                if (PAIR) mbar_wait_cluster(bar_t2empty + 8 * acc, ((i >> 1) & 1) ^ 1);
+                else mbar_wait(bar_t2empty + 8 * acc, ((i >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + acc * KC;
                 for (int kb = 0; kb < kb2; ++kb, ++it) {
@@ -264,27 +291,35 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
                     const uint32_t sa = sbase + st * kStageBytes;
                     const uint64_t ad = smem_desc_sw128(sa), bd = smem_desc_sw128(sa + kABytes);
 #pragma unroll
-                    for (int kk = 0; kk < kBK / 16; ++kk) mma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc2, (kb | kk) != 0);
-                    if (CL > 1) mma_commit_mc(bar_empty + 8 * st, kMask);
+                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                        if (PAIR) mma_bf16_pair(d, ad + 2 * kk, bd + 2 * kk, idesc2, (kb | kk) != 0);
+                        else mma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc2, (kb | kk) != 0);
+                    }
+                    if (PAIR) mma_commit_pair_mc(bar_empty + 8 * st, 3);
+                    else if (CL > 1) mma_commit_mc(bar_empty + 8 * st, kMask);
                     else mma_commit(bar_empty + 8 * st);
                 }
-                mma_commit(bar_t2full + 8 * acc);
+                if (PAIR) mma_commit_pair_mc(bar_t2full + 8 * acc, 3);
+                else mma_commit(bar_t2full + 8 * acc);
             }
         }
         __syncwarp();
     } else if (warp == kMma3Warp) {
         // ---------------------------------------------- conv3 MMA issuer --
-        if (lane == 0) {
-            const uint32_t idesc3 = idesc_bf16_f32(kBM, NC3);
+        if (lane == 0 && lead) {
+            const uint32_t idesc3 = idesc_bf16_f32(PAIR ? 2 * kBM : kBM, NC3);
             int it = 0, c3 = 0;
             for (int i = 0; i < ntl; ++i) {
                 const int hb = i % kH2Bufs;
                 const uint32_t h2b = h2s + hb * 2 * kChunkBytes;
-                mbar_wait(bar_h2full + 8 * hb, (i / kH2Bufs) & 1);  // H2 of tile i staged by epi2
+                // H2 of tile i staged by epi2 (pair: both CTAs')
+                if (PAIR) mbar_wait_cluster(bar_h2full + 8 * hb, (i / kH2Bufs) & 1);
+                else mbar_wait(bar_h2full + 8 * hb, (i / kH2Bufs) & 1);
                 tc_fence_after();
                 for (int nc = 0; nc < nch; ++nc, ++c3) {
                     const int buf = c3 % kAcc3;
-                    mbar_wait(bar_t3empty + 8 * buf, ((c3 / kAcc3) & 1) ^ 1);
+                    if (PAIR) mbar_wait_cluster(bar_t3empty + 8 * buf, ((c3 / kAcc3) & 1) ^ 1);
+                    else mbar_wait(bar_t3empty + 8 * buf, ((c3 / kAcc3) & 1) ^ 1);
                     T23C(c3, 1);
                     tc_fence_after();
                     const uint32_t d = tmem_base + acc3_col + buf * kNC3;  // kNC3 columns per buffer
@@ -296,15 +331,21 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
                         const uint64_t ad = smem_desc_sw128(h2b + kb * kChunkBytes);
                         const uint64_t bd = smem_desc_sw128(sbase + kRing3Off + st * kB3Bytes);
 #pragma unroll
-                        for (int kk = 0; kk < kBK / 16; ++kk)
-                            mma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc3, (kb | kk) != 0);
-                        if (CL > 1) mma_commit_mc(bar_empty3 + 8 * st, kMask);
+                        for (int kk = 0; kk < kBK / 16; ++kk) {
+                            if (PAIR) mma_bf16_pair(d, ad + 2 * kk, bd + 2 * kk, idesc3, (kb | kk) != 0);
+                            else mma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc3, (kb | kk) != 0);
+                        }
+                        if (PAIR) mma_commit_pair_mc(bar_empty3 + 8 * st, 3);
+                        else if (CL > 1) mma_commit_mc(bar_empty3 + 8 * st, kMask);
                         else mma_commit(bar_empty3 + 8 * st);
                     }
-                    mma_commit(bar_t3full + 8 * buf);
+                    if (PAIR) mma_commit_pair_mc(bar_t3full + 8 * buf, 3);
+                    else mma_commit(bar_t3full + 8 * buf);
                     T23C(c3, 3);
                 }
-                mma_commit(bar_h2empty + 8 * hb);  // buffer reusable once these MMAs have read it
+                // buffer reusable once these MMAs have read it
+                if (PAIR) mma_commit_pair_mc(bar_h2empty + 8 * hb, 3);
+                else mma_commit(bar_h2empty + 8 * hb);
                 T23(i, 3);
             }
         }
@@ -341,9 +382,14 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
                 }
             }
             tc_fence_before();
-            mbar_arrive(bar_t2empty + 8 * acc);
             fence_proxy_async_smem();  // generic smem writes -> visible to tcgen05.mma
-            mbar_arrive(bar_h2full + 8 * (i % kH2Bufs));
+            if (PAIR) {  // the lead CTA's MMA waits for both CTAs
+                mbar_arrive_cluster(bar_t2empty + 8 * acc, 0);
+                mbar_arrive_cluster(bar_h2full + 8 * (i % kH2Bufs), 0);
+            } else {
+                mbar_arrive(bar_t2empty + 8 * acc);
+                mbar_arrive(bar_h2full + 8 * (i % kH2Bufs));
+            }
             if (r == 0) T23(i, 2);
         }
     } else if (warp >= kEpi3Warp0 && warp < kProdWarp) {
@@ -425,7 +471,9 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
                 if (warp == kEpi3Warp0 && lane == 0) T23C(sc, 7);
                 if (part == spc - 1) {
                     tc_fence_before();
-                    mbar_arrive(bar_t3empty + 8 * buf);  // accumulator drained into registers
+                    // accumulator drained into registers
+                    if (PAIR) mbar_arrive_cluster(bar_t3empty + 8 * buf, 0);
+                    else mbar_arrive(bar_t3empty + 8 * buf);
                 }
                 // all smem loads first (smem latency is long under UMMA/TMA traffic), then math, then stores
                 uint32_t rv[4][4];
@@ -482,7 +530,8 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
     else __syncthreads();
     if (warp == kMmaWarp) {
         tc_fence_after();
-        tmem_dealloc<512>(tmem_base);
+        if (PAIR) tmem_dealloc_pair<512>(tmem_base);
+        else tmem_dealloc<512>(tmem_base);
     }
 }
 
@@ -500,12 +549,12 @@ extern "C" int lasnet_trace23c_read(unsigned long long *h) {
 }
 #endif
 
-template <bool DENSE, int CL>
+template <bool DENSE, int CL, bool PAIR = false>
 static cudaError_t launch23(const ConvArgs &a, int max_tiles, int num_sms, cudaStream_t st) {
     const int smem = c23::smem_bytes(a.N, a.n3);
     static int cfg = 0;
     if (smem > cfg) {
-        cudaError_t e = cudaFuncSetAttribute(conv23_kernel<DENSE, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(conv23_kernel<DENSE, CL, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         cfg = smem;
     }
@@ -513,7 +562,7 @@ static cudaError_t launch23(const ConvArgs &a, int max_tiles, int num_sms, cudaS
     const int want = (max_tiles + CL - 1) / CL * CL;
     const int cap = num_sms / CL * CL;
     const int grid = want < cap ? (want > 0 ? want : CL) : cap;
-    return launch_k_cluster(conv23_kernel<DENSE, CL>, dim3(grid), dim3(c23::kThreads), smem, st, CL, a);
+    return launch_k_cluster(conv23_kernel<DENSE, CL, PAIR>, dim3(grid), dim3(c23::kThreads), smem, st, CL, a);
 }
 
 // a.cluster: CTAs per cluster sharing the weight loads (1, 2 or 4; the tensor maps'
@@ -521,6 +570,7 @@ static cudaError_t launch23(const ConvArgs &a, int max_tiles, int num_sms, cudaS
 cudaError_t launch_conv23(bool dense, const ConvArgs &a, int max_tiles, int num_sms, cudaStream_t st) {
     if (!(a.N == 64 || a.N == 128) || a.n3 % 64 != 0 || a.n3 > c23::kMaxCout || a.n3 < 64 * (c23::kResBufs - 1))
         return cudaErrorInvalidValue;
+    if (a.pair) return dense ? launch23<true, 2, true>(a, max_tiles, num_sms, st) : launch23<false, 2, true>(a, max_tiles, num_sms, st);
     switch (a.cluster) {
         case 1: return dense ? launch23<true, 1>(a, max_tiles, num_sms, st) : launch23<false, 1>(a, max_tiles, num_sms, st);
         case 2: return dense ? launch23<true, 2>(a, max_tiles, num_sms, st) : launch23<false, 2>(a, max_tiles, num_sms, st);

@@ -286,7 +286,13 @@ cudaError_t run_conv23(const lasnet_block_desc *d, bool dense, ConvArgs a, const
         return (v == 1 || v == 2 || v == 4) ? v : 1;
     }();
     const int nc3 = d->c_out % 128 == 0 ? 128 : 64;  // conv3 MMA N
-    a.cluster = (C / cl_env >= 8 && nc3 / cl_env >= 8) ? cl_env : 1;
+    // 2-SM pair (LASNET_C23_PAIR=1): weight boxes of half height, cluster of 2
+    static const bool pair_env = [] {
+        const char *e = getenv("LASNET_C23_PAIR");
+        return e && e[0] == '1';
+    }();
+    a.pair = pair_env ? 1 : 0;
+    a.cluster = a.pair ? 2 : (C / cl_env >= 8 && nc3 / cl_env >= 8) ? cl_env : 1;
     bool ok = tmap2(&a.tmap_b, a.w, a.K, a.N, 64, C / a.cluster) && tmap2(&a.tmap_b3, w->w3, C, d->c_out, 64, nc3 / a.cluster);
     int tiles;
     if (dense) {

@@ -408,3 +408,27 @@ def test_full_size_config2_fused_sampled(s):
             assert np.array_equal(yc[i, yy, xx], xd[i, yy, xx])
     assert active > 20
     assert worst <= BF16_TOL
+
+
+@pytest.mark.parametrize("sched", [None, L.SCHED_FUSED])
+def test_cuda_graph_replay_equals_eager(sched):
+    """The block captured in a CUDA graph (bench.py's timed path) gives the same
+    bytes as eager launches: mask, idx, count and y."""
+    n, h, w, c_in, c_mid, s = 4, 28, 28, 512, 128, 4
+    x, wts, wm = make_case(n, h, w, c_in, c_mid, s, seed=77)
+    blk = L.DynBlock(L.BlockShape(n, h, w, c_in, c_mid, s), wts, wm, 0.0, schedule=sched)
+    blk.calibrate_bias(synth.make_x(n, h, w, c_in, seed=78).cuda(), 0.5)
+    xg = x.cuda()
+    y_e = xg.clone()
+    blk.forward(y_e)
+    m_e, c_e = blk.mask_buf.clone(), int(blk.count.item())
+    idx_e = blk.idx[:c_e].clone()
+    y_g = xg.clone()
+    g = blk.capture(y_g, warmup=0)
+    y_g.copy_(xg)
+    blk.mask_buf.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(blk.mask_buf, m_e) and int(blk.count.item()) == c_e
+    assert torch.equal(blk.idx[:c_e], idx_e)
+    assert torch.equal(y_g, y_e)
