@@ -338,17 +338,24 @@ def run_lasnet(args):
             e.record(stream)  # materialise the cudaEvent_t handles
     handles = [ctypes_array(row) for row in ev_k]
 
+    step_fn = lambda: blk.forward(y)  # noqa: E731
+    l0 = blk.launches
+    prep()
+    blk.forward(y)  # one eager step: the kernels one step launches (a graph replays exactly these)
+    n_launch = blk.launches - l0
+    if args.graph:
+        graph = blk.capture(y)
+        step_fn = graph.replay
+        for _ in range(2):
+            prep()
+            step_fn()
+
     sampler = ClockSampler(local)
     sampler.start()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = blk.launches
-    step_fn = lambda: blk.forward(y)  # noqa: E731
-    n_launch = len(names)
-    if args.graph:
-        graph = blk.capture(y)
-        step_fn = graph.replay
     # headline: CUDA events around each step only (per-kernel events would
     # serialise the programmatic-dependent launches between the kernels)
     for k in range(K):
