@@ -74,13 +74,13 @@ constexpr int kB3Bytes = kNC3 * 128;
 // smem layout (offsets from the 1024-aligned base); biases are read through L1
 constexpr int kStagesOff = 0;
 constexpr int kH2Off = kStages * kStageBytes;                 // 2 x up to 32 KB (c_mid <= 128), double-buffered
-constexpr int kResBufs = 4;  // residual prefetched kResBufs-1 64-column chunks ahead (epi3 waits on its HBM latency)
+constexpr int kResBufs = 3;  // residual prefetched kResBufs-1 64-column chunks ahead (epi3 waits on its HBM latency)
 constexpr int kResOff = kH2Off + kH2Bufs * 2 * kChunkBytes;   // kResBufs x 16 KB (one 64-col chunk)
 constexpr int kRing3Off = kResOff + kResBufs * kChunkBytes;
 constexpr int kBiasOff = kRing3Off + kStages3 * kB3Bytes;     // b2 (<= 128 floats), b3 (<= 2048 floats)
 constexpr int kMaxCout = 512;
 constexpr int kBarOff = kBiasOff + (128 + kMaxCout) * 4;      // barriers
-constexpr int smem_bytes(int, int) { return kBarOff + 256; }  // dynamic smem base is 1024-aligned (checked)
+constexpr int smem_bytes(int, int) { return 1024 + kBarOff + 256; }  // + 1 KB to round the dynamic smem base up to 1 KB
 }  // namespace c23
 
 // output pixel of row r of a conv23 tile (or -1): patch rows in dynamic mode, image rows dense
@@ -116,10 +116,10 @@ template <bool DENSE, int CL, bool PAIR = false>
 __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_constant__ ConvArgs args) {
     static_assert(!PAIR || CL == 2, "a 2-SM pair is a cluster of 2");
     using namespace c23;
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    const uint32_t sbase = smem_u32(smem_raw);
-    if (sbase & 1023u) __trap();  // the 128-B swizzle atoms need a 1024-B aligned base
-    uint8_t *sgen = smem_raw;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_u32 = smem_u32(smem_raw);
+    const uint32_t sbase = (raw_u32 + 1023u) & ~1023u;  // 128-B swizzle atoms need a 1 KB aligned base
+    uint8_t *sgen = smem_raw + (sbase - raw_u32);
     const uint32_t h2s = sbase + kH2Off;
     const uint32_t bar = sbase + kBarOff;
     const uint32_t bar_full = bar, bar_empty = bar + 8 * kStages;

@@ -100,8 +100,9 @@ template <int MODE, int BN> struct Cfg {
     static constexpr int kBiasOff = kBarOff + 256;
     // bias [n] then (masker) wm [k]
     static constexpr bool kWmSmem = kMasker;
-    // the dynamic smem base is 1024-B aligned (checked in the kernel): no alignment slack
-    static constexpr int smem_bytes(int n, int k) { return kBiasOff + n * 4 + (kWmSmem ? k * 4 : 0); }
+    // + 1 KB: the dynamic smem base is only guaranteed 16-B aligned (a CTA co-resident
+    // with another kernel's CTA may start anywhere); the kernel rounds it up to 1 KB
+    static constexpr int smem_bytes(int n, int k) { return 1024 + kBiasOff + n * 4 + (kWmSmem ? k * 4 : 0); }
 };
 
 template <int MODE, int BN> __host__ __device__ constexpr int threads_of() { return Cfg<MODE, BN>::kThreads; }
@@ -145,10 +146,10 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
     using C = Cfg<MODE, BN>;
     constexpr int ST = C::kStages, NSTG = C::kStaging, EPI = C::kEpiWarps * 32;
     constexpr bool kResid = C::kResid;
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    const uint32_t sbase = smem_u32(smem_raw);
-    if (sbase & 1023u) __trap();  // the 128-B swizzle atoms need a 1024-B aligned base
-    uint8_t *sgen = smem_raw;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_u32 = smem_u32(smem_raw);
+    const uint32_t sbase = (raw_u32 + 1023u) & ~1023u;  // 128-B swizzle atoms need a 1 KB aligned base
+    uint8_t *sgen = smem_raw + (sbase - raw_u32);
 
     const uint32_t staging = sbase + C::kStagingOff;  // NSTG x kStagingBytes
     const uint32_t bar_full = sbase + C::kBarOff;     // ST
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
         for (int s = 0; s < ST; ++s) {
             // TMA producer's arrive.expect_tx (+ one noinc arrival per gather thread for conv1 dyn)
             mbar_init(bar_full + 8 * s, C::kGather ? C::kGatherThreads + 1 : 1);
-            mbar_init(bar_empty + 8 * s, C::kMasker ? 1 + 4 : 1);  // tcgen05.commit (+ the 4 masker warps of its K parity)
+            mbar_init(bar_empty + 8 * s, C::kMasker ? 1 + C::kMaskerThreads / 32 : 1);  // tcgen05.commit (+ every masker warp)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(bar_tfull + 8 * a, 1);     // tcgen05.commit
@@ -302,53 +303,55 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
         }
     } else if (C::kMasker && warp >= C::kMaskerWarp0) {
         // -------------------------------------- masker partials (fused) --
-        // 8 warps: warp w owns A rows (w & 3) * 32 + lane (thread = pixel) and the
-        // K-blocks of parity w >> 2.  It reads the 8 16-B chunks of its 128-B
-        // swizzled row of each of its K-blocks (conflict-free: 8 consecutive rows
-        // cover all 32 banks) while the MMA consumes the same stage, and keeps fp32
-        // FFMA sums: the partial a = sum_c wm_c x[p,c] over its channels and the
-        // magnitude m = sum_c |wm_c x[p,c]|, two independent chains each.  Every
-        // channel term passes through at most c_in/8 + 8 fp32 roundings, which
+        // 8 warps, two threads per A row (pixel): thread 2r + h reads the 16-B chunks
+        // 4h .. 4h+3 of row r's 128-B swizzled row of EVERY K-block (a quarter-warp
+        // = 4 rows x 2 halves touches 8 distinct chunk slots: conflict-free) while
+        // the MMA consumes the same stage.  Every masker warp waits on every stage,
+        // so the mbarrier parity it waits for is always the current one whatever
+        // the stage count (a K-block split by parity would skip phases when the
+        // stage count is odd and read a stage before it is refilled).  fp32 FFMA
+        // sums: the partial a = sum_c wm_c x[p,c] over its half of the channels and
+        // the magnitude m = sum_c |wm_c x[p,c]|, two chains each; every channel
+        // term passes through at most c_in/16 + 10 fp32 roundings, which
         // decide_gather.cu's certified bound accounts for.  Fixed channel order.
-        const int mw = warp - C::kMaskerWarp0;
-        const int r = (mw & 3) * 32 + lane, par = mw >> 2;
-        int base = 0;
-        for (int tile = blockIdx.x; tile < geo.num_tiles; tile += gridDim.x, base += num_kb) {
+        const int mt = tid - 32 * C::kMaskerWarp0;
+        const int r = mt >> 1, h = mt & 1;
+        int it = 0;
+        for (int tile = blockIdx.x; tile < geo.num_tiles; tile += gridDim.x) {
             float acc0 = 0.f, acc1 = 0.f, mag0 = 0.f, mag1 = 0.f;
-            for (int kb = par; kb < num_kb; kb += 2) {
-                const int it = base + kb;
+            for (int kb = 0; kb < num_kb; ++kb, ++it) {
                 const int stage = it % ST;
                 mbar_wait(bar_full + 8 * stage, (it / ST) & 1);
                 const uint32_t row = sbase + C::kStageOff + stage * C::kStageBytes + r * 128;
-                uint32_t q[8][4];
+                uint32_t q[4][4];
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
+                for (int jj = 0; jj < 4; ++jj)
                     asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
-                                 : "=r"(q[j][0]), "=r"(q[j][1]), "=r"(q[j][2]), "=r"(q[j][3])
-                                 : "r"(row + ((j ^ (r & 7)) << 4)));
+                                 : "=r"(q[jj][0]), "=r"(q[jj][1]), "=r"(q[jj][2]), "=r"(q[jj][3])
+                                 : "r"(row + (((4 * h + jj) ^ (r & 7)) << 4)));
                 __syncwarp();
                 if (lane == 0) mbar_arrive(bar_empty + 8 * stage);  // this warp's reads are done
-                const float4 *w4 = reinterpret_cast<const float4 *>(wm_s + kb * kBK);
+                const float4 *w4 = reinterpret_cast<const float4 *>(wm_s + kb * kBK + 32 * h);
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const float4 wa = C::kWmSmem ? w4[2 * j] : __ldg(w4 + 2 * j);
-                    const float4 wb = C::kWmSmem ? w4[2 * j + 1] : __ldg(w4 + 2 * j + 1);
+                for (int jj = 0; jj < 4; ++jj) {
+                    const float4 wa = C::kWmSmem ? w4[2 * jj] : __ldg(w4 + 2 * jj);
+                    const float4 wb = C::kWmSmem ? w4[2 * jj + 1] : __ldg(w4 + 2 * jj + 1);
                     const float wv[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
                     float cs = 0.f, ms = 0.f;
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const float lo = bf16lo(q[j][e]), hi = bf16hi(q[j][e]);
+                        const float lo = bf16lo(q[jj][e]), hi = bf16hi(q[jj][e]);
                         cs = fmaf(wv[2 * e], lo, cs);
                         cs = fmaf(wv[2 * e + 1], hi, cs);
                         ms = fmaf(fabsf(wv[2 * e]), fabsf(lo), ms);
                         ms = fmaf(fabsf(wv[2 * e + 1]), fabsf(hi), ms);
                     }
-                    if (j & 1) { acc1 += cs; mag1 += ms; } else { acc0 += cs; mag0 += ms; }
+                    if (jj & 1) { acc1 += cs; mag1 += ms; } else { acc0 += cs; mag0 += ms; }
                 }
             }
             const int m = (tile / geo.n_tiles_n) * kBM + r;
             if (tile % geo.n_tiles_n == 0 && m < args.m_dense)
-                reinterpret_cast<float2 *>(args.mpart)[2 * m + par] = make_float2(acc0 + acc1, mag0 + mag1);
+                reinterpret_cast<float2 *>(args.mpart)[2 * m + h] = make_float2(acc0 + acc1, mag0 + mag1);
         }
     } else if (warp == C::kMmaWarp) {
         // ---------------------------------------------------- MMA issuer --

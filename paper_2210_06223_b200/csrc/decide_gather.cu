@@ -4,15 +4,15 @@
 // The paper's best schedule (Table 1; sec. 3.4; App. B
 // P:556-565) fuses the masker into a STATIC conv1: conv1 runs on every pixel and
 // the masker's pooled 1x1 conv rides along.  Here the dense conv1 kernel
-// (conv_tc.cu, CONV1_DENSE_MASK) leaves per pixel p, for the channels of the
-// even (h = 0) and of the odd (h = 1) 64-channel K-blocks, the fp32 partials
+// (conv_tc.cu, CONV1_DENSE_MASK) leaves per pixel p, for the lower (h = 0) and the
+// upper (h = 1) 32 channels of every 64-channel K-block, the fp32 partials
 //   a_ph = sum_c wm_c x[p,c]   and   m_ph = sum_c |wm_c x[p,c]|,
 // and two launches finish steps 1-2 and the gather:
 //   (a) decides each cell (P:109 avg-pool + 1x1 conv, P:562 sign form):
 //       z = sum_{p in Omega} (a_p0 + a_p1) + bm*|Omega| in fp64.  With gamma_n =
 //       n u/(1-n u) (Higham, recursive summation): every channel term of a_ph
-//       passes through at most 8 (FFMA chain of its 16-B chunk) + c_in/16 (chunk
-//       sums) + 2 fp32 roundings, and through at most 2|Omega| + 4 fp64 additions
+//       passes through at most 8 (FFMA chain of its 16-B chunk) + c_in/32 (chunk
+//       sums into two chains) + 2 fp32 roundings (the bound uses c_in/16 + 10), and through at most 2|Omega| + 4 fp64 additions
 //       here, so |z - z_exact| <= (gamma_{c_in/16+10}(2^-24) + gamma_{2|Omega|+4}(2^-53))
 //       * sum |terms|, and sum |terms| <= 1.01 sum m_ph (the m are fp32 sums of
 //       non-negative terms, relative error < 1e-3 for c_in < 16k).

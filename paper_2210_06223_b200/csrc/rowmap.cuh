@@ -75,9 +75,9 @@ struct ConvArgs {
     int32_t pair;             // fused conv2+conv3: 2-SM UMMAs over CTA pairs (cluster = 2, weight boxes of half height)
     // masker fused into the dense conv1 (CONV1_DENSE_MASK): per pixel p the fp32
     // partial logits sum_c wm_c x[p,c] and magnitudes sum_c |wm_c x[p,c]| over the
-    // channels of the even and of the odd 64-channel K-blocks
+    // lower and the upper 32 channels of every 64-channel K-block
     const float *wm;          // [c_in] reduced masker weight W_0 - W_1
-    float4 *mpart;            // [n*h*w] (partial, magnitude) of the even and of the odd K-blocks
+    float4 *mpart;            // [n*h*w] (partial, magnitude) of the lower and of the upper channel halves
 };
 
 __host__ __device__ __forceinline__ int rows_per_patch(int mode, int S) {

@@ -7,7 +7,7 @@ timeout -s KILL 300 python __graft_entry__.py --smoke > gpurun_out/smoke.log 2>&
 for sch in fused separate; do
   timeout -s KILL 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --schedule $sch > gpurun_out/bench_$sch.json 2> gpurun_out/bench_$sch.err
 done
-LASNET_NO_PDL=1 timeout -s KILL 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --schedule fused > gpurun_out/bench_nopdl.json 2> gpurun_out/bench_nopdl.err
+LASNET_PDL=1 timeout -s KILL 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --schedule fused > gpurun_out/bench_nopdl.json 2> gpurun_out/bench_nopdl.err
 tail -3 gpurun_out/pytest_gpu.log; tail -1 gpurun_out/smoke.log
 for sch in fused separate nopdl; do python - <<PY
 import json

@@ -58,6 +58,55 @@ def timed(fn, prep, steps, warmup):
     return statistics.median(a.elapsed_time(b) for a, b in ev)
 
 
+def chained(args, flush):
+    """Each stage's identity blocks as a real forward: block k's in-place output is
+    block k+1's input, every block with its own weights and masker (bias calibrated
+    in sequence on the activations it actually sees), the whole stage captured in
+    one CUDA graph; median replay time, L2 flushed before each."""
+    res, tot = [], 0.0
+    for si, (h, c_in, c_mid, s, nblk) in enumerate(STAGES):
+        n = args.n
+        x0 = synth.make_x(n, h, h, c_in, seed=10 + si).cuda()
+        y = x0.clone()
+        blks = []
+        for b in range(nblk):
+            wts = synth.make_block_weights(c_in, c_mid, c_in, seed=100 * si + 2 * b + 1)
+            wm = synth.make_masker_weights(c_in, seed=100 * si + 2 * b + 2)
+            sched = L.choose_schedule(n, h, h, c_in, c_mid, c_in, s, args.r)
+            blk = L.DynBlock(L.BlockShape(n, h, h, c_in, c_mid, s), wts, wm, 0.0, schedule=sched)
+            blk.calibrate_bias(y, args.r)  # on this block's actual input
+            blk.forward(y)
+            blks.append(blk)
+        torch.cuda.synchronize()
+        rates = [float(b.mask_buf.float().mean().item()) for b in blks]
+
+        def fwd():
+            for b in blks:
+                b.forward(y)
+
+        y.copy_(x0)
+        for _ in range(2):
+            fwd()
+        y.copy_(x0)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fwd()
+
+        def prep():
+            y.copy_(x0)
+            flush.sum()
+
+        t = timed(g.replay, prep, args.steps, args.warmup)
+        tot += t
+        res.append(dict(h=h, c_in=c_in, c_mid=c_mid, S=s, blocks=nblk, ms=t, r_patch_mean=sum(rates) / len(rates)))
+        print(f"chained stage {h}x{h}x{c_in} x{nblk}: {t * 1e3:.1f} us ({t / nblk * 1e3:.1f} us/block), "
+              f"mean r_patch {res[-1]['r_patch_mean']:.3f}", flush=True)
+        del blks, x0, y, g
+        torch.cuda.empty_cache()
+    print(f"chained identity body: {tot:.3f} ms -> {args.n / (tot * 1e-3):.0f} images/s", flush=True)
+    return dict(stages=res, body_ms=tot, images_per_s=args.n / (tot * 1e-3))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=256)
@@ -66,6 +115,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--schedule", default="auto", choices=["auto", "separate", "fused"])
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "r101_body"))
+    ap.add_argument("--per-block", type=int, default=1, help="time one block per stage (eager) and the dense comparator")
+    ap.add_argument("--chain", type=int, default=1, help="also time each stage's identity blocks chained (block k "
+                                                         "feeds block k+1, own weights and masker per block) as one "
+                                                         "CUDA graph")
     args = ap.parse_args()
     from paper_2210_06223_b200 import build
 
@@ -73,7 +126,7 @@ def main():
     hbm, tfl, _, psrc = bench.peaks()
     flush = torch.ones(32 << 20, dtype=torch.int64, device="cuda")
     rows, dyn_tot, dense_tot, roof_tot = [], 0.0, 0.0, 0.0
-    for h, c_in, c_mid, s, nblk in STAGES:
+    for h, c_in, c_mid, s, nblk in (STAGES if args.per_block else []):
         n = args.n
         x = synth.make_x(n, h, h, c_in, seed=0).cuda()
         wts = synth.make_block_weights(c_in, c_mid, c_in, seed=1)
@@ -110,7 +163,8 @@ def main():
               f"T_roof {t_roof * 1e3:.1f} us ({row['roof_frac']:.2f})", flush=True)
         del x, y, y2, blk
         torch.cuda.empty_cache()
-    out = dict(n=args.n, r=args.r, rows=rows, body_dyn_ms=dyn_tot, body_dense_ms=dense_tot, body_roof_ms=roof_tot,
+    chain = chained(args, flush) if args.chain else None
+    out = dict(n=args.n, r=args.r, rows=rows, chained=chain, body_dyn_ms=dyn_tot, body_dense_ms=dense_tot, body_roof_ms=roof_tot,
                body_images_per_s_dyn=args.n / (dyn_tot * 1e-3), body_images_per_s_dense=args.n / (dense_tot * 1e-3),
                device=torch.cuda.get_device_name(0), peaks=dict(hbm_gbs=hbm, bf16_tflops=tfl, src=psrc))
     print(f"identity body (29 of 33 blocks): dyn {dyn_tot:.3f} ms, dense {dense_tot:.3f} ms, x{dense_tot / dyn_tot:.2f}; "
@@ -132,6 +186,14 @@ def main():
                 f"**{dense_tot / dyn_tot:.2f}** | {roof_tot * 1e3:.0f} | {roof_tot / dyn_tot:.2f} |\n\n"
                 f"Body throughput: {out['body_images_per_s_dyn']:.0f} images/s dynamic vs "
                 f"{out['body_images_per_s_dense']:.0f} images/s dense (identity blocks only).\n")
+        if chain:
+            f.write("\n## Chained forward (block k feeds block k+1, own weights/masker per block, one CUDA graph per "
+                    "stage)\n\n| stage | blocks | time (us) | us/block | mean r_patch |\n|---|---|---|---|---|\n")
+            for c in chain["stages"]:
+                f.write(f"| {c['h']}x{c['h']}x{c['c_in']} | {c['blocks']} | {c['ms'] * 1e3:.1f} | "
+                        f"{c['ms'] / c['blocks'] * 1e3:.1f} | {c['r_patch_mean']:.3f} |\n")
+            f.write(f"| **body** | 29 | **{chain['body_ms'] * 1e3:.0f}** | | |\n\n"
+                    f"Chained identity body: {chain['images_per_s']:.0f} images/s.\n")
 
 
 if __name__ == "__main__":
