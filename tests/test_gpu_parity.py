@@ -466,3 +466,20 @@ def test_fused_schedule_bn256_repeated_graph_replays_stable():
         g.replay()
         torch.cuda.synchronize()
         assert torch.equal(y, ref)
+
+
+@pytest.mark.parametrize("env", ["LASNET_PDL=1", "LASNET_NO_FUSE=1", "LASNET_C23_CLUSTER=2", "LASNET_C23_CLUSTER=4",
+                                 "LASNET_C23_PAIR=1", "LASNET_MASK_MAXITEMS=8"])
+def test_library_variants(env):
+    """The opt-in library variants (read once per process: run in a subprocess)
+    give oracle-exact masks/idx and in-tolerance activations for both schedules
+    and the dense comparator."""
+    import os
+    import subprocess
+    import sys
+
+    k, v = env.split("=")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, os.path.join(here, "variant_check.py")], env=dict(os.environ, **{k: v}),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "variant ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
