@@ -483,3 +483,20 @@ def test_library_variants(env):
     r = subprocess.run([sys.executable, os.path.join(here, "variant_check.py")], env=dict(os.environ, **{k: v}),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "variant ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("sched", [L.SCHED_SEPARATE, L.SCHED_FUSED])
+def test_batch_sharding_is_bitwise_invariant(sched):
+    """images are independent, so running a batch split over two
+    'ranks' (two calls on halves) gives the same bytes as one call on the whole
+    batch -- the data-parallel sharding of bench.py --gpus N changes nothing."""
+    n, h, w, c_in, c_mid, s = 8, 28, 28, 512, 128, 4
+    x, wts, wm = make_case(n, h, w, c_in, c_mid, s, seed=33)
+    xd = synth.to_f64(x)
+    _, l0 = oracle.masker(xd, synth.to_f64(wm), 0.0, s)
+    bm = margin_bias(l0, 0.5)
+    y_all, m_all, _, _ = L.block_forward(x.cuda(), to_dev(wts), wm.cuda(), bm, s, sched)
+    for lo, hi in ((0, 3), (3, 8)):
+        y_p, m_p, _, _ = L.block_forward(x[lo:hi].contiguous().cuda(), to_dev(wts), wm.cuda(), bm, s, sched)
+        assert torch.equal(m_p, m_all[lo:hi])
+        assert torch.equal(y_p, y_all[lo:hi])
