@@ -429,6 +429,15 @@ def run_lasnet(args):
                      "algorithmic": {"bytes": kwork[dom]["bytes"], "flops": kwork[dom]["flops"]},
                      "share_of_step": round(kern_ms[dom] / sum(kern_ms.values()), 3),
                      "timing": "CUDA events around this kernel on its launch stream, breakdown pass"})
+        # every kernel of the step against its own bound (north_star: tensor-pipe work for the convolutions,
+        # achieved HBM GB/s for the mask / gather / scatter kernels)
+        kern_roof = {}
+        for nm in names:
+            e = roofline_entry(kwork[nm], kern_ms[nm], hbm, tfl)
+            e["algorithmic"] = {"bytes": kwork[nm]["bytes"], "flops": kwork[nm]["flops"]}
+            if e["bound"] == "hbm" and kwork[nm]["flops"]:
+                e["tflops"] = round(kwork[nm]["flops"] / (kern_ms[nm] * 1e-3) / 1e12, 1)
+            kern_roof[nm] = e
         blk_roof = roofline_entry(bwork, statistics.fmean(step_ms), hbm, tfl)
         t_roof = max(bwork["bytes"] / (hbm * 1e9), bwork["flops"] / (tfl * 1e12)) * 1e3
         blk_roof.update({"t_roof_ms": round(t_roof, 4), "frac_time": round(t_roof / statistics.fmean(step_ms), 4),
@@ -460,6 +469,7 @@ def run_lasnet(args):
             "dense_ms_per_step": round(dense_max, 4),
             "speedup_vs_dense": round(dense_max / (tot_max / K), 3),
             "roofline": roof,
+            "kernels_roofline": kern_roof,
             "block_roofline": blk_roof,
             "e2e": {"value": round(e2e_val, 1), "unit": "images/s", "h2d_bytes_per_step": x.numel() * 2,
                     "d2h_bytes_per_step": x.numel() * 2},
