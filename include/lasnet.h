@@ -81,7 +81,8 @@ typedef struct {
  *   w1 [c_mid][c_in]            conv1 1x1, K-major
  *   w2 [c_mid][3][3][c_mid]     conv2 3x3, OHWI (K = 9*c_mid, tap-major)
  *   w3 [c_out][c_mid]           conv3 1x1
- *   wd, bd                      downsample projection; must be NULL (stride 1) */
+ *   wd [c_out][c_in], bd [c_out] the 1x1 (stride-s) projection shortcut of lasnet_proj_block;
+ *                               must be NULL for the identity-block calls */
 typedef struct {
     const void *w1; const float *b1;
     const void *w2; const float *b2;
@@ -154,6 +155,23 @@ lasnet_status lasnet_dense_block(const lasnet_block_desc *desc, const lasnet_blo
                                  const void *x, void *y, void *ws, size_t ws_bytes,
                                  lasnet_stream_t stream);
 size_t lasnet_dense_workspace_bytes(const lasnet_block_desc *desc);
+
+/* The projection (first) block of a ResNet stage, static (SURVEY 8(f) NEXT-f1:
+ * the first blocks run dense until their dynamic form is built; the paper's
+ * LASNet keeps the downsampling shortcut dense):
+ *   h1 = ReLU(conv1x1(x) + b1)                  at the input resolution
+ *   h2 = ReLU(conv3x3(h1, stride, pad 1) + b2)  at the output resolution
+ *   y  = ReLU(conv1x1(h2, w3) + b3 + (wd * x_s + bd)),  x_s = x[:, ::stride, ::stride, :]
+ *   desc    h, w are the OUTPUT dims, stride in {1, 2}; s is ignored; bf16 only;
+ *           c_in % 64, c_mid 64 or % 128, c_out % 128, w * stride <= 128
+ *   x       [n][h*stride][w*stride][c_in];  y [n][h][w][c_out] (must not overlap x)
+ *   wts     w1..w3 as above and wd/bd (required)
+ *   ws      lasnet_proj_workspace_bytes(desc) bytes, no contract on contents.
+ * Stride 2 computes the 3x3 at every input pixel and keeps every second row and
+ * column (4x the 3x3 work of a strided kernel; correct, not yet tuned). */
+lasnet_status lasnet_proj_block(const lasnet_block_desc *desc, const lasnet_block_weights *wts, const void *x,
+                                void *y, void *ws, size_t ws_bytes, lasnet_stream_t stream);
+size_t lasnet_proj_workspace_bytes(const lasnet_block_desc *desc);
 
 /* The whole block, steps 1-5, in one call, under one of two schedules.
  *

@@ -11,7 +11,7 @@ bf16/fp32 tensors the GPU sees (bf16 -> fp64 is exact).
 
 Parity status per function:
   masker_2ch, masker, upsample, compact, static_block, dyn_block_def,
-  dyn_block_literal, block_pixel, round_bf16 -- all pinned by tests in
+  dyn_block_literal, block_pixel, round_bf16, proj_block -- all pinned by tests in
   tests/test_oracle_pins.py (library conv2d in fp64, exact rationals, closed
   forms, brute force, textbook routines).  No function is "parity unpinned".
 """
@@ -226,6 +226,43 @@ def block_pixel(x, wts, mask_cells, s, n, yy, xx, rmode=ROUND_BF16):
     active = lib.oracle_block_pixel(xp, h, w, c_in, c_mid, c_out, *wp, mcp, s, rmode,
                                     int(n), int(yy), int(xx), op)
     return out, bool(active)
+
+
+def _round_array(a, rmode):
+    if rmode == ROUND_NONE:
+        return a
+    f = round_bf16 if rmode == ROUND_BF16 else round_f32
+    return np.vectorize(f, otypes=[np.float64])(a)
+
+
+def proj_block(x, wts, stride, rmode=ROUND_BF16):
+    """Static projection (first) block of a ResNet stage, BN folded (the
+    stride-s first block whose shortcut LASNet keeps dense), written out in
+    fp64 numpy with the GPU's storage roundings (h1, h2, the shortcut, y):
+      h1 = rnd(ReLU(x W1^T + b1))                         at the input resolution
+      h2 = rnd(ReLU(sum_{dy,dx} h1p[s*oy+dy, s*ox+dx] W2[:,dy,dx,:]^T + b2)), h1p = h1 zero-padded by 1
+      ds = rnd(x[:, ::s, ::s] Wd^T + bd)                   (no ReLU)
+      y  = rnd(ReLU(h2 W3^T + b3 + ds))
+    x [n][H][W][c_in] (H, W multiples of s) -> y [n][H/s][W/s][c_out]."""
+    x = np.asarray(x, np.float64)
+    n, hi, wi, c_in = x.shape
+    s = int(stride)
+    ho, wo = hi // s, wi // s
+    w1, b1 = np.asarray(wts["w1"], np.float64), np.asarray(wts["b1"], np.float64)
+    w2, b2 = np.asarray(wts["w2"], np.float64), np.asarray(wts["b2"], np.float64)
+    w3, b3 = np.asarray(wts["w3"], np.float64), np.asarray(wts["b3"], np.float64)
+    wd, bd = np.asarray(wts["wd"], np.float64), np.asarray(wts["bd"], np.float64)
+    h1 = _round_array(np.maximum(x @ w1.T + b1, 0.0), rmode)
+    h1p = np.zeros((n, hi + 2, wi + 2, h1.shape[-1]))
+    h1p[:, 1:-1, 1:-1] = h1
+    acc = np.zeros((n, ho, wo, w2.shape[0]))
+    for dy in range(3):
+        for dx in range(3):
+            win = h1p[:, dy:dy + s * ho:s, dx:dx + s * wo:s, :]
+            acc += win @ w2[:, dy, dx, :].T
+    h2 = _round_array(np.maximum(acc + b2, 0.0), rmode)
+    ds = _round_array(x[:, ::s, ::s, :] @ wd.T + bd, rmode)
+    return _round_array(np.maximum(h2 @ w3.T + b3 + ds, 0.0), rmode)
 
 
 def num_threads() -> int:

@@ -24,6 +24,7 @@ EXPORTS = [
     "lasnet_dyn_workspace_bytes", "lasnet_dense_block", "lasnet_dense_workspace_bytes",
     "lasnet_status_str", "lasnet_abi_version", "lasnet_last_launch_count", "lasnet_set_kernel_events",
     "lasnet_block_forward", "lasnet_block_forward_workspace_bytes", "lasnet_choose_schedule",
+    "lasnet_proj_block", "lasnet_proj_workspace_bytes",
 ]
 
 # lasnet_schedule
@@ -84,6 +85,10 @@ def load(path: str = LIB_PATH):
     lib.lasnet_block_forward_workspace_bytes.restype = sz
     lib.lasnet_choose_schedule.argtypes = [D, ctypes.c_double]
     lib.lasnet_choose_schedule.restype = i32
+    lib.lasnet_proj_block.argtypes = [D, Wt, vp, vp, vp, sz, vp]
+    lib.lasnet_proj_block.restype = ctypes.c_int
+    lib.lasnet_proj_workspace_bytes.argtypes = [D]
+    lib.lasnet_proj_workspace_bytes.restype = sz
     lib.lasnet_status_str.argtypes = [ctypes.c_int]
     lib.lasnet_status_str.restype = ctypes.c_char_p
     lib.lasnet_abi_version.restype = i32

@@ -109,6 +109,27 @@ def dense_block(x: torch.Tensor, wts: dict, y: torch.Tensor | None = None, ws: t
     return y
 
 
+def proj_block(x: torch.Tensor, wts: dict, stride: int, ws: torch.Tensor | None = None):
+    """Static projection (first) block of a stage (lasnet_proj_block; NEXT-f1):
+    x [n, h*stride, w*stride, c_in] -> y [n, h, w, c_out] with the 1x1 stride-s
+    shortcut wts["wd"] [c_out][c_in], wts["bd"] [c_out]."""
+    _require_cuda(x)
+    lib = _lib.load()
+    n, hi, wi, c_in = x.shape
+    c_mid, c_out = wts["w1"].shape[0], wts["w3"].shape[0]
+    if hi % stride or wi % stride:
+        raise ValueError("input size must be a multiple of the stride")
+    h, w = hi // stride, wi // stride
+    d = _lib.BlockDesc(n, h, w, c_in, c_mid, c_out, stride, 1, _DT[x.dtype])
+    wsb = lib.lasnet_proj_workspace_bytes(ctypes.byref(d))
+    ws = ws if ws is not None else torch.empty(max(wsb, 1), dtype=torch.uint8, device=x.device)
+    y = torch.empty((n, h, w, c_out), dtype=x.dtype, device=x.device)
+    wt = _lib.BlockWeights(*(wts[k].data_ptr() for k in ("w1", "b1", "w2", "b2", "w3", "b3", "wd", "bd")))
+    _lib.check("lasnet_proj_block", lib.lasnet_proj_block(ctypes.byref(d), ctypes.byref(wt), _p(x), _p(y), _p(ws),
+                                                          ws.numel(), _stream()))
+    return y
+
+
 def block_forward(x: torch.Tensor, wts: dict, wm: torch.Tensor, bm: float, s: int, schedule: int,
                   y: torch.Tensor | None = None, ws: torch.Tensor | None = None, mask_out: bool = True):
     """Steps 1-5 in one C-ABI call (lasnet_block_forward) under `schedule`

@@ -429,8 +429,9 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                 for (int i = 0; i < 32 / kRowsPerIt; ++i) {
                     const int rl = i * kRowsPerIt + lane / kChunks, c16 = lane % kChunks;
                     const int pix = __shfl_sync(0xffffffffu, mypix, rl);
-                    const __nv_bfloat16 *g = pix >= 0 ? X + (size_t)pix * args.out_ld + n0 + c_lo + c16 * 8 : X;
-                    cp_async_16(chunk_addr(buf, rl, c16), g, pix >= 0 ? 16u : 0u);
+                    const bool ok = pix >= 0 && X != nullptr;  // no residual tensor: zero-fill
+                    const __nv_bfloat16 *g = ok ? X + (size_t)pix * args.out_ld + n0 + c_lo + c16 * 8 : Y;
+                    cp_async_16(chunk_addr(buf, rl, c16), g, ok ? 16u : 0u);
                 }
             }
             cp_async_commit();
@@ -493,7 +494,8 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     uint32_t pk[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        float lo = fmaxf(f[2 * e], 0.f), hi = fmaxf(f[2 * e + 1], 0.f);
+                        float lo = f[2 * e], hi = f[2 * e + 1];
+                        if (!args.no_relu) lo = fmaxf(lo, 0.f), hi = fmaxf(hi, 0.f);
                         if (zero) lo = hi = 0.f;
                         pk[e] = pack_bf16x2(lo, hi);
                     }

@@ -25,6 +25,8 @@ cudaError_t launch_mask_compact(int dtype_bf16, const void *x, const float *wm, 
                                 cudaStream_t st);
 cudaError_t launch_conv_tc(int mode, const ConvArgs &a, int max_tiles_m, int num_sms, cudaStream_t st);
 cudaError_t launch_conv_simt(int mode, const ConvArgs &a, int max_rows, cudaStream_t st);
+cudaError_t launch_subsample(const void *in, void *out, int n_img, int Ho, int Wo, int c_bytes, int stride, int num_sms,
+                             cudaStream_t st);
 cudaError_t launch_conv23(bool dense, const ConvArgs &a, int max_tiles, int num_sms, cudaStream_t st);
 size_t decide_sync_bytes(int ncells, int num_sms);
 cudaError_t launch_decide_gather(const float4 *mpart, const void *x, const float *wm, float bm, int n_img, int H,
@@ -396,6 +398,20 @@ size_t fwd_ws(const lasnet_block_desc *d, int schedule, uint8_t *base, FwdWs *o)
     return cv.used;
 }
 
+// Workspace of lasnet_proj_block: h1 and the stride-1 3x3 output at the input
+// resolution, then (stride 2) the subsampled h2 and x, and the shortcut output.
+size_t proj_ws(const lasnet_block_desc *d, uint8_t *base, void **h1, void **h2f, void **h2, void **xs, void **ds) {
+    const size_t e = elt_size(d->dtype);
+    const size_t po = (size_t)d->n * d->h * d->w, pi = po * d->stride * d->stride;
+    Carve cv{base};
+    void *a = cv.take(pi * d->c_mid * e), *b = cv.take(pi * d->c_mid * e);
+    void *c = d->stride > 1 ? cv.take(po * d->c_mid * e) : b;
+    void *xx = d->stride > 1 ? cv.take(po * d->c_in * e) : nullptr;
+    void *dd = cv.take(po * d->c_out * e);
+    if (h1) *h1 = a, *h2f = b, *h2 = c, *xs = xx, *ds = dd;
+    return cv.used;
+}
+
 }  // namespace
 
 extern "C" {
@@ -662,6 +678,87 @@ lasnet_status lasnet_block_forward(const lasnet_block_desc *d, const lasnet_bloc
  * gather of x for conv1 + residual/y; fused: x once + h1 write + gathered-h1
  * read + residual/y.  Tensor time is below the HBM time at every shape the
  * bf16 path supports, so bytes decide. */
+/* Static projection (first) block of a stage (see include/lasnet.h). */
+size_t lasnet_proj_workspace_bytes(const lasnet_block_desc *d) {
+    if (check_desc(d) != LASNET_OK) return 0;
+    return proj_ws(d, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+}
+
+lasnet_status lasnet_proj_block(const lasnet_block_desc *d, const lasnet_block_weights *w, const void *x, void *y,
+                                void *ws, size_t ws_bytes, lasnet_stream_t stream) {
+    lasnet_status s = check_desc(d);
+    if (s != LASNET_OK) return s;
+    if (!w || !w->w1 || !w->b1 || !w->w2 || !w->b2 || !w->w3 || !w->b3 || !w->wd || !w->bd) return LASNET_ERR_NULL;
+    if (!x || !y) return LASNET_ERR_NULL;
+    if (d->dtype != LASNET_BF16) return LASNET_ERR_UNSUPPORTED;  // tcgen05 path only
+    if (d->c_in % 64 || d->c_mid % 64 || d->c_out % 128 || d->c_out > 2048 || d->c_mid > 2048)
+        return LASNET_ERR_UNSUPPORTED;
+    if (d->c_mid != 64 && d->c_mid % 128) return LASNET_ERR_UNSUPPORTED;
+    if (d->w * d->stride > 128) return LASNET_ERR_UNSUPPORTED;  // TMA box of one input image row
+    if (misaligned(x) || misaligned(y)) return LASNET_ERR_UNSUPPORTED;
+    const size_t e = elt_size(d->dtype);
+    const long pi = (long)d->n * d->h * d->w * d->stride * d->stride;
+    if (pi * (long)(d->c_in > d->c_mid ? d->c_in : d->c_mid) > 0x7fffffffL) return LASNET_ERR_UNSUPPORTED;
+    {
+        const uint8_t *a = static_cast<const uint8_t *>(x), *b = static_cast<const uint8_t *>(y);
+        const size_t xb = (size_t)pi * d->c_in * e, yb = (size_t)d->n * d->h * d->w * d->c_out * e;
+        if (a < b + yb && b < a + xb) return LASNET_ERR_ALIAS;  // no in-place form: shapes differ
+    }
+    const size_t need = proj_ws(d, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+    if (!ws || ws_bytes < need) return LASNET_ERR_WORKSPACE;
+    g_last_launches = 0;
+    if (d->n == 0) return LASNET_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    void *h1, *h2f, *h2, *xs, *ds;
+    proj_ws(d, static_cast<uint8_t *>(ws), &h1, &h2f, &h2, &xs, &ds);
+    const int S2 = d->stride;
+    // input-resolution descriptor (conv1 and the stride-1 3x3)
+    lasnet_block_desc di = *d;
+    di.h = d->h * S2;
+    di.w = d->w * S2;
+    di.stride = 1;
+    const int pxi = di.n * di.h * di.w, pxo = d->n * d->h * d->w;
+    int launches = 0;
+    ConvArgs a = base_args(&di);
+    a.m_dense = pxi;
+    a.a_src = x; a.w = w->w1; a.bias = w->b1; a.out = h1;
+    a.K = d->c_in; a.N = d->c_mid; a.a_ld = d->c_in; a.out_ld = d->c_mid;
+    if (run_conv(&di, CONV1_DENSE, a, pxi, x, y, h1, h2f, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    a.a_src = h1; a.w = w->w2; a.bias = w->b2; a.out = h2f;
+    a.K = 9 * d->c_mid; a.N = d->c_mid; a.a_ld = d->c_mid; a.out_ld = d->c_mid;
+    if (run_conv(&di, CONV2_DENSE, a, pxi, x, y, h1, h2f, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    launches += 2;
+    if (S2 > 1) {  // stride 2: the 3x3 at every input pixel, then every 2nd row/column; x likewise
+        {
+            KernelEvents ev(st);
+            if (launch_subsample(h2f, h2, d->n, d->h, d->w, d->c_mid * (int)e, S2, num_sms(), st) != cudaSuccess)
+                return LASNET_ERR_CUDA;
+        }
+        {
+            KernelEvents ev(st);
+            if (launch_subsample(x, xs, d->n, d->h, d->w, d->c_in * (int)e, S2, num_sms(), st) != cudaSuccess)
+                return LASNET_ERR_CUDA;
+        }
+        launches += 2;
+    }
+    // shortcut: ds = wd . x_s + bd (no ReLU) -- the conv3 kernel with K = c_in and no residual
+    lasnet_block_desc dk = *d;
+    dk.c_mid = d->c_in;
+    ConvArgs b = base_args(d);
+    b.m_dense = pxo;
+    b.a_src = S2 > 1 ? xs : x; b.w = w->wd; b.bias = w->bd; b.out = ds; b.resid = nullptr; b.no_relu = 1;
+    b.K = d->c_in; b.N = d->c_out; b.a_ld = d->c_in; b.out_ld = d->c_out;
+    if (run_conv(&dk, CONV3_DENSE, b, pxo, x, y, nullptr, S2 > 1 ? xs : x, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    // y = ReLU(conv3(h2) + b3 + ds)
+    ConvArgs c = base_args(d);
+    c.m_dense = pxo;
+    c.a_src = h2; c.w = w->w3; c.bias = w->b3; c.out = y; c.resid = ds;
+    c.K = d->c_mid; c.N = d->c_out; c.a_ld = d->c_mid; c.out_ld = d->c_out;
+    if (run_conv(d, CONV3_DENSE, c, pxo, x, y, nullptr, h2, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    g_last_launches = launches + 2;
+    return LASNET_OK;
+}
+
 int32_t lasnet_choose_schedule(const lasnet_block_desc *d, double r) {
     if (check_desc(d) != LASNET_OK || d->dtype != LASNET_BF16) return LASNET_SCHED_MASKER_SEPARATE;
     const double S = d->s, hs2 = (S + 2) * (S + 2), px = (double)d->n * d->h * d->w;

@@ -59,6 +59,16 @@ def make_block_weights(c_in: int, c_mid: int, c_out: int, seed: int = 1,
     }
 
 
+def make_proj_weights(c_in: int, c_mid: int, c_out: int, seed: int = 1, dtype: str = "bf16") -> dict:
+    """Bottleneck weights plus the projection shortcut wd [c_out][c_in] (He-normal)
+    and bd [c_out] fp32, for a stage's first block."""
+    wts = make_block_weights(c_in, c_mid, c_out, seed=seed, dtype=dtype, w3_gamma=1.0)
+    g = _gen(seed + 7919)
+    wts["wd"] = (torch.randn((c_out, c_in), generator=g) * (2.0 / c_in) ** 0.5).to(_dt(dtype)).contiguous()
+    wts["bd"] = (torch.randn((c_out,), generator=g) * 0.05).float().contiguous()
+    return wts
+
+
 def make_masker_weights(c_in: int, seed: int = 3) -> torch.Tensor:
     """Reduced masker weight w = W_0 - W_1, fp32 [c_in]."""
     return (torch.randn((c_in,), generator=_gen(seed)) * (1.0 / c_in) ** 0.5).float().contiguous()

@@ -500,3 +500,25 @@ def test_batch_sharding_is_bitwise_invariant(sched):
         y_p, m_p, _, _ = L.block_forward(x[lo:hi].contiguous().cuda(), to_dev(wts), wm.cuda(), bm, s, sched)
         assert torch.equal(m_p, m_all[lo:hi])
         assert torch.equal(y_p, y_all[lo:hi])
+
+
+PROJ_CASES = [
+    # n, h_in, c_in, c_mid, c_out, stride  (LAS-R101 first blocks, reduced batch/size)
+    (2, 14, 64, 64, 256, 1),     # stage 1 (stride 1, 64 -> 256)
+    (2, 14, 256, 128, 512, 2),   # stage 2
+    (2, 14, 512, 256, 1024, 2),  # stage 3 (c_mid 256: conv1 with 256-column tiles)
+    (3, 8, 128, 64, 128, 2),
+]
+
+
+@pytest.mark.parametrize("n,h,c_in,c_mid,c_out,stride", PROJ_CASES)
+def test_proj_block_matches_oracle(n, h, c_in, c_mid, c_out, stride):
+    """Static projection (first) block through lasnet_proj_block vs the fp64 oracle
+    with the same storage roundings."""
+    x = synth.make_x(n, h, h, c_in, seed=h + stride)
+    wts = synth.make_proj_weights(c_in, c_mid, c_out, seed=7)
+    y = L.proj_block(x.cuda(), to_dev(wts), stride)
+    want = oracle.proj_block(synth.to_f64(x), synth.weights_f64(wts), stride)
+    got = synth.to_f64(y.cpu())
+    assert got.shape == want.shape
+    assert max_abs_rel(got, want) <= BF16_TOL

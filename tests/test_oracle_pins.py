@@ -345,3 +345,38 @@ def test_brute_force_exhaustive_masks(oracle_mod, h, w, s):
         want = _brute_block(x, wts, mc, s)
         assert np.allclose(got, want, rtol=0, atol=np.abs(want).max() * 2 ** -7)
         assert np.mean(got == want) > 0.99
+
+
+# ------------------------------------------------- projection block (NEXT-f1) --
+
+@pytest.mark.parametrize("stride,h,c_in,c_mid,c_out", [(1, 8, 64, 64, 128), (2, 8, 64, 64, 128), (2, 6, 32, 16, 64)])
+def test_proj_block_equals_torch_conv2d_f64(oracle_mod, stride, h, c_in, c_mid, c_out):
+    """oracle.proj_block (unrounded) == the same block built from float64
+    torch.nn.functional.conv2d (library routine): 1x1, 3x3 stride s pad 1, 1x1,
+    and the 1x1 stride-s shortcut."""
+    import torch.nn.functional as F
+
+    x = synth.make_x(2, h, h, c_in, seed=stride + h)
+    w = synth.make_proj_weights(c_in, c_mid, c_out, seed=5)
+    got = oracle_mod.proj_block(synth.to_f64(x), synth.weights_f64(w), stride, rmode=oracle_mod.ROUND_NONE)
+    xt = torch.from_numpy(synth.to_f64(x)).permute(0, 3, 1, 2)
+    W = {k: torch.from_numpy(v) for k, v in synth.weights_f64(w).items()}
+    h1 = F.relu(F.conv2d(xt, W["w1"][:, :, None, None], W["b1"]))
+    h2 = F.relu(F.conv2d(h1, W["w2"].permute(0, 3, 1, 2), W["b2"], stride=stride, padding=1))
+    ds = F.conv2d(xt, W["wd"][:, :, None, None], W["bd"], stride=stride)
+    want = F.relu(F.conv2d(h2, W["w3"][:, :, None, None], W["b3"]) + ds).permute(0, 2, 3, 1).numpy()
+    assert got.shape == want.shape
+    assert np.abs(got - want).max() <= 1e-12 * max(1.0, np.abs(want).max())
+
+
+def test_proj_block_closed_form_zero_conv1(oracle_mod):
+    """W1 = 0, b1 = 0 -> h1 = 0, h2 = ReLU(b2) everywhere, so
+    y = ReLU(W3 ReLU(b2) + b3 + Wd x_s + bd) per output pixel (rounded as stored)."""
+    x = synth.make_x(1, 6, 6, 64, seed=3)
+    w = synth.weights_f64(synth.make_proj_weights(64, 64, 128, seed=4))
+    w["w1"][:] = 0.0
+    w["b1"][:] = 0.0
+    y = oracle_mod.proj_block(synth.to_f64(x), w, 2, rmode=oracle_mod.ROUND_NONE)
+    xs = synth.to_f64(x)[:, ::2, ::2, :]
+    want = np.maximum(w["w3"] @ np.maximum(w["b2"], 0.0) + w["b3"] + xs @ w["wd"].T + w["bd"], 0.0)
+    assert np.allclose(y, want, rtol=0, atol=1e-12)
