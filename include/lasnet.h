@@ -173,6 +173,29 @@ lasnet_status lasnet_proj_block(const lasnet_block_desc *desc, const lasnet_bloc
                                 void *y, void *ws, size_t ws_bytes, lasnet_stream_t stream);
 size_t lasnet_proj_workspace_bytes(const lasnet_block_desc *desc);
 
+/* The rest of a LAS-ResNet around the blocks, bf16 NHWC:
+ *
+ * lasnet_stem: 7x7 stride-2 convolution, 64 output channels, + bias, ReLU (the
+ *   ResNet stem with BN folded) on tensor cores.
+ *   x_pad  [n][2h][2w + 8][8]: the image with its 3 channels zero-padded to 8 and
+ *          4 zero pixels on the left and right of every row (top/bottom padding
+ *          is implicit); h, w are the OUTPUT dims, w % 4 == 0
+ *   w      [64][7][7][8] OHWI (channels 3..7 zero), b [64] fp32
+ *   y      [n][h][w][64]
+ *   ws     lasnet_stem_workspace_bytes() bytes (packed weights), no contract
+ * lasnet_maxpool: 3x3 stride-2 max pool, padding 1: x [n][2h][2w][c] -> y [n][h][w][c], c % 8 == 0.
+ * lasnet_head: global average pool + fully connected classifier:
+ *   x [n][hw][c], w [classes][c] (bf16), b [classes] fp32 -> logits [n][classes] fp32,
+ *   ws lasnet_head_workspace_bytes(n, c) bytes. */
+lasnet_status lasnet_stem(int32_t n, int32_t h, int32_t w, const void *x_pad, const void *wt, const float *b, void *y,
+                          void *ws, size_t ws_bytes, lasnet_stream_t stream);
+size_t lasnet_stem_workspace_bytes(void);
+lasnet_status lasnet_maxpool(int32_t n, int32_t h, int32_t w, int32_t c, const void *x, void *y,
+                             lasnet_stream_t stream);
+lasnet_status lasnet_head(int32_t n, int32_t hw, int32_t c, int32_t classes, const void *x, const void *w,
+                          const float *b, float *logits, void *ws, size_t ws_bytes, lasnet_stream_t stream);
+size_t lasnet_head_workspace_bytes(int32_t n, int32_t c);
+
 /* The whole block, steps 1-5, in one call, under one of two schedules.
  *
  * LASNET_SCHED_MASKER_SEPARATE -- the north-star branch: masker + compaction in

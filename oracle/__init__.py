@@ -11,7 +11,7 @@ bf16/fp32 tensors the GPU sees (bf16 -> fp64 is exact).
 
 Parity status per function:
   masker_2ch, masker, upsample, compact, static_block, dyn_block_def,
-  dyn_block_literal, block_pixel, round_bf16, proj_block -- all pinned by tests in
+  dyn_block_literal, block_pixel, round_bf16, proj_block, stem, maxpool, head -- all pinned by tests in
   tests/test_oracle_pins.py (library conv2d in fp64, exact rationals, closed
   forms, brute force, textbook routines).  No function is "parity unpinned".
 """
@@ -263,6 +263,43 @@ def proj_block(x, wts, stride, rmode=ROUND_BF16):
     h2 = _round_array(np.maximum(acc + b2, 0.0), rmode)
     ds = _round_array(x[:, ::s, ::s, :] @ wd.T + bd, rmode)
     return _round_array(np.maximum(h2 @ w3.T + b3 + ds, 0.0), rmode)
+
+
+def stem(x, w, b, rmode=ROUND_BF16):
+    """ResNet stem, BN folded: y = rnd(ReLU(conv7x7(x, stride 2, pad 3) + b)).
+    x [n][H][W][c] (c = 8: 3 channels + zeros), w [64][7][7][c] OHWI -> y [n][H/2][W/2][64]."""
+    x = np.asarray(x, np.float64)
+    w, b = np.asarray(w, np.float64), np.asarray(b, np.float64)
+    n, hi, wi, c = x.shape
+    ho, wo = hi // 2, wi // 2
+    xp = np.zeros((n, hi + 6, wi + 6, c))
+    xp[:, 3:-3, 3:-3] = x
+    acc = np.zeros((n, ho, wo, w.shape[0]))
+    for dy in range(7):
+        for dx in range(7):
+            acc += xp[:, dy:dy + 2 * ho:2, dx:dx + 2 * wo:2, :] @ w[:, dy, dx, :].T
+    return _round_array(np.maximum(acc + b, 0.0), rmode)
+
+
+def maxpool(x):
+    """3x3 stride-2 max pool with padding 1 (padding never wins): [n][2h][2w][c] -> [n][h][w][c]."""
+    x = np.asarray(x, np.float64)
+    n, hi, wi, c = x.shape
+    xp = np.full((n, hi + 2, wi + 2, c), -np.inf)
+    xp[:, 1:-1, 1:-1] = x
+    out = np.full((n, hi // 2, wi // 2, c), -np.inf)
+    for dy in range(3):
+        for dx in range(3):
+            out = np.maximum(out, xp[:, dy:dy + hi:2, dx:dx + wi:2, :])
+    return out
+
+
+def head(x, w, b):
+    """Global average pool over the pixels, then the classifier: logits = mean_p x[n,p,:] W^T + b (fp64)."""
+    x = np.asarray(x, np.float64)
+    n = x.shape[0]
+    pooled = x.reshape(n, -1, x.shape[-1]).mean(axis=1)
+    return pooled @ np.asarray(w, np.float64).T + np.asarray(b, np.float64)
 
 
 def num_threads() -> int:

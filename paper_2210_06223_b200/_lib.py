@@ -24,7 +24,8 @@ EXPORTS = [
     "lasnet_dyn_workspace_bytes", "lasnet_dense_block", "lasnet_dense_workspace_bytes",
     "lasnet_status_str", "lasnet_abi_version", "lasnet_last_launch_count", "lasnet_set_kernel_events",
     "lasnet_block_forward", "lasnet_block_forward_workspace_bytes", "lasnet_choose_schedule",
-    "lasnet_proj_block", "lasnet_proj_workspace_bytes",
+    "lasnet_proj_block", "lasnet_proj_workspace_bytes", "lasnet_stem", "lasnet_stem_workspace_bytes",
+    "lasnet_maxpool", "lasnet_head", "lasnet_head_workspace_bytes",
 ]
 
 # lasnet_schedule
@@ -89,6 +90,16 @@ def load(path: str = LIB_PATH):
     lib.lasnet_proj_block.restype = ctypes.c_int
     lib.lasnet_proj_workspace_bytes.argtypes = [D]
     lib.lasnet_proj_workspace_bytes.restype = sz
+    lib.lasnet_stem.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp, sz, vp]
+    lib.lasnet_stem.restype = ctypes.c_int
+    lib.lasnet_stem_workspace_bytes.argtypes = []
+    lib.lasnet_stem_workspace_bytes.restype = sz
+    lib.lasnet_maxpool.argtypes = [i32, i32, i32, i32, vp, vp, vp]
+    lib.lasnet_maxpool.restype = ctypes.c_int
+    lib.lasnet_head.argtypes = [i32, i32, i32, i32, vp, vp, vp, vp, vp, sz, vp]
+    lib.lasnet_head.restype = ctypes.c_int
+    lib.lasnet_head_workspace_bytes.argtypes = [i32, i32]
+    lib.lasnet_head_workspace_bytes.restype = sz
     lib.lasnet_status_str.argtypes = [ctypes.c_int]
     lib.lasnet_status_str.restype = ctypes.c_char_p
     lib.lasnet_abi_version.restype = i32

@@ -130,6 +130,44 @@ def proj_block(x: torch.Tensor, wts: dict, stride: int, ws: torch.Tensor | None 
     return y
 
 
+def stem(x_pad: torch.Tensor, w: torch.Tensor, b: torch.Tensor, ws: torch.Tensor | None = None):
+    """7x7 stride-2 stem (lasnet_stem): x_pad [n, 2h, 2w + 8, 8] (3 channels zero-padded
+    to 8, 4 zero pixels left and right) -> y [n, h, w, 64]."""
+    _require_cuda(x_pad, w, b)
+    lib = _lib.load()
+    n, hi, wp, c = x_pad.shape
+    h, w_out = hi // 2, (wp - 8) // 2
+    ws = ws if ws is not None else torch.empty(lib.lasnet_stem_workspace_bytes(), dtype=torch.uint8,
+                                               device=x_pad.device)
+    y = torch.empty((n, h, w_out, 64), dtype=x_pad.dtype, device=x_pad.device)
+    _lib.check("lasnet_stem", lib.lasnet_stem(n, h, w_out, _p(x_pad), _p(w), _p(b), _p(y), _p(ws), ws.numel(),
+                                              _stream()))
+    return y
+
+
+def maxpool(x: torch.Tensor):
+    """3x3 stride-2 max pool, padding 1 (lasnet_maxpool): [n, 2h, 2w, c] -> [n, h, w, c]."""
+    _require_cuda(x)
+    n, hi, wi, c = x.shape
+    y = torch.empty((n, hi // 2, wi // 2, c), dtype=x.dtype, device=x.device)
+    _lib.check("lasnet_maxpool", _lib.load().lasnet_maxpool(n, hi // 2, wi // 2, c, _p(x), _p(y), _stream()))
+    return y
+
+
+def head(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor, ws: torch.Tensor | None = None):
+    """Global average pool + classifier (lasnet_head): x [n, h, w, c] -> fp32 logits [n, classes]."""
+    _require_cuda(x, w, b)
+    lib = _lib.load()
+    n, h, wd, c = x.shape
+    classes = w.shape[0]
+    ws = ws if ws is not None else torch.empty(max(lib.lasnet_head_workspace_bytes(n, c), 1), dtype=torch.uint8,
+                                               device=x.device)
+    logits = torch.empty((n, classes), dtype=torch.float32, device=x.device)
+    _lib.check("lasnet_head", lib.lasnet_head(n, h * wd, c, classes, _p(x), _p(w), _p(b), _p(logits), _p(ws),
+                                              ws.numel(), _stream()))
+    return logits
+
+
 def block_forward(x: torch.Tensor, wts: dict, wm: torch.Tensor, bm: float, s: int, schedule: int,
                   y: torch.Tensor | None = None, ws: torch.Tensor | None = None, mask_out: bool = True):
     """Steps 1-5 in one C-ABI call (lasnet_block_forward) under `schedule`

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "liblasnet.so")
 SOURCES = ["lasnet_capi.cu", "mask_compact.cu", "conv_tc.cu", "conv23_tc.cu", "conv_simt.cu", "decide_gather.cu",
-           "proj_block.cu"]
+           "proj_block.cu", "net_layers.cu"]
 HEADERS = ["rowmap.cuh", "sm100_ptx.cuh", "launch.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

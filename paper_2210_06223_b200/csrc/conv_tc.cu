@@ -120,7 +120,7 @@ __device__ __forceinline__ TileGeo tile_geo(const ConvArgs &a, int BN) {
     int mt;
     if (MODE == CONV2_DYN) {
         mt = (*a.count + a.units_per_tile - 1) / a.units_per_tile;  // patch-aligned tiles
-    } else if (MODE == CONV2_DENSE) {
+    } else if (MODE == CONV2_DENSE || MODE == STEM) {
         mt = a.dense_tiles;
     } else {
         mt = (gemm_rows(MODE, a) + kBM - 1) / kBM;
@@ -182,9 +182,9 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
         fence_mbar_init();
     }
     if (warp == C::kProdWarp && lane == 0) {
-        if (!C::kGather) tma_prefetch_desc(&args.tmap_a);
+        if (!C::kGather && MODE != STEM) tma_prefetch_desc(&args.tmap_a);
         tma_prefetch_desc(&args.tmap_b);
-        if (!kResid) tma_prefetch_desc(&args.tmap_out);
+        if (!kResid && MODE != STEM) tma_prefetch_desc(&args.tmap_out);
     }
     if (warp == C::kMmaWarp) tmem_alloc<C::kTmemCols>(smem_u32(tmem_slot));
     tc_fence_before();
@@ -218,6 +218,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     const uint32_t fb = bar_full + 8 * stage;
                     int a_bytes = kABytes;  // conv1 dyn: A arrives by cp.async (not counted here)
                     if (C::kGather) a_bytes = 0;
+                    else if (MODE == STEM) a_bytes = 4 * (args.W / 4) * 128;
                     else if (MODE == CONV2_DYN || MODE == CONV2_DENSE) a_bytes = args.box_rows * 128;
                     mbar_arrive_expect_tx(fb, a_bytes + C::kBBytes);
                     tma_load_2d(sb, &args.tmap_b, fb, kb * kBK, n0);
@@ -228,6 +229,13 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     } else if (MODE == CONV2_DENSE) {
                         const int tap = kb / kpt, dy = tap / 3, dx = tap - dy * 3;
                         tma_load_5d(sa, &args.tmap_a, fb, 0, dx - 1, d2y + dy - 1, d2n, kb - tap * kpt);  // [c/64][N][H][W][64]
+                    } else if (MODE == STEM) {
+                        // K-block kb = kernel row dy: 4 boxes of W/4 output columns each (residue k of
+                        // ox mod 4), every box row the 8 input pixels x 8 channels of one output pixel
+                        const int n = mt / args.H, oy = mt - n * args.H;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            tma_load_4d(sa + k * (args.W / 4) * 128, &args.tmap_s[k], fb, 0, 0, 2 * oy + kb - 3, n);
                     } else if (!C::kGather) {
                         tma_load_2d(sa, &args.tmap_a, fb, kb * kBK, mt * kBM);
                     }
@@ -543,6 +551,10 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     dense2_tile(args, mt, d2n, d2y);
                     for (int c = 0; c < BN / 64; ++c)
                         tma_store_4d(&args.tmap_out, sbuf + c * kChunkBytes, n0 + c * 64, 0, d2y, d2n);
+                } else if (MODE == STEM) {  // the tile's rows in residue order back to output columns
+                    const int n = mt / args.H, oy = mt - n * args.H;
+                    for (int k = 0; k < 4; ++k)
+                        tma_store_4d(&args.tmap_s[4 + k], sbuf + k * (args.W / 4) * 128, 0, 0, oy, n);
                 } else if (MODE == CONV1_DYN || MODE == CONV1_DENSE || MODE == CONV1_DENSE_MASK) {  // h1: [c_mid/64][rows][64]
                     for (int c = 0; c < BN / 64; ++c)
                         tma_store_3d(&args.tmap_out, sbuf + c * kChunkBytes, 0, mt * kBM, (n0 >> 6) + c);
@@ -612,6 +624,7 @@ cudaError_t launch_conv_tc(int mode, const ConvArgs &a, int max_tiles_m, int num
         case CONV1_DENSE_MASK: return launch_mode<CONV1_DENSE_MASK>(a, max_tiles_m, num_sms, st);
         case CONV2_DENSE: return launch_mode<CONV2_DENSE>(a, max_tiles_m, num_sms, st);
         case CONV3_DENSE: return launch_mode<CONV3_DENSE>(a, max_tiles_m, num_sms, st);
+        case STEM: return launch_mode_bn<STEM, 64>(a, max_tiles_m, num_sms, st);
         default: return cudaErrorInvalidValue;
     }
 }

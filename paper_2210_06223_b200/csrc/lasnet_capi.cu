@@ -27,6 +27,10 @@ cudaError_t launch_conv_tc(int mode, const ConvArgs &a, int max_tiles_m, int num
 cudaError_t launch_conv_simt(int mode, const ConvArgs &a, int max_rows, cudaStream_t st);
 cudaError_t launch_subsample(const void *in, void *out, int n_img, int Ho, int Wo, int c_bytes, int stride, int num_sms,
                              cudaStream_t st);
+cudaError_t launch_pack_stem(const void *w, void *wp, cudaStream_t st);
+cudaError_t launch_maxpool(const void *x, void *y, int n_img, int Ho, int Wo, int c, int num_sms, cudaStream_t st);
+cudaError_t launch_head(const void *x, const void *w, const float *b, float *pooled, float *logits, int n_img, int hw,
+                        int c, int classes, int num_sms, cudaStream_t st);
 cudaError_t launch_conv23(bool dense, const ConvArgs &a, int max_tiles, int num_sms, cudaStream_t st);
 size_t decide_sync_bytes(int ncells, int num_sms);
 cudaError_t launch_decide_gather(const float4 *mpart, const void *x, const float *wm, float bm, int n_img, int H,
@@ -168,6 +172,25 @@ bool tmap(CUtensorMap *m, const void *base, int rank, const uint64_t *dims, cons
         es[i] = 1;
         if (i > 0) gs[i - 1] = stride;
         stride *= dims[i];
+    }
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void *>(base), gd, gs, bx, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Tensor map with explicit byte strides (views that step over elements, e.g. every
+// 4th output column, or 8-pixel windows every 4 pixel pairs).
+bool tmap_strided(CUtensorMap *m, const void *base, int rank, const uint64_t *dims, const uint64_t *strides,
+                  const uint32_t *box) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t gd[5], gs[4];
+    cuuint32_t bx[5], es[5];
+    for (int i = 0; i < rank; ++i) {
+        gd[i] = dims[i];
+        bx[i] = box[i];
+        es[i] = 1;
+        if (i > 0) gs[i - 1] = strides[i - 1];
     }
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void *>(base), gd, gs, bx, es,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -678,6 +701,82 @@ lasnet_status lasnet_block_forward(const lasnet_block_desc *d, const lasnet_bloc
  * gather of x for conv1 + residual/y; fused: x once + h1 write + gathered-h1
  * read + residual/y.  Tensor time is below the HBM time at every shape the
  * bf16 path supports, so bytes decide. */
+/* Stem, max pool and head of a LAS-ResNet (see include/lasnet.h). */
+size_t lasnet_stem_workspace_bytes(void) { return 64 * 448 * 2; }
+
+lasnet_status lasnet_stem(int32_t n, int32_t h, int32_t w, const void *x_pad, const void *wt, const float *b, void *y,
+                          void *ws, size_t ws_bytes, lasnet_stream_t stream) {
+    if (!x_pad || !wt || !b || !y) return LASNET_ERR_NULL;
+    if (n < 0 || h <= 0 || w <= 0) return LASNET_ERR_SHAPE;
+    if (w % 4 || w / 4 > 256 || misaligned(x_pad) || misaligned(y)) return LASNET_ERR_UNSUPPORTED;
+    if (!ws || ws_bytes < lasnet_stem_workspace_bytes()) return LASNET_ERR_WORKSPACE;
+    if ((long)n * 2 * h * (2 * w + 8) * 8 > 0x7fffffffL) return LASNET_ERR_UNSUPPORTED;
+    g_last_launches = 0;
+    if (n == 0) return LASNET_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    {
+        KernelEvents ev(st);
+        if (launch_pack_stem(wt, ws, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    }
+    ConvArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.n_img = n; a.H = h; a.W = w;
+    a.w = ws; a.bias = b; a.out = y;
+    a.K = 448; a.N = 64; a.a_ld = 448; a.out_ld = 64;
+    a.dense_tiles = n * h;
+    a.m_dense = n * h * 128;
+    const uint64_t wp = 2 * (uint64_t)w + 8;  // padded input width (pixels)
+    const uint64_t row_b = wp * 16, img_b = 2 * (uint64_t)h * row_b;
+    bool ok = tmap2(&a.tmap_b, ws, 448, 64, 64, 64);
+    for (int k = 0; k < 4 && ok; ++k) {
+        // A view k: the 8-pixel window of output column ox = 4 j + k starts at padded pixel 2 ox
+        const uint64_t d[4] = {64, (uint64_t)w / 4, 2 * (uint64_t)h, (uint64_t)n};
+        const uint64_t sd[3] = {128, row_b, img_b};  // window j -> j + 1: 4 output columns = 8 pixels = 128 B
+        const uint32_t bx[4] = {64, (uint32_t)w / 4, 1, 1};
+        ok = tmap_strided(&a.tmap_s[k], static_cast<const uint8_t *>(x_pad) + 32 * k, 4, d, sd, bx);
+        // output view k: columns 4 j + k of each output row
+        const uint64_t od[4] = {64, (uint64_t)w / 4, (uint64_t)h, (uint64_t)n};
+        const uint64_t os[3] = {128 * 4, (uint64_t)w * 128, (uint64_t)h * w * 128};
+        ok = ok && tmap_strided(&a.tmap_s[4 + k], static_cast<uint8_t *>(y) + 128 * k, 4, od, os, bx);
+    }
+    if (!ok) return LASNET_ERR_CUDA;
+    {
+        KernelEvents ev(st);
+        if (launch_conv_tc(STEM, a, n * h, num_sms(), st) != cudaSuccess) return LASNET_ERR_CUDA;
+    }
+    g_last_launches = 2;
+    return LASNET_OK;
+}
+
+lasnet_status lasnet_maxpool(int32_t n, int32_t h, int32_t w, int32_t c, const void *x, void *y,
+                             lasnet_stream_t stream) {
+    if (!x || !y) return LASNET_ERR_NULL;
+    if (n < 0 || h <= 0 || w <= 0 || c <= 0) return LASNET_ERR_SHAPE;
+    if (c % 8 || misaligned(x) || misaligned(y)) return LASNET_ERR_UNSUPPORTED;
+    g_last_launches = 0;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    KernelEvents ev(st);
+    if (launch_maxpool(x, y, n, h, w, c, num_sms(), st) != cudaSuccess) return LASNET_ERR_CUDA;
+    g_last_launches = 1;
+    return LASNET_OK;
+}
+
+size_t lasnet_head_workspace_bytes(int32_t n, int32_t c) { return (size_t)(n > 0 ? n : 0) * (c > 0 ? c : 0) * 4; }
+
+lasnet_status lasnet_head(int32_t n, int32_t hw, int32_t c, int32_t classes, const void *x, const void *w,
+                          const float *b, float *logits, void *ws, size_t ws_bytes, lasnet_stream_t stream) {
+    if (!x || !w || !b || !logits) return LASNET_ERR_NULL;
+    if (n < 0 || hw <= 0 || c <= 0 || classes <= 0) return LASNET_ERR_SHAPE;
+    if (n > 0 && (!ws || ws_bytes < lasnet_head_workspace_bytes(n, c))) return LASNET_ERR_WORKSPACE;
+    g_last_launches = 0;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    KernelEvents ev(st);
+    if (launch_head(x, w, b, static_cast<float *>(ws), logits, n, hw, c, classes, num_sms(), st) != cudaSuccess)
+        return LASNET_ERR_CUDA;
+    g_last_launches = 2;
+    return LASNET_OK;
+}
+
 /* Static projection (first) block of a stage (see include/lasnet.h). */
 size_t lasnet_proj_workspace_bytes(const lasnet_block_desc *d) {
     if (check_desc(d) != LASNET_OK) return 0;

@@ -1,0 +1,130 @@
+// net_layers.cu -- the non-block layers of a LAS-ResNet:
+// stem weight packing for the tcgen05 stem (conv_tc.cu, mode STEM), the 3x3
+// stride-2 max pool after the stem, and the head (global average pool + fully
+// connected classifier).  None of these is on the dynamic block's hot path;
+// they are plain CUDA-core kernels sized for the whole batch.
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "launch.cuh"
+
+namespace lasnet {
+
+// [64][7][7][8] (OHWI, channels padded to 8) -> [64][7][8][8]: kernel row dy,
+// window position p = 0..7 holds tap dx = p - 1 (position 0 is the unused
+// input pixel 2*ox - 4 of the 8-pixel window, weight 0).
+__global__ void pack_stem_kernel(const __nv_bfloat16 *__restrict__ w, __nv_bfloat16 *__restrict__ wp) {
+    pdl_wait();
+    pdl_trigger();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;  // over 64 * 7 * 8 * 8
+    if (i >= 64 * 448) return;
+    const int c = i & 7, p = (i >> 3) & 7, dy = (i >> 6) % 7, o = i / 448;
+    wp[i] = p == 0 ? __float2bfloat16(0.f) : w[((o * 7 + dy) * 7 + (p - 1)) * 8 + c];
+}
+
+cudaError_t launch_pack_stem(const void *w, void *wp, cudaStream_t st) {
+    return launch_k(pack_stem_kernel, dim3((64 * 448 + 255) / 256), dim3(256), 0, st,
+                    static_cast<const __nv_bfloat16 *>(w), static_cast<__nv_bfloat16 *>(wp));
+}
+
+// 3x3 stride-2 max pool, padding 1 (padded positions never win: -inf), NHWC bf16;
+// one thread per 8-channel vector of an output pixel.
+__global__ void __launch_bounds__(256) maxpool_kernel(const uint4 *__restrict__ x, uint4 *__restrict__ y, int n_img,
+                                                      int Ho, int Wo, int vpp) {
+    pdl_wait();
+    pdl_trigger();
+    const int Hi = 2 * Ho, Wi = 2 * Wo;
+    const long total = (long)n_img * Ho * Wo * vpp;
+    for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+        const int v = (int)(i % vpp);
+        const long p = i / vpp;
+        const int ox = (int)(p % Wo);
+        const long q = p / Wo;
+        const int oy = (int)(q % Ho), n = (int)(q / Ho);
+        float m[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) m[e] = -INFINITY;
+        for (int dy = -1; dy <= 1; ++dy) {
+            const int yy = 2 * oy + dy;
+            if (yy < 0 || yy >= Hi) continue;
+            for (int dx = -1; dx <= 1; ++dx) {
+                const int xx = 2 * ox + dx;
+                if (xx < 0 || xx >= Wi) continue;
+                const uint4 q4 = __ldg(x + (((long)n * Hi + yy) * Wi + xx) * vpp + v);
+                const uint32_t u[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    m[2 * e] = fmaxf(m[2 * e], __uint_as_float(u[e] << 16));
+                    m[2 * e + 1] = fmaxf(m[2 * e + 1], __uint_as_float(u[e] & 0xFFFF0000u));
+                }
+            }
+        }
+        uint32_t o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)  // maxima of bf16 values are bf16 values: the conversion is exact
+            o[e] = (__float_as_uint(m[2 * e]) >> 16) | (__float_as_uint(m[2 * e + 1]) & 0xFFFF0000u);
+        y[i] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+}
+
+cudaError_t launch_maxpool(const void *x, void *y, int n_img, int Ho, int Wo, int c, int num_sms, cudaStream_t st) {
+    const long total = (long)n_img * Ho * Wo * (c / 8);
+    if (total == 0) return cudaSuccess;
+    long grid = (total + 255) / 256;
+    if (grid > 8L * num_sms) grid = 8L * num_sms;
+    return launch_k(maxpool_kernel, dim3((unsigned)grid), dim3(256), 0, st, static_cast<const uint4 *>(x),
+                    static_cast<uint4 *>(y), n_img, Ho, Wo, c / 8);
+}
+
+// Head, pass 1: global average pool [n][hw][c] bf16 -> pooled [n][c] fp32
+// (fixed-order fp32 sum over the hw pixels, then / hw).
+__global__ void __launch_bounds__(256) avgpool_kernel(const __nv_bfloat16 *__restrict__ x, float *__restrict__ pooled,
+                                                      int n_img, int hw, int c) {
+    pdl_wait();
+    pdl_trigger();
+    const long total = (long)n_img * c;
+    for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+        const int ch = (int)(i % c);
+        const long n = i / c;
+        float s = 0.f;
+        for (int p = 0; p < hw; ++p) s += __bfloat162float(x[(n * hw + p) * c + ch]);
+        pooled[i] = s / (float)hw;
+    }
+}
+
+// Head, pass 2: logits[n][k] = b[k] + sum_c pooled[n][c] w[k][c]; one warp per
+// (image, class), lanes stride the channels, fixed-order shuffle reduction.
+__global__ void __launch_bounds__(256) fc_kernel(const float *__restrict__ pooled, const __nv_bfloat16 *__restrict__ w,
+                                                 const float *__restrict__ b, float *__restrict__ logits, int n_img,
+                                                 int c, int classes) {
+    pdl_wait();
+    pdl_trigger();
+    const int lane = threadIdx.x & 31;
+    const long warps = (long)gridDim.x * (blockDim.x >> 5);
+    for (long t = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < (long)n_img * classes; t += warps) {
+        const int k = (int)(t % classes);
+        const long n = t / classes;
+        float s = 0.f;
+        for (int ch = lane; ch < c; ch += 32) s = fmaf(pooled[n * c + ch], __bfloat162float(w[(long)k * c + ch]), s);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) logits[t] = s + b[k];
+    }
+}
+
+cudaError_t launch_head(const void *x, const void *w, const float *b, float *pooled, float *logits, int n_img, int hw,
+                        int c, int classes, int num_sms, cudaStream_t st) {
+    if (n_img == 0) return cudaSuccess;
+    long g1 = ((long)n_img * c + 255) / 256;
+    if (g1 > 8L * num_sms) g1 = 8L * num_sms;
+    cudaError_t e = launch_k(avgpool_kernel, dim3((unsigned)g1), dim3(256), 0, st,
+                             static_cast<const __nv_bfloat16 *>(x), pooled, n_img, hw, c);
+    if (e != cudaSuccess) return e;
+    long g2 = ((long)n_img * classes + 7) / 8;
+    if (g2 > 16L * num_sms) g2 = 16L * num_sms;
+    return launch_k(fc_kernel, dim3((unsigned)g2), dim3(256), 0, st, static_cast<const float *>(pooled),
+                    static_cast<const __nv_bfloat16 *>(w), b, logits, n_img, c, classes);
+}
+
+}  // namespace lasnet

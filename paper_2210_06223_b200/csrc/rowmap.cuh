@@ -38,6 +38,7 @@ enum ConvMode : int {
     CONV2_DENSE = 4,  // A = im2col of h1 with zero padding, out = h2 [n*h*w][c_mid]
     CONV3_DENSE = 5,  // A = h2 rows, out = y (residual add, ReLU)
     CONV1_DENSE_MASK = 6,  // CONV1_DENSE + per-pixel masker partials (the paper's masker-conv1 fusion)
+    STEM = 7,              // ResNet stem 7x7 stride 2 on 8-channel (3 + zero) input: tile = one output row
 };
 
 struct ConvArgs {
@@ -47,6 +48,7 @@ struct ConvArgs {
     CUtensorMap tmap_out;   // output (h1, h2 or y)
     CUtensorMap tmap_res;   // residual x (conv3)
     CUtensorMap tmap_b3;    // conv3 weights [c_out][c_mid] (fused conv2+conv3 kernel)
+    CUtensorMap tmap_s[8];  // stem: A window views (residue k of the output column mod 4) [0..3], output views [4..7]
     const void *w3;         // fused kernel: conv3 weights
     const float *bias3;     // fused kernel: conv3 bias [c_out]
     int32_t n3;             // fused kernel: c_out

@@ -522,3 +522,30 @@ def test_proj_block_matches_oracle(n, h, c_in, c_mid, c_out, stride):
     got = synth.to_f64(y.cpu())
     assert got.shape == want.shape
     assert max_abs_rel(got, want) <= BF16_TOL
+
+
+@pytest.mark.parametrize("n,h,w", [(2, 16, 24), (1, 32, 16), (2, 224, 224)])
+def test_stem_maxpool_head_match_oracle(n, h, w):
+    """Stem (tcgen05, 7x7 stride 2 over 4 column-residue window views), max pool and
+    head against the fp64 oracle; the 224x224 case is the ImageNet stem."""
+    g = torch.Generator().manual_seed(n + h)
+    x = torch.randn((n, h, w, 8), generator=g).clamp(-3, 3)
+    x[..., 3:] = 0.0
+    x = x.to(torch.bfloat16)
+    wt = (torch.randn((64, 7, 7, 8), generator=g) * 0.1)
+    wt[..., 3:] = 0.0
+    wt = wt.to(torch.bfloat16)
+    b = (torch.randn((64,), generator=g) * 0.1).float()
+    x_pad = torch.zeros((n, h, w + 8, 8), dtype=torch.bfloat16)
+    x_pad[:, :, 4:4 + w] = x
+    y = L.stem(x_pad.cuda(), wt.cuda(), b.cuda())
+    want = oracle.stem(synth.to_f64(x), synth.to_f64(wt), synth.to_f64(b))
+    got = synth.to_f64(y.cpu())
+    assert max_abs_rel(got, want) <= BF16_TOL
+    mp = L.maxpool(y)
+    assert np.array_equal(synth.to_f64(mp.cpu()), oracle.maxpool(got))  # exact on the same input
+    wf = (torch.randn((1000, 64), generator=g) * 0.1).to(torch.bfloat16)
+    bf = (torch.randn((1000,), generator=g) * 0.1).float()
+    lg = L.head(mp, wf.cuda(), bf.cuda()).cpu().numpy()
+    want_lg = oracle.head(synth.to_f64(mp.cpu()), synth.to_f64(wf), synth.to_f64(bf))
+    assert np.abs(lg - want_lg).max() <= 1e-4 * max(1.0, np.abs(want_lg).max())

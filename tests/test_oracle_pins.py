@@ -380,3 +380,26 @@ def test_proj_block_closed_form_zero_conv1(oracle_mod):
     xs = synth.to_f64(x)[:, ::2, ::2, :]
     want = np.maximum(w["w3"] @ np.maximum(w["b2"], 0.0) + w["b3"] + xs @ w["wd"].T + w["bd"], 0.0)
     assert np.allclose(y, want, rtol=0, atol=1e-12)
+
+
+# --------------------------------------------------- stem, pool, head (NEXT-f1) --
+
+def test_stem_pool_head_equal_torch_f64(oracle_mod):
+    """oracle.stem / maxpool / head == float64 torch conv2d(7x7, s2, p3) + ReLU,
+    max_pool2d(3, s2, p1) and adaptive-avg-pool + linear (library routines)."""
+    g = torch.Generator().manual_seed(0)
+    x = torch.randn((2, 16, 24, 8), generator=g, dtype=torch.float64)
+    x[..., 3:] = 0.0
+    w = torch.randn((64, 7, 7, 8), generator=g, dtype=torch.float64) * 0.1
+    b = torch.randn((64,), generator=g, dtype=torch.float64) * 0.1
+    got = oracle_mod.stem(x.numpy(), w.numpy(), b.numpy(), rmode=oracle_mod.ROUND_NONE)
+    want = F.relu(F.conv2d(x.permute(0, 3, 1, 2), w.permute(0, 3, 1, 2), b, stride=2, padding=3))
+    assert np.abs(got - want.permute(0, 2, 3, 1).numpy()).max() < 1e-12
+    mp = oracle_mod.maxpool(got)
+    want_mp = F.max_pool2d(torch.from_numpy(got).permute(0, 3, 1, 2), 3, stride=2, padding=1)
+    assert np.array_equal(mp, want_mp.permute(0, 2, 3, 1).numpy())  # a max selects: exact
+    wf = torch.randn((10, 64), generator=g, dtype=torch.float64)
+    bf = torch.randn((10,), generator=g, dtype=torch.float64)
+    lg = oracle_mod.head(mp, wf.numpy(), bf.numpy())
+    want_lg = F.linear(F.adaptive_avg_pool2d(want_mp, 1).flatten(1), wf, bf)
+    assert np.abs(lg - want_lg.numpy()).max() < 1e-12
