@@ -1,0 +1,139 @@
+"""LAS-ResNet forward built from the library's layers.
+
+    stem (7x7/2, tcgen05) -> 3x3/2 max pool -> 4 stages -> global average pool + classifier
+
+Each stage is one static projection block (lasnet_proj_block: the stride-2 /
+channel-changing first block, whose shortcut LASNet keeps dense) followed
+by the stage's identity blocks as dynamic blocks (lasnet_block_forward: masker
+-> compaction -> gather + conv1 -> conv2 -> conv3 + scatter-add, in place) at
+the stage's granularity S (S_net 4-4-2-1).  ResNet-101: depths
+3-4-23-3, bottleneck widths 64-128-256-512 (x4 outputs).
+
+Every buffer is allocated once at construction, so ``forward`` is only kernel
+launches (no host synchronisation) and can be captured in one CUDA graph.  This
+module only marshals: all arithmetic runs in liblasnet.so.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from .block import BlockShape, DynBlock, _p, _stream, choose_schedule
+
+R101_DEPTHS = (3, 4, 23, 3)
+R50_DEPTHS = (3, 4, 6, 3)
+WIDTHS = (64, 128, 256, 512)
+S_NET = (4, 4, 2, 1)
+
+
+class ProjBlock:
+    """Static projection block with preallocated output and workspace."""
+
+    def __init__(self, n, h_in, w_in, c_in, c_mid, c_out, stride, wts, device="cuda"):
+        self.wts = {k: v.to(device).contiguous() for k, v in wts.items()}
+        self.h, self.w = h_in // stride, w_in // stride
+        self.desc = _lib.BlockDesc(n, self.h, self.w, c_in, c_mid, c_out, stride, 1, _lib.LASNET_BF16)
+        self.wt = _lib.BlockWeights(*(self.wts[k].data_ptr() for k in ("w1", "b1", "w2", "b2", "w3", "b3", "wd", "bd")))
+        lib = _lib.load()
+        self.ws = torch.empty(max(lib.lasnet_proj_workspace_bytes(ctypes.byref(self.desc)), 1), dtype=torch.uint8,
+                              device=device)
+        self.y = torch.empty((n, self.h, self.w, c_out), dtype=torch.bfloat16, device=device)
+
+    def forward(self, x):
+        _lib.check("lasnet_proj_block", _lib.load().lasnet_proj_block(
+            ctypes.byref(self.desc), ctypes.byref(self.wt), _p(x), _p(self.y), _p(self.ws), self.ws.numel(),
+            _stream()))
+        return self.y
+
+
+class LASResNet:
+    """LAS-ResNet forward on a batch of n images of hw x hw (3 channels zero-padded
+    to 8, given as the stem's padded layout [n][hw][hw + 8][8])."""
+
+    def __init__(self, n: int, weights: dict, hw: int = 224, depths=R101_DEPTHS, s_net=S_NET, r: float = 0.5,
+                 device="cuda"):
+        self.n, self.hw, self.device = n, hw, device
+        lib = _lib.load()
+        self.stem_w = weights["stem_w"].to(device).contiguous()
+        self.stem_b = weights["stem_b"].to(device).contiguous()
+        self.stem_ws = torch.empty(lib.lasnet_stem_workspace_bytes(), dtype=torch.uint8, device=device)
+        h = hw // 2
+        self.stem_y = torch.empty((n, h, h, 64), dtype=torch.bfloat16, device=device)
+        h //= 2
+        self.pool_y = torch.empty((n, h, h, 64), dtype=torch.bfloat16, device=device)
+        self.stages = []
+        c_in = 64
+        for si, (depth, width, s) in enumerate(zip(depths, WIDTHS, s_net)):
+            stride = 1 if si == 0 else 2
+            c_out = 4 * width
+            proj = ProjBlock(n, h, h, c_in, width, c_out, stride, weights[f"s{si}_proj"], device)
+            h //= stride
+            dyn = []
+            for b in range(1, depth):
+                wb = weights[f"s{si}_b{b}"]
+                sched = choose_schedule(n, h, h, c_out, width, c_out, s, r)
+                dyn.append(DynBlock(BlockShape(n, h, h, c_out, width, s), {k: wb[k] for k in
+                                                                           ("w1", "b1", "w2", "b2", "w3", "b3")},
+                                    wb["wm"], 0.0, device=device, schedule=sched))
+            self.stages.append((proj, dyn))
+            c_in = c_out
+        self.fc_w = weights["fc_w"].to(device).contiguous()
+        self.fc_b = weights["fc_b"].to(device).contiguous()
+        self.head_ws = torch.empty(max(lib.lasnet_head_workspace_bytes(n, c_in), 1), dtype=torch.uint8,
+                                   device=device)
+        self.logits = torch.empty((n, self.fc_w.shape[0]), dtype=torch.float32, device=device)
+        self.c_last, self.h_last = c_in, h
+
+    def blocks(self):
+        for proj, dyn in self.stages:
+            yield from dyn
+
+    def forward(self, x_pad: torch.Tensor, calibrate_r: float | None = None, dense: bool = False):
+        """Logits [n, classes] (fp32).  calibrate_r: first set every dynamic block's
+        masker bias so that ~r of its cells are active on the activations it sees
+        (host synchronisation; not for the timed path).  dense: run the identity
+        blocks on every pixel (lasnet_dense_block) -- the comparator network."""
+        lib = _lib.load()
+        n, h = self.n, self.hw // 2
+        _lib.check("lasnet_stem", lib.lasnet_stem(n, h, h, _p(x_pad), _p(self.stem_w), _p(self.stem_b),
+                                                  _p(self.stem_y), _p(self.stem_ws), self.stem_ws.numel(), _stream()))
+        _lib.check("lasnet_maxpool", lib.lasnet_maxpool(n, h // 2, h // 2, 64, _p(self.stem_y), _p(self.pool_y),
+                                                        _stream()))
+        x = self.pool_y
+        for si, (proj, dyn) in enumerate(self.stages):
+            y = proj.forward(x)
+            other = self._scratch(si, y) if dense else None
+            for blk in dyn:
+                if calibrate_r is not None:
+                    blk.calibrate_bias(y, calibrate_r)
+                if dense:  # out of place, ping-pong between the stage's two buffers
+                    blk.dense(y, other)
+                    y, other = other, y
+                else:
+                    blk.forward(y)  # in place: inactive pixels are never touched
+            x = y
+        _lib.check("lasnet_head", lib.lasnet_head(n, self.h_last * self.h_last, self.c_last, self.fc_w.shape[0],
+                                                  _p(x), _p(self.fc_w), _p(self.fc_b), _p(self.logits),
+                                                  _p(self.head_ws), self.head_ws.numel(), _stream()))
+        return self.logits
+
+    def _scratch(self, si, like):
+        if not hasattr(self, "_scr"):
+            self._scr = {}
+        if si not in self._scr:
+            self._scr[si] = torch.empty_like(like)
+        return self._scr[si]
+
+    def capture(self, x_pad: torch.Tensor, dense: bool = False) -> torch.cuda.CUDAGraph:
+        """The whole forward as one CUDA graph on these buffers."""
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.forward(x_pad, dense=dense)
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.forward(x_pad, dense=dense)
+        return g

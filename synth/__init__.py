@@ -69,6 +69,38 @@ def make_proj_weights(c_in: int, c_mid: int, c_out: int, seed: int = 1, dtype: s
     return wts
 
 
+def make_lasnet_weights(depths=(3, 4, 23, 3), widths=(64, 128, 256, 512), classes: int = 1000, seed: int = 11,
+                        dtype: str = "bf16") -> dict:
+    """Random-init weights of a LAS-ResNet (BN folded): stem [64][7][7][8] (channels
+    3..7 zero), per stage a projection block and depth-1 identity blocks (with a
+    masker weight each), classifier [classes][4*widths[-1]]."""
+    g = _gen(seed)
+    dt = _dt(dtype)
+    stem = torch.randn((64, 7, 7, 8), generator=g) * (2.0 / (7 * 7 * 3)) ** 0.5
+    stem[..., 3:] = 0.0
+    w = {"stem_w": stem.to(dt).contiguous(), "stem_b": (torch.randn((64,), generator=g) * 0.05).float().contiguous()}
+    c_in = 64
+    for si, (depth, width) in enumerate(zip(depths, widths)):
+        c_out = 4 * width
+        w[f"s{si}_proj"] = make_proj_weights(c_in, width, c_out, seed=seed * 1000 + 100 * si, dtype=dtype)
+        for b in range(1, depth):
+            wb = make_block_weights(c_out, width, c_out, seed=seed * 1000 + 100 * si + 2 * b, dtype=dtype)
+            wb["wm"] = make_masker_weights(c_out, seed=seed * 1000 + 100 * si + 2 * b + 1)
+            w[f"s{si}_b{b}"] = wb
+        c_in = c_out
+    w["fc_w"] = (torch.randn((classes, c_in), generator=g) * (1.0 / c_in) ** 0.5).to(dt).contiguous()
+    w["fc_b"] = torch.zeros((classes,)).float().contiguous()
+    return w
+
+
+def make_image_batch(n: int, hw: int = 224, seed: int = 0, dtype: str = "bf16") -> torch.Tensor:
+    """ImageNet-normalised-like input N(0,1) with 3 channels, in the stem's padded
+    layout [n][hw][hw + 8][8] (channels 3..7 and 4 pixels left/right zero)."""
+    x = torch.zeros((n, hw, hw + 8, 8), dtype=torch.float32)
+    x[:, :, 4:4 + hw, :3] = torch.randn((n, hw, hw, 3), generator=_gen(seed))
+    return x.to(_dt(dtype)).contiguous()
+
+
 def make_masker_weights(c_in: int, seed: int = 3) -> torch.Tensor:
     """Reduced masker weight w = W_0 - W_1, fp32 [c_in]."""
     return (torch.randn((c_in,), generator=_gen(seed)) * (1.0 / c_in) ** 0.5).float().contiguous()
