@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
     ap.add_argument("--detail", default=None, help="write per-kernel detail JSON here")
+    ap.add_argument("--network", type=int, default=1, help="1: also time the LAS-ResNet-101 forward (BASELINE "
+                                                             "configs[2]: 224x224, global batch 256 split over the ranks)")
     ap.add_argument("--graph", type=int, default=1, help="1: time CUDA-graph replays of the step (captured once on "
                                                           "the same buffers), 0: eager launches")
     ap.add_argument("--schedule", default="auto", choices=["auto", "separate", "fused"],
@@ -414,6 +416,21 @@ def run_lasnet(args):
     from paper_2210_06223_b200 import dist as ldist
 
     tot_max, e2e_max, dense_max = ldist.max_over_ranks([tot_ms, e2e_ms, statistics.fmean(dense_ms)], device="cuda")
+    net_info = None
+    if args.network:
+        try:
+            nd, nn_, n_loc, nrate = network_measure(world, max(5, min(K, 10)))
+            nd_max, nn_max = ldist.max_over_ranks([nd, nn_], device="cuda")
+            net_info = {"model": "LAS-ResNet-101 (S_net 4-4-2-1, projection blocks static)", "image": "224x224",
+                        "global_batch": n_loc * world, "per_gpu_batch": n_loc, "r_target": 0.5,
+                        "r_patch_mean": round(nrate, 4), "ms_per_forward": round(nd_max, 4),
+                        "images_per_s": round(n_loc * world / (nd_max * 1e-3), 1),
+                        "dense_identity_ms_per_forward": round(nn_max, 4),
+                        "dense_identity_images_per_s": round(n_loc * world / (nn_max * 1e-3), 1),
+                        "speedup_vs_dense": round(nn_max / nd_max, 3),
+                        "timing": "CUDA events around one CUDA-graph replay of the whole forward, median, max over ranks"}
+        except Exception as e:  # the block headline above stands on its own
+            net_info = {"error": f"{type(e).__name__}: {e}"[:300]}
     # the exchange step of SURVEY 8(e): summed active-cell statistics and per-rank step times
     act_all, cells_all = ldist.sum_over_ranks([stats["P"], mask_cells.size], device="cuda")
     rank_ms = [t / K for t in ldist.gather_over_ranks(tot_ms, device="cuda")]
@@ -470,6 +487,7 @@ def run_lasnet(args):
             "speedup_vs_dense": round(dense_max / (tot_max / K), 3),
             "roofline": roof,
             "kernels_roofline": kern_roof,
+            "network": net_info,
             "block_roofline": blk_roof,
             "e2e": {"value": round(e2e_val, 1), "unit": "images/s", "h2d_bytes_per_step": x.numel() * 2,
                     "d2h_bytes_per_step": x.numel() * 2},
@@ -490,6 +508,42 @@ def run_lasnet(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def network_measure(world: int, steps: int, r: float = 0.5):
+    """LAS-ResNet-101 forward (configs[2]): global batch 256 split over the ranks,
+    224x224, S_net 4-4-2-1, masker biases calibrated to r on the activations each
+    block sees; the forward and the dense-identity-block comparator each one CUDA
+    graph.  Returns per-rank (ms_dyn, ms_dense, n_local, mean r_patch)."""
+    import synth
+    import paper_2210_06223_b200 as L
+
+    n_local = max(1, 256 // world)
+    wts = synth.make_lasnet_weights(seed=11)
+    x = synth.make_image_batch(n_local, 224, seed=int(os.environ.get("RANK", "0"))).cuda()
+    net = L.LASResNet(n_local, wts, hw=224, r=r)
+    net.forward(x, calibrate_r=r)
+    torch.cuda.synchronize()
+    rate = statistics.fmean(float(b.mask_buf.float().mean().item()) for b in net.blocks())
+    out = []
+    for dense in (False, True):
+        g = net.capture(x, dense=dense)
+        for _ in range(2):
+            g.replay()
+        st = torch.cuda.current_stream()
+        ev = []
+        for _ in range(steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            g.replay()
+            b.record(st)
+            ev.append((a, b))
+        torch.cuda.synchronize()
+        out.append(statistics.median(a.elapsed_time(b) for a, b in ev))
+        del g
+    del net
+    torch.cuda.empty_cache()
+    return out[0], out[1], n_local, rate
 
 
 def ctypes_array(events):
