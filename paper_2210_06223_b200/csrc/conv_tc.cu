@@ -228,7 +228,13 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                         tma_load_5d(sa, &args.tmap_a, fb, 0, dx, dy, u0, kb - tap * kpt);  // h1 [c/64][P][S+2][S+2][64]
                     } else if (MODE == CONV2_DENSE) {
                         const int tap = kb / kpt, dy = tap / 3, dx = tap - dy * 3;
-                        tma_load_5d(sa, &args.tmap_a, fb, 0, dx - 1, d2y + dy - 1, d2n, kb - tap * kpt);  // [c/64][N][H][W][64]
+                        if (args.conv_stride == 2) {
+                            // input (2 o + d - 1): view of parity (d != 1), coordinate o - (d == 0)
+                            const int v = ((dy != 1) << 1) | (dx != 1);
+                            tma_load_5d(sa, &args.tmap_s[v], fb, 0, -(dx == 0), d2y - (dy == 0), d2n, kb - tap * kpt);
+                        } else {
+                            tma_load_5d(sa, &args.tmap_a, fb, 0, dx - 1, d2y + dy - 1, d2n, kb - tap * kpt);  // [c/64][N][H][W][64]
+                        }
                     } else if (MODE == STEM) {
                         // K-block kb = kernel row dy: 4 boxes of W/4 output columns each (residue k of
                         // ox mod 4), every box row the 8 input pixels x 8 channels of one output pixel

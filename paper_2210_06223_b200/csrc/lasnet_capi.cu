@@ -823,22 +823,43 @@ lasnet_status lasnet_proj_block(const lasnet_block_desc *d, const lasnet_block_w
     a.a_src = x; a.w = w->w1; a.bias = w->b1; a.out = h1;
     a.K = d->c_in; a.N = d->c_mid; a.a_ld = d->c_in; a.out_ld = d->c_mid;
     if (run_conv(&di, CONV1_DENSE, a, pxi, x, y, h1, h2f, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
-    a.a_src = h1; a.w = w->w2; a.bias = w->b2; a.out = h2f;
+    a.a_src = h1; a.w = w->w2; a.bias = w->b2;
     a.K = 9 * d->c_mid; a.N = d->c_mid; a.a_ld = d->c_mid; a.out_ld = d->c_mid;
-    if (run_conv(&di, CONV2_DENSE, a, pxi, x, y, h1, h2f, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
-    launches += 2;
-    if (S2 > 1) {  // stride 2: the 3x3 at every input pixel, then every 2nd row/column; x likewise
-        {
-            KernelEvents ev(st);
-            if (launch_subsample(h2f, h2, d->n, d->h, d->w, d->c_mid * (int)e, S2, num_sms(), st) != cudaSuccess)
-                return LASNET_ERR_CUDA;
+    if (S2 == 1) {
+        a.out = h2;
+        if (run_conv(&di, CONV2_DENSE, a, pxi, x, y, h1, h2, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
+        launches += 2;
+    } else {
+        // stride 2: output pixel (oy, ox), tap (dy, dx) reads h1 (2 oy + dy - 1, 2 ox + dx - 1) -- one of four
+        // parity views of h1 ([c_mid/64][n][Hi][Wi][64] with doubled pixel and row strides)
+        a.out = h2;
+        a.conv_stride = 2;
+        const uint64_t Wi = di.w, Hi = di.h;
+        bool ok = true;
+        for (int v = 0; v < 4 && ok; ++v) {
+            const int py = v >> 1, px = v & 1;
+            const uint64_t dims[5] = {64, (uint64_t)d->w, (uint64_t)d->h, (uint64_t)d->n, (uint64_t)(d->c_mid / 64)};
+            const uint64_t str[4] = {2 * 128, 2 * Wi * 128, Hi * Wi * 128, (uint64_t)d->n * Hi * Wi * 128};
+            const uint32_t box[5] = {64, (uint32_t)d->w, 1, 1, 1};  // rows/imgs set below from the tile geometry
+            uint32_t bx[5];
+            for (int i = 0; i < 5; ++i) bx[i] = box[i];
+            if (d->h * d->w <= 128) {
+                bx[2] = d->h;
+                bx[3] = 128 / (d->h * d->w);
+            } else {
+                bx[2] = 128 / d->w;
+            }
+            ok = tmap_strided(&a.tmap_s[v], static_cast<const uint8_t *>(h1) + ((uint64_t)py * Wi + px) * 128, 5, dims,
+                              str, bx);
         }
+        if (!ok) return LASNET_ERR_CUDA;
+        if (run_conv(d, CONV2_DENSE, a, pxo, x, y, h1, h2, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
         {
             KernelEvents ev(st);
             if (launch_subsample(x, xs, d->n, d->h, d->w, d->c_in * (int)e, S2, num_sms(), st) != cudaSuccess)
                 return LASNET_ERR_CUDA;
         }
-        launches += 2;
+        launches += 3;
     }
     // shortcut: ds = wd . x_s + bd (no ReLU) -- the conv3 kernel with K = c_in and no residual
     lasnet_block_desc dk = *d;
