@@ -167,8 +167,9 @@ size_t lasnet_dense_workspace_bytes(const lasnet_block_desc *desc);
  *   x       [n][h*stride][w*stride][c_in];  y [n][h][w][c_out] (must not overlap x)
  *   wts     w1..w3 as above and wd/bd (required)
  *   ws      lasnet_proj_workspace_bytes(desc) bytes, no contract on contents.
- * Stride 2 computes the 3x3 at every input pixel and keeps every second row and
- * column (4x the 3x3 work of a strided kernel; correct, not yet tuned). */
+ * Stride 2 reads h1 through four parity views (every second pixel and row); conv3
+ * and the shortcut run as one GEMM over [h2 | x_s] and [W3 | Wd] (the shortcut
+ * output is never stored or rounded). */
 lasnet_status lasnet_proj_block(const lasnet_block_desc *desc, const lasnet_block_weights *wts, const void *x,
                                 void *y, void *ws, size_t ws_bytes, lasnet_stream_t stream);
 size_t lasnet_proj_workspace_bytes(const lasnet_block_desc *desc);

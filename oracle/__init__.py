@@ -238,11 +238,11 @@ def _round_array(a, rmode):
 def proj_block(x, wts, stride, rmode=ROUND_BF16):
     """Static projection (first) block of a ResNet stage, BN folded (the
     stride-s first block whose shortcut LASNet keeps dense), written out in
-    fp64 numpy with the GPU's storage roundings (h1, h2, the shortcut, y):
+    fp64 numpy with the storage roundings of the stored tensors (h1, h2, y; the
+    shortcut x_s Wd^T + bd is an unstored term of y, reading R21):
       h1 = rnd(ReLU(x W1^T + b1))                         at the input resolution
       h2 = rnd(ReLU(sum_{dy,dx} h1p[s*oy+dy, s*ox+dx] W2[:,dy,dx,:]^T + b2)), h1p = h1 zero-padded by 1
-      ds = rnd(x[:, ::s, ::s] Wd^T + bd)                   (no ReLU)
-      y  = rnd(ReLU(h2 W3^T + b3 + ds))
+      y  = rnd(ReLU(h2 W3^T + b3 + x[:, ::s, ::s] Wd^T + bd))
     x [n][H][W][c_in] (H, W multiples of s) -> y [n][H/s][W/s][c_out]."""
     x = np.asarray(x, np.float64)
     n, hi, wi, c_in = x.shape
@@ -261,7 +261,7 @@ def proj_block(x, wts, stride, rmode=ROUND_BF16):
             win = h1p[:, dy:dy + s * ho:s, dx:dx + s * wo:s, :]
             acc += win @ w2[:, dy, dx, :].T
     h2 = _round_array(np.maximum(acc + b2, 0.0), rmode)
-    ds = _round_array(x[:, ::s, ::s, :] @ wd.T + bd, rmode)
+    ds = x[:, ::s, ::s, :] @ wd.T + bd
     return _round_array(np.maximum(h2 @ w3.T + b3 + ds, 0.0), rmode)
 
 

@@ -243,7 +243,10 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                         for (int k = 0; k < 4; ++k)
                             tma_load_4d(sa + k * (args.W / 4) * 128, &args.tmap_s[k], fb, 0, 0, 2 * oy + kb - 3, n);
                     } else if (!C::kGather) {
-                        tma_load_2d(sa, &args.tmap_a, fb, kb * kBK, mt * kBM);
+                        if (args.a2_kb && kb >= args.a2_kb)  // second A source (projection shortcut input)
+                            tma_load_2d(sa, &args.tmap_s[0], fb, (kb - args.a2_kb) * kBK, mt * kBM);
+                        else
+                            tma_load_2d(sa, &args.tmap_a, fb, kb * kBK, mt * kBM);
                     }
                 }
                 TRACE(lt, 1);

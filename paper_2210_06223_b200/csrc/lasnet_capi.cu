@@ -28,6 +28,7 @@ cudaError_t launch_conv_simt(int mode, const ConvArgs &a, int max_rows, cudaStre
 cudaError_t launch_subsample(const void *in, void *out, int n_img, int Ho, int Wo, int c_bytes, int stride, int num_sms,
                              cudaStream_t st);
 cudaError_t launch_pack_stem(const void *w, void *wp, cudaStream_t st);
+cudaError_t launch_add_bias(const float *a, const float *b, float *out, int n, cudaStream_t st);
 cudaError_t launch_maxpool(const void *x, void *y, int n_img, int Ho, int Wo, int c, int num_sms, cudaStream_t st);
 cudaError_t launch_head(const void *x, const void *w, const float *b, float *pooled, float *logits, int n_img, int hw,
                         int c, int classes, int num_sms, cudaStream_t st);
@@ -423,15 +424,17 @@ size_t fwd_ws(const lasnet_block_desc *d, int schedule, uint8_t *base, FwdWs *o)
 
 // Workspace of lasnet_proj_block: h1 and the stride-1 3x3 output at the input
 // resolution, then (stride 2) the subsampled h2 and x, and the shortcut output.
-size_t proj_ws(const lasnet_block_desc *d, uint8_t *base, void **h1, void **h2f, void **h2, void **xs, void **ds) {
+// Workspace of lasnet_proj_block: h1 at the input resolution, h2 and (stride 2)
+// the subsampled x at the output resolution, the K-concatenated [W3 | Wd] and b3 + bd.
+size_t proj_ws(const lasnet_block_desc *d, uint8_t *base, void **h1, void **h2, void **xs, void **w3d, void **b3d) {
     const size_t e = elt_size(d->dtype);
     const size_t po = (size_t)d->n * d->h * d->w, pi = po * d->stride * d->stride;
     Carve cv{base};
-    void *a = cv.take(pi * d->c_mid * e), *b = cv.take(pi * d->c_mid * e);
-    void *c = d->stride > 1 ? cv.take(po * d->c_mid * e) : b;
+    void *a = cv.take(pi * d->c_mid * e), *c = cv.take(po * d->c_mid * e);
     void *xx = d->stride > 1 ? cv.take(po * d->c_in * e) : nullptr;
-    void *dd = cv.take(po * d->c_out * e);
-    if (h1) *h1 = a, *h2f = b, *h2 = c, *xs = xx, *ds = dd;
+    void *ww = cv.take((size_t)d->c_out * (d->c_mid + d->c_in) * e);
+    void *bb = cv.take((size_t)d->c_out * 4);
+    if (h1) *h1 = a, *h2 = c, *xs = xx, *w3d = ww, *b3d = bb;
     return cv.used;
 }
 
@@ -808,8 +811,8 @@ lasnet_status lasnet_proj_block(const lasnet_block_desc *d, const lasnet_block_w
     g_last_launches = 0;
     if (d->n == 0) return LASNET_OK;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    void *h1, *h2f, *h2, *xs, *ds;
-    proj_ws(d, static_cast<uint8_t *>(ws), &h1, &h2f, &h2, &xs, &ds);
+    void *h1, *h2, *xs, *w3d, *b3d;
+    proj_ws(d, static_cast<uint8_t *>(ws), &h1, &h2, &xs, &w3d, &b3d);
     const int S2 = d->stride;
     // input-resolution descriptor (conv1 and the stride-1 3x3)
     lasnet_block_desc di = *d;
@@ -822,7 +825,7 @@ lasnet_status lasnet_proj_block(const lasnet_block_desc *d, const lasnet_block_w
     a.m_dense = pxi;
     a.a_src = x; a.w = w->w1; a.bias = w->b1; a.out = h1;
     a.K = d->c_in; a.N = d->c_mid; a.a_ld = d->c_in; a.out_ld = d->c_mid;
-    if (run_conv(&di, CONV1_DENSE, a, pxi, x, y, h1, h2f, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    if (run_conv(&di, CONV1_DENSE, a, pxi, x, y, h1, h2, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
     a.a_src = h1; a.w = w->w2; a.bias = w->b2;
     a.K = 9 * d->c_mid; a.N = d->c_mid; a.a_ld = d->c_mid; a.out_ld = d->c_mid;
     if (S2 == 1) {
@@ -861,19 +864,24 @@ lasnet_status lasnet_proj_block(const lasnet_block_desc *d, const lasnet_block_w
         }
         launches += 3;
     }
-    // shortcut: ds = wd . x_s + bd (no ReLU) -- the conv3 kernel with K = c_in and no residual
-    lasnet_block_desc dk = *d;
-    dk.c_mid = d->c_in;
-    ConvArgs b = base_args(d);
-    b.m_dense = pxo;
-    b.a_src = S2 > 1 ? xs : x; b.w = w->wd; b.bias = w->bd; b.out = ds; b.resid = nullptr; b.no_relu = 1;
-    b.K = d->c_in; b.N = d->c_out; b.a_ld = d->c_in; b.out_ld = d->c_out;
-    if (run_conv(&dk, CONV3_DENSE, b, pxo, x, y, nullptr, S2 > 1 ? xs : x, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
-    // y = ReLU(conv3(h2) + b3 + ds)
+    // y = ReLU([h2 | x_s] [W3 | Wd]^T + b3 + bd): conv3 and the 1x1 shortcut as ONE GEMM over the
+    // K-concatenated sources (the shortcut output is never stored)
+    const size_t wrow = (size_t)(d->c_mid + d->c_in) * e;
+    if (cudaMemcpy2DAsync(w3d, wrow, w->w3, (size_t)d->c_mid * e, (size_t)d->c_mid * e, d->c_out,
+                          cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+        cudaMemcpy2DAsync(static_cast<uint8_t *>(w3d) + (size_t)d->c_mid * e, wrow, w->wd, (size_t)d->c_in * e,
+                          (size_t)d->c_in * e, d->c_out, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return LASNET_ERR_CUDA;
+    {
+        KernelEvents ev(st);
+        if (launch_add_bias(w->b3, w->bd, static_cast<float *>(b3d), d->c_out, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    }
     ConvArgs c = base_args(d);
     c.m_dense = pxo;
-    c.a_src = h2; c.w = w->w3; c.bias = w->b3; c.out = y; c.resid = ds;
-    c.K = d->c_mid; c.N = d->c_out; c.a_ld = d->c_mid; c.out_ld = d->c_out;
+    c.a_src = h2; c.w = w3d; c.bias = static_cast<const float *>(b3d); c.out = y; c.resid = nullptr;
+    c.K = d->c_mid + d->c_in; c.N = d->c_out; c.a_ld = d->c_mid; c.out_ld = d->c_out;
+    c.a2_kb = d->c_mid / 64;
+    if (!tmap2(&c.tmap_s[0], S2 > 1 ? xs : x, d->c_in, (uint64_t)pxo, 64, 128)) return LASNET_ERR_CUDA;
     if (run_conv(d, CONV3_DENSE, c, pxo, x, y, nullptr, h2, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
     g_last_launches = launches + 2;
     return LASNET_OK;

@@ -39,4 +39,18 @@ cudaError_t launch_subsample(const void *in, void *out, int n_img, int Ho, int W
                     static_cast<uint4 *>(out), n_img, Ho, Wo, c_bytes / 16, stride);
 }
 
+// out[i] = a[i] + b[i] (fp32): the conv3 and shortcut biases of a projection block,
+// applied once by the K-concatenated GEMM.
+__global__ void add_bias_kernel(const float *__restrict__ a, const float *__restrict__ b, float *__restrict__ out,
+                                int n) {
+    pdl_wait();
+    pdl_trigger();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = a[i] + b[i];
+}
+
+cudaError_t launch_add_bias(const float *a, const float *b, float *out, int n, cudaStream_t st) {
+    return launch_k(add_bias_kernel, dim3((n + 255) / 256), dim3(256), 0, st, a, b, out, n);
+}
+
 }  // namespace lasnet

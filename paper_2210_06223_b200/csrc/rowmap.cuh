@@ -75,6 +75,7 @@ struct ConvArgs {
     int32_t dense_tiles;      // conv2 dense: M tiles
     int32_t cluster;          // fused conv2+conv3: CTAs per cluster sharing (multicasting) the weight loads
     int32_t conv_stride;      // dense 3x3: 2 = stride 2 through the four parity views tmap_s[(row odd) * 2 + (col odd)]
+    int32_t a2_kb;            // dense conv3: K-blocks >= a2_kb of A come from tmap_s[0] (K-concatenated sources)
     int32_t no_relu;          // 1: the epilogue stores acc + bias (+ residual) without ReLU (projection shortcut)
     int32_t pair;             // fused conv2+conv3: 2-SM UMMAs over CTA pairs (cluster = 2, weight boxes of half height)
     // masker fused into the dense conv1 (CONV1_DENSE_MASK): per pixel p the fp32
