@@ -508,6 +508,7 @@ PROJ_CASES = [
     (2, 14, 256, 128, 512, 2),   # stage 2
     (2, 14, 512, 256, 1024, 2),  # stage 3 (c_mid 256: conv1 with 256-column tiles)
     (3, 8, 128, 64, 128, 2),
+    (1, 14, 1024, 512, 2048, 2),  # stage 4
 ]
 
 

@@ -10,8 +10,9 @@ c_mid=128, bf16, in place):
   * steps 3-5 alone (lasnet_dyn_block) on synthetic cell masks with exactly
     floor(r*G+0.5) active cells per image, uniform and clustered families;
   * the dense comparator (lasnet_dense_block: the same kernels on every pixel).
-Each point: W warm-ups, then K timed runs, L2 flushed (256 MiB read) before
-each, CUDA events on the launching stream; median and p10/p90 reported, with
+Each point: the call captured once as a CUDA graph, W warm-up replays, then K
+timed replays, L2 flushed (256 MiB read) before each, CUDA events on the
+launching stream; median and p10/p90 reported, with
 the SURVEY 8(d) headline roofline time of the same mask.
 
   python tools/sweep.py [--s 1 2 4 7] [--r 0.1 ... 1.0] [--steps 20] [--out profiles/sweep_<tag>]
@@ -86,7 +87,11 @@ def main():
     rows = []
     dense_blk = L.DynBlock(L.BlockShape(n, h, w, c_in, c_mid, 1), wts, wm, 0.0)
     y2 = torch.empty_like(x)
-    dense = timed(lambda: dense_blk.dense(x, y2), lambda: flush.sum(), args.steps, args.warmup, stream)
+    dense_blk.dense(x, y2)
+    gd = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gd):
+        dense_blk.dense(x, y2)
+    dense = timed(gd.replay, lambda: flush.sum(), args.steps, args.warmup, stream)
     _, _, dwork, _ = bench.algorithmic_work(np.ones((n, h, w), np.uint8), n, h, w, c_in, c_mid, c_in, 1)
     t_dense_roof = max(dwork["bytes"] / (hbm * 1e9), dwork["flops"] / (tfl * 1e12)) * 1e3
     print(f"dense: {dense['p50']:.4f} ms (ideal {t_dense_roof:.4f} ms)", flush=True)
@@ -99,7 +104,9 @@ def main():
             row = {"S": s, "r_target": r}
             for name, blk in blks.items():
                 blk.calibrate_bias(xc, r)
-                row[name] = timed(lambda: blk.forward(y), prep, args.steps, args.warmup, stream)
+                g = blk.capture(y)  # timed as a CUDA-graph replay, as bench.py does
+                row[name] = timed(g.replay, prep, args.steps, args.warmup, stream)
+                del g
             # masker-driven mask of the timed input (same for both schedules)
             blks["fused"].forward(y.copy_(x))
             torch.cuda.synchronize()
@@ -114,7 +121,12 @@ def main():
                 cm = synth.make_cell_mask(n, shape.gh, shape.gw, r, seed=2, family=fam)
                 mt = torch.from_numpy(cm).cuda()
                 B.compact(mt, convs.idx, convs.count)
-                row["convs_" + fam] = timed(lambda: convs.convs(y), prep, args.steps, args.warmup, stream)
+                convs.convs(y)
+                gc = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gc):
+                    convs.convs(y)
+                row["convs_" + fam] = timed(gc.replay, prep, args.steps, args.warmup, stream)
+                del gc
             row["dense"] = dense["p50"]
             best = min(row["separate"]["p50"], row["fused"]["p50"])
             row["speedup_vs_dense"] = dense["p50"] / best
