@@ -152,3 +152,42 @@ def test_missing_library_fails_loudly(tmp_path):
             _lib.load(str(tmp_path / "nope.so"))
         finally:
             _lib._lib = _lib._lib_backup
+
+
+def test_network_layer_entry_points_validate_before_launch(lib):
+    """lasnet_proj_block / lasnet_stem / lasnet_maxpool / lasnet_head reject bad
+    arguments on the host with the documented status (nothing launched)."""
+    ST = {v: k for k, v in _lib.STATUS.items()}
+    z = ctypes.c_void_p(0)
+    # projection block: missing shortcut weights -> ERR_NULL; fp32 -> UNSUPPORTED; c_out % 128 -> UNSUPPORTED
+    d = desc(c_in=256, c_mid=64, c_out=512, stride=2, h=7, w=7)
+    w_no_ds = _lib.BlockWeights(FAKE.value, FAKE.value, FAKE.value, FAKE.value, FAKE.value, FAKE.value, None, None)
+    w_ok = _lib.BlockWeights(*([FAKE.value] * 8))
+    assert lib.lasnet_proj_block(ctypes.byref(d), ctypes.byref(w_no_ds), FAKE, FAKE, FAKE, 1 << 30, z) == \
+        ST["LASNET_ERR_NULL"]
+    d32 = desc(c_in=256, c_mid=64, c_out=512, stride=2, h=7, w=7, dtype=_lib.LASNET_F32)
+    assert lib.lasnet_proj_block(ctypes.byref(d32), ctypes.byref(w_ok), FAKE, FAKE, FAKE, 1 << 30, z) == \
+        ST["LASNET_ERR_UNSUPPORTED"]
+    dbad = desc(c_in=256, c_mid=64, c_out=320, stride=2, h=7, w=7)
+    assert lib.lasnet_proj_block(ctypes.byref(dbad), ctypes.byref(w_ok), FAKE, FAKE, FAKE, 1 << 30, z) == \
+        ST["LASNET_ERR_UNSUPPORTED"]
+    dst3 = desc(stride=3)
+    assert lib.lasnet_proj_block(ctypes.byref(dst3), ctypes.byref(w_ok), FAKE, FAKE, FAKE, 1 << 30, z) == \
+        ST["LASNET_ERR_DOMAIN"]
+    far = ctypes.c_void_p(FAKE.value + (1 << 32))  # a y that does not overlap x
+    assert lib.lasnet_proj_block(ctypes.byref(d), ctypes.byref(w_ok), FAKE, far, FAKE, 0, z) == \
+        ST["LASNET_ERR_WORKSPACE"]
+    # overlapping x / y -> ERR_ALIAS
+    assert lib.lasnet_proj_block(ctypes.byref(d), ctypes.byref(w_ok), FAKE, ctypes.c_void_p(FAKE.value + 64), FAKE,
+                                 1 << 30, z) == ST["LASNET_ERR_ALIAS"]
+    assert lib.lasnet_proj_workspace_bytes(ctypes.byref(d)) > 0
+    # stem: w % 4 -> UNSUPPORTED, null -> NULL, no workspace -> WORKSPACE
+    assert lib.lasnet_stem(2, 112, 110, FAKE, FAKE, FAKE, FAKE, FAKE, 1 << 20, z) == ST["LASNET_ERR_UNSUPPORTED"]
+    assert lib.lasnet_stem(2, 112, 112, None, FAKE, FAKE, FAKE, FAKE, 1 << 20, z) == ST["LASNET_ERR_NULL"]
+    assert lib.lasnet_stem(2, 112, 112, FAKE, FAKE, FAKE, FAKE, FAKE, 16, z) == ST["LASNET_ERR_WORKSPACE"]
+    assert lib.lasnet_stem_workspace_bytes() == 64 * 448 * 2
+    # max pool: c % 8 -> UNSUPPORTED; head: bad sizes -> SHAPE, small workspace -> WORKSPACE
+    assert lib.lasnet_maxpool(2, 56, 56, 60, FAKE, FAKE, z) == ST["LASNET_ERR_UNSUPPORTED"]
+    assert lib.lasnet_head(2, 49, 0, 1000, FAKE, FAKE, FAKE, FAKE, FAKE, 1 << 20, z) == ST["LASNET_ERR_SHAPE"]
+    assert lib.lasnet_head(2, 49, 2048, 1000, FAKE, FAKE, FAKE, FAKE, FAKE, 8, z) == ST["LASNET_ERR_WORKSPACE"]
+    assert lib.lasnet_head_workspace_bytes(2, 2048) == 2 * 2048 * 4
