@@ -40,24 +40,27 @@ __global__ void __launch_bounds__(256) maxpool_kernel(const uint4 *__restrict__ 
         const int v = (int)(i % vpp);
         const long p = i / vpp;
         const int ox = (int)(p % Wo);
-        const long q = p / Wo;
-        const int oy = (int)(q % Ho), n = (int)(q / Ho);
+        const long pr = p / Wo;
+        const int oy = (int)(pr % Ho), n = (int)(pr / Ho);
+        // all nine loads issued before the maxima (out-of-image taps load nothing and never win)
+        uint4 q[9];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+            const int yy = 2 * oy + t / 3 - 1, xx = 2 * ox + t % 3 - 1;
+            const bool ok = yy >= 0 && yy < Hi && xx >= 0 && xx < Wi;
+            q[t] = ok ? __ldg(x + (((long)n * Hi + yy) * Wi + xx) * vpp + v) : make_uint4(0xFF80FF80u, 0xFF80FF80u,
+                                                                                          0xFF80FF80u, 0xFF80FF80u);
+        }
         float m[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) m[e] = -INFINITY;
-        for (int dy = -1; dy <= 1; ++dy) {
-            const int yy = 2 * oy + dy;
-            if (yy < 0 || yy >= Hi) continue;
-            for (int dx = -1; dx <= 1; ++dx) {
-                const int xx = 2 * ox + dx;
-                if (xx < 0 || xx >= Wi) continue;
-                const uint4 q4 = __ldg(x + (((long)n * Hi + yy) * Wi + xx) * vpp + v);
-                const uint32_t u[4] = {q4.x, q4.y, q4.z, q4.w};
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    m[2 * e] = fmaxf(m[2 * e], __uint_as_float(u[e] << 16));
-                    m[2 * e + 1] = fmaxf(m[2 * e + 1], __uint_as_float(u[e] & 0xFFFF0000u));
-                }
+        for (int t = 0; t < 9; ++t) {
+            const uint32_t u[4] = {q[t].x, q[t].y, q[t].z, q[t].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                m[2 * e] = fmaxf(m[2 * e], __uint_as_float(u[e] << 16));
+                m[2 * e + 1] = fmaxf(m[2 * e + 1], __uint_as_float(u[e] & 0xFFFF0000u));
             }
         }
         uint32_t o[4];
@@ -72,7 +75,7 @@ cudaError_t launch_maxpool(const void *x, void *y, int n_img, int Ho, int Wo, in
     const long total = (long)n_img * Ho * Wo * (c / 8);
     if (total == 0) return cudaSuccess;
     long grid = (total + 255) / 256;
-    if (grid > 8L * num_sms) grid = 8L * num_sms;
+    if (grid > 32L * num_sms) grid = 32L * num_sms;
     return launch_k(maxpool_kernel, dim3((unsigned)grid), dim3(256), 0, st, static_cast<const uint4 *>(x),
                     static_cast<uint4 *>(y), n_img, Ho, Wo, c / 8);
 }
