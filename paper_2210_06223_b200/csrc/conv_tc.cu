@@ -82,7 +82,11 @@ template <int MODE, int BN> struct Cfg {
     static constexpr int kThreads =
         32 * (kEpiWarps + 2) + (kGather ? kGatherThreads : 0) + (kMasker ? kMaskerThreads : 0);
     static constexpr int kBBytes = BN * kBK * 2;
-    static constexpr int kStageBytes = kABytes + kBBytes;
+    // stem: the whole packed weight (7 K-blocks of 64 x 64, 56 KB) stays resident in smem,
+    // loaded once per CTA; its stages carry A only (it was L2-throughput bound re-streaming it)
+    static constexpr bool kBRes = MODE == STEM;
+    static constexpr int kBResBytes = kBRes ? 7 * kBBytes : 0;
+    static constexpr int kStageBytes = kABytes + (kBRes ? 0 : kBBytes);
     static constexpr int kStagingBytes = (BN / 64) * kChunkBytes;
     // conv1 dyn: HBM gather -> deep pipeline, 1 staging buffer (TMA store drains fast)
     // conv3: short K (2-8 blocks) -> 3 stages, 3 staging buffers (residual prefetched 2 tiles ahead)
@@ -94,7 +98,7 @@ template <int MODE, int BN> struct Cfg {
     static constexpr int kStages =
         BN == 256 ? 3 : (kGather ? (BN == 128 ? 6 : 8) : (kResid ? 3 : (BN == 128 ? 4 : 6)));
     static constexpr int kTmemCols = 2 * BN;
-    static constexpr int kStageOff = 0;  // [stages][staging][barriers][bias (+wm)]
+    static constexpr int kStageOff = kBResBytes;  // [resident B][stages][staging][barriers][bias (+wm)]
     static constexpr int kStagingOff = kStageOff + kStages * kStageBytes;
     static constexpr int kBarOff = kStagingOff + kStaging * kStagingBytes;
     static constexpr int kBiasOff = kBarOff + 256;
@@ -157,6 +161,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
     const uint32_t bar_tfull = bar_empty + ST * 8;    // 2
     const uint32_t bar_tempty = bar_tfull + 16;       // 2
     const uint32_t bar_sempty = bar_tempty + 16;      // 2 (TMA-store modes: staging free again)
+    const uint32_t bar_bres = bar_sempty + 16;        // 1 (stem: resident weights landed)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sgen + C::kBarOff + ST * 16 + 64);
     float *bias_s = reinterpret_cast<float *>(sgen + C::kBiasOff);
 
@@ -179,6 +184,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             mbar_init(bar_tempty + 8 * a, EPI);  // every epilogue thread
             mbar_init(bar_sempty + 8 * a, 1);    // store thread, after the TMA store read smem
         }
+        mbar_init(bar_bres, 1);
         fence_mbar_init();
     }
     if (warp == C::kProdWarp && lane == 0) {
@@ -202,6 +208,10 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
     if (warp == C::kProdWarp) {
         // --------------------------------------------------- TMA producer --
         if (lane == 0) {
+            if (C::kBRes) {
+                mbar_arrive_expect_tx(bar_bres, (uint32_t)(num_kb * C::kBBytes));
+                for (int kb = 0; kb < num_kb; ++kb) tma_load_2d(sbase + kb * C::kBBytes, &args.tmap_b, bar_bres, kb * kBK, 0);
+            }
             int it = 0, lt = 0;
             for (int tile = blockIdx.x; tile < geo.num_tiles; tile += gridDim.x, ++lt) {
                 const int mt = tile / geo.n_tiles_n;
@@ -220,8 +230,8 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     if (C::kGather) a_bytes = 0;
                     else if (MODE == STEM) a_bytes = 4 * (args.W / 4) * 128;
                     else if (MODE == CONV2_DYN || MODE == CONV2_DENSE) a_bytes = args.box_rows * 128;
-                    mbar_arrive_expect_tx(fb, a_bytes + C::kBBytes);
-                    tma_load_2d(sb, &args.tmap_b, fb, kb * kBK, n0);
+                    mbar_arrive_expect_tx(fb, a_bytes + (C::kBRes ? 0 : C::kBBytes));
+                    if (!C::kBRes) tma_load_2d(sb, &args.tmap_b, fb, kb * kBK, n0);
                     KTRACE(it, 1);
                     if (MODE == CONV2_DYN) {
                         const int tap = kb / kpt, dy = tap / 3, dx = tap - dy * 3;
@@ -374,6 +384,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
         // ---------------------------------------------------- MMA issuer --
         if (lane == 0) {
             constexpr uint32_t idesc = idesc_bf16_f32(kBM, BN);
+            if (C::kBRes) mbar_wait(bar_bres, 0);
             int it = 0, lt = 0;
             for (int tile = blockIdx.x; tile < geo.num_tiles; tile += gridDim.x, ++lt) {
                 const int acc = lt & 1;
@@ -389,7 +400,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     tc_fence_after();
                     const uint32_t sa = sbase + C::kStageOff + stage * C::kStageBytes;
                     const uint64_t adesc = smem_desc_sw128(sa);
-                    const uint64_t bdesc = smem_desc_sw128(sa + kABytes);
+                    const uint64_t bdesc = smem_desc_sw128(C::kBRes ? sbase + kb * C::kBBytes : sa + kABytes);
 #pragma unroll
                     for (int kk = 0; kk < kBK / 16; ++kk)
                         mma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kb | kk) != 0);
