@@ -418,9 +418,17 @@ def run_lasnet(args):
     tot_max, e2e_max, dense_max = ldist.max_over_ranks([tot_ms, e2e_ms, statistics.fmean(dense_ms)], device="cuda")
     net_info = None
     if args.network:
+        err = None
         try:
             nd, nn_, n_loc, nrate = network_measure(world, max(5, min(K, 10)))
-            nd_max, nn_max = ldist.max_over_ranks([nd, nn_], device="cuda")
+        except Exception as e:  # the block headline above stands on its own
+            nd = nn_ = float("inf")
+            n_loc, nrate, err = 256 // world, 0.0, f"{type(e).__name__}: {e}"[:300]
+        # every rank joins the reduction, failed or not (a rank skipping it would hang the others)
+        nd_max, nn_max = ldist.max_over_ranks([nd, nn_], device="cuda")
+        if err is not None or nd_max == float("inf"):
+            net_info = {"error": err or "failed on another rank"}
+        else:
             net_info = {"model": "LAS-ResNet-101 (S_net 4-4-2-1, projection blocks static)", "image": "224x224",
                         "global_batch": n_loc * world, "per_gpu_batch": n_loc, "r_target": 0.5,
                         "r_patch_mean": round(nrate, 4), "ms_per_forward": round(nd_max, 4),
@@ -429,8 +437,6 @@ def run_lasnet(args):
                         "dense_identity_images_per_s": round(n_loc * world / (nn_max * 1e-3), 1),
                         "speedup_vs_dense": round(nn_max / nd_max, 3),
                         "timing": "CUDA events around one CUDA-graph replay of the whole forward, median, max over ranks"}
-        except Exception as e:  # the block headline above stands on its own
-            net_info = {"error": f"{type(e).__name__}: {e}"[:300]}
     # the exchange step of SURVEY 8(e): summed active-cell statistics and per-rank step times
     act_all, cells_all = ldist.sum_over_ranks([stats["P"], mask_cells.size], device="cuda")
     rank_ms = [t / K for t in ldist.gather_over_ranks(tot_ms, device="cuda")]
