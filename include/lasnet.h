@@ -207,8 +207,10 @@ size_t lasnet_head_workspace_bytes(int32_t n, int32_t c);
  *   P:336-342; sec. 3.4; App. B): the masker is fused into a
  *   STATIC conv1 that reads x once and computes h1 on every pixel together with
  *   the masker's per-pixel partial logits; one launch then decides every cell,
- *   compacts the indices and gathers the h1 halos of the active patches (the
- *   "gather fused into the 3x3 conv" of Table 1 feeds conv2 from them); conv2 +
+ *   a second compacts the indices; conv2 reads the (s+2)^2 h1 halo of every
+ *   active patch straight out of the dense h1 (the "gather fused into the 3x3
+ *   conv" of Table 1: one TMA box per patch and K-block, zero-filled outside the
+ *   image) when c_mid <= 128 and s >= 2, else from a gathered copy; conv2 +
  *   conv3 + scatter-add as in lasnet_dyn_block.  bf16 only.
  * Both produce bit-identical mask / idx / count (the decision rule is the one
  * of lasnet_mask: certified fp32 with an exact fp64 re-sum when the bound does

@@ -206,7 +206,45 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
     for (int t = cl * CL; t < num_tiles; t += ncl * CL) ++ntl;
     auto tile_of = [&](int i) { return (cl + i * ncl) * CL + rank; };
 
-    if (warp == kProdWarp) {
+    if (warp == kProdWarp && !DENSE && args.direct) {
+        // ------------------- conv2 TMA producer, direct from the dense h1 --
+        // lane u owns patch u of the tile: one {64, S, S} box per K-block at the
+        // cell's halo origin (TMA zero-fills the halo outside the image)
+        int it = 0;
+        const int ss128 = args.S * args.S * 128;
+        const int cnt = *args.count;
+        // the next tile's cell ids are loaded while this tile's boxes are issued
+        auto ids_of = [&](int i) {
+            const int t = tile_of(i) * args.units_per_tile + lane;
+            return (i < ntl && lane < args.units_per_tile && t < cnt) ? __ldg(args.idx + t) : -1;
+        };
+        int next = ids_of(0);
+        for (int i = 0; i < ntl; ++i) {
+            const int t0 = tile_of(i) * args.units_per_tile;
+            const int nval = min(args.units_per_tile, cnt - t0);
+            const int cell = next;
+            next = ids_of(i + 1);
+            int n = 0, y0 = 0, x0 = 0;
+            if (cell >= 0) {
+                int gy, gx;
+                cell_decode(args, cell, n, gy, gx);
+                y0 = gy * args.S - 1;
+                x0 = gx * args.S - 1;
+            }
+            for (int kb = 0; kb < kb2; ++kb, ++it) {
+                const int st = it % kStages;
+                const uint32_t sa = sbase + st * kStageBytes, fb = bar_full + 8 * st;
+                const int tap = kb / kpt, dy = tap / 3, dx = tap - dy * 3, c0 = (kb - tap * kpt) * kBK;
+                if (lane == 0) {
+                    mbar_wait(bar_empty + 8 * st, ((it / kStages) & 1) ^ 1);
+                    mbar_arrive_expect_tx(fb, nval * ss128 + KC * 128);
+                    tma_load_2d(sa + kABytes, &args.tmap_b, fb, kb * kBK, 0);
+                }
+                __syncwarp();
+                if (lane < nval) tma_load_5d(sa + lane * ss128, &args.tmap_a, fb, 0, x0 + dx, y0 + dy, n, c0 >> 6);
+            }
+        }
+    } else if (warp == kProdWarp) {
         // ------------------------------------------ conv2 TMA producer --
         int it = 0;
         for (int i = 0; i < ntl; ++i) {

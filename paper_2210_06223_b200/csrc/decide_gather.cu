@@ -263,13 +263,30 @@ __global__ void __launch_bounds__(256) compact_gather_kernel(const GatherArgs a)
     }
 }
 
+// Compaction only (the direct schedule, no gather): one warp per 32-cell group
+// writes the ids of its active cells at the group's prefix.
+__global__ void __launch_bounds__(256) compact_idx_kernel(const uint8_t *__restrict__ dec, const int32_t *__restrict__ gpre,
+                                                          int32_t *__restrict__ idx, int ncells, int ngroups) {
+    pdl_wait();
+    pdl_trigger();
+    const int lane = threadIdx.x & 31;
+    const int g = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (g >= ngroups) return;
+    const int cell = g * 32 + lane;
+    const int d = cell < ncells ? dec[cell] : 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, d);
+    if (d) idx[gpre[g] + __popc(bal & ((1u << lane) - 1u))] = cell;
+}
+
 size_t decide_sync_bytes(int ncells, int) {
     // done counter (16 B) + decisions (ncells) + group prefixes (ngroups ints)
     const long ngroups = ((long)ncells + 31) / 32;
     return 16 + ((size_t)ncells + 15) / 16 * 16 + (size_t)ngroups * 4;
 }
 
-// sync: decide_sync_bytes() bytes whose first 16 are zero (left zero)
+// sync: decide_sync_bytes() bytes whose first 16 are zero (left zero).
+// h1d == nullptr: decisions, prefixes and count only; h1g == nullptr: + ids;
+// else + ids and the halo gather of h1d into h1g.
 cudaError_t launch_decide_gather(const float4 *mpart, const void *x, const float *wm, float bm, int n_img, int H,
                                  int W, int c_in, int S, uint8_t *mask, int32_t *idx, int32_t *count, void *sync,
                                  const void *h1d, void *h1g, int c_mid, int cap, int num_sms, cudaStream_t st) {
@@ -297,6 +314,10 @@ cudaError_t launch_decide_gather(const float4 *mpart, const void *x, const float
     a.count = count;
     cudaError_t e = launch_k(decide_kernel, dim3((a.ncells + kDecThreads - 1) / kDecThreads), dim3(kDecThreads), 0, st, a);
     if (e != cudaSuccess || h1d == nullptr) return e;
+    if (h1g == nullptr)  // ids only: steps 4-5 read the dense h1 directly
+        return launch_k(compact_idx_kernel, dim3((unsigned)((a.ngroups + 7) / 8)), dim3(256), 0, st,
+                        static_cast<const uint8_t *>(a.dec), static_cast<const int32_t *>(a.gpre), idx, a.ncells,
+                        a.ngroups);
     GatherArgs g;
     g.dec = a.dec;
     g.gpre = a.gpre;

@@ -299,6 +299,18 @@ bool use_fused23(const lasnet_block_desc *d) {
            d->c_out <= 512 && d->c_out >= 192;
 }
 
+// Masker-fused schedule: the fused conv23 reads its patches straight from the
+// dense h1 (one TMA box per active cell and K-block) instead of a gathered copy,
+// for S >= 2 (S = 1 would take 128 boxes per K-block).  LASNET_GATHER=1 in the
+// environment keeps the gather (A/B measurements).
+bool use_direct(const lasnet_block_desc *d) {
+    static const bool off = [] {
+        const char *e = getenv("LASNET_GATHER");
+        return e && e[0] == '1';
+    }();
+    return !off && use_fused23(d) && d->s >= 2;
+}
+
 cudaError_t run_conv23(const lasnet_block_desc *d, bool dense, ConvArgs a, const lasnet_block_weights *w,
                        const void *x, void *y, const void *h1, int cap, cudaStream_t st) {
     const int S = d->s, hs = S + 2, C = d->c_mid;
@@ -317,8 +329,8 @@ cudaError_t run_conv23(const lasnet_block_desc *d, bool dense, ConvArgs a, const
         const char *e = getenv("LASNET_C23_PAIR");
         return e && e[0] == '1';
     }();
-    a.pair = pair_env ? 1 : 0;
-    a.cluster = a.pair ? 2 : (C / cl_env >= 8 && nc3 / cl_env >= 8) ? cl_env : 1;
+    a.pair = pair_env && !a.direct ? 1 : 0;
+    a.cluster = a.direct ? 1 : a.pair ? 2 : (C / cl_env >= 8 && nc3 / cl_env >= 8) ? cl_env : 1;
     bool ok = tmap2(&a.tmap_b, a.w, a.K, a.N, 64, C / a.cluster) && tmap2(&a.tmap_b3, w->w3, C, d->c_out, 64, nc3 / a.cluster);
     int tiles;
     if (dense) {
@@ -338,8 +350,12 @@ cudaError_t run_conv23(const lasnet_block_desc *d, bool dense, ConvArgs a, const
     } else {
         a.units_per_tile = 128 / (S * S);
         a.box_rows = a.units_per_tile * S * S;
-        ok = ok && tmap5(&a.tmap_a, h1, {64, (uint64_t)hs, (uint64_t)hs, (uint64_t)cap, (uint64_t)(C / 64)},
-                         {64, (uint32_t)S, (uint32_t)S, (uint32_t)a.units_per_tile, 1});
+        if (a.direct)  // dense h1 [C/64][N][H][W][64], one {64, S, S} box per active cell
+            ok = ok && tmap5(&a.tmap_a, h1, {64, (uint64_t)d->w, (uint64_t)d->h, (uint64_t)d->n, (uint64_t)(C / 64)},
+                             {64, (uint32_t)S, (uint32_t)S, 1, 1});
+        else
+            ok = ok && tmap5(&a.tmap_a, h1, {64, (uint64_t)hs, (uint64_t)hs, (uint64_t)cap, (uint64_t)(C / 64)},
+                             {64, (uint32_t)S, (uint32_t)S, (uint32_t)a.units_per_tile, 1});
         tiles = (cap + a.units_per_tile - 1) / a.units_per_tile;
     }
     if (!ok) return cudaErrorInvalidValue;
@@ -412,7 +428,7 @@ size_t fwd_ws(const lasnet_block_desc *d, int schedule, uint8_t *base, FwdWs *o)
         r.sync = cv.take(decide_sync_bytes((int)ncells, num_sms()));
         r.mpart = cv.take(px * 16);
         r.h1d = cv.take(px * d->c_mid * e);
-        r.h1g = cv.take((size_t)ncells * (d->s + 2) * (d->s + 2) * d->c_mid * e);
+        r.h1g = use_direct(d) ? nullptr : cv.take((size_t)ncells * (d->s + 2) * (d->s + 2) * d->c_mid * e);
         r.h2 = use_fused23(d) ? nullptr : cv.take((size_t)ncells * d->s * d->s * d->c_mid * e);
     } else {
         r.sync = cv.take(mask_compact_workspace_bytes(ncells));
@@ -693,8 +709,14 @@ lasnet_status lasnet_block_forward(const lasnet_block_desc *d, const lasnet_bloc
     b.idx = idx;
     b.count = count;
     int k = 0;
-    if (run_steps45(d, w, b, x, y, r.h1g, r.h2, ncells, st, &k) != cudaSuccess) return LASNET_ERR_CUDA;
-    g_last_launches = 3 + k;  // conv1+masker, decide, compact+gather, steps 4-5
+    if (r.h1g == nullptr) {  // direct: steps 4-5 read the dense h1
+        b.direct = 1;
+        k = 1;
+        if (run_conv23(d, false, b, w, x, y, r.h1d, ncells, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    } else if (run_steps45(d, w, b, x, y, r.h1g, r.h2, ncells, st, &k) != cudaSuccess) {
+        return LASNET_ERR_CUDA;
+    }
+    g_last_launches = 3 + k;  // conv1+masker, decide, compaction (+ gather), steps 4-5
     return LASNET_OK;
 }
 
@@ -893,7 +915,8 @@ int32_t lasnet_choose_schedule(const lasnet_block_desc *d, double r) {
     const double xb = px * d->c_in * 2.0, h1b = px * d->c_mid * 2.0;
     const double halo = hs2 / (S * S);
     const double sep = xb + r * halo * xb;
-    const double fused = xb + h1b + r * halo * h1b * 2.0;
+    // fused: h1 written once, then its halos read (direct) or gathered, written and read again
+    const double fused = xb + h1b + r * halo * h1b * (use_direct(d) ? 1.0 : 2.0);
     return fused < sep ? LASNET_SCHED_MASKER_FUSED : LASNET_SCHED_MASKER_SEPARATE;
 }
 
