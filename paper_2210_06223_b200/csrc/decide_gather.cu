@@ -83,75 +83,85 @@ __device__ double cell_exact(const DecideArgs &a, int n, int y0, int x0, int ch,
     return s;
 }
 
+// Four lanes per cell (a quad): lane j of the quad sums the partials of the
+// cell's pixel rows j, j+4, ... in fp64, the quad combines them (fixed order).
+constexpr int kDecCells = kDecThreads / 4;  // cells per CTA (a multiple of 32)
+
 __global__ void __launch_bounds__(kDecThreads) decide_kernel(const DecideArgs a) {
-    __shared__ int s_unc[kDecThreads], s_nunc;
-    __shared__ uint8_t s_dec[kDecThreads];
+    __shared__ int s_unc[kDecCells], s_nunc;
+    __shared__ uint8_t s_dec[kDecCells];
     __shared__ int s_last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = a.Gh * a.Gw;
-    const int cell0 = blockIdx.x * kDecThreads;
+    const int cell0 = blockIdx.x * kDecCells;
+    const int lc = tid >> 2, q = tid & 3;  // local cell, lane in the quad
     pdl_wait();
     pdl_trigger();
     if (tid == 0) s_nunc = 0;
     __syncthreads();
 
     // certified decision per cell from the fused conv1's partials
-    const int cell = cell0 + tid;
+    const int cell = cell0 + lc;
     const bool valid = cell < a.ncells;
-    int dec = 0;
+    int n = 0, y0 = 0, x0 = 0, ch = 0, cw = 0;
+    double z = 0.0, m = 0.0;
     if (valid) {
-        const int n = cell / G, g = cell - n * G, gy = g / a.Gw, gx = g - gy * a.Gw;
-        const int y0 = gy * a.S, x0 = gx * a.S;
-        const int ch = min(y0 + a.S, a.H) - y0, cw = min(x0 + a.S, a.W) - x0;
-        double z = 0.0, m = 0.0;
-        // all loads of a batch of 16 pixels in flight before the (fixed-order) sums
-        const float4 *base = a.mpart + (size_t)(n * a.H + y0) * a.W + x0;
-        const int npix = ch * cw;
-        int py = 0, px = 0;
-        for (int p0 = 0; p0 < npix; p0 += 16) {
-            float4 v[16];
+        n = cell / G;
+        const int g = cell - n * G, gy = g / a.Gw, gx = g - gy * a.Gw;
+        y0 = gy * a.S;
+        x0 = gx * a.S;
+        ch = min(y0 + a.S, a.H) - y0;
+        cw = min(x0 + a.S, a.W) - x0;
+        for (int py = q; py < ch; py += 4) {  // rows q, q + 4, ...: a row's loads in flight first
+            const float4 *row = a.mpart + (size_t)(n * a.H + y0 + py) * a.W + x0;
+            for (int p0 = 0; p0 < cw; p0 += 8) {
+                float4 v[8];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (p0 + i < npix) {
-                    v[i] = __ldg(base + py * a.W + px);
-                    if (++px == cw) px = 0, ++py;
+                for (int i = 0; i < 8; ++i)
+                    v[i] = p0 + i < cw ? __ldg(row + p0 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    z += (double)v[i].x + (double)v[i].z;
+                    m += (double)v[i].y + (double)v[i].w;
                 }
             }
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                z += (double)v[i].x + (double)v[i].z;
-                m += (double)v[i].y + (double)v[i].w;
-            }
         }
+    }
+    z += __shfl_xor_sync(0xffffffffu, z, 1);
+    m += __shfl_xor_sync(0xffffffffu, m, 1);
+    z += __shfl_xor_sync(0xffffffffu, z, 2);
+    m += __shfl_xor_sync(0xffffffffu, m, 2);
+    int dec = 0;
+    if (valid && q == 0) {
         const double u32 = 5.9604644775390625e-8, u64 = 1.1102230246251565e-16;  // 2^-24, 2^-53
         const double n32 = (double)(a.c_in / 16 + 10), n64 = (double)(2 * ch * cw + 4);
         const double gam = n32 * u32 / (1.0 - n32 * u32) + n64 * u64 / (1.0 - n64 * u64);
         // m_p are fp32 sums (relative error <= c_in 2^-24 < 1e-3 for c_in < 16k): x1.01
         const double err = m * 1.01 * gam + 1e-300;
         z += (double)a.bm * (double)(ch * cw);
-        if (fabs(z) > err) {
-            dec = z > 0.0;
-        } else {
-            s_unc[atomicAdd(&s_nunc, 1)] = tid;
-        }
+        if (fabs(z) > err) dec = z > 0.0;
+        else s_unc[atomicAdd(&s_nunc, 1)] = lc;
+        s_dec[lc] = (uint8_t)dec;
     }
     __syncthreads();
     // exact re-sum of the undecided cells, one warp each (rare)
     for (int k = warp; k < s_nunc; k += kDecThreads / 32) {
         const int t = s_unc[k], c = cell0 + t;
-        const int n = c / G, g = c - n * G, gy = g / a.Gw, gx = g - gy * a.Gw;
-        const int y0 = gy * a.S, x0 = gx * a.S;
-        const int ch = min(y0 + a.S, a.H) - y0, cw = min(x0 + a.S, a.W) - x0;
-        const double sum = cell_exact(a, n, y0, x0, ch, cw, lane);
-        if (lane == 0) s_dec[t] = (sum / (double)(ch * cw) + (double)a.bm) > 0.0;
+        const int cn = c / G, g = c - cn * G, gy = g / a.Gw, gx = g - gy * a.Gw;
+        const int cy0 = gy * a.S, cx0 = gx * a.S;
+        const int cch = min(cy0 + a.S, a.H) - cy0, ccw = min(cx0 + a.S, a.W) - cx0;
+        const double sum = cell_exact(a, cn, cy0, cx0, cch, ccw, lane);
+        if (lane == 0) s_dec[t] = (sum / (double)(cch * ccw) + (double)a.bm) > 0.0;
     }
     __syncthreads();
-    for (int k = 0; k < s_nunc; ++k)
-        if (s_unc[k] == tid) dec = s_dec[tid];
-    if (valid) a.dec[cell] = (uint8_t)dec;
-    const unsigned bal = __ballot_sync(0xffffffffu, dec);
-    if (lane == 0 && cell0 / 32 + warp < a.ngroups) a.gpre[cell0 / 32 + warp] = __popc(bal);
+    // decisions out, one count per 32-cell group (warps 0 .. kDecCells/32 - 1)
+    if (tid < kDecCells) {
+        const int c = cell0 + tid;
+        const int d = c < a.ncells ? s_dec[tid] : 0;
+        if (c < a.ncells) a.dec[c] = (uint8_t)d;
+        const unsigned bal = __ballot_sync(0xffffffffu, d);
+        if (lane == 0 && cell0 / 32 + warp < a.ngroups) a.gpre[cell0 / 32 + warp] = __popc(bal);
+    }
 
     // the last CTA: exclusive prefix over the group counts, total count
     __syncthreads();
@@ -312,7 +322,7 @@ cudaError_t launch_decide_gather(const float4 *mpart, const void *x, const float
     a.dec = mask ? mask : decs;
     a.gpre = reinterpret_cast<int32_t *>(decs + ((size_t)a.ncells + 15) / 16 * 16);
     a.count = count;
-    cudaError_t e = launch_k(decide_kernel, dim3((a.ncells + kDecThreads - 1) / kDecThreads), dim3(kDecThreads), 0, st, a);
+    cudaError_t e = launch_k(decide_kernel, dim3((a.ncells + kDecCells - 1) / kDecCells), dim3(kDecThreads), 0, st, a);
     if (e != cudaSuccess || h1d == nullptr) return e;
     if (h1g == nullptr)  // ids only: steps 4-5 read the dense h1 directly
         return launch_k(compact_idx_kernel, dim3((unsigned)((a.ngroups + 7) / 8)), dim3(256), 0, st,
