@@ -210,7 +210,7 @@ size_t lasnet_head_workspace_bytes(int32_t n, int32_t c);
  *   a second compacts the indices; conv2 reads the (s+2)^2 h1 halo of every
  *   active patch straight out of the dense h1 (the "gather fused into the 3x3
  *   conv" of Table 1: one TMA box per patch and K-block, zero-filled outside the
- *   image) when c_mid <= 128 and s >= 2, else from a gathered copy; conv2 +
+ *   image) when c_mid <= 128 and s >= 4, else from a gathered copy; conv2 +
  *   conv3 + scatter-add as in lasnet_dyn_block.  bf16 only.
  * Both produce bit-identical mask / idx / count (the decision rule is the one
  * of lasnet_mask: certified fp32 with an exact fp64 re-sum when the bound does

@@ -60,27 +60,49 @@ __device__ __forceinline__ unsigned atom_add_acqrel(unsigned *p, unsigned v) {
     return old;
 }
 
-// exact fp64 sum_{p in Omega} sum_c wm_c x[p,c] of one cell by one warp (bf16 x
-// fp32 products are exact in fp64; lanes own 16-B channel vectors, fixed order)
-__device__ double cell_exact(const DecideArgs &a, int n, int y0, int x0, int ch, int cw, int lane) {
+// fp64 sum_{p in Omega} sum_c wm_c x[p,c] of one cell by the whole CTA (bf16 x
+// fp32 products are exact in fp64): thread t takes the 16-B channel vectors
+// t, t + 256, ... of the cell, four loads in flight, then a fixed-order warp and
+// CTA reduction.  Every thread calls it; the result is returned to all.
+__device__ double cell_exact(const DecideArgs &a, int n, int y0, int x0, int ch, int cw, double *s_red) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nvec = a.c_in / 8, total = ch * cw * nvec;  // 16-B vectors of the cell
     double s = 0.0;
-    const int nvec = a.c_in / 8;  // 16-B vectors per pixel
-    for (int py = 0; py < ch; ++py)
-        for (int px = 0; px < cw; ++px) {
-            const uint4 *row = reinterpret_cast<const uint4 *>(a.x + ((size_t)((n * a.H + y0 + py) * a.W) + x0 + px) * a.c_in);
-            for (int v = lane; v < nvec; v += 32) {
-                const uint4 q = __ldg(row + v);
-                const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
+    for (int i0 = tid; i0 < total; i0 += 4 * kDecThreads) {
+        uint4 q[4];
+        int v8[4];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const uint32_t b = (e & 1) ? (qq[e >> 1] >> 16) : (qq[e >> 1] & 0xFFFFu);
-                    s = fma((double)a.wm[8 * v + e], (double)__uint_as_float(b << 16), s);
-                }
+        for (int u = 0; u < 4; ++u) {
+            const int i = i0 + u * kDecThreads;
+            q[u] = make_uint4(0u, 0u, 0u, 0u);
+            v8[u] = 0;
+            if (i < total) {
+                const int p = i / nvec, v = i - p * nvec, py = p / cw, px = p - py * cw;
+                const uint4 *row = reinterpret_cast<const uint4 *>(
+                    a.x + ((size_t)((n * a.H + y0 + py) * a.W) + x0 + px) * a.c_in);
+                q[u] = __ldg(row + v);
+                v8[u] = 8 * v;
             }
         }
 #pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t qq[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {  // a zero vector (past the end) adds exact zeros
+                const uint32_t b = (e & 1) ? (qq[e >> 1] >> 16) : (qq[e >> 1] & 0xFFFFu);
+                s = fma((double)__ldg(a.wm + v8[u] + e), (double)__uint_as_float(b << 16), s);
+            }
+        }
+    }
+#pragma unroll
     for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    return s;
+    if (lane == 0) s_red[warp] = s;
+    __syncthreads();
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < kDecThreads / 32; ++w) t += s_red[w];
+    __syncthreads();  // s_red is reused by the next call
+    return t;
 }
 
 // Four lanes per cell (a quad): lane j of the quad sums the partials of the
@@ -144,14 +166,16 @@ __global__ void __launch_bounds__(kDecThreads) decide_kernel(const DecideArgs a)
         s_dec[lc] = (uint8_t)dec;
     }
     __syncthreads();
-    // exact re-sum of the undecided cells, one warp each (rare)
-    for (int k = warp; k < s_nunc; k += kDecThreads / 32) {
+    // fp64 re-sum of the undecided cells (rare), each by the whole CTA: one
+    // load round trip per 1024 vectors instead of a warp's serial pixel loop
+    __shared__ double s_red[kDecThreads / 32];
+    for (int k = 0; k < s_nunc; ++k) {
         const int t = s_unc[k], c = cell0 + t;
         const int cn = c / G, g = c - cn * G, gy = g / a.Gw, gx = g - gy * a.Gw;
         const int cy0 = gy * a.S, cx0 = gx * a.S;
         const int cch = min(cy0 + a.S, a.H) - cy0, ccw = min(cx0 + a.S, a.W) - cx0;
-        const double sum = cell_exact(a, cn, cy0, cx0, cch, ccw, lane);
-        if (lane == 0) s_dec[t] = (sum / (double)(cch * ccw) + (double)a.bm) > 0.0;
+        const double sum = cell_exact(a, cn, cy0, cx0, cch, ccw, s_red);
+        if (tid == 0) s_dec[t] = (sum / (double)(cch * ccw) + (double)a.bm) > 0.0;
     }
     __syncthreads();
     // decisions out, one count per 32-cell group (warps 0 .. kDecCells/32 - 1)

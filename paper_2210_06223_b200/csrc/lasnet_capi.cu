@@ -301,14 +301,15 @@ bool use_fused23(const lasnet_block_desc *d) {
 
 // Masker-fused schedule: the fused conv23 reads its patches straight from the
 // dense h1 (one TMA box per active cell and K-block) instead of a gathered copy,
-// for S >= 2 (S = 1 would take 128 boxes per K-block).  LASNET_GATHER=1 in the
+// for S >= 4: at most 8 boxes per K-block (S = 2 takes 32 small boxes and runs
+// slower than gather + one box, profiles/sweep_r1e.md).  LASNET_GATHER=1 in the
 // environment keeps the gather (A/B measurements).
 bool use_direct(const lasnet_block_desc *d) {
     static const bool off = [] {
         const char *e = getenv("LASNET_GATHER");
         return e && e[0] == '1';
     }();
-    return !off && use_fused23(d) && d->s >= 2;
+    return !off && use_fused23(d) && d->s >= 4;
 }
 
 cudaError_t run_conv23(const lasnet_block_desc *d, bool dense, ConvArgs a, const lasnet_block_weights *w,

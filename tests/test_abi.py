@@ -134,7 +134,7 @@ def test_block_forward_workspace_and_schedule_choice(lib):
     px, cells = 128 * 28 * 28, 128 * 7 * 7
     fused = lib.lasnet_block_forward_workspace_bytes(ctypes.byref(d), _lib.SCHED_FUSED)
     # mpart + dense h1 dominate (conv2 reads its halos straight from the dense h1
-    # at c_mid <= 128, s >= 2: no gathered copy); control words are small
+    # at c_mid <= 128, s >= 4: no gathered copy); control words are small
     assert fused >= px * 16 + px * 128 * 2
     assert fused < px * 16 + px * 128 * 2 + 64 * 1024
     # s = 1: conv2 reads a gathered copy of the 3x3 halos of every cell

@@ -10,7 +10,7 @@ timeout -s KILL 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dr
 timeout -s KILL 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 200 --csv \
    --log-file gpurun_out/launches_${TAG}_sep.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --schedule separate > gpurun_out/ncu_launch_${TAG}_sep.log 2>&1
 timeout -s KILL 900 ncu --set full --clock-control none --import-source on \
-   -k regex:"conv_tc_kernel|conv23_kernel|decide|gather|masker" -s 6 -c 6 -o gpurun_out/full_${TAG} \
+   -k regex:"conv_tc_kernel|conv23_kernel|decide|gather|compact_idx|masker" -s 8 -c 8 -o gpurun_out/full_${TAG} \
    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --schedule fused > gpurun_out/ncu_full_${TAG}.log 2>&1
 timeout -s KILL 900 ncu --set full --clock-control none --import-source on \
    -k regex:"masker_compact|conv_tc_kernel" -s 4 -c 2 -o gpurun_out/full_${TAG}_sep \

@@ -12,7 +12,7 @@ c_mid=128, bf16, in place):
   * the dense comparator (lasnet_dense_block: the same kernels on every pixel).
 Each point: the call captured once as a CUDA graph, W warm-up replays, then K
 timed replays, L2 flushed (256 MiB read) before each, CUDA events on the
-launching stream; median and p10/p90 reported, with
+launching stream; mean (event pairs are quantised to 4.096 us), median and p10/p90 reported, with
 the SURVEY 8(d) headline roofline time of the same mask.
 
   python tools/sweep.py [--s 1 2 4 7] [--r 0.1 ... 1.0] [--steps 20] [--out profiles/sweep_<tag>]
@@ -51,7 +51,10 @@ def timed(fn, prep, steps, warmup, stream):
         ev.append((a, b))
     torch.cuda.synchronize()
     ms = sorted(a.elapsed_time(b) for a, b in ev)
-    return {"p50": statistics.median(ms), "p10": float(np.percentile(ms, 10)), "p90": float(np.percentile(ms, 90))}
+    # single-replay event pairs are quantised (4.096 us steps observed on the B200 boxes):
+    # the headline "p50" is the mean over the samples, which the run-to-run jitter dithers
+    return {"p50": statistics.fmean(ms), "median": statistics.median(ms), "p10": float(np.percentile(ms, 10)),
+            "p90": float(np.percentile(ms, 90))}
 
 
 def main():
@@ -62,7 +65,7 @@ def main():
     ap.add_argument("--hw", type=int, default=28)
     ap.add_argument("--c-in", type=int, default=512)
     ap.add_argument("--c-mid", type=int, default=128)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep"))
     args = ap.parse_args()
@@ -145,7 +148,8 @@ def main():
     with open(args.out + ".md", "w") as f:
         f.write(f"# Block latency vs activation rate and S ({out['device']})\n\n")
         f.write(f"Workload: N={n}, {h}x{w}x{c_in}, c_mid={c_mid}, bf16, in place, L2 flushed before every run; "
-                f"median of {args.steps} (p10-p90 in the JSON). Masker-driven rows: masker bias calibrated on a "
+                f"mean of {args.steps} single-replay event timings (quantised to 4.096 us on these boxes; median, "
+                f"p10-p90 in the JSON). Masker-driven rows: masker bias calibrated on a "
                 f"separate batch. convs-*: steps 3-5 only (lasnet_dyn_block) on synthetic masks. Dense comparator "
                 f"(same kernels on every pixel): {dense['p50'] * 1e3:.1f} us. T_roof: SURVEY 8(d) headline "
                 f"definition at {hbm:.0f} GB/s / {tfl:.0f} TFLOP/s ({psrc}).\n\n")
