@@ -29,7 +29,8 @@ def short(name):
              ("conv23_kernel<0", "conv23_dyn"), ("conv23_kernel<false", "conv23_dyn"),
              ("conv23_kernel<1", "conv23_dense"), ("conv23_kernel<true", "conv23_dense"),
              ("masker_compact_kernel", "mask_compact"), ("masker_kernel", "mask"), ("compact_kernel", "compact"),
-             ("decide_kernel", "decide"), ("compact_gather_kernel", "compact_gather")]
+             ("decide_kernel", "decide"), ("compact_gather_kernel", "compact_gather"),
+             ("compact_idx_kernel", "compact_idx")]
     for k, v in table:
         if k in n:
             return v
@@ -98,7 +99,7 @@ def full(rep):
 
 lf = launches(os.path.join(GO, f"launches_{tag}.csv"))
 lsep = launches(os.path.join(GO, f"launches_{tag}_sep.csv"))
-step_f = last_step(lf, "conv1_mask", ("decide", "compact_gather", "conv23_dyn", "conv2_dyn", "conv3_dyn"))
+step_f = last_step(lf, "conv1_mask", ("decide", "compact_gather", "compact_idx", "conv23_dyn", "conv2_dyn", "conv3_dyn"))
 step_s = last_step(lsep, "mask_compact", ("conv1_dyn", "conv23_dyn", "conv2_dyn", "conv3_dyn"))
 dense = last_step(lf, "conv1_dense", ("conv23_dense", "conv2_dense", "conv3_dense"))
 full_f = full(os.path.join(GO, f"full_{tag}.ncu-rep"))
@@ -107,8 +108,9 @@ full_s = full(os.path.join(GO, f"full_{tag}_sep.ncu-rep")) if os.path.exists(os.
 fullk = {}
 for d in full_f + full_s:
     fullk.setdefault(d["kernel"], d)
-if "decide" in fullk and "compact_gather" in fullk:
-    a, b = fullk["decide"], fullk["compact_gather"]
+second = "compact_gather" if "compact_gather" in fullk else "compact_idx"
+if "decide" in fullk and second in fullk:
+    a, b = fullk["decide"], fullk[second]
     fullk["decide_gather"] = {"kernel": "decide_gather", "time_ns": a["time_ns"] + b["time_ns"],
                               "dram_read": a["dram_read"] + b["dram_read"], "dram_write": a["dram_write"] + b["dram_write"]}
 
