@@ -317,6 +317,9 @@ FWD_CASES = [
     (2, 56, 56, 256, 64, 4, 0.5),    # LAS-R101 stage 1 identity block (config 3), reduced batch
     (2, 14, 14, 1024, 256, 2, 0.5),  # stage 3
     (2, 7, 7, 2048, 512, 1, 0.5),    # stage 4
+    (2, 19, 17, 256, 64, 5, 0.5),    # direct conv23 patches: 5 per tile, clipped edge cells
+    (2, 22, 20, 256, 128, 8, 0.6),   # direct: 2 patches (128 rows) per tile
+    (2, 23, 21, 256, 64, 11, 0.7),   # direct: 1 patch of 121 rows per tile
 ]
 
 
