@@ -352,6 +352,47 @@ class DynBlock:
         y_host.copy_(x_dev, non_blocking=True)
         return y_host
 
+    def stream_host(self, x_hosts, y_hosts, x_devs, steps: int, before_step=None):
+        """Pipelined end-to-end batches with HOST buffers (a serving loop): step i
+        copies x_hosts[i % len] (pinned) into x_devs[i % len(x_devs)] on an H2D
+        stream, runs the five steps in place on the current stream, and copies the
+        result into y_hosts[i % len] (pinned) on a D2H stream, so the two copy
+        directions of neighbouring steps overlap each other and the compute.
+        Enqueues everything and returns; the current stream then waits for the
+        last D2H.  before_step(i), if given, is enqueued on the compute stream
+        before step i (e.g. an L2 flush)."""
+        comp = torch.cuda.current_stream()
+        if not hasattr(self, "_copy_streams"):
+            self._copy_streams = (torch.cuda.Stream(), torch.cuda.Stream())
+        h2d, d2h = self._copy_streams
+        nb = len(x_devs)
+        h2d.wait_stream(comp)
+        d2h.wait_stream(comp)
+        freed = [None] * nb  # D2H done with x_devs[b]: it may be overwritten
+        for i in range(steps):
+            b = i % nb
+            xd = x_devs[b]
+            with torch.cuda.stream(h2d):
+                if freed[b] is not None:
+                    h2d.wait_event(freed[b])
+                xd.copy_(x_hosts[i % len(x_hosts)], non_blocking=True)
+                loaded = torch.cuda.Event()
+                loaded.record(h2d)
+            comp.wait_event(loaded)
+            if before_step is not None:
+                before_step(i)
+            self.forward(xd)
+            done = torch.cuda.Event()
+            done.record(comp)
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(done)
+                y_hosts[i % len(y_hosts)].copy_(xd, non_blocking=True)
+                freed[b] = torch.cuda.Event()
+                freed[b].record(d2h)
+        comp.wait_stream(h2d)
+        comp.wait_stream(d2h)
+        return y_hosts
+
     def calibrate_bias(self, x: torch.Tensor, r: float) -> float:
         """Pick the masker bias so that ~r of the cells are active on x, from the
         product masker's own logits (b = 0): bm = -(the (1-r) quantile), placed

@@ -437,6 +437,26 @@ def test_cuda_graph_replay_equals_eager(sched):
     assert torch.equal(y_g, y_e)
 
 
+@pytest.mark.parametrize("sched", [None, L.SCHED_FUSED])
+def test_stream_host_pipeline_equals_per_batch_forward(sched):
+    """DynBlock.stream_host (bench.py's e2e serving loop: H2D, block and D2H of
+    consecutive batches overlapped on three streams, two device buffers) returns
+    for every batch the same bytes as a plain forward of that batch."""
+    n, h, w, c_in, c_mid, s = 4, 28, 28, 512, 128, 4
+    _, wts, wm = make_case(n, h, w, c_in, c_mid, s, seed=81)
+    blk = L.DynBlock(L.BlockShape(n, h, w, c_in, c_mid, s), wts, wm, 0.0, schedule=sched)
+    blk.calibrate_bias(synth.make_x(n, h, w, c_in, seed=82).cuda(), 0.5)
+    xs = [synth.make_x(n, h, w, c_in, seed=90 + i).pin_memory() for i in range(5)]
+    ys = [torch.empty_like(x).pin_memory() for x in xs]
+    devs = [torch.empty_like(xs[0], device="cuda") for _ in range(2)]
+    blk.stream_host(xs, ys, devs, len(xs))
+    torch.cuda.synchronize()
+    for x, y in zip(xs, ys):
+        want = x.cuda()
+        blk.forward(want)
+        assert torch.equal(y, want.cpu())
+
+
 def test_fused_schedule_bn256_repeated_graph_replays_stable():
     """conv1 with 256-column tiles runs 3 pipeline stages (odd): every masker warp
     must consume every stage (a K-parity split read stages before they were
