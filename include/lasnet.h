@@ -223,7 +223,8 @@ size_t lasnet_head_workspace_bytes(int32_t n, int32_t c);
  *   idx      [n*gh*gw] int32 out (capacity = all cells), count int32 device out
  *   ws       lasnet_block_forward_workspace_bytes(desc, schedule) bytes, ALL ZERO
  *            before the first call (its leading control words are left zero by
- *            every call; the rest is scratch).  Concurrent calls must not share it. */
+ *            every call, except one grid-barrier generation word whose value is
+ *            arbitrary; the rest is scratch).  Concurrent calls must not share it. */
 typedef enum { LASNET_SCHED_MASKER_SEPARATE = 0, LASNET_SCHED_MASKER_FUSED = 1 } lasnet_schedule;
 lasnet_status lasnet_block_forward(const lasnet_block_desc *desc, const lasnet_block_weights *wts,
                                    const void *x, void *y, const float *wm, float bm, int32_t schedule,

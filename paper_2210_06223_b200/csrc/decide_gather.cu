@@ -49,7 +49,8 @@ struct DecideArgs {
     uint8_t *dec;               // [ncells] decisions (caller's mask or workspace)
     int32_t *gpre;              // [ngroups] group counts -> exclusive prefixes
     int32_t *count;
-    unsigned *done;             // CTAs finished (zero on entry, reset by the last)
+    int32_t *idx;               // COOP: active cell ids
+    unsigned *done;             // [0] CTAs finished (zero on entry, reset by the last); COOP: [1] arrivals, [2] generation
 };
 
 constexpr int kDecThreads = 256;
@@ -109,6 +110,16 @@ __device__ double cell_exact(const DecideArgs &a, int n, int y0, int x0, int ch,
 // cell's pixel rows j, j+4, ... in fp64, the quad combines them (fixed order).
 constexpr int kDecCells = kDecThreads / 4;  // cells per CTA (a multiple of 32)
 
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// COOP (all CTAs co-resident; the direct schedule): after the decisions a grid
+// barrier, then every CTA sums the group counts before its own and writes the
+// ids of its active cells -- no last-CTA scan and no second launch.
+template <bool COOP>
 __global__ void __launch_bounds__(kDecThreads) decide_kernel(const DecideArgs a) {
     __shared__ int s_unc[kDecCells], s_nunc;
     __shared__ uint8_t s_dec[kDecCells];
@@ -187,6 +198,55 @@ __global__ void __launch_bounds__(kDecThreads) decide_kernel(const DecideArgs a)
         if (lane == 0 && cell0 / 32 + warp < a.ngroups) a.gpre[cell0 / 32 + warp] = __popc(bal);
     }
 
+    if constexpr (COOP) {
+        // grid barrier, sense reversal: done[1] counts arrivals (reset by the last), done[2] is
+        // the generation the last arrival advances (read before arriving; any start value)
+        __syncthreads();
+        if (tid == 0) {
+            const unsigned gen = ld_acquire(a.done + 2);
+            if (atom_add_acqrel(a.done + 1, 1u) == gridDim.x - 1) {
+                a.done[1] = 0u;
+                atom_add_acqrel(a.done + 2, 1u);
+            } else {
+                while (ld_acquire(a.done + 2) == gen) __nanosleep(64);
+            }
+        }
+        __syncthreads();
+        // this CTA's base: the active cells of all groups before its first one
+        __shared__ int s_part[kDecThreads / 32], s_wcnt[kDecCells / 32];
+        const int g0 = cell0 / 32;
+        int part = 0;
+        for (int g = tid; g < g0; g += kDecThreads) {
+            int v;
+            asm volatile("ld.global.cg.b32 %0, [%1];" : "=r"(v) : "l"(a.gpre + g));
+            part += v;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+        if (lane == 0) s_part[warp] = part;
+        int d = 0;
+        unsigned bal = 0u;
+        if (tid < kDecCells) {
+            d = cell0 + tid < a.ncells ? s_dec[tid] : 0;
+            bal = __ballot_sync(0xffffffffu, d);
+            if (lane == 0) s_wcnt[warp] = __popc(bal);
+        }
+        __syncthreads();
+        int base = 0;
+#pragma unroll
+        for (int w = 0; w < kDecThreads / 32; ++w) base += s_part[w];
+        if (tid < kDecCells) {
+            int off = base;
+            for (int w = 0; w < warp; ++w) off += s_wcnt[w];
+            if (d) a.idx[off + __popc(bal & ((1u << lane) - 1u))] = cell0 + tid;
+        }
+        if (tid == 0 && blockIdx.x == gridDim.x - 1) {
+            int tot = base;
+            for (int w = 0; w < kDecCells / 32; ++w) tot += s_wcnt[w];
+            *a.count = tot;
+        }
+        return;
+    }
     // the last CTA: exclusive prefix over the group counts, total count
     __syncthreads();
     if (tid == 0) s_last = atom_add_acqrel(a.done, 1u) == gridDim.x - 1;
@@ -318,7 +378,8 @@ size_t decide_sync_bytes(int ncells, int) {
     return 16 + ((size_t)ncells + 15) / 16 * 16 + (size_t)ngroups * 4;
 }
 
-// sync: decide_sync_bytes() bytes whose first 16 are zero (left zero).
+// sync: decide_sync_bytes() bytes whose first 16 are zero before the first call
+// (words 0-1 are left zero; word 2 is a barrier generation of any value).
 // h1d == nullptr: decisions, prefixes and count only; h1g == nullptr: + ids;
 // else + ids and the halo gather of h1d into h1g.
 cudaError_t launch_decide_gather(const float4 *mpart, const void *x, const float *wm, float bm, int n_img, int H,
@@ -346,7 +407,22 @@ cudaError_t launch_decide_gather(const float4 *mpart, const void *x, const float
     a.dec = mask ? mask : decs;
     a.gpre = reinterpret_cast<int32_t *>(decs + ((size_t)a.ncells + 15) / 16 * 16);
     a.count = count;
-    cudaError_t e = launch_k(decide_kernel, dim3((a.ncells + kDecCells - 1) / kDecCells), dim3(kDecThreads), 0, st, a);
+    a.idx = idx;
+    const int grid = (a.ncells + kDecCells - 1) / kDecCells;
+    // ids-only with every CTA co-resident: one cooperative launch (LASNET_DECIDE_2K=1: two launches)
+    static const int coop_cap = [] {
+        const char *e = getenv("LASNET_DECIDE_2K");
+        if (e && e[0] == '1') return 0;
+        int per_sm = 0, dev = 0, sms = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decide_kernel<true>, kDecThreads, 0) != cudaSuccess)
+            return 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        return per_sm * sms;
+    }();
+    if (h1d != nullptr && h1g == nullptr && grid <= coop_cap)
+        return launch_k(decide_kernel<true>, dim3(grid), dim3(kDecThreads), 0, st, a);
+    cudaError_t e = launch_k(decide_kernel<false>, dim3(grid), dim3(kDecThreads), 0, st, a);
     if (e != cudaSuccess || h1d == nullptr) return e;
     if (h1g == nullptr)  // ids only: steps 4-5 read the dense h1 directly
         return launch_k(compact_idx_kernel, dim3((unsigned)((a.ngroups + 7) / 8)), dim3(256), 0, st,
