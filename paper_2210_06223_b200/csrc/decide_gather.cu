@@ -384,7 +384,9 @@ size_t decide_sync_bytes(int ncells, int) {
 // else + ids and the halo gather of h1d into h1g.
 cudaError_t launch_decide_gather(const float4 *mpart, const void *x, const float *wm, float bm, int n_img, int H,
                                  int W, int c_in, int S, uint8_t *mask, int32_t *idx, int32_t *count, void *sync,
-                                 const void *h1d, void *h1g, int c_mid, int cap, int num_sms, cudaStream_t st) {
+                                 const void *h1d, void *h1g, int c_mid, int cap, int num_sms, cudaStream_t st,
+                                 int *launched) {
+    *launched = 1;
     (void)num_sms;
     DecideArgs a;
     a.mpart = mpart;
@@ -424,6 +426,7 @@ cudaError_t launch_decide_gather(const float4 *mpart, const void *x, const float
         return launch_k(decide_kernel<true>, dim3(grid), dim3(kDecThreads), 0, st, a);
     cudaError_t e = launch_k(decide_kernel<false>, dim3(grid), dim3(kDecThreads), 0, st, a);
     if (e != cudaSuccess || h1d == nullptr) return e;
+    *launched = 2;
     if (h1g == nullptr)  // ids only: steps 4-5 read the dense h1 directly
         return launch_k(compact_idx_kernel, dim3((unsigned)((a.ngroups + 7) / 8)), dim3(256), 0, st,
                         static_cast<const uint8_t *>(a.dec), static_cast<const int32_t *>(a.gpre), idx, a.ncells,

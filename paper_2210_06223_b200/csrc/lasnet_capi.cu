@@ -36,7 +36,8 @@ cudaError_t launch_conv23(bool dense, const ConvArgs &a, int max_tiles, int num_
 size_t decide_sync_bytes(int ncells, int num_sms);
 cudaError_t launch_decide_gather(const float4 *mpart, const void *x, const float *wm, float bm, int n_img, int H,
                                  int W, int c_in, int S, uint8_t *mask, int32_t *idx, int32_t *count, void *sync,
-                                 const void *h1d, void *h1g, int c_mid, int cap, int num_sms, cudaStream_t st);
+                                 const void *h1d, void *h1g, int c_mid, int cap, int num_sms, cudaStream_t st,
+                                 int *launched);
 }  // namespace lasnet
 
 using namespace lasnet;
@@ -699,10 +700,11 @@ lasnet_status lasnet_block_forward(const lasnet_block_desc *d, const lasnet_bloc
     a.K = d->c_in; a.N = d->c_mid; a.a_ld = d->c_in; a.out_ld = d->c_mid;
     a.wm = wm; a.mpart = static_cast<float4 *>(r.mpart);
     if (run_conv(d, CONV1_DENSE_MASK, a, px, x, y, r.h1d, nullptr, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    int nd = 0;
     {
         KernelEvents ev(st);
         if (launch_decide_gather(static_cast<const float4 *>(r.mpart), x, wm, bm, d->n, d->h, d->w, d->c_in, d->s,
-                                 mask, idx, count, r.sync, r.h1d, r.h1g, d->c_mid, ncells, num_sms(), st) !=
+                                 mask, idx, count, r.sync, r.h1d, r.h1g, d->c_mid, ncells, num_sms(), st, &nd) !=
             cudaSuccess)
             return LASNET_ERR_CUDA;
     }
@@ -717,7 +719,7 @@ lasnet_status lasnet_block_forward(const lasnet_block_desc *d, const lasnet_bloc
     } else if (run_steps45(d, w, b, x, y, r.h1g, r.h2, ncells, st, &k) != cudaSuccess) {
         return LASNET_ERR_CUDA;
     }
-    g_last_launches = 3 + k;  // conv1+masker, decide, compaction (+ gather), steps 4-5
+    g_last_launches = 1 + nd + k;  // conv1+masker, decide (+ compaction / gather), steps 4-5
     return LASNET_OK;
 }
 
