@@ -50,6 +50,7 @@ struct DecideArgs {
     int32_t *gpre;              // [ngroups] group counts -> exclusive prefixes
     int32_t *count;
     int32_t *idx;               // COOP: active cell ids
+    int32_t *gpx;               // COOP: [ngroups] exclusive group prefixes
     unsigned *done;             // [0] CTAs finished (zero on entry, reset by the last); COOP: [1] arrivals, [2] generation
 };
 
@@ -239,6 +240,9 @@ __global__ void __launch_bounds__(kDecThreads) decide_kernel(const DecideArgs a)
             int off = base;
             for (int w = 0; w < warp; ++w) off += s_wcnt[w];
             if (d) a.idx[off + __popc(bal & ((1u << lane) - 1u))] = cell0 + tid;
+            // exclusive group prefixes for the gather (a separate array: other CTAs may
+            // still be summing the counts)
+            if (lane == 0 && g0 + warp < a.ngroups) a.gpx[g0 + warp] = off;
         }
         if (tid == 0 && blockIdx.x == gridDim.x - 1) {
             int tot = base;
@@ -373,9 +377,9 @@ __global__ void __launch_bounds__(256) compact_idx_kernel(const uint8_t *__restr
 }
 
 size_t decide_sync_bytes(int ncells, int) {
-    // done counter (16 B) + decisions (ncells) + group prefixes (ngroups ints)
+    // control words (16 B) + decisions (ncells) + group counts / prefixes + cooperative prefixes (ngroups ints each)
     const long ngroups = ((long)ncells + 31) / 32;
-    return 16 + ((size_t)ncells + 15) / 16 * 16 + (size_t)ngroups * 4;
+    return 16 + ((size_t)ncells + 15) / 16 * 16 + (size_t)ngroups * 8;
 }
 
 // sync: decide_sync_bytes() bytes whose first 16 are zero before the first call
@@ -422,10 +426,11 @@ cudaError_t launch_decide_gather(const float4 *mpart, const void *x, const float
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         return per_sm * sms;
     }();
-    if (h1d != nullptr && h1g == nullptr && grid <= coop_cap)
-        return launch_k(decide_kernel<true>, dim3(grid), dim3(kDecThreads), 0, st, a);
-    cudaError_t e = launch_k(decide_kernel<false>, dim3(grid), dim3(kDecThreads), 0, st, a);
-    if (e != cudaSuccess || h1d == nullptr) return e;
+    a.gpx = a.gpre + a.ngroups;
+    const bool coop = h1d != nullptr && grid <= coop_cap;
+    cudaError_t e = coop ? launch_k(decide_kernel<true>, dim3(grid), dim3(kDecThreads), 0, st, a)
+                         : launch_k(decide_kernel<false>, dim3(grid), dim3(kDecThreads), 0, st, a);
+    if (e != cudaSuccess || h1d == nullptr || (coop && h1g == nullptr)) return e;
     *launched = 2;
     if (h1g == nullptr)  // ids only: steps 4-5 read the dense h1 directly
         return launch_k(compact_idx_kernel, dim3((unsigned)((a.ngroups + 7) / 8)), dim3(256), 0, st,
@@ -433,7 +438,7 @@ cudaError_t launch_decide_gather(const float4 *mpart, const void *x, const float
                         a.ngroups);
     GatherArgs g;
     g.dec = a.dec;
-    g.gpre = a.gpre;
+    g.gpre = coop ? a.gpx : a.gpre;  // exclusive prefixes
     g.idx = idx;
     g.h1d = static_cast<const __nv_bfloat16 *>(h1d);
     g.h1g = static_cast<__nv_bfloat16 *>(h1g);
