@@ -105,6 +105,23 @@ __device__ __forceinline__ int tile_pixel(const ConvArgs &args, int tile, int r,
     return out_pixel(args, tile * rows_per_tile + r, M);
 }
 
+// Dynamic tiles: tile t holds patches [t0, t0 + nv).  Fixed: units_per_tile each.
+// Balanced (args.balance): the count is spread over T = whole rounds of the grid
+// (q or q + 1 patches per tile), so the last round is not a partial one.
+struct DynTiles {
+    int upt, cnt, q, rem;
+    bool bal;
+    __device__ __forceinline__ void range(int t, int &t0, int &nv) const {
+        if (bal) {
+            t0 = t * q + min(t, rem);
+            nv = q + (t < rem ? 1 : 0);
+        } else {
+            t0 = t * upt;
+            nv = min(upt, cnt - t0);
+        }
+    }
+};
+
 // PAIR (CL == 2): the two CTAs of a cluster run conv2 and conv3 as 2-SM UMMAs
 // (tcgen05.mma.cta_group::2, M = 256): each CTA stages its own 128 A rows but only
 // HALF of every W2 / W3 K-block (the pair shares them), so per output row the
@@ -192,6 +209,13 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
         num_tiles = (*args.count + args.units_per_tile - 1) / args.units_per_tile;
         rows_per_tile = args.units_per_tile * args.S * args.S;
     }
+    DynTiles dt{args.units_per_tile, DENSE ? 0 : *args.count, 0, 0, false};
+    if (!DENSE && CL == 1 && args.balance && num_tiles > (int)gridDim.x) {
+        num_tiles = (num_tiles + gridDim.x - 1) / gridDim.x * gridDim.x;
+        dt.bal = true;
+        dt.q = dt.cnt / num_tiles;
+        dt.rem = dt.cnt - dt.q * num_tiles;
+    }
     const int M = DENSE ? 0 : (*args.count) * args.S * args.S;  // valid h2 rows (dynamic)
     const int kb2 = 9 * KC / kBK;                                 // conv2 K-blocks
     const int kpt = KC / kBK;                                     // K-blocks per tap
@@ -215,13 +239,15 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
         const int cnt = *args.count;
         // the next tile's cell ids are loaded while this tile's boxes are issued
         auto ids_of = [&](int i) {
-            const int t = tile_of(i) * args.units_per_tile + lane;
-            return (i < ntl && lane < args.units_per_tile && t < cnt) ? __ldg(args.idx + t) : -1;
+            if (i >= ntl) return -1;
+            int t0, nv;
+            dt.range(tile_of(i), t0, nv);
+            return lane < nv ? __ldg(args.idx + t0 + lane) : -1;
         };
         int next = ids_of(0);
         for (int i = 0; i < ntl; ++i) {
-            const int t0 = tile_of(i) * args.units_per_tile;
-            const int nval = min(args.units_per_tile, cnt - t0);
+            int t0, nval;
+            dt.range(tile_of(i), t0, nval);
             const int cell = next;
             next = ids_of(i + 1);
             int n = 0, y0 = 0, x0 = 0;
@@ -274,6 +300,8 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
                         continue;
                     }
                     mbar_arrive_expect_tx(fb, args.box_rows * 128 + KC * 128);
+                    int t0 = 0, nv;
+                    if (!DENSE) dt.range(tile, t0, nv);
                     if (CL > 1)  // this CTA's 1/CL of the W2 K-block, into every CTA of the cluster
                         tma_load_2d_mc(sa + kABytes + rank * (KC / CL) * 128, &args.tmap_b, fb, kb * kBK,
                                        rank * (KC / CL), kMask);
@@ -281,7 +309,7 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
                         tma_load_2d(sa + kABytes, &args.tmap_b, fb, kb * kBK, 0);
                     // h1 is channel-chunk-major: [c_mid/64][P][S+2][S+2][64] (dense: [c_mid/64][N][H][W][64])
                     if (DENSE) tma_load_5d(sa, &args.tmap_a, fb, 0, dx - 1, y0 + dy - 1, n0, c0 >> 6);
-                    else tma_load_5d(sa, &args.tmap_a, fb, 0, dx, dy, tile * args.units_per_tile, c0 >> 6);
+                    else tma_load_5d(sa, &args.tmap_a, fb, 0, dx, dy, t0, c0 >> 6);
                 }
             }
             __syncwarp();
@@ -441,6 +469,11 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
         __nv_bfloat16 *Y = static_cast<__nv_bfloat16 *>(args.out);
         // output pixel of tile-row r of local tile i (or -1)
         auto pixel_of = [&](int i) -> int {
+            if (!DENSE && dt.bal) {
+                int t0, nv;
+                dt.range(tile_of(i), t0, nv);
+                return r < nv * args.S * args.S ? out_pixel(args, t0 * args.S * args.S + r, M) : -1;
+            }
             return tile_pixel<DENSE>(args, tile_of(i), r, rows_per_tile, M);
         };
         constexpr int kChunks = 32 / 8;           // 16-B chunks of this warp's 32 columns

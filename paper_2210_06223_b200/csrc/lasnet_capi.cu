@@ -331,6 +331,13 @@ cudaError_t run_conv23(const lasnet_block_desc *d, bool dense, ConvArgs a, const
         const char *e = getenv("LASNET_C23_PAIR");
         return e && e[0] == '1';
     }();
+    // balanced dynamic tiles: the active patches spread over whole rounds of the grid
+    // (LASNET_C23_BALANCE=0: fixed units_per_tile patches per tile, a partial last round)
+    static const bool bal_env = [] {
+        const char *e = getenv("LASNET_C23_BALANCE");
+        return !(e && e[0] == '0');
+    }();
+    a.balance = bal_env ? 1 : 0;
     a.pair = pair_env && !a.direct ? 1 : 0;
     a.cluster = a.direct ? 1 : a.pair ? 2 : (C / cl_env >= 8 && nc3 / cl_env >= 8) ? cl_env : 1;
     bool ok = tmap2(&a.tmap_b, a.w, a.K, a.N, 64, C / a.cluster) && tmap2(&a.tmap_b3, w->w3, C, d->c_out, 64, nc3 / a.cluster);
