@@ -98,7 +98,10 @@ typedef struct {
  *   mask   [n][gh][gw] uint8 out: 1 iff logit > 0 (ties inactive, R3)
  *   logits [n][gh][gw] fp64 out, nullable: logit = sum_c wm_c * avgpool_c(x) + bm,
  *          average over the in-image pixels of the cell (R1, R7).
- * Accumulation is fp64 so the 1-bit decision is reproducible. */
+ * The decision is the one exact arithmetic takes (reading R20): fp32
+ * accumulation with a rigorous rounding bound, and an fp64 re-sum of any cell
+ * whose logit the bound does not separate from 0; logits (if requested) are
+ * accumulated in fp64. */
 lasnet_status lasnet_mask(const lasnet_block_desc *desc, const void *x, const float *wm,
                           float bm, uint8_t *mask, double *logits, lasnet_stream_t stream);
 
@@ -242,6 +245,14 @@ int32_t lasnet_choose_schedule(const lasnet_block_desc *desc, double r);
  * this call).  events are cudaEvent_t handles owned by the caller and must stay
  * valid until recorded; n_pairs = 0 disables.  Host-side, launches nothing. */
 lasnet_status lasnet_set_kernel_events(void *const *events, int32_t n_pairs);
+/* Kernel name of the i-th event pair recorded since the last
+ * lasnet_set_kernel_events call on this host thread (e.g. "conv1_mask",
+ * "conv23_direct", "decide+ids" for a group of two launches), or NULL when i is
+ * out of range.  Static strings; host-side, pure. */
+const char *lasnet_kernel_event_name(int32_t i);
+/* Number of event pairs recorded since the last lasnet_set_kernel_events call on
+ * this host thread (0 when disarmed).  Host-side, pure. */
+int32_t lasnet_kernel_event_count(void);
 
 /* Host-side, pure helpers. */
 const char *lasnet_status_str(lasnet_status st);

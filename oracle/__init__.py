@@ -308,3 +308,47 @@ def num_threads() -> int:
 
 def set_threads(t: int) -> None:
     _load().oracle_set_threads(int(t))
+
+
+def lasnet_forward(x, weights, meta, calibrate_r=None, return_masks=False):
+    """LAS-ResNet forward composed from the functions above (fp64 accumulation, bf16
+    storage rounding at every stored tensor): stem -> max pool -> per stage the
+    projection (first) block, then the identity blocks as dynamic blocks (masker
+    -> compaction -> literal gather/conv/scatter) ->
+    head (global average pool + classifier).  The network of SURVEY 8(f) NEXT-f1 /
+    BASELINE configs[2] (ResNet-101 depths 3-4-23-3, S_net 4-4-2-1).
+      x        [n][H][W][8] fp64 image (channels 3..7 zero)
+      weights  nested dict of fp64 arrays (synth.make_lasnet_weights layout)
+      meta     {"depths", "s_net", "bm": {block key: masker bias}} as the GPU network's
+               LASResNet.oracle_meta(); with calibrate_r set, each block's bias is
+               instead chosen from this forward's own logits so that ~r of its cells
+               are active (midway between two neighbouring logits) and written to meta.
+    Returns logits [n][classes] (and the per-block masks when return_masks)."""
+    depths, s_net = meta["depths"], meta["s_net"]
+    bms = meta.setdefault("bm", {})
+    cur = maxpool(stem(x, weights["stem_w"], weights["stem_b"]))
+    masks = {}
+    for si, (depth, s) in enumerate(zip(depths, s_net)):
+        stride = 1 if si == 0 else 2
+        pw = weights[f"s{si}_proj"]
+        cur = proj_block(cur, pw, stride)
+        for b in range(1, depth):
+            key = f"s{si}_b{b}"
+            wb = weights[key]
+            if calibrate_r is not None:
+                _, l0 = masker(cur, wb["wm"], 0.0, s)
+                lg = np.sort(l0.reshape(-1))
+                k = int(round(calibrate_r * lg.size))
+                if k <= 0:
+                    bm = -(lg[-1] + 1.0)
+                elif k >= lg.size:
+                    bm = -(lg[0] - 1.0)
+                else:
+                    bm = -0.5 * (lg[lg.size - k - 1] + lg[lg.size - k])
+                bms[key] = float(np.float32(bm))
+            m, _ = masker(cur, wb["wm"], bms[key], s)
+            idx, _ = compact(m)
+            masks[key] = m
+            cur = dyn_block_literal(cur, wb, idx, s)
+    logits = head(cur, weights["fc_w"], weights["fc_b"])
+    return (logits, masks) if return_masks else logits

@@ -25,7 +25,8 @@ EXPORTS = [
     "lasnet_status_str", "lasnet_abi_version", "lasnet_last_launch_count", "lasnet_set_kernel_events",
     "lasnet_block_forward", "lasnet_block_forward_workspace_bytes", "lasnet_choose_schedule",
     "lasnet_proj_block", "lasnet_proj_workspace_bytes", "lasnet_stem", "lasnet_stem_workspace_bytes",
-    "lasnet_maxpool", "lasnet_head", "lasnet_head_workspace_bytes",
+    "lasnet_maxpool", "lasnet_head", "lasnet_head_workspace_bytes", "lasnet_kernel_event_name",
+    "lasnet_kernel_event_count",
 ]
 
 # lasnet_schedule
@@ -106,6 +107,9 @@ def load(path: str = LIB_PATH):
     lib.lasnet_last_launch_count.restype = i32
     lib.lasnet_set_kernel_events.argtypes = [ctypes.POINTER(ctypes.c_void_p), i32]
     lib.lasnet_set_kernel_events.restype = ctypes.c_int
+    lib.lasnet_kernel_event_name.argtypes = [i32]
+    lib.lasnet_kernel_event_name.restype = ctypes.c_char_p
+    lib.lasnet_kernel_event_count.restype = i32
     _lib = lib
     return lib
 

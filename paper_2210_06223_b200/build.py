@@ -39,18 +39,25 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
     lib = LIB if not trace else LIB.replace(".so", "_trace.so")
     if not force and not trace and not _stale():
         return LIB
-    objs = []
     bdir = os.path.join(HERE, "build" if not trace else "build_trace")
     os.makedirs(bdir, exist_ok=True)
-    for src in SOURCES:
+
+    def compile_one(src):
         obj = os.path.join(bdir, src.replace(".cu", ".o"))
         cmd = [NVCC, *FLAGS, *(["-DLASNET_TRACE"] if trace else []), "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
-        if verbose or r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-        if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {src}")
-        objs.append(obj)
+        return src, obj, r
+
+    from concurrent.futures import ThreadPoolExecutor
+
+    objs = []
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        for src, obj, r in ex.map(compile_one, SOURCES):
+            if verbose or r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+            if r.returncode != 0:
+                raise RuntimeError(f"nvcc failed for {src}")
+            objs.append(obj)
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", lib, *objs]
     subprocess.run(cmd, check=True)
     return lib

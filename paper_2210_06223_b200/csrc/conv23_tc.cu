@@ -211,10 +211,15 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
     }
     DynTiles dt{args.units_per_tile, DENSE ? 0 : *args.count, 0, 0, false};
     if (!DENSE && CL == 1 && args.balance && num_tiles > (int)gridDim.x) {
-        num_tiles = (num_tiles + gridDim.x - 1) / gridDim.x * gridDim.x;
-        dt.bal = true;
-        dt.q = dt.cnt / num_tiles;
-        dt.rem = dt.cnt - dt.q * num_tiles;
+        // only when every tile of the rounded-up count gets at least one patch (q >= 1):
+        // an empty tile would still stream the weights and issue its MMAs
+        const int t_bal = (num_tiles + gridDim.x - 1) / gridDim.x * gridDim.x;
+        if (dt.cnt >= t_bal) {
+            num_tiles = t_bal;
+            dt.bal = true;
+            dt.q = dt.cnt / num_tiles;
+            dt.rem = dt.cnt - dt.q * num_tiles;
+        }
     }
     const int M = DENSE ? 0 : (*args.count) * args.S * args.S;  // valid h2 rows (dynamic)
     const int kb2 = 9 * KC / kBK;                                 // conv2 K-blocks

@@ -415,21 +415,44 @@ cudaError_t launch_decide_gather(const float4 *mpart, const void *x, const float
     a.count = count;
     a.idx = idx;
     const int grid = (a.ncells + kDecCells - 1) / kDecCells;
-    // ids-only with every CTA co-resident: one cooperative launch (LASNET_DECIDE_2K=1: two launches)
-    static const int coop_cap = [] {
+    // ids-only with every CTA co-resident: one cooperative launch (LASNET_DECIDE_2K=1: two launches).
+    // The co-residency capacity is measured per device; the launch itself carries the
+    // cooperative attribute, so the runtime refuses it (nothing runs) rather than let a
+    // grid barrier spin on CTAs that cannot be scheduled -- then the two-launch path runs.
+    static const bool two_k = [] {
         const char *e = getenv("LASNET_DECIDE_2K");
-        if (e && e[0] == '1') return 0;
-        int per_sm = 0, dev = 0, sms = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decide_kernel<true>, kDecThreads, 0) != cudaSuccess)
-            return 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        return per_sm * sms;
+        return e && e[0] == '1';
     }();
+    constexpr int kMaxDev = 64;
+    static int coop_cap_dev[kMaxDev] = {};  // 0 = not measured yet, -1 = unavailable
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int coop_cap = 0;
+    if (!two_k && dev >= 0 && dev < kMaxDev) {
+        if (coop_cap_dev[dev] == 0) {
+            int per_sm = 0, sms = 0, coop_ok = 0;
+            cudaDeviceGetAttribute(&coop_ok, cudaDevAttrCooperativeLaunch, dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            if (coop_ok &&
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decide_kernel<true>, kDecThreads, 0) == cudaSuccess &&
+                per_sm * sms > 0)
+                coop_cap_dev[dev] = per_sm * sms;
+            else
+                coop_cap_dev[dev] = -1;
+        }
+        coop_cap = coop_cap_dev[dev] > 0 ? coop_cap_dev[dev] : 0;
+    }
     a.gpx = a.gpre + a.ngroups;
-    const bool coop = h1d != nullptr && grid <= coop_cap;
-    cudaError_t e = coop ? launch_k(decide_kernel<true>, dim3(grid), dim3(kDecThreads), 0, st, a)
-                         : launch_k(decide_kernel<false>, dim3(grid), dim3(kDecThreads), 0, st, a);
+    bool coop = h1d != nullptr && grid <= coop_cap;
+    cudaError_t e = cudaErrorUnknown;
+    if (coop) {
+        e = launch_k_coop(decide_kernel<true>, dim3(grid), dim3(kDecThreads), 0, st, a);
+        if (e == cudaErrorCooperativeLaunchTooLarge) {  // not co-resident now: the two-launch form
+            (void)cudaGetLastError();
+            coop = false;
+        }
+    }
+    if (!coop) e = launch_k(decide_kernel<false>, dim3(grid), dim3(kDecThreads), 0, st, a);
     if (e != cudaSuccess || h1d == nullptr || (coop && h1g == nullptr)) return e;
     *launched = 2;
     if (h1g == nullptr)  // ids only: steps 4-5 read the dense h1 directly

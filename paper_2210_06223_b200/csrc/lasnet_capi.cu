@@ -47,21 +47,42 @@ namespace {
 thread_local int32_t g_last_launches = 0;
 thread_local void *const *g_events = nullptr;
 thread_local int32_t g_event_pairs = 0, g_event_next = 0;
+constexpr int kMaxEventNames = 4096;
+thread_local const char *g_event_names[kMaxEventNames];
 
-// Brackets one kernel launch with the caller's benchmark events, if armed.
+// Brackets one kernel launch (or a fixed group of launches) with the caller's
+// benchmark events, if armed, and records the launch's kernel name for
+// lasnet_kernel_event_name().
 struct KernelEvents {
     cudaStream_t st;
     bool on;
-    explicit KernelEvents(cudaStream_t s) : st(s), on(g_events && g_event_next < g_event_pairs) {
+    const char *name;
+    KernelEvents(cudaStream_t s, const char *nm) : st(s), on(g_events && g_event_next < g_event_pairs), name(nm) {
         if (on) cudaEventRecord(static_cast<cudaEvent_t>(g_events[2 * g_event_next]), st);
     }
     ~KernelEvents() {
         if (on) {
             cudaEventRecord(static_cast<cudaEvent_t>(g_events[2 * g_event_next + 1]), st);
+            if (g_event_next < kMaxEventNames) g_event_names[g_event_next] = name;
             ++g_event_next;
         }
     }
 };
+
+// kernel name of a convolution mode (benchmark bookkeeping)
+const char *conv_name(int mode) {
+    switch (mode) {
+        case CONV1_DYN: return "conv1_dyn";
+        case CONV2_DYN: return "conv2_dyn";
+        case CONV3_DYN: return "conv3_dyn";
+        case CONV1_DENSE: return "conv1_dense";
+        case CONV2_DENSE: return "conv2_dense";
+        case CONV3_DENSE: return "conv3_dense";
+        case CONV1_DENSE_MASK: return "conv1_mask";
+        case STEM: return "stem_conv";
+    }
+    return "conv";
+}
 
 int num_sms() {
     static int cached = 0;
@@ -368,7 +389,7 @@ cudaError_t run_conv23(const lasnet_block_desc *d, bool dense, ConvArgs a, const
         tiles = (cap + a.units_per_tile - 1) / a.units_per_tile;
     }
     if (!ok) return cudaErrorInvalidValue;
-    KernelEvents ev(st);
+    KernelEvents ev(st, dense ? "conv23_dense" : a.direct ? "conv23_direct" : "conv23");
     return launch_conv23(dense, a, tiles, num_sms(), st);
 }
 
@@ -378,10 +399,10 @@ cudaError_t run_conv(const lasnet_block_desc *d, int mode, ConvArgs &a, int max_
     if (d->dtype == LASNET_BF16) {
         const int tiles = prepare_tc(mode, a, d, x, y, h1, h2, cap);
         if (tiles < 0) return cudaErrorInvalidValue;
-        KernelEvents ev(st);
+        KernelEvents ev(st, conv_name(mode));
         return launch_conv_tc(mode, a, tiles, num_sms(), st);
     }
-    KernelEvents ev(st);
+    KernelEvents ev(st, "conv_simt");
     return launch_conv_simt(mode, a, max_rows, st);
 }
 
@@ -485,6 +506,13 @@ int32_t lasnet_abi_version(void) { return LASNET_ABI_VERSION; }
 
 int32_t lasnet_last_launch_count(void) { return g_last_launches; }
 
+int32_t lasnet_kernel_event_count(void) { return g_events ? g_event_next : 0; }
+
+const char *lasnet_kernel_event_name(int32_t i) {
+    if (i < 0 || i >= g_event_next || i >= kMaxEventNames) return nullptr;
+    return g_event_names[i];
+}
+
 lasnet_status lasnet_set_kernel_events(void *const *events, int32_t n_pairs) {
     if (n_pairs < 0) return LASNET_ERR_SHAPE;
     if (n_pairs > 0 && !events) return LASNET_ERR_NULL;
@@ -516,7 +544,7 @@ lasnet_status lasnet_mask(const lasnet_block_desc *d, const void *x, const float
     if (!masker_channels_ok(d->c_in, vec) || misaligned(x)) return LASNET_ERR_UNSUPPORTED;
     g_last_launches = 0;
     if (d->n == 0) return LASNET_OK;
-    KernelEvents ev(reinterpret_cast<cudaStream_t>(stream));
+    KernelEvents ev(reinterpret_cast<cudaStream_t>(stream), "mask");
     cudaError_t e = launch_masker(d->dtype == LASNET_BF16, x, wm, bm, d->n, d->h, d->w, d->c_in, d->s, mask,
                                   logits, reinterpret_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return LASNET_ERR_CUDA;
@@ -541,7 +569,7 @@ lasnet_status lasnet_mask_compact(const lasnet_block_desc *d, const void *x, con
     if (!ws || ws_bytes < lasnet_mask_compact_workspace_bytes(d)) return LASNET_ERR_WORKSPACE;
     g_last_launches = 0;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    KernelEvents ev(st);
+    KernelEvents ev(st, "mask_compact");
     cudaError_t e = launch_mask_compact(d->dtype == LASNET_BF16, x, wm, bm, d->n, d->h, d->w, d->c_in, d->s, mask,
                                         logits, idx, count, ws, st);
     if (e != cudaSuccess) return LASNET_ERR_CUDA;
@@ -556,7 +584,7 @@ lasnet_status lasnet_compact(const uint8_t *mask, int32_t ncells, int32_t *idx, 
     if (ncells > 0 && (!ws || ws_bytes < compact_workspace_bytes(ncells))) return LASNET_ERR_WORKSPACE;
     cudaError_t e = cudaSuccess;
     g_last_launches = 0;
-    KernelEvents ev(reinterpret_cast<cudaStream_t>(stream));
+    KernelEvents ev(reinterpret_cast<cudaStream_t>(stream), "compact");
     const int k = launch_compact(mask, ncells, idx, count, ws, reinterpret_cast<cudaStream_t>(stream), &e);
     if (e != cudaSuccess) return LASNET_ERR_CUDA;
     g_last_launches = k;
@@ -687,7 +715,7 @@ lasnet_status lasnet_block_forward(const lasnet_block_desc *d, const lasnet_bloc
     if (schedule == LASNET_SCHED_MASKER_SEPARATE) {
         // north-star branch: masker+compaction (one launch), then gather+conv1 on the halos, conv2, conv3
         {
-            KernelEvents ev(st);
+            KernelEvents ev(st, "mask_compact");
             if (launch_mask_compact(d->dtype == LASNET_BF16, x, wm, bm, d->n, d->h, d->w, d->c_in, d->s, mask, nullptr,
                                     idx, count, r.sync, st) != cudaSuccess)
                 return LASNET_ERR_CUDA;
@@ -709,11 +737,12 @@ lasnet_status lasnet_block_forward(const lasnet_block_desc *d, const lasnet_bloc
     if (run_conv(d, CONV1_DENSE_MASK, a, px, x, y, r.h1d, nullptr, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
     int nd = 0;
     {
-        KernelEvents ev(st);
+        KernelEvents ev(st, r.h1g ? "decide+gather" : "decide");
         if (launch_decide_gather(static_cast<const float4 *>(r.mpart), x, wm, bm, d->n, d->h, d->w, d->c_in, d->s,
                                  mask, idx, count, r.sync, r.h1d, r.h1g, d->c_mid, ncells, num_sms(), st, &nd) !=
             cudaSuccess)
             return LASNET_ERR_CUDA;
+        if (!r.h1g && nd == 2) ev.name = "decide+ids";  // decide, then a separate id-writing launch
     }
     ConvArgs b = base_args(d);
     b.idx = idx;
@@ -750,7 +779,7 @@ lasnet_status lasnet_stem(int32_t n, int32_t h, int32_t w, const void *x_pad, co
     if (n == 0) return LASNET_OK;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     {
-        KernelEvents ev(st);
+        KernelEvents ev(st, "stem_pack");
         if (launch_pack_stem(wt, ws, st) != cudaSuccess) return LASNET_ERR_CUDA;
     }
     ConvArgs a;
@@ -776,7 +805,7 @@ lasnet_status lasnet_stem(int32_t n, int32_t h, int32_t w, const void *x_pad, co
     }
     if (!ok) return LASNET_ERR_CUDA;
     {
-        KernelEvents ev(st);
+        KernelEvents ev(st, "stem_conv");
         if (launch_conv_tc(STEM, a, n * h, num_sms(), st) != cudaSuccess) return LASNET_ERR_CUDA;
     }
     g_last_launches = 2;
@@ -790,7 +819,7 @@ lasnet_status lasnet_maxpool(int32_t n, int32_t h, int32_t w, int32_t c, const v
     if (c % 8 || misaligned(x) || misaligned(y)) return LASNET_ERR_UNSUPPORTED;
     g_last_launches = 0;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    KernelEvents ev(st);
+    KernelEvents ev(st, "maxpool");
     if (launch_maxpool(x, y, n, h, w, c, num_sms(), st) != cudaSuccess) return LASNET_ERR_CUDA;
     g_last_launches = 1;
     return LASNET_OK;
@@ -805,7 +834,7 @@ lasnet_status lasnet_head(int32_t n, int32_t hw, int32_t c, int32_t classes, con
     if (n > 0 && (!ws || ws_bytes < lasnet_head_workspace_bytes(n, c))) return LASNET_ERR_WORKSPACE;
     g_last_launches = 0;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    KernelEvents ev(st);
+    KernelEvents ev(st, "head");
     if (launch_head(x, w, b, static_cast<float *>(ws), logits, n, hw, c, classes, num_sms(), st) != cudaSuccess)
         return LASNET_ERR_CUDA;
     g_last_launches = 2;
@@ -890,7 +919,7 @@ lasnet_status lasnet_proj_block(const lasnet_block_desc *d, const lasnet_block_w
         if (!ok) return LASNET_ERR_CUDA;
         if (run_conv(d, CONV2_DENSE, a, pxo, x, y, h1, h2, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
         {
-            KernelEvents ev(st);
+            KernelEvents ev(st, "subsample");
             if (launch_subsample(x, xs, d->n, d->h, d->w, d->c_in * (int)e, S2, num_sms(), st) != cudaSuccess)
                 return LASNET_ERR_CUDA;
         }
@@ -905,7 +934,7 @@ lasnet_status lasnet_proj_block(const lasnet_block_desc *d, const lasnet_block_w
                           (size_t)d->c_in * e, d->c_out, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
         return LASNET_ERR_CUDA;
     {
-        KernelEvents ev(st);
+        KernelEvents ev(st, "add_bias");
         if (launch_add_bias(w->b3, w->bd, static_cast<float *>(b3d), d->c_out, st) != cudaSuccess) return LASNET_ERR_CUDA;
     }
     ConvArgs c = base_args(d);

@@ -63,6 +63,25 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
     return debug_check(kern, cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...), st);
 }
 
+// A cooperative launch (cudaLaunchAttributeCooperative): the runtime guarantees
+// that every CTA of the grid is co-resident, or fails the launch (then nothing
+// runs) -- required by kernels that spin in a software grid barrier.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k_coop(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                          Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return debug_check(kern, cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...), st);
+}
+
 // The same with a 1-D thread-block cluster of `cluster` CTAs (grid.x % cluster == 0).
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int cluster,

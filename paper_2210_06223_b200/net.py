@@ -55,6 +55,7 @@ class LASResNet:
     def __init__(self, n: int, weights: dict, hw: int = 224, depths=R101_DEPTHS, s_net=S_NET, r: float = 0.5,
                  device="cuda"):
         self.n, self.hw, self.device = n, hw, device
+        self.depths, self.s_net = tuple(depths), tuple(s_net)
         lib = _lib.load()
         self.stem_w = weights["stem_w"].to(device).contiguous()
         self.stem_b = weights["stem_b"].to(device).contiguous()
@@ -86,26 +87,50 @@ class LASResNet:
         self.logits = torch.empty((n, self.fc_w.shape[0]), dtype=torch.float32, device=device)
         self.c_last, self.h_last = c_in, h
 
+    def oracle_meta(self) -> dict:
+        """Depths, S_net and every dynamic block's masker bias, keyed like the weight
+        dict ("s{stage}_b{block}") -- what an oracle forward needs to take the same
+        decisions (test / bench bookkeeping; no arithmetic)."""
+        bm = {}
+        for si, (proj, dyn) in enumerate(self.stages):
+            for bi, blk in enumerate(dyn):
+                bm[f"s{si}_b{bi + 1}"] = float(blk.bm)
+        return {"depths": self.depths, "s_net": self.s_net, "bm": bm}
+
     def blocks(self):
         for proj, dyn in self.stages:
             yield from dyn
 
-    def forward(self, x_pad: torch.Tensor, calibrate_r: float | None = None, dense: bool = False):
+    def forward(self, x_pad: torch.Tensor, calibrate_r: float | None = None, dense: bool = False,
+                trace: list | None = None):
         """Logits [n, classes] (fp32).  calibrate_r: first set every dynamic block's
         masker bias so that ~r of its cells are active on the activations it sees
         (host synchronisation; not for the timed path).  dense: run the identity
-        blocks on every pixel (lasnet_dense_block) -- the comparator network."""
+        blocks on every pixel (lasnet_dense_block) -- the comparator network.
+        trace: if a list, one dict per library call is appended (layer kind, the
+        block object, and the range [ev0, ev1) of kernel event pairs the call
+        recorded when lasnet_set_kernel_events is armed) -- bench bookkeeping."""
         lib = _lib.load()
         n, h = self.n, self.hw // 2
+        self.launches = 0
+
+        def mark(kind, obj=None, **kw):
+            if trace is not None:
+                trace.append(dict(kind=kind, obj=obj, ev1=int(lib.lasnet_kernel_event_count()), **kw))
+            self.launches += int(lib.lasnet_last_launch_count())
+
         _lib.check("lasnet_stem", lib.lasnet_stem(n, h, h, _p(x_pad), _p(self.stem_w), _p(self.stem_b),
                                                   _p(self.stem_y), _p(self.stem_ws), self.stem_ws.numel(), _stream()))
+        mark("stem", None, n=n, h=h, w=h)
         _lib.check("lasnet_maxpool", lib.lasnet_maxpool(n, h // 2, h // 2, 64, _p(self.stem_y), _p(self.pool_y),
                                                         _stream()))
+        mark("maxpool", None, n=n, h=h // 2, w=h // 2, c=64)
         x = self.pool_y
         for si, (proj, dyn) in enumerate(self.stages):
             y = proj.forward(x)
+            mark("proj", proj, stage=si)
             other = self._scratch(si, y) if dense else None
-            for blk in dyn:
+            for bi, blk in enumerate(dyn):
                 if calibrate_r is not None:
                     blk.calibrate_bias(y, calibrate_r)
                 if dense:  # out of place, ping-pong between the stage's two buffers
@@ -113,11 +138,56 @@ class LASResNet:
                     y, other = other, y
                 else:
                     blk.forward(y)  # in place: inactive pixels are never touched
+                mark("dense" if dense else "dyn", blk, stage=si, block=bi + 1)
             x = y
         _lib.check("lasnet_head", lib.lasnet_head(n, self.h_last * self.h_last, self.c_last, self.fc_w.shape[0],
                                                   _p(x), _p(self.fc_w), _p(self.fc_b), _p(self.logits),
                                                   _p(self.head_ws), self.head_ws.numel(), _stream()))
+        mark("head", None, n=n, hw=self.h_last * self.h_last, c=self.c_last, classes=self.fc_w.shape[0])
+        if trace is not None:  # ev0 of each call = ev1 of the previous one
+            for i, t in enumerate(trace):
+                t["ev0"] = trace[i - 1]["ev1"] if i else 0
         return self.logits
+
+    def stream_host(self, x_hosts, logits_hosts, x_devs, graphs, steps: int):
+        """End-to-end serving loop with HOST buffers (e2e of bench.py): step i copies
+        the pinned image batch x_hosts[i % len] into x_devs[i % 2] on an H2D stream,
+        replays graphs[i % 2] (the forward captured on that input buffer) on the
+        current stream and copies the logits into logits_hosts[i % len] (pinned) on a
+        D2H stream; the H2D of step i+1 overlaps the forward of step i.  Enqueues
+        everything; the current stream then waits for the last D2H."""
+        comp = torch.cuda.current_stream()
+        if not hasattr(self, "_copy_streams"):
+            self._copy_streams = (torch.cuda.Stream(), torch.cuda.Stream())
+        h2d, d2h = self._copy_streams
+        h2d.wait_stream(comp)
+        d2h.wait_stream(comp)
+        nb = len(x_devs)
+        freed = [None] * nb  # the forward that read x_devs[b] has finished: it may be overwritten
+        out_done = None
+        for i in range(steps):
+            b = i % nb
+            with torch.cuda.stream(h2d):
+                if freed[b] is not None:
+                    h2d.wait_event(freed[b])
+                x_devs[b].copy_(x_hosts[i % len(x_hosts)], non_blocking=True)
+                loaded = torch.cuda.Event()
+                loaded.record(h2d)
+            comp.wait_event(loaded)
+            if out_done is not None:
+                comp.wait_event(out_done)  # the previous step's logits have been read out
+            graphs[b].replay()
+            done = torch.cuda.Event()
+            done.record(comp)
+            freed[b] = done
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(done)
+                logits_hosts[i % len(logits_hosts)].copy_(self.logits, non_blocking=True)
+                out_done = torch.cuda.Event()
+                out_done.record(d2h)
+        comp.wait_stream(h2d)
+        comp.wait_stream(d2h)
+        return logits_hosts
 
     def _scratch(self, si, like):
         if not hasattr(self, "_scr"):

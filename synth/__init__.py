@@ -149,3 +149,16 @@ def to_f64(t: torch.Tensor) -> np.ndarray:
 
 def weights_f64(wts: dict) -> dict:
     return {k: to_f64(v) for k, v in wts.items()}
+
+
+def weights_f64_nested(wts: dict) -> dict:
+    """weights_f64 over a nested weight dict (make_lasnet_weights)."""
+    return {k: weights_f64_nested(v) if isinstance(v, dict) else to_f64(v) for k, v in wts.items()}
+
+
+def lasnet_oracle_biases(weights: dict, seed: int = 5000, depths=(3, 4, 23, 3), s_net=(4, 4, 2, 1)) -> dict:
+    """Network metadata for oracle runs without a GPU network (bench.py's reference
+    arm): depths, S_net and an empty bias table that oracle.lasnet_forward fills by
+    calibrating on its own first forward (it is the oracle that calibrates; this
+    module only states the configuration)."""
+    return {"depths": tuple(depths), "s_net": tuple(s_net), "bm": {}, "calibrate_seed": int(seed)}

@@ -1,0 +1,110 @@
+"""Element-wise parity at the sizes and launch paths the bench and network run (-m gpu).
+
+Round-1 checked the full-size config-2 launches on 96 sampled pixels only, while
+every element-wise case stayed below the 148-CTA grid.  Here:
+  * config 2 at full size (N = 128, 28x28x512, c_mid 128) for S in {1, 2, 4, 7}
+    and both schedules, compared with the fp64 oracle over the WHOLE output
+    tensor -- these shapes run multi-round persistent tiles and the balanced
+    conv23 tiles (more tiles than CTAs: S = 4 has ~400 tiles at r = 0.5);
+  * signed block inputs (SURVEY 8(c) reading 5 pins y = ReLU(x + F) on active
+    pixels and y = x elsewhere, which differs from ReLU(x) for x < 0);
+  * a forced balanced-tile case far above the grid at small cost.
+Masks, ids and counts bit-exact; activations max-abs-rel <= 2e-2 (north_star);
+inactive pixels bitwise x.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from parity_util import BF16_TOL, make_case, margin_bias, max_abs_rel, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2210_06223_b200 import build, _lib
+    build.build()
+    _lib.load()
+    oracle.build()
+
+
+import paper_2210_06223_b200 as L  # noqa: E402
+
+
+def _check_block(x, wts, wm, bm, s, y, mask, idx, count):
+    """mask/idx/count bit-exact vs the oracle masker + compaction; y element-wise
+    vs the oracle's literal gather -> conv -> scatter (OpenMP over patches)."""
+    h, w = x.shape[1], x.shape[2]
+    xd = synth.to_f64(x)
+    m_or, _ = oracle.masker(xd, synth.to_f64(wm), bm, s)
+    idx_or, cnt = oracle.compact(m_or)
+    assert np.array_equal(mask, m_or), "mask"
+    assert count == cnt, "count"
+    assert np.array_equal(idx[:cnt], idx_or), "idx"
+    want = oracle.dyn_block_literal(xd, synth.weights_f64(wts), idx_or, s)
+    got = synth.to_f64(y)
+    up = oracle.upsample(m_or, h, w, s).astype(bool)
+    err = max_abs_rel(got[up], want[up])
+    assert err <= BF16_TOL, f"active pixels: max-abs-rel {err}"
+    assert np.array_equal(got[~up], xd[~up]), "inactive pixels must stay x bitwise"
+    return cnt, err
+
+
+@pytest.mark.parametrize("sched", ["separate", "fused"])
+@pytest.mark.parametrize("s", [1, 2, 4, 7])
+def test_config2_full_tensor(s, sched):
+    """The bench's block launch (DynBlock, masker bias calibrated to r = 0.5) at
+    full size, every output element against the oracle."""
+    n, h, w, c_in, c_mid = 128, 28, 28, 512, 128
+    x, wts, wm = make_case(n, h, w, c_in, c_mid, s, seed=200 + s)
+    schedule = L.SCHED_FUSED if sched == "fused" else None
+    blk = L.DynBlock(L.BlockShape(n, h, w, c_in, c_mid, s), wts, wm, 0.0, schedule=schedule)
+    xg = x.cuda()
+    blk.calibrate_bias(synth.make_x(n, h, w, c_in, seed=300 + s).cuda(), 0.5)
+    y = xg.clone()
+    blk.forward(y)
+    torch.cuda.synchronize()
+    cnt, _ = _check_block(x, wts, wm, blk.bm, s, y.cpu(), blk.mask_buf.cpu().numpy(), blk.idx.cpu().numpy(),
+                          int(blk.count.item()))
+    gh, gw = L.grid(h, w, s)
+    tiles = -(-cnt // max(1, 128 // (s * s)))
+    assert tiles > 148, "the case must exercise multi-round / balanced persistent tiles"
+
+
+@pytest.mark.parametrize("sched", [L.SCHED_SEPARATE, L.SCHED_FUSED])
+@pytest.mark.parametrize("n,h,w,c_in,c_mid,s,r", [
+    (4, 28, 28, 512, 128, 4, 0.5),
+    (3, 13, 11, 256, 64, 3, 0.6),
+    (2, 14, 14, 1024, 256, 2, 0.5),
+])
+def test_signed_input(sched, n, h, w, c_in, c_mid, s, r):
+    """Signed x (not a post-ReLU map): active pixels ReLU(x + F(x)), inactive
+    pixels x itself, negative values included."""
+    x, wts, wm = make_case(n, h, w, c_in, c_mid, s, seed=400 + s, relu=False)
+    assert (x < 0).any()
+    xd = synth.to_f64(x)
+    _, l0 = oracle.masker(xd, synth.to_f64(wm), 0.0, s)
+    bm = margin_bias(l0, r)
+    y, m, idx, count = L.block_forward(x.cuda(), to_dev(wts), wm.cuda(), bm, s, sched)
+    _check_block(x, wts, wm, bm, s, y.cpu(), m.cpu().numpy(), idx.cpu().numpy(), int(count.item()))
+
+
+@pytest.mark.parametrize("sched", [L.SCHED_SEPARATE, L.SCHED_FUSED])
+@pytest.mark.parametrize("s", [4, 7])
+def test_balanced_tiles_many_rounds(sched, s):
+    """Many more patch tiles than CTAs at a small channel count (cheap for the
+    oracle): 64 images of 28x28, c 256 / 64, every cell active -> 784 (S = 4) or
+    1024 (S = 7) patches, i.e. several rounds of the 148-CTA grid, balanced."""
+    n, h, w, c_in, c_mid = 64, 28, 28, 256, 64
+    x, wts, wm = make_case(n, h, w, c_in, c_mid, s, seed=500 + s)
+    xd = synth.to_f64(x)
+    _, l0 = oracle.masker(xd, synth.to_f64(wm), 0.0, s)
+    for r in (1.0, 0.7):
+        bm = margin_bias(l0, r)
+        y, m, idx, count = L.block_forward(x.cuda(), to_dev(wts), wm.cuda(), bm, s, sched)
+        _check_block(x, wts, wm, bm, s, y.cpu(), m.cpu().numpy(), idx.cpu().numpy(), int(count.item()))

@@ -576,18 +576,21 @@ def test_stem_maxpool_head_match_oracle(n, h, w):
     assert np.abs(lg - want_lg).max() <= 1e-4 * max(1.0, np.abs(want_lg).max())
 
 
-def test_lasnet_network_layerwise_matches_oracle():
-    """A small LAS-ResNet-101 (64x64 input: stages 16/8/4/2 px, S_net 4-4-2-1) run
-    layer by layer through the library; each layer's output is checked against
-    the fp64 oracle applied to the same GPU input: stem, pool, every projection
-    block, every dynamic block (mask bit-exact, activations in tolerance), head."""
-    n, hw = 2, 64
+@pytest.mark.parametrize("n,hw", [(2, 64), (4, 224)])
+def test_lasnet_network_layerwise_matches_oracle(n, hw):
+    """LAS-ResNet-101 run layer by layer through the library (64x64: stages of
+    16/8/4/2 px; 224x224: the measured ImageNet shape, stages 56/28/14/7 px,
+    multi-round persistent tiles); each layer's output is checked against the
+    fp64 oracle applied to the same GPU input (teacher forcing): stem, pool,
+    every projection block, every dynamic block (mask bit-exact, activations in
+    tolerance, inactive pixels bitwise), head; then the oracle's own end-to-end
+    forward (oracle.lasnet_forward, the GPU network's masker biases) against the
+    GPU logits."""
     wts = synth.make_lasnet_weights(seed=5)
     net = L.LASResNet(n, wts, hw=hw)
     x = synth.make_image_batch(n, hw, seed=6).cuda()
-    net.forward(x, calibrate_r=0.5)  # masker biases from the activations each block sees
+    net.forward(synth.make_image_batch(n, hw, seed=7).cuda(), calibrate_r=0.5)  # biases from a separate batch
     torch.cuda.synchronize()
-    # layer by layer
     h = hw // 2
     y = L.stem(x, net.stem_w, net.stem_b)
     xin = synth.to_f64(x.cpu())[:, :, 4:4 + hw, :]
@@ -606,9 +609,14 @@ def test_lasnet_network_layerwise_matches_oracle():
             blk.forward(out)
             m_or, _ = oracle.masker(xin, synth.to_f64(blk.wm.cpu()), blk.bm, blk.shape.s)
             assert np.array_equal(blk.mask_buf.cpu().numpy(), m_or), f"stage {si} block {bi} mask"
-            want = oracle.dyn_block_def(xin, synth.weights_f64({k: v.cpu() for k, v in blk.wts.items()}), m_or,
-                                        blk.shape.s)
-            assert max_abs_rel(synth.to_f64(out.cpu()), want) <= BF16_TOL, f"stage {si} block {bi}"
+            idx_or, cnt = oracle.compact(m_or)
+            assert int(blk.count.item()) == cnt, f"stage {si} block {bi} count"
+            want = oracle.dyn_block_literal(xin, synth.weights_f64({k: v.cpu() for k, v in blk.wts.items()}), idx_or,
+                                            blk.shape.s)
+            got = synth.to_f64(out.cpu())
+            up = oracle.upsample(m_or, blk.shape.h, blk.shape.w, blk.shape.s).astype(bool)
+            assert max_abs_rel(got[up], want[up]) <= BF16_TOL, f"stage {si} block {bi}"
+            assert np.array_equal(got[~up], xin[~up]), f"stage {si} block {bi} inactive pixels"
         cur = out
     lg = L.head(cur, net.fc_w, net.fc_b).cpu().numpy()
     want_lg = oracle.head(synth.to_f64(cur.cpu()), synth.to_f64(net.fc_w.cpu()), synth.to_f64(net.fc_b.cpu()))
@@ -619,3 +627,20 @@ def test_lasnet_network_layerwise_matches_oracle():
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(net.logits, lg_eager)
+    # end to end: the oracle's own forward from the image with the same masker biases
+    meta = net.oracle_meta()
+    want_e2e, masks = oracle.lasnet_forward(xin_img(x, hw), synth.weights_f64_nested(wts), meta, return_masks=True)
+    diff_cells = sum(int((masks[k] != b.mask_buf.cpu().numpy()).sum()) for k, b in
+                     zip(sorted(masks, key=_block_order), net.blocks()))
+    total_cells = sum(b.shape.ncells for b in net.blocks())
+    assert diff_cells <= max(1, total_cells // 1000), f"{diff_cells} of {total_cells} decisions differ end to end"
+    assert max_abs_rel(lg_eager.cpu().numpy(), want_e2e) <= BF16_TOL
+
+
+def xin_img(x, hw):
+    return synth.to_f64(x.cpu())[:, :, 4:4 + hw, :]
+
+
+def _block_order(key):
+    si, b = key[1:].split("_b")
+    return int(si), int(b)

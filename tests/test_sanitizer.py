@@ -1,0 +1,38 @@
+"""compute-sanitizer tier: memcheck, racecheck, synccheck and
+initcheck over tests/sanitize_run.py, a tiny invocation of every kernel and
+schedule (incl. the cooperative decide's grid barrier).  -m gpu."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    if not os.path.exists(SAN):
+        pytest.skip("compute-sanitizer not installed")
+    from paper_2210_06223_b200 import build
+    build.build()
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
+def test_sanitizer_clean(tool):
+    cmd = [SAN, "--tool", tool, "--error-exitcode", "9", "--target-processes", "all"]
+    if tool == "initcheck":
+        cmd += ["--track-unused-memory", "no"]
+    cmd += [sys.executable, os.path.join(HERE, "sanitize_run.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500)
+    out = r.stdout + r.stderr
+    assert "sanitize run ok" in out, out[-4000:]
+    assert r.returncode == 0, out[-4000:]
+    assert "ERROR SUMMARY: 0 errors" in out or "RACECHECK SUMMARY: 0 hazards" in out, out[-4000:]
