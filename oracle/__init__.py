@@ -63,6 +63,7 @@ def _load():
         _lib.oracle_dyn_block_literal.argtypes = [D, i, i, i, i, i, i, D, D, D, D, D, D, I32, i, i, i, D]
         _lib.oracle_block_pixel.restype = ctypes.c_int
         _lib.oracle_block_pixel.argtypes = [D, i, i, i, i, i, D, D, D, D, D, D, U8, i, i, i, i, i, D]
+        _lib.oracle_proj_dyn_literal.argtypes = [D, i, i, i, i, i, i, D, D, D, D, D, D, D, D, I32, i, i, i, i, D]
         _lib.oracle_num_threads.restype = ctypes.c_int
         _lib.oracle_set_threads.argtypes = [i]
     return _lib
@@ -235,7 +236,7 @@ def _round_array(a, rmode):
     return np.vectorize(f, otypes=[np.float64])(a)
 
 
-def proj_block(x, wts, stride, rmode=ROUND_BF16):
+def proj_block(x, wts, stride, rmode=ROUND_BF16, round_shortcut=False):
     """Static projection (first) block of a ResNet stage, BN folded (the
     stride-s first block whose shortcut LASNet keeps dense), written out in
     fp64 numpy with the storage roundings of the stored tensors (h1, h2, y; the
@@ -262,7 +263,48 @@ def proj_block(x, wts, stride, rmode=ROUND_BF16):
             acc += win @ w2[:, dy, dx, :].T
     h2 = _round_array(np.maximum(acc + b2, 0.0), rmode)
     ds = x[:, ::s, ::s, :] @ wd.T + bd
+    if round_shortcut:  # the dynamic projection block stores R (reading R22)
+        ds = _round_array(ds, rmode)
     return _round_array(np.maximum(h2 @ w3.T + b3 + ds, 0.0), rmode)
+
+
+def proj_dyn_literal(x, wts, idx, s, stride, rmode=ROUND_BF16, threads: int | None = None):
+    """Dynamic projection (first) block, literal mode (C; NEXT-f1, reading R22):
+    R = rnd(Wd x_s + bd) dense; y = ReLU(R) everywhere, then for every active cell
+    of the output grid: gather the input window (side stride*(S-1)+3), conv1, the
+    valid 3x3 at stride `stride`, conv3 + R, ReLU, scatter."""
+    lib = _load()
+    if threads is not None:
+        lib.oracle_set_threads(int(threads))
+    x, xp = _d(x)
+    n, hi, wi, c_in = x.shape
+    c_mid = wts["w1"].shape[0]
+    c_out = wts["w3"].shape[0]
+    keep, wp = _weights(wts)
+    wd, wdp = _d(wts["wd"])
+    bd, bdp = _d(wts["bd"])
+    idx = np.asarray(idx, dtype=np.int32).reshape(-1)
+    count = int(idx.size)
+    idx, ip = _i32(idx if count else np.zeros(1, np.int32))
+    y = np.zeros((n, hi // stride, wi // stride, c_out))
+    _, yp = _d(y)
+    lib.oracle_proj_dyn_literal(xp, n, hi, wi, c_in, c_mid, c_out, *wp, wdp, bdp, ip, count, int(s), int(stride),
+                                rmode, yp)
+    return y
+
+
+def proj_dyn_def(x, wts, mask_cells, s, stride, rmode=ROUND_BF16):
+    """Dynamic projection block, definition mode (numpy): y = M ? static projection
+    with the stored shortcut : ReLU(rnd(Wd x_s + bd)), M = upsample(mask_cells, S)
+    on the output grid (reading R22)."""
+    x = np.asarray(x, np.float64)
+    st = int(stride)
+    ystat = proj_block(x, wts, st, rmode, round_shortcut=True)
+    wd, bd = np.asarray(wts["wd"], np.float64), np.asarray(wts["bd"], np.float64)
+    r = _round_array(x[:, ::st, ::st, :] @ wd.T + bd, rmode)
+    n, h, w, _ = ystat.shape
+    m = upsample(mask_cells, h, w, s).astype(bool)
+    return np.where(m[..., None], ystat, np.maximum(r, 0.0))
 
 
 def stem(x, w, b, rmode=ROUND_BF16):

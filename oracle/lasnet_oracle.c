@@ -374,6 +374,100 @@ int oracle_block_pixel(const double *x, int h, int w, int c_in, int c_mid, int c
     return 1;
 }
 
+/* ------------------------------------------------------------------------ */
+/* Dynamic projection (first) block of a stage, literal mode (SURVEY 8(f)    */
+/* NEXT-f1; 8(c) reading 9; reading R22).  The stage's first block  */
+/* changes resolution (stride 1 or 2) and channels (c_in -> c_out), so its    */
+/* residual is the 1x1 stride-s projection R = Wd x_s + bd, computed densely  */
+/* (the paper keeps the downsampling shortcut dense) and stored like   */
+/* any feature map (rounded).  The block output is y = ReLU(R + M F(x)) with   */
+/* the mask M on the OUTPUT grid ("the corresponding location of the     */
+/* output feature"): y = rnd(ReLU(R + conv3(h2) + b3)) on active pixels and   */
+/* ReLU(R) on the others -- for an identity block (R = x >= 0) this is the    */
+/* input fill of P:86.                                                         */
+/* The residual function F follows the gather -> compute -> scatter steps     */
+/* (P:89): an output patch of S x S pixels at stride s reads the   */
+/* input window of side s(S-1)+3 at origin (s S gy - 1, s S gx - 1); conv1 runs */
+/* on every in-image window pixel (0 outside the image, R6), conv2 is the     */
+/* valid 3x3 conv at stride s over the window, conv3 + R, ReLU, scatter.      */
+/*   x [n][hi][wi][c_in] (hi, wi multiples of s); y [n][hi/s][wi/s][c_out]     */
+/*   Wd [c_out][c_in], bd [c_out]; idx/count: active cells of the output grid   */
+/* ------------------------------------------------------------------------ */
+void oracle_proj_dyn_literal(const double *x, int n_img, int hi, int wi, int c_in,
+                             int c_mid, int c_out, const double *W1, const double *b1,
+                             const double *W2, const double *b2, const double *W3,
+                             const double *b3, const double *Wd, const double *bd,
+                             const int32_t *idx, int count, int s, int stride,
+                             int rmode, double *y)
+{
+    int h = hi / stride, w = wi / stride;
+    int gh = ceil_div(h, s), gw = ceil_div(w, s);
+    int side = stride * (s - 1) + 3;
+    size_t npx = (size_t)n_img * h * w;
+    double *R = (double *)malloc(sizeof(double) * npx * c_out);
+    /* the dense projection shortcut, stored rounded; y := ReLU(R) everywhere */
+    for (int n = 0; n < n_img; ++n)
+        for (int oy = 0; oy < h; ++oy)
+            for (int ox = 0; ox < w; ++ox) {
+                size_t p = ((size_t)n * h + oy) * w + ox;
+                const double *xs = x + (((size_t)n * hi + (size_t)oy * stride) * wi + (size_t)ox * stride) * c_in;
+                for (int co = 0; co < c_out; ++co) {
+                    double a = bd[co];
+                    const double *wr = Wd + (size_t)co * c_in;
+                    for (int ci = 0; ci < c_in; ++ci) a += wr[ci] * xs[ci];
+                    R[p * c_out + co] = store_round(a, rmode);
+                    y[p * c_out + co] = relu(R[p * c_out + co]);
+                }
+            }
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic, 1)
+#endif
+    for (int t = 0; t < count; ++t) {
+        double *win = (double *)malloc(sizeof(double) * (size_t)side * side * c_mid);
+        double *h2 = (double *)malloc(sizeof(double) * (size_t)s * s * c_mid);
+        int id = idx[t];
+        int n = id / (gh * gw), g = id % (gh * gw);
+        int gy = g / gw, gx = g % gw;
+        int oy0 = gy * s * stride - 1, ox0 = gx * s * stride - 1;
+        /* gather + conv1 over the input window */
+        for (int wy = 0; wy < side; ++wy)
+            for (int wx = 0; wx < side; ++wx) {
+                int sy = oy0 + wy, sx = ox0 + wx;
+                double *o = win + ((size_t)wy * side + wx) * c_mid;
+                if (sy < 0 || sy >= hi || sx < 0 || sx >= wi) {
+                    for (int c = 0; c < c_mid; ++c) o[c] = 0.0;
+                } else {
+                    conv1_pixel(x + (((size_t)n * hi + sy) * wi + sx) * c_in, c_in, c_mid, W1, b1, rmode, o);
+                }
+            }
+        /* valid 3x3 conv2 at stride s over the window -> S x S */
+        for (int py = 0; py < s; ++py)
+            for (int px = 0; px < s; ++px)
+                for (int c = 0; c < c_mid; ++c) {
+                    double a = b2[c];
+                    for (int dy = 0; dy < 3; ++dy)
+                        for (int dx = 0; dx < 3; ++dx) {
+                            const double *hp = win + ((size_t)(stride * py + dy) * side + (stride * px + dx)) * c_mid;
+                            const double *wr = W2 + (((size_t)c * 3 + dy) * 3 + dx) * c_mid;
+                            for (int ci = 0; ci < c_mid; ++ci) a += wr[ci] * hp[ci];
+                        }
+                    h2[((size_t)py * s + px) * c_mid + c] = store_round(relu(a), rmode);
+                }
+        /* conv3 + the stored shortcut R, ReLU, scatter (edge patches clipped, R7) */
+        for (int py = 0; py < s; ++py)
+            for (int px = 0; px < s; ++px) {
+                int yy = gy * s + py, xx = gx * s + px;
+                if (yy >= h || xx >= w) continue;
+                size_t p = ((size_t)n * h + yy) * w + xx;
+                conv3_residual_pixel(h2 + ((size_t)py * s + px) * c_mid, R + p * c_out, c_mid, c_out, W3, b3,
+                                     rmode, y + p * c_out);
+            }
+        free(win);
+        free(h2);
+    }
+    free(R);
+}
+
 int oracle_num_threads(void)
 {
 #ifdef _OPENMP
