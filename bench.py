@@ -167,7 +167,7 @@ def kernel_work(name: str, m: dict) -> dict:
     n, h, w (output), c_in, c_mid, c_out, stride, s, and for dynamic layers the
     mask geometry (P, halo_px, out_px, side, cells)."""
     e = 2
-    n, h, w = m["n"], m["h"], m["w"]
+    n, h, w = m["n"], m.get("h", 0), m.get("w", 0)
     c_in, c_mid, c_out, st = m.get("c_in", 0), m.get("c_mid", 0), m.get("c_out", 0), m.get("stride", 1)
     px, pxi = n * h * w, n * h * w * st * st
     W1, W2, W3 = c_mid * c_in * e, 9 * c_mid * c_mid * e, c_out * c_mid * e
@@ -183,6 +183,8 @@ def kernel_work(name: str, m: dict) -> dict:
         "conv1_dense": (pxi * (c_in + c_mid) * e + W1, 2 * pxi * c_in * c_mid),
         "conv2_dense": (pxi * c_mid * e + px * c_mid * e + W2, 2 * px * 9 * c_mid * c_mid),
         "subsample": (2 * px * c_in * e, 0),
+        # the dynamic projection block's dense shortcut R = Wd x_s + bd (masked ReLU epilogue)
+        "shortcut": (px * c_in * e + px * c_out * e + c_out * c_in * e + cells, 2 * px * c_in * c_out),
         "add_bias": (3 * c_out * 4, 0),
         "conv23_dense": (px * c_mid * e + 2 * px * c_out * e + W2 + W3,
                          2 * px * (9 * c_mid * c_mid + c_mid * c_out)),
@@ -203,8 +205,6 @@ def kernel_work(name: str, m: dict) -> dict:
     if name == "conv3_dense":
         if m.get("proj"):  # [h2 | x_s] x [W3 | Wd]^T, no residual read
             b, f = px * (c_mid + c_in) * e + px * c_out * e + c_out * (c_mid + c_in) * e, 2 * px * (c_mid + c_in) * c_out
-        elif m.get("shortcut"):  # the dynamic projection block's dense shortcut R = Wd x_s + bd
-            b, f = px * c_in * e + px * c_out * e + c_out * c_in * e + cells, 2 * px * c_in * c_out
         else:
             b, f = px * c_mid * e + 2 * px * c_out * e + W3, 2 * px * c_mid * c_out
         return {"bytes": int(b), "flops": int(f)}
@@ -458,7 +458,7 @@ def network_measure(args, world, rank, local, hbm, tfl):
                                  work=kernel_work(names[i], m)))
     # per-stage dynamic activation statistics (SURVEY 8(e) exchange step below)
     act = [int(b.count.item()) for b in net.blocks()]
-    cells = [b.shape.ncells for b in net.blocks()]
+    cells = [b.ncells for b in net.blocks()]
 
     # headline: the forward as one CUDA graph; N > 1 adds the logits all-gather (NCCL)
     g = net.capture(x)

@@ -72,7 +72,7 @@ typedef struct CUstream_st *lasnet_stream_t;
 typedef struct {
     int32_t n, h, w;              /* batch, output height, output width              */
     int32_t c_in, c_mid, c_out;   /* bottleneck widths; identity block: c_in == c_out */
-    int32_t stride;               /* 1 (stride-2 first blocks: not built, ERR_UNSUPPORTED) */
+    int32_t stride;               /* 1, or 2 for a stage's first (projection) block   */
     int32_t s;                    /* spatial granularity S >= 1               */
     int32_t dtype;                /* lasnet_dtype of x, y and w1..w3                  */
 } lasnet_block_desc;
@@ -189,7 +189,7 @@ size_t lasnet_proj_workspace_bytes(const lasnet_block_desc *desc);
  *   ws     lasnet_stem_workspace_bytes() bytes (packed weights), no contract
  * lasnet_maxpool: 3x3 stride-2 max pool, padding 1: x [n][2h][2w][c] -> y [n][h][w][c], c % 8 == 0.
  * lasnet_head: global average pool + fully connected classifier:
- *   x [n][hw][c], w [classes][c] (bf16), b [classes] fp32 -> logits [n][classes] fp32,
+ *   x [n][hw][c] (c % 8 == 0), w [classes][c] (bf16), b [classes] fp32 -> logits [n][classes] fp32,
  *   ws lasnet_head_workspace_bytes(n, c) bytes. */
 lasnet_status lasnet_stem(int32_t n, int32_t h, int32_t w, const void *x_pad, const void *wt, const float *b, void *y,
                           void *ws, size_t ws_bytes, lasnet_stream_t stream);
@@ -227,7 +227,21 @@ size_t lasnet_head_workspace_bytes(int32_t n, int32_t c);
  *   ws       lasnet_block_forward_workspace_bytes(desc, schedule) bytes, ALL ZERO
  *            before the first call (its leading control words are left zero by
  *            every call, except one grid-barrier generation word whose value is
- *            arbitrary; the rest is scratch).  Concurrent calls must not share it. */
+ *            arbitrary; the rest is scratch).  Concurrent calls must not share it.
+ *
+ * A stage's FIRST block (the dynamic projection block, SURVEY 8(f) NEXT-f1;
+ * DESIGN.md reading R22) is selected by non-NULL wts->wd / wts->bd: x is
+ * [n][h*stride][w*stride][c_in] (stride 1 or 2, desc h, w the OUTPUT dims),
+ * y [n][h][w][c_out] must not overlap x, and
+ *   R = Wd x_s + bd            dense 1x1 stride-s shortcut, stored bf16
+ *   mask on the output grid    the masker pools each cell's (stride*s)^2 input
+ *                              window (== lasnet_mask on x at granularity stride*s)
+ *   y  = ReLU(R)               on inactive cells
+ *   y  = ReLU(R + conv3(h2) + b3) on active cells, h2 the stride-s 3x3 over the
+ *                              input window of side stride*(s-1)+3 at origin
+ *                              (stride*s*gy - 1, stride*s*gx - 1), conv1 on it
+ * Only LASNET_SCHED_MASKER_SEPARATE (else ERR_UNSUPPORTED); bf16; c_in % 64,
+ * c_mid 64 or % 128, c_out % 128 (<= 2048); mask may be NULL (kept in ws). */
 typedef enum { LASNET_SCHED_MASKER_SEPARATE = 0, LASNET_SCHED_MASKER_FUSED = 1 } lasnet_schedule;
 lasnet_status lasnet_block_forward(const lasnet_block_desc *desc, const lasnet_block_weights *wts,
                                    const void *x, void *y, const float *wm, float bm, int32_t schedule,

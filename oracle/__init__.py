@@ -352,7 +352,7 @@ def set_threads(t: int) -> None:
     _load().oracle_set_threads(int(t))
 
 
-def lasnet_forward(x, weights, meta, calibrate_r=None, return_masks=False):
+def lasnet_forward(x, weights, meta, calibrate_r=None, return_masks=False, force_masks=None, backbone=False):
     """LAS-ResNet forward composed from the functions above (fp64 accumulation, bf16
     storage rounding at every stored tensor): stem -> max pool -> per stage the
     projection (first) block, then the identity blocks as dynamic blocks (masker
@@ -361,36 +361,56 @@ def lasnet_forward(x, weights, meta, calibrate_r=None, return_masks=False):
     BASELINE configs[2] (ResNet-101 depths 3-4-23-3, S_net 4-4-2-1).
       x        [n][H][W][8] fp64 image (channels 3..7 zero)
       weights  nested dict of fp64 arrays (synth.make_lasnet_weights layout)
-      meta     {"depths", "s_net", "bm": {block key: masker bias}} as the GPU network's
+      meta     {"depths", "s_net", "bm": {block key: masker bias}, "dyn_proj"} as the GPU network's
                LASResNet.oracle_meta(); with calibrate_r set, each block's bias is
                instead chosen from this forward's own logits so that ~r of its cells
                are active (midway between two neighbouring logits) and written to meta.
-    Returns logits [n][classes] (and the per-block masks when return_masks)."""
+    force_masks  {block key: cell mask}: take these decisions instead of the masker's
+               (the masker still runs and its own masks are returned) -- lets a test
+               follow another implementation's decisions through the whole chain.
+    backbone   stop after the last stage and return the four stage outputs.
+    Returns logits [n][classes] (or the stage outputs), and the per-block masks
+    when return_masks."""
     depths, s_net = meta["depths"], meta["s_net"]
     bms = meta.setdefault("bm", {})
+    dyn_proj = meta.get("dyn_proj", True)
     cur = maxpool(stem(x, weights["stem_w"], weights["stem_b"]))
     masks = {}
+    feats = []
+
+    def decide(key, xin, wm, s_mask):
+        if calibrate_r is not None:
+            _, l0 = masker(xin, wm, 0.0, s_mask)
+            lg = np.sort(l0.reshape(-1))
+            k = int(round(calibrate_r * lg.size))
+            if k <= 0:
+                bm = -(lg[-1] + 1.0)
+            elif k >= lg.size:
+                bm = -(lg[0] - 1.0)
+            else:
+                bm = -0.5 * (lg[lg.size - k - 1] + lg[lg.size - k])
+            bms[key] = float(np.float32(bm))
+        m, _ = masker(xin, wm, bms[key], s_mask)
+        masks[key] = m
+        if force_masks is not None and key in force_masks:
+            m = np.asarray(force_masks[key], np.uint8)
+        return compact(m)[0]
+
     for si, (depth, s) in enumerate(zip(depths, s_net)):
         stride = 1 if si == 0 else 2
         pw = weights[f"s{si}_proj"]
-        cur = proj_block(cur, pw, stride)
+        if dyn_proj:  # the dynamic first block (reading R22): masker over each cell's stride*S input window
+            idx = decide(f"s{si}_proj", cur, pw["wm"], s * stride)
+            cur = proj_dyn_literal(cur, pw, idx, s, stride)
+        else:
+            cur = proj_block(cur, pw, stride)
         for b in range(1, depth):
             key = f"s{si}_b{b}"
             wb = weights[key]
-            if calibrate_r is not None:
-                _, l0 = masker(cur, wb["wm"], 0.0, s)
-                lg = np.sort(l0.reshape(-1))
-                k = int(round(calibrate_r * lg.size))
-                if k <= 0:
-                    bm = -(lg[-1] + 1.0)
-                elif k >= lg.size:
-                    bm = -(lg[0] - 1.0)
-                else:
-                    bm = -0.5 * (lg[lg.size - k - 1] + lg[lg.size - k])
-                bms[key] = float(np.float32(bm))
-            m, _ = masker(cur, wb["wm"], bms[key], s)
-            idx, _ = compact(m)
-            masks[key] = m
+            idx = decide(key, cur, wb["wm"], s)
             cur = dyn_block_literal(cur, wb, idx, s)
+        feats.append(cur)
+    if backbone:
+        return (feats, masks) if return_masks else feats
     logits = head(cur, weights["fc_w"], weights["fc_b"])
     return (logits, masks) if return_masks else logits

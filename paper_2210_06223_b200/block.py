@@ -13,6 +13,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
+from ._lib import SCHED_SEPARATE
 
 _DT = {torch.bfloat16: _lib.LASNET_BF16, torch.float32: _lib.LASNET_F32}
 
@@ -193,6 +194,36 @@ def block_forward(x: torch.Tensor, wts: dict, wm: torch.Tensor, bm: float, s: in
     return y, m, idx, count
 
 
+def proj_block_forward(x: torch.Tensor, wts: dict, wm: torch.Tensor, bm: float, s: int, stride: int,
+                       ws: torch.Tensor | None = None):
+    """The dynamic projection (first) block of a stage, steps 1-5 in one C-ABI call
+    (lasnet_block_forward with the shortcut weights wts["wd"], wts["bd"]; NEXT-f1,
+    DESIGN.md reading R22): x [n, h*stride, w*stride, c_in] -> y [n, h, w, c_out]
+    with y = ReLU(R + M F(x)), R = Wd x_s + bd computed densely, the mask on the
+    output grid from the masker pooling each cell's stride*S input window.
+    Returns (y, mask, idx, count)."""
+    _require_cuda(x, wm)
+    lib = _lib.load()
+    n, hi, wi, c_in = x.shape
+    c_mid, c_out = wts["w1"].shape[0], wts["w3"].shape[0]
+    if hi % stride or wi % stride:
+        raise ValueError("input size must be a multiple of the stride")
+    h, w = hi // stride, wi // stride
+    gh, gw = grid(h, w, s)
+    d = _lib.BlockDesc(n, h, w, c_in, c_mid, c_out, stride, s, _DT[x.dtype])
+    wsb = lib.lasnet_block_forward_workspace_bytes(ctypes.byref(d), SCHED_SEPARATE)
+    ws = ws if ws is not None else torch.zeros(max(wsb, 1), dtype=torch.uint8, device=x.device)
+    y = torch.empty((n, h, w, c_out), dtype=x.dtype, device=x.device)
+    m = torch.empty((n, gh, gw), dtype=torch.uint8, device=x.device)
+    idx = torch.empty(max(n * gh * gw, 1), dtype=torch.int32, device=x.device)
+    count = torch.empty(1, dtype=torch.int32, device=x.device)
+    wt = _lib.BlockWeights(*(wts[k].data_ptr() for k in ("w1", "b1", "w2", "b2", "w3", "b3", "wd", "bd")))
+    _lib.check("lasnet_block_forward", lib.lasnet_block_forward(
+        ctypes.byref(d), ctypes.byref(wt), _p(x), _p(y), _p(wm), float(bm), SCHED_SEPARATE, _p(m), _p(idx),
+        _p(count), _p(ws), ws.numel(), _stream()))
+    return y, m, idx, count
+
+
 def choose_schedule(n, h, w, c_in, c_mid, c_out, s, r, dtype=torch.bfloat16) -> int:
     d = make_desc(n, h, w, c_in, c_mid, c_out, s, dtype)
     return int(_lib.load().lasnet_choose_schedule(ctypes.byref(d), float(r)))
@@ -265,6 +296,10 @@ class DynBlock:
         self.dense_desc = dd
         self._dense_ws = None
         self.launches = 0
+
+    @property
+    def ncells(self):
+        return self.shape.ncells
 
     def mask(self, x: torch.Tensor, want_logits: bool = False):
         lib = _lib.load()
@@ -402,6 +437,62 @@ class DynBlock:
         self.mask(x, want_logits=True)
         lg = self.logits.flatten().double().sort().values.cpu()
         self.bm = saved
+        G = lg.numel()
+        k = int(round(r * G))
+        if k <= 0:
+            b = -(float(lg[-1]) + 1.0)
+        elif k >= G:
+            b = -(float(lg[0]) - 1.0)
+        else:
+            b = -0.5 * (float(lg[G - k - 1]) + float(lg[G - k]))
+        self.bm = float(torch.tensor(b, dtype=torch.float32))
+        return self.bm
+
+
+class ProjDynBlock:
+    """The dynamic projection (first) block of a stage (NEXT-f1, reading R22) with
+    device-resident weights and preallocated buffers: x [n, h*stride, w*stride,
+    c_in] -> self.y [n, h, w, c_out].  One lasnet_block_forward call per forward:
+    masker (stride*S input window per output cell) + compaction, the dense 1x1
+    stride-s shortcut, gather + conv1 over the active windows, the stride-s 3x3,
+    conv3 + scatter-add onto the shortcut."""
+
+    dynamic = True
+
+    def __init__(self, n, h_in, w_in, c_in, c_mid, c_out, stride, s, wts, wm, bm=0.0, device="cuda"):
+        self.wts = {k: v.to(device).contiguous() for k, v in wts.items() if k != "wm"}
+        self.wm = wm.to(device).float().contiguous()
+        self.bm = float(bm)
+        self.stride, self.s = stride, s
+        self.h, self.w = h_in // stride, w_in // stride
+        self.c_out = c_out
+        self.desc = _lib.BlockDesc(n, self.h, self.w, c_in, c_mid, c_out, stride, s, _lib.LASNET_BF16)
+        # the masker's view: the input at granularity stride * S (same cell grid)
+        self.mask_desc = _lib.BlockDesc(n, h_in, w_in, c_in, c_in, c_in, 1, s * stride, _lib.LASNET_BF16)
+        self.wt = _lib.BlockWeights(*(self.wts[k].data_ptr() for k in ("w1", "b1", "w2", "b2", "w3", "b3", "wd", "bd")))
+        lib = _lib.load()
+        gh, gw = grid(self.h, self.w, s)
+        self.ncells = n * gh * gw
+        self.mask_buf = torch.empty((n, gh, gw), dtype=torch.uint8, device=device)
+        self.logits = torch.empty((n, gh, gw), dtype=torch.float64, device=device)
+        self.idx = torch.empty(max(self.ncells, 1), dtype=torch.int32, device=device)
+        self.count = torch.zeros(1, dtype=torch.int32, device=device)
+        self.ws = torch.zeros(max(lib.lasnet_block_forward_workspace_bytes(ctypes.byref(self.desc), SCHED_SEPARATE), 1),
+                              dtype=torch.uint8, device=device)
+        self.y = torch.empty((n, self.h, self.w, c_out), dtype=torch.bfloat16, device=device)
+
+    def forward(self, x):
+        _lib.check("lasnet_block_forward", _lib.load().lasnet_block_forward(
+            ctypes.byref(self.desc), ctypes.byref(self.wt), _p(x), _p(self.y), _p(self.wm), self.bm, SCHED_SEPARATE,
+            _p(self.mask_buf), _p(self.idx), _p(self.count), _p(self.ws), self.ws.numel(), _stream()))
+        return self.y
+
+    def calibrate_bias(self, x: torch.Tensor, r: float) -> float:
+        """Masker bias placing ~r of the cells above threshold on x (as DynBlock)."""
+        lib = _lib.load()
+        _lib.check("lasnet_mask", lib.lasnet_mask(ctypes.byref(self.mask_desc), _p(x), _p(self.wm), 0.0,
+                                                  _p(self.mask_buf), _p(self.logits), _stream()))
+        lg = self.logits.flatten().double().sort().values.cpu()
         G = lg.numel()
         k = int(round(r * G))
         if k <= 0:

@@ -88,19 +88,12 @@ template <bool DENSE>
 __device__ __forceinline__ int tile_pixel(const ConvArgs &args, int tile, int r, int rows_per_tile, int M) {
     if (r >= rows_per_tile) return -1;
     if (DENSE) {
-        const int per_img = args.W * args.rows_h;
-        int n0, y0;
-        if (args.rows_h < args.H) {
-            const int tpi = (args.H + args.rows_h - 1) / args.rows_h;
-            n0 = tile / tpi;
-            y0 = (tile - n0 * tpi) * args.rows_h;
-        } else {
-            n0 = tile * args.imgs_box;
-            y0 = 0;
-        }
-        const int im = r / per_img, rr = r - im * per_img, yy = y0 + rr / args.W, xx = rr % args.W;
+        const int per_img = args.cols_w * args.rows_h;
+        int n0, y0, x0;
+        dense_tile_origin(args, tile, n0, y0, x0);
+        const int im = r / per_img, rr = r - im * per_img, yy = y0 + rr / args.cols_w, xx = x0 + rr % args.cols_w;
         const int n = n0 + im;
-        return (n < args.n_img && yy < args.H) ? (n * args.H + yy) * args.W + xx : -1;
+        return (n < args.n_img && yy < args.H && xx < args.W) ? (n * args.H + yy) * args.W + xx : -1;
     }
     return out_pixel(args, tile * rows_per_tile + r, M);
 }
@@ -281,16 +274,8 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
         for (int i = 0; i < ntl; ++i) {
             const int tile = tile_of(i);
             if (lane == 0) {
-                int n0 = 0, y0 = 0;
-                if (DENSE) {
-                    if (args.rows_h < args.H) {
-                        const int tpi = (args.H + args.rows_h - 1) / args.rows_h;
-                        n0 = tile / tpi;
-                        y0 = (tile - n0 * tpi) * args.rows_h;
-                    } else {
-                        n0 = tile * args.imgs_box;
-                    }
-                }
+                int n0 = 0, y0 = 0, x0 = 0;
+                if (DENSE) dense_tile_origin(args, tile, n0, y0, x0);
                 T23(i, 0);
                 for (int kb = 0; kb < kb2; ++kb, ++it) {
                     const int st = it % kStages;
@@ -300,7 +285,7 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
                     if (PAIR) {  // own A rows + own half of the W2 K-block; both complete on the lead's barrier
                         if (lead) mbar_arrive_expect_tx(fb, 2 * (args.box_rows * 128 + (KC / 2) * 128));
                         tma_load_2d_pair(sa + kABytes, &args.tmap_b, fb, kb * kBK, rank * (KC / 2));
-                        if (DENSE) tma_load_5d_pair(sa, &args.tmap_a, fb, 0, dx - 1, y0 + dy - 1, n0, c0 >> 6);
+                        if (DENSE) tma_load_5d_pair(sa, &args.tmap_a, fb, 0, x0 + dx - 1, y0 + dy - 1, n0, c0 >> 6);
                         else tma_load_5d_pair(sa, &args.tmap_a, fb, 0, dx, dy, tile * args.units_per_tile, c0 >> 6);
                         continue;
                     }
@@ -313,7 +298,9 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
                     else
                         tma_load_2d(sa + kABytes, &args.tmap_b, fb, kb * kBK, 0);
                     // h1 is channel-chunk-major: [c_mid/64][P][S+2][S+2][64] (dense: [c_mid/64][N][H][W][64])
-                    if (DENSE) tma_load_5d(sa, &args.tmap_a, fb, 0, dx - 1, y0 + dy - 1, n0, c0 >> 6);
+                    if (DENSE) tma_load_5d(sa, &args.tmap_a, fb, 0, x0 + dx - 1, y0 + dy - 1, n0, c0 >> 6);
+                    else if (args.conv_stride == 2)  // stride-2 3x3 (projection block): parity view of the windows
+                        tma_load_5d(sa, &args.tmap_s[((dy & 1) << 1) | (dx & 1)], fb, 0, dx >> 1, dy >> 1, t0, c0 >> 6);
                     else tma_load_5d(sa, &args.tmap_a, fb, 0, dx, dy, t0, c0 >> 6);
                 }
             }

@@ -29,7 +29,7 @@ __device__ __forceinline__ const float *simt_row_ptr(const ConvArgs &a, int src,
             if (sy < 0 || sy >= a.H || sx < 0 || sx >= a.W) return nullptr;
             return A + (size_t)(src + (dy - 1) * a.W + (dx - 1)) * a.a_ld + c0;
         }
-        return A + (size_t)(src + (dy - 1) * (a.S + 2) + (dx - 1)) * a.a_ld + c0;
+        return A + (size_t)(src + (dy - 1) * a.hs + (dx - 1)) * a.a_ld + c0;
     }
     return A + (size_t)src * a.a_ld + c0;
 }

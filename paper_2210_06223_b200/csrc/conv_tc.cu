@@ -133,18 +133,6 @@ __device__ __forceinline__ TileGeo tile_geo(const ConvArgs &a, int BN) {
     return g;
 }
 
-// CONV2_DENSE tile -> (first image, first image row) of its box.
-__device__ __forceinline__ void dense2_tile(const ConvArgs &a, int mt, int &n0, int &y0) {
-    if (a.rows_h < a.H) {
-        const int tpi = (a.H + a.rows_h - 1) / a.rows_h;
-        n0 = mt / tpi;
-        y0 = (mt - n0 * tpi) * a.rows_h;
-    } else {
-        n0 = mt * a.imgs_box;
-        y0 = 0;
-    }
-}
-
 template <int MODE, int BN>
 __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(const __grid_constant__ ConvArgs args) {
     using C = Cfg<MODE, BN>;
@@ -217,8 +205,8 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                 const int mt = tile / geo.n_tiles_n;
                 const int n0 = (tile - mt * geo.n_tiles_n) * BN;
                 const int u0 = MODE == CONV2_DYN ? mt * args.units_per_tile : 0;  // first patch (conv2 dyn)
-                int d2n = 0, d2y = 0;
-                if (MODE == CONV2_DENSE) dense2_tile(args, mt, d2n, d2y);
+                int d2n = 0, d2y = 0, d2x = 0;
+                if (MODE == CONV2_DENSE) dense_tile_origin(args, mt, d2n, d2y, d2x);
                 TRACE(lt, 0);
                 for (int kb = 0; kb < num_kb; ++kb, ++it) {
                     const int stage = it % ST;
@@ -235,15 +223,19 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     KTRACE(it, 1);
                     if (MODE == CONV2_DYN) {
                         const int tap = kb / kpt, dy = tap / 3, dx = tap - dy * 3;
-                        tma_load_5d(sa, &args.tmap_a, fb, 0, dx, dy, u0, kb - tap * kpt);  // h1 [c/64][P][S+2][S+2][64]
+                        if (args.conv_stride == 2)  // stride-2 3x3: parity view (dy&1, dx&1) of the windows
+                            tma_load_5d(sa, &args.tmap_s[((dy & 1) << 1) | (dx & 1)], fb, 0, dx >> 1, dy >> 1, u0,
+                                        kb - tap * kpt);
+                        else
+                            tma_load_5d(sa, &args.tmap_a, fb, 0, dx, dy, u0, kb - tap * kpt);  // h1 [c/64][P][hs][hs][64]
                     } else if (MODE == CONV2_DENSE) {
                         const int tap = kb / kpt, dy = tap / 3, dx = tap - dy * 3;
                         if (args.conv_stride == 2) {
                             // input (2 o + d - 1): view of parity (d != 1), coordinate o - (d == 0)
                             const int v = ((dy != 1) << 1) | (dx != 1);
-                            tma_load_5d(sa, &args.tmap_s[v], fb, 0, -(dx == 0), d2y - (dy == 0), d2n, kb - tap * kpt);
+                            tma_load_5d(sa, &args.tmap_s[v], fb, 0, d2x - (dx == 0), d2y - (dy == 0), d2n, kb - tap * kpt);
                         } else {
-                            tma_load_5d(sa, &args.tmap_a, fb, 0, dx - 1, d2y + dy - 1, d2n, kb - tap * kpt);  // [c/64][N][H][W][64]
+                            tma_load_5d(sa, &args.tmap_a, fb, 0, d2x + dx - 1, d2y + dy - 1, d2n, kb - tap * kpt);  // [c/64][N][H][W][64]
                         }
                     } else if (MODE == STEM) {
                         // K-block kb = kernel row dy: 4 boxes of W/4 output columns each (residue k of
@@ -273,7 +265,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
         const int prow = pt >> 3, pch = pt & 7;
         const __nv_bfloat16 *X = static_cast<const __nv_bfloat16 *>(args.a_src);
         const int M = gemm_rows(MODE, args);
-        const int hs = args.S + 2, hs2 = hs * hs;
+        const int hs = args.hs, hs2 = hs * hs;
         auto load_cells = [&](int tile, int (&cell)[RPT], int (&jj)[RPT]) {
             const int r0 = (tile / geo.n_tiles_n) * kBM + prow;
             int t = args.fd_hs2.div(r0), j = r0 - t * hs2;
@@ -298,7 +290,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     int n, gy, gx;
                     cell_decode(args, cell[i], n, gy, gx);
                     const int jy = args.fd_hs.div(jj[i]);
-                    const int hy = gy * args.S - 1 + jy, hx = gx * args.S - 1 + (jj[i] - jy * hs);
+                    const int hy = gy * args.S_in - 1 + jy, hx = gx * args.S_in - 1 + (jj[i] - jy * hs);
                     if (hy >= 0 && hy < args.H && hx >= 0 && hx < args.W) src[i] = (n * args.H + hy) * args.W + hx;
                 }
             }
@@ -483,6 +475,17 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             const uint32_t sbuf = staging + b * C::kStagingBytes;
             bool zero = false;  // conv1: halo pixel outside the image stores 0 (R6)
             if (MODE == CONV1_DYN) zero = mt * kBM + r < M && halo_pixel(args, mt * kBM + r, M) < 0;
+            bool relu = !args.no_relu;
+            if (MODE == CONV3_DENSE && args.relu_mask != nullptr) {
+                // dynamic projection shortcut: ReLU(R) on inactive cells, R itself on active ones
+                const int m = mt * kBM + r;
+                if (m < M) {
+                    const int n = args.fd_HW.div(m), rem = m - n * (int)args.fd_HW.d;
+                    const int yy = args.fd_W.div(rem), xx = rem - yy * args.W;
+                    const int cell = (n * args.Gh + args.fd_S.div(yy)) * args.Gw + args.fd_S.div(xx);
+                    relu = __ldg(args.relu_mask + cell) == 0;
+                }
+            }
             int cell_ahead = -2;
             if (kResid) {
                 cell_ahead = row_cell(tile + (NSTG - 1) * gridDim.x);  // idx load in flight during this tile
@@ -523,7 +526,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         float lo = f[2 * e], hi = f[2 * e + 1];
-                        if (!args.no_relu) lo = fmaxf(lo, 0.f), hi = fmaxf(hi, 0.f);
+                        if (relu) lo = fmaxf(lo, 0.f), hi = fmaxf(hi, 0.f);
                         if (zero) lo = hi = 0.f;
                         pk[e] = pack_bf16x2(lo, hi);
                     }
@@ -567,10 +570,10 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             if (tid == 0) TRACE(lt, 5);
             if (tid == 0) {
                 if (MODE == CONV2_DENSE) {
-                    int d2n, d2y;
-                    dense2_tile(args, mt, d2n, d2y);
+                    int d2n, d2y, d2x;
+                    dense_tile_origin(args, mt, d2n, d2y, d2x);
                     for (int c = 0; c < BN / 64; ++c)
-                        tma_store_4d(&args.tmap_out, sbuf + c * kChunkBytes, n0 + c * 64, 0, d2y, d2n);
+                        tma_store_4d(&args.tmap_out, sbuf + c * kChunkBytes, n0 + c * 64, d2x, d2y, d2n);
                 } else if (MODE == STEM) {  // the tile's rows in residue order back to output columns
                     const int n = mt / args.H, oy = mt - n * args.H;
                     for (int k = 0; k < 4; ++k)

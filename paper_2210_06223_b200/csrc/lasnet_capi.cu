@@ -127,7 +127,7 @@ lasnet_status check_channels(const lasnet_block_desc *d) {
     // tcgen05 N tiles are 64 (N == 64) or 128 wide
     if ((d->c_mid != 64 && d->c_mid % 128) || (d->c_out != 64 && d->c_out % 128)) return LASNET_ERR_UNSUPPORTED;
     if (d->c_out > 2048 || d->c_mid > 2048) return LASNET_ERR_UNSUPPORTED;  // bias staged in smem
-    if (d->dtype == LASNET_BF16 && (d->s > 11 || d->w > 128)) return LASNET_ERR_UNSUPPORTED;  // TMA box limits
+    if (d->dtype == LASNET_BF16 && d->s > 11) return LASNET_ERR_UNSUPPORTED;  // TMA box limits
     if (d->stride != 1) return LASNET_ERR_UNSUPPORTED;  // stride-2 first blocks: NEXT-f1
     if (d->c_in != d->c_out) return LASNET_ERR_UNSUPPORTED;  // identity residual only
     return LASNET_OK;
@@ -244,6 +244,35 @@ bool tmap5(CUtensorMap *m, const void *base, const uint64_t (&d)[5], const uint3
     return tmap(m, base, 5, d, b);
 }
 
+// Tile geometry of a dense 3x3 over an n x h x w map (128-row tiles): whole
+// images per box when h*w <= 128; else bands of rows_h rows of the whole width
+// (w <= 128), or, for w > 128 (COCO-shaped maps), column blocks of cols_w columns
+// x rows_h rows, cols_w chosen to fill the 128 rows best.
+void dense_tiling(ConvArgs &a, int n, int h, int w) {
+    a.tiles_x = 1;
+    a.cols_w = w;
+    if (h * w <= 128) {
+        a.rows_h = h;
+        a.imgs_box = 128 / (h * w);
+        a.dense_tiles = (n + a.imgs_box - 1) / a.imgs_box;
+    } else {
+        a.imgs_box = 1;
+        if (w <= 128) {
+            a.rows_h = 128 / w;
+        } else {
+            int best = 0;
+            for (int k = (w + 127) / 128; k <= (w + 7) / 8; ++k) {
+                const int cw = (w + k - 1) / k, rh = 128 / cw;
+                const int rows = rh < h ? rh : h;
+                if (rows * cw > best) best = rows * cw, a.cols_w = cw, a.rows_h = rows;
+            }
+            a.tiles_x = (w + a.cols_w - 1) / a.cols_w;
+        }
+        a.dense_tiles = n * ((h + a.rows_h - 1) / a.rows_h) * a.tiles_x;
+    }
+    a.box_rows = a.cols_w * a.rows_h * a.imgs_box;
+}
+
 // N tile of conv_tc's launch for `mode` (must match launch_mode in conv_tc.cu)
 int bn_of(int n, int mode) {
     if (n == 64) return 64;
@@ -254,9 +283,27 @@ int bn_of(int n, int mode) {
 // Fills the TMA descriptors and tile geometry of one tcgen05 convolution and
 // returns the capacity bound on its M tiles (grid sizing), or -1 on failure.
 // x/y: block input/output; h1/h2: workspace intermediates; cap: patch capacity.
+// The stride-2 3x3 over gathered windows [c/64][cap][hs][hs][64] reads, for tap (dy, dx),
+// window positions (2 py + dy, 2 px + dx): the parity view (dy & 1, dx & 1) -- every second
+// position and row starting at (dy & 1, dx & 1) -- at coordinates (dx >> 1, dy >> 1).
+bool window_parity_views(ConvArgs &a, const void *h1, int cap, int hs, int S, int C, int units) {
+    bool ok = true;
+    for (int v = 0; v < 4 && ok; ++v) {
+        const int py = v >> 1, px = v & 1;
+        const uint64_t dims[5] = {64, (uint64_t)(hs - px + 1) / 2, (uint64_t)(hs - py + 1) / 2, (uint64_t)cap,
+                                  (uint64_t)(C / 64)};
+        const uint64_t str[4] = {2 * 128, 2 * (uint64_t)hs * 128, (uint64_t)hs * hs * 128,
+                                 (uint64_t)cap * hs * hs * 128};
+        const uint32_t box[5] = {64, (uint32_t)S, (uint32_t)S, (uint32_t)units, 1};
+        ok = tmap_strided(&a.tmap_s[v], static_cast<const uint8_t *>(h1) + ((uint64_t)py * hs + px) * 128, 5, dims, str,
+                          box);
+    }
+    return ok;
+}
+
 int prepare_tc(int mode, ConvArgs &a, const lasnet_block_desc *d, const void *x, const void *y, const void *h1,
                const void *h2, int cap) {
-    const int S = d->s, hs = S + 2, C = d->c_mid;
+    const int S = d->s, hs = a.hs, C = d->c_mid;
     const uint64_t px = (uint64_t)d->n * d->h * d->w;
     bool ok = tmap2(&a.tmap_b, a.w, a.K, a.N, 64, bn_of(a.N, mode));
     switch (mode) {
@@ -271,6 +318,7 @@ int prepare_tc(int mode, ConvArgs &a, const lasnet_block_desc *d, const void *x,
             a.box_rows = a.units_per_tile * S * S;
             ok = ok && tmap5(&a.tmap_a, h1, {64, (uint64_t)hs, (uint64_t)hs, (uint64_t)cap, (uint64_t)(C / 64)},
                              {64, (uint32_t)S, (uint32_t)S, (uint32_t)a.units_per_tile, 1});
+            if (a.conv_stride == 2) ok = ok && window_parity_views(a, h1, cap, hs, S, C, a.units_per_tile);
             ok = ok && tmap2(&a.tmap_out, h2, C, (uint64_t)cap * S * S, 64, a.box_rows);
             return ok ? (cap + a.units_per_tile - 1) / a.units_per_tile : -1;
         }
@@ -286,19 +334,10 @@ int prepare_tc(int mode, ConvArgs &a, const lasnet_block_desc *d, const void *x,
             return ok ? (int)((px + 127) / 128) : -1;
         }
         case CONV2_DENSE: {
-            if (d->h * d->w <= 128) {
-                a.rows_h = d->h;
-                a.imgs_box = 128 / (d->h * d->w);
-                a.dense_tiles = (d->n + a.imgs_box - 1) / a.imgs_box;
-            } else {
-                a.rows_h = 128 / d->w;
-                a.imgs_box = 1;
-                a.dense_tiles = d->n * ((d->h + a.rows_h - 1) / a.rows_h);
-            }
-            a.box_rows = d->w * a.rows_h * a.imgs_box;
+            dense_tiling(a, d->n, d->h, d->w);
             ok = ok && tmap5(&a.tmap_a, h1, {64, (uint64_t)d->w, (uint64_t)d->h, (uint64_t)d->n, (uint64_t)(C / 64)},
-                             {64, (uint32_t)d->w, (uint32_t)a.rows_h, (uint32_t)a.imgs_box, 1});
-            ok = ok && tmap4(&a.tmap_out, h2, C, d->w, d->h, d->n, 64, d->w, a.rows_h, a.imgs_box);
+                             {64, (uint32_t)a.cols_w, (uint32_t)a.rows_h, (uint32_t)a.imgs_box, 1});
+            ok = ok && tmap4(&a.tmap_out, h2, C, d->w, d->h, d->n, 64, a.cols_w, a.rows_h, a.imgs_box);
             return ok ? a.dense_tiles : -1;
         }
         case CONV3_DENSE: {
@@ -336,7 +375,7 @@ bool use_direct(const lasnet_block_desc *d) {
 
 cudaError_t run_conv23(const lasnet_block_desc *d, bool dense, ConvArgs a, const lasnet_block_weights *w,
                        const void *x, void *y, const void *h1, int cap, cudaStream_t st) {
-    const int S = d->s, hs = S + 2, C = d->c_mid;
+    const int S = d->s, hs = a.hs, C = d->c_mid;
     a.a_src = h1; a.w = w->w2; a.bias = w->b2; a.out = y; a.resid = x;
     a.K = 9 * C; a.N = C; a.a_ld = C; a.out_ld = d->c_out;
     a.w3 = w->w3; a.bias3 = w->b3; a.n3 = d->c_out;
@@ -359,23 +398,14 @@ cudaError_t run_conv23(const lasnet_block_desc *d, bool dense, ConvArgs a, const
         return !(e && e[0] == '0');
     }();
     a.balance = bal_env ? 1 : 0;
-    a.pair = pair_env && !a.direct ? 1 : 0;
+    a.pair = pair_env && !a.direct && a.conv_stride == 1 ? 1 : 0;
     a.cluster = a.direct ? 1 : a.pair ? 2 : (C / cl_env >= 8 && nc3 / cl_env >= 8) ? cl_env : 1;
     bool ok = tmap2(&a.tmap_b, a.w, a.K, a.N, 64, C / a.cluster) && tmap2(&a.tmap_b3, w->w3, C, d->c_out, 64, nc3 / a.cluster);
     int tiles;
     if (dense) {
-        if (d->h * d->w <= 128) {
-            a.rows_h = d->h;
-            a.imgs_box = 128 / (d->h * d->w);
-            a.dense_tiles = (d->n + a.imgs_box - 1) / a.imgs_box;
-        } else {
-            a.rows_h = 128 / d->w;
-            a.imgs_box = 1;
-            a.dense_tiles = d->n * ((d->h + a.rows_h - 1) / a.rows_h);
-        }
-        a.box_rows = d->w * a.rows_h * a.imgs_box;
+        dense_tiling(a, d->n, d->h, d->w);
         ok = ok && tmap5(&a.tmap_a, h1, {64, (uint64_t)d->w, (uint64_t)d->h, (uint64_t)d->n, (uint64_t)(C / 64)},
-                         {64, (uint32_t)d->w, (uint32_t)a.rows_h, (uint32_t)a.imgs_box, 1});
+                         {64, (uint32_t)a.cols_w, (uint32_t)a.rows_h, (uint32_t)a.imgs_box, 1});
         tiles = a.dense_tiles;
     } else {
         a.units_per_tile = 128 / (S * S);
@@ -386,6 +416,8 @@ cudaError_t run_conv23(const lasnet_block_desc *d, bool dense, ConvArgs a, const
         else
             ok = ok && tmap5(&a.tmap_a, h1, {64, (uint64_t)hs, (uint64_t)hs, (uint64_t)cap, (uint64_t)(C / 64)},
                              {64, (uint32_t)S, (uint32_t)S, (uint32_t)a.units_per_tile, 1});
+        if (!a.direct && a.conv_stride == 2)
+            ok = ok && window_parity_views(a, h1, cap, hs, S, C, a.units_per_tile);
         tiles = (cap + a.units_per_tile - 1) / a.units_per_tile;
     }
     if (!ok) return cudaErrorInvalidValue;
@@ -437,11 +469,28 @@ ConvArgs base_args(const lasnet_block_desc *d) {
     a.Gw = (d->w + d->s - 1) / d->s;
     a.fd_G = FastDiv((uint32_t)(a.Gh * a.Gw));
     a.fd_Gw = FastDiv((uint32_t)a.Gw);
+    a.S_in = d->s;
+    a.hs = d->s + 2;
     a.fd_hs = FastDiv((uint32_t)(d->s + 2));
     a.fd_hs2 = FastDiv((uint32_t)((d->s + 2) * (d->s + 2)));
     a.fd_S = FastDiv((uint32_t)d->s);
     a.fd_SS = FastDiv((uint32_t)(d->s * d->s));
+    a.fd_HW = FastDiv((uint32_t)(d->h * d->w));
+    a.fd_W = FastDiv((uint32_t)d->w);
+    a.relu_mask = nullptr;
+    a.conv_stride = 1;
     return a;
+}
+
+// conv1 windows of a stride-`st` block at the input resolution (window side
+// st(S-1)+3 at pitch st*S; reading R22) -- the gather geometry of CONV1_DYN.
+void set_windows(ConvArgs &a, int S, int st, int Hi, int Wi) {
+    a.H = Hi;
+    a.W = Wi;
+    a.S_in = S * st;
+    a.hs = st * (S - 1) + 3;
+    a.fd_hs = FastDiv((uint32_t)a.hs);
+    a.fd_hs2 = FastDiv((uint32_t)(a.hs * a.hs));
 }
 
 // Workspace of lasnet_block_forward: zero-contract control words first, then
@@ -679,12 +728,130 @@ lasnet_status lasnet_dense_block(const lasnet_block_desc *d, const lasnet_block_
 
 }  // extern "C"
 
+namespace {
+
+// ---- dynamic projection (first) block of a stage (NEXT-f1, reading R22) ----
+// Workspace: masker+compaction control words (zero contract) first, then the mask
+// (when the caller passes none), the gathered conv1 windows, h2 (unfused steps 4-5)
+// and the subsampled input x_s (stride 2).
+struct ProjWs {
+    void *sync, *mask, *h1g, *h2, *xs;
+};
+size_t proj_dyn_ws(const lasnet_block_desc *d, uint8_t *base, ProjWs *o) {
+    const long ncells = (long)d->n * ((d->h + d->s - 1) / d->s) * ((d->w + d->s - 1) / d->s);
+    const size_t e = elt_size(d->dtype);
+    const int hs = d->stride * (d->s - 1) + 3;
+    Carve cv{base};
+    ProjWs r{};
+    r.sync = cv.take(mask_compact_workspace_bytes(ncells));
+    r.mask = cv.take((size_t)ncells);
+    r.h1g = cv.take((size_t)ncells * hs * hs * d->c_mid * e);
+    r.h2 = use_fused23(d) ? nullptr : cv.take((size_t)ncells * d->s * d->s * d->c_mid * e);
+    r.xs = d->stride > 1 ? cv.take((size_t)d->n * d->h * d->w * d->c_in * e) : nullptr;
+    if (o) *o = r;
+    return cv.used;
+}
+
+// a projection-shaped block (the caller may still pass identity weights when c_in == c_out, stride 1)
+bool proj_shape(const lasnet_block_desc *d) { return d->stride != 1 || d->c_in != d->c_out; }
+
+lasnet_status proj_dyn_forward(const lasnet_block_desc *d, const lasnet_block_weights *w, const void *x, void *y,
+                               const float *wm, float bm, int32_t schedule, uint8_t *mask, int32_t *idx,
+                               int32_t *count, void *ws, size_t ws_bytes, cudaStream_t st) {
+    if (!w->w1 || !w->b1 || !w->w2 || !w->b2 || !w->w3 || !w->b3 || !w->wd || !w->bd) return LASNET_ERR_NULL;
+    if (!x || !y || !wm || !idx || !count) return LASNET_ERR_NULL;
+    if (schedule != LASNET_SCHED_MASKER_SEPARATE) return LASNET_ERR_UNSUPPORTED;  // masker fused into conv1: identity only
+    if (d->dtype != LASNET_BF16) return LASNET_ERR_UNSUPPORTED;
+    if (d->c_in % 64 || d->c_mid % 64 || d->c_out % 128 || d->c_out > 2048 || d->c_mid > 2048)
+        return LASNET_ERR_UNSUPPORTED;
+    if (d->c_mid != 64 && d->c_mid % 128) return LASNET_ERR_UNSUPPORTED;
+    if (d->s > 11 || !masker_channels_ok(d->c_in, 8)) return LASNET_ERR_UNSUPPORTED;
+    if (misaligned(x) || misaligned(y)) return LASNET_ERR_UNSUPPORTED;
+    const int st_ = d->stride, Hi = d->h * st_, Wi = d->w * st_;
+    const long pi = (long)d->n * Hi * Wi, po = (long)d->n * d->h * d->w;
+    if (pi * d->c_in > 0x7fffffffL || po * d->c_out > 0x7fffffffL) return LASNET_ERR_UNSUPPORTED;
+    {
+        const uint8_t *a = static_cast<const uint8_t *>(x), *b = static_cast<const uint8_t *>(y);
+        const size_t xb = (size_t)pi * d->c_in * 2, yb = (size_t)po * d->c_out * 2;
+        if (a < b + yb && b < a + xb) return LASNET_ERR_ALIAS;  // shapes differ: no in-place form
+    }
+    if (!ws || ws_bytes < proj_dyn_ws(d, nullptr, nullptr)) return LASNET_ERR_WORKSPACE;
+    g_last_launches = 0;
+    if (d->n == 0) return cudaMemsetAsync(count, 0, sizeof(int32_t), st) == cudaSuccess ? LASNET_OK : LASNET_ERR_CUDA;
+    ProjWs r;
+    proj_dyn_ws(d, static_cast<uint8_t *>(ws), &r);
+    uint8_t *m = mask ? mask : static_cast<uint8_t *>(r.mask);
+    const int ncells = d->n * ((d->h + d->s - 1) / d->s) * ((d->w + d->s - 1) / d->s);
+    int launches = 0;
+    // step 1+2: the masker pools each output cell's st*S x st*S input window (reading R22): the
+    // input-resolution masker at granularity st*S has exactly the output grid
+    {
+        KernelEvents ev(st, "mask_compact");
+        if (launch_mask_compact(1, x, wm, bm, d->n, Hi, Wi, d->c_in, d->s * st_, m, nullptr, idx, count, r.sync,
+                                st) != cudaSuccess)
+            return LASNET_ERR_CUDA;
+        ++launches;
+    }
+    // the dense projection shortcut R = Wd x_s + bd (the downsampling shortcut stays dense):
+    // ReLU(R) on inactive pixels (final), R on active ones (the residual of the scatter-add)
+    const void *xs = x;
+    if (st_ > 1) {
+        KernelEvents ev(st, "subsample");
+        if (launch_subsample(x, r.xs, d->n, d->h, d->w, d->c_in * 2, st_, num_sms(), st) != cudaSuccess)
+            return LASNET_ERR_CUDA;
+        xs = r.xs;
+        ++launches;
+    }
+    {
+        ConvArgs c = base_args(d);
+        c.m_dense = (int)po;
+        c.a_src = xs; c.w = w->wd; c.bias = w->bd; c.out = y; c.resid = nullptr;
+        c.K = d->c_in; c.N = d->c_out; c.a_ld = d->c_in; c.out_ld = d->c_out;
+        c.relu_mask = m;
+        bool ok = tmap2(&c.tmap_b, w->wd, d->c_in, d->c_out, 64, bn_of(d->c_out, CONV3_DENSE)) &&
+                  tmap2(&c.tmap_a, xs, d->c_in, (uint64_t)po, 64, 128);
+        if (!ok) return LASNET_ERR_CUDA;
+        KernelEvents ev(st, "shortcut");
+        if (launch_conv_tc(CONV3_DENSE, c, (int)((po + 127) / 128), num_sms(), st) != cudaSuccess)
+            return LASNET_ERR_CUDA;
+        ++launches;
+    }
+    // step 3: gather + conv1 over each active cell's input window (side st(S-1)+3)
+    ConvArgs a = base_args(d);
+    set_windows(a, d->s, st_, Hi, Wi);
+    a.idx = idx;
+    a.count = count;
+    a.a_src = x; a.w = w->w1; a.bias = w->b1; a.out = r.h1g; a.resid = nullptr;
+    a.K = d->c_in; a.N = d->c_mid; a.a_ld = d->c_in; a.out_ld = d->c_mid;
+    if (run_conv(d, CONV1_DYN, a, ncells * a.hs * a.hs, x, y, r.h1g, r.h2, ncells, st) != cudaSuccess)
+        return LASNET_ERR_CUDA;
+    ++launches;
+    // steps 4-5: the stride-st 3x3 over the windows, conv3 + scatter-add onto R (in y, in place)
+    ConvArgs b = base_args(d);
+    b.hs = a.hs;
+    b.S_in = a.S_in;
+    b.fd_hs = a.fd_hs;
+    b.fd_hs2 = a.fd_hs2;
+    b.conv_stride = st_;
+    b.idx = idx;
+    b.count = count;
+    int k = 0;
+    if (run_steps45(d, w, b, y, y, r.h1g, r.h2, ncells, st, &k) != cudaSuccess) return LASNET_ERR_CUDA;
+    g_last_launches = launches + k;
+    return LASNET_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 size_t lasnet_block_forward_workspace_bytes(const lasnet_block_desc *d, int32_t schedule) {
     if (check_desc(d) != LASNET_OK) return 0;
     if (schedule != LASNET_SCHED_MASKER_SEPARATE && schedule != LASNET_SCHED_MASKER_FUSED) return 0;
-    return fwd_ws(d, schedule, nullptr, nullptr);
+    const size_t pw = schedule == LASNET_SCHED_MASKER_SEPARATE ? proj_dyn_ws(d, nullptr, nullptr) : 0;
+    if (proj_shape(d)) return pw;
+    const size_t iw = fwd_ws(d, schedule, nullptr, nullptr);
+    return iw > pw ? iw : pw;
 }
 
 lasnet_status lasnet_block_forward(const lasnet_block_desc *d, const lasnet_block_weights *w, const void *x, void *y,
@@ -693,6 +860,9 @@ lasnet_status lasnet_block_forward(const lasnet_block_desc *d, const lasnet_bloc
     lasnet_status s = check_desc(d);
     if (s != LASNET_OK) return s;
     if (schedule != LASNET_SCHED_MASKER_SEPARATE && schedule != LASNET_SCHED_MASKER_FUSED) return LASNET_ERR_DOMAIN;
+    if (w && (w->wd || w->bd))  // a stage's first block: projection shortcut, stride 1 or 2
+        return proj_dyn_forward(d, w, x, y, wm, bm, schedule, mask, idx, count, ws, ws_bytes,
+                                reinterpret_cast<cudaStream_t>(stream));
     if ((s = check_weights(w)) != LASNET_OK) return s;
     if (!x || !y || !wm || !idx || !count) return LASNET_ERR_NULL;
     if ((s = check_channels(d)) != LASNET_OK) return s;
@@ -832,6 +1002,7 @@ lasnet_status lasnet_head(int32_t n, int32_t hw, int32_t c, int32_t classes, con
     if (!x || !w || !b || !logits) return LASNET_ERR_NULL;
     if (n < 0 || hw <= 0 || c <= 0 || classes <= 0) return LASNET_ERR_SHAPE;
     if (n > 0 && (!ws || ws_bytes < lasnet_head_workspace_bytes(n, c))) return LASNET_ERR_WORKSPACE;
+    if (c % 8 || misaligned(x)) return LASNET_ERR_UNSUPPORTED;  // 16-B channel vectors
     g_last_launches = 0;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     KernelEvents ev(st, "head");
@@ -857,7 +1028,6 @@ lasnet_status lasnet_proj_block(const lasnet_block_desc *d, const lasnet_block_w
     if (d->c_in % 64 || d->c_mid % 64 || d->c_out % 128 || d->c_out > 2048 || d->c_mid > 2048)
         return LASNET_ERR_UNSUPPORTED;
     if (d->c_mid != 64 && d->c_mid % 128) return LASNET_ERR_UNSUPPORTED;
-    if (d->w * d->stride > 128) return LASNET_ERR_UNSUPPORTED;  // TMA box of one input image row
     if (misaligned(x) || misaligned(y)) return LASNET_ERR_UNSUPPORTED;
     const size_t e = elt_size(d->dtype);
     const long pi = (long)d->n * d->h * d->w * d->stride * d->stride;
@@ -898,21 +1068,18 @@ lasnet_status lasnet_proj_block(const lasnet_block_desc *d, const lasnet_block_w
         // parity views of h1 ([c_mid/64][n][Hi][Wi][64] with doubled pixel and row strides)
         a.out = h2;
         a.conv_stride = 2;
+        // the tile geometry of the stride-2 3x3 is the OUTPUT's (dense2_tile reads H)
+        a.H = d->h;
+        a.W = d->w;
         const uint64_t Wi = di.w, Hi = di.h;
         bool ok = true;
         for (int v = 0; v < 4 && ok; ++v) {
             const int py = v >> 1, px = v & 1;
             const uint64_t dims[5] = {64, (uint64_t)d->w, (uint64_t)d->h, (uint64_t)d->n, (uint64_t)(d->c_mid / 64)};
             const uint64_t str[4] = {2 * 128, 2 * Wi * 128, Hi * Wi * 128, (uint64_t)d->n * Hi * Wi * 128};
-            const uint32_t box[5] = {64, (uint32_t)d->w, 1, 1, 1};  // rows/imgs set below from the tile geometry
-            uint32_t bx[5];
-            for (int i = 0; i < 5; ++i) bx[i] = box[i];
-            if (d->h * d->w <= 128) {
-                bx[2] = d->h;
-                bx[3] = 128 / (d->h * d->w);
-            } else {
-                bx[2] = 128 / d->w;
-            }
+            ConvArgs geo;
+            dense_tiling(geo, d->n, d->h, d->w);  // the tile geometry prepare_tc sets for this conv
+            const uint32_t bx[5] = {64, (uint32_t)geo.cols_w, (uint32_t)geo.rows_h, (uint32_t)geo.imgs_box, 1};
             ok = tmap_strided(&a.tmap_s[v], static_cast<const uint8_t *>(h1) + ((uint64_t)py * Wi + px) * 128, 5, dims,
                               str, bx);
         }

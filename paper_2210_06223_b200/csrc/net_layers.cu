@@ -81,52 +81,87 @@ cudaError_t launch_maxpool(const void *x, void *y, int n_img, int Ho, int Wo, in
 }
 
 // Head, pass 1: global average pool [n][hw][c] bf16 -> pooled [n][c] fp32
-// (fixed-order fp32 sum over the hw pixels, then / hw).
+// (fixed-order fp32 sum over the hw pixels, then / hw); a thread owns 8
+// consecutive channels (16-B loads, coalesced along the channels).
 __global__ void __launch_bounds__(256) avgpool_kernel(const __nv_bfloat16 *__restrict__ x, float *__restrict__ pooled,
                                                       int n_img, int hw, int c) {
     pdl_wait();
     pdl_trigger();
-    const long total = (long)n_img * c;
+    const int cv = c / 8;
+    const long total = (long)n_img * cv;
     for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
-        const int ch = (int)(i % c);
-        const long n = i / c;
-        float s = 0.f;
-        for (int p = 0; p < hw; ++p) s += __bfloat162float(x[(n * hw + p) * c + ch]);
-        pooled[i] = s / (float)hw;
+        const int v = (int)(i % cv);
+        const long n = i / cv;
+        float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const uint4 *src = reinterpret_cast<const uint4 *>(x + n * hw * c) + v;
+        for (int p = 0; p < hw; ++p) {
+            const uint4 q = __ldg(src + (long)p * cv);
+            const uint32_t u[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                s[2 * e] += __uint_as_float(u[e] << 16);
+                s[2 * e + 1] += __uint_as_float(u[e] & 0xffff0000u);
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) pooled[n * c + 8 * v + e] = s[e] / (float)hw;
     }
 }
 
-// Head, pass 2: logits[n][k] = b[k] + sum_c pooled[n][c] w[k][c]; one warp per
-// (image, class), lanes stride the channels, fixed-order shuffle reduction.
+// Head, pass 2: logits[n][k] = b[k] + sum_c pooled[n][c] w[k][c], a tiled SIMT
+// GEMM: one CTA per 32 images x 32 classes, K staged through shared memory in
+// chunks of 64 channels, each thread 2 x 2 outputs with a fixed-order fp32 sum
+// (the classifier is 2*256*2048*1000 = 1 GFLOP; per-(image, class) warps re-read
+// every weight row once per image).
+constexpr int kFcT = 32, kFcK = 64;
 __global__ void __launch_bounds__(256) fc_kernel(const float *__restrict__ pooled, const __nv_bfloat16 *__restrict__ w,
                                                  const float *__restrict__ b, float *__restrict__ logits, int n_img,
                                                  int c, int classes) {
     pdl_wait();
     pdl_trigger();
-    const int lane = threadIdx.x & 31;
-    const long warps = (long)gridDim.x * (blockDim.x >> 5);
-    for (long t = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < (long)n_img * classes; t += warps) {
-        const int k = (int)(t % classes);
-        const long n = t / classes;
-        float s = 0.f;
-        for (int ch = lane; ch < c; ch += 32) s = fmaf(pooled[n * c + ch], __bfloat162float(w[(long)k * c + ch]), s);
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        if (lane == 0) logits[t] = s + b[k];
+    __shared__ float sa[kFcT][kFcK + 1], sb[kFcT][kFcK + 1];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int k0 = blockIdx.x * kFcT, n0 = blockIdx.y * kFcT;
+    float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+    for (int c0 = 0; c0 < c; c0 += kFcK) {
+        for (int e = threadIdx.x; e < kFcT * kFcK; e += 256) {
+            const int r = e / kFcK, cc = e % kFcK;
+            const int n = n0 + r, k = k0 + r, ch = c0 + cc;
+            sa[r][cc] = (n < n_img && ch < c) ? pooled[(long)n * c + ch] : 0.f;
+            sb[r][cc] = (k < classes && ch < c) ? __bfloat162float(w[(long)k * c + ch]) : 0.f;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int cc = 0; cc < kFcK; ++cc) {
+            const float a0 = sa[ty][cc], a1 = sa[ty + 16][cc];
+            const float b0 = sb[tx][cc], b1 = sb[tx + 16][cc];
+            acc[0][0] = fmaf(a0, b0, acc[0][0]);
+            acc[0][1] = fmaf(a0, b1, acc[0][1]);
+            acc[1][0] = fmaf(a1, b0, acc[1][0]);
+            acc[1][1] = fmaf(a1, b1, acc[1][1]);
+        }
+        __syncthreads();
     }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int n = n0 + ty + 16 * i, k = k0 + tx + 16 * j;
+            if (n < n_img && k < classes) logits[(long)n * classes + k] = acc[i][j] + b[k];
+        }
 }
 
 cudaError_t launch_head(const void *x, const void *w, const float *b, float *pooled, float *logits, int n_img, int hw,
                         int c, int classes, int num_sms, cudaStream_t st) {
     if (n_img == 0) return cudaSuccess;
-    long g1 = ((long)n_img * c + 255) / 256;
+    if (c % 8) return cudaErrorInvalidValue;
+    long g1 = ((long)n_img * (c / 8) + 255) / 256;
     if (g1 > 8L * num_sms) g1 = 8L * num_sms;
     cudaError_t e = launch_k(avgpool_kernel, dim3((unsigned)g1), dim3(256), 0, st,
                              static_cast<const __nv_bfloat16 *>(x), pooled, n_img, hw, c);
     if (e != cudaSuccess) return e;
-    long g2 = ((long)n_img * classes + 7) / 8;
-    if (g2 > 16L * num_sms) g2 = 16L * num_sms;
-    return launch_k(fc_kernel, dim3((unsigned)g2), dim3(256), 0, st, static_cast<const float *>(pooled),
+    const dim3 g2((unsigned)((classes + kFcT - 1) / kFcT), (unsigned)((n_img + kFcT - 1) / kFcT));
+    return launch_k(fc_kernel, g2, dim3(256), 0, st, static_cast<const float *>(pooled),
                     static_cast<const __nv_bfloat16 *>(w), b, logits, n_img, c, classes);
 }
 

@@ -64,7 +64,15 @@ struct ConvArgs {
     int32_t a_ld;           // elements per A source row (c_in for conv1, c_mid otherwise)
     int32_t out_ld;         // elements per output row
     int32_t n_img, H, W, S, Gh, Gw;
-    FastDiv fd_G, fd_Gw, fd_hs, fd_hs2, fd_S, fd_SS;  // G = Gh*Gw, hs = S+2, SS = S*S
+    // conv1 windows (gather modes): cell pitch at the block INPUT resolution (S_in = stride * S)
+    // and window side (hs = stride * (S - 1) + 3: S + 2 for stride 1, 2S + 1 for stride 2);
+    // H, W are the input dims for conv1 and the output dims for conv2 / conv3
+    int32_t S_in, hs;
+    FastDiv fd_G, fd_Gw, fd_hs, fd_hs2, fd_S, fd_SS;  // G = Gh*Gw, hs (window side), SS = S*S
+    FastDiv fd_HW, fd_W;                             // dense rows -> (image, y, x) (relu_mask)
+    // dense epilogue: ReLU only on pixels of INACTIVE cells of this mask [n][Gh][Gw] (the dynamic
+    // projection block's shortcut R: inactive pixels store ReLU(R), active ones R for the scatter-add)
+    const uint8_t *relu_mask;
     // tcgen05 tile geometry (host-computed)
     int32_t units_per_tile;   // dynamic: TMA boxes (conv1) / patches (conv2, conv3) per 128-row tile
     int32_t units_per_patch;  // conv1: 1 (whole halo box) or S+2 (one box per halo row)
@@ -72,6 +80,7 @@ struct ConvArgs {
     int32_t unit_halo_rows;   // conv1: halo rows per box
     int32_t box_rows;         // rows one A box delivers (conv2 dyn/dense, conv3 dyn)
     int32_t rows_h, imgs_box; // conv2 dense: image rows / images per box
+    int32_t cols_w, tiles_x;  // conv2 dense: image columns per box, column blocks per row band (W > 128)
     int32_t dense_tiles;      // conv2 dense: M tiles
     int32_t cluster;          // fused conv2+conv3: CTAs per cluster sharing (multicasting) the weight loads
     int32_t conv_stride;      // dense 3x3: 2 = stride 2 through the four parity views tmap_s[(row odd) * 2 + (col odd)]
@@ -88,14 +97,29 @@ struct ConvArgs {
     float4 *mpart;            // [n*h*w] (partial, magnitude) of the lower and of the upper channel halves
 };
 
-__host__ __device__ __forceinline__ int rows_per_patch(int mode, int S) {
-    return mode == CONV1_DYN ? (S + 2) * (S + 2) : S * S;
-}
-
 // Total GEMM rows; dynamic modes read the device-resident active count.
 __device__ __forceinline__ int gemm_rows(int mode, const ConvArgs &a) {
-    if (mode <= CONV3_DYN) return (*a.count) * rows_per_patch(mode, a.S);
+    if (mode <= CONV3_DYN) return (*a.count) * (mode == CONV1_DYN ? a.hs * a.hs : a.S * a.S);
     return a.m_dense;
+}
+
+// Dense 3x3 tile mt -> (first image, first row, first column) of its box: a box
+// covers imgs_box whole images (h*w <= 128), or rows_h rows x cols_w columns of one
+// image (tiles_x column blocks per row band when w > 128).
+__device__ __forceinline__ void dense_tile_origin(const ConvArgs &a, int mt, int &n0, int &y0, int &x0) {
+    if (a.rows_h < a.H || a.tiles_x > 1) {
+        const int bands = (a.H + a.rows_h - 1) / a.rows_h;
+        const int tpi = bands * a.tiles_x;
+        n0 = mt / tpi;
+        const int rem = mt - n0 * tpi;
+        const int band = rem / a.tiles_x;
+        y0 = band * a.rows_h;
+        x0 = (rem - band * a.tiles_x) * a.cols_w;
+    } else {
+        n0 = mt * a.imgs_box;
+        y0 = 0;
+        x0 = 0;
+    }
 }
 
 // Active cell t -> (image n, cell row gy, cell col gx).
@@ -113,12 +137,12 @@ __device__ __forceinline__ void cell_coords(const ConvArgs &a, int t, int &n, in
 // the image / a row past the end (zero row; the epilogue also writes 0, R6).
 __device__ __forceinline__ int halo_pixel(const ConvArgs &a, int r, int M) {
     if (r >= M) return -1;
-    const int hs = a.S + 2, hs2 = hs * hs;
+    const int hs = a.hs, hs2 = hs * hs;
     const int t = a.fd_hs2.div(r), j = r - t * hs2;
     int n, gy, gx;
     cell_coords(a, t, n, gy, gx);
     const int jy = a.fd_hs.div(j);
-    const int hy = gy * a.S - 1 + jy, hx = gx * a.S - 1 + (j - jy * hs);
+    const int hy = gy * a.S_in - 1 + jy, hx = gx * a.S_in - 1 + (j - jy * hs);
     if (hy < 0 || hy >= a.H || hx < 0 || hx >= a.W) return -1;
     return (n * a.H + hy) * a.W + hx;
 }
@@ -126,7 +150,7 @@ __device__ __forceinline__ int halo_pixel(const ConvArgs &a, int r, int M) {
 // conv2 (dynamic): GEMM row -> h1 row of the window centre of output pixel j of patch t.
 __device__ __forceinline__ int conv2_center_row(const ConvArgs &a, int r, int M) {
     if (r >= M) return -1;
-    const int ss = a.S * a.S, hs = a.S + 2;
+    const int ss = a.S * a.S, hs = a.hs;
     const int t = a.fd_SS.div(r), j = r - t * ss;
     const int py = a.fd_S.div(j), px = j - py * a.S;
     return t * hs * hs + (py + 1) * hs + (px + 1);

@@ -20,7 +20,7 @@ import ctypes
 import torch
 
 from . import _lib
-from .block import BlockShape, DynBlock, _p, _stream, choose_schedule
+from .block import BlockShape, DynBlock, ProjDynBlock, _p, _stream, choose_schedule
 
 R101_DEPTHS = (3, 4, 23, 3)
 R50_DEPTHS = (3, 4, 6, 3)
@@ -49,33 +49,45 @@ class ProjBlock:
 
 
 class LASResNet:
-    """LAS-ResNet forward on a batch of n images of hw x hw (3 channels zero-padded
-    to 8, given as the stem's padded layout [n][hw][hw + 8][8])."""
+    """LAS-ResNet forward on a batch of n images of H x W (hw: an int for square
+    ImageNet input, or (H, W), e.g. the COCO backbone's 800 x 1344; 3 channels
+    zero-padded to 8, given as the stem's padded layout [n][H][W + 8][8]).
+    backbone=True stops after the last stage (detection-shaped feature maps,
+    BASELINE configs[4]): forward returns the four stage outputs."""
 
-    def __init__(self, n: int, weights: dict, hw: int = 224, depths=R101_DEPTHS, s_net=S_NET, r: float = 0.5,
-                 device="cuda"):
-        self.n, self.hw, self.device = n, hw, device
+    def __init__(self, n: int, weights: dict, hw=224, depths=R101_DEPTHS, s_net=S_NET, r: float = 0.5,
+                 device="cuda", dynamic_proj: bool = True, backbone: bool = False):
+        H, W = (hw, hw) if isinstance(hw, int) else tuple(hw)
+        if H % 32 or W % 32:
+            raise ValueError("input height and width must be multiples of 32")
+        self.n, self.hw, self.H, self.W, self.device = n, hw, H, W, device
+        self.backbone = backbone
         self.depths, self.s_net = tuple(depths), tuple(s_net)
         lib = _lib.load()
         self.stem_w = weights["stem_w"].to(device).contiguous()
         self.stem_b = weights["stem_b"].to(device).contiguous()
         self.stem_ws = torch.empty(lib.lasnet_stem_workspace_bytes(), dtype=torch.uint8, device=device)
-        h = hw // 2
-        self.stem_y = torch.empty((n, h, h, 64), dtype=torch.bfloat16, device=device)
-        h //= 2
-        self.pool_y = torch.empty((n, h, h, 64), dtype=torch.bfloat16, device=device)
+        h, w = H // 2, W // 2
+        self.stem_y = torch.empty((n, h, w, 64), dtype=torch.bfloat16, device=device)
+        h, w = h // 2, w // 2
+        self.pool_y = torch.empty((n, h, w, 64), dtype=torch.bfloat16, device=device)
         self.stages = []
+        self.static_proj = []
         c_in = 64
         for si, (depth, width, s) in enumerate(zip(depths, WIDTHS, s_net)):
             stride = 1 if si == 0 else 2
             c_out = 4 * width
-            proj = ProjBlock(n, h, h, c_in, width, c_out, stride, weights[f"s{si}_proj"], device)
-            h //= stride
+            pw = weights[f"s{si}_proj"]
+            static = ProjBlock(n, h, w, c_in, width, c_out, stride, pw, device)  # the dense comparator's
+            proj = (ProjDynBlock(n, h, w, c_in, width, c_out, stride, s, pw, pw["wm"], 0.0, device)
+                    if dynamic_proj else static)
+            self.static_proj.append(static)
+            h, w = h // stride, w // stride
             dyn = []
             for b in range(1, depth):
                 wb = weights[f"s{si}_b{b}"]
-                sched = choose_schedule(n, h, h, c_out, width, c_out, s, r)
-                dyn.append(DynBlock(BlockShape(n, h, h, c_out, width, s), {k: wb[k] for k in
+                sched = choose_schedule(n, h, w, c_out, width, c_out, s, r)
+                dyn.append(DynBlock(BlockShape(n, h, w, c_out, width, s), {k: wb[k] for k in
                                                                            ("w1", "b1", "w2", "b2", "w3", "b3")},
                                     wb["wm"], 0.0, device=device, schedule=sched))
             self.stages.append((proj, dyn))
@@ -85,7 +97,8 @@ class LASResNet:
         self.head_ws = torch.empty(max(lib.lasnet_head_workspace_bytes(n, c_in), 1), dtype=torch.uint8,
                                    device=device)
         self.logits = torch.empty((n, self.fc_w.shape[0]), dtype=torch.float32, device=device)
-        self.c_last, self.h_last = c_in, h
+        self.c_last, self.h_last, self.w_last = c_in, h, w
+        self.features = [None] * len(self.stages)
 
     def oracle_meta(self) -> dict:
         """Depths, S_net and every dynamic block's masker bias, keyed like the weight
@@ -93,12 +106,18 @@ class LASResNet:
         decisions (test / bench bookkeeping; no arithmetic)."""
         bm = {}
         for si, (proj, dyn) in enumerate(self.stages):
+            if getattr(proj, "dynamic", False):
+                bm[f"s{si}_proj"] = float(proj.bm)
             for bi, blk in enumerate(dyn):
                 bm[f"s{si}_b{bi + 1}"] = float(blk.bm)
-        return {"depths": self.depths, "s_net": self.s_net, "bm": bm}
+        return {"depths": self.depths, "s_net": self.s_net, "bm": bm,
+                "dyn_proj": all(getattr(p, "dynamic", False) for p, _ in self.stages)}
 
     def blocks(self):
+        """Every dynamic block in forward order (the dynamic first blocks included)."""
         for proj, dyn in self.stages:
+            if getattr(proj, "dynamic", False):
+                yield proj
             yield from dyn
 
     def forward(self, x_pad: torch.Tensor, calibrate_r: float | None = None, dense: bool = False,
@@ -111,7 +130,7 @@ class LASResNet:
         block object, and the range [ev0, ev1) of kernel event pairs the call
         recorded when lasnet_set_kernel_events is armed) -- bench bookkeeping."""
         lib = _lib.load()
-        n, h = self.n, self.hw // 2
+        n, h, w = self.n, self.H // 2, self.W // 2
         self.launches = 0
 
         def mark(kind, obj=None, **kw):
@@ -119,14 +138,18 @@ class LASResNet:
                 trace.append(dict(kind=kind, obj=obj, ev1=int(lib.lasnet_kernel_event_count()), **kw))
             self.launches += int(lib.lasnet_last_launch_count())
 
-        _lib.check("lasnet_stem", lib.lasnet_stem(n, h, h, _p(x_pad), _p(self.stem_w), _p(self.stem_b),
+        _lib.check("lasnet_stem", lib.lasnet_stem(n, h, w, _p(x_pad), _p(self.stem_w), _p(self.stem_b),
                                                   _p(self.stem_y), _p(self.stem_ws), self.stem_ws.numel(), _stream()))
-        mark("stem", None, n=n, h=h, w=h)
-        _lib.check("lasnet_maxpool", lib.lasnet_maxpool(n, h // 2, h // 2, 64, _p(self.stem_y), _p(self.pool_y),
+        mark("stem", None, n=n, h=h, w=w)
+        _lib.check("lasnet_maxpool", lib.lasnet_maxpool(n, h // 2, w // 2, 64, _p(self.stem_y), _p(self.pool_y),
                                                         _stream()))
-        mark("maxpool", None, n=n, h=h // 2, w=h // 2, c=64)
+        mark("maxpool", None, n=n, h=h // 2, w=w // 2, c=64)
         x = self.pool_y
         for si, (proj, dyn) in enumerate(self.stages):
+            if dense:
+                proj = self.static_proj[si]
+            elif calibrate_r is not None and getattr(proj, "dynamic", False):
+                proj.calibrate_bias(x, calibrate_r)
             y = proj.forward(x)
             mark("proj", proj, stage=si)
             other = self._scratch(si, y) if dense else None
@@ -139,15 +162,17 @@ class LASResNet:
                 else:
                     blk.forward(y)  # in place: inactive pixels are never touched
                 mark("dense" if dense else "dyn", blk, stage=si, block=bi + 1)
+            self.features[si] = y
             x = y
-        _lib.check("lasnet_head", lib.lasnet_head(n, self.h_last * self.h_last, self.c_last, self.fc_w.shape[0],
-                                                  _p(x), _p(self.fc_w), _p(self.fc_b), _p(self.logits),
-                                                  _p(self.head_ws), self.head_ws.numel(), _stream()))
-        mark("head", None, n=n, hw=self.h_last * self.h_last, c=self.c_last, classes=self.fc_w.shape[0])
+        if not self.backbone:
+            _lib.check("lasnet_head", lib.lasnet_head(n, self.h_last * self.w_last, self.c_last, self.fc_w.shape[0],
+                                                      _p(x), _p(self.fc_w), _p(self.fc_b), _p(self.logits),
+                                                      _p(self.head_ws), self.head_ws.numel(), _stream()))
+            mark("head", None, n=n, hw=self.h_last * self.w_last, c=self.c_last, classes=self.fc_w.shape[0])
         if trace is not None:  # ev0 of each call = ev1 of the previous one
             for i, t in enumerate(trace):
                 t["ev0"] = trace[i - 1]["ev1"] if i else 0
-        return self.logits
+        return list(self.features) if self.backbone else self.logits
 
     def stream_host(self, x_hosts, logits_hosts, x_devs, graphs, steps: int):
         """End-to-end serving loop with HOST buffers (e2e of bench.py): step i copies

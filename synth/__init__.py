@@ -83,6 +83,8 @@ def make_lasnet_weights(depths=(3, 4, 23, 3), widths=(64, 128, 256, 512), classe
     for si, (depth, width) in enumerate(zip(depths, widths)):
         c_out = 4 * width
         w[f"s{si}_proj"] = make_proj_weights(c_in, width, c_out, seed=seed * 1000 + 100 * si, dtype=dtype)
+        # masker of the (dynamic) first block: it pools the block INPUT (c_in channels)
+        w[f"s{si}_proj"]["wm"] = make_masker_weights(c_in, seed=seed * 1000 + 100 * si + 99)
         for b in range(1, depth):
             wb = make_block_weights(c_out, width, c_out, seed=seed * 1000 + 100 * si + 2 * b, dtype=dtype)
             wb["wm"] = make_masker_weights(c_out, seed=seed * 1000 + 100 * si + 2 * b + 1)
@@ -93,11 +95,13 @@ def make_lasnet_weights(depths=(3, 4, 23, 3), widths=(64, 128, 256, 512), classe
     return w
 
 
-def make_image_batch(n: int, hw: int = 224, seed: int = 0, dtype: str = "bf16") -> torch.Tensor:
-    """ImageNet-normalised-like input N(0,1) with 3 channels, in the stem's padded
-    layout [n][hw][hw + 8][8] (channels 3..7 and 4 pixels left/right zero)."""
-    x = torch.zeros((n, hw, hw + 8, 8), dtype=torch.float32)
-    x[:, :, 4:4 + hw, :3] = torch.randn((n, hw, hw, 3), generator=_gen(seed))
+def make_image_batch(n: int, hw=224, seed: int = 0, dtype: str = "bf16") -> torch.Tensor:
+    """ImageNet/COCO-normalised-like input N(0,1) with 3 channels, in the stem's
+    padded layout [n][H][W + 8][8] (channels 3..7 and 4 pixels left/right zero);
+    hw is H = W or (H, W)."""
+    H, W = (hw, hw) if isinstance(hw, int) else tuple(hw)
+    x = torch.zeros((n, H, W + 8, 8), dtype=torch.float32)
+    x[:, :, 4:4 + W, :3] = torch.randn((n, H, W, 3), generator=_gen(seed))
     return x.to(_dt(dtype)).contiguous()
 
 

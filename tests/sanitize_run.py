@@ -31,6 +31,14 @@ def main():
         for sched in (L.SCHED_SEPARATE, L.SCHED_FUSED):
             L.block_forward(x.clone(), wts, wm, 0.0, s, sched)
         L.dense_block(x, wts)
+    # fp32 CUDA-core path (config 1)
+    x = synth.make_x(1, 14, 14, 256, seed=8, dtype="f32").cuda()
+    wts = dev(synth.make_block_weights(256, 64, 256, seed=9, dtype="f32"))
+    wm = synth.make_masker_weights(256, seed=10).cuda()
+    m = L.mask(x, wm, 0.0, 2)
+    idx, cnt = L.compact(m)
+    L.dyn_block(x.clone(), wts, idx, cnt, 2)
+    L.dense_block(x, wts)
     xp = synth.make_x(2, 16, 16, 128, seed=4).cuda()
     L.proj_block(xp, dev(synth.make_proj_weights(128, 64, 256, seed=5)), 2)
     net = L.LASResNet(1, synth.make_lasnet_weights(seed=6), hw=64)
