@@ -73,6 +73,7 @@ def parse():
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work per cpu_baseline")
     ap.add_argument("--no-sweep", action="store_true", help="skip the S x r block sweep")
     ap.add_argument("--no-block", action="store_true", help="skip the block sub-object")
+    ap.add_argument("--no-coco", action="store_true", help="skip the COCO backbone sub-object (configs[4])")
     ap.add_argument("--detail", default=None, help="write per-kernel detail JSON here")
     ap.add_argument("--schedule", default="auto", choices=["auto", "separate", "fused"],
                     help="block sub-object: separate = north-star branch (masker, then gather+conv1 on halos); "
@@ -748,6 +749,55 @@ def block_sweep(args, rank, hbm, tfl):
                       "roofline_frac = SURVEY 8(d) headline T_roof / measured"}
 
 
+# ----------------------------------------------------------- COCO backbone ----
+
+def coco_measure(args, rank):
+    """BASELINE configs[4]: the LAS-ResNet-101 backbone at COCO 800x1333 (padded to
+    800x1344), 8 images per GPU, S_net 4-4-2-1 and 4-4-7-1, r = 0.5,
+    detection-shaped stage outputs (200x336 ... 25x42); one CUDA graph per forward,
+    the dense comparator the same backbone with every block static."""
+    import synth
+    import paper_2210_06223_b200 as L
+
+    n, hw = 8, (800, 1344)
+    weights = synth.make_lasnet_weights(seed=11)
+    x = synth.make_image_batch(n, hw, seed=200 + rank).cuda()
+    xc = synth.make_image_batch(n, hw, seed=6000 + rank).cuda()
+    stream = torch.cuda.current_stream()
+    steps = max(3, min(args.steps, 10))
+    out = {}
+    for s_net in ((4, 4, 2, 1), (4, 4, 7, 1)):
+        net = L.LASResNet(n, weights, hw=hw, s_net=s_net, r=0.5, backbone=True)
+        net.forward(xc, calibrate_r=0.5)
+        res = {}
+        for dense in (False, True):
+            g = net.capture(x, dense=dense)
+            for _ in range(2):
+                g.replay()
+            a, b = ev_pair()
+            torch.cuda.synchronize()
+            a.record(stream)
+            for _ in range(steps):
+                g.replay()
+            b.record(stream)
+            torch.cuda.synchronize()
+            res[dense] = a.elapsed_time(b) / steps
+            del g
+        r_blocks = [int(b.count.item()) / b.ncells for b in net.blocks()]
+        key = "s_net_" + "-".join(map(str, s_net))
+        out[key] = {"ms_per_forward": round(res[False], 4), "images_per_s": round(n / (res[False] * 1e-3), 1),
+                    "ms_per_image": round(res[False] / n, 4), "dense_ms_per_forward": round(res[True], 4),
+                    "speedup_vs_dense": round(res[True] / res[False], 3),
+                    "r_patch_mean": round(statistics.fmean(r_blocks), 4)}
+        del net
+        torch.cuda.empty_cache()
+    out.update({"workload": "LAS-ResNet-101 backbone (BASELINE configs[4]): 8 images/GPU of 800x1344 (1333 padded "
+                            "to a multiple of 32), stage outputs 200x336 / 100x168 / 50x84 / 25x42, r = 0.5",
+                "timing": f"mean of {steps} CUDA-graph replays per forward", "paper_context_ms_per_image": {
+                    "V100 4-4-2-1": 30.7, "V100 4-4-7-1": 25.3, "V100 static": 39.5, "note": "P:400-405, batch 1"}})
+    return out
+
+
 # ---------------------------------------------------------------- lasnet ----
 
 def run_lasnet(args):
@@ -777,6 +827,7 @@ def run_lasnet(args):
     net = network_measure(args, world, rank, local, hbm, tfl)
     blk = None if args.no_block else block_measure(args, world, rank, hbm, tfl)
     sweep = None if args.no_sweep else block_sweep(args, rank, hbm, tfl)
+    coco = None if args.no_coco else coco_measure(args, rank)
     clocks = sampler.stop()
     if blk is not None:
         b_tot = sum(blk["step_ms"])
@@ -863,6 +914,8 @@ def run_lasnet(args):
             line["block"] = block_obj
         if sweep is not None:
             line["block_sweep"] = sweep
+        if coco is not None:
+            line["coco_backbone"] = coco
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_net(net["x_cpu"], net["weights"], net["net"].oracle_meta(),
                                                     args.cpu_budget)

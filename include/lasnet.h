@@ -249,9 +249,52 @@ lasnet_status lasnet_block_forward(const lasnet_block_desc *desc, const lasnet_b
                                    lasnet_stream_t stream);
 size_t lasnet_block_forward_workspace_bytes(const lasnet_block_desc *desc, int32_t schedule);
 /* Host-side schedule choice for an expected activation rate r (the paper's
- * threshold r_th, from a B200 HBM-bytes model): returns the
- * lasnet_schedule that moves fewer bytes.  Pure, launches nothing. */
+ * threshold r_th): the lasnet_schedule the B200 latency predictor
+ * (lasnet_predict_latency, built-in calibration) predicts faster; a stage's
+ * first block (stride 2 or c_in != c_out) always gets MASKER_SEPARATE.  Pure,
+ * launches nothing. */
 int32_t lasnet_choose_schedule(const lasnet_block_desc *desc, double r);
+
+/* Latency predictor G(H, P, S, r) (sec. 3.3 "Latency prediction
+ * model", App. A) re-targeted to B200.  Host-
+ * side, pure: launches nothing.
+ *   H  lasnet_hw: the device as `sms` processing engines behind off-chip (HBM),
+ *      on-chip (L2 -> shared memory) and in-PE (tensor core) levels, a per-launch
+ *      overhead, and per kernel type the achieved fraction of its bound
+ *      (lasnet_hw_b200 fills the built-in B200 calibration)
+ *   P  desc (layer parameters; stride 2 / c_in != c_out = a stage's first block)
+ *   S  desc->s;  r  the activation rate (expected geometry of r*cells uniformly
+ *      active cells, border clipping included)
+ *   schedule  LASNET_SCHED_MASKER_SEPARATE, LASNET_SCHED_MASKER_FUSED, or
+ *      LASNET_SCHED_DENSE (predictor only: the static block, lasnet_dense_block /
+ *      lasnet_proj_block) for the latency ratio r_l = l_dyn / l_stat
+ * The operators are exactly the launches the library makes for that schedule;
+ * each is split into its 128-row GEMM tiles run by a persistent grid of one CTA
+ * per SM: t = launch + t0 + ceil(tiles/sms) * max(HBM, L2, tensor time per tile) / eff.
+ * Returns the predicted latency in microseconds (-1 on invalid arguments or an
+ * unsupported schedule); kinds / kernel_us (nullable, max_kernels entries)
+ * receive the per-launch kernel types and predicted times, n_kernels the count. */
+typedef enum {
+    LASNET_K_MASK_COMPACT = 0, LASNET_K_CONV1_DYN, LASNET_K_CONV1_MASK, LASNET_K_DECIDE, LASNET_K_DECIDE_GATHER,
+    LASNET_K_CONV23, LASNET_K_CONV23_DIRECT, LASNET_K_CONV2_DYN, LASNET_K_CONV3_DYN, LASNET_K_CONV1_DENSE,
+    LASNET_K_CONV2_DENSE, LASNET_K_CONV3_DENSE, LASNET_K_CONV23_DENSE, LASNET_K_SUBSAMPLE, LASNET_K_SHORTCUT,
+    LASNET_K_COUNT
+} lasnet_kernel_type;
+#define LASNET_SCHED_DENSE 2
+typedef struct {
+    int32_t sms;       /* processing engines (SMs)                                  */
+    double hbm_gbs;    /* off-chip memory bandwidth, GB/s                           */
+    double l2_gbs;     /* on-chip (L2 -> shared memory) bandwidth, GB/s, all SMs    */
+    double tc_tflops;  /* dense bf16 tensor throughput, TFLOP/s                     */
+    double launch_us;  /* per-kernel launch / fill / drain, us                      */
+    double eff[LASNET_K_COUNT]; /* achieved fraction of the bound per kernel type   */
+    double t0_us[LASNET_K_COUNT]; /* fixed per-launch cost per kernel type (pipeline
+                                     fill, tails, dependent latency chains), us    */
+} lasnet_hw;
+void lasnet_hw_b200(lasnet_hw *hw);
+const char *lasnet_kernel_type_name(int32_t kind);  /* "conv1_mask", ... (the event names) */
+double lasnet_predict_latency(const lasnet_block_desc *desc, int32_t schedule, double r, const lasnet_hw *hw,
+                              int32_t *kinds, double *kernel_us, int32_t max_kernels, int32_t *n_kernels);
 
 /* Benchmark instrumentation.  The next n_pairs kernels this host thread
  * launches through the ABI are bracketed by cudaEventRecord(events[2i]) and

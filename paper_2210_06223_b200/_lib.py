@@ -26,11 +26,19 @@ EXPORTS = [
     "lasnet_block_forward", "lasnet_block_forward_workspace_bytes", "lasnet_choose_schedule",
     "lasnet_proj_block", "lasnet_proj_workspace_bytes", "lasnet_stem", "lasnet_stem_workspace_bytes",
     "lasnet_maxpool", "lasnet_head", "lasnet_head_workspace_bytes", "lasnet_kernel_event_name",
-    "lasnet_kernel_event_count",
+    "lasnet_kernel_event_count", "lasnet_hw_b200", "lasnet_kernel_type_name", "lasnet_predict_latency",
 ]
 
-# lasnet_schedule
-SCHED_SEPARATE, SCHED_FUSED = 0, 1
+# lasnet_schedule (SCHED_DENSE: predictor only, the static block)
+SCHED_SEPARATE, SCHED_FUSED, SCHED_DENSE = 0, 1, 2
+K_COUNT = 15
+
+
+class HW(ctypes.Structure):
+    """lasnet_hw: the predictor's hardware model."""
+    _fields_ = [("sms", ctypes.c_int32), ("hbm_gbs", ctypes.c_double), ("l2_gbs", ctypes.c_double),
+                ("tc_tflops", ctypes.c_double), ("launch_us", ctypes.c_double), ("eff", ctypes.c_double * K_COUNT),
+                ("t0_us", ctypes.c_double * K_COUNT)]
 
 
 class BlockDesc(ctypes.Structure):
@@ -110,6 +118,13 @@ def load(path: str = LIB_PATH):
     lib.lasnet_kernel_event_name.argtypes = [i32]
     lib.lasnet_kernel_event_name.restype = ctypes.c_char_p
     lib.lasnet_kernel_event_count.restype = i32
+    lib.lasnet_hw_b200.argtypes = [ctypes.POINTER(HW)]
+    lib.lasnet_hw_b200.restype = None
+    lib.lasnet_kernel_type_name.argtypes = [i32]
+    lib.lasnet_kernel_type_name.restype = ctypes.c_char_p
+    lib.lasnet_predict_latency.argtypes = [D, i32, ctypes.c_double, ctypes.POINTER(HW), ctypes.POINTER(i32),
+                                           ctypes.POINTER(ctypes.c_double), i32, ctypes.POINTER(i32)]
+    lib.lasnet_predict_latency.restype = ctypes.c_double
     _lib = lib
     return lib
 

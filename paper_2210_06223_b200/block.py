@@ -224,6 +224,30 @@ def proj_block_forward(x: torch.Tensor, wts: dict, wm: torch.Tensor, bm: float, 
     return y, m, idx, count
 
 
+def predict_latency(n, h, w, c_in, c_mid, c_out, s, r, schedule, stride: int = 1, hw=None):
+    """lasnet_predict_latency (the B200 latency predictor G(H, P, S, r)):
+    (total_us, [(kernel type, us), ...]) of one block call; schedule SCHED_SEPARATE,
+    SCHED_FUSED or SCHED_DENSE (the static block); h, w the output dims.  hw: an
+    _lib.HW (None = the built-in B200 calibration)."""
+    lib = _lib.load()
+    d = _lib.BlockDesc(n, h, w, c_in, c_mid, c_out, stride, s, _lib.LASNET_BF16)
+    kinds = (ctypes.c_int32 * 8)()
+    us = (ctypes.c_double * 8)()
+    nk = ctypes.c_int32(0)
+    t = lib.lasnet_predict_latency(ctypes.byref(d), int(schedule), float(r), ctypes.byref(hw) if hw else None,
+                                   kinds, us, 8, ctypes.byref(nk))
+    if t < 0:
+        raise ValueError("lasnet_predict_latency: invalid arguments or unsupported schedule")
+    return t, [(lib.lasnet_kernel_type_name(kinds[i]).decode(), us[i]) for i in range(nk.value)]
+
+
+def hw_b200():
+    """The predictor's built-in B200 hardware model (an _lib.HW to modify)."""
+    h = _lib.HW()
+    _lib.load().lasnet_hw_b200(ctypes.byref(h))
+    return h
+
+
 def choose_schedule(n, h, w, c_in, c_mid, c_out, s, r, dtype=torch.bfloat16) -> int:
     d = make_desc(n, h, w, c_in, c_mid, c_out, s, dtype)
     return int(_lib.load().lasnet_choose_schedule(ctypes.byref(d), float(r)))

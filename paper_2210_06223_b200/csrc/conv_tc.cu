@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     const uint32_t fb = bar_full + 8 * stage;
                     int a_bytes = kABytes;  // conv1 dyn: A arrives by cp.async (not counted here)
                     if (C::kGather) a_bytes = 0;
-                    else if (MODE == STEM) a_bytes = 4 * (args.W / 4) * 128;
+                    else if (MODE == STEM) a_bytes = args.cols_w * 128;  // 4 boxes of cols_w / 4 columns
                     else if (MODE == CONV2_DYN || MODE == CONV2_DENSE) a_bytes = args.box_rows * 128;
                     mbar_arrive_expect_tx(fb, a_bytes + (C::kBRes ? 0 : C::kBBytes));
                     if (!C::kBRes) tma_load_2d(sb, &args.tmap_b, fb, kb * kBK, n0);
@@ -240,10 +240,13 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     } else if (MODE == STEM) {
                         // K-block kb = kernel row dy: 4 boxes of W/4 output columns each (residue k of
                         // ox mod 4), every box row the 8 input pixels x 8 channels of one output pixel
-                        const int n = mt / args.H, oy = mt - n * args.H;
+                        // tile = (image, output row, column block of cols_w columns)
+                        const int xb = mt % args.tiles_x, row = mt / args.tiles_x;
+                        const int n = row / args.H, oy = row - n * args.H;
+                        const int q = args.cols_w / 4;
 #pragma unroll
                         for (int k = 0; k < 4; ++k)
-                            tma_load_4d(sa + k * (args.W / 4) * 128, &args.tmap_s[k], fb, 0, 0, 2 * oy + kb - 3, n);
+                            tma_load_4d(sa + k * q * 128, &args.tmap_s[k], fb, 0, xb * q, 2 * oy + kb - 3, n);
                     } else if (!C::kGather) {
                         if (args.a2_kb && kb >= args.a2_kb)  // second A source (projection shortcut input)
                             tma_load_2d(sa, &args.tmap_s[0], fb, (kb - args.a2_kb) * kBK, mt * kBM);
@@ -575,9 +578,11 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     for (int c = 0; c < BN / 64; ++c)
                         tma_store_4d(&args.tmap_out, sbuf + c * kChunkBytes, n0 + c * 64, d2x, d2y, d2n);
                 } else if (MODE == STEM) {  // the tile's rows in residue order back to output columns
-                    const int n = mt / args.H, oy = mt - n * args.H;
+                    const int xb = mt % args.tiles_x, row = mt / args.tiles_x;
+                    const int n = row / args.H, oy = row - n * args.H;
+                    const int q = args.cols_w / 4;
                     for (int k = 0; k < 4; ++k)
-                        tma_store_4d(&args.tmap_s[4 + k], sbuf + k * (args.W / 4) * 128, 0, 0, oy, n);
+                        tma_store_4d(&args.tmap_s[4 + k], sbuf + k * q * 128, 0, xb * q, oy, n);
                 } else if (MODE == CONV1_DYN || MODE == CONV1_DENSE || MODE == CONV1_DENSE_MASK) {  // h1: [c_mid/64][rows][64]
                     for (int c = 0; c < BN / 64; ++c)
                         tma_store_3d(&args.tmap_out, sbuf + c * kChunkBytes, 0, mt * kBM, (n0 >> 6) + c);

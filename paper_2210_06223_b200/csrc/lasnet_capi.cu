@@ -535,6 +535,12 @@ size_t proj_ws(const lasnet_block_desc *d, uint8_t *base, void **h1, void **h2, 
 
 }  // namespace
 
+namespace lasnet {
+// the library's launch plan, for the latency predictor (predictor.cu)
+bool plan_fused23(const lasnet_block_desc *d) { return use_fused23(d); }
+bool plan_direct(const lasnet_block_desc *d) { return use_direct(d); }
+}  // namespace lasnet
+
 extern "C" {
 
 const char *lasnet_status_str(lasnet_status st) {
@@ -942,7 +948,7 @@ lasnet_status lasnet_stem(int32_t n, int32_t h, int32_t w, const void *x_pad, co
                           void *ws, size_t ws_bytes, lasnet_stream_t stream) {
     if (!x_pad || !wt || !b || !y) return LASNET_ERR_NULL;
     if (n < 0 || h <= 0 || w <= 0) return LASNET_ERR_SHAPE;
-    if (w % 4 || w / 4 > 256 || misaligned(x_pad) || misaligned(y)) return LASNET_ERR_UNSUPPORTED;
+    if (w % 4 || misaligned(x_pad) || misaligned(y)) return LASNET_ERR_UNSUPPORTED;
     if (!ws || ws_bytes < lasnet_stem_workspace_bytes()) return LASNET_ERR_WORKSPACE;
     if ((long)n * 2 * h * (2 * w + 8) * 8 > 0x7fffffffL) return LASNET_ERR_UNSUPPORTED;
     g_last_launches = 0;
@@ -957,8 +963,13 @@ lasnet_status lasnet_stem(int32_t n, int32_t h, int32_t w, const void *x_pad, co
     a.n_img = n; a.H = h; a.W = w;
     a.w = ws; a.bias = b; a.out = y;
     a.K = 448; a.N = 64; a.a_ld = 448; a.out_ld = 64;
-    a.dense_tiles = n * h;
-    a.m_dense = n * h * 128;
+    // a tile = one output row, or a block of cols_w (<= 128, a multiple of 4 dividing w) of its columns
+    int tx = (w + 127) / 128;
+    while (w % tx || (w / tx) % 4) ++tx;
+    a.tiles_x = tx;
+    a.cols_w = w / tx;
+    a.dense_tiles = n * h * tx;
+    a.m_dense = n * h * tx * 128;
     const uint64_t wp = 2 * (uint64_t)w + 8;  // padded input width (pixels)
     const uint64_t row_b = wp * 16, img_b = 2 * (uint64_t)h * row_b;
     bool ok = tmap2(&a.tmap_b, ws, 448, 64, 64, 64);
@@ -966,7 +977,7 @@ lasnet_status lasnet_stem(int32_t n, int32_t h, int32_t w, const void *x_pad, co
         // A view k: the 8-pixel window of output column ox = 4 j + k starts at padded pixel 2 ox
         const uint64_t d[4] = {64, (uint64_t)w / 4, 2 * (uint64_t)h, (uint64_t)n};
         const uint64_t sd[3] = {128, row_b, img_b};  // window j -> j + 1: 4 output columns = 8 pixels = 128 B
-        const uint32_t bx[4] = {64, (uint32_t)w / 4, 1, 1};
+        const uint32_t bx[4] = {64, (uint32_t)a.cols_w / 4, 1, 1};
         ok = tmap_strided(&a.tmap_s[k], static_cast<const uint8_t *>(x_pad) + 32 * k, 4, d, sd, bx);
         // output view k: columns 4 j + k of each output row
         const uint64_t od[4] = {64, (uint64_t)w / 4, (uint64_t)h, (uint64_t)n};
@@ -976,7 +987,7 @@ lasnet_status lasnet_stem(int32_t n, int32_t h, int32_t w, const void *x_pad, co
     if (!ok) return LASNET_ERR_CUDA;
     {
         KernelEvents ev(st, "stem_conv");
-        if (launch_conv_tc(STEM, a, n * h, num_sms(), st) != cudaSuccess) return LASNET_ERR_CUDA;
+        if (launch_conv_tc(STEM, a, a.dense_tiles, num_sms(), st) != cudaSuccess) return LASNET_ERR_CUDA;
     }
     g_last_launches = 2;
     return LASNET_OK;
@@ -1116,14 +1127,15 @@ lasnet_status lasnet_proj_block(const lasnet_block_desc *d, const lasnet_block_w
 }
 
 int32_t lasnet_choose_schedule(const lasnet_block_desc *d, double r) {
+    // the paper's r_th choice made by the B200 latency predictor
+    // (lasnet_predict_latency, predictor.cu): the schedule predicted faster at rate r
     if (check_desc(d) != LASNET_OK || d->dtype != LASNET_BF16) return LASNET_SCHED_MASKER_SEPARATE;
-    const double S = d->s, hs2 = (S + 2) * (S + 2), px = (double)d->n * d->h * d->w;
-    const double xb = px * d->c_in * 2.0, h1b = px * d->c_mid * 2.0;
-    const double halo = hs2 / (S * S);
-    const double sep = xb + r * halo * xb;
-    // fused: h1 written once, then its halos read (direct) or gathered, written and read again
-    const double fused = xb + h1b + r * halo * h1b * (use_direct(d) ? 1.0 : 2.0);
-    return fused < sep ? LASNET_SCHED_MASKER_FUSED : LASNET_SCHED_MASKER_SEPARATE;
+    if (d->stride != 1 || d->c_in != d->c_out) return LASNET_SCHED_MASKER_SEPARATE;  // first blocks: separate only
+    const double ts = lasnet_predict_latency(d, LASNET_SCHED_MASKER_SEPARATE, r, nullptr, nullptr, nullptr, 0, nullptr);
+    const double tf = lasnet_predict_latency(d, LASNET_SCHED_MASKER_FUSED, r, nullptr, nullptr, nullptr, 0, nullptr);
+    if (ts < 0) return LASNET_SCHED_MASKER_FUSED;
+    if (tf < 0) return LASNET_SCHED_MASKER_SEPARATE;
+    return tf < ts ? LASNET_SCHED_MASKER_FUSED : LASNET_SCHED_MASKER_SEPARATE;
 }
 
 }  // extern "C"

@@ -94,7 +94,8 @@ __global__ void __launch_bounds__(256) avgpool_kernel(const __nv_bfloat16 *__res
         const long n = i / cv;
         float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         const uint4 *src = reinterpret_cast<const uint4 *>(x + n * hw * c) + v;
-        for (int p = 0; p < hw; ++p) {
+#pragma unroll 8
+        for (int p = 0; p < hw; ++p) {  // loads hoisted by the unroll; the adds stay in pixel order
             const uint4 q = __ldg(src + (long)p * cv);
             const uint32_t u[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll

@@ -585,7 +585,7 @@ def test_proj_dyn_block_matches_oracle(n, hi, wi, c_in, c_mid, c_out, stride, s,
     assert max_abs_rel(got, want) <= BF16_TOL
 
 
-@pytest.mark.parametrize("n,h,w", [(2, 16, 24), (1, 32, 16), (2, 224, 224)])
+@pytest.mark.parametrize("n,h,w", [(2, 16, 24), (1, 32, 16), (2, 224, 224), (1, 32, 672)])
 def test_stem_maxpool_head_match_oracle(n, h, w):
     """Stem (tcgen05, 7x7 stride 2 over 4 column-residue window views), max pool and
     head against the fp64 oracle; the 224x224 case is the ImageNet stem."""
@@ -612,24 +612,34 @@ def test_stem_maxpool_head_match_oracle(n, h, w):
     assert np.abs(lg - want_lg).max() <= 1e-4 * max(1.0, np.abs(want_lg).max())
 
 
-@pytest.mark.parametrize("n,hw", [(2, 64), (4, 224)])
-def test_lasnet_network_layerwise_matches_oracle(n, hw):
+NET_CASES = [
+    # n, hw, s_net, backbone
+    (2, 64, (4, 4, 2, 1), False),
+    (4, 224, (4, 4, 2, 1), False),          # the measured ImageNet shape (configs[2])
+    (1, (256, 672), (4, 4, 2, 1), True),     # COCO-shaped backbone (configs[4]): W = 168 > 128 at stage 1
+    (1, (256, 672), (4, 4, 7, 1), True),     # S_net 4-4-7-1: clipped S = 7 cells on 16 x 42
+]
+
+
+@pytest.mark.parametrize("n,hw,s_net,backbone", NET_CASES)
+def test_lasnet_network_layerwise_matches_oracle(n, hw, s_net, backbone):
     """LAS-ResNet-101 run layer by layer through the library (64x64: stages of
     16/8/4/2 px; 224x224: the measured ImageNet shape, stages 56/28/14/7 px,
-    multi-round persistent tiles); each layer's output is checked against the
-    fp64 oracle applied to the same GPU input (teacher forcing): stem, pool,
-    every projection block, every dynamic block (mask bit-exact, activations in
-    tolerance, inactive pixels bitwise), head; then the oracle's own end-to-end
-    forward (oracle.lasnet_forward, the GPU network's masker biases) against the
-    GPU logits."""
+    multi-round persistent tiles; 256x672: a COCO-shaped backbone with
+    column-blocked dense tiles and clipped cells); each layer's output is checked
+    against the fp64 oracle applied to the same GPU input (teacher forcing): stem,
+    pool, every first block (dynamic: mask bit-exact), every dynamic block (mask
+    bit-exact, activations in tolerance, inactive pixels bitwise), head; then the
+    oracle's own end-to-end forward (oracle.lasnet_forward with the GPU network's
+    masker biases and decisions) against the GPU logits / stage outputs."""
+    H, W = (hw, hw) if isinstance(hw, int) else hw
     wts = synth.make_lasnet_weights(seed=5)
-    net = L.LASResNet(n, wts, hw=hw)
+    net = L.LASResNet(n, wts, hw=hw, s_net=s_net, backbone=backbone)
     x = synth.make_image_batch(n, hw, seed=6).cuda()
     net.forward(synth.make_image_batch(n, hw, seed=7).cuda(), calibrate_r=0.5)  # biases from a separate batch
     torch.cuda.synchronize()
-    h = hw // 2
     y = L.stem(x, net.stem_w, net.stem_b)
-    xin = synth.to_f64(x.cpu())[:, :, 4:4 + hw, :]
+    xin = synth.to_f64(x.cpu())[:, :, 4:4 + W, :]
     assert max_abs_rel(synth.to_f64(y.cpu()), oracle.stem(xin, synth.to_f64(net.stem_w.cpu()),
                                                            synth.to_f64(net.stem_b.cpu()))) <= BF16_TOL
     p = L.maxpool(y)
@@ -662,28 +672,37 @@ def test_lasnet_network_layerwise_matches_oracle(n, hw):
             assert max_abs_rel(got[up], want[up]) <= BF16_TOL, f"stage {si} block {bi}"
             assert np.array_equal(got[~up], xin[~up]), f"stage {si} block {bi} inactive pixels"
         cur = out
-    lg = L.head(cur, net.fc_w, net.fc_b).cpu().numpy()
-    want_lg = oracle.head(synth.to_f64(cur.cpu()), synth.to_f64(net.fc_w.cpu()), synth.to_f64(net.fc_b.cpu()))
-    assert np.abs(lg - want_lg).max() <= 1e-4 * max(1.0, np.abs(want_lg).max())
+    if not backbone:
+        lg = L.head(cur, net.fc_w, net.fc_b).cpu().numpy()
+        want_lg = oracle.head(synth.to_f64(cur.cpu()), synth.to_f64(net.fc_w.cpu()), synth.to_f64(net.fc_b.cpu()))
+        assert np.abs(lg - want_lg).max() <= 1e-4 * max(1.0, np.abs(want_lg).max())
     # the captured graph reproduces the eager forward
-    lg_eager = net.forward(x).clone()
+    out_eager = net.forward(x)
+    out_eager = [t.clone() for t in out_eager] if backbone else out_eager.clone()
     g = net.capture(x)
     g.replay()
     torch.cuda.synchronize()
-    assert torch.equal(net.logits, lg_eager)
+    if backbone:
+        assert all(torch.equal(a, b) for a, b in zip(net.features, out_eager))
+    else:
+        assert torch.equal(net.logits, out_eager)
     # end to end: the oracle's own forward from the image with the same masker biases, following the
     # GPU network's decisions (force_masks) so that one 1-ulp bf16 difference upstream cannot flip a
     # near-threshold cell and diverge the two chains; its own (free-running) decisions are counted
     meta = net.oracle_meta()
     keys = sorted(meta["bm"], key=_block_order)
     gpu_masks = {k: b.mask_buf.cpu().numpy() for k, b in zip(keys, net.blocks())}
-    want_e2e, masks = oracle.lasnet_forward(xin_img(x, hw), synth.weights_f64_nested(wts), meta, return_masks=True,
-                                            force_masks=gpu_masks)
+    want_e2e, masks = oracle.lasnet_forward(xin_img(x, W), synth.weights_f64_nested(wts), meta, return_masks=True,
+                                            force_masks=gpu_masks, backbone=backbone)
     diff_cells = sum(int((masks[k] != gpu_masks[k]).sum()) for k in keys)
     total_cells = sum(b.ncells for b in net.blocks())
     # free-running decisions of the fp64 chain agree on >= 99% of the cells
     assert diff_cells <= max(1, total_cells // 100), f"{diff_cells} of {total_cells} decisions differ end to end"
-    assert max_abs_rel(lg_eager.cpu().numpy(), want_e2e) <= BF16_TOL
+    if backbone:
+        for si, (a, b) in enumerate(zip(out_eager, want_e2e)):
+            assert max_abs_rel(synth.to_f64(a.cpu()), b) <= BF16_TOL, f"stage {si} features"
+    else:
+        assert max_abs_rel(out_eager.cpu().numpy(), want_e2e) <= BF16_TOL
 
 
 def xin_img(x, hw):
