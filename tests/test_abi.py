@@ -20,7 +20,7 @@ def lib():
 
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "lasnet.h")).read()
-    return sorted(set(re.findall(r"\b(lasnet_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(lasnet_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_header_and_binding_agree():
