@@ -414,3 +414,174 @@ def lasnet_forward(x, weights, meta, calibrate_r=None, return_masks=False, force
         return (feats, masks) if return_masks else feats
     logits = head(cur, weights["fc_w"], weights["fc_b"])
     return (logits, masks) if return_masks else logits
+
+
+# ------------------------------------------------------------ LAS-RegNetY (NEXT-f3) --
+
+def gconv3x3(h, w, b, stride=1, group_width=16):
+    """Grouped 3x3 convolution, zero padding 1, stride `stride`, + bias (fp64, no
+    activation): the RegNet Y-block's middle conv ("different channel numbers
+    and convolution groups"; group width 16).  h [n][H][W][C]; w [C][3][3][gw] (OHWI
+    with the gw = group_width input channels of the output channel's group)."""
+    h = np.asarray(h, np.float64)
+    w, b = np.asarray(w, np.float64), np.asarray(b, np.float64)
+    n, H, W, C = h.shape
+    gw = group_width
+    s = int(stride)
+    Ho, Wo = -(-H // s), -(-W // s)
+    hp = np.zeros((n, H + 2, W + 2, C))
+    hp[:, 1:-1, 1:-1] = h
+    out = np.zeros((n, Ho, Wo, C))
+    G = C // gw
+    for dy in range(3):
+        for dx in range(3):
+            win = hp[:, dy:dy + s * (Ho - 1) + 1:s, dx:dx + s * (Wo - 1) + 1:s, :]  # [n][Ho][Wo][C]
+            wg = w[:, dy, dx, :].reshape(G, gw, gw)                                 # [g][out][in]
+            out += np.einsum("nyxgi,goi->nyxgo", win.reshape(n, Ho, Wo, G, gw), wg).reshape(n, Ho, Wo, C)
+    return out + b
+
+
+def se_scale(pooled, wts):
+    """Squeeze-and-excitation of a pooled feature (Hu et al.): s = sigmoid(W2
+    ReLU(W1 p + b1) + b2), fp64.  pooled [n][C] -> s [n][C]."""
+    p = np.asarray(pooled, np.float64)
+    z = np.maximum(p @ np.asarray(wts["se_w1"], np.float64).T + np.asarray(wts["se_b1"], np.float64), 0.0)
+    t = z @ np.asarray(wts["se_w2"], np.float64).T + np.asarray(wts["se_b2"], np.float64)
+    return 1.0 / (1.0 + np.exp(-t))
+
+
+def regnet_block(x, wts, stride=1, mask_cells=None, s=1, rmode=ROUND_BF16):
+    """RegNet Y-block (BN folded), static or dynamic (NEXT-f3):
+      h1  = rnd(ReLU(x Wa^T + ba))                          1x1
+      h2  = rnd(ReLU(gconv3x3(h1, Wb, stride) + bb))        grouped 3x3, group width 16
+      p   = mean of h2 over the computed output pixels      (reading R23: in a dynamic
+                                                             block, the ACTIVE pixels only)
+      h2s = rnd(h2 * se_scale(p))                           squeeze-and-excitation
+      R   = x (identity) or Wd x_s + bd (projection, unstored, reading R21)
+      y   = rnd(ReLU(R + h2s Wc^T + bc)) on computed pixels; x on the others
+    x [n][H][W][c_in]; mask_cells [n][gh][gw] on the output grid (None: static block,
+    every pixel computed); projection when wts has "wd" (stride 1 or 2, static only).
+    An image without active cells keeps y = x (no pooled mean is needed)."""
+    x = np.asarray(x, np.float64)
+    f = {k: np.asarray(v, np.float64) for k, v in wts.items()}
+    st = int(stride)
+    h1 = _round_array(np.maximum(x @ f["wa"].T + f["ba"], 0.0), rmode)
+    h2 = _round_array(np.maximum(gconv3x3(h1, f["wb"], f["bb"], st), 0.0), rmode)
+    n, Ho, Wo, C = h2.shape
+    if mask_cells is None:
+        m = np.ones((n, Ho, Wo), bool)
+    else:
+        m = upsample(mask_cells, Ho, Wo, s).astype(bool)
+    cnt = m.reshape(n, -1).sum(axis=1)
+    pooled = (h2 * m[..., None]).reshape(n, -1, C).sum(axis=1) / np.maximum(cnt, 1)[:, None]
+    sc = se_scale(pooled, f)
+    h2s = _round_array(h2 * sc[:, None, None, :], rmode)
+    if "wd" in f:
+        R = x[:, ::st, ::st, :] @ f["wd"].T + f["bd"]
+    else:
+        R = x
+    y = _round_array(np.maximum(R + h2s @ f["wc"].T + f["bc"], 0.0), rmode)
+    if mask_cells is None:
+        return y
+    return np.where(m[..., None], y, x)
+
+
+def regnet_block_literal(x, wts, idx, s, rmode=ROUND_BF16):
+    """Dynamic RegNet Y identity block, literal gather -> compute -> scatter (P:89,
+    P:163-170) in plain loops over the active patches, in two passes because the
+    SE pool needs every active pixel of the image first (reading R23):
+      pass 1, per active patch: gather the (S+2)^2 halo window of x, conv1 (0 outside
+        the image, R6), valid grouped 3x3 -> S x S h2, accumulate the in-image h2
+        into the image's pooled sum;
+      SE per image over its active pixels;
+      pass 2, per active patch: h2s = rnd(h2 * s), conv3 + residual, ReLU, scatter.
+    Small inputs only (Python loops)."""
+    x = np.asarray(x, np.float64)
+    f = {k: np.asarray(v, np.float64) for k, v in wts.items()}
+    n, H, W, _ = x.shape
+    C = f["wa"].shape[0]
+    gh, gw = grid(H, W, s)
+    hs = s + 2
+    y = x.copy()
+    patches = []
+    psum = np.zeros((n, C))
+    pcnt = np.zeros(n)
+    for cid in np.asarray(idx).reshape(-1):
+        img, g = divmod(int(cid), gh * gw)
+        gy, gx = divmod(g, gw)
+        win = np.zeros((hs, hs, C))
+        for wy in range(hs):
+            for wx in range(hs):
+                sy, sx = gy * s - 1 + wy, gx * s - 1 + wx
+                if 0 <= sy < H and 0 <= sx < W:
+                    win[wy, wx] = _round_array(np.maximum(x[img, sy, sx] @ f["wa"].T + f["ba"], 0.0), rmode)
+        h2 = np.zeros((s, s, C))
+        for py in range(s):
+            for px in range(s):
+                acc = f["bb"].copy()
+                for o in range(C):
+                    g0 = (o // 16) * 16
+                    for dy in range(3):
+                        for dx in range(3):
+                            acc[o] += f["wb"][o, dy, dx, :] @ win[py + dy, px + dx, g0:g0 + 16]
+                h2[py, px] = _round_array(np.maximum(acc, 0.0), rmode)
+                if gy * s + py < H and gx * s + px < W:
+                    psum[img] += h2[py, px]
+                    pcnt[img] += 1
+        patches.append((img, gy, gx, h2))
+    sc = se_scale(psum / np.maximum(pcnt, 1)[:, None], f)
+    for img, gy, gx, h2 in patches:
+        for py in range(s):
+            for px in range(s):
+                yy, xx = gy * s + py, gx * s + px
+                if yy < H and xx < W:
+                    h2s = _round_array(h2[py, px] * sc[img], rmode)
+                    y[img, yy, xx] = _round_array(np.maximum(x[img, yy, xx] + h2s @ f["wc"].T + f["bc"], 0.0), rmode)
+    return y
+
+
+def regnet_stem(x, w, b, rmode=ROUND_BF16):
+    """RegNet stem, BN folded: y = rnd(ReLU(conv3x3(x, stride 2, pad 1) + b)).
+    x [n][H][W][c]; w [co][3][3][c] OHWI -> y [n][H/2][W/2][co]."""
+    x = np.asarray(x, np.float64)
+    w, b = np.asarray(w, np.float64), np.asarray(b, np.float64)
+    n, hi, wi, c = x.shape
+    ho, wo = hi // 2, wi // 2
+    xp = np.zeros((n, hi + 2, wi + 2, c))
+    xp[:, 1:-1, 1:-1] = x
+    acc = np.zeros((n, ho, wo, w.shape[0]))
+    for dy in range(3):
+        for dx in range(3):
+            acc += xp[:, dy:dy + 2 * ho:2, dx:dx + 2 * wo:2, :] @ w[:, dy, dx, :].T
+    return _round_array(np.maximum(acc + b, 0.0), rmode)
+
+
+def regnet_forward(x, weights, meta, calibrate_r=None, force_masks=None, return_masks=False):
+    """LAS-RegNetY forward (BASELINE configs[3]; NEXT-f3): RegNet stem -> per stage the
+    static first block (stride 2, projection) and the identity Y-blocks as dynamic
+    blocks (masker -> compaction -> regnet_block with the mask) ->
+    head.  meta: {"depths", "s_net", "bm": {key: bias}}; calibrate_r / force_masks as
+    lasnet_forward.  x [n][H][W][8] (channels 3..7 zero)."""
+    depths, s_net = meta["depths"], meta["s_net"]
+    bms = meta.setdefault("bm", {})
+    cur = regnet_stem(x, weights["stem_w"], weights["stem_b"])
+    masks = {}
+    for si, (depth, s) in enumerate(zip(depths, s_net)):
+        cur = regnet_block(cur, weights[f"s{si}_b0"], stride=2)
+        for b in range(1, depth):
+            key = f"s{si}_b{b}"
+            wb = weights[key]
+            if calibrate_r is not None:
+                _, l0 = masker(cur, wb["wm"], 0.0, s)
+                lg = np.sort(l0.reshape(-1))
+                k = int(round(calibrate_r * lg.size))
+                bm = -(lg[-1] + 1.0) if k <= 0 else (-(lg[0] - 1.0) if k >= lg.size else
+                                                      -0.5 * (lg[lg.size - k - 1] + lg[lg.size - k]))
+                bms[key] = float(np.float32(bm))
+            m, _ = masker(cur, wb["wm"], bms[key], s)
+            masks[key] = m
+            if force_masks is not None and key in force_masks:
+                m = np.asarray(force_masks[key], np.uint8)
+            cur = regnet_block(cur, wb, stride=1, mask_cells=m, s=s)
+    logits = head(cur, weights["fc_w"], weights["fc_b"])
+    return (logits, masks) if return_masks else logits

@@ -166,3 +166,78 @@ def lasnet_oracle_biases(weights: dict, seed: int = 5000, depths=(3, 4, 23, 3), 
     calibrating on its own first forward (it is the oracle that calibrates; this
     module only states the configuration)."""
     return {"depths": tuple(depths), "s_net": tuple(s_net), "bm": {}, "calibrate_seed": int(seed)}
+
+
+# ----------------------------------------------------------- LAS-RegNetY-800MF --
+# torchvision regnet_y_800mf: stem 32; stages (width, depth) = (64, 1), (144, 3),
+# (320, 8), (784, 2); group width 16; bottleneck ratio 1; SE ratio 0.25 of the
+# block INPUT width; every stage's first block has stride 2 (projection shortcut).
+REGNET_Y_800MF = dict(stem=32, widths=(64, 144, 320, 784), depths=(1, 3, 8, 2), group_width=16, se_ratio=0.25)
+
+
+def pad64(c: int) -> int:
+    """Channel count rounded up to the tensor-core K-block of 64 (zero channels)."""
+    return -(-c // 64) * 64
+
+
+def _padded(real: torch.Tensor, shape) -> torch.Tensor:
+    out = torch.zeros(shape, dtype=real.dtype)
+    out[tuple(slice(0, s) for s in real.shape)] = real
+    return out
+
+
+def make_regnet_block_weights(c_in: int, w_out: int, w_se: int, proj: bool, seed: int, dtype: str = "bf16",
+                              group_width: int = 16) -> dict:
+    """Y-block weights (BN folded) at REAL widths c_in -> w_out (bottleneck = w_out),
+    stored zero-padded to pad64 widths: wa [wb][cin], wb [wb][3][3][16] (grouped),
+    se_w1 [w_se][wb], se_w2 [wb][w_se], wc [wout][wb], (proj) wd [wout][cin]; fp32
+    biases; masker weight wm [cin] for the dynamic identity blocks."""
+    g = _gen(seed)
+    dt = _dt(dtype)
+    ci, co = pad64(c_in), pad64(w_out)
+    wa = torch.randn((w_out, c_in), generator=g) * (2.0 / c_in) ** 0.5
+    wb = torch.randn((w_out, 3, 3, group_width), generator=g) * (2.0 / (9 * group_width)) ** 0.5
+    s1 = torch.randn((w_se, w_out), generator=g) * (1.0 / w_out) ** 0.5
+    s2 = torch.randn((w_out, w_se), generator=g) * (1.0 / w_se) ** 0.5
+    wc = torch.randn((w_out, w_out), generator=g) * (2.0 / w_out) ** 0.5 * (1.0 if proj else 0.1)
+    b = {k: torch.randn((n,), generator=g) * 0.05 for k, n in (("ba", w_out), ("bb", w_out), ("bc", w_out),
+                                                                ("se_b1", w_se), ("se_b2", w_out))}
+    out = {
+        "wa": _padded(wa, (co, ci)).to(dt).contiguous(), "ba": _padded(b["ba"], (co,)).float().contiguous(),
+        "wb": _padded(wb, (co, 3, 3, group_width)).to(dt).contiguous(), "bb": _padded(b["bb"], (co,)).float().contiguous(),
+        "se_w1": _padded(s1, (w_se, co)).float().contiguous(), "se_b1": b["se_b1"].float().contiguous(),
+        "se_w2": _padded(s2, (co, w_se)).float().contiguous(), "se_b2": _padded(b["se_b2"], (co,)).float().contiguous(),
+        "wc": _padded(wc, (co, co)).to(dt).contiguous(), "bc": _padded(b["bc"], (co,)).float().contiguous(),
+    }
+    if proj:
+        wd = torch.randn((w_out, c_in), generator=g) * (2.0 / c_in) ** 0.5
+        out["wd"] = _padded(wd, (co, ci)).to(dt).contiguous()
+        out["bd"] = _padded(torch.randn((w_out,), generator=g) * 0.05, (co,)).float().contiguous()
+    else:
+        out["wm"] = _padded((torch.randn((c_in,), generator=g) * (1.0 / c_in) ** 0.5), (ci,)).float().contiguous()
+    return out
+
+
+def make_regnet_weights(cfg=None, classes: int = 1000, seed: int = 21, dtype: str = "bf16") -> dict:
+    """Random-init LAS-RegNetY weights (default RegNetY-800MF) at pad64 widths: stem
+    [64][3][3][8] (32 real output channels, 3 real input channels), per stage block
+    0 (stride 2, projection) and the identity blocks, classifier [classes][pad64(784)]."""
+    cfg = cfg or REGNET_Y_800MF
+    g = _gen(seed)
+    dt = _dt(dtype)
+    stem = torch.randn((cfg["stem"], 3, 3, 3), generator=g) * (2.0 / 27) ** 0.5
+    w = {"stem_w": _padded(stem, (pad64(cfg["stem"]), 3, 3, 8)).to(dt).contiguous(),
+         "stem_b": _padded(torch.randn((cfg["stem"],), generator=g) * 0.05, (pad64(cfg["stem"]),)).float().contiguous()}
+    c_in = cfg["stem"]
+    for si, (width, depth) in enumerate(zip(cfg["widths"], cfg["depths"])):
+        for b in range(depth):
+            w_in = c_in if b == 0 else width
+            w_se = int(round(cfg["se_ratio"] * w_in))
+            w[f"s{si}_b{b}"] = make_regnet_block_weights(w_in, width, w_se, proj=(b == 0),
+                                                         seed=seed * 1000 + 100 * si + b, dtype=dtype,
+                                                         group_width=cfg["group_width"])
+        c_in = width
+    fc = torch.randn((classes, c_in), generator=g) * (1.0 / c_in) ** 0.5
+    w["fc_w"] = _padded(fc, (classes, pad64(c_in))).to(dt).contiguous()
+    w["fc_b"] = torch.zeros((classes,)).float().contiguous()
+    return w
