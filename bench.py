@@ -74,6 +74,7 @@ def parse():
     ap.add_argument("--no-sweep", action="store_true", help="skip the S x r block sweep")
     ap.add_argument("--no-block", action="store_true", help="skip the block sub-object")
     ap.add_argument("--no-coco", action="store_true", help="skip the COCO backbone sub-object (configs[4])")
+    ap.add_argument("--no-regnet", action="store_true", help="skip the LAS-RegNetY sub-object (configs[3])")
     ap.add_argument("--detail", default=None, help="write per-kernel detail JSON here")
     ap.add_argument("--schedule", default="auto", choices=["auto", "separate", "fused"],
                     help="block sub-object: separate = north-star branch (masker, then gather+conv1 on halos); "
@@ -468,7 +469,7 @@ def network_measure(args, world, rank, local, hbm, tfl):
     def step():
         g.replay()
         if world > 1:
-            dist.all_gather_into_tensor(gathered, net.logits)
+            ldist.exchange_logits(net.logits, gathered)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -523,7 +524,7 @@ def network_measure(args, world, rank, local, hbm, tfl):
     del graphs
 
     tot_max, dense_max, e2e_max = ldist.max_over_ranks([tot_ms, dense_ms, e2e_ms], device="cuda")
-    act_all = ldist.sum_over_ranks(act + cells, device="cuda")
+    act_all = ldist.active_counts(act + cells, device="cuda")
     rank_ms = ldist.gather_over_ranks(tot_ms / K, device="cuda")
     res = dict(n_loc=n_loc, step_ms=step_ms, tot_ms=tot_ms, tot_max=tot_max, dense_ms=dense_max, e2e_ms=e2e_max,
                launches=launches, trace=trace, launches_per_step=launches_per_step, rank_ms=rank_ms,
@@ -798,6 +799,52 @@ def coco_measure(args, rank):
     return out
 
 
+# ------------------------------------------------------------ LAS-RegNetY ----
+
+def regnet_measure(args, rank, world):
+    """BASELINE configs[3]: LAS-RegNetY-800MF at ImageNet 224x224, global batch 512
+    sharded over the ranks, S_net 4-4-2-1, r = 0.5 (masker biases calibrated on a
+    separate batch); one CUDA graph per forward; the dense comparator runs every
+    identity Y-block static."""
+    import synth
+    import paper_2210_06223_b200 as L
+    from paper_2210_06223_b200 import dist as ldist
+
+    lo, hi = ldist.shard(512, rank, world)
+    n = hi - lo
+    weights = synth.make_regnet_weights(seed=21)
+    x = synth.make_image_batch(n, 224, seed=300 + rank).cuda()
+    net = L.LASRegNet(n, weights, hw=224)
+    net.forward(synth.make_image_batch(n, 224, seed=7000 + rank).cuda(), calibrate_r=0.5)
+    stream = torch.cuda.current_stream()
+    steps = max(3, min(args.steps, 10))
+    res = {}
+    for dense in (False, True):
+        g = net.capture(x, dense=dense)
+        for _ in range(2):
+            g.replay()
+        a, b = ev_pair()
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(steps):
+            g.replay()
+        b.record(stream)
+        torch.cuda.synchronize()
+        res[dense] = a.elapsed_time(b) / steps
+        del g
+    r_blocks = [int(b.count.item()) / b.ncells for b in net.blocks()]
+    t_dyn, t_dense = ldist.max_over_ranks([res[False], res[True]], device="cuda")
+    del net
+    torch.cuda.empty_cache()
+    return {"workload": "LAS-RegNetY-800MF forward (BASELINE configs[3]): 224x224, global batch 512 sharded over the "
+                        "GPUs, S_net 4-4-2-1 (identity Y-blocks dynamic, stage-first blocks static), r = 0.5; widths "
+                        "zero-padded to multiples of 64",
+            "per_gpu_batch": n, "ms_per_forward": round(t_dyn, 4), "images_per_s": round(512 / (t_dyn * 1e-3), 1),
+            "dense_ms_per_forward": round(t_dense, 4), "speedup_vs_dense": round(t_dense / t_dyn, 3),
+            "r_patch_mean": round(statistics.fmean(r_blocks), 4),
+            "timing": f"mean of {steps} CUDA-graph replays per forward, max over ranks"}
+
+
 # ---------------------------------------------------------------- lasnet ----
 
 def run_lasnet(args):
@@ -828,6 +875,7 @@ def run_lasnet(args):
     blk = None if args.no_block else block_measure(args, world, rank, hbm, tfl)
     sweep = None if args.no_sweep else block_sweep(args, rank, hbm, tfl)
     coco = None if args.no_coco else coco_measure(args, rank)
+    regnet = None if args.no_regnet else regnet_measure(args, rank, world)
     clocks = sampler.stop()
     if blk is not None:
         b_tot = sum(blk["step_ms"])
@@ -916,6 +964,8 @@ def run_lasnet(args):
             line["block_sweep"] = sweep
         if coco is not None:
             line["coco_backbone"] = coco
+        if regnet is not None:
+            line["regnet"] = regnet
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_net(net["x_cpu"], net["weights"], net["net"].oracle_meta(),
                                                     args.cpu_budget)

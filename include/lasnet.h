@@ -255,6 +255,43 @@ size_t lasnet_block_forward_workspace_bytes(const lasnet_block_desc *desc, int32
  * launches nothing. */
 int32_t lasnet_choose_schedule(const lasnet_block_desc *desc, double r);
 
+/* LAS-RegNetY Y-block ("bottleneck structure with
+ * different channel numbers and convolution groups ... Squeeze-and-Excitation"),
+ * BN folded, bf16, all widths multiples of 64 (RegNet widths zero-padded):
+ *   h1  = ReLU(x Wa^T + ba)                         1x1, c_in -> c_mid
+ *   h2  = ReLU(gconv3x3(h1, Wb, stride) + bb)       grouped 3x3, group width 16
+ *   s   = sigmoid(W2 ReLU(W1 mean(h2) + b1) + b2)   SE; the mean over the computed
+ *                                                   pixels (dynamic: the image's
+ *                                                   ACTIVE pixels, R23)
+ *   y   = ReLU(R + (h2 * s) Wc^T + bc)              R = x, or Wd x_s + bd (projection)
+ * Dynamic (wm != NULL; identity only: stride 1, c_in == c_out, no wd): the five
+ * steps -- masker + compaction, gather + conv1 on the (s+2)^2 halos, the grouped
+ * 3x3 on the gathered windows, SE over the active pixels, conv3 + scatter-add in
+ * place; y == x runs in place, else x is copied to y first; inactive pixels keep
+ * x; mask nullable.  Static (wm == NULL): every pixel, stride 1 or 2, y
+ * must not overlap x.  h1, h2, h2*s and y are stored bf16 (RNE).
+ *   w      weights; se_* fp32 [w_se][c_mid], [w_se], [c_mid][w_se], [c_mid]
+ *   ws     lasnet_regnet_workspace_bytes(desc, dynamic) bytes, ALL ZERO before the
+ *          first dynamic call (masker control words, left zero by every call). */
+typedef struct {
+    const void *wa; const float *ba;          /* [c_mid][c_in]                           */
+    const void *wb; const float *bb;          /* [c_mid][3][3][16] grouped (OHWI in-group) */
+    const float *se_w1; const float *se_b1;   /* [w_se][c_mid], [w_se]                   */
+    const float *se_w2; const float *se_b2;   /* [c_mid][w_se], [c_mid]                  */
+    int32_t w_se;
+    const void *wc; const float *bc;          /* [c_out][c_mid]                          */
+    const void *wd; const float *bd;          /* projection [c_out][c_in], or NULL       */
+} lasnet_regnet_weights;
+lasnet_status lasnet_regnet_block(const lasnet_block_desc *desc, const lasnet_regnet_weights *wts, const void *x,
+                                  void *y, const float *wm, float bm, uint8_t *mask, int32_t *idx, int32_t *count,
+                                  void *ws, size_t ws_bytes, lasnet_stream_t stream);
+size_t lasnet_regnet_workspace_bytes(const lasnet_block_desc *desc, int32_t dynamic);
+/* RegNet stem: 3x3 stride-2 conv, c_real (<= 64, even) output channels + bias +
+ * ReLU, channels c_real..63 written 0: x_pad [n][2h][2w + 8][8] (as lasnet_stem),
+ * wt [64][3][3][8] OHWI, b [64] fp32 -> y [n][h][w][64].  CUDA-core kernel. */
+lasnet_status lasnet_regnet_stem(int32_t n, int32_t h, int32_t w, int32_t c_real, const void *x_pad, const void *wt,
+                                 const float *b, void *y, lasnet_stream_t stream);
+
 /* Latency predictor G(H, P, S, r) (sec. 3.3 "Latency prediction
  * model", App. A) re-targeted to B200.  Host-
  * side, pure: launches nothing.

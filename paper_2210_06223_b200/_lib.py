@@ -27,6 +27,7 @@ EXPORTS = [
     "lasnet_proj_block", "lasnet_proj_workspace_bytes", "lasnet_stem", "lasnet_stem_workspace_bytes",
     "lasnet_maxpool", "lasnet_head", "lasnet_head_workspace_bytes", "lasnet_kernel_event_name",
     "lasnet_kernel_event_count", "lasnet_hw_b200", "lasnet_kernel_type_name", "lasnet_predict_latency",
+    "lasnet_regnet_block", "lasnet_regnet_workspace_bytes", "lasnet_regnet_stem",
 ]
 
 # lasnet_schedule (SCHED_DENSE: predictor only, the static block)
@@ -47,6 +48,13 @@ class BlockDesc(ctypes.Structure):
 
 class BlockWeights(ctypes.Structure):
     _fields_ = [(k, ctypes.c_void_p) for k in ("w1", "b1", "w2", "b2", "w3", "b3", "wd", "bd")]
+
+
+class RegnetWeights(ctypes.Structure):
+    _fields_ = [("wa", ctypes.c_void_p), ("ba", ctypes.c_void_p), ("wb", ctypes.c_void_p), ("bb", ctypes.c_void_p),
+                ("se_w1", ctypes.c_void_p), ("se_b1", ctypes.c_void_p), ("se_w2", ctypes.c_void_p),
+                ("se_b2", ctypes.c_void_p), ("w_se", ctypes.c_int32), ("wc", ctypes.c_void_p), ("bc", ctypes.c_void_p),
+                ("wd", ctypes.c_void_p), ("bd", ctypes.c_void_p)]
 
 
 class LasnetError(RuntimeError):
@@ -125,6 +133,13 @@ def load(path: str = LIB_PATH):
     lib.lasnet_predict_latency.argtypes = [D, i32, ctypes.c_double, ctypes.POINTER(HW), ctypes.POINTER(i32),
                                            ctypes.POINTER(ctypes.c_double), i32, ctypes.POINTER(i32)]
     lib.lasnet_predict_latency.restype = ctypes.c_double
+    RW = ctypes.POINTER(RegnetWeights)
+    lib.lasnet_regnet_block.argtypes = [D, RW, vp, vp, vp, ctypes.c_float, vp, vp, vp, vp, sz, vp]
+    lib.lasnet_regnet_block.restype = ctypes.c_int
+    lib.lasnet_regnet_workspace_bytes.argtypes = [D, i32]
+    lib.lasnet_regnet_workspace_bytes.restype = sz
+    lib.lasnet_regnet_stem.argtypes = [i32, i32, i32, i32, vp, vp, vp, vp, vp]
+    lib.lasnet_regnet_stem.restype = ctypes.c_int
     _lib = lib
     return lib
 

@@ -13,8 +13,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "liblasnet.so")
 SOURCES = ["lasnet_capi.cu", "mask_compact.cu", "conv_tc.cu", "conv23_tc.cu", "conv_simt.cu", "decide_gather.cu",
-           "proj_block.cu", "net_layers.cu", "predictor.cu"]
-HEADERS = ["rowmap.cuh", "sm100_ptx.cuh", "launch.cuh", "predictor_b200.inc"]
+           "proj_block.cu", "net_layers.cu", "predictor.cu",
+           "regnet.cu"]
+HEADERS = ["rowmap.cuh", "sm100_ptx.cuh", "launch.cuh", "predictor_b200.inc", "regnet.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

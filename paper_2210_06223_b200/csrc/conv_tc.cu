@@ -630,11 +630,23 @@ static cudaError_t launch_mode_bn(const ConvArgs &a, int max_tiles_m, int num_sm
     return launch_k(kern, dim3(grid), dim3(threads_of<MODE, BN>()), smem, st, a);
 }
 
+// conv2 (dynamic) stays on 128-column tiles: 256-column tiles measured no faster
+// (stage-3 blocks of LAS-R101: 1.121 vs 1.115 ms over 26 launches); LASNET_CONV2_BN=256 opts in
+inline bool bn256_enabled(int mode) {
+    static const bool conv2_256 = [] {
+        const char *e = getenv("LASNET_CONV2_BN");
+        return e && atoi(e) == 256;
+    }();
+    return mode != CONV2_DYN || conv2_256;
+}
+
 template <int MODE>
 static cudaError_t launch_mode(const ConvArgs &a, int max_tiles_m, int num_sms, cudaStream_t st) {
-    if (a.N == 64) return launch_mode_bn<MODE, 64>(a, max_tiles_m, num_sms, st);
-    if constexpr (MODE == CONV1_DYN || MODE == CONV1_DENSE || MODE == CONV1_DENSE_MASK) {
-        if (a.N % 256 == 0) return launch_mode_bn<MODE, 256>(a, max_tiles_m, num_sms, st);
+    if (a.N % 128 != 0) return launch_mode_bn<MODE, 64>(a, max_tiles_m, num_sms, st);  // 64-column N tiles
+    if constexpr (MODE == CONV1_DYN || MODE == CONV1_DENSE || MODE == CONV1_DENSE_MASK || MODE == CONV2_DYN) {
+        // 256-column tiles: A (the gathered rows / the im2col taps) is staged once per M
+        // tile instead of once per 128-column N tile
+        if (a.N % 256 == 0 && bn256_enabled(MODE)) return launch_mode_bn<MODE, 256>(a, max_tiles_m, num_sms, st);
     }
     if (a.N % 128 == 0) return launch_mode_bn<MODE, 128>(a, max_tiles_m, num_sms, st);
     return cudaErrorInvalidValue;

@@ -100,7 +100,7 @@ int num_sms() {
 bool masker_channels_ok(int c, int vec) {
     if (c % vec) return false;
     const int nvec = c / vec;
-    return nvec < 32 || nvec == 32 || nvec == 64 || nvec == 128 || nvec == 256;  // 1, 2, 4, 8 slots
+    return nvec <= 256;  // up to 8 slots of 32 vectors (the last one partial)
 }
 
 size_t elt_size(int dtype) { return dtype == LASNET_BF16 ? 2 : 4; }
@@ -275,8 +275,12 @@ void dense_tiling(ConvArgs &a, int n, int h, int w) {
 
 // N tile of conv_tc's launch for `mode` (must match launch_mode in conv_tc.cu)
 int bn_of(int n, int mode) {
-    if (n == 64) return 64;
+    if (n % 128 != 0) return 64;
     if (n % 256 == 0 && (mode == CONV1_DYN || mode == CONV1_DENSE || mode == CONV1_DENSE_MASK)) return 256;
+    if (n % 256 == 0 && mode == CONV2_DYN) {  // opt-in (conv_tc.cu bn256_enabled)
+        const char *e = getenv("LASNET_CONV2_BN");
+        if (e && atoi(e) == 256) return 256;
+    }
     return 128;
 }
 
@@ -1136,6 +1140,237 @@ int32_t lasnet_choose_schedule(const lasnet_block_desc *d, double r) {
     if (ts < 0) return LASNET_SCHED_MASKER_FUSED;
     if (tf < 0) return LASNET_SCHED_MASKER_SEPARATE;
     return tf < ts ? LASNET_SCHED_MASKER_FUSED : LASNET_SCHED_MASKER_SEPARATE;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// LAS-RegNetY Y-block (include/lasnet.h lasnet_regnet_block)
+// ---------------------------------------------------------------------------
+#include "regnet.cuh"
+
+namespace {
+
+struct RegWs {
+    void *sync, *mask, *h1, *h2, *scale, *xs, *w3d, *b3d;
+};
+
+size_t regnet_ws(const lasnet_block_desc *d, bool dyn, uint8_t *base, RegWs *o) {
+    const size_t e = 2;
+    const int S = d->s, st = d->stride;
+    const long ncells = (long)d->n * ((d->h + S - 1) / S) * ((d->w + S - 1) / S);
+    const size_t pxo = (size_t)d->n * d->h * d->w, pxi = pxo * st * st;
+    Carve cv{base};
+    RegWs r{};
+    if (dyn) {
+        r.sync = cv.take(mask_compact_workspace_bytes(ncells));
+        r.mask = cv.take((size_t)ncells);
+        r.h1 = cv.take((size_t)ncells * (S + 2) * (S + 2) * d->c_mid * e);
+        r.h2 = cv.take((size_t)ncells * S * S * d->c_mid * e);
+    } else {
+        r.h1 = cv.take(pxi * d->c_mid * e);
+        r.h2 = cv.take(pxo * d->c_mid * e);
+        if (st > 1) r.xs = cv.take(pxo * d->c_in * e);
+        r.w3d = cv.take((size_t)d->c_out * (d->c_mid + d->c_in) * e);
+        r.b3d = cv.take((size_t)d->c_out * 4);
+    }
+    r.scale = cv.take((size_t)d->n * d->c_mid * 4);
+    if (o) *o = r;
+    return cv.used;
+}
+
+lasnet_status regnet_check(const lasnet_block_desc *d, const lasnet_regnet_weights *w, bool dyn) {
+    lasnet_status s = check_desc(d);
+    if (s != LASNET_OK) return s;
+    if (!w || !w->wa || !w->ba || !w->wb || !w->bb || !w->se_w1 || !w->se_b1 || !w->se_w2 || !w->se_b2 || !w->wc ||
+        !w->bc)
+        return LASNET_ERR_NULL;
+    if (w->w_se <= 0) return LASNET_ERR_SHAPE;
+    if (d->dtype != LASNET_BF16) return LASNET_ERR_UNSUPPORTED;
+    if (d->c_in % 64 || d->c_mid % 64 || d->c_out % 64 || d->c_mid > 2048 || d->c_out > 2048)
+        return LASNET_ERR_UNSUPPORTED;
+    const bool proj = w->wd != nullptr || w->bd != nullptr;
+    if (proj && (!w->wd || !w->bd)) return LASNET_ERR_NULL;
+    if (!proj && (d->stride != 1 || d->c_in != d->c_out)) return LASNET_ERR_SHAPE;  // identity needs a same-shape residual
+    if (dyn && (proj || d->s > 11 || !masker_channels_ok(d->c_in, 8))) return LASNET_ERR_UNSUPPORTED;
+    return LASNET_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t lasnet_regnet_workspace_bytes(const lasnet_block_desc *d, int32_t dynamic) {
+    if (check_desc(d) != LASNET_OK) return 0;
+    return regnet_ws(d, dynamic != 0, nullptr, nullptr);
+}
+
+lasnet_status lasnet_regnet_block(const lasnet_block_desc *d, const lasnet_regnet_weights *w, const void *x, void *y,
+                                  const float *wm, float bm, uint8_t *mask, int32_t *idx, int32_t *count, void *ws,
+                                  size_t ws_bytes, lasnet_stream_t stream) {
+    const bool dyn = wm != nullptr;
+    lasnet_status s = regnet_check(d, w, dyn);
+    if (s != LASNET_OK) return s;
+    if (!x || !y || (dyn && (!idx || !count))) return LASNET_ERR_NULL;
+    if (misaligned(x) || misaligned(y)) return LASNET_ERR_UNSUPPORTED;
+    const int st_ = d->stride, S = d->s, C = d->c_mid;
+    const int Hi = d->h * st_, Wi = d->w * st_;
+    const long pxo = (long)d->n * d->h * d->w, pxi = pxo * st_ * st_;
+    if (pxi * (d->c_in > C ? d->c_in : C) > 0x7fffffffL || pxo * d->c_out > 0x7fffffffL) return LASNET_ERR_UNSUPPORTED;
+    {
+        const size_t xb = (size_t)pxi * d->c_in * 2;
+        if (dyn) {
+            if ((s = check_alias(x, y, xb)) != LASNET_OK) return s;
+        } else {
+            const uint8_t *a = static_cast<const uint8_t *>(x), *b = static_cast<const uint8_t *>(y);
+            const size_t yb = (size_t)pxo * d->c_out * 2;
+            if (a < b + yb && b < a + xb) return LASNET_ERR_ALIAS;  // static: out of place
+        }
+    }
+    if (!ws || ws_bytes < regnet_ws(d, dyn, nullptr, nullptr)) return LASNET_ERR_WORKSPACE;
+    g_last_launches = 0;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (d->n == 0) return dyn ? (cudaMemsetAsync(count, 0, 4, st) == cudaSuccess ? LASNET_OK : LASNET_ERR_CUDA)
+                              : LASNET_OK;
+    RegWs r;
+    regnet_ws(d, dyn, static_cast<uint8_t *>(ws), &r);
+    const int gh = (d->h + S - 1) / S, gw = (d->w + S - 1) / S, G = gh * gw;
+    const int ncells = d->n * G;
+    int launches = 0;
+    GconvArgs g{};
+    g.wb = static_cast<const __nv_bfloat16 *>(w->wb);
+    g.bias = w->bb;
+    g.h2 = static_cast<__nv_bfloat16 *>(r.h2);
+    g.C = C;
+    SeArgs se{};
+    se.h2 = static_cast<const __nv_bfloat16 *>(r.h2);
+    se.w1 = w->se_w1; se.b1 = w->se_b1; se.w2 = w->se_w2; se.b2 = w->se_b2;
+    se.scale = static_cast<float *>(r.scale);
+    se.C = C; se.w_se = w->w_se; se.n_img = d->n;
+    se.S = S; se.H = d->h; se.W = d->w; se.G = G; se.Gw = gw; se.HW = d->h * d->w;
+    if (dyn) {
+        uint8_t *m = mask ? mask : static_cast<uint8_t *>(r.mask);
+        if (x != y && cudaMemcpyAsync(y, x, (size_t)pxi * d->c_in * 2, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+            return LASNET_ERR_CUDA;
+        {  // steps 1+2: masker + compaction
+            KernelEvents ev(st, "mask_compact");
+            if (launch_mask_compact(1, x, wm, bm, d->n, d->h, d->w, d->c_in, S, m, nullptr, idx, count, r.sync, st) !=
+                cudaSuccess)
+                return LASNET_ERR_CUDA;
+            ++launches;
+        }
+        // step 3: gather + conv1 over the (S+2)^2 halo of every active patch
+        ConvArgs a = base_args(d);
+        a.idx = idx; a.count = count;
+        a.a_src = x; a.w = w->wa; a.bias = w->ba; a.out = r.h1; a.resid = nullptr;
+        a.K = d->c_in; a.N = C; a.a_ld = d->c_in; a.out_ld = C;
+        const int hs = S + 2;
+        if (run_conv(d, CONV1_DYN, a, ncells * hs * hs, x, y, r.h1, r.h2, ncells, st) != cudaSuccess)
+            return LASNET_ERR_CUDA;
+        ++launches;
+        // step 4: grouped 3x3 on the windows, then SE pooled over the active pixels (reading R23)
+        g.h1 = static_cast<const __nv_bfloat16 *>(r.h1);
+        g.h1_rows = (int64_t)ncells * hs * hs;
+        g.count = count;
+        g.S = S; g.hs = hs;
+        {
+            KernelEvents ev(st, "gconv_dyn");
+            if (launch_gconv(true, g, ncells * S * S, num_sms(), st) != cudaSuccess) return LASNET_ERR_CUDA;
+        }
+        se.idx = idx; se.count = count;
+        {
+            KernelEvents ev(st, "se");
+            if (launch_se(se, st) != cudaSuccess) return LASNET_ERR_CUDA;
+        }
+        {
+            KernelEvents ev(st, "se_apply");
+            if (launch_se_apply(static_cast<__nv_bfloat16 *>(r.h2), se.scale, idx, count, ncells * S * S, C, S, G,
+                                d->h * d->w, num_sms(), st) != cudaSuccess)
+                return LASNET_ERR_CUDA;
+        }
+        // step 5: conv3 + residual + scatter-add, in place on y
+        ConvArgs c3 = base_args(d);
+        c3.idx = idx; c3.count = count;
+        c3.a_src = r.h2; c3.w = w->wc; c3.bias = w->bc; c3.out = y; c3.resid = y;
+        c3.K = C; c3.N = d->c_out; c3.a_ld = C; c3.out_ld = d->c_out;
+        if (run_conv(d, CONV3_DYN, c3, ncells * S * S, y, y, r.h1, r.h2, ncells, st) != cudaSuccess)
+            return LASNET_ERR_CUDA;
+        g_last_launches = launches + 4;
+        return LASNET_OK;
+    }
+    // static Y-block (every pixel; identity or projection, stride 1 or 2)
+    lasnet_block_desc di = *d;
+    di.h = Hi; di.w = Wi; di.stride = 1;
+    ConvArgs a = base_args(&di);
+    a.m_dense = (int)pxi;
+    a.a_src = x; a.w = w->wa; a.bias = w->ba; a.out = r.h1;
+    a.K = d->c_in; a.N = C; a.a_ld = d->c_in; a.out_ld = C;
+    if (run_conv(&di, CONV1_DENSE, a, (int)pxi, x, y, r.h1, r.h2, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    g.h1 = static_cast<const __nv_bfloat16 *>(r.h1);
+    g.h1_rows = pxi;
+    g.rows = (int)pxo;
+    g.H = Hi; g.W = Wi; g.Ho = d->h; g.Wo = d->w; g.stride = st_;
+    {
+        KernelEvents ev(st, "gconv_dense");
+        if (launch_gconv(false, g, (int)pxo, num_sms(), st) != cudaSuccess) return LASNET_ERR_CUDA;
+    }
+    {
+        KernelEvents ev(st, "se");
+        if (launch_se(se, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    }
+    {
+        KernelEvents ev(st, "se_apply");
+        if (launch_se_apply(static_cast<__nv_bfloat16 *>(r.h2), se.scale, nullptr, nullptr, (int)pxo, C, 1, 1,
+                            d->h * d->w, num_sms(), st) != cudaSuccess)
+            return LASNET_ERR_CUDA;
+    }
+    launches = 4;
+    ConvArgs c = base_args(d);
+    c.m_dense = (int)pxo;
+    c.a_src = r.h2; c.out = y; c.out_ld = d->c_out; c.a_ld = C; c.N = d->c_out;
+    if (w->wd) {  // y = ReLU([h2s | x_s] [Wc | Wd]^T + bc + bd): one K-concatenated GEMM (reading R21)
+        const void *xs = x;
+        if (st_ > 1) {
+            KernelEvents ev(st, "subsample");
+            if (launch_subsample(x, r.xs, d->n, d->h, d->w, d->c_in * 2, st_, num_sms(), st) != cudaSuccess)
+                return LASNET_ERR_CUDA;
+            xs = r.xs;
+            ++launches;
+        }
+        const size_t wrow = (size_t)(C + d->c_in) * 2;
+        if (cudaMemcpy2DAsync(r.w3d, wrow, w->wc, (size_t)C * 2, (size_t)C * 2, d->c_out, cudaMemcpyDeviceToDevice,
+                              st) != cudaSuccess ||
+            cudaMemcpy2DAsync(static_cast<uint8_t *>(r.w3d) + (size_t)C * 2, wrow, w->wd, (size_t)d->c_in * 2,
+                              (size_t)d->c_in * 2, d->c_out, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+            return LASNET_ERR_CUDA;
+        {
+            KernelEvents ev(st, "add_bias");
+            if (launch_add_bias(w->bc, w->bd, static_cast<float *>(r.b3d), d->c_out, st) != cudaSuccess)
+                return LASNET_ERR_CUDA;
+            ++launches;
+        }
+        c.w = r.w3d; c.bias = static_cast<const float *>(r.b3d); c.resid = nullptr;
+        c.K = C + d->c_in; c.a2_kb = C / 64;
+        if (!tmap2(&c.tmap_s[0], xs, d->c_in, (uint64_t)pxo, 64, 128)) return LASNET_ERR_CUDA;
+    } else {
+        c.w = w->wc; c.bias = w->bc; c.resid = x; c.K = C;
+    }
+    if (run_conv(d, CONV3_DENSE, c, (int)pxo, x, y, nullptr, r.h2, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    g_last_launches = launches + 1;
+    return LASNET_OK;
+}
+
+lasnet_status lasnet_regnet_stem(int32_t n, int32_t h, int32_t w, int32_t c_real, const void *x_pad, const void *wt,
+                                 const float *b, void *y, lasnet_stream_t stream) {
+    if (!x_pad || !wt || !b || !y) return LASNET_ERR_NULL;
+    if (n < 0 || h <= 0 || w <= 0 || c_real <= 0 || c_real > 64 || c_real % 2) return LASNET_ERR_SHAPE;
+    if (misaligned(x_pad) || misaligned(y)) return LASNET_ERR_UNSUPPORTED;
+    g_last_launches = 0;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    KernelEvents ev(st, "regnet_stem");
+    if (launch_regnet_stem(x_pad, wt, b, y, n, h, w, c_real, num_sms(), st) != cudaSuccess) return LASNET_ERR_CUDA;
+    g_last_launches = n > 0 ? 1 : 0;
+    return LASNET_OK;
 }
 
 }  // extern "C"

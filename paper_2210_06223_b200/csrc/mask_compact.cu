@@ -129,7 +129,9 @@ __device__ __forceinline__ void warp_items_s(const T *__restrict__ x, const floa
                 if (qp < npix) {
                     const uint4 *pix = base + qy * rowpitch + (long)qx * (C / PV);
 #pragma unroll
-                    for (int sl = 0; sl < SLOTS; ++sl) q[i * SLOTS + sl] = __ldg(pix + sl * 32);
+                    for (int sl = 0; sl < SLOTS; ++sl)  // a partial last slot (nvec % 32) loads zeros
+                        q[i * SLOTS + sl] = (!wide || sl * 32 + vlane < mg.nvec) ? __ldg(pix + sl * 32)
+                                                                                  : make_uint4(0u, 0u, 0u, 0u);
                     ++np;
                 }
                 qp += pstride;
@@ -148,11 +150,12 @@ __device__ __forceinline__ void warp_items_s(const T *__restrict__ x, const floa
             if (i >= np) break;
 #pragma unroll
             for (int sl = 0; sl < SLOTS; ++sl) {
-                const float4 *wp = reinterpret_cast<const float4 *>(wm + (sl * 32 + vlane) * PV);
+                const bool live = !wide || sl * 32 + vlane < mg.nvec;
+                const float4 *wp = reinterpret_cast<const float4 *>(wm + (live ? sl * 32 + vlane : 0) * PV);
                 float w[PV];
 #pragma unroll
                 for (int e = 0; e < PV / 4; ++e) {
-                    const float4 f = __ldg(wp + e);  // L1-resident
+                    const float4 f = live ? __ldg(wp + e) : make_float4(0.f, 0.f, 0.f, 0.f);  // L1-resident
                     w[4 * e] = f.x;
                     w[4 * e + 1] = f.y;
                     w[4 * e + 2] = f.z;
@@ -162,7 +165,7 @@ __device__ __forceinline__ void warp_items_s(const T *__restrict__ x, const floa
                     Elem<T>::fma8(q[i * SLOTS + sl], w, dacc);
                 } else {
                     Elem<T>::ffma8(q[i * SLOTS + sl], w, facc, fmag);
-                    nterms += PV;
+                    nterms += live ? PV : 0;
                 }
             }
         }
@@ -290,7 +293,10 @@ MaskGeo mask_geo(int C, int PV, int S) {
     MaskGeo g;
     g.nvec = C / PV;
     g.ppw = g.nvec < 32 ? 32 / g.nvec : 1;
-    g.nvl = g.nvec >= 32 ? g.nvec / 32 : 1;
+    // vector slots per lane: ceil(nvec / 32) rounded up to a power of two (the kernel's
+    // SLOTS template); lanes past nvec in the last slot load nothing
+    g.nvl = 1;
+    while (g.nvec >= 32 && g.nvl * 32 < g.nvec) g.nvl *= 2;
     const int items = g.nvec >= 32 ? S * S * g.nvl : (S * S + g.ppw - 1) / g.ppw;  // loads per lane per cell
     // warps per cell: LASNET_MASK_MAXITEMS (default 8 = loads per lane per round
     // trip) bounds a warp's share; 1 warp per cell walks the cell in several round trips

@@ -1,0 +1,342 @@
+// regnet.cu -- the kernels the LAS-RegNetY Y-block needs beyond the ResNet
+// bottleneck's ("bottleneck structure with different
+// channel numbers and convolution groups ... equipped with Squeeze-and-Excitation"):
+//
+//   gconv_kernel      grouped 3x3 (group width 16), bias, ReLU, bf16: on the gathered
+//                     (S+2)^2 windows of the active patches (dynamic block, valid conv,
+//                     P:163-166) or on a dense map (static block, zero padding 1,
+//                     stride 1 or 2).  Per group the contraction is only 144 deep and 16
+//                     wide, so it runs on warp-level mma.sync m16n8k16 (bf16 x bf16 ->
+//                     fp32) rather than 128-row tcgen05 tiles: a warp owns 16 output
+//                     rows and walks all groups, nine taps x two 8-wide halves each.
+//   se_kernel         squeeze-and-excitation per image: the mean of h2 over the image's
+//                     computed pixels (its ACTIVE in-image pixels in a dynamic block,
+//                     reading R23), then s = sigmoid(W2 ReLU(W1 p + b1) + b2); one CTA
+//                     per image, fixed summation order (deterministic).
+//   se_apply_kernel   h2 <- rnd(h2 * s[image]) in place, 16-B vectors.
+//   regnet_stem_kernel the RegNet stem: 3x3 stride-2 conv 3 -> 32 channels + bias +
+//                     ReLU (zero channels 32..63 for the 64-wide K-blocks downstream).
+// Layouts: h1 channel-chunk-major [C/64][rows][64] (what conv_tc's conv1 stores);
+// h2 row-major [rows][C]; weights wb [C][3][3][16] (OHWI within the group).
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "launch.cuh"
+#include "regnet.cuh"
+
+namespace lasnet {
+
+__device__ __forceinline__ uint32_t ldg_u32(const __nv_bfloat16 *p) {
+    return __ldg(reinterpret_cast<const uint32_t *>(p));
+}
+
+template <bool DYN>
+__global__ void __launch_bounds__(128) gconv_kernel(const GconvArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    const int lane = threadIdx.x & 31;
+    const int warp_g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int rows = DYN ? (*a.count) * a.S * a.S : a.rows;
+    const int r0 = warp_g * 16;
+    if (r0 >= rows) return;
+    const int gq = lane >> 2, tq = lane & 3;  // mma groupID / threadID_in_group
+    // the two output rows this lane's A fragments cover: r0 + gq and r0 + gq + 8
+    int src[2][9];  // h1 row of each tap (or -1: zero padding / past the end)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int r = r0 + gq + 8 * h;
+#pragma unroll
+        for (int t = 0; t < 9; ++t) src[h][t] = -1;
+        if (r < rows) {
+            if (DYN) {
+                const int ss = a.S * a.S;
+                const int p = r / ss, j = r - p * ss, py = j / a.S, px = j - py * a.S;
+                const int base = p * a.hs * a.hs;
+#pragma unroll
+                for (int t = 0; t < 9; ++t) src[h][t] = base + (py + t / 3) * a.hs + (px + t % 3);
+            } else {
+                const int hw = a.Ho * a.Wo;
+                const int n = r / hw, j = r - n * hw, oy = j / a.Wo, ox = j - oy * a.Wo;
+#pragma unroll
+                for (int t = 0; t < 9; ++t) {
+                    const int iy = a.stride * oy + t / 3 - 1, ix = a.stride * ox + t % 3 - 1;
+                    if (iy >= 0 && iy < a.H && ix >= 0 && ix < a.W) src[h][t] = (n * a.H + iy) * a.W + ix;
+                }
+            }
+        }
+    }
+    const int groups = a.C / 16;
+    for (int g = 0; g < groups; ++g) {
+        // channel g*16 + k lives at chunk g/4, offset (g%4)*16 + k
+        const __nv_bfloat16 *hb = a.h1 + (int64_t)(g >> 2) * a.h1_rows * 64 + (g & 3) * 16;
+        float acc[2][4];
+#pragma unroll
+        for (int nh = 0; nh < 2; ++nh)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[nh][e] = 0.f;
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+            uint32_t af[4];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int s = src[h][t];
+                const __nv_bfloat16 *p = hb + (int64_t)(s < 0 ? 0 : s) * 64 + 2 * tq;
+                af[h] = s < 0 ? 0u : ldg_u32(p);          // k = 2tq, 2tq+1
+                af[2 + h] = s < 0 ? 0u : ldg_u32(p + 8);  // k = 2tq+8, 2tq+9
+            }
+#pragma unroll
+            for (int nh = 0; nh < 2; ++nh) {
+                const __nv_bfloat16 *wp = a.wb + ((int64_t)(g * 16 + nh * 8 + gq) * 9 + t) * 16 + 2 * tq;
+                const uint32_t b0 = ldg_u32(wp), b1 = ldg_u32(wp + 8);
+                asm volatile(
+                    "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                    "{%0,%1,%2,%3};"
+                    : "+f"(acc[nh][0]), "+f"(acc[nh][1]), "+f"(acc[nh][2]), "+f"(acc[nh][3])
+                    : "r"(af[0]), "r"(af[1]), "r"(af[2]), "r"(af[3]), "r"(b0), "r"(b1));
+            }
+        }
+        // epilogue: rows r0 + gq (+8), channels g*16 + nh*8 + 2tq (+1)
+#pragma unroll
+        for (int nh = 0; nh < 2; ++nh) {
+            const int c = g * 16 + nh * 8 + 2 * tq;
+            const float b0 = __ldg(a.bias + c), b1 = __ldg(a.bias + c + 1);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int r = r0 + gq + 8 * h;
+                if (r < rows) {
+                    const __nv_bfloat162 v =
+                        __floats2bfloat162_rn(fmaxf(acc[nh][2 * h] + b0, 0.f), fmaxf(acc[nh][2 * h + 1] + b1, 0.f));
+                    *reinterpret_cast<__nv_bfloat162 *>(a.h2 + (int64_t)r * a.C + c) = v;
+                }
+            }
+        }
+    }
+}
+
+// One CTA (256 threads) per image.  Dynamic: the image's patches are the contiguous
+// idx range of its cell ids (ascending); only in-image output pixels are pooled.
+// Pooling: thread (slice rs, vector v) sums 8 channels (one 16-B load per row) of
+// rows rs, rs + RS, ... in order; the RS slice partials are then added in slice
+// order per channel -- a fixed summation tree (deterministic).
+constexpr int kSeThreads = 256;
+__global__ void __launch_bounds__(kSeThreads) se_kernel(const SeArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    extern __shared__ float sm[];
+    const int cv = a.C / 8;
+    const int RS = cv >= kSeThreads ? 1 : kSeThreads / cv;  // row slices
+    float *part = sm;                  // [RS][C]
+    float *pooled = sm + RS * a.C;     // [C]
+    float *z = pooled + a.C;           // [w_se]
+    __shared__ int range[2];
+    __shared__ int npix_s[kSeThreads];
+    const int n = blockIdx.x;
+    int t0 = 0, t1 = 0;
+    if (a.count) {
+        if (threadIdx.x == 0) {
+            const int cnt = *a.count;
+            int lo = 0, hi = cnt;  // first patch of image n
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (a.idx[mid] / a.G < n) lo = mid + 1; else hi = mid;
+            }
+            int lo2 = lo, hi2 = cnt;  // first patch of image n + 1
+            while (lo2 < hi2) {
+                const int mid = (lo2 + hi2) >> 1;
+                if (a.idx[mid] / a.G < n + 1) lo2 = mid + 1; else hi2 = mid;
+            }
+            range[0] = lo;
+            range[1] = lo2;
+        }
+        __syncthreads();
+        t0 = range[0];
+        t1 = range[1];
+        if (t0 == t1) return;  // no active cell: the block leaves the image untouched
+    }
+    const int ss = a.S * a.S;
+    const int64_t row0 = a.count ? (int64_t)t0 * ss : (int64_t)n * a.HW;
+    const int nrows = a.count ? (t1 - t0) * ss : a.HW;
+    const int rs = threadIdx.x / cv, v = threadIdx.x - rs * cv;
+    int np = 0;
+    if (rs < RS) {
+        for (int vv = v; vv < cv; vv += (RS == 1 ? kSeThreads : cv)) {
+            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            int cntp = 0;
+            for (int r = rs; r < nrows; r += RS) {
+                if (a.count) {  // clipped edge cells: only in-image pixels
+                    const int t = t0 + r / ss, j = r - (r / ss) * ss;
+                    const int cell = __ldg(a.idx + t) - n * a.G;
+                    const int gy = cell / a.Gw, gx = cell - gy * a.Gw;
+                    const int py = j / a.S, px = j - py * a.S;
+                    if (gy * a.S + py >= a.H || gx * a.S + px >= a.W) continue;
+                }
+                const uint4 q = __ldg(reinterpret_cast<const uint4 *>(a.h2 + (row0 + r) * a.C) + vv);
+                const uint32_t u[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    acc[2 * e] += __uint_as_float(u[e] << 16);
+                    acc[2 * e + 1] += __uint_as_float(u[e] & 0xffff0000u);
+                }
+                ++cntp;
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) part[rs * a.C + 8 * vv + e] = acc[e];
+            np = cntp;
+        }
+    }
+    npix_s[threadIdx.x] = (rs < RS && v == 0) ? np : 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {  // pixels pooled: the slices of vector 0, in order
+        int t = 0;
+        for (int k = 0; k < RS; ++k) t += npix_s[k * cv];
+        range[0] = t;
+    }
+    __syncthreads();
+    const float inv = 1.f / (float)range[0];
+    for (int c = threadIdx.x; c < a.C; c += blockDim.x) {
+        float s = 0.f;
+        for (int k = 0; k < RS; ++k) s += part[k * a.C + c];
+        pooled[c] = s * inv;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < a.w_se; j += blockDim.x) {
+        float s = a.b1[j];
+        for (int c = 0; c < a.C; ++c) s = fmaf(a.w1[(int64_t)j * a.C + c], pooled[c], s);
+        z[j] = fmaxf(s, 0.f);
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < a.C; c += blockDim.x) {
+        float s = a.b2[c];
+        for (int j = 0; j < a.w_se; ++j) s = fmaf(a.w2[(int64_t)c * a.w_se + j], z[j], s);
+        a.scale[(int64_t)n * a.C + c] = 1.f / (1.f + __expf(-s));
+    }
+}
+
+// h2[row][:] *= scale[image(row)][:] (bf16 RNE), 8 channels per thread
+__global__ void __launch_bounds__(256) se_apply_kernel(__nv_bfloat16 *h2, const float *scale, const int32_t *idx,
+                                                       const int32_t *count, int rows_dense, int C, int S, int G,
+                                                       int HW) {
+    pdl_wait();
+    pdl_trigger();
+    const int ss = S * S;
+    const int rows = count ? (*count) * ss : rows_dense;
+    const int cv = C / 8;
+    const int64_t total = (int64_t)rows * cv;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(i / cv), v = (int)(i - (int64_t)r * cv);
+        const int n = count ? __ldg(idx + r / ss) / G : r / HW;
+        uint4 *p = reinterpret_cast<uint4 *>(h2 + (int64_t)r * C) + v;
+        uint4 q = *p;
+        uint32_t u[4] = {q.x, q.y, q.z, q.w};
+        const float *sc = scale + (int64_t)n * C + 8 * v;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float lo = __uint_as_float(u[e] << 16) * sc[2 * e];
+            const float hi = __uint_as_float(u[e] & 0xffff0000u) * sc[2 * e + 1];
+            const __nv_bfloat162 b = __floats2bfloat162_rn(lo, hi);
+            u[e] = *reinterpret_cast<const uint32_t *>(&b);
+        }
+        *p = make_uint4(u[0], u[1], u[2], u[3]);
+    }
+}
+
+// RegNet stem: x_pad [n][2h][2w + 8][8] (image at column offset 4, channels 3..7 zero),
+// w [64][3][3][8] OHWI, b [64] -> y [n][h][w][64]; one thread per output pixel.
+__global__ void __launch_bounds__(128) regnet_stem_kernel(const __nv_bfloat16 *__restrict__ x,
+                                                          const __nv_bfloat16 *__restrict__ w,
+                                                          const float *__restrict__ b, __nv_bfloat16 *__restrict__ y,
+                                                          int n_img, int h, int wo, int co_real) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ float ws[27][64];
+    __shared__ float bs[64];
+    for (int i = threadIdx.x; i < 27 * 64; i += blockDim.x) {
+        const int o = i % 64, k = i / 64, t = k / 3, c = k % 3;
+        ws[k][o] = __bfloat162float(w[(o * 9 + t) * 8 + c]);
+    }
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) bs[i] = b[i];
+    __syncthreads();
+    const int hi = 2 * h, wp = 2 * wo + 8;
+    const int64_t total = (int64_t)n_img * h * wo;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < total; p += (int64_t)gridDim.x * blockDim.x) {
+        const int ox = (int)(p % wo);
+        const int64_t q = p / wo;
+        const int oy = (int)(q % h), n = (int)(q / h);
+        float xin[27];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+            const int iy = 2 * oy + t / 3 - 1, ix = 2 * ox + t % 3 - 1;  // padded column ix + 4
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (iy >= 0 && iy < hi) v = __ldg(reinterpret_cast<const uint4 *>(x + (((int64_t)n * hi + iy) * wp + ix + 4) * 8));
+            xin[3 * t] = __uint_as_float(v.x << 16);
+            xin[3 * t + 1] = __uint_as_float(v.x & 0xffff0000u);
+            xin[3 * t + 2] = __uint_as_float(v.y << 16);
+        }
+        uint4 out[8];
+        uint32_t *o32 = reinterpret_cast<uint32_t *>(out);
+#pragma unroll 4
+        for (int o = 0; o < 64; o += 2) {
+            float s0 = o < co_real ? bs[o] : 0.f, s1 = o < co_real ? bs[o + 1] : 0.f;
+            if (o < co_real) {
+#pragma unroll
+                for (int k = 0; k < 27; ++k) {
+                    s0 = fmaf(ws[k][o], xin[k], s0);
+                    s1 = fmaf(ws[k][o + 1], xin[k], s1);
+                }
+            }
+            const __nv_bfloat162 v = __floats2bfloat162_rn(fmaxf(s0, 0.f), fmaxf(s1, 0.f));
+            o32[o / 2] = *reinterpret_cast<const uint32_t *>(&v);
+        }
+        uint4 *yp = reinterpret_cast<uint4 *>(y + p * 64);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) yp[k] = out[k];
+    }
+}
+
+// ----------------------------------------------------------------- host ----
+
+cudaError_t launch_gconv(bool dyn, const GconvArgs &a, int max_rows, int num_sms, cudaStream_t st) {
+    (void)num_sms;
+    const long warps = ((long)max_rows + 15) / 16;
+    const long grid = (warps + 3) / 4;
+    if (grid == 0) return cudaSuccess;
+    return dyn ? launch_k(gconv_kernel<true>, dim3((unsigned)grid), dim3(128), 0, st, a)
+               : launch_k(gconv_kernel<false>, dim3((unsigned)grid), dim3(128), 0, st, a);
+}
+
+cudaError_t launch_se(const SeArgs &a, cudaStream_t st) {
+    if (a.n_img == 0) return cudaSuccess;
+    const int cv = a.C / 8;
+    const int RS = cv >= kSeThreads ? 1 : kSeThreads / cv;
+    const size_t smem = (size_t)((RS + 1) * a.C + a.w_se) * 4;
+    static size_t configured = 48 * 1024;
+    if (smem > configured) {
+        if (cudaFuncSetAttribute(se_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return cudaErrorInvalidValue;
+        configured = smem;
+    }
+    return launch_k(se_kernel, dim3((unsigned)a.n_img), dim3(kSeThreads), smem, st, a);
+}
+
+cudaError_t launch_se_apply(__nv_bfloat16 *h2, const float *scale, const int32_t *idx, const int32_t *count,
+                            int max_rows, int C, int S, int G, int HW, int num_sms, cudaStream_t st) {
+    const long total = (long)max_rows * (C / 8);
+    long grid = (total + 255) / 256;
+    if (grid > 8L * num_sms) grid = 8L * num_sms;
+    if (grid == 0) return cudaSuccess;
+    return launch_k(se_apply_kernel, dim3((unsigned)grid), dim3(256), 0, st, h2, scale, idx, count, max_rows, C, S,
+                    G, HW);
+}
+
+cudaError_t launch_regnet_stem(const void *x, const void *w, const float *b, void *y, int n_img, int h, int wo,
+                               int co_real, int num_sms, cudaStream_t st) {
+    const long total = (long)n_img * h * wo;
+    long grid = (total + 127) / 128;
+    if (grid > 16L * num_sms) grid = 16L * num_sms;
+    if (grid == 0) return cudaSuccess;
+    return launch_k(regnet_stem_kernel, dim3((unsigned)grid), dim3(128), 0, st, static_cast<const __nv_bfloat16 *>(x),
+                    static_cast<const __nv_bfloat16 *>(w), b, static_cast<__nv_bfloat16 *>(y), n_img, h, wo, co_real);
+}
+
+}  // namespace lasnet

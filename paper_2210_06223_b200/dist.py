@@ -61,3 +61,31 @@ def gather_over_ranks(value: float, device="cpu"):
 def throughput(images_per_rank: int, world: int, steps: int, max_total_ms: float) -> float:
     """Whole-job images/s of a weak-scaling run: all ranks' images over the slowest rank's time."""
     return images_per_rank * world * steps / (max_total_ms / 1e3)
+
+
+def exchange_logits(logits_local: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """The network's exchange step: every rank's logits [n_local, classes]
+    gathered in rank order into [world * n_local, classes] (all_gather_into_tensor;
+    NCCL on GPUs, gloo in the CPU tests).  Single process: a copy."""
+    world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+    if out is None:
+        out = torch.empty((world * logits_local.shape[0],) + tuple(logits_local.shape[1:]), dtype=logits_local.dtype,
+                          device=logits_local.device)
+    if world > 1:
+        if logits_local.is_cuda:
+            dist.all_gather_into_tensor(out, logits_local)
+        else:  # gloo has no all_gather_into_tensor
+            parts = [torch.empty_like(logits_local) for _ in range(world)]
+            dist.all_gather(parts, logits_local)
+            torch.cat(parts, out=out)
+    else:
+        out.copy_(logits_local)
+    return out
+
+
+def active_counts(counts_local, device="cpu"):
+    """Per-block active-cell counts summed over the ranks (int64)."""
+    t = torch.tensor([int(c) for c in counts_local], dtype=torch.int64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t)
+    return [int(v) for v in t.tolist()]

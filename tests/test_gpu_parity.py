@@ -712,3 +712,21 @@ def xin_img(x, hw):
 def _block_order(key):
     si, b = key[1:].split("_")
     return int(si), 0 if b == "proj" else int(b[1:])
+
+
+def test_network_batch_sharding_is_bitwise_invariant():
+    """sharding the global batch over ranks changes nothing -- the logits
+    of two half-batch networks (what two ranks compute before the all-gather) equal
+    the whole-batch network's bit for bit, with the same masker biases."""
+    wts = synth.make_lasnet_weights(seed=9)
+    x = synth.make_image_batch(4, 64, seed=10).cuda()
+    full = L.LASResNet(4, wts, hw=64)
+    full.forward(synth.make_image_batch(4, 64, seed=11).cuda(), calibrate_r=0.5)
+    lg_full = full.forward(x).clone()
+    parts = []
+    for lo, hi in ((0, 2), (2, 4)):
+        half = L.LASResNet(2, wts, hw=64)
+        for a, b in zip(half.blocks(), full.blocks()):
+            a.bm = b.bm
+        parts.append(half.forward(x[lo:hi].contiguous()).clone())
+    assert torch.equal(torch.cat(parts), lg_full)
