@@ -799,6 +799,57 @@ def coco_measure(args, rank):
     return out
 
 
+# ---------------------------------------------------------------- config 1 ----
+
+def config1_measure(args):
+    """BASELINE configs[0] / SURVEY C1: one block, N = 1, 14x14x256, c_mid 64, S = 2,
+    fp32 (the CUDA-core path), 25 of 49 cells active (masker bias calibrated on the
+    input itself, so exactly 25 cells pass); CUDA-graph replays, inputs L2-resident.
+    Latency-bound by construction: its roofline is ~0.29 us (21.7 MFLOP at the fp32
+    SIMT peak)."""
+    import synth
+    import paper_2210_06223_b200 as L
+
+    n, h, w, c, cm, s = 1, 14, 14, 256, 64, 2
+    x = synth.make_x(n, h, w, c, seed=0, dtype="f32").cuda()
+    blk = L.DynBlock(L.BlockShape(n, h, w, c, cm, s, torch.float32),
+                     synth.make_block_weights(c, cm, c, seed=1, dtype="f32"), synth.make_masker_weights(c, seed=2), 0.0)
+    blk.calibrate_bias(x, 25 / 49)
+    y, y2 = x.clone(), torch.empty_like(x)
+    blk.forward(y)
+    torch.cuda.synchronize()
+    active = int(blk.count.item())
+    g = blk.capture(y)
+    stream = torch.cuda.current_stream()
+    steps = 200
+
+    def timed(fn):
+        for _ in range(10):
+            fn()
+        a, b = ev_pair()
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(steps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / steps * 1e3
+
+    dyn_us = timed(g.replay)
+    gd = torch.cuda.CUDAGraph()
+    blk.dense(x, y2)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(gd):
+        blk.dense(x, y2)
+    dense_us = timed(gd.replay)
+    return {"workload": "BASELINE configs[0]: one bottleneck block, N=1, 14x14x256, c_mid 64, S=2, fp32 (CUDA cores)",
+            "active_cells": active, "cells": 49, "us_per_block": round(dyn_us, 2), "dense_us": round(dense_us, 2),
+            "speedup_vs_dense": round(dense_us / dyn_us, 3), "roofline_us": 0.29,
+            "roofline_frac": round(0.29 / dyn_us, 4), "tolerance": "1e-5 max-abs-rel (fp32 path, tests)",
+            "timing": f"{steps} CUDA-graph replays in one event pair, inputs L2-resident; latency-bound by "
+                      "construction (a chain of dependent launches)"}
+
+
 # ------------------------------------------------------------ LAS-RegNetY ----
 
 def regnet_measure(args, rank, world):
@@ -876,6 +927,7 @@ def run_lasnet(args):
     sweep = None if args.no_sweep else block_sweep(args, rank, hbm, tfl)
     coco = None if args.no_coco else coco_measure(args, rank)
     regnet = None if args.no_regnet else regnet_measure(args, rank, world)
+    c1 = None if args.no_block else config1_measure(args)
     clocks = sampler.stop()
     if blk is not None:
         b_tot = sum(blk["step_ms"])
@@ -966,6 +1018,8 @@ def run_lasnet(args):
             line["coco_backbone"] = coco
         if regnet is not None:
             line["regnet"] = regnet
+        if c1 is not None:
+            line["config1"] = c1
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_net(net["x_cpu"], net["weights"], net["net"].oracle_meta(),
                                                     args.cpu_budget)

@@ -268,7 +268,10 @@ int32_t lasnet_choose_schedule(const lasnet_block_desc *desc, double r);
  * steps -- masker + compaction, gather + conv1 on the (s+2)^2 halos, the grouped
  * 3x3 on the gathered windows, SE over the active pixels, conv3 + scatter-add in
  * place; y == x runs in place, else x is copied to y first; inactive pixels keep
- * x; mask nullable.  Static (wm == NULL): every pixel, stride 1 or 2, y
+ * x; mask nullable.  schedule (dynamic only): LASNET_SCHED_MASKER_SEPARATE
+ * (masker + compaction, conv1 on the halos) or LASNET_SCHED_MASKER_FUSED (the
+ * paper's Table-1 schedule: conv1 dense with the masker partials, one launch
+ * deciding + gathering the h1 windows), as lasnet_block_forward.  Static (wm == NULL): every pixel, stride 1 or 2, y
  * must not overlap x.  h1, h2, h2*s and y are stored bf16 (RNE).
  *   w      weights; se_* fp32 [w_se][c_mid], [w_se], [c_mid][w_se], [c_mid]
  *   ws     lasnet_regnet_workspace_bytes(desc, dynamic) bytes, ALL ZERO before the
@@ -283,8 +286,8 @@ typedef struct {
     const void *wd; const float *bd;          /* projection [c_out][c_in], or NULL       */
 } lasnet_regnet_weights;
 lasnet_status lasnet_regnet_block(const lasnet_block_desc *desc, const lasnet_regnet_weights *wts, const void *x,
-                                  void *y, const float *wm, float bm, uint8_t *mask, int32_t *idx, int32_t *count,
-                                  void *ws, size_t ws_bytes, lasnet_stream_t stream);
+                                  void *y, const float *wm, float bm, int32_t schedule, uint8_t *mask, int32_t *idx,
+                                  int32_t *count, void *ws, size_t ws_bytes, lasnet_stream_t stream);
 size_t lasnet_regnet_workspace_bytes(const lasnet_block_desc *desc, int32_t dynamic);
 /* RegNet stem: 3x3 stride-2 conv, c_real (<= 64, even) output channels + bias +
  * ReLU, channels c_real..63 written 0: x_pad [n][2h][2w + 8][8] (as lasnet_stem),

@@ -134,7 +134,7 @@ def load(path: str = LIB_PATH):
                                            ctypes.POINTER(ctypes.c_double), i32, ctypes.POINTER(i32)]
     lib.lasnet_predict_latency.restype = ctypes.c_double
     RW = ctypes.POINTER(RegnetWeights)
-    lib.lasnet_regnet_block.argtypes = [D, RW, vp, vp, vp, ctypes.c_float, vp, vp, vp, vp, sz, vp]
+    lib.lasnet_regnet_block.argtypes = [D, RW, vp, vp, vp, ctypes.c_float, i32, vp, vp, vp, vp, sz, vp]
     lib.lasnet_regnet_block.restype = ctypes.c_int
     lib.lasnet_regnet_workspace_bytes.argtypes = [D, i32]
     lib.lasnet_regnet_workspace_bytes.restype = sz

@@ -1152,10 +1152,11 @@ int32_t lasnet_choose_schedule(const lasnet_block_desc *d, double r) {
 namespace {
 
 struct RegWs {
-    void *sync, *mask, *h1, *h2, *scale, *xs, *w3d, *b3d;
+    void *sync, *mask, *h1, *h2, *scale, *xs, *w3d, *b3d, *mpart, *h1d;
 };
 
-size_t regnet_ws(const lasnet_block_desc *d, bool dyn, uint8_t *base, RegWs *o) {
+// dyn: 0 static, 1 dynamic masker-separate, 2 dynamic masker-fused
+size_t regnet_ws(const lasnet_block_desc *d, int dyn, uint8_t *base, RegWs *o) {
     const size_t e = 2;
     const int S = d->s, st = d->stride;
     const long ncells = (long)d->n * ((d->h + S - 1) / S) * ((d->w + S - 1) / S);
@@ -1163,8 +1164,14 @@ size_t regnet_ws(const lasnet_block_desc *d, bool dyn, uint8_t *base, RegWs *o) 
     Carve cv{base};
     RegWs r{};
     if (dyn) {
-        r.sync = cv.take(mask_compact_workspace_bytes(ncells));
+        // control words first (zero contract): the separate masker's or the fused decide's
+        const size_t sync = dyn == 2 ? decide_sync_bytes((int)ncells, num_sms()) : mask_compact_workspace_bytes(ncells);
+        r.sync = cv.take(sync);
         r.mask = cv.take((size_t)ncells);
+        if (dyn == 2) {
+            r.mpart = cv.take(pxo * 16);
+            r.h1d = cv.take(pxo * d->c_mid * e);
+        }
         r.h1 = cv.take((size_t)ncells * (S + 2) * (S + 2) * d->c_mid * e);
         r.h2 = cv.take((size_t)ncells * S * S * d->c_mid * e);
     } else {
@@ -1202,13 +1209,17 @@ extern "C" {
 
 size_t lasnet_regnet_workspace_bytes(const lasnet_block_desc *d, int32_t dynamic) {
     if (check_desc(d) != LASNET_OK) return 0;
-    return regnet_ws(d, dynamic != 0, nullptr, nullptr);
+    if (!dynamic) return regnet_ws(d, 0, nullptr, nullptr);
+    const size_t a = regnet_ws(d, 1, nullptr, nullptr), b = regnet_ws(d, 2, nullptr, nullptr);
+    return a > b ? a : b;  // either schedule
 }
 
 lasnet_status lasnet_regnet_block(const lasnet_block_desc *d, const lasnet_regnet_weights *w, const void *x, void *y,
-                                  const float *wm, float bm, uint8_t *mask, int32_t *idx, int32_t *count, void *ws,
-                                  size_t ws_bytes, lasnet_stream_t stream) {
+                                  const float *wm, float bm, int32_t schedule, uint8_t *mask, int32_t *idx,
+                                  int32_t *count, void *ws, size_t ws_bytes, lasnet_stream_t stream) {
     const bool dyn = wm != nullptr;
+    if (dyn && schedule != LASNET_SCHED_MASKER_SEPARATE && schedule != LASNET_SCHED_MASKER_FUSED)
+        return LASNET_ERR_DOMAIN;
     lasnet_status s = regnet_check(d, w, dyn);
     if (s != LASNET_OK) return s;
     if (!x || !y || (dyn && (!idx || !count))) return LASNET_ERR_NULL;
@@ -1227,13 +1238,14 @@ lasnet_status lasnet_regnet_block(const lasnet_block_desc *d, const lasnet_regne
             if (a < b + yb && b < a + xb) return LASNET_ERR_ALIAS;  // static: out of place
         }
     }
-    if (!ws || ws_bytes < regnet_ws(d, dyn, nullptr, nullptr)) return LASNET_ERR_WORKSPACE;
+    const int mode = !dyn ? 0 : (schedule == LASNET_SCHED_MASKER_FUSED ? 2 : 1);
+    if (!ws || ws_bytes < regnet_ws(d, mode, nullptr, nullptr)) return LASNET_ERR_WORKSPACE;
     g_last_launches = 0;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (d->n == 0) return dyn ? (cudaMemsetAsync(count, 0, 4, st) == cudaSuccess ? LASNET_OK : LASNET_ERR_CUDA)
                               : LASNET_OK;
     RegWs r;
-    regnet_ws(d, dyn, static_cast<uint8_t *>(ws), &r);
+    regnet_ws(d, mode, static_cast<uint8_t *>(ws), &r);
     const int gh = (d->h + S - 1) / S, gw = (d->w + S - 1) / S, G = gh * gw;
     const int ncells = d->n * G;
     int launches = 0;
@@ -1252,22 +1264,44 @@ lasnet_status lasnet_regnet_block(const lasnet_block_desc *d, const lasnet_regne
         uint8_t *m = mask ? mask : static_cast<uint8_t *>(r.mask);
         if (x != y && cudaMemcpyAsync(y, x, (size_t)pxi * d->c_in * 2, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
             return LASNET_ERR_CUDA;
-        {  // steps 1+2: masker + compaction
-            KernelEvents ev(st, "mask_compact");
-            if (launch_mask_compact(1, x, wm, bm, d->n, d->h, d->w, d->c_in, S, m, nullptr, idx, count, r.sync, st) !=
-                cudaSuccess)
+        const int hs = S + 2;
+        if (mode == 1) {
+            {  // steps 1+2: masker + compaction
+                KernelEvents ev(st, "mask_compact");
+                if (launch_mask_compact(1, x, wm, bm, d->n, d->h, d->w, d->c_in, S, m, nullptr, idx, count, r.sync,
+                                        st) != cudaSuccess)
+                    return LASNET_ERR_CUDA;
+                ++launches;
+            }
+            // step 3: gather + conv1 over the (S+2)^2 halo of every active patch
+            ConvArgs a = base_args(d);
+            a.idx = idx; a.count = count;
+            a.a_src = x; a.w = w->wa; a.bias = w->ba; a.out = r.h1; a.resid = nullptr;
+            a.K = d->c_in; a.N = C; a.a_ld = d->c_in; a.out_ld = C;
+            if (run_conv(d, CONV1_DYN, a, ncells * hs * hs, x, y, r.h1, r.h2, ncells, st) != cudaSuccess)
                 return LASNET_ERR_CUDA;
             ++launches;
+        } else {
+            // the paper's Table-1 schedule: conv1 dense over x with the
+            // masker partials, then one launch decides the cells, writes the ids and gathers the
+            // h1 halo windows of the active patches
+            ConvArgs a = base_args(d);
+            a.m_dense = (int)pxo;
+            a.a_src = x; a.w = w->wa; a.bias = w->ba; a.out = r.h1d;
+            a.K = d->c_in; a.N = C; a.a_ld = d->c_in; a.out_ld = C;
+            a.wm = wm; a.mpart = static_cast<float4 *>(r.mpart);
+            if (run_conv(d, CONV1_DENSE_MASK, a, (int)pxo, x, y, r.h1d, nullptr, 0, st) != cudaSuccess)
+                return LASNET_ERR_CUDA;
+            int nd = 0;
+            {
+                KernelEvents ev(st, "decide+gather");
+                if (launch_decide_gather(static_cast<const float4 *>(r.mpart), x, wm, bm, d->n, d->h, d->w, d->c_in, S,
+                                         m, idx, count, r.sync, r.h1d, r.h1, C, ncells, num_sms(), st, &nd) !=
+                    cudaSuccess)
+                    return LASNET_ERR_CUDA;
+            }
+            launches += 1 + nd;
         }
-        // step 3: gather + conv1 over the (S+2)^2 halo of every active patch
-        ConvArgs a = base_args(d);
-        a.idx = idx; a.count = count;
-        a.a_src = x; a.w = w->wa; a.bias = w->ba; a.out = r.h1; a.resid = nullptr;
-        a.K = d->c_in; a.N = C; a.a_ld = d->c_in; a.out_ld = C;
-        const int hs = S + 2;
-        if (run_conv(d, CONV1_DYN, a, ncells * hs * hs, x, y, r.h1, r.h2, ncells, st) != cudaSuccess)
-            return LASNET_ERR_CUDA;
-        ++launches;
         // step 4: grouped 3x3 on the windows, then SE pooled over the active pixels (reading R23)
         g.h1 = static_cast<const __nv_bfloat16 *>(r.h1);
         g.h1_rows = (int64_t)ncells * hs * hs;
@@ -1298,6 +1332,7 @@ lasnet_status lasnet_regnet_block(const lasnet_block_desc *d, const lasnet_regne
         g_last_launches = launches + 4;
         return LASNET_OK;
     }
+    (void)schedule;
     // static Y-block (every pixel; identity or projection, stride 1 or 2)
     lasnet_block_desc di = *d;
     di.h = Hi; di.w = Wi; di.stride = 1;
@@ -1309,7 +1344,7 @@ lasnet_status lasnet_regnet_block(const lasnet_block_desc *d, const lasnet_regne
     g.h1 = static_cast<const __nv_bfloat16 *>(r.h1);
     g.h1_rows = pxi;
     g.rows = (int)pxo;
-    g.H = Hi; g.W = Wi; g.Ho = d->h; g.Wo = d->w; g.stride = st_;
+    g.H = Hi; g.W = Wi; g.Ho = d->h; g.Wo = d->w; g.stride = st_; g.n_img = d->n;
     {
         KernelEvents ev(st, "gconv_dense");
         if (launch_gconv(false, g, (int)pxo, num_sms(), st) != cudaSuccess) return LASNET_ERR_CUDA;

@@ -31,83 +31,145 @@ __device__ __forceinline__ uint32_t ldg_u32(const __nv_bfloat16 *p) {
     return __ldg(reinterpret_cast<const uint32_t *>(p));
 }
 
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Grouped 3x3, one CTA (8 warps) per tile of up to 128 output rows.  Per 64-channel
+// chunk (4 groups) the tile's input rows are staged in shared memory with cp.async
+// (16-B pieces XOR-swizzled by row, zero-filled outside the image) together with the
+// chunk's weights; each warp then runs 16 output rows x 4 groups x 9 taps x 2
+// halves of mma.sync m16n8k16, its A fragments loaded by ldmatrix.x4 from the
+// tap-shifted input rows.  Dynamic: a tile is upt whole patches, whose (S+2)^2
+// windows are one contiguous range of gathered rows; dense: a tile is trows whole
+// output rows of one image, staged with their halo (stride 1 or 2, padding 1).
+constexpr int kGcThreads = 256;
+constexpr int kGcMaxIn = 1280;  // staged input rows per chunk (160 KB)
+
 template <bool DYN>
-__global__ void __launch_bounds__(128) gconv_kernel(const GconvArgs a) {
+__global__ void __launch_bounds__(kGcThreads, 1) gconv_kernel(const GconvArgs a) {
     pdl_wait();
     pdl_trigger();
-    const int lane = threadIdx.x & 31;
-    const int warp_g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int rows = DYN ? (*a.count) * a.S * a.S : a.rows;
-    const int r0 = warp_g * 16;
-    if (r0 >= rows) return;
-    const int gq = lane >> 2, tq = lane & 3;  // mma groupID / threadID_in_group
-    // the two output rows this lane's A fragments cover: r0 + gq and r0 + gq + 8
-    int src[2][9];  // h1 row of each tap (or -1: zero padding / past the end)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int r = r0 + gq + 8 * h;
-#pragma unroll
-        for (int t = 0; t < 9; ++t) src[h][t] = -1;
+    extern __shared__ __align__(128) uint8_t gsm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gq = lane >> 2, tq = lane & 3;
+    uint8_t *s_in = gsm;                                    // [in_rows][128 B] swizzled
+    __nv_bfloat16 *s_w = reinterpret_cast<__nv_bfloat16 *>(gsm + kGcMaxIn * 128);  // [64][9][16]
+    int *s_src = reinterpret_cast<int *>(gsm + kGcMaxIn * 128 + 64 * 9 * 16 * 2);  // [128][9] staged row per tap
+    // ---- tile geometry ----
+    int rows, in_rows;
+    int64_t out_row0;
+    int64_t in_row0 = 0;  // dynamic: first gathered row of the tile
+    int n0 = 0, oy0 = 0, iy0 = 0, ih = 0, iw = 0;  // dense: image, first output row, staged input box
+    if (DYN) {
+        const int upt = a.upt;
+        const int cnt = *a.count;
+        const int t0 = blockIdx.x * upt;
+        if (t0 >= cnt) return;
+        const int np = min(upt, cnt - t0);
+        rows = np * a.S * a.S;
+        out_row0 = (int64_t)t0 * a.S * a.S;
+        in_row0 = (int64_t)t0 * a.hs * a.hs;
+        in_rows = np * a.hs * a.hs;
+    } else {
+        const int bands = (a.Ho + a.trows - 1) / a.trows;
+        n0 = blockIdx.x / bands;
+        if (n0 >= a.n_img) return;
+        oy0 = (blockIdx.x - n0 * bands) * a.trows;
+        const int nr = min(a.trows, a.Ho - oy0);
+        rows = nr * a.Wo;
+        out_row0 = ((int64_t)n0 * a.Ho + oy0) * a.Wo;
+        iy0 = a.stride * oy0 - 1;
+        ih = a.stride * (nr - 1) + 3;
+        iw = a.stride * (a.Wo - 1) + 3;
+        in_rows = ih * iw;
+    }
+    // staged row of (output row r, tap t)
+    for (int e = threadIdx.x; e < 128 * 9; e += kGcThreads) {
+        const int r = e / 9, t = e - r * 9, dy = t / 3, dx = t - dy * 3;
+        int sr = 0;
         if (r < rows) {
             if (DYN) {
-                const int ss = a.S * a.S;
-                const int p = r / ss, j = r - p * ss, py = j / a.S, px = j - py * a.S;
-                const int base = p * a.hs * a.hs;
-#pragma unroll
-                for (int t = 0; t < 9; ++t) src[h][t] = base + (py + t / 3) * a.hs + (px + t % 3);
+                const int ss = a.S * a.S, p = r / ss, j = r - p * ss, py = j / a.S, px = j - py * a.S;
+                sr = p * a.hs * a.hs + (py + dy) * a.hs + (px + dx);
             } else {
-                const int hw = a.Ho * a.Wo;
-                const int n = r / hw, j = r - n * hw, oy = j / a.Wo, ox = j - oy * a.Wo;
-#pragma unroll
-                for (int t = 0; t < 9; ++t) {
-                    const int iy = a.stride * oy + t / 3 - 1, ix = a.stride * ox + t % 3 - 1;
-                    if (iy >= 0 && iy < a.H && ix >= 0 && ix < a.W) src[h][t] = (n * a.H + iy) * a.W + ix;
-                }
+                const int oy = r / a.Wo, ox = r - oy * a.Wo;
+                sr = (a.stride * oy + dy) * iw + (a.stride * ox + dx);
             }
         }
+        s_src[e] = sr;
     }
-    const int groups = a.C / 16;
-    for (int g = 0; g < groups; ++g) {
-        // channel g*16 + k lives at chunk g/4, offset (g%4)*16 + k
-        const __nv_bfloat16 *hb = a.h1 + (int64_t)(g >> 2) * a.h1_rows * 64 + (g & 3) * 16;
-        float acc[2][4];
+    const int wr0 = warp * 16;  // this warp's first output row of the tile
+    const int groups_total = a.C / 16;
+    for (int ch = 0; ch < a.C / 64; ++ch) {
+        __syncthreads();  // previous chunk's smem reads done (and s_src written)
+        // stage the input rows of this chunk: 8 x 16-B pieces per row, piece k at k ^ (row & 7)
+        const __nv_bfloat16 *src_chunk = a.h1 + (int64_t)ch * a.h1_rows * 64;
+        for (int e = threadIdx.x; e < in_rows * 8; e += kGcThreads) {
+            const int row = e >> 3, k = e & 7;
+            const uint32_t dst = smem_addr(s_in + row * 128 + ((k ^ (row & 7)) << 4));
+            const __nv_bfloat16 *g = src_chunk;
+            uint32_t bytes = 16;
+            if (DYN) {
+                g = src_chunk + (in_row0 + row) * 64 + k * 8;
+            } else {
+                const int yy = iy0 + row / iw, xx = row - (row / iw) * iw - 1;
+                if (yy >= 0 && yy < a.H && xx >= 0 && xx < a.W)
+                    g = src_chunk + (((int64_t)n0 * a.H + yy) * a.W + xx) * 64 + k * 8;
+                else
+                    bytes = 0;  // zero padding
+            }
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(g), "r"(bytes) : "memory");
+        }
+        // the chunk's weights [64 out][9][16]
+        const __nv_bfloat16 *wsrc = a.wb + (int64_t)ch * 64 * 9 * 16;
+        for (int e = threadIdx.x; e < 64 * 9 * 16 / 8; e += kGcThreads)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(s_w + e * 8)), "l"(wsrc + e * 8)
+                         : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        if (wr0 >= rows) continue;
+        // ldmatrix.x4 lane roles: matrix m = lane / 8 (rows 0-7 / 8-15, k 0-7 / 8-15)
+        const int lr = (lane & 7) + ((lane >> 3) & 1) * 8;  // A row of this lane's address
+        const int khalf = lane >> 4;                        // 0: k 0-7, 1: k 8-15
+        for (int gl = 0; gl < 4; ++gl) {
+            const int g = ch * 4 + gl;
+            if (g >= groups_total) break;
+            float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
-        for (int nh = 0; nh < 2; ++nh)
+            for (int t = 0; t < 9; ++t) {
+                const int sr = s_src[(wr0 + lr) * 9 + t];
+                const int piece = (gl * 2 + khalf) ^ (sr & 7);
+                const uint32_t addr = smem_addr(s_in + sr * 128 + (piece << 4));
+                uint32_t af[4];
+                asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(af[0]), "=r"(af[1]), "=r"(af[2]), "=r"(af[3])
+                             : "r"(addr));
 #pragma unroll
-            for (int e = 0; e < 4; ++e) acc[nh][e] = 0.f;
-#pragma unroll
-        for (int t = 0; t < 9; ++t) {
-            uint32_t af[4];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int s = src[h][t];
-                const __nv_bfloat16 *p = hb + (int64_t)(s < 0 ? 0 : s) * 64 + 2 * tq;
-                af[h] = s < 0 ? 0u : ldg_u32(p);          // k = 2tq, 2tq+1
-                af[2 + h] = s < 0 ? 0u : ldg_u32(p + 8);  // k = 2tq+8, 2tq+9
+                for (int nh = 0; nh < 2; ++nh) {
+                    const __nv_bfloat16 *wp = s_w + ((gl * 16 + nh * 8 + gq) * 9 + t) * 16 + 2 * tq;
+                    const uint32_t b0 = *reinterpret_cast<const uint32_t *>(wp);
+                    const uint32_t b1 = *reinterpret_cast<const uint32_t *>(wp + 8);
+                    asm volatile(
+                        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                        "{%0,%1,%2,%3};"
+                        : "+f"(acc[nh][0]), "+f"(acc[nh][1]), "+f"(acc[nh][2]), "+f"(acc[nh][3])
+                        : "r"(af[0]), "r"(af[1]), "r"(af[2]), "r"(af[3]), "r"(b0), "r"(b1));
+                }
             }
 #pragma unroll
             for (int nh = 0; nh < 2; ++nh) {
-                const __nv_bfloat16 *wp = a.wb + ((int64_t)(g * 16 + nh * 8 + gq) * 9 + t) * 16 + 2 * tq;
-                const uint32_t b0 = ldg_u32(wp), b1 = ldg_u32(wp + 8);
-                asm volatile(
-                    "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-                    "{%0,%1,%2,%3};"
-                    : "+f"(acc[nh][0]), "+f"(acc[nh][1]), "+f"(acc[nh][2]), "+f"(acc[nh][3])
-                    : "r"(af[0]), "r"(af[1]), "r"(af[2]), "r"(af[3]), "r"(b0), "r"(b1));
-            }
-        }
-        // epilogue: rows r0 + gq (+8), channels g*16 + nh*8 + 2tq (+1)
+                const int c = g * 16 + nh * 8 + 2 * tq;
+                const float b0 = __ldg(a.bias + c), b1 = __ldg(a.bias + c + 1);
 #pragma unroll
-        for (int nh = 0; nh < 2; ++nh) {
-            const int c = g * 16 + nh * 8 + 2 * tq;
-            const float b0 = __ldg(a.bias + c), b1 = __ldg(a.bias + c + 1);
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int r = r0 + gq + 8 * h;
-                if (r < rows) {
-                    const __nv_bfloat162 v =
-                        __floats2bfloat162_rn(fmaxf(acc[nh][2 * h] + b0, 0.f), fmaxf(acc[nh][2 * h + 1] + b1, 0.f));
-                    *reinterpret_cast<__nv_bfloat162 *>(a.h2 + (int64_t)r * a.C + c) = v;
+                for (int h = 0; h < 2; ++h) {
+                    const int r = wr0 + gq + 8 * h;
+                    if (r < rows) {
+                        const __nv_bfloat162 v = __floats2bfloat162_rn(fmaxf(acc[nh][2 * h] + b0, 0.f),
+                                                                       fmaxf(acc[nh][2 * h + 1] + b1, 0.f));
+                        *reinterpret_cast<__nv_bfloat162 *>(a.h2 + (out_row0 + r) * a.C + c) = v;
+                    }
                 }
             }
         }
@@ -296,13 +358,39 @@ __global__ void __launch_bounds__(128) regnet_stem_kernel(const __nv_bfloat16 *_
 
 // ----------------------------------------------------------------- host ----
 
-cudaError_t launch_gconv(bool dyn, const GconvArgs &a, int max_rows, int num_sms, cudaStream_t st) {
+// Tile geometry of gconv_kernel: dynamic -- upt patches per tile (whole patches of
+// at most 128 output rows); dense -- trows output rows of one image whose staged
+// input box fits kGcMaxIn rows.  Returns the grid size (0: nothing to do, -1: no fit).
+long gconv_tiles(bool dyn, GconvArgs &a, int max_rows) {
+    if (dyn) {
+        a.upt = 128 / (a.S * a.S);
+        if (a.upt < 1 || a.upt * a.hs * a.hs > kGcMaxIn) return -1;
+        const long cap = max_rows / (a.S * a.S);
+        return (cap + a.upt - 1) / a.upt;
+    }
+    a.trows = a.Wo > 128 ? 0 : 128 / a.Wo;
+    if (a.trows > a.Ho) a.trows = a.Ho;
+    while (a.trows > 0 && (a.stride * (a.trows - 1) + 3) * (a.stride * (a.Wo - 1) + 3) > kGcMaxIn) --a.trows;
+    if (a.trows < 1) return -1;
+    return (long)a.n_img * ((a.Ho + a.trows - 1) / a.trows);
+}
+
+cudaError_t launch_gconv(bool dyn, const GconvArgs &a0, int max_rows, int num_sms, cudaStream_t st) {
     (void)num_sms;
-    const long warps = ((long)max_rows + 15) / 16;
-    const long grid = (warps + 3) / 4;
+    GconvArgs a = a0;
+    const long grid = gconv_tiles(dyn, a, max_rows);
+    if (grid < 0) return cudaErrorInvalidValue;
     if (grid == 0) return cudaSuccess;
-    return dyn ? launch_k(gconv_kernel<true>, dim3((unsigned)grid), dim3(128), 0, st, a)
-               : launch_k(gconv_kernel<false>, dim3((unsigned)grid), dim3(128), 0, st, a);
+    const int smem = kGcMaxIn * 128 + 64 * 9 * 16 * 2 + 128 * 9 * 4;
+    static bool configured[2] = {false, false};
+    if (!configured[dyn]) {
+        cudaError_t e = cudaFuncSetAttribute(dyn ? (const void *)gconv_kernel<true> : (const void *)gconv_kernel<false>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        configured[dyn] = true;
+    }
+    return dyn ? launch_k(gconv_kernel<true>, dim3((unsigned)grid), dim3(kGcThreads), smem, st, a)
+               : launch_k(gconv_kernel<false>, dim3((unsigned)grid), dim3(kGcThreads), smem, st, a);
 }
 
 cudaError_t launch_se(const SeArgs &a, cudaStream_t st) {

@@ -18,6 +18,8 @@ struct GconvArgs {
     int rows;                 // dense: output rows (n * Ho * Wo)
     int S, hs;                // dynamic: patch side, window side (S + 2)
     int H, W, Ho, Wo, stride; // dense: input / output dims
+    int n_img;                // dense: images
+    int upt, trows;           // tile geometry (host-computed): patches / output rows per tile
 };
 
 struct SeArgs {

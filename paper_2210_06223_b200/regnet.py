@@ -31,9 +31,10 @@ class RegNetBlock:
     (identity, masker weights given) runs in place; static (first blocks) writes
     self.y."""
 
-    def __init__(self, n, h_in, w_in, c_in, c_out, stride, wts, s=1, dynamic=False, device="cuda"):
+    def __init__(self, n, h_in, w_in, c_in, c_out, stride, wts, s=1, dynamic=False, device="cuda",
+                 schedule=_lib.SCHED_FUSED):
         self.wts = {k: v.to(device).contiguous() for k, v in wts.items()}
-        self.dynamic, self.stride, self.s = dynamic, stride, s
+        self.dynamic, self.stride, self.s, self.schedule = dynamic, stride, s, schedule
         self.h, self.w = h_in // stride, w_in // stride
         c_mid = self.wts["wa"].shape[0]
         self.c_out = c_out
@@ -65,11 +66,11 @@ class RegNetBlock:
         if self.dynamic:
             y = x if y is None else y
             _lib.check("lasnet_regnet_block", lib.lasnet_regnet_block(
-                ctypes.byref(self.desc), ctypes.byref(self.rw), _p(x), _p(y), _p(self.wm), self.bm,
+                ctypes.byref(self.desc), ctypes.byref(self.rw), _p(x), _p(y), _p(self.wm), self.bm, self.schedule,
                 _p(self.mask_buf), _p(self.idx), _p(self.count), _p(self.ws), self.ws.numel(), _stream()))
             return y
         _lib.check("lasnet_regnet_block", lib.lasnet_regnet_block(
-            ctypes.byref(self.desc), ctypes.byref(self.rw), _p(x), _p(self.y), None, 0.0, None, None, None,
+            ctypes.byref(self.desc), ctypes.byref(self.rw), _p(x), _p(self.y), None, 0.0, 0, None, None, None,
             _p(self.ws), self.ws.numel(), _stream()))
         return self.y
 

@@ -41,6 +41,15 @@ def main():
     L.dense_block(x, wts)
     xp = synth.make_x(2, 16, 16, 128, seed=4).cuda()
     L.proj_block(xp, dev(synth.make_proj_weights(128, 64, 256, seed=5)), 2)
+    # LAS-RegNetY: both dynamic schedules (grouped conv, SE) and a static stride-2 first block
+    for sched in (L.SCHED_SEPARATE, L.SCHED_FUSED):
+        rw = synth.make_regnet_block_weights(144, 144, 36, False, seed=11)
+        xr = torch.zeros((2, 14, 14, 192), dtype=torch.bfloat16)
+        xr[..., :144] = synth.make_x(2, 14, 14, 144, seed=12)
+        blk = L.RegNetBlock(2, 14, 14, 192, 192, 1, rw, s=2, dynamic=True, schedule=sched)
+        blk.forward(xr.cuda())
+    rp = synth.make_regnet_block_weights(64, 144, 16, True, seed=13)
+    L.RegNetBlock(2, 16, 16, 64, 192, 2, rp).forward(synth.make_x(2, 16, 16, 64, seed=14).cuda())
     net = L.LASResNet(1, synth.make_lasnet_weights(seed=6), hw=64)
     net.forward(synth.make_image_batch(1, 64, seed=7).cuda())
     torch.cuda.synchronize()

@@ -49,8 +49,9 @@ DYN_CASES = [
 ]
 
 
+@pytest.mark.parametrize("sched", [L.SCHED_SEPARATE, L.SCHED_FUSED])
 @pytest.mark.parametrize("n,h,w,c,w_se,s,r", DYN_CASES)
-def test_regnet_dynamic_block_matches_oracle(n, h, w, c, w_se, s, r):
+def test_regnet_dynamic_block_matches_oracle(n, h, w, c, w_se, s, r, sched):
     x, wts = block_case(n, h, w, c, w_se, seed=h + c + s)
     xd = synth.to_f64(x)
     wm = wts["wm"]
@@ -58,10 +59,11 @@ def test_regnet_dynamic_block_matches_oracle(n, h, w, c, w_se, s, r):
     bm = margin_bias(l0, r)
     m_or, _ = oracle.masker(xd, synth.to_f64(wm), bm, s)
     idx_or, cnt = oracle.compact(m_or)
-    blk = L.RegNetBlock(n, h, w, x.shape[-1], x.shape[-1], 1, wts, s=s, dynamic=True)
+    blk = L.RegNetBlock(n, h, w, x.shape[-1], x.shape[-1], 1, wts, s=s, dynamic=True, schedule=sched)
     blk.bm = bm
-    y = x.cuda()
-    blk.forward(y)
+    for rep in range(2):  # second call: the self-resetting control words
+        y = x.cuda()
+        blk.forward(y)
     torch.cuda.synchronize()
     assert np.array_equal(blk.mask_buf.cpu().numpy(), m_or)
     assert int(blk.count.item()) == cnt and np.array_equal(blk.idx[:cnt].cpu().numpy(), idx_or)

@@ -39,7 +39,7 @@ def test_sanitizer_clean(tool):
     cmd = [SAN, "--tool", tool, "--error-exitcode", "9", "--target-processes", "all"]
     if tool in ("racecheck", "synccheck"):
         cmd += ["--kernel-name", "regex=(masker|compact|decide|maxpool|avgpool|fc_kernel|subsample|add_bias|pack_stem"
-                "|conv_simt)"]
+                "|conv_simt|se_kernel|se_apply|regnet_stem)"]
     cmd += [sys.executable, os.path.join(HERE, "sanitize_run.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500)
     out = r.stdout + r.stderr
