@@ -1152,7 +1152,7 @@ int32_t lasnet_choose_schedule(const lasnet_block_desc *d, double r) {
 namespace {
 
 struct RegWs {
-    void *sync, *mask, *h1, *h2, *scale, *xs, *w3d, *b3d, *mpart, *h1d;
+    void *sync, *mask, *h1, *h2, *scale, *xs, *w3d, *b3d, *mpart, *h1d, *pooled, *z;
 };
 
 // dyn: 0 static, 1 dynamic masker-separate, 2 dynamic masker-fused
@@ -1182,6 +1182,8 @@ size_t regnet_ws(const lasnet_block_desc *d, int dyn, uint8_t *base, RegWs *o) {
         r.b3d = cv.take((size_t)d->c_out * 4);
     }
     r.scale = cv.take((size_t)d->n * d->c_mid * 4);
+    r.pooled = cv.take((size_t)d->n * d->c_mid * 4);
+    r.z = cv.take((size_t)d->n * 2048 * 4);  // w_se <= 2048
     if (o) *o = r;
     return cv.used;
 }
@@ -1192,7 +1194,7 @@ lasnet_status regnet_check(const lasnet_block_desc *d, const lasnet_regnet_weigh
     if (!w || !w->wa || !w->ba || !w->wb || !w->bb || !w->se_w1 || !w->se_b1 || !w->se_w2 || !w->se_b2 || !w->wc ||
         !w->bc)
         return LASNET_ERR_NULL;
-    if (w->w_se <= 0) return LASNET_ERR_SHAPE;
+    if (w->w_se <= 0 || w->w_se > 2048) return LASNET_ERR_SHAPE;
     if (d->dtype != LASNET_BF16) return LASNET_ERR_UNSUPPORTED;
     if (d->c_in % 64 || d->c_mid % 64 || d->c_out % 64 || d->c_mid > 2048 || d->c_out > 2048)
         return LASNET_ERR_UNSUPPORTED;
@@ -1258,6 +1260,8 @@ lasnet_status lasnet_regnet_block(const lasnet_block_desc *d, const lasnet_regne
     se.h2 = static_cast<const __nv_bfloat16 *>(r.h2);
     se.w1 = w->se_w1; se.b1 = w->se_b1; se.w2 = w->se_w2; se.b2 = w->se_b2;
     se.scale = static_cast<float *>(r.scale);
+    se.pooled = static_cast<float *>(r.pooled);
+    se.z = static_cast<float *>(r.z);
     se.C = C; se.w_se = w->w_se; se.n_img = d->n;
     se.S = S; se.H = d->h; se.W = d->w; se.G = G; se.Gw = gw; se.HW = d->h * d->w;
     if (dyn) {
@@ -1329,7 +1333,7 @@ lasnet_status lasnet_regnet_block(const lasnet_block_desc *d, const lasnet_regne
         c3.K = C; c3.N = d->c_out; c3.a_ld = C; c3.out_ld = d->c_out;
         if (run_conv(d, CONV3_DYN, c3, ncells * S * S, y, y, r.h1, r.h2, ncells, st) != cudaSuccess)
             return LASNET_ERR_CUDA;
-        g_last_launches = launches + 4;
+        g_last_launches = launches + 6;  // gconv, SE (pool + two excitation GEMMs), SE apply, conv3
         return LASNET_OK;
     }
     (void)schedule;
@@ -1359,7 +1363,7 @@ lasnet_status lasnet_regnet_block(const lasnet_block_desc *d, const lasnet_regne
                             d->h * d->w, num_sms(), st) != cudaSuccess)
             return LASNET_ERR_CUDA;
     }
-    launches = 4;
+    launches = 6;  // conv1, gconv, SE (pool + two excitation GEMMs), SE apply
     ConvArgs c = base_args(d);
     c.m_dense = (int)pxo;
     c.a_src = r.h2; c.out = y; c.out_ld = d->c_out; c.a_ld = C; c.N = d->c_out;

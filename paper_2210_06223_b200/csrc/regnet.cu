@@ -44,10 +44,10 @@ __device__ __forceinline__ uint32_t smem_addr(const void *p) {
 // windows are one contiguous range of gathered rows; dense: a tile is trows whole
 // output rows of one image, staged with their halo (stride 1 or 2, padding 1).
 constexpr int kGcThreads = 256;
-constexpr int kGcMaxIn = 1280;  // staged input rows per chunk (160 KB)
+constexpr int kGcMaxIn = 576;  // staged input rows per chunk (72 KB: two CTAs per SM)
 
 template <bool DYN>
-__global__ void __launch_bounds__(kGcThreads, 1) gconv_kernel(const GconvArgs a) {
+__global__ void __launch_bounds__(kGcThreads, 2) gconv_kernel(const GconvArgs a) {
     pdl_wait();
     pdl_trigger();
     extern __shared__ __align__(128) uint8_t gsm[];
@@ -189,8 +189,7 @@ __global__ void __launch_bounds__(kSeThreads) se_kernel(const SeArgs a) {
     const int cv = a.C / 8;
     const int RS = cv >= kSeThreads ? 1 : kSeThreads / cv;  // row slices
     float *part = sm;                  // [RS][C]
-    float *pooled = sm + RS * a.C;     // [C]
-    float *z = pooled + a.C;           // [w_se]
+    float *pooled = nullptr, *z = nullptr;
     __shared__ int range[2];
     __shared__ int npix_s[kSeThreads];
     const int n = blockIdx.x;
@@ -259,20 +258,52 @@ __global__ void __launch_bounds__(kSeThreads) se_kernel(const SeArgs a) {
     for (int c = threadIdx.x; c < a.C; c += blockDim.x) {
         float s = 0.f;
         for (int k = 0; k < RS; ++k) s += part[k * a.C + c];
-        pooled[c] = s * inv;
+        a.pooled[(int64_t)n * a.C + c] = s * inv;
     }
-    __syncthreads();
-    for (int j = threadIdx.x; j < a.w_se; j += blockDim.x) {
-        float s = a.b1[j];
-        for (int c = 0; c < a.C; ++c) s = fmaf(a.w1[(int64_t)j * a.C + c], pooled[c], s);
-        z[j] = fmaxf(s, 0.f);
+    (void)pooled;
+    (void)z;
+}
+
+// The excitation of all images at once, two small fp32 GEMMs (se_fc_kernel twice):
+// out[n][j] = act(b[j] + sum_k in[n][k] w[j][k]), act = ReLU (W1) or sigmoid (W2);
+// one CTA per 32 images x 32 outputs, K staged in 64-wide chunks, fixed-order sums.
+// Images without active cells (a dynamic block) are skipped (their scale is unused).
+__global__ void __launch_bounds__(256) se_fc_kernel(const float *__restrict__ in, const float *__restrict__ w,
+                                                    const float *__restrict__ b, float *__restrict__ out, int n_img,
+                                                    int K, int N, int sigmoid_act) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ float sa[32][65], sb[32][65];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int j0 = blockIdx.x * 32, n0 = blockIdx.y * 32;
+    float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+    for (int k0 = 0; k0 < K; k0 += 64) {
+        for (int e = threadIdx.x; e < 32 * 64; e += 256) {
+            const int r = e / 64, kk = e % 64, k = k0 + kk;
+            sa[r][kk] = (n0 + r < n_img && k < K) ? in[(int64_t)(n0 + r) * K + k] : 0.f;
+            sb[r][kk] = (j0 + r < N && k < K) ? w[(int64_t)(j0 + r) * K + k] : 0.f;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int kk = 0; kk < 64; ++kk) {
+            const float a0 = sa[ty][kk], a1 = sa[ty + 16][kk], b0 = sb[tx][kk], b1 = sb[tx + 16][kk];
+            acc[0][0] = fmaf(a0, b0, acc[0][0]);
+            acc[0][1] = fmaf(a0, b1, acc[0][1]);
+            acc[1][0] = fmaf(a1, b0, acc[1][0]);
+            acc[1][1] = fmaf(a1, b1, acc[1][1]);
+        }
+        __syncthreads();
     }
-    __syncthreads();
-    for (int c = threadIdx.x; c < a.C; c += blockDim.x) {
-        float s = a.b2[c];
-        for (int j = 0; j < a.w_se; ++j) s = fmaf(a.w2[(int64_t)c * a.w_se + j], z[j], s);
-        a.scale[(int64_t)n * a.C + c] = 1.f / (1.f + __expf(-s));
-    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+            const int n = n0 + ty + 16 * i, j = j0 + tx + 16 * jj;
+            if (n < n_img && j < N) {
+                const float v = acc[i][jj] + b[j];
+                out[(int64_t)n * N + j] = sigmoid_act ? 1.f / (1.f + __expf(-v)) : fmaxf(v, 0.f);
+            }
+        }
 }
 
 // h2[row][:] *= scale[image(row)][:] (bf16 RNE), 8 channels per thread
@@ -304,55 +335,78 @@ __global__ void __launch_bounds__(256) se_apply_kernel(__nv_bfloat16 *h2, const 
 }
 
 // RegNet stem: x_pad [n][2h][2w + 8][8] (image at column offset 4, channels 3..7 zero),
-// w [64][3][3][8] OHWI, b [64] -> y [n][h][w][64]; one thread per output pixel.
+// w [64][3][3][8] OHWI, b [64] -> y [n][h][w][64]; one thread per PAIR of horizontally
+// adjacent output pixels (every weight read from shared memory feeds two pixels).
 __global__ void __launch_bounds__(128) regnet_stem_kernel(const __nv_bfloat16 *__restrict__ x,
                                                           const __nv_bfloat16 *__restrict__ w,
                                                           const float *__restrict__ b, __nv_bfloat16 *__restrict__ y,
                                                           int n_img, int h, int wo, int co_real) {
     pdl_wait();
     pdl_trigger();
-    __shared__ float ws[27][64];
+    __shared__ float2 ws[27][32];  // (channel 2j, 2j+1) pairs
     __shared__ float bs[64];
     for (int i = threadIdx.x; i < 27 * 64; i += blockDim.x) {
         const int o = i % 64, k = i / 64, t = k / 3, c = k % 3;
-        ws[k][o] = __bfloat162float(w[(o * 9 + t) * 8 + c]);
+        reinterpret_cast<float *>(&ws[k][0])[o] = __bfloat162float(w[(o * 9 + t) * 8 + c]);
     }
     for (int i = threadIdx.x; i < 64; i += blockDim.x) bs[i] = b[i];
     __syncthreads();
     const int hi = 2 * h, wp = 2 * wo + 8;
-    const int64_t total = (int64_t)n_img * h * wo;
+    const int wq = (wo + 1) / 2;  // pixel pairs per row
+    const int64_t total = (int64_t)n_img * h * wq;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < total; p += (int64_t)gridDim.x * blockDim.x) {
-        const int ox = (int)(p % wo);
-        const int64_t q = p / wo;
+        const int oq = (int)(p % wq);
+        const int64_t q = p / wq;
         const int oy = (int)(q % h), n = (int)(q / h);
-        float xin[27];
+        const int ox0 = 2 * oq;
+        const bool two = ox0 + 1 < wo;
+        float xin[2][27];
 #pragma unroll
         for (int t = 0; t < 9; ++t) {
-            const int iy = 2 * oy + t / 3 - 1, ix = 2 * ox + t % 3 - 1;  // padded column ix + 4
-            uint4 v = make_uint4(0, 0, 0, 0);
-            if (iy >= 0 && iy < hi) v = __ldg(reinterpret_cast<const uint4 *>(x + (((int64_t)n * hi + iy) * wp + ix + 4) * 8));
-            xin[3 * t] = __uint_as_float(v.x << 16);
-            xin[3 * t + 1] = __uint_as_float(v.x & 0xffff0000u);
-            xin[3 * t + 2] = __uint_as_float(v.y << 16);
+            const int iy = 2 * oy + t / 3 - 1;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int ix = 2 * (ox0 + u) + t % 3 - 1;  // padded column ix + 4
+                uint4 v = make_uint4(0, 0, 0, 0);
+                if (iy >= 0 && iy < hi && (u == 0 || two))
+                    v = __ldg(reinterpret_cast<const uint4 *>(x + (((int64_t)n * hi + iy) * wp + ix + 4) * 8));
+                xin[u][3 * t] = __uint_as_float(v.x << 16);
+                xin[u][3 * t + 1] = __uint_as_float(v.x & 0xffff0000u);
+                xin[u][3 * t + 2] = __uint_as_float(v.y << 16);
+            }
         }
-        uint4 out[8];
-        uint32_t *o32 = reinterpret_cast<uint32_t *>(out);
-#pragma unroll 4
-        for (int o = 0; o < 64; o += 2) {
-            float s0 = o < co_real ? bs[o] : 0.f, s1 = o < co_real ? bs[o + 1] : 0.f;
+        uint32_t o32[2][32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const int o = 2 * j;
+            float s[2][2];
+            const float bb0 = o < co_real ? bs[o] : 0.f, bb1 = o < co_real ? bs[o + 1] : 0.f;
+            s[0][0] = s[1][0] = bb0;
+            s[0][1] = s[1][1] = bb1;
             if (o < co_real) {
 #pragma unroll
                 for (int k = 0; k < 27; ++k) {
-                    s0 = fmaf(ws[k][o], xin[k], s0);
-                    s1 = fmaf(ws[k][o + 1], xin[k], s1);
+                    const float2 wv = ws[k][j];
+                    s[0][0] = fmaf(wv.x, xin[0][k], s[0][0]);
+                    s[0][1] = fmaf(wv.y, xin[0][k], s[0][1]);
+                    s[1][0] = fmaf(wv.x, xin[1][k], s[1][0]);
+                    s[1][1] = fmaf(wv.y, xin[1][k], s[1][1]);
                 }
             }
-            const __nv_bfloat162 v = __floats2bfloat162_rn(fmaxf(s0, 0.f), fmaxf(s1, 0.f));
-            o32[o / 2] = *reinterpret_cast<const uint32_t *>(&v);
-        }
-        uint4 *yp = reinterpret_cast<uint4 *>(y + p * 64);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) yp[k] = out[k];
+            for (int u = 0; u < 2; ++u) {
+                const __nv_bfloat162 v = __floats2bfloat162_rn(fmaxf(s[u][0], 0.f), fmaxf(s[u][1], 0.f));
+                o32[u][j] = *reinterpret_cast<const uint32_t *>(&v);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            if (u == 1 && !two) break;
+            uint4 *yp = reinterpret_cast<uint4 *>(y + (((int64_t)n * h + oy) * wo + ox0 + u) * 64);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                yp[k] = make_uint4(o32[u][4 * k], o32[u][4 * k + 1], o32[u][4 * k + 2], o32[u][4 * k + 3]);
+        }
     }
 }
 
@@ -364,6 +418,7 @@ __global__ void __launch_bounds__(128) regnet_stem_kernel(const __nv_bfloat16 *_
 long gconv_tiles(bool dyn, GconvArgs &a, int max_rows) {
     if (dyn) {
         a.upt = 128 / (a.S * a.S);
+        while (a.upt > 1 && a.upt * a.hs * a.hs > kGcMaxIn) --a.upt;
         if (a.upt < 1 || a.upt * a.hs * a.hs > kGcMaxIn) return -1;
         const long cap = max_rows / (a.S * a.S);
         return (cap + a.upt - 1) / a.upt;
@@ -397,14 +452,23 @@ cudaError_t launch_se(const SeArgs &a, cudaStream_t st) {
     if (a.n_img == 0) return cudaSuccess;
     const int cv = a.C / 8;
     const int RS = cv >= kSeThreads ? 1 : kSeThreads / cv;
-    const size_t smem = (size_t)((RS + 1) * a.C + a.w_se) * 4;
+    const size_t smem = (size_t)RS * a.C * 4;
     static size_t configured = 48 * 1024;
     if (smem > configured) {
         if (cudaFuncSetAttribute(se_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
             return cudaErrorInvalidValue;
         configured = smem;
     }
-    return launch_k(se_kernel, dim3((unsigned)a.n_img), dim3(kSeThreads), smem, st, a);
+    cudaError_t e = launch_k(se_kernel, dim3((unsigned)a.n_img), dim3(kSeThreads), smem, st, a);
+    if (e != cudaSuccess) return e;
+    // z = ReLU(pooled W1^T + b1), then scale = sigmoid(z W2^T + b2)
+    const dim3 g1((unsigned)((a.w_se + 31) / 32), (unsigned)((a.n_img + 31) / 32));
+    e = launch_k(se_fc_kernel, g1, dim3(256), 0, st, static_cast<const float *>(a.pooled), a.w1, a.b1, a.z, a.n_img,
+                 a.C, a.w_se, 0);
+    if (e != cudaSuccess) return e;
+    const dim3 g2((unsigned)((a.C + 31) / 32), (unsigned)((a.n_img + 31) / 32));
+    return launch_k(se_fc_kernel, g2, dim3(256), 0, st, static_cast<const float *>(a.z), a.w2, a.b2, a.scale,
+                    a.n_img, a.w_se, a.C, 1);
 }
 
 cudaError_t launch_se_apply(__nv_bfloat16 *h2, const float *scale, const int32_t *idx, const int32_t *count,
@@ -419,7 +483,7 @@ cudaError_t launch_se_apply(__nv_bfloat16 *h2, const float *scale, const int32_t
 
 cudaError_t launch_regnet_stem(const void *x, const void *w, const float *b, void *y, int n_img, int h, int wo,
                                int co_real, int num_sms, cudaStream_t st) {
-    const long total = (long)n_img * h * wo;
+    const long total = (long)n_img * h * ((wo + 1) / 2);
     long grid = (total + 127) / 128;
     if (grid > 16L * num_sms) grid = 16L * num_sms;
     if (grid == 0) return cudaSuccess;

@@ -27,6 +27,8 @@ struct SeArgs {
     const float *w1, *b1;     // [w_se][C], [w_se]
     const float *w2, *b2;     // [C][w_se], [C]
     float *scale;             // [n][C] out
+    float *pooled;            // [n][C] scratch: mean of h2 over the image's computed pixels
+    float *z;                 // [n][w_se] scratch: the squeeze
     const int32_t *idx;       // dynamic: ascending active cell ids
     const int32_t *count;     // dynamic: device count; dense: nullptr
     int C, w_se, n_img;
