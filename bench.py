@@ -252,17 +252,26 @@ def t_roof_ms(work, hbm, tfl):
     return max(work["bytes"] / (hbm * 1e9), work["flops"] / (tfl * 1e12)) * 1e3
 
 
-def ncu_traffic(kernel: str):
-    """DRAM bytes (read + write) per launch of `kernel` from the latest committed
-    ncu --set full capture (profiles/ncu_full_<tag>.json), or (None, None)."""
+def ncu_traffic(kernel: str, scope: str = "net"):
+    """DRAM bytes (read + write) per launch of `kernel` from the latest committed ncu
+    evidence (profiles/ncu_full_<tag>.json), or (None, None).  scope "net": the mean
+    over that kernel's launches in one eager LAS-R101 forward (r2 layout); "block":
+    the --set full capture of the configs[1] block (conv23_direct is the conv23
+    kernel reading the dense h1)."""
     import glob
 
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_full_*.json")))
     for f in reversed(files):
         d = json.load(open(f))
-        for e in d.get("full", []):
-            if e.get("kernel") == kernel or e.get("name") == kernel:
-                return int(e.get("dram_read", 0) + e.get("dram_write", 0)), os.path.relpath(f, ROOT)
+        if scope == "net" and isinstance(d.get("net"), list):
+            for e in d["net"]:
+                if e.get("kernel") == kernel:
+                    return int(e.get("dram_read", 0) + e.get("dram_write", 0)), os.path.relpath(f, ROOT)
+        if scope == "block":
+            want = "conv23" if kernel.startswith("conv23") else kernel
+            for e in d.get("full", []):
+                if e.get("capture", "block") == "block" and e.get("kernel") in (want, kernel) and "launches" not in e:
+                    return int(e.get("dram_read", 0) + e.get("dram_write", 0)), os.path.relpath(f, ROOT)
     return None, None
 
 
@@ -981,7 +990,7 @@ def run_lasnet(args):
             bms = b_max / K
             dom = max(bl["kern_ms"], key=lambda k: bl["kern_ms"][k])
             broof = roofline_entry(bl["kwork"][dom], bl["kern_ms"][dom], hbm, tfl)
-            traffic, tsrc = ncu_traffic(dom)
+            traffic, tsrc = ncu_traffic(dom, scope="block")
             broof.update({"kernel": dom, "traffic": traffic, "traffic_source": tsrc,
                           "algorithmic": bl["kwork"][dom],
                           "share_of_step": round(bl["kern_ms"][dom] / sum(bl["kern_ms"].values()), 3)})

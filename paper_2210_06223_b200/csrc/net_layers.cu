@@ -114,26 +114,47 @@ __global__ void __launch_bounds__(256) avgpool_kernel(const __nv_bfloat16 *__res
 // chunks of 64 channels, each thread 2 x 2 outputs with a fixed-order fp32 sum
 // (the classifier is 2*256*2048*1000 = 1 GFLOP; per-(image, class) warps re-read
 // every weight row once per image).
-constexpr int kFcT = 32, kFcK = 64;
+constexpr int kFcT = 32, kFcK = 256;
 __global__ void __launch_bounds__(256) fc_kernel(const float *__restrict__ pooled, const __nv_bfloat16 *__restrict__ w,
                                                  const float *__restrict__ b, float *__restrict__ logits, int n_img,
                                                  int c, int classes) {
     pdl_wait();
     pdl_trigger();
-    __shared__ float sa[kFcT][kFcK + 1], sb[kFcT][kFcK + 1];
+    // K staged 256 channels at a time (8 chunks for c = 2048): the chunk loads of a CTA are
+    // a latency chain, so few, wide chunks
+    extern __shared__ float fsm[];
+    float(*sa)[kFcK + 1] = reinterpret_cast<float(*)[kFcK + 1]>(fsm);
+    float(*sb)[kFcK + 1] = reinterpret_cast<float(*)[kFcK + 1]>(fsm + kFcT * (kFcK + 1));
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const int k0 = blockIdx.x * kFcT, n0 = blockIdx.y * kFcT;
     float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
     for (int c0 = 0; c0 < c; c0 += kFcK) {
-        for (int e = threadIdx.x; e < kFcT * kFcK; e += 256) {
-            const int r = e / kFcK, cc = e % kFcK;
+        for (int e = threadIdx.x; e < kFcT * kFcK / 8; e += 256) {  // 8 channels per load
+            const int r = e / (kFcK / 8), cc = (e % (kFcK / 8)) * 8;
             const int n = n0 + r, k = k0 + r, ch = c0 + cc;
-            sa[r][cc] = (n < n_img && ch < c) ? pooled[(long)n * c + ch] : 0.f;
-            sb[r][cc] = (k < classes && ch < c) ? __bfloat162float(w[(long)k * c + ch]) : 0.f;
+            if (n < n_img && ch < c) {
+                const float4 p0 = *reinterpret_cast<const float4 *>(pooled + (long)n * c + ch);
+                const float4 p1 = *reinterpret_cast<const float4 *>(pooled + (long)n * c + ch + 4);
+                sa[r][cc] = p0.x; sa[r][cc + 1] = p0.y; sa[r][cc + 2] = p0.z; sa[r][cc + 3] = p0.w;
+                sa[r][cc + 4] = p1.x; sa[r][cc + 5] = p1.y; sa[r][cc + 6] = p1.z; sa[r][cc + 7] = p1.w;
+            } else {
+                for (int q = 0; q < 8; ++q) sa[r][cc + q] = 0.f;
+            }
+            if (k < classes && ch < c) {
+                const uint4 q = __ldg(reinterpret_cast<const uint4 *>(w + (long)k * c + ch));
+                const uint32_t u[4] = {q.x, q.y, q.z, q.w};
+                for (int e2 = 0; e2 < 4; ++e2) {
+                    sb[r][cc + 2 * e2] = __uint_as_float(u[e2] << 16);
+                    sb[r][cc + 2 * e2 + 1] = __uint_as_float(u[e2] & 0xffff0000u);
+                }
+            } else {
+                for (int q = 0; q < 8; ++q) sb[r][cc + q] = 0.f;
+            }
         }
         __syncthreads();
+        const int kk_end = min(kFcK, c - c0);
 #pragma unroll 8
-        for (int cc = 0; cc < kFcK; ++cc) {
+        for (int cc = 0; cc < kk_end; ++cc) {
             const float a0 = sa[ty][cc], a1 = sa[ty + 16][cc];
             const float b0 = sb[tx][cc], b1 = sb[tx + 16][cc];
             acc[0][0] = fmaf(a0, b0, acc[0][0]);
@@ -162,7 +183,14 @@ cudaError_t launch_head(const void *x, const void *w, const float *b, float *poo
                              static_cast<const __nv_bfloat16 *>(x), pooled, n_img, hw, c);
     if (e != cudaSuccess) return e;
     const dim3 g2((unsigned)((classes + kFcT - 1) / kFcT), (unsigned)((n_img + kFcT - 1) / kFcT));
-    return launch_k(fc_kernel, g2, dim3(256), 0, st, static_cast<const float *>(pooled),
+    const int smem = 2 * kFcT * (kFcK + 1) * 4;
+    static bool configured = false;
+    if (!configured) {
+        e = cudaFuncSetAttribute(fc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    return launch_k(fc_kernel, g2, dim3(256), smem, st, static_cast<const float *>(pooled),
                     static_cast<const __nv_bfloat16 *>(w), b, logits, n_img, c, classes);
 }
 
