@@ -17,6 +17,8 @@ SOURCES = ["lasnet_capi.cu", "mask_compact.cu", "conv_tc.cu", "conv23_tc.cu", "c
            "regnet.cu"]
 HEADERS = ["rowmap.cuh", "sm100_ptx.cuh", "launch.cuh", "predictor_b200.inc", "regnet.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+# A/B experiments only: extra nvcc flags (e.g. -DLASNET_C23_STAGES=2); the product build sets none
+EXTRA = os.environ.get("LASNET_EXTRA_NVCC", "").split()
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -45,7 +47,7 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
 
     def compile_one(src):
         obj = os.path.join(bdir, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, *(["-DLASNET_TRACE"] if trace else []), "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *FLAGS, *EXTRA, *(["-DLASNET_TRACE"] if trace else []), "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         return src, obj, r
 

@@ -61,8 +61,14 @@ __device__ unsigned long long g_trace23c[64 * 16];
 namespace c23 {
 constexpr int kBM = 128, kBK = 64;
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB
-constexpr int kStages = 3;  // conv2 ring depth
-constexpr int kH2Bufs = 1;  // H2 tiles (double-buffering lets epi2 of tile i+1 overlap conv3 of tile i)
+#ifndef LASNET_C23_STAGES
+#define LASNET_C23_STAGES 3
+#endif
+#ifndef LASNET_C23_H2BUFS
+#define LASNET_C23_H2BUFS 1
+#endif
+constexpr int kStages = LASNET_C23_STAGES;  // conv2 ring depth
+constexpr int kH2Bufs = LASNET_C23_H2BUFS;  // H2 tiles (double-buffering lets epi2 of tile i+1 overlap conv3 of tile i)
 constexpr int kStageBytes = 2 * kABytes;  // A 16 KB + B (<= 128 rows) 16 KB
 constexpr int kNC3 = 128;                 // max conv3 output channels per MMA chunk (64 when c_out % 128 != 0)
 constexpr int kAcc3 = 2;                  // conv3 accumulator buffers (128 TMEM columns each)

@@ -81,7 +81,8 @@ template <int MODE, int BN> struct Cfg {
     static constexpr int kMaskerWarp0 = kEpiWarps + 2, kMaskerThreads = 256;
     static constexpr int kThreads =
         32 * (kEpiWarps + 2) + (kGather ? kGatherThreads : 0) + (kMasker ? kMaskerThreads : 0);
-    static constexpr int kBBytes = BN * kBK * 2;
+    // stem: B is the 64-channel weight (its BN = 128 spans two output rows' accumulators)
+    static constexpr int kBBytes = (MODE == STEM ? 64 : BN) * kBK * 2;
     // stem: the whole packed weight (7 K-blocks of 64 x 64, 56 KB) stays resident in smem,
     // loaded once per CTA; its stages carry A only (it was L2-throughput bound re-streaming it)
     static constexpr bool kBRes = MODE == STEM;
@@ -126,6 +127,7 @@ __device__ __forceinline__ TileGeo tile_geo(const ConvArgs &a, int BN) {
         mt = (*a.count + a.units_per_tile - 1) / a.units_per_tile;  // patch-aligned tiles
     } else if (MODE == CONV2_DENSE || MODE == STEM) {
         mt = a.dense_tiles;
+        if (MODE == STEM) g.n_tiles_n = 1;  // one 64-channel weight, two output rows per tile
     } else {
         mt = (gemm_rows(MODE, a) + kBM - 1) / kBM;
     }
@@ -190,15 +192,20 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
     pdl_trigger();
 
     const TileGeo geo = tile_geo<MODE>(args, BN);
-    const int num_kb = args.K / kBK;
+    // stem: a tile is TWO output rows (2 oy0, 2 oy0 + 1 -> accumulator columns 0-63 / 64-127);
+    // its K loop walks the 9 input rows they need, each staged once and used by both rows'
+    // MMAs (kernel row j for the first, j - 2 for the second): 9 instead of 14 row loads
+    const int num_kb = MODE == STEM ? 9 : args.K / kBK;
+    const int num_kb_b = args.K / kBK;  // resident weight K-blocks (stem: 7 kernel rows)
     const int kpt = args.a_ld / kBK;  // K-blocks per 3x3 tap (conv2)
 
     if (warp == C::kProdWarp) {
         // --------------------------------------------------- TMA producer --
         if (lane == 0) {
             if (C::kBRes) {
-                mbar_arrive_expect_tx(bar_bres, (uint32_t)(num_kb * C::kBBytes));
-                for (int kb = 0; kb < num_kb; ++kb) tma_load_2d(sbase + kb * C::kBBytes, &args.tmap_b, bar_bres, kb * kBK, 0);
+                mbar_arrive_expect_tx(bar_bres, (uint32_t)(num_kb_b * C::kBBytes));
+                for (int kb = 0; kb < num_kb_b; ++kb)
+                    tma_load_2d(sbase + kb * C::kBBytes, &args.tmap_b, bar_bres, kb * kBK, 0);
             }
             int it = 0, lt = 0;
             for (int tile = blockIdx.x; tile < geo.num_tiles; tile += gridDim.x, ++lt) {
@@ -240,13 +247,15 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     } else if (MODE == STEM) {
                         // K-block kb = kernel row dy: 4 boxes of W/4 output columns each (residue k of
                         // ox mod 4), every box row the 8 input pixels x 8 channels of one output pixel
-                        // tile = (image, output row, column block of cols_w columns)
+                        // tile = (image, output row pair, column block of cols_w columns); K-block kb =
+                        // input row 2 oy0 + kb - 3 (out of the image: TMA zero fill)
                         const int xb = mt % args.tiles_x, row = mt / args.tiles_x;
-                        const int n = row / args.H, oy = row - n * args.H;
+                        const int pairs = (args.H + 1) / 2;
+                        const int n = row / pairs, oy0 = 2 * (row - n * pairs);
                         const int q = args.cols_w / 4;
 #pragma unroll
                         for (int k = 0; k < 4; ++k)
-                            tma_load_4d(sa + k * q * 128, &args.tmap_s[k], fb, 0, xb * q, 2 * oy + kb - 3, n);
+                            tma_load_4d(sa + k * q * 128, &args.tmap_s[k], fb, 0, xb * q, 2 * oy0 + kb - 3, n);
                     } else if (!C::kGather) {
                         if (args.a2_kb && kb >= args.a2_kb)  // second A source (projection shortcut input)
                             tma_load_2d(sa, &args.tmap_s[0], fb, (kb - args.a2_kb) * kBK, mt * kBM);
@@ -395,6 +404,23 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     tc_fence_after();
                     const uint32_t sa = sbase + C::kStageOff + stage * C::kStageBytes;
                     const uint64_t adesc = smem_desc_sw128(sa);
+                    if (MODE == STEM) {  // input row kb: kernel row kb of output row 0, kb - 2 of row 1
+                        constexpr uint32_t idesc64 = idesc_bf16_f32(kBM, 64);
+                        if (kb <= 6) {
+                            const uint64_t bd = smem_desc_sw128(sbase + kb * C::kBBytes);
+#pragma unroll
+                            for (int kk = 0; kk < kBK / 16; ++kk)
+                                mma_bf16(d_tmem, adesc + 2 * kk, bd + 2 * kk, idesc64, (kb | kk) != 0);
+                        }
+                        if (kb >= 2) {
+                            const uint64_t bd = smem_desc_sw128(sbase + (kb - 2) * C::kBBytes);
+#pragma unroll
+                            for (int kk = 0; kk < kBK / 16; ++kk)
+                                mma_bf16(d_tmem + 64, adesc + 2 * kk, bd + 2 * kk, idesc64, ((kb - 2) | kk) != 0);
+                        }
+                        mma_commit(bar_empty + 8 * stage);
+                        continue;
+                    }
                     const uint64_t bdesc = smem_desc_sw128(C::kBRes ? sbase + kb * C::kBBytes : sa + kABytes);
 #pragma unroll
                     for (int kk = 0; kk < kBK / 16; ++kk)
@@ -513,7 +539,8 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     const uint32_t saddr = rowbase + ((((c & 63) >> 3) + q) ^ (r & 7)) * 16;
                     float f[8];
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[8 * q + e]) + bias_s[n0 + c + 8 * q + e];
+                    for (int e = 0; e < 8; ++e)  // (stem: columns 64-127 are the second row's 64 channels)
+                        f[e] = __uint_as_float(v[8 * q + e]) + bias_s[(n0 + c + 8 * q + e) & (MODE == STEM ? 63 : 0x7fffffff)];
                     if (kResid) {
                         uint32_t rv[4];
                         asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
@@ -579,10 +606,13 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                         tma_store_4d(&args.tmap_out, sbuf + c * kChunkBytes, n0 + c * 64, d2x, d2y, d2n);
                 } else if (MODE == STEM) {  // the tile's rows in residue order back to output columns
                     const int xb = mt % args.tiles_x, row = mt / args.tiles_x;
-                    const int n = row / args.H, oy = row - n * args.H;
+                    const int pairs = (args.H + 1) / 2;
+                    const int n = row / pairs, oy0 = 2 * (row - n * pairs);
                     const int q = args.cols_w / 4;
-                    for (int k = 0; k < 4; ++k)
-                        tma_store_4d(&args.tmap_s[4 + k], sbuf + k * q * 128, 0, xb * q, oy, n);
+                    for (int r2 = 0; r2 < 2; ++r2)  // 64-column chunk r2 = output row oy0 + r2 (row H: clipped)
+                        for (int k = 0; k < 4; ++k)
+                            tma_store_4d(&args.tmap_s[4 + k], sbuf + r2 * kChunkBytes + k * q * 128, 0, xb * q,
+                                         oy0 + r2, n);
                 } else if (MODE == CONV1_DYN || MODE == CONV1_DENSE || MODE == CONV1_DENSE_MASK) {  // h1: [c_mid/64][rows][64]
                     for (int c = 0; c < BN / 64; ++c)
                         tma_store_3d(&args.tmap_out, sbuf + c * kChunkBytes, 0, mt * kBM, (n0 >> 6) + c);
@@ -664,7 +694,18 @@ cudaError_t launch_conv_tc(int mode, const ConvArgs &a, int max_tiles_m, int num
         case CONV1_DENSE_MASK: return launch_mode<CONV1_DENSE_MASK>(a, max_tiles_m, num_sms, st);
         case CONV2_DENSE: return launch_mode<CONV2_DENSE>(a, max_tiles_m, num_sms, st);
         case CONV3_DENSE: return launch_mode<CONV3_DENSE>(a, max_tiles_m, num_sms, st);
-        case STEM: return launch_mode_bn<STEM, 64>(a, max_tiles_m, num_sms, st);
+        case STEM: {  // BN = 128: the two output rows' 64-channel accumulators
+            auto kern = conv_tc_kernel<STEM, 128>;
+            const int smem = Cfg<STEM, 128>::smem_bytes(64, a.K);
+            static int configured = 0;
+            if (smem > configured) {
+                cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                if (e != cudaSuccess) return e;
+                configured = smem;
+            }
+            const int grid = max_tiles_m < num_sms ? (max_tiles_m > 0 ? max_tiles_m : 1) : num_sms;
+            return launch_k(kern, dim3(grid), dim3(threads_of<STEM, 128>()), smem, st, a);
+        }
         default: return cudaErrorInvalidValue;
     }
 }

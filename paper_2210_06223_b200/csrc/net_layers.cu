@@ -109,68 +109,88 @@ __global__ void __launch_bounds__(256) avgpool_kernel(const __nv_bfloat16 *__res
     }
 }
 
-// Head, pass 2: logits[n][k] = b[k] + sum_c pooled[n][c] w[k][c], a tiled SIMT
-// GEMM: one CTA per 32 images x 32 classes, K staged through shared memory in
-// chunks of 64 channels, each thread 2 x 2 outputs with a fixed-order fp32 sum
-// (the classifier is 2*256*2048*1000 = 1 GFLOP; per-(image, class) warps re-read
-// every weight row once per image).
-constexpr int kFcT = 32, kFcK = 256;
+// Head, pass 2: logits[n][k] = b[k] + sum_c pooled[n][c] w[k][c] -- a SIMT GEMM tile
+// of 32 images x 32 classes per 256-thread CTA: four K slices of 64 threads, each
+// thread a 4 x 4 register block over its slice's 64-channel chunks (transposed in
+// shared memory so every thread's four images / classes are one 16-B load); the four
+// slice partials are then added in slice order (deterministic).  8 warps per CTA keep
+// the FMA pipes fed (a 2-warp CTA was latency-bound at ~120 us).
+constexpr int kFcT = 32, kFcK = 64, kFcP = 36, kFcS = 4;  // tile, K chunk, padded row, K slices
 __global__ void __launch_bounds__(256) fc_kernel(const float *__restrict__ pooled, const __nv_bfloat16 *__restrict__ w,
                                                  const float *__restrict__ b, float *__restrict__ logits, int n_img,
                                                  int c, int classes) {
     pdl_wait();
     pdl_trigger();
-    // K staged 256 channels at a time (8 chunks for c = 2048): the chunk loads of a CTA are
-    // a latency chain, so few, wide chunks
-    extern __shared__ float fsm[];
-    float(*sa)[kFcK + 1] = reinterpret_cast<float(*)[kFcK + 1]>(fsm);
-    float(*sb)[kFcK + 1] = reinterpret_cast<float(*)[kFcK + 1]>(fsm + kFcT * (kFcK + 1));
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    extern __shared__ __align__(16) float fsm[];
+    const int slice = threadIdx.x >> 6, lt = threadIdx.x & 63;
+    float(*sa)[kFcP] = reinterpret_cast<float(*)[kFcP]>(fsm + slice * 2 * kFcK * kFcP);
+    float(*sb)[kFcP] = reinterpret_cast<float(*)[kFcP]>(fsm + slice * 2 * kFcK * kFcP + kFcK * kFcP);
+    const int tx = lt & 7, ty = lt >> 3;
     const int k0 = blockIdx.x * kFcT, n0 = blockIdx.y * kFcT;
-    float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
-    for (int c0 = 0; c0 < c; c0 += kFcK) {
-        for (int e = threadIdx.x; e < kFcT * kFcK / 8; e += 256) {  // 8 channels per load
-            const int r = e / (kFcK / 8), cc = (e % (kFcK / 8)) * 8;
-            const int n = n0 + r, k = k0 + r, ch = c0 + cc;
+    float acc[4][4] = {};
+    for (int c0 = slice * kFcK; c0 < c; c0 += kFcS * kFcK) {
+        for (int e = lt; e < kFcT * kFcK / 8; e += 64) {  // 8 channels of one row per step
+            const int r = e / (kFcK / 8), cc = (e % (kFcK / 8)) * 8, ch = c0 + cc;
+            const int n = n0 + r, k = k0 + r;
+            float av[8], bv[8];
             if (n < n_img && ch < c) {
                 const float4 p0 = *reinterpret_cast<const float4 *>(pooled + (long)n * c + ch);
                 const float4 p1 = *reinterpret_cast<const float4 *>(pooled + (long)n * c + ch + 4);
-                sa[r][cc] = p0.x; sa[r][cc + 1] = p0.y; sa[r][cc + 2] = p0.z; sa[r][cc + 3] = p0.w;
-                sa[r][cc + 4] = p1.x; sa[r][cc + 5] = p1.y; sa[r][cc + 6] = p1.z; sa[r][cc + 7] = p1.w;
+                av[0] = p0.x; av[1] = p0.y; av[2] = p0.z; av[3] = p0.w;
+                av[4] = p1.x; av[5] = p1.y; av[6] = p1.z; av[7] = p1.w;
             } else {
-                for (int q = 0; q < 8; ++q) sa[r][cc + q] = 0.f;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) av[q] = 0.f;
             }
             if (k < classes && ch < c) {
                 const uint4 q = __ldg(reinterpret_cast<const uint4 *>(w + (long)k * c + ch));
                 const uint32_t u[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
                 for (int e2 = 0; e2 < 4; ++e2) {
-                    sb[r][cc + 2 * e2] = __uint_as_float(u[e2] << 16);
-                    sb[r][cc + 2 * e2 + 1] = __uint_as_float(u[e2] & 0xffff0000u);
+                    bv[2 * e2] = __uint_as_float(u[e2] << 16);
+                    bv[2 * e2 + 1] = __uint_as_float(u[e2] & 0xffff0000u);
                 }
             } else {
-                for (int q = 0; q < 8; ++q) sb[r][cc + q] = 0.f;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) bv[q] = 0.f;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                sa[cc + q][r] = av[q];
+                sb[cc + q][r] = bv[q];
             }
         }
-        __syncthreads();
+        __syncwarp();
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + slice));  // this slice's 2 warps
         const int kk_end = min(kFcK, c - c0);
-#pragma unroll 8
-        for (int cc = 0; cc < kk_end; ++cc) {
-            const float a0 = sa[ty][cc], a1 = sa[ty + 16][cc];
-            const float b0 = sb[tx][cc], b1 = sb[tx + 16][cc];
-            acc[0][0] = fmaf(a0, b0, acc[0][0]);
-            acc[0][1] = fmaf(a0, b1, acc[0][1]);
-            acc[1][0] = fmaf(a1, b0, acc[1][0]);
-            acc[1][1] = fmaf(a1, b1, acc[1][1]);
+#pragma unroll 4
+        for (int kk = 0; kk < kk_end; ++kk) {
+            const float4 a4 = *reinterpret_cast<const float4 *>(&sa[kk][ty * 4]);
+            const float4 b4 = *reinterpret_cast<const float4 *>(&sb[kk][tx * 4]);
+            const float av[4] = {a4.x, a4.y, a4.z, a4.w}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
         }
-        __syncthreads();
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + slice));
     }
+    // slice partials -> logits, added in slice order
+    __syncthreads();
+    float *red = fsm;  // [kFcS][32][33]
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            const int n = n0 + ty + 16 * i, k = k0 + tx + 16 * j;
-            if (n < n_img && k < classes) logits[(long)n * classes + k] = acc[i][j] + b[k];
+        for (int j = 0; j < 4; ++j) red[(slice * 32 + ty * 4 + i) * 33 + tx * 4 + j] = acc[i][j];
+    __syncthreads();
+    for (int e = threadIdx.x; e < kFcT * kFcT; e += 256) {
+        const int r = e / kFcT, col = e % kFcT, n = n0 + r, k = k0 + col;
+        if (n < n_img && k < classes) {
+            float v = red[r * 33 + col];
+            for (int sl = 1; sl < kFcS; ++sl) v += red[(sl * 32 + r) * 33 + col];
+            logits[(long)n * classes + k] = v + b[k];
         }
+    }
 }
 
 cudaError_t launch_head(const void *x, const void *w, const float *b, float *pooled, float *logits, int n_img, int hw,
@@ -183,7 +203,7 @@ cudaError_t launch_head(const void *x, const void *w, const float *b, float *poo
                              static_cast<const __nv_bfloat16 *>(x), pooled, n_img, hw, c);
     if (e != cudaSuccess) return e;
     const dim3 g2((unsigned)((classes + kFcT - 1) / kFcT), (unsigned)((n_img + kFcT - 1) / kFcT));
-    const int smem = 2 * kFcT * (kFcK + 1) * 4;
+    const int smem = kFcS * 2 * kFcK * kFcP * 4;  // >= the [4][32][33] partials
     static bool configured = false;
     if (!configured) {
         e = cudaFuncSetAttribute(fc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
