@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             return buf + (col >> 6) * kChunkBytes + row * 128 + ((((col & 63) >> 3) ^ (row & 7)) << 4);
         };
         auto prefetch_resid = [&](int tl, int mypix, uint32_t buf) {
-            if (tl < geo.num_tiles) {
+            if (tl < geo.num_tiles && X != nullptr) {  // no residual tensor: nothing to stage
                 const int n0 = (tl % geo.n_tiles_n) * BN;
 #pragma unroll
                 for (int i = 0; i < 32 / kRowsPerIt; ++i) {
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
 #pragma unroll
                     for (int e = 0; e < 8; ++e)  // (stem: columns 64-127 are the second row's 64 channels)
                         f[e] = __uint_as_float(v[8 * q + e]) + bias_s[(n0 + c + 8 * q + e) & (MODE == STEM ? 63 : 0x7fffffff)];
-                    if (kResid) {
+                    if (kResid && X != nullptr) {
                         uint32_t rv[4];
                         asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
                                      : "=r"(rv[0]), "=r"(rv[1]), "=r"(rv[2]), "=r"(rv[3])
@@ -567,7 +567,20 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             }
             tc_fence_before();
             mbar_arrive(bar_tempty + 8 * acc);
-            if (kResid) {
+            if (kResid && MODE == CONV3_DENSE && args.tma_y) {
+                // dense rows: the staged (128-B swizzled) tile is y's rows [mt*128, +128) --
+                // one TMA store per 64-column chunk (rows past the end are clipped); the
+                // buffer the next prefetch reuses was read by the previous tile's store
+                fence_proxy_async_smem();
+                named_bar_sync(1, EPI);
+                if (tid == 0) {
+                    for (int c = 0; c < BN / 64; ++c)
+                        tma_store_2d(&args.tmap_out, sbuf + c * kChunkBytes, n0 + c * 64, mt * kBM);
+                    bulk_commit();
+                    bulk_wait_read<1>();
+                }
+                named_bar_sync(1, EPI);
+            } else if (kResid) {
                 // scatter-add store: the warp's 32 rows x kCols columns, 16-B chunks,
                 // kRowsPerIt rows per instruction (full 128-B lines)
                 __syncwarp();
@@ -585,6 +598,8 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                             make_uint4(o[0], o[1], o[2], o[3]);
                 }
                 __syncwarp();
+            }
+            if (kResid) {
                 // residual prefetch for tile lt+NSTG-1 into the buffer tile lt-1 used
                 const int ahead = tile + (NSTG - 1) * gridDim.x;
                 const int slot = (lt + NSTG - 1) % NSTG;
@@ -632,7 +647,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                 }
             }
         }
-        if (tid == 0 && !kResid) bulk_wait_all<0>();
+        if (tid == 0 && (!kResid || (MODE == CONV3_DENSE && args.tma_y))) bulk_wait_all<0>();
     }
 
     tc_fence_before();

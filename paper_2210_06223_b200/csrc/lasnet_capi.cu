@@ -346,6 +346,9 @@ int prepare_tc(int mode, ConvArgs &a, const lasnet_block_desc *d, const void *x,
         }
         case CONV3_DENSE: {
             ok = ok && tmap2(&a.tmap_a, h2, C, px, 64, 128);
+            // y rows are contiguous: the epilogue TMA-stores whole tiles (tma_y)
+            ok = ok && tmap2(&a.tmap_out, a.out, a.N, px, 64, 128);
+            a.tma_y = 1;
             return ok ? (int)((px + 127) / 128) : -1;
         }
     }
@@ -819,7 +822,9 @@ lasnet_status proj_dyn_forward(const lasnet_block_desc *d, const lasnet_block_we
         c.K = d->c_in; c.N = d->c_out; c.a_ld = d->c_in; c.out_ld = d->c_out;
         c.relu_mask = m;
         bool ok = tmap2(&c.tmap_b, w->wd, d->c_in, d->c_out, 64, bn_of(d->c_out, CONV3_DENSE)) &&
-                  tmap2(&c.tmap_a, xs, d->c_in, (uint64_t)po, 64, 128);
+                  tmap2(&c.tmap_a, xs, d->c_in, (uint64_t)po, 64, 128) &&
+                  tmap2(&c.tmap_out, y, d->c_out, (uint64_t)po, 64, 128);
+        c.tma_y = 1;
         if (!ok) return LASNET_ERR_CUDA;
         KernelEvents ev(st, "shortcut");
         if (launch_conv_tc(CONV3_DENSE, c, (int)((po + 127) / 128), num_sms(), st) != cudaSuccess)

@@ -73,6 +73,7 @@ struct ConvArgs {
     // dense epilogue: ReLU only on pixels of INACTIVE cells of this mask [n][Gh][Gw] (the dynamic
     // projection block's shortcut R: inactive pixels store ReLU(R), active ones R for the scatter-add)
     const uint8_t *relu_mask;
+    int32_t tma_y;            // dense conv3: the epilogue TMA-stores whole 128-row tiles of y (tmap_out = y [px][c_out])
     // tcgen05 tile geometry (host-computed)
     int32_t units_per_tile;   // dynamic: TMA boxes (conv1) / patches (conv2, conv3) per 128-row tile
     int32_t units_per_patch;  // conv1: 1 (whole halo box) or S+2 (one box per halo row)
