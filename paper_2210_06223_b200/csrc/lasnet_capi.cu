@@ -748,7 +748,7 @@ namespace {
 // (when the caller passes none), the gathered conv1 windows, h2 (unfused steps 4-5)
 // and the subsampled input x_s (stride 2).
 struct ProjWs {
-    void *sync, *mask, *h1g, *h2, *xs;
+    void *sync, *mask, *h1g, *h2, *xs, *cws;
 };
 size_t proj_dyn_ws(const lasnet_block_desc *d, uint8_t *base, ProjWs *o) {
     const long ncells = (long)d->n * ((d->h + d->s - 1) / d->s) * ((d->w + d->s - 1) / d->s);
@@ -761,8 +761,21 @@ size_t proj_dyn_ws(const lasnet_block_desc *d, uint8_t *base, ProjWs *o) {
     r.h1g = cv.take((size_t)ncells * hs * hs * d->c_mid * e);
     r.h2 = use_fused23(d) ? nullptr : cv.take((size_t)ncells * d->s * d->s * d->c_mid * e);
     r.xs = d->stride > 1 ? cv.take((size_t)d->n * d->h * d->w * d->c_in * e) : nullptr;
+    r.cws = cv.take(compact_workspace_bytes((int)ncells));
     if (o) *o = r;
     return cv.used;
+}
+
+// The first block's masker: decisions (masker_kernel) then the decoupled look-back
+// compaction (4096 cells per CTA) -- the fused masker+compaction ends in ONE CTA
+// compacting every cell, which dominated at the 50 176 cells of LAS-R101's first
+// block (84 us); LASNET_PROJ_MASK_FUSED=1 keeps the fused launch (A/B measurements).
+bool proj_mask_fused() {
+    static const bool on = [] {
+        const char *e = getenv("LASNET_PROJ_MASK_FUSED");
+        return e && e[0] == '1';
+    }();
+    return on;
 }
 
 // a projection-shaped block (the caller may still pass identity weights when c_in == c_out, stride 1)
@@ -798,12 +811,23 @@ lasnet_status proj_dyn_forward(const lasnet_block_desc *d, const lasnet_block_we
     int launches = 0;
     // step 1+2: the masker pools each output cell's st*S x st*S input window (reading R22): the
     // input-resolution masker at granularity st*S has exactly the output grid
-    {
+    if (proj_mask_fused()) {
         KernelEvents ev(st, "mask_compact");
         if (launch_mask_compact(1, x, wm, bm, d->n, Hi, Wi, d->c_in, d->s * st_, m, nullptr, idx, count, r.sync,
                                 st) != cudaSuccess)
             return LASNET_ERR_CUDA;
         ++launches;
+    } else {
+        {
+            KernelEvents ev(st, "mask");
+            if (launch_masker(1, x, wm, bm, d->n, Hi, Wi, d->c_in, d->s * st_, m, nullptr, st) != cudaSuccess)
+                return LASNET_ERR_CUDA;
+        }
+        KernelEvents ev(st, "compact");
+        cudaError_t ce = cudaSuccess;
+        const int k = launch_compact(m, ncells, idx, count, r.cws, st, &ce);
+        if (ce != cudaSuccess) return LASNET_ERR_CUDA;
+        launches += 1 + k;
     }
     // the dense projection shortcut R = Wd x_s + bd (the downsampling shortcut stays dense):
     // ReLU(R) on inactive pixels (final), R on active ones (the residual of the scatter-add)
@@ -1418,3 +1442,7 @@ lasnet_status lasnet_regnet_stem(int32_t n, int32_t h, int32_t w, int32_t c_real
 }
 
 }  // extern "C"
+
+namespace lasnet {
+bool plan_proj_mask_fused() { return proj_mask_fused(); }
+}  // namespace lasnet

@@ -34,13 +34,15 @@
 namespace lasnet {
 bool plan_fused23(const lasnet_block_desc *d);
 bool plan_direct(const lasnet_block_desc *d);
+bool plan_proj_mask_fused();
 }  // namespace lasnet
 
 namespace {
 
 const char *const kNames[LASNET_K_COUNT] = {
     "mask_compact", "conv1_dyn", "conv1_mask", "decide", "decide+gather", "conv23", "conv23_direct", "conv2_dyn",
-    "conv3_dyn", "conv1_dense", "conv2_dense", "conv3_dense", "conv23_dense", "subsample", "shortcut"};
+    "conv3_dyn", "conv1_dense", "conv2_dense", "conv3_dense", "conv23_dense", "subsample", "shortcut", "mask",
+    "compact"};
 
 struct Work {
     int type;
@@ -129,7 +131,12 @@ bool build_plan(Plan &p, const lasnet_block_desc *d, int schedule, double r) {
     }
     if (proj) {  // the dynamic first block (reading R22): separate schedule only
         if (schedule != LASNET_SCHED_MASKER_SEPARATE) return false;
-        p.add(LASNET_K_MASK_COMPACT, pxi * CI * e + G + 4 * P, 0, 2 * pxi * CI, 0);
+        if (lasnet::plan_proj_mask_fused()) {
+            p.add(LASNET_K_MASK_COMPACT, pxi * CI * e + G + 4 * P, 0, 2 * pxi * CI, 0);
+        } else {
+            p.add(LASNET_K_MASK, pxi * CI * e + G, 0, 2 * pxi * CI, 0);
+            p.add(LASNET_K_COMPACT, G + 4 * P, 0, 0, 0);
+        }
         if (st > 1) p.add(LASNET_K_SUBSAMPLE, 2 * px * CI * e, 0, 0, 0);
         const double ts = ceil_div(px, 128) * (CO / 128);
         p.add(LASNET_K_SHORTCUT, px * CI * e + px * CO * e + CO * CI * e + G, ts * 256 * CI * e, 2 * px * CI * CO, ts);
