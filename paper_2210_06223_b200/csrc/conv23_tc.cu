@@ -166,14 +166,14 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(bar_t2full + 8 * a, 1);
-            mbar_init(bar_t2empty + 8 * a, 128 * kPeers);
+            mbar_init(bar_t2empty + 8 * a, PAIR ? 4 * kPeers : 128);  // epi2 threads (pair: one per warp)
         }
         for (int a = 0; a < kAcc3; ++a) {
             mbar_init(bar_t3full + 8 * a, 1);
-            mbar_init(bar_t3empty + 8 * a, 256 * kPeers);
+            mbar_init(bar_t3empty + 8 * a, PAIR ? 8 * kPeers : 256);  // epi3 threads (pair: one per warp)
         }
         for (int a = 0; a < 2; ++a) {
-            mbar_init(bar_h2full + 8 * a, 128 * kPeers);
+            mbar_init(bar_h2full + 8 * a, PAIR ? 4 * kPeers : 128);
             mbar_init(bar_h2empty + 8 * a, 1);
         }
         fence_mbar_init();
@@ -447,9 +447,19 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
             }
             tc_fence_before();
             fence_proxy_async_smem();  // generic smem writes -> visible to tcgen05.mma
-            if (PAIR) {  // the lead CTA's MMA waits for both CTAs
-                mbar_arrive_cluster(bar_t2empty + 8 * acc, 0);
-                mbar_arrive_cluster(bar_h2full + 8 * (i % kH2Bufs), 0);
+            if (PAIR) {
+                // the lead CTA's MMA waits for both CTAs: one arrival per warp (a remote
+                // release arrive per thread costs a cluster-scope membar each)
+                __syncwarp();
+                if (lane == 0) {
+                    if (lead) {
+                        mbar_arrive(bar_t2empty + 8 * acc);
+                        mbar_arrive(bar_h2full + 8 * (i % kH2Bufs));
+                    } else {
+                        mbar_arrive_cluster(bar_t2empty + 8 * acc, 0);
+                        mbar_arrive_cluster(bar_h2full + 8 * (i % kH2Bufs), 0);
+                    }
+                }
             } else {
                 mbar_arrive(bar_t2empty + 8 * acc);
                 mbar_arrive(bar_h2full + 8 * (i % kH2Bufs));
@@ -541,8 +551,15 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
                 if (part == spc - 1) {
                     tc_fence_before();
                     // accumulator drained into registers
-                    if (PAIR) mbar_arrive_cluster(bar_t3empty + 8 * buf, 0);
-                    else mbar_arrive(bar_t3empty + 8 * buf);
+                    if (PAIR) {
+                        __syncwarp();
+                        if (lane == 0) {
+                            if (lead) mbar_arrive(bar_t3empty + 8 * buf);
+                            else mbar_arrive_cluster(bar_t3empty + 8 * buf, 0);
+                        }
+                    } else {
+                        mbar_arrive(bar_t3empty + 8 * buf);
+                    }
                 }
                 // all smem loads first (smem latency is long under UMMA/TMA traffic), then math, then stores
                 uint32_t rv[4][4];

@@ -71,7 +71,11 @@ constexpr int kChunkBytes = kBM * 128;  // one 64-column bf16 chunk of a 128-row
 
 // Per-mode configuration.  Warp roles: [0, E) epilogue, E TMA producer,
 // E+1 MMA issuer, E+2 .. E+9 cp.async gather (conv1 dyn only).
-template <int MODE, int BN> struct Cfg {
+// PAIR: the two CTAs of a cluster pair run 2-SM UMMAs (cta_group::2, M = 256):
+// each stages its own 128 A rows but only HALF of the BN weight rows of every
+// K-block, so the weight bytes each SM pulls through L2 halve (the TMA/L2 path,
+// ~43 B/clk/SM, bounds a 128 x 256 tile that re-streams all of B: 64 B/clk).
+template <int MODE, int BN, bool PAIR = false> struct Cfg {
     static constexpr bool kResid = MODE == CONV3_DYN || MODE == CONV3_DENSE;
     static constexpr bool kGather = MODE == CONV1_DYN;
     static constexpr bool kMasker = MODE == CONV1_DENSE_MASK;
@@ -82,7 +86,8 @@ template <int MODE, int BN> struct Cfg {
     static constexpr int kThreads =
         32 * (kEpiWarps + 2) + (kGather ? kGatherThreads : 0) + (kMasker ? kMaskerThreads : 0);
     // stem: B is the 64-channel weight (its BN = 128 spans two output rows' accumulators)
-    static constexpr int kBBytes = (MODE == STEM ? 64 : BN) * kBK * 2;
+    static constexpr int kBBytes = (MODE == STEM ? 64 : (PAIR ? BN / 2 : BN)) * kBK * 2;
+    static_assert(!PAIR || (MODE != STEM && MODE != CONV1_DYN), "pairs: TMA-fed modes only");
     // stem: the whole packed weight (7 K-blocks of 64 x 64, 56 KB) stays resident in smem,
     // loaded once per CTA; its stages carry A only (it was L2-throughput bound re-streaming it)
     static constexpr bool kBRes = MODE == STEM;
@@ -96,8 +101,10 @@ template <int MODE, int BN> struct Cfg {
     // per clock; 3 stages of 48 KB + one 64 KB staging tile
     static_assert(BN != 256 || !kResid, "BN = 256 only without the residual epilogue");
     static constexpr int kStaging = BN == 256 ? 1 : (kGather ? 1 : (kResid ? 3 : 2));
+    // pairs: stages of 32 KB (BN 256) / 24 KB (BN 128) -> deeper rings in the same smem
     static constexpr int kStages =
-        BN == 256 ? 3 : (kGather ? (BN == 128 ? 6 : 8) : (kResid ? 3 : (BN == 128 ? 4 : 6)));
+        PAIR ? (BN == 256 ? 4 : (kResid ? 4 : 6))
+             : (BN == 256 ? 3 : (kGather ? (BN == 128 ? 6 : 8) : (kResid ? 3 : (BN == 128 ? 4 : 6))));
     static constexpr int kTmemCols = 2 * BN;
     static constexpr int kStageOff = kBResBytes;  // [resident B][stages][staging][barriers][bias (+wm)]
     static constexpr int kStagingOff = kStageOff + kStages * kStageBytes;
@@ -111,6 +118,19 @@ template <int MODE, int BN> struct Cfg {
 };
 
 template <int MODE, int BN> __host__ __device__ constexpr int threads_of() { return Cfg<MODE, BN>::kThreads; }
+
+// Persistent tile walk.  One CTA: unit u = tile u.  Pair: unit u = (M-tile pair,
+// N tile); rank r of the cluster takes M tile 2 * pair + r (a tile past the end,
+// odd M-tile count, still runs: zero-filled / never-stored rows).
+struct TileWalk {
+    int first, step, units, nn, rank;
+    bool pair;
+    __device__ __forceinline__ int tile(int u) const {
+        if (!pair) return u;
+        const int pm = u / nn;
+        return (2 * pm + rank) * nn + (u - pm * nn);
+    }
+};
 
 // Tile geometry shared by all roles.
 struct TileGeo {
@@ -135,9 +155,9 @@ __device__ __forceinline__ TileGeo tile_geo(const ConvArgs &a, int BN) {
     return g;
 }
 
-template <int MODE, int BN>
+template <int MODE, int BN, bool PAIR = false>
 __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(const __grid_constant__ ConvArgs args) {
-    using C = Cfg<MODE, BN>;
+    using C = Cfg<MODE, BN, PAIR>;
     constexpr int ST = C::kStages, NSTG = C::kStaging, EPI = C::kEpiWarps * 32;
     constexpr bool kResid = C::kResid;
     extern __shared__ uint8_t smem_raw[];
@@ -157,6 +177,8 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
+    const int rank = PAIR ? (int)cluster_ctarank() : 0;
+    const bool lead = rank == 0;
 
     for (int i = tid; i < args.N; i += C::kThreads) bias_s[i] = args.bias[i];
     // masker weight (CONV1_DENSE_MASK); N % 64 == 0 keeps it 16-B aligned
@@ -170,8 +192,8 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             mbar_init(bar_empty + 8 * s, C::kMasker ? 1 + C::kMaskerThreads / 32 : 1);  // tcgen05.commit (+ every masker warp)
         }
         for (int a = 0; a < 2; ++a) {
-            mbar_init(bar_tfull + 8 * a, 1);     // tcgen05.commit
-            mbar_init(bar_tempty + 8 * a, EPI);  // every epilogue thread
+            mbar_init(bar_tfull + 8 * a, 1);     // tcgen05.commit (pair: the lead's, multicast)
+            mbar_init(bar_tempty + 8 * a, PAIR ? 2 * C::kEpiWarps : EPI);  // every epilogue thread (pair: warp of both CTAs)
             mbar_init(bar_sempty + 8 * a, 1);    // store thread, after the TMA store read smem
         }
         mbar_init(bar_bres, 1);
@@ -182,9 +204,13 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
         tma_prefetch_desc(&args.tmap_b);
         if (!kResid && MODE != STEM) tma_prefetch_desc(&args.tmap_out);
     }
-    if (warp == C::kMmaWarp) tmem_alloc<C::kTmemCols>(smem_u32(tmem_slot));
+    if (warp == C::kMmaWarp) {
+        if (PAIR) tmem_alloc_pair<C::kTmemCols>(smem_u32(tmem_slot));
+        else tmem_alloc<C::kTmemCols>(smem_u32(tmem_slot));
+    }
     tc_fence_before();
-    __syncthreads();
+    if (PAIR) cluster_sync();  // the peer's barriers are initialised before any remote arrive / TMA
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -192,6 +218,20 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
     pdl_trigger();
 
     const TileGeo geo = tile_geo<MODE>(args, BN);
+    TileWalk walk;
+    walk.pair = PAIR;
+    walk.rank = rank;
+    walk.nn = geo.n_tiles_n;
+    if (PAIR) {
+        const int mt_all = geo.num_tiles / geo.n_tiles_n;
+        walk.first = blockIdx.x >> 1;
+        walk.step = gridDim.x >> 1;
+        walk.units = (mt_all + 1) / 2 * geo.n_tiles_n;
+    } else {
+        walk.first = blockIdx.x;
+        walk.step = gridDim.x;
+        walk.units = geo.num_tiles;
+    }
     // stem: a tile is TWO output rows (2 oy0, 2 oy0 + 1 -> accumulator columns 0-63 / 64-127);
     // its K loop walks the 9 input rows they need, each staged once and used by both rows'
     // MMAs (kernel row j for the first, j - 2 for the second): 9 instead of 14 row loads
@@ -208,7 +248,8 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     tma_load_2d(sbase + kb * C::kBBytes, &args.tmap_b, bar_bres, kb * kBK, 0);
             }
             int it = 0, lt = 0;
-            for (int tile = blockIdx.x; tile < geo.num_tiles; tile += gridDim.x, ++lt) {
+            for (int u = walk.first; u < walk.units; u += walk.step, ++lt) {
+                const int tile = walk.tile(u);
                 const int mt = tile / geo.n_tiles_n;
                 const int n0 = (tile - mt * geo.n_tiles_n) * BN;
                 const int u0 = MODE == CONV2_DYN ? mt * args.units_per_tile : 0;  // first patch (conv2 dyn)
@@ -225,6 +266,33 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     if (C::kGather) a_bytes = 0;
                     else if (MODE == STEM) a_bytes = args.cols_w * 128;  // 4 boxes of cols_w / 4 columns
                     else if (MODE == CONV2_DYN || MODE == CONV2_DENSE) a_bytes = args.box_rows * 128;
+                    if (PAIR) {
+                        // own A rows + own half of the B rows; both CTAs' bytes complete on the lead's barrier
+                        if (lead) mbar_arrive_expect_tx(fb, 2 * (a_bytes + C::kBBytes));
+                        tma_load_2d_pair(sb, &args.tmap_b, fb, kb * kBK, n0 + rank * (BN / 2));
+                        if (MODE == CONV2_DYN) {
+                            const int tap = kb / kpt, dy = tap / 3, dx = tap - dy * 3;
+                            if (args.conv_stride == 2)
+                                tma_load_5d_pair(sa, &args.tmap_s[((dy & 1) << 1) | (dx & 1)], fb, 0, dx >> 1, dy >> 1,
+                                                 u0, kb - tap * kpt);
+                            else
+                                tma_load_5d_pair(sa, &args.tmap_a, fb, 0, dx, dy, u0, kb - tap * kpt);
+                        } else if (MODE == CONV2_DENSE) {
+                            const int tap = kb / kpt, dy = tap / 3, dx = tap - dy * 3;
+                            if (args.conv_stride == 2) {
+                                const int v = ((dy != 1) << 1) | (dx != 1);
+                                tma_load_5d_pair(sa, &args.tmap_s[v], fb, 0, d2x - (dx == 0), d2y - (dy == 0), d2n,
+                                                 kb - tap * kpt);
+                            } else {
+                                tma_load_5d_pair(sa, &args.tmap_a, fb, 0, d2x + dx - 1, d2y + dy - 1, d2n, kb - tap * kpt);
+                            }
+                        } else if (args.a2_kb && kb >= args.a2_kb) {
+                            tma_load_2d_pair(sa, &args.tmap_s[0], fb, (kb - args.a2_kb) * kBK, mt * kBM);
+                        } else {
+                            tma_load_2d_pair(sa, &args.tmap_a, fb, kb * kBK, mt * kBM);
+                        }
+                        continue;
+                    }
                     mbar_arrive_expect_tx(fb, a_bytes + (C::kBRes ? 0 : C::kBBytes));
                     if (!C::kBRes) tma_load_2d(sb, &args.tmap_b, fb, kb * kBK, n0);
                     KTRACE(it, 1);
@@ -348,11 +416,20 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
         const int mt = tid - 32 * C::kMaskerWarp0;
         const int r = mt >> 1, h = mt & 1;
         int it = 0;
-        for (int tile = blockIdx.x; tile < geo.num_tiles; tile += gridDim.x) {
+        for (int u = walk.first; u < walk.units; u += walk.step) {
+            const int tile = walk.tile(u);
             float acc0 = 0.f, acc1 = 0.f, mag0 = 0.f, mag1 = 0.f;
             for (int kb = 0; kb < num_kb; ++kb, ++it) {
                 const int stage = it % ST;
-                mbar_wait(bar_full + 8 * stage, (it / ST) & 1);
+                // pair: the peer's full barrier is relayed by the lead's MMA thread (cluster scope)
+                if (PAIR && !lead) {
+                    mbar_wait_cluster(bar_full + 8 * stage, (it / ST) & 1);
+                } else {
+                    mbar_wait(bar_full + 8 * stage, (it / ST) & 1);
+                    // the peer's maskers: relayed by one lead masker thread (a remote release
+                    // arrive on the MMA thread's path measured ~0.5 us per K-block)
+                    if (PAIR && mt == 0) mbar_arrive_cluster(bar_full + 8 * stage, 1);
+                }
                 const uint32_t row = sbase + C::kStageOff + stage * C::kStageBytes + r * 128;
                 uint32_t q[4][4];
 #pragma unroll
@@ -386,13 +463,14 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
         }
     } else if (warp == C::kMmaWarp) {
         // ---------------------------------------------------- MMA issuer --
-        if (lane == 0) {
-            constexpr uint32_t idesc = idesc_bf16_f32(kBM, BN);
+        if (lane == 0 && lead) {
+            constexpr uint32_t idesc = idesc_bf16_f32(PAIR ? 2 * kBM : kBM, BN);
             if (C::kBRes) mbar_wait(bar_bres, 0);
             int it = 0, lt = 0;
-            for (int tile = blockIdx.x; tile < geo.num_tiles; tile += gridDim.x, ++lt) {
+            for (int u = walk.first; u < walk.units; u += walk.step, ++lt) {
                 const int acc = lt & 1;
-                mbar_wait(bar_tempty + 8 * acc, ((lt >> 1) & 1) ^ 1);
+                if (PAIR) mbar_wait_cluster(bar_tempty + 8 * acc, ((lt >> 1) & 1) ^ 1);
+                else mbar_wait(bar_tempty + 8 * acc, ((lt >> 1) & 1) ^ 1);
                 tc_fence_after();
                 TRACE(lt, 2);
                 const uint32_t d_tmem = tmem_base + acc * BN;
@@ -422,12 +500,20 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                         continue;
                     }
                     const uint64_t bdesc = smem_desc_sw128(C::kBRes ? sbase + kb * C::kBBytes : sa + kABytes);
+                    if (PAIR) {
+#pragma unroll
+                        for (int kk = 0; kk < kBK / 16; ++kk)
+                            mma_bf16_pair(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kb | kk) != 0);
+                        mma_commit_pair_mc(bar_empty + 8 * stage, 3);
+                        continue;
+                    }
 #pragma unroll
                     for (int kk = 0; kk < kBK / 16; ++kk)
                         mma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kb | kk) != 0);
                     mma_commit(bar_empty + 8 * stage);
                 }
-                mma_commit(bar_tfull + 8 * acc);
+                if (PAIR) mma_commit_pair_mc(bar_tfull + 8 * acc, 3);
+                else mma_commit(bar_tfull + 8 * acc);
                 TRACE(lt, 3);
             }
         }
@@ -486,18 +572,21 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             cp_async_commit();
         };
         int lt = 0;
+        // tile of the local unit u (past the end: an invalid tile, nothing staged or stored)
+        auto tile_at = [&](int u) -> int { return u < walk.units ? walk.tile(u) : geo.num_tiles; };
         int pix_ring[NSTG];  // output pixel of this thread's row for tiles lt .. lt+NSTG-2 (rotated)
 #pragma unroll
         for (int k = 0; k < NSTG; ++k) pix_ring[k] = -1;
         if (kResid) {  // residual of the first NSTG-1 tiles
 #pragma unroll
             for (int k = 0; k < NSTG - 1; ++k) {
-                const int tl = blockIdx.x + k * gridDim.x;
+                const int tl = tile_at(walk.first + k * walk.step);
                 pix_ring[k] = cell_pixel(tl, row_cell(tl));
                 prefetch_resid(tl, pix_ring[k], staging + k * C::kStagingBytes);
             }
         }
-        for (int tile = blockIdx.x; tile < geo.num_tiles; tile += gridDim.x, ++lt) {
+        for (int u = walk.first; u < walk.units; u += walk.step, ++lt) {
+            const int tile = walk.tile(u);
             const int mt = tile / geo.n_tiles_n;
             const int n0 = (tile - mt * geo.n_tiles_n) * BN;
             const int acc = lt & 1, b = lt % NSTG;
@@ -517,7 +606,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             }
             int cell_ahead = -2;
             if (kResid) {
-                cell_ahead = row_cell(tile + (NSTG - 1) * gridDim.x);  // idx load in flight during this tile
+                cell_ahead = row_cell(tile_at(u + (NSTG - 1) * walk.step));  // idx load in flight during this tile
                 cp_async_wait<NSTG - 2>();  // this tile's residual has landed
                 __syncwarp();
             } else {
@@ -566,7 +655,15 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                 }
             }
             tc_fence_before();
-            mbar_arrive(bar_tempty + 8 * acc);
+            if (PAIR) {  // the lead's MMA waits for the epilogue warps of both CTAs
+                __syncwarp();
+                if (lane == 0) {
+                    if (lead) mbar_arrive(bar_tempty + 8 * acc);
+                    else mbar_arrive_cluster(bar_tempty + 8 * acc, 0);
+                }
+            } else {
+                mbar_arrive(bar_tempty + 8 * acc);
+            }
             if (kResid && MODE == CONV3_DENSE && args.tma_y) {
                 // dense rows: the staged (128-B swizzled) tile is y's rows [mt*128, +128) --
                 // one TMA store per 64-column chunk (rows past the end are clipped); the
@@ -601,7 +698,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             }
             if (kResid) {
                 // residual prefetch for tile lt+NSTG-1 into the buffer tile lt-1 used
-                const int ahead = tile + (NSTG - 1) * gridDim.x;
+                const int ahead = tile_at(u + (NSTG - 1) * walk.step);
                 const int slot = (lt + NSTG - 1) % NSTG;
 #pragma unroll
                 for (int k = 0; k + 1 < NSTG - 1; ++k) pix_ring[k] = pix_ring[k + 1];
@@ -651,49 +748,97 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
     }
 
     tc_fence_before();
-    __syncthreads();
+    // pair: no CTA leaves while its peer may still arrive on its barriers or its MMAs write its TMEM
+    if (PAIR) cluster_sync();
+    else __syncthreads();
     if (warp == C::kMmaWarp) {
         tc_fence_after();
-        tmem_dealloc<C::kTmemCols>(tmem_base);
+        if (PAIR) tmem_dealloc_pair<C::kTmemCols>(tmem_base);
+        else tmem_dealloc<C::kTmemCols>(tmem_base);
     }
 }
 
 // ----------------------------------------------------------------- host ----
 
-template <int MODE, int BN>
+template <int MODE, int BN, bool PAIR>
 static cudaError_t launch_mode_bn(const ConvArgs &a, int max_tiles_m, int num_sms, cudaStream_t st) {
-    auto kern = conv_tc_kernel<MODE, BN>;
-    const int smem = Cfg<MODE, BN>::smem_bytes(a.N, a.K);
+    auto kern = conv_tc_kernel<MODE, BN, PAIR>;
+    const int smem = Cfg<MODE, BN, PAIR>::smem_bytes(a.N, a.K);
     static int configured = 0;  // per instantiation: largest dynamic smem enabled so far
     if (smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         configured = smem;
     }
+    if (PAIR) {  // whole pairs, at most one CTA per SM
+        const long units = (long)(max_tiles_m + 1) / 2 * (a.N / BN);
+        const int cap = num_sms / 2;
+        const int pairs = (int)(units < cap ? (units > 0 ? units : 1) : cap);
+        return launch_k_cluster(kern, dim3(2 * pairs), dim3(threads_of<MODE, BN>()), smem, st, 2, a);
+    }
     const long tiles = (long)max_tiles_m * (a.N / BN);
     const int grid = (int)(tiles < num_sms ? (tiles > 0 ? tiles : 1) : num_sms);
     return launch_k(kern, dim3(grid), dim3(threads_of<MODE, BN>()), smem, st, a);
 }
 
-// conv2 (dynamic) stays on 128-column tiles: 256-column tiles measured no faster
+// LASNET_TC_PAIR (bit mask, default 8): 2-SM pairs for 1 = 256-column conv1 tiles,
+// 8 = 256-column conv2 tiles, 16 = 128-column conv2 tiles, 2 = conv3 (128-column tiles),
+// 4 = 128-column conv1 tiles
+static int pair_bits() {
+    static const int bits = [] {
+        const char *e = getenv("LASNET_TC_PAIR");
+        return e ? atoi(e) : 8;
+    }();
+    return bits;
+}
+
+// conv2 (dynamic) without pairs stays on 128-column tiles: 256-column tiles measured no faster
 // (stage-3 blocks of LAS-R101: 1.121 vs 1.115 ms over 26 launches); LASNET_CONV2_BN=256 opts in
-inline bool bn256_enabled(int mode) {
-    static const bool conv2_256 = [] {
+static bool conv2_bn256() {
+    static const bool on = [] {
         const char *e = getenv("LASNET_CONV2_BN");
         return e && atoi(e) == 256;
     }();
-    return mode != CONV2_DYN || conv2_256;
+    return on;
+}
+
+// N tile of a conv_tc launch and whether it runs on CTA pairs; the host encodes the
+// weight (B) box with bn / 2 rows for a pair (each CTA stages half of the N rows).
+int conv_tc_plan(int mode, int n, int *pair) {
+    *pair = 0;
+    if (n % 128 != 0) return 64;  // 64-column N tiles
+    const bool c1 = mode == CONV1_DENSE || mode == CONV1_DENSE_MASK, c2 = mode == CONV2_DYN || mode == CONV2_DENSE;
+    const int bits = pair_bits();
+    *pair = 1;
+    if (n % 256 == 0 && ((c1 && (bits & 1)) || (c2 && (bits & 8)))) return 256;
+    if ((mode == CONV3_DYN || mode == CONV3_DENSE) && (bits & 2)) return 128;
+    if ((c1 && (bits & 4)) || (c2 && (bits & 16))) return 128;
+    *pair = 0;
+    // 256-column tiles: A (the gathered rows / the im2col taps) is staged once per M
+    // tile instead of once per 128-column N tile
+    if (n % 256 == 0 && (mode == CONV1_DYN || mode == CONV1_DENSE || mode == CONV1_DENSE_MASK ||
+                         (mode == CONV2_DYN && conv2_bn256())))
+        return 256;
+    return 128;
 }
 
 template <int MODE>
 static cudaError_t launch_mode(const ConvArgs &a, int max_tiles_m, int num_sms, cudaStream_t st) {
-    if (a.N % 128 != 0) return launch_mode_bn<MODE, 64>(a, max_tiles_m, num_sms, st);  // 64-column N tiles
-    if constexpr (MODE == CONV1_DYN || MODE == CONV1_DENSE || MODE == CONV1_DENSE_MASK || MODE == CONV2_DYN) {
-        // 256-column tiles: A (the gathered rows / the im2col taps) is staged once per M
-        // tile instead of once per 128-column N tile
-        if (a.N % 256 == 0 && bn256_enabled(MODE)) return launch_mode_bn<MODE, 256>(a, max_tiles_m, num_sms, st);
+    int pair = 0;
+    const int bn = conv_tc_plan(MODE, a.N, &pair);
+    if (pair != a.pair_tc) return cudaErrorInvalidValue;  // the host encoded B for the other plan
+    constexpr bool kResid = MODE == CONV3_DYN || MODE == CONV3_DENSE;
+    if constexpr (MODE != CONV1_DYN) {
+        if (pair && bn == 256) {
+            if constexpr (!kResid) return launch_mode_bn<MODE, 256, true>(a, max_tiles_m, num_sms, st);
+        }
+        if (pair && bn == 128) return launch_mode_bn<MODE, 128, true>(a, max_tiles_m, num_sms, st);
     }
-    if (a.N % 128 == 0) return launch_mode_bn<MODE, 128>(a, max_tiles_m, num_sms, st);
+    if (bn == 64) return launch_mode_bn<MODE, 64, false>(a, max_tiles_m, num_sms, st);
+    if constexpr (!kResid) {
+        if (bn == 256) return launch_mode_bn<MODE, 256, false>(a, max_tiles_m, num_sms, st);
+    }
+    if (bn == 128) return launch_mode_bn<MODE, 128, false>(a, max_tiles_m, num_sms, st);
     return cudaErrorInvalidValue;
 }
 
@@ -710,7 +855,7 @@ cudaError_t launch_conv_tc(int mode, const ConvArgs &a, int max_tiles_m, int num
         case CONV2_DENSE: return launch_mode<CONV2_DENSE>(a, max_tiles_m, num_sms, st);
         case CONV3_DENSE: return launch_mode<CONV3_DENSE>(a, max_tiles_m, num_sms, st);
         case STEM: {  // BN = 128: the two output rows' 64-channel accumulators
-            auto kern = conv_tc_kernel<STEM, 128>;
+            auto kern = conv_tc_kernel<STEM, 128, false>;
             const int smem = Cfg<STEM, 128>::smem_bytes(64, a.K);
             static int configured = 0;
             if (smem > configured) {

@@ -24,6 +24,7 @@ cudaError_t launch_mask_compact(int dtype_bf16, const void *x, const float *wm, 
                                 int C, int S, uint8_t *mask, double *logits, int32_t *idx, int32_t *count, void *ws,
                                 cudaStream_t st);
 cudaError_t launch_conv_tc(int mode, const ConvArgs &a, int max_tiles_m, int num_sms, cudaStream_t st);
+int conv_tc_plan(int mode, int n, int *pair);
 cudaError_t launch_conv_simt(int mode, const ConvArgs &a, int max_rows, cudaStream_t st);
 cudaError_t launch_subsample(const void *in, void *out, int n_img, int Ho, int Wo, int c_bytes, int stride, int num_sms,
                              cudaStream_t st);
@@ -45,6 +46,17 @@ using namespace lasnet;
 namespace {
 
 thread_local int32_t g_last_launches = 0;
+
+// Dense conv3 / shortcut epilogues TMA-store whole y tiles.  LASNET_TMA_Y=0 selects the
+// plain 16-B store epilogue instead: compute-sanitizer's initcheck does not count
+// async-proxy (TMA) stores as initialisation, so its tier runs with it off.
+int32_t tma_y_enabled() {
+    static const int32_t on = [] {
+        const char *e = getenv("LASNET_TMA_Y");
+        return (e && e[0] == '0') ? 0 : 1;
+    }();
+    return on;
+}
 thread_local void *const *g_events = nullptr;
 thread_local int32_t g_event_pairs = 0, g_event_next = 0;
 constexpr int kMaxEventNames = 4096;
@@ -273,15 +285,12 @@ void dense_tiling(ConvArgs &a, int n, int h, int w) {
     a.box_rows = a.cols_w * a.rows_h * a.imgs_box;
 }
 
-// N tile of conv_tc's launch for `mode` (must match launch_mode in conv_tc.cu)
-int bn_of(int n, int mode) {
-    if (n % 128 != 0) return 64;
-    if (n % 256 == 0 && (mode == CONV1_DYN || mode == CONV1_DENSE || mode == CONV1_DENSE_MASK)) return 256;
-    if (n % 256 == 0 && mode == CONV2_DYN) {  // opt-in (conv_tc.cu bn256_enabled)
-        const char *e = getenv("LASNET_CONV2_BN");
-        if (e && atoi(e) == 256) return 256;
-    }
-    return 128;
+// weight (B) box rows of conv_tc's launch for `mode` (conv_tc_plan: N tile, CTA pairs); sets a.pair_tc
+int b_box_rows(ConvArgs &a, int n, int mode) {
+    int pair = 0;
+    const int bn = conv_tc_plan(mode, n, &pair);
+    a.pair_tc = pair;
+    return pair ? bn / 2 : bn;
 }
 
 // Fills the TMA descriptors and tile geometry of one tcgen05 convolution and
@@ -309,7 +318,7 @@ int prepare_tc(int mode, ConvArgs &a, const lasnet_block_desc *d, const void *x,
                const void *h2, int cap) {
     const int S = d->s, hs = a.hs, C = d->c_mid;
     const uint64_t px = (uint64_t)d->n * d->h * d->w;
-    bool ok = tmap2(&a.tmap_b, a.w, a.K, a.N, 64, bn_of(a.N, mode));
+    bool ok = tmap2(&a.tmap_b, a.w, a.K, a.N, 64, b_box_rows(a, a.N, mode));
     switch (mode) {
         case CONV1_DYN: {
             // A = halo rows gathered by cp.async; h1 stored channel-chunk-major
@@ -348,7 +357,7 @@ int prepare_tc(int mode, ConvArgs &a, const lasnet_block_desc *d, const void *x,
             ok = ok && tmap2(&a.tmap_a, h2, C, px, 64, 128);
             // y rows are contiguous: the epilogue TMA-stores whole tiles (tma_y)
             ok = ok && tmap2(&a.tmap_out, a.out, a.N, px, 64, 128);
-            a.tma_y = 1;
+            a.tma_y = tma_y_enabled();
             return ok ? (int)((px + 127) / 128) : -1;
         }
     }
@@ -357,7 +366,8 @@ int prepare_tc(int mode, ConvArgs &a, const lasnet_block_desc *d, const void *x,
 
 // Steps 4+5 fused in one tcgen05 kernel (conv23_tc.cu): bf16, c_mid in {64, 128},
 // c_out a multiple of 128.  LASNET_NO_FUSE=1 in the environment selects the
-// separate conv2 / conv3 kernels (A/B measurements).
+// separate conv2 / conv3 kernels (A/B measurements).  (c_mid 256 was built as a 2-SM
+// pair variant and measured slower than the two paired / unfused kernels: DESIGN.md 8.)
 bool use_fused23(const lasnet_block_desc *d) {
     static const bool off = [] {
         const char *e = getenv("LASNET_NO_FUSE");
@@ -845,10 +855,10 @@ lasnet_status proj_dyn_forward(const lasnet_block_desc *d, const lasnet_block_we
         c.a_src = xs; c.w = w->wd; c.bias = w->bd; c.out = y; c.resid = nullptr;
         c.K = d->c_in; c.N = d->c_out; c.a_ld = d->c_in; c.out_ld = d->c_out;
         c.relu_mask = m;
-        bool ok = tmap2(&c.tmap_b, w->wd, d->c_in, d->c_out, 64, bn_of(d->c_out, CONV3_DENSE)) &&
+        bool ok = tmap2(&c.tmap_b, w->wd, d->c_in, d->c_out, 64, b_box_rows(c, d->c_out, CONV3_DENSE)) &&
                   tmap2(&c.tmap_a, xs, d->c_in, (uint64_t)po, 64, 128) &&
                   tmap2(&c.tmap_out, y, d->c_out, (uint64_t)po, 64, 128);
-        c.tma_y = 1;
+        c.tma_y = tma_y_enabled();
         if (!ok) return LASNET_ERR_CUDA;
         KernelEvents ev(st, "shortcut");
         if (launch_conv_tc(CONV3_DENSE, c, (int)((po + 127) / 128), num_sms(), st) != cudaSuccess)

@@ -88,6 +88,7 @@ struct ConvArgs {
     int32_t a2_kb;            // dense conv3: K-blocks >= a2_kb of A come from tmap_s[0] (K-concatenated sources)
     int32_t no_relu;          // 1: the epilogue stores acc + bias (+ residual) without ReLU (projection shortcut)
     int32_t pair;             // fused conv2+conv3: 2-SM UMMAs over CTA pairs (cluster = 2, weight boxes of half height)
+    int32_t pair_tc;          // conv_tc: 2-SM UMMAs over CTA pairs (conv_tc_plan; weight box of bn / 2 rows)
     int32_t balance;          // dynamic fused conv23: spread the active cells evenly over whole rounds of tiles
     int32_t direct;           // dynamic conv2 (fused conv23): A patches read straight from the dense h1
                               // [c_mid/64][N][H][W][64] by one {64, S, S} TMA box per active cell (no gather)

@@ -108,3 +108,28 @@ def test_balanced_tiles_many_rounds(sched, s):
         bm = margin_bias(l0, r)
         y, m, idx, count = L.block_forward(x.cuda(), to_dev(wts), wm.cuda(), bm, s, sched)
         _check_block(x, wts, wm, bm, s, y.cpu(), m.cpu().numpy(), idx.cpu().numpy(), int(count.item()))
+
+
+def test_stage3_wide_pairs_many_rounds():
+    """LAS-R101 stage-3 shape (14x14x1024, c_mid 256, S = 2): the fused conv23 on
+    2-SM pairs (c_mid 256) and the paired conv2 tiles, with more 256-row pair
+    tiles than the 74 pairs of the grid (N = 128 at r = 0.9: ~176 tiles), every
+    element against the oracle; then the dense comparator at N = 96 (192 tiles)."""
+    n, h, w, c_in, c_mid, s = 128, 14, 14, 1024, 256, 2
+    x, wts, wm = make_case(n, h, w, c_in, c_mid, s, seed=610)
+    xd = synth.to_f64(x)
+    _, l0 = oracle.masker(xd, synth.to_f64(wm), 0.0, s)
+    bm = margin_bias(l0, 0.9)
+    for sched in (L.SCHED_FUSED, L.SCHED_SEPARATE):
+        y, m, idx, count = L.block_forward(x.cuda(), to_dev(wts), wm.cuda(), bm, s, sched)
+        cnt, _ = _check_block(x, wts, wm, bm, s, y.cpu(), m.cpu().numpy(), idx.cpu().numpy(), int(count.item()))
+        assert (cnt + 31) // 32 > 2 * 74, "must run more pair tiles than pairs"
+    nd = 96
+    xs = x[:nd].contiguous()
+    yd = L.dense_block(xs.cuda(), to_dev(wts))
+    from concurrent.futures import ThreadPoolExecutor  # images are independent: one oracle call per image
+    xsd, wd = synth.to_f64(xs), synth.weights_f64(wts)
+    with ThreadPoolExecutor(16) as ex:
+        want = np.concatenate(list(ex.map(lambda i: oracle.static_block(xsd[i:i + 1], wd, rmode=oracle.ROUND_BF16),
+                                          range(nd))))
+    assert max_abs_rel(synth.to_f64(yd.cpu()), want) <= BF16_TOL

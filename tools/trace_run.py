@@ -8,18 +8,20 @@ import torch
 sys.path.insert(0, ".")
 import synth  # noqa: E402
 from paper_2210_06223_b200 import _lib, build  # noqa: E402
+import paper_2210_06223_b200 as L  # noqa: E402
 
 path = build.build(trace=True)
 lib = _lib.load(path)
 lib.lasnet_trace_read.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
 lib.lasnet_trace_clear.argtypes = [ctypes.c_int]
 lib.lasnet_ktrace_read.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
-import paper_2210_06223_b200 as L  # noqa: E402
-
 n, h, w, c, cm, s = 128, 28, 28, 512, 128, int(sys.argv[1]) if len(sys.argv) > 1 else 4
+if len(sys.argv) > 2:  # n,h,w,c,cm (e.g. 256,14,14,1024,256 for the LAS-R101 stage-3 block)
+    n, h, w, c, cm = (int(v) for v in sys.argv[2].split(","))
+sched = L.SCHED_FUSED if len(sys.argv) > 3 and sys.argv[3] == "fused" else None
 x = synth.make_x(n, h, w, c, seed=0).cuda()
 blk = L.DynBlock(L.BlockShape(n, h, w, c, cm, s), synth.make_block_weights(c, cm, c, seed=1),
-                 synth.make_masker_weights(c, seed=2), 0.0)
+                 synth.make_masker_weights(c, seed=2), 0.0, schedule=sched)
 blk.calibrate_bias(synth.make_x(n, h, w, c, seed=1000).cuda(), 0.5)
 y = x.clone()
 y2 = torch.empty_like(x)
@@ -60,8 +62,9 @@ if hasattr(lib, "lasnet_trace23_read"):
         for c in range(64):
             if tc[c, 0]:
                 print(f"   {c:5d} " + " ".join(f"{(v - t0) / 1e3:7.2f}" if v else "    nan" for v in tc[c, :10]))
-names = {0: "conv1_dyn", 1: "conv2_dyn", 2: "conv3_dyn", 3: "conv1_dense", 4: "conv2_dense", 5: "conv3_dense"}
-for mode in range(6):
+names = {0: "conv1_dyn", 1: "conv2_dyn", 2: "conv3_dyn", 3: "conv1_dense", 4: "conv2_dense", 5: "conv3_dense",
+         6: "conv1_mask"}
+for mode in range(7):
     for _ in range(2):
         y.copy_(x)
         blk.forward(y)
@@ -84,7 +87,7 @@ for mode in range(6):
             continue
         row = [(v - t0) / 1e3 if v > 0 else float('nan') for v in t[i, :7]]
         print(f"   {i:4d} " + " ".join(f"{v:7.2f}" for v in row))
-    if mode in (0, 2, 3):
+    if mode in (0, 2, 3, 6):
         kb = (ctypes.c_ulonglong * 512)()
         lib.lasnet_ktrace_read(kb)
         k = np.array(kb, dtype=np.int64).reshape(128, 4)
