@@ -318,7 +318,7 @@ typedef enum {
     LASNET_K_MASK_COMPACT = 0, LASNET_K_CONV1_DYN, LASNET_K_CONV1_MASK, LASNET_K_DECIDE, LASNET_K_DECIDE_GATHER,
     LASNET_K_CONV23, LASNET_K_CONV23_DIRECT, LASNET_K_CONV2_DYN, LASNET_K_CONV3_DYN, LASNET_K_CONV1_DENSE,
     LASNET_K_CONV2_DENSE, LASNET_K_CONV3_DENSE, LASNET_K_CONV23_DENSE, LASNET_K_SUBSAMPLE, LASNET_K_SHORTCUT,
-    LASNET_K_MASK, LASNET_K_COMPACT, LASNET_K_COUNT
+    LASNET_K_MASK, LASNET_K_COMPACT, LASNET_K_CONV2_GATHER, LASNET_K_COUNT
 } lasnet_kernel_type;
 #define LASNET_SCHED_DENSE 2
 typedef struct {

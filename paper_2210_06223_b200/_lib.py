@@ -32,7 +32,7 @@ EXPORTS = [
 
 # lasnet_schedule (SCHED_DENSE: predictor only, the static block)
 SCHED_SEPARATE, SCHED_FUSED, SCHED_DENSE = 0, 1, 2
-K_COUNT = 17
+K_COUNT = 18
 
 
 class HW(ctypes.Structure):

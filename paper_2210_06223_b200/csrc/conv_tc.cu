@@ -77,7 +77,7 @@ constexpr int kChunkBytes = kBM * 128;  // one 64-column bf16 chunk of a 128-row
 // ~43 B/clk/SM, bounds a 128 x 256 tile that re-streams all of B: 64 B/clk).
 template <int MODE, int BN, bool PAIR = false> struct Cfg {
     static constexpr bool kResid = MODE == CONV3_DYN || MODE == CONV3_DENSE;
-    static constexpr bool kGather = MODE == CONV1_DYN;
+    static constexpr bool kGather = MODE == CONV1_DYN || MODE == CONV2_GATHER;
     static constexpr bool kMasker = MODE == CONV1_DENSE_MASK;
     static constexpr int kEpiWarps = kResid ? 8 : 4;
     static constexpr int kProdWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1, kGatherWarp0 = kEpiWarps + 2;
@@ -87,7 +87,9 @@ template <int MODE, int BN, bool PAIR = false> struct Cfg {
         32 * (kEpiWarps + 2) + (kGather ? kGatherThreads : 0) + (kMasker ? kMaskerThreads : 0);
     // stem: B is the 64-channel weight (its BN = 128 spans two output rows' accumulators)
     static constexpr int kBBytes = (MODE == STEM ? 64 : (PAIR ? BN / 2 : BN)) * kBK * 2;
-    static_assert(!PAIR || (MODE != STEM && MODE != CONV1_DYN), "pairs: TMA-fed modes only");
+    // (a cp.async-fed pair needs a relay of the peer's stage to the lead's barrier: measured
+    // 45 -> 65 us for the stage-3 conv2, so the gather modes run one CTA per tile)
+    static_assert(!PAIR || (MODE != STEM && !kGather), "pairs: TMA-fed modes only");
     // stem: the whole packed weight (7 K-blocks of 64 x 64, 56 KB) stays resident in smem,
     // loaded once per CTA; its stages carry A only (it was L2-throughput bound re-streaming it)
     static constexpr bool kBRes = MODE == STEM;
@@ -143,7 +145,7 @@ __device__ __forceinline__ TileGeo tile_geo(const ConvArgs &a, int BN) {
     TileGeo g;
     g.n_tiles_n = a.N / BN;
     int mt;
-    if (MODE == CONV2_DYN) {
+    if (MODE == CONV2_DYN || MODE == CONV2_GATHER) {
         mt = (*a.count + a.units_per_tile - 1) / a.units_per_tile;  // patch-aligned tiles
     } else if (MODE == CONV2_DENSE || MODE == STEM) {
         mt = a.dense_tiles;
@@ -335,6 +337,79 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             }
         }
     } else if (C::kGather && warp >= C::kGatherWarp0) {
+        if constexpr (MODE == CONV2_GATHER) {
+            // ------------------------- cp.async im2col gather from the dense h1 --
+            // thread -> (row group prow, 16-B chunk pch); tile rows prow + 32 i, i < 4: row =
+            // (patch t, pixel j of its S x S cell); K-block kb = (tap, 64-channel chunk cb) reads
+            // h1 pixel (cell origin + (py + dy - 1, px + dx - 1)) of chunk cb, 0 outside the image
+            // (conv2's zero padding, R6).  The next tile's idx loads are in flight during this
+            // tile's K-loop.
+            constexpr int RPT = 128 * 8 / C::kGatherThreads;
+            constexpr int RSTEP = 128 / RPT;
+            const int pt = tid - 32 * C::kGatherWarp0;
+            const int prow = pt >> 3, pch = pt & 7;
+            const __nv_bfloat16 *H1 = static_cast<const __nv_bfloat16 *>(args.a_src);
+            const int cnt = *args.count, ss = args.S * args.S, rows_pt = args.units_per_tile * ss;
+            auto load_cells = [&](int tile, int (&cell)[RPT]) {
+                const int mt = tile / geo.n_tiles_n;
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                    const int row = prow + RSTEP * i;
+                    const int t = mt * args.units_per_tile + args.fd_SS.div(row);
+                    cell[i] = (tile < geo.num_tiles && row < rows_pt && t < cnt) ? ld_nc_volatile(args.idx + t) : -1;
+                }
+            };
+            // base pixel (image row origin) and (y0, x0) = the output pixel's window origin
+            auto decode = [&](const int (&cell)[RPT], int (&img)[RPT], int (&y0)[RPT], int (&x0)[RPT]) {
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                    img[i] = -1;
+                    y0[i] = x0[i] = 0;
+                    if (cell[i] >= 0) {
+                        int n, gy, gx;
+                        cell_decode(args, cell[i], n, gy, gx);
+                        const int row = prow + RSTEP * i;
+                        const int j = row - args.fd_SS.div(row) * ss;
+                        const int py = args.fd_S.div(j);
+                        img[i] = n;
+                        y0[i] = gy * args.S + py - 1;
+                        x0[i] = gx * args.S + (j - py * args.S) - 1;
+                    }
+                }
+            };
+            int cell[RPT], img[RPT], y0[RPT], x0[RPT];
+            int ncell[RPT], nimg[RPT], ny0[RPT], nx0[RPT];
+            auto tile_at = [&](int u) -> int { return u < walk.units ? walk.tile(u) : geo.num_tiles; };
+            load_cells(tile_at(walk.first), cell);
+            decode(cell, img, y0, x0);
+            int it = 0;
+            for (int u = walk.first; u < walk.units; u += walk.step) {
+                load_cells(tile_at(u + walk.step), ncell);  // next tile: loads in flight during this K-loop
+                for (int kb = 0; kb < num_kb; ++kb, ++it) {
+                    const int stage = it % ST;
+                    const int tap = kb / kpt, cb = kb - tap * kpt, dy = tap / 3, dx = tap - dy * 3;
+                    mbar_wait(bar_empty + 8 * stage, ((it / ST) & 1) ^ 1);
+                    const uint32_t sa = sbase + C::kStageOff + stage * C::kStageBytes;
+                    const __nv_bfloat16 *cbase = H1 + (size_t)cb * args.m_dense * 64 + pch * 8;
+#pragma unroll
+                    for (int i = 0; i < RPT; ++i) {
+                        const int row = prow + RSTEP * i;
+                        const int yy = y0[i] + dy, xx = x0[i] + dx;
+                        const bool ok = img[i] >= 0 && yy >= 0 && yy < args.H && xx >= 0 && xx < args.W;
+                        const __nv_bfloat16 *g = ok ? cbase + (size_t)((img[i] * args.H + yy) * args.W + xx) * 64 : H1;
+                        cp_async_16(sa + row * 128 + ((pch ^ (row & 7)) << 4), g, ok ? 16u : 0u);
+                    }
+                    cp_async_arrive_noinc(bar_full + 8 * stage);
+                    if (kb == (num_kb >> 1)) decode(ncell, nimg, ny0, nx0);  // mid-loop: off the tile boundary
+                }
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                    img[i] = nimg[i];
+                    y0[i] = ny0[i];
+                    x0[i] = nx0[i];
+                }
+            }
+        } else {
         // ------------------------------------------ cp.async halo gather --
         // thread -> (row group prow, 16-B chunk pch); rows prow + 32 i, i < 4.
         // The idx loads of tile t+1 are issued before the K-loop of tile t and
@@ -400,6 +475,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
 #pragma unroll
             for (int i = 0; i < RPT; ++i) src[i] = src_next[i];
         }
+        }  // CONV1_DYN gather
     } else if (C::kMasker && warp >= C::kMaskerWarp0) {
         // -------------------------------------- masker partials (fused) --
         // 8 warps, two threads per A row (pixel): thread 2r + h reads the 16-B chunks
@@ -729,7 +805,8 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     for (int c = 0; c < BN / 64; ++c)
                         tma_store_3d(&args.tmap_out, sbuf + c * kChunkBytes, 0, mt * kBM, (n0 >> 6) + c);
                 } else {
-                    const int row0 = MODE == CONV2_DYN ? mt * args.units_per_tile * args.S * args.S : mt * kBM;
+                    const int row0 = (MODE == CONV2_DYN || MODE == CONV2_GATHER) ? mt * args.units_per_tile * args.S * args.S
+                                                                                 : mt * kBM;
                     for (int c = 0; c < BN / 64; ++c)
                         tma_store_2d(&args.tmap_out, sbuf + c * kChunkBytes, n0 + c * 64, row0);
                 }
@@ -807,7 +884,8 @@ static bool conv2_bn256() {
 int conv_tc_plan(int mode, int n, int *pair) {
     *pair = 0;
     if (n % 128 != 0) return 64;  // 64-column N tiles
-    const bool c1 = mode == CONV1_DENSE || mode == CONV1_DENSE_MASK, c2 = mode == CONV2_DYN || mode == CONV2_DENSE;
+    const bool c1 = mode == CONV1_DENSE || mode == CONV1_DENSE_MASK,
+               c2 = mode == CONV2_DYN || mode == CONV2_DENSE;
     const int bits = pair_bits();
     *pair = 1;
     if (n % 256 == 0 && ((c1 && (bits & 1)) || (c2 && (bits & 8)))) return 256;
@@ -816,7 +894,7 @@ int conv_tc_plan(int mode, int n, int *pair) {
     *pair = 0;
     // 256-column tiles: A (the gathered rows / the im2col taps) is staged once per M
     // tile instead of once per 128-column N tile
-    if (n % 256 == 0 && (mode == CONV1_DYN || mode == CONV1_DENSE || mode == CONV1_DENSE_MASK ||
+    if (n % 256 == 0 && (mode == CONV1_DYN || mode == CONV1_DENSE || mode == CONV1_DENSE_MASK || mode == CONV2_GATHER ||
                          (mode == CONV2_DYN && conv2_bn256())))
         return 256;
     return 128;
@@ -828,7 +906,7 @@ static cudaError_t launch_mode(const ConvArgs &a, int max_tiles_m, int num_sms, 
     const int bn = conv_tc_plan(MODE, a.N, &pair);
     if (pair != a.pair_tc) return cudaErrorInvalidValue;  // the host encoded B for the other plan
     constexpr bool kResid = MODE == CONV3_DYN || MODE == CONV3_DENSE;
-    if constexpr (MODE != CONV1_DYN) {
+    if constexpr (!Cfg<MODE, 128>::kGather) {
         if (pair && bn == 256) {
             if constexpr (!kResid) return launch_mode_bn<MODE, 256, true>(a, max_tiles_m, num_sms, st);
         }
@@ -849,6 +927,7 @@ cudaError_t launch_conv_tc(int mode, const ConvArgs &a, int max_tiles_m, int num
     switch (mode) {
         case CONV1_DYN: return launch_mode<CONV1_DYN>(a, max_tiles_m, num_sms, st);
         case CONV2_DYN: return launch_mode<CONV2_DYN>(a, max_tiles_m, num_sms, st);
+        case CONV2_GATHER: return launch_mode<CONV2_GATHER>(a, max_tiles_m, num_sms, st);
         case CONV3_DYN: return launch_mode<CONV3_DYN>(a, max_tiles_m, num_sms, st);
         case CONV1_DENSE: return launch_mode<CONV1_DENSE>(a, max_tiles_m, num_sms, st);
         case CONV1_DENSE_MASK: return launch_mode<CONV1_DENSE_MASK>(a, max_tiles_m, num_sms, st);

@@ -86,6 +86,7 @@ const char *conv_name(int mode) {
     switch (mode) {
         case CONV1_DYN: return "conv1_dyn";
         case CONV2_DYN: return "conv2_dyn";
+        case CONV2_GATHER: return "conv2_gather";
         case CONV3_DYN: return "conv3_dyn";
         case CONV1_DENSE: return "conv1_dense";
         case CONV2_DENSE: return "conv2_dense";
@@ -335,6 +336,14 @@ int prepare_tc(int mode, ConvArgs &a, const lasnet_block_desc *d, const void *x,
             ok = ok && tmap2(&a.tmap_out, h2, C, (uint64_t)cap * S * S, 64, a.box_rows);
             return ok ? (cap + a.units_per_tile - 1) / a.units_per_tile : -1;
         }
+        case CONV2_GATHER: {
+            // A = im2col rows gathered by cp.async from the dense h1 [C/64][px][64] (a.m_dense = px)
+            a.units_per_tile = 128 / (S * S);
+            a.box_rows = a.units_per_tile * S * S;
+            a.m_dense = (int)px;
+            ok = ok && tmap2(&a.tmap_out, h2, C, (uint64_t)cap * S * S, 64, a.box_rows);
+            return ok ? (cap + a.units_per_tile - 1) / a.units_per_tile : -1;
+        }
         case CONV3_DYN: {
             // A = h2 rows (2-D TMA); residual and scatter by the epilogue warps
             ok = ok && tmap2(&a.tmap_a, h2, C, (uint64_t)cap * S * S, 64, 128);
@@ -388,6 +397,17 @@ bool use_direct(const lasnet_block_desc *d) {
         return e && e[0] == '1';
     }();
     return !off && use_fused23(d) && d->s >= 4;
+}
+
+// Masker-fused schedule without the fused conv23 (c_mid 256 / 512: LAS-R101 stages 3-4):
+// conv2 gathers its im2col rows from the dense h1 by cp.async (CONV2_GATHER), so the decide
+// step writes only the ids (no gathered window copy).  LASNET_C2_GATHER=0 keeps the copy.
+bool use_gather2(const lasnet_block_desc *d) {
+    static const bool off = [] {
+        const char *e = getenv("LASNET_C2_GATHER");
+        return e && e[0] == '0';
+    }();
+    return !off && d->dtype == LASNET_BF16 && !use_fused23(d) && d->stride == 1;
 }
 
 cudaError_t run_conv23(const lasnet_block_desc *d, bool dense, ConvArgs a, const lasnet_block_weights *w,
@@ -524,7 +544,8 @@ size_t fwd_ws(const lasnet_block_desc *d, int schedule, uint8_t *base, FwdWs *o)
         r.sync = cv.take(decide_sync_bytes((int)ncells, num_sms()));
         r.mpart = cv.take(px * 16);
         r.h1d = cv.take(px * d->c_mid * e);
-        r.h1g = use_direct(d) ? nullptr : cv.take((size_t)ncells * (d->s + 2) * (d->s + 2) * d->c_mid * e);
+        r.h1g = (use_direct(d) || use_gather2(d)) ? nullptr
+                                                  : cv.take((size_t)ncells * (d->s + 2) * (d->s + 2) * d->c_mid * e);
         r.h2 = use_fused23(d) ? nullptr : cv.take((size_t)ncells * d->s * d->s * d->c_mid * e);
     } else {
         r.sync = cv.take(mask_compact_workspace_bytes(ncells));
@@ -556,6 +577,7 @@ namespace lasnet {
 // the library's launch plan, for the latency predictor (predictor.cu)
 bool plan_fused23(const lasnet_block_desc *d) { return use_fused23(d); }
 bool plan_direct(const lasnet_block_desc *d) { return use_direct(d); }
+bool plan_gather2(const lasnet_block_desc *d) { return use_gather2(d); }
 }  // namespace lasnet
 
 extern "C" {
@@ -967,10 +989,22 @@ lasnet_status lasnet_block_forward(const lasnet_block_desc *d, const lasnet_bloc
     b.idx = idx;
     b.count = count;
     int k = 0;
-    if (r.h1g == nullptr) {  // direct: steps 4-5 read the dense h1
+    if (r.h1g == nullptr && use_direct(d)) {  // direct: steps 4-5 read the dense h1
         b.direct = 1;
         k = 1;
         if (run_conv23(d, false, b, w, x, y, r.h1d, ncells, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    } else if (r.h1g == nullptr) {  // conv2 gathers from the dense h1, then conv3 + scatter-add
+        b.a_src = r.h1d; b.w = w->w2; b.bias = w->b2; b.out = r.h2;
+        b.K = 9 * d->c_mid; b.N = d->c_mid; b.a_ld = d->c_mid; b.out_ld = d->c_mid;
+        const int ss = d->s * d->s;
+        if (run_conv(d, CONV2_GATHER, b, ncells * ss, x, y, r.h1d, r.h2, ncells, st) != cudaSuccess)
+            return LASNET_ERR_CUDA;
+        b.a_src = r.h2; b.w = w->w3; b.bias = w->b3; b.out = y; b.resid = x;
+        b.K = d->c_mid; b.N = d->c_out; b.a_ld = d->c_mid; b.out_ld = d->c_out;
+        b.m_dense = 0;
+        if (run_conv(d, CONV3_DYN, b, ncells * ss, x, y, r.h1d, r.h2, ncells, st) != cudaSuccess)
+            return LASNET_ERR_CUDA;
+        k = 2;
     } else if (run_steps45(d, w, b, x, y, r.h1g, r.h2, ncells, st, &k) != cudaSuccess) {
         return LASNET_ERR_CUDA;
     }

@@ -34,6 +34,7 @@
 namespace lasnet {
 bool plan_fused23(const lasnet_block_desc *d);
 bool plan_direct(const lasnet_block_desc *d);
+bool plan_gather2(const lasnet_block_desc *d);
 bool plan_proj_mask_fused();
 }  // namespace lasnet
 
@@ -42,7 +43,7 @@ namespace {
 const char *const kNames[LASNET_K_COUNT] = {
     "mask_compact", "conv1_dyn", "conv1_mask", "decide", "decide+gather", "conv23", "conv23_direct", "conv2_dyn",
     "conv3_dyn", "conv1_dense", "conv2_dense", "conv3_dense", "conv23_dense", "subsample", "shortcut", "mask",
-    "compact"};
+    "compact", "conv2_gather"};
 
 struct Work {
     int type;
@@ -160,6 +161,20 @@ bool build_plan(Plan &p, const lasnet_block_desc *d, int schedule, double r) {
               t1);
         const bool direct = lasnet::plan_direct(d);
         const double h1_halo = halo * C * e;
+        if (lasnet::plan_gather2(d)) {
+            // conv2 gathers the im2col rows from the dense h1 (L2): the windows' bytes once from
+            // HBM, 9 taps re-read per tile from L2; then conv3 + scatter-add
+            p.add(LASNET_K_DECIDE, 16 * px + G + 4 * P, 0, 0, 0);
+            const double S2 = (double)d->s * d->s, rows = P * S2;
+            const double t2 = ceil_div(P, std::floor(128.0 / S2)) * (C / 256 >= 1 ? C / 256 : 1);
+            const double bn2 = (int)C % 256 == 0 ? 256 : 128;
+            p.add(LASNET_K_CONV2_GATHER, h1_halo + rows * C * e + 9 * C * C * e,
+                  t2 * (128 * 9 * C * e + 9 * C * bn2 * e), 2 * out_px * 9 * C * C, t2);
+            const double t3 = ceil_div(rows, 128) * (CO / 128);
+            p.add(LASNET_K_CONV3_DYN, rows * C * e + 2 * out_px * CO * e + CO * C * e, t3 * (128 * C * e + 128 * C * e),
+                  2 * out_px * C * CO, t3);
+            return true;
+        }
         if (direct) {
             p.add(LASNET_K_DECIDE, 16 * px + G + 4 * P, 0, 0, 0);
         } else {

@@ -39,6 +39,8 @@ enum ConvMode : int {
     CONV3_DENSE = 5,  // A = h2 rows, out = y (residual add, ReLU)
     CONV1_DENSE_MASK = 6,  // CONV1_DENSE + per-pixel masker partials (the paper's masker-conv1 fusion)
     STEM = 7,              // ResNet stem 7x7 stride 2 on 8-channel (3 + zero) input: tile = one output row
+    CONV2_GATHER = 8,      // CONV2_DYN whose A rows are gathered by cp.async straight from the DENSE h1
+                           // [c_mid/64][m_dense][64] (masker-fused schedule: no gathered window copy)
 };
 
 struct ConvArgs {
@@ -101,7 +103,7 @@ struct ConvArgs {
 
 // Total GEMM rows; dynamic modes read the device-resident active count.
 __device__ __forceinline__ int gemm_rows(int mode, const ConvArgs &a) {
-    if (mode <= CONV3_DYN) return (*a.count) * (mode == CONV1_DYN ? a.hs * a.hs : a.S * a.S);
+    if (mode <= CONV3_DYN || mode == CONV2_GATHER) return (*a.count) * (mode == CONV1_DYN ? a.hs * a.hs : a.S * a.S);
     return a.m_dense;
 }
 
