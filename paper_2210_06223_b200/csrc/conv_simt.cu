@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "launch.cuh"
 #include "rowmap.cuh"
 
 namespace lasnet {
@@ -39,6 +40,8 @@ __global__ void __launch_bounds__(kSThreads) conv_simt_kernel(const __grid_const
     __shared__ float As[2][kSBK][kSBM + 1];
     __shared__ float Bs[2][kSBK][kSBN + 1];
     __shared__ int src_s[kSBM], aux_s[kSBM], orow_s[kSBM], zero_s[kSBM];
+    pdl_wait();  // the previous kernel's outputs (x / h1 / h2, idx, count) are complete from here on
+    pdl_trigger();
     const int M = gemm_rows(MODE, a);
     const int m0 = blockIdx.x * kSBM, n0 = blockIdx.y * kSBN;
     if (m0 >= M) return;

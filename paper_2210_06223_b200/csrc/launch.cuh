@@ -6,7 +6,7 @@
 // access to memory written by an earlier kernel (griddepcontrol.wait returns
 // once the prerequisite grid has completed and its writes are visible), and
 // pdl_trigger() once it no longer needs to delay its dependents.
-// Enabled with LASNET_PDL=1 (see pdl_enabled).
+// On by default; LASNET_PDL=0 disables it (see pdl_enabled).
 #pragma once
 #include <cstdio>
 #include <cstdlib>
@@ -18,12 +18,13 @@ namespace lasnet {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-// PDL is opt-in (LASNET_PDL=1): with the block captured in a CUDA graph (bench.py's
-// timed path) it gains nothing measurable (88.7 vs 90.9 us per step).
+// PDL is on by default (LASNET_PDL=0: off): as CUDA-graph replays the LAS-R101 forward
+// takes 5.57 instead of 5.72 ms and the configs[1] block 84.0 instead of 88.1 us (round 2;
+// round 1 measured it neutral on the block before the kernels' prologues grew).
 inline bool pdl_enabled() {
     static const bool on = [] {
         const char *e = getenv("LASNET_PDL");
-        return e && e[0] == '1';
+        return !(e && e[0] == '0');
     }();
     return on;
 }
@@ -74,11 +75,13 @@ cudaError_t launch_k_coop(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t 
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeCooperative;
     at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     return debug_check(kern, cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...), st);
 }
 
