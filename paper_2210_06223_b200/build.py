@@ -14,8 +14,8 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "liblasnet.so")
 SOURCES = ["lasnet_capi.cu", "mask_compact.cu", "conv_tc.cu", "conv23_tc.cu", "conv_simt.cu", "decide_gather.cu",
            "proj_block.cu", "net_layers.cu", "predictor.cu",
-           "regnet.cu"]
-HEADERS = ["rowmap.cuh", "sm100_ptx.cuh", "launch.cuh", "predictor_b200.inc", "regnet.cuh"]
+           "regnet.cu", "small_block.cu"]
+HEADERS = ["rowmap.cuh", "sm100_ptx.cuh", "launch.cuh", "predictor_b200.inc", "regnet.cuh", "small_block.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # A/B experiments only: extra nvcc flags (e.g. -DLASNET_C23_STAGES=2); the product build sets none
 EXTRA = os.environ.get("LASNET_EXTRA_NVCC", "").split()

@@ -12,6 +12,7 @@
 
 #include "../../include/lasnet.h"
 #include "rowmap.cuh"
+#include "small_block.cuh"
 
 namespace lasnet {
 cudaError_t launch_masker(int dtype_bf16, const void *x, const float *wm, float bm, int n_img, int H, int W,
@@ -24,6 +25,7 @@ cudaError_t launch_mask_compact(int dtype_bf16, const void *x, const float *wm, 
                                 int C, int S, uint8_t *mask, double *logits, int32_t *idx, int32_t *count, void *ws,
                                 cudaStream_t st);
 cudaError_t launch_conv_tc(int mode, const ConvArgs &a, int max_tiles_m, int num_sms, cudaStream_t st);
+
 int conv_tc_plan(int mode, int n, int *pair);
 cudaError_t launch_conv_simt(int mode, const ConvArgs &a, int max_rows, cudaStream_t st);
 cudaError_t launch_subsample(const void *in, void *out, int n_img, int Ho, int Wo, int c_bytes, int stride, int num_sms,
@@ -175,9 +177,60 @@ size_t dyn_ws_bytes(const lasnet_block_desc *d, int32_t cap) {
     return align_up((size_t)cap * hs * d->c_mid * e, 256) + align_up((size_t)cap * ss * d->c_mid * e, 256);
 }
 
+// fp32 small batches: the whole block as one cooperative launch (small_block.cu) when
+// the cell and pixel lists fit a CTA's shared memory (config 1: N = 1).  LASNET_SMALL=0
+// keeps the per-step kernels.
+bool small_ok(const lasnet_block_desc *d) {
+    static const bool off = [] {
+        const char *e = getenv("LASNET_SMALL");
+        return e && e[0] == '0';
+    }();
+    const long ncells = (long)d->n * ((d->h + d->s - 1) / d->s) * ((d->w + d->s - 1) / d->s);
+    const long px = (long)d->n * d->h * d->w;
+    return !off && d->dtype == LASNET_F32 && d->stride == 1 && d->c_in == d->c_out && d->c_in % 4 == 0 &&
+           d->c_mid % 32 == 0 && d->c_out % 32 == 0 && ncells <= 4096 && px <= 8192 && ncells * d->s * d->s <= 8192;
+}
+// its workspace: barrier words (16 B, zero on entry), mask, h1 [px][c_mid], h2 [rows][c_mid]
+size_t small_ws_bytes(const lasnet_block_desc *d) {
+    const size_t ncells = (size_t)d->n * ((d->h + d->s - 1) / d->s) * ((d->w + d->s - 1) / d->s);
+    const size_t px = (size_t)d->n * d->h * d->w, rows = ncells * d->s * d->s;
+    return 256 + align_up(ncells, 256) + align_up(px * d->c_mid * 4, 256) +
+           align_up((rows > px ? rows : px) * d->c_mid * 4, 256);
+}
+SmallArgs small_args(const lasnet_block_desc *d, const lasnet_block_weights *w, const void *x, void *y, const float *wm,
+                     float bm, uint8_t *mask, int32_t *idx, int32_t *count, void *ws) {
+    SmallArgs a;
+    a.x = static_cast<const float *>(x);
+    a.y = static_cast<float *>(y);
+    a.w1 = static_cast<const float *>(w->w1); a.b1 = w->b1;
+    a.w2 = static_cast<const float *>(w->w2); a.b2 = w->b2;
+    a.w3 = static_cast<const float *>(w->w3); a.b3 = w->b3;
+    a.wm = wm;
+    a.bm = bm;
+    a.n = d->n; a.H = d->h; a.W = d->w; a.ci = d->c_in; a.cm = d->c_mid; a.co = d->c_out; a.S = d->s;
+    a.Gh = (d->h + d->s - 1) / d->s;
+    a.Gw = (d->w + d->s - 1) / d->s;
+    a.ncells = d->n * a.Gh * a.Gw;
+    a.px = d->n * d->h * d->w;
+    uint8_t *b = static_cast<uint8_t *>(ws);
+    a.bar = reinterpret_cast<unsigned *>(b);
+    b += 256;
+    uint8_t *mws = b;
+    b += align_up((size_t)a.ncells, 256);
+    a.h1 = reinterpret_cast<float *>(b);
+    b += align_up((size_t)a.px * a.cm * 4, 256);
+    a.h2 = reinterpret_cast<float *>(b);
+    a.mask = mask ? mask : mws;
+    a.idx = idx;
+    a.count = count;
+    return a;
+}
+
 size_t dense_ws_bytes(const lasnet_block_desc *d) {
     const size_t px = (size_t)d->n * d->h * d->w;
-    return 2 * align_up(px * d->c_mid * elt_size(d->dtype), 256);
+    const size_t conv = 2 * align_up(px * d->c_mid * elt_size(d->dtype), 256);
+    const size_t sm = small_ok(d) ? small_ws_bytes(d) : 0;
+    return conv > sm ? conv : sm;
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (the only
@@ -533,7 +586,7 @@ void set_windows(ConvArgs &a, int S, int st, int Hi, int Wi) {
 // Workspace of lasnet_block_forward: zero-contract control words first, then
 // scratch.  Returns the byte size; with base != NULL also the region pointers.
 struct FwdWs {
-    void *sync, *mpart, *h1d, *h1g, *h2, *sep_dyn;
+    void *sync, *mpart, *h1d, *h1g, *h2, *sep_dyn, *small;
 };
 size_t fwd_ws(const lasnet_block_desc *d, int schedule, uint8_t *base, FwdWs *o) {
     const long ncells = (long)d->n * ((d->h + d->s - 1) / d->s) * ((d->w + d->s - 1) / d->s);
@@ -550,6 +603,7 @@ size_t fwd_ws(const lasnet_block_desc *d, int schedule, uint8_t *base, FwdWs *o)
     } else {
         r.sync = cv.take(mask_compact_workspace_bytes(ncells));
         r.sep_dyn = cv.take(dyn_ws_bytes(d, (int32_t)ncells));
+        if (small_ok(d)) r.small = cv.take(small_ws_bytes(d));  // zero-contract words first
     }
     if (o) *o = r;
     return cv.used;
@@ -746,6 +800,16 @@ lasnet_status lasnet_dense_block(const lasnet_block_desc *d, const lasnet_block_
     if (d->n == 0) return LASNET_OK;
 
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (small_ok(d)) {  // small fp32 batch: conv1, conv2, conv3 + residual in one launch
+        // (the dense workspace carries no zero contract: clear the barrier words first)
+        if (cudaMemsetAsync(ws, 0, 16, st) != cudaSuccess) return LASNET_ERR_CUDA;
+        KernelEvents ev(st, "small_dense");
+        if (launch_small_block(small_args(d, w, x, y, nullptr, 0.f, nullptr, nullptr, nullptr, ws), num_sms(), st) !=
+            cudaSuccess)
+            return LASNET_ERR_CUDA;
+        g_last_launches = 1;
+        return LASNET_OK;
+    }
     Carve cv{static_cast<uint8_t *>(ws)};
     const int px = d->n * d->h * d->w;
     void *h1 = cv.take((size_t)px * d->c_mid * e);
@@ -953,6 +1017,16 @@ lasnet_status lasnet_block_forward(const lasnet_block_desc *d, const lasnet_bloc
     FwdWs r;
     fwd_ws(d, schedule, static_cast<uint8_t *>(ws), &r);
 
+    if (schedule == LASNET_SCHED_MASKER_SEPARATE && r.small) {
+        // small fp32 batch: masker, compaction, conv1 on the dilated union, conv2, conv3 in one launch
+        if (x != y && cudaMemcpyAsync(y, x, xbytes, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+            return LASNET_ERR_CUDA;
+        KernelEvents ev(st, "small_block");
+        if (launch_small_block(small_args(d, w, x, y, wm, bm, mask, idx, count, r.small), num_sms(), st) != cudaSuccess)
+            return LASNET_ERR_CUDA;
+        g_last_launches = 1;
+        return LASNET_OK;
+    }
     if (schedule == LASNET_SCHED_MASKER_SEPARATE) {
         // north-star branch: masker+compaction (one launch), then gather+conv1 on the halos, conv2, conv3
         {

@@ -38,7 +38,8 @@ def main():
     m = L.mask(x, wm, 0.0, 2)
     idx, cnt = L.compact(m)
     L.dyn_block(x.clone(), wts, idx, cnt, 2)
-    L.dense_block(x, wts)
+    L.dense_block(x, wts)  # the single-launch small-batch block (fp32)
+    L.block_forward(x.clone(), wts, wm, 0.0, 2, L.SCHED_SEPARATE)
     xp = synth.make_x(2, 16, 16, 128, seed=4).cuda()
     L.proj_block(xp, dev(synth.make_proj_weights(128, 64, 256, seed=5)), 2)
     # LAS-RegNetY: both dynamic schedules (grouped conv, SE) and a static stride-2 first block

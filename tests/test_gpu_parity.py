@@ -730,3 +730,52 @@ def test_network_batch_sharding_is_bitwise_invariant():
             a.bm = b.bm
         parts.append(half.forward(x[lo:hi].contiguous()).clone())
     assert torch.equal(torch.cat(parts), lg_full)
+
+
+# ------------------------- single-launch fp32 small-batch block (small_block.cu) --
+
+SMALL_CASES = [
+    # n, h, w, c, c_mid, s, r
+    (1, 14, 14, 256, 64, 2, 25 / 49),  # config 1
+    (2, 13, 11, 128, 64, 3, 0.5),      # clipped edge cells
+    (3, 9, 9, 128, 64, 1, 0.4),        # S = 1: pixel-level
+    (1, 14, 14, 256, 64, 4, 1.0),      # every cell active
+    (1, 14, 14, 256, 64, 2, 0.0),      # no cell active
+    (4, 14, 14, 64, 64, 7, 0.5),       # narrow widths
+]
+
+
+@pytest.mark.parametrize("n,h,w,c,c_mid,s,r", SMALL_CASES)
+def test_small_block_matches_oracle(n, h, w, c, c_mid, s, r):
+    """fp32 small batches run the whole block as ONE cooperative launch (masker,
+    compaction, conv1 once per pixel of the dilated union of the active cells,
+    conv2, conv3 + scatter-add): mask/idx/count bit-exact, y within 1e-5, inactive
+    pixels bitwise x; the dense comparator likewise against the static block."""
+    x, wts, wm = make_case(n, h, w, c, c_mid, s, seed=900 + n + s, dtype="f32")
+    xd = synth.to_f64(x)
+    _, l0 = oracle.masker(xd, synth.to_f64(wm), 0.0, s)
+    bm = margin_bias(l0, r)
+    m_or, _ = oracle.masker(xd, synth.to_f64(wm), bm, s)
+    idx_or, cnt = oracle.compact(m_or)
+    xg, wd = x.cuda(), to_dev(wts)
+    import ctypes
+    from paper_2210_06223_b200 import _lib
+    d = L.make_desc(n, h, w, c, c_mid, c, s, torch.float32)
+    ws = torch.zeros(_lib.load().lasnet_block_forward_workspace_bytes(ctypes.byref(d), L.SCHED_SEPARATE),
+                     dtype=torch.uint8, device="cuda")
+    for rep in range(3):  # repeated calls on one workspace: the barrier words are left zero
+        y, m, idx, count = L.block_forward(xg.clone(), wd, wm.cuda(), bm, s, L.SCHED_SEPARATE, ws=ws)
+        assert L.last_launch_count() == 1
+        assert np.array_equal(m.cpu().numpy(), m_or)
+        assert int(count.item()) == cnt
+        assert np.array_equal(idx[:cnt].cpu().numpy(), idx_or)
+    want = oracle.dyn_block_literal(xd, synth.weights_f64(wts), idx_or, s, rmode=oracle.ROUND_F32)
+    got = synth.to_f64(y.cpu())
+    up = oracle.upsample(m_or, h, w, s).astype(bool)
+    if up.any():
+        assert max_abs_rel(got[up], want[up]) <= 1e-5
+    assert np.array_equal(got[~up], xd[~up])
+    yd = L.dense_block(xg, wd)
+    assert L.last_launch_count() == 1
+    wdense = oracle.static_block(xd, synth.weights_f64(wts), rmode=oracle.ROUND_F32)
+    assert max_abs_rel(synth.to_f64(yd.cpu()), wdense) <= 1e-5

@@ -39,7 +39,7 @@ def test_sanitizer_clean(tool):
     cmd = [SAN, "--tool", tool, "--error-exitcode", "9", "--target-processes", "all"]
     if tool in ("racecheck", "synccheck"):
         cmd += ["--kernel-name", "regex=(masker|compact|decide|maxpool|avgpool|fc_kernel|subsample|add_bias|pack_stem"
-                "|conv_simt|se_kernel|se_apply|regnet_stem)"]
+                "|conv_simt|se_kernel|se_apply|regnet_stem|small_block)"]
     cmd += [sys.executable, os.path.join(HERE, "sanitize_run.py")]
     env = dict(os.environ)
     if tool == "initcheck":  # TMA (async-proxy) stores are not seen as initialisation by initcheck

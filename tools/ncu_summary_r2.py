@@ -33,6 +33,7 @@ def short(name):
     table = [("conv_tc_kernel<0,", "conv1_dyn"), ("conv_tc_kernel<1,", "conv2_dyn"), ("conv_tc_kernel<2,", "conv3_dyn"),
              ("conv_tc_kernel<3,", "conv1_dense"), ("conv_tc_kernel<4,", "conv2_dense"),
              ("conv_tc_kernel<5,", "conv3_dense"), ("conv_tc_kernel<6,", "conv1_mask"), ("conv_tc_kernel<7,", "stem_conv"),
+             ("conv_tc_kernel<8,", "conv2_gather"),
              ("conv23_kernel<0", "conv23"), ("conv23_kernel<false", "conv23"),
              ("conv23_kernel<1", "conv23_dense"), ("conv23_kernel<true", "conv23_dense"),
              ("masker_compact_kernel", "mask_compact"), ("masker_kernel", "mask"), ("compact_kernel", "compact"),
