@@ -199,6 +199,8 @@ def kernel_work(name: str, m: dict) -> dict:
         "decide+gather": (px * 16 + cells + 4 * P + halo * c_mid * e + win, 0),
         "conv1_dyn": (halo * c_in * e + win + W1, 2 * halo * c_in * c_mid),
         "conv2_dyn": (win + P * ss * c_mid * e + W2, 2 * out * 9 * c_mid * c_mid),
+        # conv2 gathering its im2col rows from the dense h1: the windows' in-image pixels once, h2 out
+        "conv2_gather": (halo * c_mid * e + P * ss * c_mid * e + W2, 2 * out * 9 * c_mid * c_mid),
         "conv3_dyn": (P * ss * c_mid * e + 2 * out * c_out * e + W3, 2 * out * c_mid * c_out),
         "conv23": (win + 2 * out * c_out * e + W2 + W3, 2 * out * (9 * c_mid * c_mid + c_mid * c_out)),
         "conv23_direct": (halo * c_mid * e + 2 * out * c_out * e + W2 + W3,

@@ -20,8 +20,8 @@ timeout -s KILL 1500 ncu --set full --clock-control none --import-source on --pr
    -k regex:"conv_tc_kernel|conv23_kernel|decide_kernel|compact_gather_kernel|masker_compact_kernel" \
    --launch-skip 30 -c 10 -o gpurun_out/full_net_r2 python tools/net_once.py --names gpurun_out/net_once_names_full.json > gpurun_out/ncu_full_net_r2.log 2>&1
 echo full-net rc=$?
-timeout -s KILL 1200 ncu --set full --clock-control none --import-source on \
-   -k regex:"conv_tc_kernel|conv23_kernel|decide_kernel" -s 6 -c 3 -o gpurun_out/full_block_r2 \
-   python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-sweep --no-coco --no-regnet > gpurun_out/ncu_full_block_r2.log 2>&1
+timeout -s KILL 1200 ncu --set full --clock-control none --import-source on --profile-from-start off \
+   -k regex:"conv_tc_kernel|conv23_kernel|decide_kernel|masker_compact_kernel" -o gpurun_out/full_block_r2 \
+   python tools/block_once.py > gpurun_out/ncu_full_block_r2.log 2>&1
 echo full-block rc=$?
 ls -la gpurun_out/*.ncu-rep
