@@ -104,9 +104,11 @@ template <int MODE, int BN, bool PAIR = false> struct Cfg {
     static_assert(BN != 256 || !kResid, "BN = 256 only without the residual epilogue");
     static constexpr int kStaging = BN == 256 ? 1 : (kGather ? 1 : (kResid ? 3 : 2));
     // pairs: stages of 32 KB (BN 256) / 24 KB (BN 128) -> deeper rings in the same smem
+    // stem: resident weights, 16 KB A-only stages
     static constexpr int kStages =
-        PAIR ? (BN == 256 ? 4 : (kResid ? 4 : 6))
-             : (BN == 256 ? 3 : (kGather ? (BN == 128 ? 6 : 8) : (kResid ? 3 : (BN == 128 ? 4 : 6))));
+        MODE == STEM ? 6
+        : PAIR ? (BN == 256 ? 4 : (kResid ? 4 : 6))
+               : (BN == 256 ? 3 : (kGather ? (BN == 128 ? 6 : 8) : (kResid ? 3 : (BN == 128 ? 4 : 6))));
     static constexpr int kTmemCols = 2 * BN;
     static constexpr int kStageOff = kBResBytes;  // [resident B][stages][staging][barriers][bias (+wm)]
     static constexpr int kStagingOff = kStageOff + kStages * kStageBytes;
@@ -149,7 +151,7 @@ __device__ __forceinline__ TileGeo tile_geo(const ConvArgs &a, int BN) {
         mt = (*a.count + a.units_per_tile - 1) / a.units_per_tile;  // patch-aligned tiles
     } else if (MODE == CONV2_DENSE || MODE == STEM) {
         mt = a.dense_tiles;
-        if (MODE == STEM) g.n_tiles_n = 1;  // one 64-channel weight, two output rows per tile
+        if (MODE == STEM) g.n_tiles_n = 1;  // one 64-channel weight, BN / 64 output rows per tile
     } else {
         mt = (gemm_rows(MODE, a) + kBM - 1) / kBM;
     }
@@ -237,7 +239,10 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
     // stem: a tile is TWO output rows (2 oy0, 2 oy0 + 1 -> accumulator columns 0-63 / 64-127);
     // its K loop walks the 9 input rows they need, each staged once and used by both rows'
     // MMAs (kernel row j for the first, j - 2 for the second): 9 instead of 14 row loads
-    const int num_kb = MODE == STEM ? 9 : args.K / kBK;
+    // stem: a tile = R = BN / 64 output rows; its K loop walks the 2 R + 5 input rows they need, each
+    // staged once and used by every row whose 7-row window covers it (kernel row kb - 2 j of row j)
+    constexpr int kStemRows = BN / 64;
+    const int num_kb = MODE == STEM ? 2 * kStemRows + 5 : args.K / kBK;
     const int num_kb_b = args.K / kBK;  // resident weight K-blocks (stem: 7 kernel rows)
     const int kpt = args.a_ld / kBK;  // K-blocks per 3x3 tap (conv2)
 
@@ -320,8 +325,8 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                         // tile = (image, output row pair, column block of cols_w columns); K-block kb =
                         // input row 2 oy0 + kb - 3 (out of the image: TMA zero fill)
                         const int xb = mt % args.tiles_x, row = mt / args.tiles_x;
-                        const int pairs = (args.H + 1) / 2;
-                        const int n = row / pairs, oy0 = 2 * (row - n * pairs);
+                        const int groups = (args.H + kStemRows - 1) / kStemRows;
+                        const int n = row / groups, oy0 = kStemRows * (row - n * groups);
                         const int q = args.cols_w / 4;
 #pragma unroll
                         for (int k = 0; k < 4; ++k)
@@ -558,19 +563,16 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     tc_fence_after();
                     const uint32_t sa = sbase + C::kStageOff + stage * C::kStageBytes;
                     const uint64_t adesc = smem_desc_sw128(sa);
-                    if (MODE == STEM) {  // input row kb: kernel row kb of output row 0, kb - 2 of row 1
+                    if (MODE == STEM) {  // input row kb: kernel row kb - 2 j of output row j (TMEM columns 64 j..)
                         constexpr uint32_t idesc64 = idesc_bf16_f32(kBM, 64);
-                        if (kb <= 6) {
-                            const uint64_t bd = smem_desc_sw128(sbase + kb * C::kBBytes);
+#pragma unroll
+                        for (int j = 0; j < kStemRows; ++j) {
+                            const int kr = kb - 2 * j;
+                            if (kr < 0 || kr > 6) continue;
+                            const uint64_t bd = smem_desc_sw128(sbase + kr * C::kBBytes);
 #pragma unroll
                             for (int kk = 0; kk < kBK / 16; ++kk)
-                                mma_bf16(d_tmem, adesc + 2 * kk, bd + 2 * kk, idesc64, (kb | kk) != 0);
-                        }
-                        if (kb >= 2) {
-                            const uint64_t bd = smem_desc_sw128(sbase + (kb - 2) * C::kBBytes);
-#pragma unroll
-                            for (int kk = 0; kk < kBK / 16; ++kk)
-                                mma_bf16(d_tmem + 64, adesc + 2 * kk, bd + 2 * kk, idesc64, ((kb - 2) | kk) != 0);
+                                mma_bf16(d_tmem + 64 * j, adesc + 2 * kk, bd + 2 * kk, idesc64, (kr | kk) != 0);
                         }
                         mma_commit(bar_empty + 8 * stage);
                         continue;
@@ -794,10 +796,10 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                         tma_store_4d(&args.tmap_out, sbuf + c * kChunkBytes, n0 + c * 64, d2x, d2y, d2n);
                 } else if (MODE == STEM) {  // the tile's rows in residue order back to output columns
                     const int xb = mt % args.tiles_x, row = mt / args.tiles_x;
-                    const int pairs = (args.H + 1) / 2;
-                    const int n = row / pairs, oy0 = 2 * (row - n * pairs);
+                    const int groups = (args.H + kStemRows - 1) / kStemRows;
+                    const int n = row / groups, oy0 = kStemRows * (row - n * groups);
                     const int q = args.cols_w / 4;
-                    for (int r2 = 0; r2 < 2; ++r2)  // 64-column chunk r2 = output row oy0 + r2 (row H: clipped)
+                    for (int r2 = 0; r2 < kStemRows; ++r2)  // 64-column chunk r2 = output row oy0 + r2 (rows >= H: clipped)
                         for (int k = 0; k < 4; ++k)
                             tma_store_4d(&args.tmap_s[4 + k], sbuf + r2 * kChunkBytes + k * q * 128, 0, xb * q,
                                          oy0 + r2, n);
@@ -933,7 +935,7 @@ cudaError_t launch_conv_tc(int mode, const ConvArgs &a, int max_tiles_m, int num
         case CONV1_DENSE_MASK: return launch_mode<CONV1_DENSE_MASK>(a, max_tiles_m, num_sms, st);
         case CONV2_DENSE: return launch_mode<CONV2_DENSE>(a, max_tiles_m, num_sms, st);
         case CONV3_DENSE: return launch_mode<CONV3_DENSE>(a, max_tiles_m, num_sms, st);
-        case STEM: {  // BN = 128: the two output rows' 64-channel accumulators
+        case STEM: {  // BN = 128: the two output rows' 64-channel accumulators (four rows, BN 256: 0.32 -> 0.36 ms)
             auto kern = conv_tc_kernel<STEM, 128, false>;
             const int smem = Cfg<STEM, 128>::smem_bytes(64, a.K);
             static int configured = 0;

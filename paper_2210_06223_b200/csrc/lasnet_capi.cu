@@ -1119,7 +1119,7 @@ lasnet_status lasnet_stem(int32_t n, int32_t h, int32_t w, const void *x_pad, co
     while (w % tx || (w / tx) % 4) ++tx;
     a.tiles_x = tx;
     a.cols_w = w / tx;
-    a.dense_tiles = n * ((h + 1) / 2) * tx;  // a tile = two output rows (conv_tc.cu STEM)
+    a.dense_tiles = n * ((h + 1) / 2) * tx;  // a tile = two output rows (conv_tc.cu STEM, BN 128)
     a.m_dense = a.dense_tiles * 128;
     const uint64_t wp = 2 * (uint64_t)w + 8;  // padded input width (pixels)
     const uint64_t row_b = wp * 16, img_b = 2 * (uint64_t)h * row_b;

@@ -128,40 +128,44 @@ __global__ void __launch_bounds__(256) fc_kernel(const float *__restrict__ poole
     const int tx = lt & 7, ty = lt >> 3;
     const int k0 = blockIdx.x * kFcT, n0 = blockIdx.y * kFcT;
     float acc[4][4] = {};
-    for (int c0 = slice * kFcK; c0 < c; c0 += kFcS * kFcK) {
-        for (int e = lt; e < kFcT * kFcK / 8; e += 64) {  // 8 channels of one row per step
+    // the next chunk's 8 (pooled, weight) vectors per thread are loaded into registers while the
+    // current chunk is multiplied out of shared memory (the loads were a round trip per chunk)
+    constexpr int kPer = kFcT * kFcK / 8 / 64;  // 16-B vector pairs per thread per chunk (4)
+    float4 pa[kPer][2];
+    uint4 pw[kPer];
+    auto load = [&](int c0) {
+#pragma unroll
+        for (int t = 0; t < kPer; ++t) {
+            const int e = lt + 64 * t;
             const int r = e / (kFcK / 8), cc = (e % (kFcK / 8)) * 8, ch = c0 + cc;
             const int n = n0 + r, k = k0 + r;
-            float av[8], bv[8];
-            if (n < n_img && ch < c) {
-                const float4 p0 = *reinterpret_cast<const float4 *>(pooled + (long)n * c + ch);
-                const float4 p1 = *reinterpret_cast<const float4 *>(pooled + (long)n * c + ch + 4);
-                av[0] = p0.x; av[1] = p0.y; av[2] = p0.z; av[3] = p0.w;
-                av[4] = p1.x; av[5] = p1.y; av[6] = p1.z; av[7] = p1.w;
-            } else {
-#pragma unroll
-                for (int q = 0; q < 8; ++q) av[q] = 0.f;
+            pa[t][0] = pa[t][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+            pw[t] = make_uint4(0u, 0u, 0u, 0u);
+            if (c0 < c && n < n_img && ch < c) {
+                pa[t][0] = *reinterpret_cast<const float4 *>(pooled + (long)n * c + ch);
+                pa[t][1] = *reinterpret_cast<const float4 *>(pooled + (long)n * c + ch + 4);
             }
-            if (k < classes && ch < c) {
-                const uint4 q = __ldg(reinterpret_cast<const uint4 *>(w + (long)k * c + ch));
-                const uint32_t u[4] = {q.x, q.y, q.z, q.w};
+            if (c0 < c && k < classes && ch < c) pw[t] = __ldg(reinterpret_cast<const uint4 *>(w + (long)k * c + ch));
+        }
+    };
+    load(slice * kFcK);
+    for (int c0 = slice * kFcK; c0 < c; c0 += kFcS * kFcK) {
 #pragma unroll
-                for (int e2 = 0; e2 < 4; ++e2) {
-                    bv[2 * e2] = __uint_as_float(u[e2] << 16);
-                    bv[2 * e2 + 1] = __uint_as_float(u[e2] & 0xffff0000u);
-                }
-            } else {
-#pragma unroll
-                for (int q = 0; q < 8; ++q) bv[q] = 0.f;
-            }
+        for (int t = 0; t < kPer; ++t) {
+            const int e = lt + 64 * t;
+            const int r = e / (kFcK / 8), cc = (e % (kFcK / 8)) * 8;
+            const float av[8] = {pa[t][0].x, pa[t][0].y, pa[t][0].z, pa[t][0].w,
+                                 pa[t][1].x, pa[t][1].y, pa[t][1].z, pa[t][1].w};
+            const uint32_t u[4] = {pw[t].x, pw[t].y, pw[t].z, pw[t].w};
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 sa[cc + q][r] = av[q];
-                sb[cc + q][r] = bv[q];
+                sb[cc + q][r] = (q & 1) ? __uint_as_float(u[q >> 1] & 0xffff0000u) : __uint_as_float(u[q >> 1] << 16);
             }
         }
         __syncwarp();
         asm volatile("bar.sync %0, 64;" ::"r"(1 + slice));  // this slice's 2 warps
+        load(c0 + kFcS * kFcK);  // in flight during this chunk's products
         const int kk_end = min(kFcK, c - c0);
 #pragma unroll 4
         for (int kk = 0; kk < kk_end; ++kk) {

@@ -65,12 +65,7 @@ def test_calibration_reproduces_held_out_measurements():
         c = rec["cfg"]
         t, ks = L.predict_latency(c["n"], c["h"], c["w"], c["c_in"], c["c_mid"], c["c_out"], c["s"], rec["r_meas"],
                                   c["sched"], stride=c["stride"])
-        names = [k for k, _ in ks]
-        if rec["names"][0] == "mask_compact" and names[:2] == ["mask", "compact"]:
-            names = ["mask_compact"] + names[2:]  # first blocks measured before the mask / compact split
-        if "decide+gather" in rec["names"] and "conv2_gather" in names:  # measured before conv2 gathered itself
-            names = [{"decide": "decide+gather", "conv2_gather": "conv2_dyn"}.get(k, k) for k in names]
-        assert names == rec["names"], (c, ks, rec["names"])
+        assert [k for k, _ in ks] == rec["names"], (c, ks, rec["names"])
         m = sum(rec["measured_us"])
         errs["val" if abs(c["r"] - 0.5) < 1e-9 else "cal"].append(abs(t - m) / m)
     assert len(errs["val"]) >= 20

@@ -34,7 +34,7 @@ sys.path.insert(0, ROOT)
 
 K_NAMES = ["mask_compact", "conv1_dyn", "conv1_mask", "decide", "decide+gather", "conv23", "conv23_direct", "conv2_dyn",
            "conv3_dyn", "conv1_dense", "conv2_dense", "conv3_dense", "conv23_dense", "subsample", "shortcut", "mask",
-           "compact"]
+           "compact", "conv2_gather"]
 ALIASES = {"decide+ids": "decide"}  # the two-launch decide of the same kernel type
 
 
@@ -151,9 +151,20 @@ def unit_hw():
     import paper_2210_06223_b200 as L
 
     hw = L.hw_b200()
-    for k in range(len(K_NAMES)):
+    for k in range(len(K_NAMES)):  # the bare bound: efficiency 1, no fixed cost (the fit's model)
         hw.eff[k] = 1.0
+        hw.t0_us[k] = 0.0
     return hw
+
+
+def cmd_repredict(args):
+    """Recompute the stored predictions at efficiency 1 (pred_eff1) for the recorded
+    configurations (host-only: the predictor runs on the CPU)."""
+    data = json.load(open(args.data))
+    for rec in data:
+        _, ks = predict(dict(rec["cfg"], r=rec["r_meas"]), unit_hw())
+        rec["pred_eff1"] = [[k, t] for k, t in ks]
+    json.dump(data, open(args.data, "w"), indent=1)
 
 
 def cmd_fit(args):
@@ -243,8 +254,10 @@ def main():
     f = sub.add_parser("fit")
     f.add_argument("data")
     f.add_argument("--report", default=None)
+    rp = sub.add_parser("repredict")
+    rp.add_argument("data")
     args = ap.parse_args()
-    cmd_measure(args) if args.cmd == "measure" else cmd_fit(args)
+    {"measure": cmd_measure, "fit": cmd_fit, "repredict": cmd_repredict}[args.cmd](args)
 
 
 if __name__ == "__main__":
