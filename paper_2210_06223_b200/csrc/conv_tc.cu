@@ -134,6 +134,12 @@ struct TileWalk {
         const int pm = u / nn;
         return (2 * pm + rank) * nn + (u - pm * nn);
     }
+    // i-th tile of this CTA (i >= 0), -1 past the end (a pair's odd-count tail tile is returned
+    // even though it lies past num_tiles: it runs on zero-filled rows and stores nothing)
+    __device__ __forceinline__ int at(int i) const {
+        const int u = first + i * step;
+        return u < units ? tile(u) : -1;
+    }
 };
 
 // Tile geometry shared by all roles.
@@ -255,8 +261,9 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     tma_load_2d(sbase + kb * C::kBBytes, &args.tmap_b, bar_bres, kb * kBK, 0);
             }
             int it = 0, lt = 0;
-            for (int u = walk.first; u < walk.units; u += walk.step, ++lt) {
-                const int tile = walk.tile(u);
+            for (int i = 0;; ++i, ++lt) {
+                const int tile = walk.at(i);
+                if (tile < 0) break;
                 const int mt = tile / geo.n_tiles_n;
                 const int n0 = (tile - mt * geo.n_tiles_n) * BN;
                 const int u0 = MODE == CONV2_DYN ? mt * args.units_per_tile : 0;  // first patch (conv2 dyn)
@@ -384,12 +391,12 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             };
             int cell[RPT], img[RPT], y0[RPT], x0[RPT];
             int ncell[RPT], nimg[RPT], ny0[RPT], nx0[RPT];
-            auto tile_at = [&](int u) -> int { return u < walk.units ? walk.tile(u) : geo.num_tiles; };
-            load_cells(tile_at(walk.first), cell);
+            auto tile_at = [&](int i) -> int { const int t = walk.at(i); return t < 0 ? geo.num_tiles : t; };
+            load_cells(tile_at(0), cell);
             decode(cell, img, y0, x0);
             int it = 0;
-            for (int u = walk.first; u < walk.units; u += walk.step) {
-                load_cells(tile_at(u + walk.step), ncell);  // next tile: loads in flight during this K-loop
+            for (int i = 0; walk.at(i) >= 0; ++i) {
+                load_cells(tile_at(i + 1), ncell);  // next tile: loads in flight during this K-loop
                 for (int kb = 0; kb < num_kb; ++kb, ++it) {
                     const int stage = it % ST;
                     const int tap = kb / kpt, cb = kb - tap * kpt, dy = tap / 3, dx = tap - dy * 3;
@@ -497,8 +504,9 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
         const int mt = tid - 32 * C::kMaskerWarp0;
         const int r = mt >> 1, h = mt & 1;
         int it = 0;
-        for (int u = walk.first; u < walk.units; u += walk.step) {
-            const int tile = walk.tile(u);
+        for (int i = 0;; ++i) {
+            const int tile = walk.at(i);
+            if (tile < 0) break;
             float acc0 = 0.f, acc1 = 0.f, mag0 = 0.f, mag1 = 0.f;
             for (int kb = 0; kb < num_kb; ++kb, ++it) {
                 const int stage = it % ST;
@@ -548,7 +556,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             constexpr uint32_t idesc = idesc_bf16_f32(PAIR ? 2 * kBM : kBM, BN);
             if (C::kBRes) mbar_wait(bar_bres, 0);
             int it = 0, lt = 0;
-            for (int u = walk.first; u < walk.units; u += walk.step, ++lt) {
+            for (int i = 0; walk.at(i) >= 0; ++i, ++lt) {
                 const int acc = lt & 1;
                 if (PAIR) mbar_wait_cluster(bar_tempty + 8 * acc, ((lt >> 1) & 1) ^ 1);
                 else mbar_wait(bar_tempty + 8 * acc, ((lt >> 1) & 1) ^ 1);
@@ -651,20 +659,21 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
         };
         int lt = 0;
         // tile of the local unit u (past the end: an invalid tile, nothing staged or stored)
-        auto tile_at = [&](int u) -> int { return u < walk.units ? walk.tile(u) : geo.num_tiles; };
+        auto tile_at = [&](int i) -> int { const int t = walk.at(i); return t < 0 ? geo.num_tiles : t; };
         int pix_ring[NSTG];  // output pixel of this thread's row for tiles lt .. lt+NSTG-2 (rotated)
 #pragma unroll
         for (int k = 0; k < NSTG; ++k) pix_ring[k] = -1;
         if (kResid) {  // residual of the first NSTG-1 tiles
 #pragma unroll
             for (int k = 0; k < NSTG - 1; ++k) {
-                const int tl = tile_at(walk.first + k * walk.step);
+                const int tl = tile_at(k);
                 pix_ring[k] = cell_pixel(tl, row_cell(tl));
                 prefetch_resid(tl, pix_ring[k], staging + k * C::kStagingBytes);
             }
         }
-        for (int u = walk.first; u < walk.units; u += walk.step, ++lt) {
-            const int tile = walk.tile(u);
+        for (int i = 0;; ++i, ++lt) {
+            const int tile = walk.at(i);
+            if (tile < 0) break;
             const int mt = tile / geo.n_tiles_n;
             const int n0 = (tile - mt * geo.n_tiles_n) * BN;
             const int acc = lt & 1, b = lt % NSTG;
@@ -684,7 +693,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             }
             int cell_ahead = -2;
             if (kResid) {
-                cell_ahead = row_cell(tile_at(u + (NSTG - 1) * walk.step));  // idx load in flight during this tile
+                cell_ahead = row_cell(tile_at(i + NSTG - 1));  // idx load in flight during this tile
                 cp_async_wait<NSTG - 2>();  // this tile's residual has landed
                 __syncwarp();
             } else {
@@ -776,7 +785,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             }
             if (kResid) {
                 // residual prefetch for tile lt+NSTG-1 into the buffer tile lt-1 used
-                const int ahead = tile_at(u + (NSTG - 1) * walk.step);
+                const int ahead = tile_at(i + NSTG - 1);
                 const int slot = (lt + NSTG - 1) % NSTG;
 #pragma unroll
                 for (int k = 0; k + 1 < NSTG - 1; ++k) pix_ring[k] = pix_ring[k + 1];

@@ -48,7 +48,7 @@ if hasattr(lib, "lasnet_trace23_read"):
     b23 = (ctypes.c_ulonglong * 512)()
     lib.lasnet_trace23_read(b23)
     t = np.array(b23, dtype=np.int64).reshape(64, 8)
-    t0 = t[t[:, 0] > 0][:, 0].min()
+    t0 = t[t[:, 0] > 0][:, 0].min() if (t[:, 0] > 0).any() else 0
     print("== conv23 (fused conv2+conv3), CTA0; us: conv2 start | acc2 ready | H2 staged | conv3 MMAs done | stored")
     for i in range(64):
         if t[i, 0]:
@@ -63,8 +63,8 @@ if hasattr(lib, "lasnet_trace23_read"):
             if tc[c, 0]:
                 print(f"   {c:5d} " + " ".join(f"{(v - t0) / 1e3:7.2f}" if v else "    nan" for v in tc[c, :10]))
 names = {0: "conv1_dyn", 1: "conv2_dyn", 2: "conv3_dyn", 3: "conv1_dense", 4: "conv2_dense", 5: "conv3_dense",
-         6: "conv1_mask"}
-for mode in range(7):
+         6: "conv1_mask", 8: "conv2_gather"}
+for mode in (0, 1, 2, 3, 4, 5, 6, 8):
     for _ in range(2):
         y.copy_(x)
         blk.forward(y)
@@ -87,7 +87,7 @@ for mode in range(7):
             continue
         row = [(v - t0) / 1e3 if v > 0 else float('nan') for v in t[i, :7]]
         print(f"   {i:4d} " + " ".join(f"{v:7.2f}" for v in row))
-    if mode in (0, 2, 3, 6):
+    if mode in (0, 2, 3, 6, 8):
         kb = (ctypes.c_ulonglong * 512)()
         lib.lasnet_ktrace_read(kb)
         k = np.array(kb, dtype=np.int64).reshape(128, 4)
