@@ -15,15 +15,9 @@
 // K-loop of tile i+1 instead of stalling it.  Warps: 0-3 epi2, 4-11 epi3,
 // 12 conv2 producer, 13 conv2 MMA + TMEM allocator, 14 conv3 MMA, 15 conv3 producer.
 //
-// Weight multicast (CL = 2 or 4 CTAs per cluster): the CTAs of a cluster run
-// their tiles in lockstep K-block by K-block; each loads 1/CL of every W2 / W3
-// K-block and multicasts it into the same stage of all CL CTAs, and each CTA's
-// MMA commit releases that stage in all of them.  Every 128-row tile otherwise
-// re-streams the whole W2 (288 KB at c_mid 128) and W3 through L2, and conv2's
-// K-loop is bound by L2 throughput (profiles/ncu_summary_r1c.md): multicast
-// cuts the weight share of that traffic by CL.  Tiles are dealt cluster-major
-// (tile = (cluster + i * clusters) * CL + rank); a CTA whose tile lies past the
-// end runs it anyway on zero-filled (out-of-bounds) operands and stores nothing.
+// (Weight multicast over 2- / 4-CTA clusters and 2-SM pair UMMAs were built and measured
+// slower -- lockstep and cross-CTA arrivals cost more than the weight traffic they save,
+// and removed in round 2.)
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -121,16 +115,8 @@ struct DynTiles {
     }
 };
 
-// PAIR (CL == 2): the two CTAs of a cluster run conv2 and conv3 as 2-SM UMMAs
-// (tcgen05.mma.cta_group::2, M = 256): each CTA stages its own 128 A rows but only
-// HALF of every W2 / W3 K-block (the pair shares them), so per output row the
-// weight bytes written to and read from shared memory halve.  The even CTA
-// issues the MMAs; both CTAs' TMA loads complete on its barriers; its commits
-// multicast to both CTAs' barriers; both CTAs' epilogues drain their own TMEM
-// rows and arrive on its barriers (cluster scope).
-template <bool DENSE, int CL, bool PAIR = false>
+template <bool DENSE>
 __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_constant__ ConvArgs args) {
-    static_assert(!PAIR || CL == 2, "a 2-SM pair is a cluster of 2");
     using namespace c23;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_u32 = smem_u32(smem_raw);
@@ -151,29 +137,25 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
     float *b3_s = b2_s + 128;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int rank = CL > 1 ? (int)cluster_ctarank() : 0;
-    constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
-    constexpr int kPeers = PAIR ? 2 : 1;  // CTAs whose epilogues arrive on the MMA-side barriers
-    const bool lead = !PAIR || rank == 0;
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(bar_full + 8 * s, 1);
-            mbar_init(bar_empty + 8 * s, PAIR ? 1 : CL);  // the MMA commits of all CL CTAs (pair: the lead's)
+            mbar_init(bar_empty + 8 * s, 1);  // the MMA commit
         }
         for (int s = 0; s < kStages3; ++s) {
             mbar_init(bar_full3 + 8 * s, 1);
-            mbar_init(bar_empty3 + 8 * s, PAIR ? 1 : CL);
+            mbar_init(bar_empty3 + 8 * s, 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(bar_t2full + 8 * a, 1);
-            mbar_init(bar_t2empty + 8 * a, PAIR ? 4 * kPeers : 128);  // epi2 threads (pair: one per warp)
+            mbar_init(bar_t2empty + 8 * a, 128);  // epi2 threads
         }
         for (int a = 0; a < kAcc3; ++a) {
             mbar_init(bar_t3full + 8 * a, 1);
-            mbar_init(bar_t3empty + 8 * a, PAIR ? 8 * kPeers : 256);  // epi3 threads (pair: one per warp)
+            mbar_init(bar_t3empty + 8 * a, 256);  // epi3 threads
         }
         for (int a = 0; a < 2; ++a) {
-            mbar_init(bar_h2full + 8 * a, PAIR ? 4 * kPeers : 128);
+            mbar_init(bar_h2full + 8 * a, 128);
             mbar_init(bar_h2empty + 8 * a, 1);
         }
         fence_mbar_init();
@@ -184,14 +166,12 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
         tma_prefetch_desc(&args.tmap_b3);
     }
     if (warp == kMmaWarp) {
-        if (PAIR) tmem_alloc_pair<512>(smem_u32(tmem_slot));
-        else tmem_alloc<512>(smem_u32(tmem_slot));
+        tmem_alloc<512>(smem_u32(tmem_slot));
     }
     for (int c = tid; c < args.N; c += kThreads) b2_s[c] = args.bias[c];
     for (int c = tid; c < args.n3; c += kThreads) b3_s[c] = args.bias3[c];
     tc_fence_before();
-    if (CL > 1) cluster_sync();  // every CTA's barriers are initialised before any multicast lands
-    else __syncthreads();
+    __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     pdl_wait();  // h1, idx and count of the previous kernels are complete from here on
@@ -209,7 +189,7 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
         rows_per_tile = args.units_per_tile * args.S * args.S;
     }
     DynTiles dt{args.units_per_tile, DENSE ? 0 : *args.count, 0, 0, false};
-    if (!DENSE && CL == 1 && args.balance && num_tiles > (int)gridDim.x) {
+    if (!DENSE && args.balance && num_tiles > (int)gridDim.x) {
         // only when every tile of the rounded-up count gets at least one patch (q >= 1):
         // an empty tile would still stream the weights and issue its MMAs
         const int t_bal = (num_tiles + gridDim.x - 1) / gridDim.x * gridDim.x;
@@ -227,12 +207,9 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
     const int NC3 = CO % kNC3 == 0 ? kNC3 : 64;                   // conv3 MMA N
     const int nch = CO / NC3;                                     // conv3 MMA chunks
     const int nsub = CO / 64;                                     // 64-column epilogue sub-chunks
-    // tiles dealt cluster-major: local tile i of this CTA is ((cl + i * ncl) * CL + rank);
-    // every CTA of a cluster runs the same ntl (lockstep multicast)
-    const int cl = blockIdx.x / CL, ncl = gridDim.x / CL;
-    int ntl = 0;
-    for (int t = cl * CL; t < num_tiles; t += ncl * CL) ++ntl;
-    auto tile_of = [&](int i) { return (cl + i * ncl) * CL + rank; };
+    // local tile i of this CTA: blockIdx.x + i * gridDim.x
+    const int ntl = (int)blockIdx.x < num_tiles ? (num_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    auto tile_of = [&](int i) { return (int)blockIdx.x + i * (int)gridDim.x; };
 
     if (warp == kProdWarp && !DENSE && args.direct) {
         // ------------------- conv2 TMA producer, direct from the dense h1 --
@@ -288,21 +265,10 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
                     mbar_wait(bar_empty + 8 * st, ((it / kStages) & 1) ^ 1);
                     const uint32_t sa = sbase + st * kStageBytes, fb = bar_full + 8 * st;
                     const int tap = kb / kpt, dy = tap / 3, dx = tap - dy * 3, c0 = (kb - tap * kpt) * kBK;
-                    if (PAIR) {  // own A rows + own half of the W2 K-block; both complete on the lead's barrier
-                        if (lead) mbar_arrive_expect_tx(fb, 2 * (args.box_rows * 128 + (KC / 2) * 128));
-                        tma_load_2d_pair(sa + kABytes, &args.tmap_b, fb, kb * kBK, rank * (KC / 2));
-                        if (DENSE) tma_load_5d_pair(sa, &args.tmap_a, fb, 0, x0 + dx - 1, y0 + dy - 1, n0, c0 >> 6);
-                        else tma_load_5d_pair(sa, &args.tmap_a, fb, 0, dx, dy, tile * args.units_per_tile, c0 >> 6);
-                        continue;
-                    }
                     mbar_arrive_expect_tx(fb, args.box_rows * 128 + KC * 128);
                     int t0 = 0, nv;
                     if (!DENSE) dt.range(tile, t0, nv);
-                    if (CL > 1)  // this CTA's 1/CL of the W2 K-block, into every CTA of the cluster
-                        tma_load_2d_mc(sa + kABytes + rank * (KC / CL) * 128, &args.tmap_b, fb, kb * kBK,
-                                       rank * (KC / CL), kMask);
-                    else
-                        tma_load_2d(sa + kABytes, &args.tmap_b, fb, kb * kBK, 0);
+                    tma_load_2d(sa + kABytes, &args.tmap_b, fb, kb * kBK, 0);
                     // h1 is channel-chunk-major: [c_mid/64][P][S+2][S+2][64] (dense: [c_mid/64][N][H][W][64])
                     if (DENSE) tma_load_5d(sa, &args.tmap_a, fb, 0, x0 + dx - 1, y0 + dy - 1, n0, c0 >> 6);
                     else if (args.conv_stride == 2)  // stride-2 3x3 (projection block): parity view of the windows
@@ -323,29 +289,18 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
                         mbar_wait(bar_empty3 + 8 * st, ((it / kStages3) & 1) ^ 1);
                         if (kb == 0) T23C(i * nch + nc, 0);
                         const uint32_t fb = bar_full3 + 8 * st;
-                        if (PAIR) {
-                            if (lead) mbar_arrive_expect_tx(fb, NC3 * 128);  // both halves
-                            tma_load_2d_pair(sbase + kRing3Off + st * kB3Bytes, &args.tmap_b3, fb, kb * kBK,
-                                             nc * NC3 + rank * (NC3 / 2));
-                            continue;
-                        }
                         mbar_arrive_expect_tx(fb, NC3 * 128);
-                        if (CL > 1)
-                            tma_load_2d_mc(sbase + kRing3Off + st * kB3Bytes + rank * (NC3 / CL) * 128, &args.tmap_b3,
-                                           fb, kb * kBK, nc * NC3 + rank * (NC3 / CL), kMask);
-                        else
-                            tma_load_2d(sbase + kRing3Off + st * kB3Bytes, &args.tmap_b3, fb, kb * kBK, nc * NC3);
+                        tma_load_2d(sbase + kRing3Off + st * kB3Bytes, &args.tmap_b3, fb, kb * kBK, nc * NC3);
                     }
         }
     } else if (warp == kMmaWarp) {
         // ---------------------------------------------- conv2 MMA issuer --
-        if (lane == 0 && lead) {
-            const uint32_t idesc2 = idesc_bf16_f32(PAIR ? 2 * kBM : kBM, KC);
+        if (lane == 0) {
+            const uint32_t idesc2 = idesc_bf16_f32(kBM, KC);
             int it = 0;
             for (int i = 0; i < ntl; ++i) {
                 const int acc = i & 1;
-                if (PAIR) mbar_wait_cluster(bar_t2empty + 8 * acc, ((i >> 1) & 1) ^ 1);
-                else mbar_wait(bar_t2empty + 8 * acc, ((i >> 1) & 1) ^ 1);
+                mbar_wait(bar_t2empty + 8 * acc, ((i >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + acc * KC;
                 for (int kb = 0; kb < kb2; ++kb, ++it) {
@@ -355,35 +310,27 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
                     const uint32_t sa = sbase + st * kStageBytes;
                     const uint64_t ad = smem_desc_sw128(sa), bd = smem_desc_sw128(sa + kABytes);
 #pragma unroll
-                    for (int kk = 0; kk < kBK / 16; ++kk) {
-                        if (PAIR) mma_bf16_pair(d, ad + 2 * kk, bd + 2 * kk, idesc2, (kb | kk) != 0);
-                        else mma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc2, (kb | kk) != 0);
-                    }
-                    if (PAIR) mma_commit_pair_mc(bar_empty + 8 * st, 3);
-                    else if (CL > 1) mma_commit_mc(bar_empty + 8 * st, kMask);
-                    else mma_commit(bar_empty + 8 * st);
+                    for (int kk = 0; kk < kBK / 16; ++kk) mma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc2, (kb | kk) != 0);
+                    mma_commit(bar_empty + 8 * st);
                 }
-                if (PAIR) mma_commit_pair_mc(bar_t2full + 8 * acc, 3);
-                else mma_commit(bar_t2full + 8 * acc);
+                mma_commit(bar_t2full + 8 * acc);
             }
         }
         __syncwarp();
     } else if (warp == kMma3Warp) {
         // ---------------------------------------------- conv3 MMA issuer --
-        if (lane == 0 && lead) {
-            const uint32_t idesc3 = idesc_bf16_f32(PAIR ? 2 * kBM : kBM, NC3);
+        if (lane == 0) {
+            const uint32_t idesc3 = idesc_bf16_f32(kBM, NC3);
             int it = 0, c3 = 0;
             for (int i = 0; i < ntl; ++i) {
                 const int hb = i % kH2Bufs;
                 const uint32_t h2b = h2s + hb * 2 * kChunkBytes;
                 // H2 of tile i staged by epi2 (pair: both CTAs')
-                if (PAIR) mbar_wait_cluster(bar_h2full + 8 * hb, (i / kH2Bufs) & 1);
-                else mbar_wait(bar_h2full + 8 * hb, (i / kH2Bufs) & 1);
+                mbar_wait(bar_h2full + 8 * hb, (i / kH2Bufs) & 1);
                 tc_fence_after();
                 for (int nc = 0; nc < nch; ++nc, ++c3) {
                     const int buf = c3 % kAcc3;
-                    if (PAIR) mbar_wait_cluster(bar_t3empty + 8 * buf, ((c3 / kAcc3) & 1) ^ 1);
-                    else mbar_wait(bar_t3empty + 8 * buf, ((c3 / kAcc3) & 1) ^ 1);
+                    mbar_wait(bar_t3empty + 8 * buf, ((c3 / kAcc3) & 1) ^ 1);
                     T23C(c3, 1);
                     tc_fence_after();
                     const uint32_t d = tmem_base + acc3_col + buf * kNC3;  // kNC3 columns per buffer
@@ -395,21 +342,15 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
                         const uint64_t ad = smem_desc_sw128(h2b + kb * kChunkBytes);
                         const uint64_t bd = smem_desc_sw128(sbase + kRing3Off + st * kB3Bytes);
 #pragma unroll
-                        for (int kk = 0; kk < kBK / 16; ++kk) {
-                            if (PAIR) mma_bf16_pair(d, ad + 2 * kk, bd + 2 * kk, idesc3, (kb | kk) != 0);
-                            else mma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc3, (kb | kk) != 0);
-                        }
-                        if (PAIR) mma_commit_pair_mc(bar_empty3 + 8 * st, 3);
-                        else if (CL > 1) mma_commit_mc(bar_empty3 + 8 * st, kMask);
-                        else mma_commit(bar_empty3 + 8 * st);
+                        for (int kk = 0; kk < kBK / 16; ++kk)
+                            mma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc3, (kb | kk) != 0);
+                        mma_commit(bar_empty3 + 8 * st);
                     }
-                    if (PAIR) mma_commit_pair_mc(bar_t3full + 8 * buf, 3);
-                    else mma_commit(bar_t3full + 8 * buf);
+                    mma_commit(bar_t3full + 8 * buf);
                     T23C(c3, 3);
                 }
                 // buffer reusable once these MMAs have read it
-                if (PAIR) mma_commit_pair_mc(bar_h2empty + 8 * hb, 3);
-                else mma_commit(bar_h2empty + 8 * hb);
+                mma_commit(bar_h2empty + 8 * hb);
                 T23(i, 3);
             }
         }
@@ -447,23 +388,8 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
             }
             tc_fence_before();
             fence_proxy_async_smem();  // generic smem writes -> visible to tcgen05.mma
-            if (PAIR) {
-                // the lead CTA's MMA waits for both CTAs: one arrival per warp (a remote
-                // release arrive per thread costs a cluster-scope membar each)
-                __syncwarp();
-                if (lane == 0) {
-                    if (lead) {
-                        mbar_arrive(bar_t2empty + 8 * acc);
-                        mbar_arrive(bar_h2full + 8 * (i % kH2Bufs));
-                    } else {
-                        mbar_arrive_cluster(bar_t2empty + 8 * acc, 0);
-                        mbar_arrive_cluster(bar_h2full + 8 * (i % kH2Bufs), 0);
-                    }
-                }
-            } else {
-                mbar_arrive(bar_t2empty + 8 * acc);
-                mbar_arrive(bar_h2full + 8 * (i % kH2Bufs));
-            }
+            mbar_arrive(bar_t2empty + 8 * acc);
+            mbar_arrive(bar_h2full + 8 * (i % kH2Bufs));
             if (r == 0) T23(i, 2);
         }
     } else if (warp >= kEpi3Warp0 && warp < kProdWarp) {
@@ -551,15 +477,7 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
                 if (part == spc - 1) {
                     tc_fence_before();
                     // accumulator drained into registers
-                    if (PAIR) {
-                        __syncwarp();
-                        if (lane == 0) {
-                            if (lead) mbar_arrive(bar_t3empty + 8 * buf);
-                            else mbar_arrive_cluster(bar_t3empty + 8 * buf, 0);
-                        }
-                    } else {
-                        mbar_arrive(bar_t3empty + 8 * buf);
-                    }
+                    mbar_arrive(bar_t3empty + 8 * buf);
                 }
                 // all smem loads first (smem latency is long under UMMA/TMA traffic), then math, then stores
                 uint32_t rv[4][4];
@@ -611,13 +529,10 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
     }
 
     tc_fence_before();
-    // no CTA leaves while a peer may still multicast into its smem or arrive on its barriers
-    if (CL > 1) cluster_sync();
-    else __syncthreads();
+    __syncthreads();
     if (warp == kMmaWarp) {
         tc_fence_after();
-        if (PAIR) tmem_dealloc_pair<512>(tmem_base);
-        else tmem_dealloc<512>(tmem_base);
+        tmem_dealloc<512>(tmem_base);
     }
 }
 
@@ -635,34 +550,23 @@ extern "C" int lasnet_trace23c_read(unsigned long long *h) {
 }
 #endif
 
-template <bool DENSE, int CL, bool PAIR = false>
+template <bool DENSE>
 static cudaError_t launch23(const ConvArgs &a, int max_tiles, int num_sms, cudaStream_t st) {
     const int smem = c23::smem_bytes(a.N, a.n3);
     static int cfg = 0;
     if (smem > cfg) {
-        cudaError_t e = cudaFuncSetAttribute(conv23_kernel<DENSE, CL, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(conv23_kernel<DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         cfg = smem;
     }
-    // whole clusters, at most one CTA per SM
-    const int want = (max_tiles + CL - 1) / CL * CL;
-    const int cap = num_sms / CL * CL;
-    const int grid = want < cap ? (want > 0 ? want : CL) : cap;
-    return launch_k_cluster(conv23_kernel<DENSE, CL, PAIR>, dim3(grid), dim3(c23::kThreads), smem, st, CL, a);
+    const int grid = max_tiles < num_sms ? (max_tiles > 0 ? max_tiles : 1) : num_sms;  // at most one CTA per SM
+    return launch_k(conv23_kernel<DENSE>, dim3(grid), dim3(c23::kThreads), smem, st, a);
 }
 
-// a.cluster: CTAs per cluster sharing the weight loads (1, 2 or 4; the tensor maps'
-// weight boxes were encoded with KC / cluster and NC3 / cluster rows).
 cudaError_t launch_conv23(bool dense, const ConvArgs &a, int max_tiles, int num_sms, cudaStream_t st) {
     if (!(a.N == 64 || a.N == 128) || a.n3 % 64 != 0 || a.n3 > c23::kMaxCout || a.n3 < 64 * (c23::kResBufs - 1))
         return cudaErrorInvalidValue;
-    if (a.pair) return dense ? launch23<true, 2, true>(a, max_tiles, num_sms, st) : launch23<false, 2, true>(a, max_tiles, num_sms, st);
-    switch (a.cluster) {
-        case 1: return dense ? launch23<true, 1>(a, max_tiles, num_sms, st) : launch23<false, 1>(a, max_tiles, num_sms, st);
-        case 2: return dense ? launch23<true, 2>(a, max_tiles, num_sms, st) : launch23<false, 2>(a, max_tiles, num_sms, st);
-        case 4: return dense ? launch23<true, 4>(a, max_tiles, num_sms, st) : launch23<false, 4>(a, max_tiles, num_sms, st);
-        default: return cudaErrorInvalidValue;
-    }
+    return dense ? launch23<true>(a, max_tiles, num_sms, st) : launch23<false>(a, max_tiles, num_sms, st);
 }
 
 }  // namespace lasnet

@@ -469,18 +469,7 @@ cudaError_t run_conv23(const lasnet_block_desc *d, bool dense, ConvArgs a, const
     a.a_src = h1; a.w = w->w2; a.bias = w->b2; a.out = y; a.resid = x;
     a.K = 9 * C; a.N = C; a.a_ld = C; a.out_ld = d->c_out;
     a.w3 = w->w3; a.bias3 = w->b3; a.n3 = d->c_out;
-    // CTAs per cluster multicasting the weight K-blocks (LASNET_C23_CLUSTER = 1, 2, 4)
-    static const int cl_env = [] {
-        const char *e = getenv("LASNET_C23_CLUSTER");
-        const int v = e ? atoi(e) : 1;
-        return (v == 1 || v == 2 || v == 4) ? v : 1;
-    }();
     const int nc3 = d->c_out % 128 == 0 ? 128 : 64;  // conv3 MMA N
-    // 2-SM pair (LASNET_C23_PAIR=1): weight boxes of half height, cluster of 2
-    static const bool pair_env = [] {
-        const char *e = getenv("LASNET_C23_PAIR");
-        return e && e[0] == '1';
-    }();
     // balanced dynamic tiles: the active patches spread over whole rounds of the grid
     // (LASNET_C23_BALANCE=0: fixed units_per_tile patches per tile, a partial last round)
     static const bool bal_env = [] {
@@ -488,9 +477,7 @@ cudaError_t run_conv23(const lasnet_block_desc *d, bool dense, ConvArgs a, const
         return !(e && e[0] == '0');
     }();
     a.balance = bal_env ? 1 : 0;
-    a.pair = pair_env && !a.direct && a.conv_stride == 1 ? 1 : 0;
-    a.cluster = a.direct ? 1 : a.pair ? 2 : (C / cl_env >= 8 && nc3 / cl_env >= 8) ? cl_env : 1;
-    bool ok = tmap2(&a.tmap_b, a.w, a.K, a.N, 64, C / a.cluster) && tmap2(&a.tmap_b3, w->w3, C, d->c_out, 64, nc3 / a.cluster);
+    bool ok = tmap2(&a.tmap_b, a.w, a.K, a.N, 64, C) && tmap2(&a.tmap_b3, w->w3, C, d->c_out, 64, nc3);
     int tiles;
     if (dense) {
         dense_tiling(a, d->n, d->h, d->w);

@@ -85,11 +85,9 @@ struct ConvArgs {
     int32_t rows_h, imgs_box; // conv2 dense: image rows / images per box
     int32_t cols_w, tiles_x;  // conv2 dense: image columns per box, column blocks per row band (W > 128)
     int32_t dense_tiles;      // conv2 dense: M tiles
-    int32_t cluster;          // fused conv2+conv3: CTAs per cluster sharing (multicasting) the weight loads
     int32_t conv_stride;      // dense 3x3: 2 = stride 2 through the four parity views tmap_s[(row odd) * 2 + (col odd)]
     int32_t a2_kb;            // dense conv3: K-blocks >= a2_kb of A come from tmap_s[0] (K-concatenated sources)
     int32_t no_relu;          // 1: the epilogue stores acc + bias (+ residual) without ReLU (projection shortcut)
-    int32_t pair;             // fused conv2+conv3: 2-SM UMMAs over CTA pairs (cluster = 2, weight boxes of half height)
     int32_t pair_tc;          // conv_tc: 2-SM UMMAs over CTA pairs (conv_tc_plan; weight box of bn / 2 rows)
     int32_t balance;          // dynamic fused conv23: spread the active cells evenly over whole rounds of tiles
     int32_t direct;           // dynamic conv2 (fused conv23): A patches read straight from the dense h1

@@ -491,8 +491,8 @@ def test_fused_schedule_bn256_repeated_graph_replays_stable():
         assert torch.equal(y, ref)
 
 
-@pytest.mark.parametrize("env", ["LASNET_PDL=0", "LASNET_NO_FUSE=1", "LASNET_C23_CLUSTER=2", "LASNET_C23_CLUSTER=4",
-                                 "LASNET_C23_PAIR=1", "LASNET_MASK_MAXITEMS=8", "LASNET_GATHER=1",
+@pytest.mark.parametrize("env", ["LASNET_PDL=0", "LASNET_NO_FUSE=1", "LASNET_TC_PAIR=0", "LASNET_C2_GATHER=0",
+                                 "LASNET_SMALL=0", "LASNET_MASK_MAXITEMS=8", "LASNET_GATHER=1",
                                  "LASNET_DECIDE_2K=1", "LASNET_C23_BALANCE=0", "LASNET_TMA_Y=0"])
 def test_library_variants(env):
     """The opt-in library variants (read once per process: run in a subprocess)
