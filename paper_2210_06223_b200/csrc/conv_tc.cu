@@ -155,7 +155,7 @@ __device__ __forceinline__ TileGeo tile_geo(const ConvArgs &a, int BN) {
     int mt;
     if (MODE == CONV2_DYN || MODE == CONV2_GATHER) {
         mt = (*a.count + a.units_per_tile - 1) / a.units_per_tile;  // patch-aligned tiles
-    } else if (MODE == CONV2_DENSE || MODE == STEM) {
+    } else if (MODE == CONV2_DENSE || MODE == STEM || (MODE == CONV3_DENSE && a.view4)) {
         mt = a.dense_tiles;
         if (MODE == STEM) g.n_tiles_n = 1;  // one 64-channel weight, BN / 64 output rows per tile
     } else {
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                 const int n0 = (tile - mt * geo.n_tiles_n) * BN;
                 const int u0 = MODE == CONV2_DYN ? mt * args.units_per_tile : 0;  // first patch (conv2 dyn)
                 int d2n = 0, d2y = 0, d2x = 0;
-                if (MODE == CONV2_DENSE) dense_tile_origin(args, mt, d2n, d2y, d2x);
+                if (MODE == CONV2_DENSE || (MODE == CONV3_DENSE && args.view4)) dense_tile_origin(args, mt, d2n, d2y, d2x);
                 TRACE(lt, 0);
                 for (int kb = 0; kb < num_kb; ++kb, ++it) {
                     const int stage = it % ST;
@@ -279,7 +279,8 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     int a_bytes = kABytes;  // conv1 dyn: A arrives by cp.async (not counted here)
                     if (C::kGather) a_bytes = 0;
                     else if (MODE == STEM) a_bytes = args.cols_w * 128;  // 4 boxes of cols_w / 4 columns
-                    else if (MODE == CONV2_DYN || MODE == CONV2_DENSE) a_bytes = args.box_rows * 128;
+                    else if (MODE == CONV2_DYN || MODE == CONV2_DENSE || (MODE == CONV3_DENSE && args.view4))
+                        a_bytes = args.box_rows * 128;
                     if (PAIR) {
                         // own A rows + own half of the B rows; both CTAs' bytes complete on the lead's barrier
                         if (lead) mbar_arrive_expect_tx(fb, 2 * (a_bytes + C::kBBytes));
@@ -338,6 +339,10 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
 #pragma unroll
                         for (int k = 0; k < 4; ++k)
                             tma_load_4d(sa + k * q * 128, &args.tmap_s[k], fb, 0, xb * q, 2 * oy0 + kb - 3, n);
+                    } else if (MODE == CONV3_DENSE && args.view4) {
+                        // the strided projection shortcut: A = a 4-D view of x at every stride-th pixel
+                        // (dense tiles of rows_h x cols_w output pixels of imgs_box images): no subsample copy
+                        tma_load_4d(sa, &args.tmap_a, fb, kb * kBK, d2x, d2y, d2n);
                     } else if (!C::kGather) {
                         if (args.a2_kb && kb >= args.a2_kb)  // second A source (projection shortcut input)
                             tma_load_2d(sa, &args.tmap_s[0], fb, (kb - args.a2_kb) * kBK, mt * kBM);
@@ -683,10 +688,25 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             bool relu = !args.no_relu;
             if (MODE == CONV3_DENSE && args.relu_mask != nullptr) {
                 // dynamic projection shortcut: ReLU(R) on inactive cells, R itself on active ones
-                const int m = mt * kBM + r;
-                if (m < M) {
-                    const int n = args.fd_HW.div(m), rem = m - n * (int)args.fd_HW.d;
-                    const int yy = args.fd_W.div(rem), xx = rem - yy * args.W;
+                int n = -1, yy = 0, xx = 0;
+                if (args.view4) {  // dense tile geometry (rows_h x cols_w pixels of imgs_box images)
+                    int t0n, t0y, t0x;
+                    dense_tile_origin(args, mt, t0n, t0y, t0x);
+                    const int per_img = args.cols_w * args.rows_h, im = r / per_img, rr = r - im * per_img;
+                    yy = t0y + rr / args.cols_w;
+                    xx = t0x + rr % args.cols_w;
+                    n = t0n + im;
+                    if (n >= args.n_img || yy >= args.H || xx >= args.W || r >= args.box_rows) n = -1;
+                } else {
+                    const int m = mt * kBM + r;
+                    if (m < M) {
+                        n = args.fd_HW.div(m);
+                        const int rem = m - n * (int)args.fd_HW.d;
+                        yy = args.fd_W.div(rem);
+                        xx = rem - yy * args.W;
+                    }
+                }
+                if (n >= 0) {
                     const int cell = (n * args.Gh + args.fd_S.div(yy)) * args.Gw + args.fd_S.div(xx);
                     relu = __ldg(args.relu_mask + cell) == 0;
                 }
@@ -758,8 +778,15 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                 fence_proxy_async_smem();
                 named_bar_sync(1, EPI);
                 if (tid == 0) {
-                    for (int c = 0; c < BN / 64; ++c)
-                        tma_store_2d(&args.tmap_out, sbuf + c * kChunkBytes, n0 + c * 64, mt * kBM);
+                    if (args.view4) {  // y through the 4-D output view of the dense tile
+                        int t0n, t0y, t0x;
+                        dense_tile_origin(args, mt, t0n, t0y, t0x);
+                        for (int c = 0; c < BN / 64; ++c)
+                            tma_store_4d(&args.tmap_out, sbuf + c * kChunkBytes, n0 + c * 64, t0x, t0y, t0n);
+                    } else {
+                        for (int c = 0; c < BN / 64; ++c)
+                            tma_store_2d(&args.tmap_out, sbuf + c * kChunkBytes, n0 + c * 64, mt * kBM);
+                    }
                     bulk_commit();
                     bulk_wait_read<1>();
                 }

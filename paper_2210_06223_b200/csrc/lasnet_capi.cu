@@ -915,7 +915,14 @@ lasnet_status proj_dyn_forward(const lasnet_block_desc *d, const lasnet_block_we
     // the dense projection shortcut R = Wd x_s + bd (the downsampling shortcut stays dense):
     // ReLU(R) on inactive pixels (final), R on active ones (the residual of the scatter-add)
     const void *xs = x;
-    if (st_ > 1) {
+    // stride 2: the shortcut reads x_s through a strided 4-D view of x (no subsample copy);
+    // LASNET_SUBSAMPLE=1 keeps the copy (A/B)
+    static const bool sub_env = [] {
+        const char *e = getenv("LASNET_SUBSAMPLE");
+        return e && e[0] == '1';
+    }();
+    const bool view4 = st_ > 1 && !sub_env;
+    if (st_ > 1 && !view4) {
         KernelEvents ev(st, "subsample");
         if (launch_subsample(x, r.xs, d->n, d->h, d->w, d->c_in * 2, st_, num_sms(), st) != cudaSuccess)
             return LASNET_ERR_CUDA;
@@ -928,14 +935,27 @@ lasnet_status proj_dyn_forward(const lasnet_block_desc *d, const lasnet_block_we
         c.a_src = xs; c.w = w->wd; c.bias = w->bd; c.out = y; c.resid = nullptr;
         c.K = d->c_in; c.N = d->c_out; c.a_ld = d->c_in; c.out_ld = d->c_out;
         c.relu_mask = m;
-        bool ok = tmap2(&c.tmap_b, w->wd, d->c_in, d->c_out, 64, b_box_rows(c, d->c_out, CONV3_DENSE)) &&
-                  tmap2(&c.tmap_a, xs, d->c_in, (uint64_t)po, 64, 128) &&
-                  tmap2(&c.tmap_out, y, d->c_out, (uint64_t)po, 64, 128);
-        c.tma_y = tma_y_enabled();
+        bool ok = tmap2(&c.tmap_b, w->wd, d->c_in, d->c_out, 64, b_box_rows(c, d->c_out, CONV3_DENSE));
+        int tiles = (int)((po + 127) / 128);
+        if (view4) {
+            dense_tiling(c, d->n, d->h, d->w);  // tiles of rows_h x cols_w output pixels (x imgs_box images)
+            const uint64_t dims[4] = {(uint64_t)d->c_in, (uint64_t)d->w, (uint64_t)d->h, (uint64_t)d->n};
+            const uint64_t str[3] = {(uint64_t)st_ * d->c_in * 2, (uint64_t)st_ * Wi * d->c_in * 2,
+                                     (uint64_t)Hi * Wi * d->c_in * 2};
+            const uint32_t box[4] = {64, (uint32_t)c.cols_w, (uint32_t)c.rows_h, (uint32_t)c.imgs_box};
+            ok = ok && tmap_strided(&c.tmap_a, x, 4, dims, str, box) &&
+                 tmap4(&c.tmap_out, y, d->c_out, d->w, d->h, d->n, 64, c.cols_w, c.rows_h, c.imgs_box);
+            c.view4 = 1;
+            c.tma_y = 1;
+            tiles = c.dense_tiles;
+        } else {
+            ok = ok && tmap2(&c.tmap_a, xs, d->c_in, (uint64_t)po, 64, 128) &&
+                 tmap2(&c.tmap_out, y, d->c_out, (uint64_t)po, 64, 128);
+            c.tma_y = tma_y_enabled();
+        }
         if (!ok) return LASNET_ERR_CUDA;
         KernelEvents ev(st, "shortcut");
-        if (launch_conv_tc(CONV3_DENSE, c, (int)((po + 127) / 128), num_sms(), st) != cudaSuccess)
-            return LASNET_ERR_CUDA;
+        if (launch_conv_tc(CONV3_DENSE, c, tiles, num_sms(), st) != cudaSuccess) return LASNET_ERR_CUDA;
         ++launches;
     }
     // step 3: gather + conv1 over each active cell's input window (side st(S-1)+3)

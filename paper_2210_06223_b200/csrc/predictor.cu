@@ -138,7 +138,7 @@ bool build_plan(Plan &p, const lasnet_block_desc *d, int schedule, double r) {
             p.add(LASNET_K_MASK, pxi * CI * e + G, 0, 2 * pxi * CI, 0);
             p.add(LASNET_K_COMPACT, G + 4 * P, 0, 0, 0);
         }
-        if (st > 1) p.add(LASNET_K_SUBSAMPLE, 2 * px * CI * e, 0, 0, 0);
+        // the shortcut reads x_s through a strided view of x (no subsample launch)
         const double ts = ceil_div(px, 128) * (CO / 128);
         p.add(LASNET_K_SHORTCUT, px * CI * e + px * CO * e + CO * CI * e + G, ts * 256 * CI * e, 2 * px * CI * CO, ts);
         const double rows = P * hs * hs;

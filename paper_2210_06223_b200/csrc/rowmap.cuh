@@ -76,6 +76,8 @@ struct ConvArgs {
     // projection block's shortcut R: inactive pixels store ReLU(R), active ones R for the scatter-add)
     const uint8_t *relu_mask;
     int32_t tma_y;            // dense conv3: the epilogue TMA-stores whole 128-row tiles of y (tmap_out = y [px][c_out])
+    int32_t view4;            // dense conv3 (strided projection shortcut): A = a 4-D strided view of x, dense tiles
+                              // (dense_tiling), y stored through a 4-D view (tmap_out)
     // tcgen05 tile geometry (host-computed)
     int32_t units_per_tile;   // dynamic: TMA boxes (conv1) / patches (conv2, conv3) per 128-row tile
     int32_t units_per_patch;  // conv1: 1 (whole halo box) or S+2 (one box per halo row)

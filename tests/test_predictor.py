@@ -37,7 +37,7 @@ def test_plan_lists_the_library_launches():
     assert names(pred(256, 14, 1024, 256, 2, 0.5, L.SCHED_FUSED)) == ["conv1_mask", "decide", "conv2_gather",
                                                                       "conv3_dyn"]
     assert names(pred(64, 28, 256, 128, 4, 0.5, L.SCHED_SEPARATE, stride=2, c_out=512)) == [
-        "mask", "compact", "subsample", "shortcut", "conv1_dyn", "conv23"]
+        "mask", "compact", "shortcut", "conv1_dyn", "conv23"]
     assert names(pred(128, 28, 512, 128, 4, 1.0, L.SCHED_DENSE)) == ["conv1_dense", "conv23_dense"]
 
 
