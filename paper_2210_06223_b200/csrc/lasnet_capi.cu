@@ -921,7 +921,8 @@ lasnet_status proj_dyn_forward(const lasnet_block_desc *d, const lasnet_block_we
         const char *e = getenv("LASNET_SUBSAMPLE");
         return e && e[0] == '1';
     }();
-    const bool view4 = st_ > 1 && !sub_env;
+    // (it stores y by TMA: LASNET_TMA_Y=0, the initcheck tier, keeps the copy and plain stores)
+    const bool view4 = st_ > 1 && !sub_env && tma_y_enabled();
     if (st_ > 1 && !view4) {
         KernelEvents ev(st, "subsample");
         if (launch_subsample(x, r.xs, d->n, d->h, d->w, d->c_in * 2, st_, num_sms(), st) != cudaSuccess)

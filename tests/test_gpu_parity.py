@@ -320,6 +320,8 @@ FWD_CASES = [
     (2, 19, 17, 256, 64, 5, 0.5),    # direct conv23 patches: 5 per tile, clipped edge cells
     (2, 22, 20, 256, 128, 8, 0.6),   # direct: 2 patches (128 rows) per tile
     (2, 23, 21, 256, 64, 11, 0.7),   # direct: 1 patch of 121 rows per tile
+    (2, 13, 11, 256, 256, 3, 0.5),   # conv2 cp.async gather (c_mid 256): clipped cells, 14 patches per tile
+    (2, 9, 9, 512, 512, 5, 0.6),     # conv2 gather at c_mid 512, 5 patches (125 rows) per tile
 ]
 
 
