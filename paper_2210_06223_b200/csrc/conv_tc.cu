@@ -87,9 +87,11 @@ template <int MODE, int BN, bool PAIR = false> struct Cfg {
         32 * (kEpiWarps + 2) + (kGather ? kGatherThreads : 0) + (kMasker ? kMaskerThreads : 0);
     // stem: B is the 64-channel weight (its BN = 128 spans two output rows' accumulators)
     static constexpr int kBBytes = (MODE == STEM ? 64 : (PAIR ? BN / 2 : BN)) * kBK * 2;
-    // (a cp.async-fed pair needs a relay of the peer's stage to the lead's barrier: measured
-    // 45 -> 65 us for the stage-3 conv2, so the gather modes run one CTA per tile)
-    static_assert(!PAIR || (MODE != STEM && !kGather), "pairs: TMA-fed modes only");
+    // Pairs serve the 256-column conv2 tiles only.  Measured and dropped: pairs for conv1 + masker
+    // (the odd CTA's masker warps need the stage-full event relayed from the even CTA: 43 -> 62 us
+    // at stage 3, with one or two relay hops), for conv3 and 128-column tiles (slower), and for
+    // the cp.async-fed conv2 gather (45 -> 65 us).
+    static_assert(!PAIR || MODE == CONV2_DYN || MODE == CONV2_DENSE, "pairs: conv2 only");
     // stem: the whole packed weight (7 K-blocks of 64 x 64, 56 KB) stays resident in smem,
     // loaded once per CTA; its stages carry A only (it was L2-throughput bound re-streaming it)
     static constexpr bool kBRes = MODE == STEM;
@@ -515,15 +517,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             float acc0 = 0.f, acc1 = 0.f, mag0 = 0.f, mag1 = 0.f;
             for (int kb = 0; kb < num_kb; ++kb, ++it) {
                 const int stage = it % ST;
-                // pair: the peer's full barrier is relayed by the lead's MMA thread (cluster scope)
-                if (PAIR && !lead) {
-                    mbar_wait_cluster(bar_full + 8 * stage, (it / ST) & 1);
-                } else {
-                    mbar_wait(bar_full + 8 * stage, (it / ST) & 1);
-                    // the peer's maskers: relayed by one lead masker thread (a remote release
-                    // arrive on the MMA thread's path measured ~0.5 us per K-block)
-                    if (PAIR && mt == 0) mbar_arrive_cluster(bar_full + 8 * stage, 1);
-                }
+                mbar_wait(bar_full + 8 * stage, (it / ST) & 1);
                 const uint32_t row = sbase + C::kStageOff + stage * C::kStageBytes + r * 128;
                 uint32_t q[4][4];
 #pragma unroll
@@ -896,15 +890,13 @@ static cudaError_t launch_mode_bn(const ConvArgs &a, int max_tiles_m, int num_sm
     return launch_k(kern, dim3(grid), dim3(threads_of<MODE, BN>()), smem, st, a);
 }
 
-// LASNET_TC_PAIR (bit mask, default 8): 2-SM pairs for 1 = 256-column conv1 tiles,
-// 8 = 256-column conv2 tiles, 16 = 128-column conv2 tiles, 2 = conv3 (128-column tiles),
-// 4 = 128-column conv1 tiles
-static int pair_bits() {
-    static const int bits = [] {
+// LASNET_TC_PAIR=0: no 2-SM pairs (the 256-column conv2 tiles run one CTA per tile)
+static bool pairs_enabled() {
+    static const bool on = [] {
         const char *e = getenv("LASNET_TC_PAIR");
-        return e ? atoi(e) : 8;
+        return !(e && e[0] == '0');
     }();
-    return bits;
+    return on;
 }
 
 // conv2 (dynamic) without pairs stays on 128-column tiles: 256-column tiles measured no faster
@@ -922,14 +914,10 @@ static bool conv2_bn256() {
 int conv_tc_plan(int mode, int n, int *pair) {
     *pair = 0;
     if (n % 128 != 0) return 64;  // 64-column N tiles
-    const bool c1 = mode == CONV1_DENSE || mode == CONV1_DENSE_MASK,
-               c2 = mode == CONV2_DYN || mode == CONV2_DENSE;
-    const int bits = pair_bits();
-    *pair = 1;
-    if (n % 256 == 0 && ((c1 && (bits & 1)) || (c2 && (bits & 8)))) return 256;
-    if ((mode == CONV3_DYN || mode == CONV3_DENSE) && (bits & 2)) return 128;
-    if ((c1 && (bits & 4)) || (c2 && (bits & 16))) return 128;
-    *pair = 0;
+    if ((mode == CONV2_DYN || mode == CONV2_DENSE) && n % 256 == 0 && pairs_enabled()) {
+        *pair = 1;
+        return 256;
+    }
     // 256-column tiles: A (the gathered rows / the im2col taps) is staged once per M
     // tile instead of once per 128-column N tile
     if (n % 256 == 0 && (mode == CONV1_DYN || mode == CONV1_DENSE || mode == CONV1_DENSE_MASK || mode == CONV2_GATHER ||
@@ -944,11 +932,8 @@ static cudaError_t launch_mode(const ConvArgs &a, int max_tiles_m, int num_sms, 
     const int bn = conv_tc_plan(MODE, a.N, &pair);
     if (pair != a.pair_tc) return cudaErrorInvalidValue;  // the host encoded B for the other plan
     constexpr bool kResid = MODE == CONV3_DYN || MODE == CONV3_DENSE;
-    if constexpr (!Cfg<MODE, 128>::kGather) {
-        if (pair && bn == 256) {
-            if constexpr (!kResid) return launch_mode_bn<MODE, 256, true>(a, max_tiles_m, num_sms, st);
-        }
-        if (pair && bn == 128) return launch_mode_bn<MODE, 128, true>(a, max_tiles_m, num_sms, st);
+    if constexpr (MODE == CONV2_DYN || MODE == CONV2_DENSE) {
+        if (pair && bn == 256) return launch_mode_bn<MODE, 256, true>(a, max_tiles_m, num_sms, st);
     }
     if (bn == 64) return launch_mode_bn<MODE, 64, false>(a, max_tiles_m, num_sms, st);
     if constexpr (!kResid) {
