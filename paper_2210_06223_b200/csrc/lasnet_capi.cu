@@ -570,6 +570,16 @@ void set_windows(ConvArgs &a, int S, int st, int Hi, int Wi) {
     a.fd_hs2 = FastDiv((uint32_t)(a.hs * a.hs));
 }
 
+// LAS-RegNetY masker-fused schedule: the grouped 3x3 reads the windows from the dense h1
+// (LASNET_REG_GATHER=1: a gathered copy)
+bool reg_direct() {
+    static const bool off = [] {
+        const char *e = getenv("LASNET_REG_GATHER");
+        return e && e[0] == '1';
+    }();
+    return !off;
+}
+
 // Workspace of lasnet_block_forward: zero-contract control words first, then
 // scratch.  Returns the byte size; with base != NULL also the region pointers.
 struct FwdWs {
@@ -1453,17 +1463,28 @@ lasnet_status lasnet_regnet_block(const lasnet_block_desc *d, const lasnet_regne
                 return LASNET_ERR_CUDA;
             int nd = 0;
             {
-                KernelEvents ev(st, "decide+gather");
+                // the grouped 3x3 reads its windows straight from the dense h1 (LASNET_REG_GATHER=1: a
+                // gathered copy): the decide step then writes only the ids
+                KernelEvents ev(st, reg_direct() ? "decide" : "decide+gather");
                 if (launch_decide_gather(static_cast<const float4 *>(r.mpart), x, wm, bm, d->n, d->h, d->w, d->c_in, S,
-                                         m, idx, count, r.sync, r.h1d, r.h1, C, ncells, num_sms(), st, &nd) !=
-                    cudaSuccess)
+                                         m, idx, count, r.sync, r.h1d, reg_direct() ? nullptr : r.h1, C, ncells,
+                                         num_sms(), st, &nd) != cudaSuccess)
                     return LASNET_ERR_CUDA;
+                if (reg_direct() && nd == 2) ev.name = "decide+ids";
             }
             launches += 1 + nd;
+            if (reg_direct()) {
+                g.direct = 1;
+                g.idx = idx;
+                g.G = G;
+                g.Gw = gw;
+                g.H = d->h;
+                g.W = d->w;
+            }
         }
         // step 4: grouped 3x3 on the windows, then SE pooled over the active pixels (reading R23)
-        g.h1 = static_cast<const __nv_bfloat16 *>(r.h1);
-        g.h1_rows = (int64_t)ncells * hs * hs;
+        g.h1 = static_cast<const __nv_bfloat16 *>(g.direct ? r.h1d : r.h1);
+        g.h1_rows = g.direct ? (int64_t)pxo : (int64_t)ncells * hs * hs;
         g.count = count;
         g.S = S; g.hs = hs;
         {

@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(kGcThreads, 2) gconv_kernel(const GconvArgs a)
     uint8_t *s_in = gsm;                                    // [in_rows][128 B] swizzled
     __nv_bfloat16 *s_w = reinterpret_cast<__nv_bfloat16 *>(gsm + kGcMaxIn * 128);  // [64][9][16]
     int *s_src = reinterpret_cast<int *>(gsm + kGcMaxIn * 128 + 64 * 9 * 16 * 2);  // [128][9] staged row per tap
+    int *s_pn = s_src + 128 * 9, *s_py = s_pn + 128, *s_px = s_py + 128;         // direct: window origin per patch
     // ---- tile geometry ----
     int rows, in_rows;
     int64_t out_row0;
@@ -71,6 +72,13 @@ __global__ void __launch_bounds__(kGcThreads, 2) gconv_kernel(const GconvArgs a)
         out_row0 = (int64_t)t0 * a.S * a.S;
         in_row0 = (int64_t)t0 * a.hs * a.hs;
         in_rows = np * a.hs * a.hs;
+        if (a.direct)  // window origin (image, y, x) of each patch of the tile, from its cell id
+            for (int p = threadIdx.x; p < np; p += kGcThreads) {
+                const int c = __ldg(a.idx + t0 + p), n = c / a.G, g = c - n * a.G, gy = g / a.Gw;
+                s_pn[p] = n;
+                s_py[p] = gy * a.S - 1;
+                s_px[p] = (g - gy * a.Gw) * a.S - 1;
+            }
     } else {
         const int bands = (a.Ho + a.trows - 1) / a.trows;
         n0 = blockIdx.x / bands;
@@ -110,7 +118,14 @@ __global__ void __launch_bounds__(kGcThreads, 2) gconv_kernel(const GconvArgs a)
             const uint32_t dst = smem_addr(s_in + row * 128 + ((k ^ (row & 7)) << 4));
             const __nv_bfloat16 *g = src_chunk;
             uint32_t bytes = 16;
-            if (DYN) {
+            if (DYN && a.direct) {  // window pixel (wy, wx) of patch p, read from the dense h1
+                const int hs2 = a.hs * a.hs, p = row / hs2, j = row - p * hs2, wy = j / a.hs;
+                const int yy = s_py[p] + wy, xx = s_px[p] + (j - wy * a.hs);
+                if (yy >= 0 && yy < a.H && xx >= 0 && xx < a.W)
+                    g = src_chunk + (((int64_t)s_pn[p] * a.H + yy) * a.W + xx) * 64 + k * 8;
+                else
+                    bytes = 0;  // conv2's zero padding outside the image (R6)
+            } else if (DYN) {
                 g = src_chunk + (in_row0 + row) * 64 + k * 8;
             } else {
                 const int yy = iy0 + row / iw, xx = row - (row / iw) * iw - 1;
@@ -436,7 +451,7 @@ cudaError_t launch_gconv(bool dyn, const GconvArgs &a0, int max_rows, int num_sm
     const long grid = gconv_tiles(dyn, a, max_rows);
     if (grid < 0) return cudaErrorInvalidValue;
     if (grid == 0) return cudaSuccess;
-    const int smem = kGcMaxIn * 128 + 64 * 9 * 16 * 2 + 128 * 9 * 4;
+    const int smem = kGcMaxIn * 128 + 64 * 9 * 16 * 2 + 128 * 9 * 4 + 3 * 128 * 4;
     static bool configured[2] = {false, false};
     if (!configured[dyn]) {
         cudaError_t e = cudaFuncSetAttribute(dyn ? (const void *)gconv_kernel<true> : (const void *)gconv_kernel<false>,

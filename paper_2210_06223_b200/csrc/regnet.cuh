@@ -20,6 +20,11 @@ struct GconvArgs {
     int H, W, Ho, Wo, stride; // dense: input / output dims
     int n_img;                // dense: images
     int upt, trows;           // tile geometry (host-computed): patches / output rows per tile
+    // dynamic, direct: the windows are read straight from the DENSE h1 [C/64][h1_rows = n H W][64] at the
+    // active cells' positions (ids in idx; G cells per image, Gw per grid row; H, W the map), 0 outside
+    int direct;
+    const int32_t *idx;
+    int G, Gw;
 };
 
 struct SeArgs {
