@@ -79,7 +79,20 @@ template <int MODE, int BN, bool PAIR = false> struct Cfg {
     static constexpr bool kResid = MODE == CONV3_DYN || MODE == CONV3_DENSE;
     static constexpr bool kGather = MODE == CONV1_DYN || MODE == CONV2_GATHER;
     static constexpr bool kMasker = MODE == CONV1_DENSE_MASK;
-    static constexpr int kEpiWarps = kResid ? 8 : 4;
+#ifndef LASNET_RESID_EPI_WARPS
+#define LASNET_RESID_EPI_WARPS 16
+#endif
+#ifndef LASNET_EPI_WARPS
+#define LASNET_EPI_WARPS 8
+#endif
+    // conv3 (residual epilogue): its epilogue bounds the kernel (the MMAs of a 128-column tile
+    // take ~1.5 us, the residual / ReLU / scatter of its 128 rows ~2.5 us): 16 warps, 32 columns
+    // each (8 warps: conv3_dyn 0.944 -> 0.846 ms per LAS-R101 forward with 16); conv1 / conv2:
+    // 8 warps (4: LAS-R101 5.30 -> 5.26 ms with 8)
+    // (each warp drains >= 32 columns: 64-column tiles take at most 8 warps)
+    static constexpr int kEpiWarpsWant = kResid ? LASNET_RESID_EPI_WARPS : (MODE == STEM ? 4 : LASNET_EPI_WARPS);
+    static constexpr int kEpiWarps = kEpiWarpsWant * 32 / 4 > BN ? 4 * BN / 32 : kEpiWarpsWant;
+    static_assert(BN / (kEpiWarps / 4) >= 32, "an epilogue warp drains at least 32 TMEM columns");
     static constexpr int kProdWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1, kGatherWarp0 = kEpiWarps + 2;
     static constexpr int kGatherThreads = 256;
     static constexpr int kMaskerWarp0 = kEpiWarps + 2, kMaskerThreads = 256;
