@@ -67,8 +67,15 @@ constexpr int kStageBytes = 2 * kABytes;  // A 16 KB + B (<= 128 rows) 16 KB
 constexpr int kNC3 = 128;                 // max conv3 output channels per MMA chunk (64 when c_out % 128 != 0)
 constexpr int kAcc3 = 2;                  // conv3 accumulator buffers (128 TMEM columns each)
 constexpr int kChunkBytes = kBM * 128;    // one 64-column bf16 chunk of a 128-row tile
-constexpr int kThreads = 16 * 32;
-constexpr int kEpi2Warp0 = 0, kEpi3Warp0 = 4, kProdWarp = 12, kMmaWarp = 13, kMma3Warp = 14, kProd3Warp = 15;
+#ifndef LASNET_C23_EPI3_WARPS
+#define LASNET_C23_EPI3_WARPS 8
+#endif
+// epi3 warps: 8, each 32 rows x 32 columns of a 64-column part (16 warps of 16 columns measured
+// slower: configs[1] block conv23 51.2 -> 52.9 us, unlike conv_tc's conv3 epilogue)
+constexpr int kEpi3Warps = LASNET_C23_EPI3_WARPS;
+constexpr int kThreads = (8 + kEpi3Warps) * 32;
+constexpr int kEpi2Warp0 = 0, kEpi3Warp0 = 4, kProdWarp = 4 + kEpi3Warps, kMmaWarp = kProdWarp + 1,
+              kMma3Warp = kProdWarp + 2, kProd3Warp = kProdWarp + 3;
 constexpr int kStages3 = 2;                // conv3 weight ring (<= 16 KB stages: kNC3 rows x 64 K)
 constexpr int kB3Bytes = kNC3 * 128;
 // smem layout (offsets from the 1024-aligned base); biases are read through L1
@@ -152,7 +159,7 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
         }
         for (int a = 0; a < kAcc3; ++a) {
             mbar_init(bar_t3full + 8 * a, 1);
-            mbar_init(bar_t3empty + 8 * a, 256);  // epi3 threads
+            mbar_init(bar_t3empty + 8 * a, 32 * kEpi3Warps);  // epi3 threads
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(bar_h2full + 8 * a, 128);
@@ -394,9 +401,10 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
         }
     } else if (warp >= kEpi3Warp0 && warp < kProdWarp) {
         // ------------------------------- epi3: acc3 + b3 + x -> ReLU -> y --
-        // 8 warps per 64-column chunk: rows 32*quarter.., columns 32*half..
+        // kEpi3Warps warps per 64-column part: rows 32*quarter.., columns kColsW*cg..
+        constexpr int kColsW = 64 / (kEpi3Warps / 4);
         const int ew = warp - kEpi3Warp0;
-        const int quarter = ew & 3, half = ew >> 2;
+        const int quarter = ew & 3, cg = ew >> 2;
         const int r = quarter * 32 + lane;
         const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
         const __nv_bfloat16 *X = static_cast<const __nv_bfloat16 *>(args.resid);
@@ -410,13 +418,13 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
             }
             return tile_pixel<DENSE>(args, tile_of(i), r, rows_per_tile, M);
         };
-        constexpr int kChunks = 32 / 8;           // 16-B chunks of this warp's 32 columns
-        constexpr int kRowsPerIt = 32 / kChunks;  // 8 rows (64 B each) per instruction
-        constexpr int kIt = 32 / kRowsPerIt;      // 4 instructions per 32 rows
+        constexpr int kChunks = kColsW / 8;       // 16-B chunks of this warp's columns
+        constexpr int kRowsPerIt = 32 / kChunks;  // rows per store instruction
+        constexpr int kIt = 32 / kRowsPerIt;      // store instructions per 32 rows
         const int c16 = lane % kChunks, rl0 = lane / kChunks;
         auto chunk_addr = [&](uint32_t buf, int rl) -> uint32_t {
             const int row = quarter * 32 + rl;
-            return buf + row * 128 + (((half * kChunks + c16) ^ (row & 7)) << 4);
+            return buf + row * 128 + (((cg * kChunks + c16) ^ (row & 7)) << 4);
         };
         // element offsets (pixel * out_ld + this lane's 8 columns) of the rows this lane moves in the
         // coalesced pattern (rows k*8 + lane/4 of the warp's 32); constant over the chunks of a tile
@@ -425,7 +433,7 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
 #pragma unroll
             for (int k = 0; k < kIt; ++k) {
                 const int p = __shfl_sync(0xffffffffu, pix, k * kRowsPerIt + rl0);
-                o[k] = p >= 0 ? (long long)p * args.out_ld + half * 32 + c16 * 8 : -1;
+                o[k] = p >= 0 ? (long long)p * args.out_ld + cg * kColsW + c16 * 8 : -1;
             }
         };
         auto prefetch = [&](const long long (&o)[kIt], int nc, uint32_t buf) {
@@ -469,9 +477,9 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
                 if (part == 0) mbar_wait(bar_t3full + 8 * buf, (c3 / kAcc3) & 1);
                 if (warp == kEpi3Warp0 && lane == 0) T23C(sc, 5);
                 tc_fence_after();
-                const int col0 = nc * 64 + half * 32;
-                uint32_t v[32];
-                tmem_ld32(tmem_base + lane_base + acc3_col + buf * kNC3 + part * 64 + half * 32, v);
+                const int col0 = nc * 64 + cg * kColsW;
+                uint32_t v[kColsW];
+                tmem_ld_cols(tmem_base + lane_base + acc3_col + buf * kNC3 + part * 64 + cg * kColsW, v);
                 tmem_ld_wait();
                 if (warp == kEpi3Warp0 && lane == 0) T23C(sc, 7);
                 if (part == spc - 1) {
@@ -480,19 +488,19 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
                     mbar_arrive(bar_t3empty + 8 * buf);
                 }
                 // all smem loads first (smem latency is long under UMMA/TMA traffic), then math, then stores
-                uint32_t rv[4][4];
+                uint32_t rv[kChunks][4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
+                for (int q = 0; q < kChunks; ++q)
                     asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
                                  : "=r"(rv[q][0]), "=r"(rv[q][1]), "=r"(rv[q][2]), "=r"(rv[q][3])
-                                 : "r"(sres + r * 128 + (((half * kChunks + q) ^ (r & 7)) << 4)));
-                float4 bsv[8];
+                                 : "r"(sres + r * 128 + (((cg * kChunks + q) ^ (r & 7)) << 4)));
+                float4 bsv[kColsW / 4];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) bsv[j] = reinterpret_cast<const float4 *>(b3_s + col0)[j];
+                for (int j = 0; j < kColsW / 4; ++j) bsv[j] = reinterpret_cast<const float4 *>(b3_s + col0)[j];
                 const float *bias = reinterpret_cast<const float *>(bsv);
-                uint32_t pk[4][4];
+                uint32_t pk[kChunks][4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
+                for (int q = 0; q < kChunks; ++q)
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int c = 8 * q + 2 * e;
@@ -501,9 +509,9 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
                         pk[q][e] = pack_bf16x2(lo, hi);
                     }
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
+                for (int q = 0; q < kChunks; ++q)
                     asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(
-                                     sres + r * 128 + (((half * kChunks + q) ^ (r & 7)) << 4)),
+                                     sres + r * 128 + (((cg * kChunks + q) ^ (r & 7)) << 4)),
                                  "r"(pk[q][0]), "r"(pk[q][1]), "r"(pk[q][2]), "r"(pk[q][3])
                                  : "memory");
                 if (warp == kEpi3Warp0 && lane == 0) T23C(sc, 8);
