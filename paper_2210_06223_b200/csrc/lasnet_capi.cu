@@ -801,11 +801,16 @@ lasnet_status lasnet_dense_block(const lasnet_block_desc *d, const lasnet_block_
         // (the dense workspace carries no zero contract: clear the barrier words first)
         if (cudaMemsetAsync(ws, 0, 16, st) != cudaSuccess) return LASNET_ERR_CUDA;
         KernelEvents ev(st, "small_dense");
-        if (launch_small_block(small_args(d, w, x, y, nullptr, 0.f, nullptr, nullptr, nullptr, ws), num_sms(), st) !=
-            cudaSuccess)
-            return LASNET_ERR_CUDA;
-        g_last_launches = 1;
-        return LASNET_OK;
+        const cudaError_t e =
+            launch_small_block(small_args(d, w, x, y, nullptr, 0.f, nullptr, nullptr, nullptr, ws), num_sms(), st);
+        if (e == cudaSuccess) {
+            g_last_launches = 1;
+            return LASNET_OK;
+        }
+        // the runtime refuses a cooperative grid it cannot keep co-resident (nothing ran): the
+        // per-step kernels below
+        if (e != cudaErrorCooperativeLaunchTooLarge) return LASNET_ERR_CUDA;
+        (void)cudaGetLastError();
     }
     Carve cv{static_cast<uint8_t *>(ws)};
     const int px = d->n * d->h * d->w;
@@ -1040,10 +1045,13 @@ lasnet_status lasnet_block_forward(const lasnet_block_desc *d, const lasnet_bloc
         if (x != y && cudaMemcpyAsync(y, x, xbytes, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
             return LASNET_ERR_CUDA;
         KernelEvents ev(st, "small_block");
-        if (launch_small_block(small_args(d, w, x, y, wm, bm, mask, idx, count, r.small), num_sms(), st) != cudaSuccess)
-            return LASNET_ERR_CUDA;
-        g_last_launches = 1;
-        return LASNET_OK;
+        const cudaError_t e = launch_small_block(small_args(d, w, x, y, wm, bm, mask, idx, count, r.small), num_sms(), st);
+        if (e == cudaSuccess) {
+            g_last_launches = 1;
+            return LASNET_OK;
+        }
+        if (e != cudaErrorCooperativeLaunchTooLarge) return LASNET_ERR_CUDA;
+        (void)cudaGetLastError();  // not co-resident now: the per-step kernels below (nothing ran)
     }
     if (schedule == LASNET_SCHED_MASKER_SEPARATE) {
         // north-star branch: masker+compaction (one launch), then gather+conv1 on the halos, conv2, conv3
