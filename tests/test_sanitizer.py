@@ -30,6 +30,10 @@ def _cuda():
         pytest.skip("needs a GPU")
     if not os.path.exists(SAN):
         pytest.skip("compute-sanitizer not installed")
+    # opt-in: the GPU pool may close compute-sanitizer (runs under it have left GPUs needing
+    # a reset there); LASNET_SANITIZE=1 runs this tier where the tool is allowed
+    if os.environ.get("LASNET_SANITIZE") != "1":
+        pytest.skip("sanitizer tier is opt-in (LASNET_SANITIZE=1)")
     from paper_2210_06223_b200 import build
     build.build()
 
@@ -46,6 +50,8 @@ def test_sanitizer_clean(tool):
         env["LASNET_TMA_Y"] = "0"
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, env=env)
     out = r.stdout + r.stderr
+    if "compute-sanitizer is closed" in out:
+        pytest.skip("compute-sanitizer is closed on this GPU pool")
     assert "sanitize run ok" in out, out[-4000:]
     assert r.returncode == 0, out[-4000:]
     assert "ERROR SUMMARY: 0 errors" in out or "RACECHECK SUMMARY: 0 hazards" in out, out[-4000:]
