@@ -170,7 +170,7 @@ __device__ __forceinline__ TileGeo tile_geo(const ConvArgs &a, int BN) {
     int mt;
     if (MODE == CONV2_DYN || MODE == CONV2_GATHER) {
         mt = (*a.count + a.units_per_tile - 1) / a.units_per_tile;  // patch-aligned tiles
-    } else if (MODE == CONV2_DENSE || MODE == STEM || (MODE == CONV3_DENSE && a.view4)) {
+    } else if (MODE == CONV2_DENSE || MODE == STEM || ((MODE == CONV3_DENSE || MODE == PROJ_SC) && a.view4)) {
         mt = a.dense_tiles;
         if (MODE == STEM) g.n_tiles_n = 1;  // one 64-channel weight, BN / 64 output rows per tile
     } else {
@@ -283,7 +283,8 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                 const int n0 = (tile - mt * geo.n_tiles_n) * BN;
                 const int u0 = MODE == CONV2_DYN ? mt * args.units_per_tile : 0;  // first patch (conv2 dyn)
                 int d2n = 0, d2y = 0, d2x = 0;
-                if (MODE == CONV2_DENSE || (MODE == CONV3_DENSE && args.view4)) dense_tile_origin(args, mt, d2n, d2y, d2x);
+                if (MODE == CONV2_DENSE || ((MODE == CONV3_DENSE || MODE == PROJ_SC) && args.view4))
+                    dense_tile_origin(args, mt, d2n, d2y, d2x);
                 TRACE(lt, 0);
                 for (int kb = 0; kb < num_kb; ++kb, ++it) {
                     const int stage = it % ST;
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     int a_bytes = kABytes;  // conv1 dyn: A arrives by cp.async (not counted here)
                     if (C::kGather) a_bytes = 0;
                     else if (MODE == STEM) a_bytes = args.cols_w * 128;  // 4 boxes of cols_w / 4 columns
-                    else if (MODE == CONV2_DYN || MODE == CONV2_DENSE || (MODE == CONV3_DENSE && args.view4))
+                    else if (MODE == CONV2_DYN || MODE == CONV2_DENSE || ((MODE == CONV3_DENSE || MODE == PROJ_SC) && args.view4))
                         a_bytes = args.box_rows * 128;
                     if (PAIR) {
                         // own A rows + own half of the B rows; both CTAs' bytes complete on the lead's barrier
@@ -354,7 +355,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
 #pragma unroll
                         for (int k = 0; k < 4; ++k)
                             tma_load_4d(sa + k * q * 128, &args.tmap_s[k], fb, 0, xb * q, 2 * oy0 + kb - 3, n);
-                    } else if (MODE == CONV3_DENSE && args.view4) {
+                    } else if ((MODE == CONV3_DENSE || MODE == PROJ_SC) && args.view4) {
                         // the strided projection shortcut: A = a 4-D view of x at every stride-th pixel
                         // (dense tiles of rows_h x cols_w output pixels of imgs_box images): no subsample copy
                         tma_load_4d(sa, &args.tmap_a, fb, kb * kBK, d2x, d2y, d2n);
@@ -693,7 +694,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             bool zero = false;  // conv1: halo pixel outside the image stores 0 (R6)
             if (MODE == CONV1_DYN) zero = mt * kBM + r < M && halo_pixel(args, mt * kBM + r, M) < 0;
             bool relu = !args.no_relu;
-            if (MODE == CONV3_DENSE && args.relu_mask != nullptr) {
+            if ((MODE == CONV3_DENSE || MODE == PROJ_SC) && args.relu_mask != nullptr) {
                 // dynamic projection shortcut: ReLU(R) on inactive cells, R itself on active ones
                 int n = -1, yy = 0, xx = 0;
                 if (args.view4) {  // dense tile geometry (rows_h x cols_w pixels of imgs_box images)
@@ -832,7 +833,7 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             named_bar_sync(1, EPI);
             if (tid == 0) TRACE(lt, 5);
             if (tid == 0) {
-                if (MODE == CONV2_DENSE) {
+                if (MODE == CONV2_DENSE || (MODE == PROJ_SC && args.view4)) {  // 4-D output view of the dense tile
                     int d2n, d2y, d2x;
                     dense_tile_origin(args, mt, d2n, d2y, d2x);
                     for (int c = 0; c < BN / 64; ++c)
@@ -934,6 +935,7 @@ int conv_tc_plan(int mode, int n, int *pair) {
     // 256-column tiles: A (the gathered rows / the im2col taps) is staged once per M
     // tile instead of once per 128-column N tile
     if (n % 256 == 0 && (mode == CONV1_DYN || mode == CONV1_DENSE || mode == CONV1_DENSE_MASK || mode == CONV2_GATHER ||
+                         mode == PROJ_SC ||
                          (mode == CONV2_DYN && conv2_bn256())))
         return 256;
     return 128;
@@ -969,6 +971,7 @@ cudaError_t launch_conv_tc(int mode, const ConvArgs &a, int max_tiles_m, int num
         case CONV1_DENSE_MASK: return launch_mode<CONV1_DENSE_MASK>(a, max_tiles_m, num_sms, st);
         case CONV2_DENSE: return launch_mode<CONV2_DENSE>(a, max_tiles_m, num_sms, st);
         case CONV3_DENSE: return launch_mode<CONV3_DENSE>(a, max_tiles_m, num_sms, st);
+        case PROJ_SC: return launch_mode<PROJ_SC>(a, max_tiles_m, num_sms, st);
         case STEM: {  // BN = 128: the two output rows' 64-channel accumulators (four rows, BN 256: 0.32 -> 0.36 ms)
             auto kern = conv_tc_kernel<STEM, 128, false>;
             const int smem = Cfg<STEM, 128>::smem_bytes(64, a.K);

@@ -93,6 +93,7 @@ const char *conv_name(int mode) {
         case CONV1_DENSE: return "conv1_dense";
         case CONV2_DENSE: return "conv2_dense";
         case CONV3_DENSE: return "conv3_dense";
+        case PROJ_SC: return "conv3_dense";  // (no residual: the projection block's [W3 | Wd] conv)
         case CONV1_DENSE_MASK: return "conv1_mask";
         case STEM: return "stem_conv";
     }
@@ -415,7 +416,8 @@ int prepare_tc(int mode, ConvArgs &a, const lasnet_block_desc *d, const void *x,
             ok = ok && tmap4(&a.tmap_out, h2, C, d->w, d->h, d->n, 64, a.cols_w, a.rows_h, a.imgs_box);
             return ok ? a.dense_tiles : -1;
         }
-        case CONV3_DENSE: {
+        case CONV3_DENSE:
+        case PROJ_SC: {
             ok = ok && tmap2(&a.tmap_a, h2, C, px, 64, 128);
             // y rows are contiguous: the epilogue TMA-stores whole tiles (tma_y)
             ok = ok && tmap2(&a.tmap_out, a.out, a.N, px, 64, 128);
@@ -512,7 +514,7 @@ cudaError_t run_conv(const lasnet_block_desc *d, int mode, ConvArgs &a, int max_
         return launch_conv_tc(mode, a, tiles, num_sms(), st);
     }
     KernelEvents ev(st, "conv_simt");
-    return launch_conv_simt(mode, a, max_rows, st);
+    return launch_conv_simt(mode == PROJ_SC ? CONV3_DENSE : mode, a, max_rows, st);
 }
 
 // Steps 4+5 on the gathered h1 [c_mid/64][cap][S+2][S+2][64]: one fused kernel
@@ -951,7 +953,7 @@ lasnet_status proj_dyn_forward(const lasnet_block_desc *d, const lasnet_block_we
         c.a_src = xs; c.w = w->wd; c.bias = w->bd; c.out = y; c.resid = nullptr;
         c.K = d->c_in; c.N = d->c_out; c.a_ld = d->c_in; c.out_ld = d->c_out;
         c.relu_mask = m;
-        bool ok = tmap2(&c.tmap_b, w->wd, d->c_in, d->c_out, 64, b_box_rows(c, d->c_out, CONV3_DENSE));
+        bool ok = tmap2(&c.tmap_b, w->wd, d->c_in, d->c_out, 64, b_box_rows(c, d->c_out, PROJ_SC));
         int tiles = (int)((po + 127) / 128);
         if (view4) {
             dense_tiling(c, d->n, d->h, d->w);  // tiles of rows_h x cols_w output pixels (x imgs_box images)
@@ -971,7 +973,7 @@ lasnet_status proj_dyn_forward(const lasnet_block_desc *d, const lasnet_block_we
         }
         if (!ok) return LASNET_ERR_CUDA;
         KernelEvents ev(st, "shortcut");
-        if (launch_conv_tc(CONV3_DENSE, c, tiles, num_sms(), st) != cudaSuccess) return LASNET_ERR_CUDA;
+        if (launch_conv_tc(PROJ_SC, c, tiles, num_sms(), st) != cudaSuccess) return LASNET_ERR_CUDA;
         ++launches;
     }
     // step 3: gather + conv1 over each active cell's input window (side st(S-1)+3)
@@ -1298,7 +1300,7 @@ lasnet_status lasnet_proj_block(const lasnet_block_desc *d, const lasnet_block_w
     c.K = d->c_mid + d->c_in; c.N = d->c_out; c.a_ld = d->c_mid; c.out_ld = d->c_out;
     c.a2_kb = d->c_mid / 64;
     if (!tmap2(&c.tmap_s[0], S2 > 1 ? xs : x, d->c_in, (uint64_t)pxo, 64, 128)) return LASNET_ERR_CUDA;
-    if (run_conv(d, CONV3_DENSE, c, pxo, x, y, nullptr, h2, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    if (run_conv(d, PROJ_SC, c, pxo, x, y, nullptr, h2, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
     g_last_launches = launches + 2;
     return LASNET_OK;
 }
@@ -1578,7 +1580,8 @@ lasnet_status lasnet_regnet_block(const lasnet_block_desc *d, const lasnet_regne
     } else {
         c.w = w->wc; c.bias = w->bc; c.resid = x; c.K = C;
     }
-    if (run_conv(d, CONV3_DENSE, c, (int)pxo, x, y, nullptr, r.h2, 0, st) != cudaSuccess) return LASNET_ERR_CUDA;
+    if (run_conv(d, c.resid ? CONV3_DENSE : PROJ_SC, c, (int)pxo, x, y, nullptr, r.h2, 0, st) != cudaSuccess)
+        return LASNET_ERR_CUDA;
     g_last_launches = launches + 1;
     return LASNET_OK;
 }

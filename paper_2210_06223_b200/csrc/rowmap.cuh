@@ -41,6 +41,8 @@ enum ConvMode : int {
     STEM = 7,              // ResNet stem 7x7 stride 2 on 8-channel (3 + zero) input: tile = one output row
     CONV2_GATHER = 8,      // CONV2_DYN whose A rows are gathered by cp.async straight from the DENSE h1
                            // [c_mid/64][m_dense][64] (masker-fused schedule: no gathered window copy)
+    PROJ_SC = 9,           // CONV3_DENSE without a residual (the projection blocks' dense 1x1 shortcut / the
+                           // static block's [W3 | Wd] conv): 256-column tiles, whole tiles stored by TMA
 };
 
 struct ConvArgs {
