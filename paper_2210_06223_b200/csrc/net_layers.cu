@@ -80,22 +80,26 @@ cudaError_t launch_maxpool(const void *x, void *y, int n_img, int Ho, int Wo, in
                     static_cast<uint4 *>(y), n_img, Ho, Wo, c / 8);
 }
 
-// Head, pass 1: global average pool [n][hw][c] bf16 -> pooled [n][c] fp32
-// (fixed-order fp32 sum over the hw pixels, then / hw); a thread owns 8
-// consecutive channels (16-B loads, coalesced along the channels).
-__global__ void __launch_bounds__(256) avgpool_kernel(const __nv_bfloat16 *__restrict__ x, float *__restrict__ pooled,
-                                                      int n_img, int hw, int c) {
+// Head, pass 1: global average pool [n][hw][c] bf16 -> pooled [n][c] fp32.  CTA =
+// (image, 32 channel vectors of 8 channels); its 8 warps take the pixels p = warp,
+// warp + 8, ... (fp32 sums in pixel order), and the 8 partials are added in warp order
+// (fixed order), then / hw.  16-B loads coalesced along the channels.
+constexpr int kPoolGroups = 8;
+__global__ void __launch_bounds__(32 * kPoolGroups) avgpool_kernel(const __nv_bfloat16 *__restrict__ x,
+                                                                   float *__restrict__ pooled, int n_img, int hw,
+                                                                   int c) {
     pdl_wait();
     pdl_trigger();
-    const int cv = c / 8;
-    const long total = (long)n_img * cv;
-    for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
-        const int v = (int)(i % cv);
-        const long n = i / cv;
-        float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    __shared__ float part[kPoolGroups][32][9];
+    const int cv = c / 8, lane = threadIdx.x & 31, pg = threadIdx.x >> 5;
+    const int vblocks = (cv + 31) / 32;
+    const long n = blockIdx.x / vblocks;
+    const int v = (blockIdx.x - (int)(n * vblocks)) * 32 + lane;
+    float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (v < cv) {
         const uint4 *src = reinterpret_cast<const uint4 *>(x + n * hw * c) + v;
-#pragma unroll 8
-        for (int p = 0; p < hw; ++p) {  // loads hoisted by the unroll; the adds stay in pixel order
+#pragma unroll 4
+        for (int p = pg; p < hw; p += kPoolGroups) {
             const uint4 q = __ldg(src + (long)p * cv);
             const uint32_t u[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
@@ -104,94 +108,107 @@ __global__ void __launch_bounds__(256) avgpool_kernel(const __nv_bfloat16 *__res
                 s[2 * e + 1] += __uint_as_float(u[e] & 0xffff0000u);
             }
         }
+    }
 #pragma unroll
-        for (int e = 0; e < 8; ++e) pooled[n * c + 8 * v + e] = s[e] / (float)hw;
+    for (int e = 0; e < 8; ++e) part[pg][lane][e] = s[e];
+    __syncthreads();
+    // thread (lane, e = pg): channel 8 v + e, partials added in group order
+    if (v < cv) {
+        float t = part[0][lane][pg];
+#pragma unroll
+        for (int k = 1; k < kPoolGroups; ++k) t += part[k][lane][pg];
+        pooled[n * c + 8 * v + pg] = t / (float)hw;
     }
 }
 
-// Head, pass 2: logits[n][k] = b[k] + sum_c pooled[n][c] w[k][c] -- a SIMT GEMM tile
-// of 32 images x 32 classes per 256-thread CTA: four K slices of 64 threads, each
-// thread a 4 x 4 register block over its slice's 64-channel chunks (transposed in
-// shared memory so every thread's four images / classes are one 16-B load); the four
-// slice partials are then added in slice order (deterministic).  8 warps per CTA keep
-// the FMA pipes fed (a 2-warp CTA was latency-bound at ~120 us).
-constexpr int kFcT = 32, kFcK = 64, kFcP = 36, kFcS = 4;  // tile, K chunk, padded row, K slices
-__global__ void __launch_bounds__(256) fc_kernel(const float *__restrict__ pooled, const __nv_bfloat16 *__restrict__ w,
-                                                 const float *__restrict__ b, float *__restrict__ logits, int n_img,
-                                                 int c, int classes) {
+// Head, pass 2: logits[n][k] = b[k] + sum_c pooled[n][c] w[k][c] on the tensor cores
+// (mma.sync m16n8k16, bf16 x bf16 -> fp32).  The fp32 pooled operand is split into three
+// bf16 terms, p = p0 + p1 + p2 (p0 = RNE_bf16(p), p1 = RNE_bf16(p - p0), p2 = RNE_bf16(p - p0 - p1):
+// 3 x 8 significand bits cover fp32's 24), and the bf16 x bf16 products are exact in fp32,
+// so the three MMAs over the same bf16 weights see the fp32 operand; only the fp32
+// accumulation order differs from a scalar loop.  CTA = 16 images x 32 classes, its four
+// warps take four K slices (each warp: 16 x 32 as four n8 blocks), and the slice partials
+// are added in slice order (deterministic).  (The SIMT GEMM this replaces took 74 us.)
+constexpr int kFcImg = 16, kFcCls = 32, kFcSlices = 4;
+
+__device__ __forceinline__ void split3_bf16x2(float2 v, uint32_t (&o)[3]) {
+    float x = v.x, y = v.y;
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+        const __nv_bfloat16 bx = __float2bfloat16_rn(x), by = __float2bfloat16_rn(y);
+        o[p] = (uint32_t)__bfloat16_as_ushort(bx) | ((uint32_t)__bfloat16_as_ushort(by) << 16);
+        x -= __bfloat162float(bx);
+        y -= __bfloat162float(by);
+    }
+}
+
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__global__ void __launch_bounds__(32 * kFcSlices) fc_kernel(const float *__restrict__ pooled,
+                                                            const __nv_bfloat16 *__restrict__ w,
+                                                            const float *__restrict__ b, float *__restrict__ logits,
+                                                            int n_img, int c, int classes) {
     pdl_wait();
     pdl_trigger();
-    extern __shared__ __align__(16) float fsm[];
-    const int slice = threadIdx.x >> 6, lt = threadIdx.x & 63;
-    float(*sa)[kFcP] = reinterpret_cast<float(*)[kFcP]>(fsm + slice * 2 * kFcK * kFcP);
-    float(*sb)[kFcP] = reinterpret_cast<float(*)[kFcP]>(fsm + slice * 2 * kFcK * kFcP + kFcK * kFcP);
-    const int tx = lt & 7, ty = lt >> 3;
-    const int k0 = blockIdx.x * kFcT, n0 = blockIdx.y * kFcT;
+    __shared__ float red[kFcSlices][kFcImg][kFcCls + 1];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int n0 = blockIdx.y * kFcImg, k0 = blockIdx.x * kFcCls;
+    // fragment rows (images) g, g + 8 and columns (classes) g of the four n8 blocks; rows / classes
+    // past the end read a valid row (clamped) and are never stored
+    const float *pa0 = pooled + (long)min(n0 + g, n_img - 1) * c;
+    const float *pa1 = pooled + (long)min(n0 + g + 8, n_img - 1) * c;
+    const __nv_bfloat16 *wb[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) wb[j] = w + (long)min(k0 + 8 * j + g, classes - 1) * c;
+    const int ksl = (c + 16 * kFcSlices - 1) / (16 * kFcSlices) * 16;  // K slice (multiple of 16)
+    const int kbeg = warp * ksl, kend = min(c, kbeg + ksl);
     float acc[4][4] = {};
-    // the next chunk's 8 (pooled, weight) vectors per thread are loaded into registers while the
-    // current chunk is multiplied out of shared memory (the loads were a round trip per chunk)
-    constexpr int kPer = kFcT * kFcK / 8 / 64;  // 16-B vector pairs per thread per chunk (4)
-    float4 pa[kPer][2];
-    uint4 pw[kPer];
-    auto load = [&](int c0) {
-#pragma unroll
-        for (int t = 0; t < kPer; ++t) {
-            const int e = lt + 64 * t;
-            const int r = e / (kFcK / 8), cc = (e % (kFcK / 8)) * 8, ch = c0 + cc;
-            const int n = n0 + r, k = k0 + r;
-            pa[t][0] = pa[t][1] = make_float4(0.f, 0.f, 0.f, 0.f);
-            pw[t] = make_uint4(0u, 0u, 0u, 0u);
-            if (c0 < c && n < n_img && ch < c) {
-                pa[t][0] = *reinterpret_cast<const float4 *>(pooled + (long)n * c + ch);
-                pa[t][1] = *reinterpret_cast<const float4 *>(pooled + (long)n * c + ch + 4);
-            }
-            if (c0 < c && k < classes && ch < c) pw[t] = __ldg(reinterpret_cast<const uint4 *>(w + (long)k * c + ch));
-        }
-    };
-    load(slice * kFcK);
-    for (int c0 = slice * kFcK; c0 < c; c0 += kFcS * kFcK) {
-#pragma unroll
-        for (int t = 0; t < kPer; ++t) {
-            const int e = lt + 64 * t;
-            const int r = e / (kFcK / 8), cc = (e % (kFcK / 8)) * 8;
-            const float av[8] = {pa[t][0].x, pa[t][0].y, pa[t][0].z, pa[t][0].w,
-                                 pa[t][1].x, pa[t][1].y, pa[t][1].z, pa[t][1].w};
-            const uint32_t u[4] = {pw[t].x, pw[t].y, pw[t].z, pw[t].w};
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                sa[cc + q][r] = av[q];
-                sb[cc + q][r] = (q & 1) ? __uint_as_float(u[q >> 1] & 0xffff0000u) : __uint_as_float(u[q >> 1] << 16);
-            }
-        }
-        __syncwarp();
-        asm volatile("bar.sync %0, 64;" ::"r"(1 + slice));  // this slice's 2 warps
-        load(c0 + kFcS * kFcK);  // in flight during this chunk's products
-        const int kk_end = min(kFcK, c - c0);
 #pragma unroll 4
-        for (int kk = 0; kk < kk_end; ++kk) {
-            const float4 a4 = *reinterpret_cast<const float4 *>(&sa[kk][ty * 4]);
-            const float4 b4 = *reinterpret_cast<const float4 *>(&sb[kk][tx * 4]);
-            const float av[4] = {a4.x, a4.y, a4.z, a4.w}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
+    for (int kk = kbeg; kk < kend; kk += 16) {
+        const int ka = kk + 2 * t, kb = ka + 8;  // (c % 8 == 0: kb < c unless c % 16 == 8 at the tail)
+        const float2 z = make_float2(0.f, 0.f);
+        const float2 x00 = __ldg(reinterpret_cast<const float2 *>(pa0 + ka));
+        const float2 x10 = __ldg(reinterpret_cast<const float2 *>(pa1 + ka));
+        const float2 x01 = kb < c ? __ldg(reinterpret_cast<const float2 *>(pa0 + kb)) : z;
+        const float2 x11 = kb < c ? __ldg(reinterpret_cast<const float2 *>(pa1 + kb)) : z;
+        uint32_t bw[4][2];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j) {
+            bw[j][0] = __ldg(reinterpret_cast<const unsigned *>(wb[j] + ka));
+            bw[j][1] = kb < c ? __ldg(reinterpret_cast<const unsigned *>(wb[j] + kb)) : 0u;
         }
-        asm volatile("bar.sync %0, 64;" ::"r"(1 + slice));
+        uint32_t s00[3], s10[3], s01[3], s11[3];
+        split3_bf16x2(x00, s00);
+        split3_bf16x2(x10, s10);
+        split3_bf16x2(x01, s01);
+        split3_bf16x2(x11, s11);
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+            const uint32_t a[4] = {s00[p], s10[p], s01[p], s11[p]};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) mma_bf16_16816(acc[j], a, bw[j][0], bw[j][1]);
+        }
     }
-    // slice partials -> logits, added in slice order
-    __syncthreads();
-    float *red = fsm;  // [kFcS][32][33]
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) red[(slice * 32 + ty * 4 + i) * 33 + tx * 4 + j] = acc[i][j];
+    for (int j = 0; j < 4; ++j) {
+        red[warp][g][8 * j + 2 * t] = acc[j][0];
+        red[warp][g][8 * j + 2 * t + 1] = acc[j][1];
+        red[warp][g + 8][8 * j + 2 * t] = acc[j][2];
+        red[warp][g + 8][8 * j + 2 * t + 1] = acc[j][3];
+    }
     __syncthreads();
-    for (int e = threadIdx.x; e < kFcT * kFcT; e += 256) {
-        const int r = e / kFcT, col = e % kFcT, n = n0 + r, k = k0 + col;
+    for (int e = threadIdx.x; e < kFcImg * kFcCls; e += 32 * kFcSlices) {
+        const int r = e / kFcCls, col = e % kFcCls, n = n0 + r, k = k0 + col;
         if (n < n_img && k < classes) {
-            float v = red[r * 33 + col];
-            for (int sl = 1; sl < kFcS; ++sl) v += red[(sl * 32 + r) * 33 + col];
+            float v = red[0][r][col];
+#pragma unroll
+            for (int sl = 1; sl < kFcSlices; ++sl) v += red[sl][r][col];
             logits[(long)n * classes + k] = v + b[k];
         }
     }
@@ -201,20 +218,13 @@ cudaError_t launch_head(const void *x, const void *w, const float *b, float *poo
                         int c, int classes, int num_sms, cudaStream_t st) {
     if (n_img == 0) return cudaSuccess;
     if (c % 8) return cudaErrorInvalidValue;
-    long g1 = ((long)n_img * (c / 8) + 255) / 256;
-    if (g1 > 8L * num_sms) g1 = 8L * num_sms;
-    cudaError_t e = launch_k(avgpool_kernel, dim3((unsigned)g1), dim3(256), 0, st,
+    (void)num_sms;
+    const long g1 = (long)n_img * ((c / 8 + 31) / 32);
+    cudaError_t e = launch_k(avgpool_kernel, dim3((unsigned)g1), dim3(32 * kPoolGroups), 0, st,
                              static_cast<const __nv_bfloat16 *>(x), pooled, n_img, hw, c);
     if (e != cudaSuccess) return e;
-    const dim3 g2((unsigned)((classes + kFcT - 1) / kFcT), (unsigned)((n_img + kFcT - 1) / kFcT));
-    const int smem = kFcS * 2 * kFcK * kFcP * 4;  // >= the [4][32][33] partials
-    static bool configured = false;
-    if (!configured) {
-        e = cudaFuncSetAttribute(fc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
-    return launch_k(fc_kernel, g2, dim3(256), smem, st, static_cast<const float *>(pooled),
+    const dim3 g2((unsigned)((classes + kFcCls - 1) / kFcCls), (unsigned)((n_img + kFcImg - 1) / kFcImg));
+    return launch_k(fc_kernel, g2, dim3(32 * kFcSlices), 0, st, static_cast<const float *>(pooled),
                     static_cast<const __nv_bfloat16 *>(w), b, logits, n_img, c, classes);
 }
 
