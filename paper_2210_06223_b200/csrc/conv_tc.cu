@@ -79,6 +79,10 @@ template <int MODE, int BN, bool PAIR = false> struct Cfg {
     static constexpr bool kResid = MODE == CONV3_DYN || MODE == CONV3_DENSE;
     static constexpr bool kGather = MODE == CONV1_DYN || MODE == CONV2_GATHER;
     static constexpr bool kMasker = MODE == CONV1_DENSE_MASK;
+    // conv2 gather at BN = 256: the h2 tile is staged and stored in two 128-column halves through
+    // one 32 KB buffer, which frees room for a 4th stage (its cp.async A gather is bound by the bytes
+    // in flight per SM)
+    static constexpr bool kHalfStage = MODE == CONV2_GATHER && BN == 256 && !PAIR;
 #ifndef LASNET_RESID_EPI_WARPS
 #define LASNET_RESID_EPI_WARPS 16
 #endif
@@ -110,7 +114,7 @@ template <int MODE, int BN, bool PAIR = false> struct Cfg {
     static constexpr bool kBRes = MODE == STEM;
     static constexpr int kBResBytes = kBRes ? 7 * kBBytes : 0;
     static constexpr int kStageBytes = kABytes + (kBRes ? 0 : kBBytes);
-    static constexpr int kStagingBytes = (BN / 64) * kChunkBytes;
+    static constexpr int kStagingBytes = (kHalfStage ? BN / 128 : BN / 64) * kChunkBytes;
     // conv1 dyn: HBM gather -> deep pipeline, 1 staging buffer (TMA store drains fast)
     // conv3: short K (2-8 blocks) -> 3 stages, 3 staging buffers (residual prefetched 2 tiles ahead)
     // BN = 256 (conv1 at c_mid >= 256): A is read once per M tile instead
@@ -122,6 +126,7 @@ template <int MODE, int BN, bool PAIR = false> struct Cfg {
     // stem: resident weights, 16 KB A-only stages
     static constexpr int kStages =
         MODE == STEM ? 6
+        : kHalfStage ? 4
         : PAIR ? (BN == 256 ? 4 : (kResid ? 4 : 6))
                : (BN == 256 ? 3 : (kGather ? (BN == 128 ? 6 : 8) : (kResid ? 3 : (BN == 128 ? 4 : 6))));
     static constexpr int kTmemCols = 2 * BN;
@@ -133,7 +138,10 @@ template <int MODE, int BN, bool PAIR = false> struct Cfg {
     static constexpr bool kWmSmem = kMasker;
     // + 1 KB: the dynamic smem base is only guaranteed 16-B aligned (a CTA co-resident
     // with another kernel's CTA may start anywhere); the kernel rounds it up to 1 KB
-    static constexpr int smem_bytes(int n, int k) { return 1024 + kBiasOff + n * 4 + (kWmSmem ? k * 4 : 0); }
+    static constexpr bool kBiasSmem = !kHalfStage;  // (kHalfStage: bias read through L1, smem is full)
+    static constexpr int smem_bytes(int n, int k) {
+        return 1024 + kBiasOff + (kBiasSmem ? n * 4 : 0) + (kWmSmem ? k * 4 : 0);
+    }
 };
 
 template <int MODE, int BN> __host__ __device__ constexpr int threads_of() { return Cfg<MODE, BN>::kThreads; }
@@ -205,7 +213,8 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
     const int rank = PAIR ? (int)cluster_ctarank() : 0;
     const bool lead = rank == 0;
 
-    for (int i = tid; i < args.N; i += C::kThreads) bias_s[i] = args.bias[i];
+    if (C::kBiasSmem)
+        for (int i = tid; i < args.N; i += C::kThreads) bias_s[i] = args.bias[i];
     // masker weight (CONV1_DENSE_MASK); N % 64 == 0 keeps it 16-B aligned
     const float *wm_s = C::kWmSmem ? bias_s + args.N : args.wm;
     if (C::kWmSmem)
@@ -691,6 +700,57 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             const int n0 = (tile - mt * geo.n_tiles_n) * BN;
             const int acc = lt & 1, b = lt % NSTG;
             const uint32_t sbuf = staging + b * C::kStagingBytes;
+            if constexpr (C::kHalfStage) {
+                // two passes of 128 columns through the one 32 KB staging buffer: pass p stages
+                // columns [128 p, 128 p + 128) (warp: its 32 rows x 64 columns) and TMA-stores them
+                mbar_wait(bar_tfull + 8 * acc, (lt >> 1) & 1);
+                tc_fence_after();
+                const int row0 = mt * args.units_per_tile * args.S * args.S;
+#pragma unroll 1
+                for (int p = 0; p < 2; ++p) {
+                    const int qp = 2 * lt + p;  // pass counter: the buffer's use
+                    mbar_wait(bar_sempty, (qp & 1) ^ 1);
+#pragma unroll 1
+                    for (int cc = 0; cc < 64; cc += 32) {
+                        const int c = 128 * p + (warp >> 2) * 64 + cc, hc = c - 128 * p;
+                        uint32_t v[32];
+                        tmem_ld32(tmem_base + lane_base + acc * BN + c, v);
+                        tmem_ld_wait();
+                        const uint32_t rowbase = staging + (hc >> 6) * kChunkBytes + r * 128;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const uint32_t saddr = rowbase + ((((hc & 63) >> 3) + q) ^ (r & 7)) * 16;
+                            const float4 b0 = __ldg(reinterpret_cast<const float4 *>(args.bias + n0 + c + 8 * q));
+                            const float4 b1 = __ldg(reinterpret_cast<const float4 *>(args.bias + n0 + c + 8 * q + 4));
+                            const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                            uint32_t pk[4];
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const float lo = fmaxf(__uint_as_float(v[8 * q + 2 * e]) + bb[2 * e], 0.f);
+                                const float hi = fmaxf(__uint_as_float(v[8 * q + 2 * e + 1]) + bb[2 * e + 1], 0.f);
+                                pk[e] = pack_bf16x2(lo, hi);
+                            }
+                            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(saddr), "r"(pk[0]), "r"(pk[1]),
+                                         "r"(pk[2]), "r"(pk[3])
+                                         : "memory");
+                        }
+                    }
+                    if (p == 1) {  // every TMEM read of this tile is done
+                        tc_fence_before();
+                        mbar_arrive(bar_tempty + 8 * acc);
+                    }
+                    fence_proxy_async_smem();
+                    named_bar_sync(1, EPI);
+                    if (tid == 0) {
+                        for (int c2 = 0; c2 < 2; ++c2)
+                            tma_store_2d(&args.tmap_out, staging + c2 * kChunkBytes, n0 + 128 * p + 64 * c2, row0);
+                        bulk_commit();
+                        bulk_wait_read<0>();  // the buffer is free once this store has read it
+                        mbar_arrive(bar_sempty);
+                    }
+                }
+                continue;
+            }
             bool zero = false;  // conv1: halo pixel outside the image stores 0 (R6)
             if (MODE == CONV1_DYN) zero = mt * kBM + r < M && halo_pixel(args, mt * kBM + r, M) < 0;
             bool relu = !args.no_relu;
