@@ -82,7 +82,8 @@ template <int MODE, int BN, bool PAIR = false> struct Cfg {
     // conv2 gather at BN = 256: the h2 tile is staged and stored in two 128-column halves through
     // one 32 KB buffer, which frees room for a 4th stage (its cp.async A gather is bound by the bytes
     // in flight per SM)
-    static constexpr bool kHalfStage = MODE == CONV2_GATHER && BN == 256 && !PAIR;
+    static constexpr bool kHalfStage =
+        (MODE == CONV2_GATHER || MODE == CONV1_DENSE || MODE == CONV1_DENSE_MASK) && BN == 256 && !PAIR;
 #ifndef LASNET_RESID_EPI_WARPS
 #define LASNET_RESID_EPI_WARPS 16
 #endif
@@ -114,7 +115,9 @@ template <int MODE, int BN, bool PAIR = false> struct Cfg {
     static constexpr bool kBRes = MODE == STEM;
     static constexpr int kBResBytes = kBRes ? 7 * kBBytes : 0;
     static constexpr int kStageBytes = kABytes + (kBRes ? 0 : kBBytes);
-    static constexpr int kStagingBytes = (kHalfStage ? BN / 128 : BN / 64) * kChunkBytes;
+    // kHalfStage: 64-column chunks per staging pass (the masker's weights keep their smem: one chunk)
+    static constexpr int kStagingChunks = kHalfStage ? (kMasker ? 1 : 2) : BN / 64;
+    static constexpr int kStagingBytes = kStagingChunks * kChunkBytes;
     // conv1 dyn: HBM gather -> deep pipeline, 1 staging buffer (TMA store drains fast)
     // conv3: short K (2-8 blocks) -> 3 stages, 3 staging buffers (residual prefetched 2 tiles ahead)
     // BN = 256 (conv1 at c_mid >= 256): A is read once per M tile instead
@@ -216,9 +219,10 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
     if (C::kBiasSmem)
         for (int i = tid; i < args.N; i += C::kThreads) bias_s[i] = args.bias[i];
     // masker weight (CONV1_DENSE_MASK); N % 64 == 0 keeps it 16-B aligned
-    const float *wm_s = C::kWmSmem ? bias_s + args.N : args.wm;
+    const int wm_off = C::kBiasSmem ? args.N : 0;  // the masker weight follows the bias (if that is in smem)
+    const float *wm_s = C::kWmSmem ? bias_s + wm_off : args.wm;
     if (C::kWmSmem)
-        for (int i = tid; i < args.K; i += C::kThreads) bias_s[args.N + i] = args.wm[i];
+        for (int i = tid; i < args.K; i += C::kThreads) bias_s[wm_off + i] = args.wm[i];
     if (tid == 0) {
         for (int s = 0; s < ST; ++s) {
             // TMA producer's arrive.expect_tx (+ one noinc arrival per gather thread for conv1 dyn)
@@ -701,18 +705,19 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             const int acc = lt & 1, b = lt % NSTG;
             const uint32_t sbuf = staging + b * C::kStagingBytes;
             if constexpr (C::kHalfStage) {
-                // two passes of 128 columns through the one 32 KB staging buffer: pass p stages
-                // columns [128 p, 128 p + 128) (warp: its 32 rows x 64 columns) and TMA-stores them
+                // BN / CP passes of CP columns through the one staging buffer: pass p stages columns
+                // [CP p, CP p + CP) (warp: its 32 rows x CP / 2 columns) and TMA-stores them
+                constexpr int CP = 64 * C::kStagingChunks, NP = BN / CP;
                 mbar_wait(bar_tfull + 8 * acc, (lt >> 1) & 1);
                 tc_fence_after();
-                const int row0 = mt * args.units_per_tile * args.S * args.S;
+                const int row0 = MODE == CONV2_GATHER ? mt * args.units_per_tile * args.S * args.S : mt * kBM;
 #pragma unroll 1
-                for (int p = 0; p < 2; ++p) {
-                    const int qp = 2 * lt + p;  // pass counter: the buffer's use
+                for (int p = 0; p < NP; ++p) {
+                    const int qp = NP * lt + p;  // pass counter: the buffer's use
                     mbar_wait(bar_sempty, (qp & 1) ^ 1);
 #pragma unroll 1
-                    for (int cc = 0; cc < 64; cc += 32) {
-                        const int c = 128 * p + (warp >> 2) * 64 + cc, hc = c - 128 * p;
+                    for (int cc = 0; cc < CP / 2; cc += 32) {
+                        const int c = CP * p + (warp >> 2) * (CP / 2) + cc, hc = c - CP * p;
                         uint32_t v[32];
                         tmem_ld32(tmem_base + lane_base + acc * BN + c, v);
                         tmem_ld_wait();
@@ -735,15 +740,20 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                                          : "memory");
                         }
                     }
-                    if (p == 1) {  // every TMEM read of this tile is done
+                    if (p == NP - 1) {  // every TMEM read of this tile is done
                         tc_fence_before();
                         mbar_arrive(bar_tempty + 8 * acc);
                     }
                     fence_proxy_async_smem();
                     named_bar_sync(1, EPI);
                     if (tid == 0) {
-                        for (int c2 = 0; c2 < 2; ++c2)
-                            tma_store_2d(&args.tmap_out, staging + c2 * kChunkBytes, n0 + 128 * p + 64 * c2, row0);
+                        for (int c2 = 0; c2 < C::kStagingChunks; ++c2) {
+                            if (MODE == CONV2_GATHER)
+                                tma_store_2d(&args.tmap_out, staging + c2 * kChunkBytes, n0 + CP * p + 64 * c2, row0);
+                            else  // conv1: h1 [c_mid/64][rows][64]
+                                tma_store_3d(&args.tmap_out, staging + c2 * kChunkBytes, 0, mt * kBM,
+                                             ((n0 + CP * p) >> 6) + c2);
+                        }
                         bulk_commit();
                         bulk_wait_read<0>();  // the buffer is free once this store has read it
                         mbar_arrive(bar_sempty);
