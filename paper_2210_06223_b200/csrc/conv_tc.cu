@@ -83,7 +83,8 @@ template <int MODE, int BN, bool PAIR = false> struct Cfg {
     // one 32 KB buffer, which frees room for a 4th stage (its cp.async A gather is bound by the bytes
     // in flight per SM)
     static constexpr bool kHalfStage =
-        (MODE == CONV2_GATHER || MODE == CONV1_DENSE || MODE == CONV1_DENSE_MASK) && BN == 256 && !PAIR;
+        (MODE == CONV2_GATHER || MODE == CONV1_DENSE || MODE == CONV1_DENSE_MASK || MODE == CONV1_DYN) && BN == 256 &&
+        !PAIR;
 #ifndef LASNET_RESID_EPI_WARPS
 #define LASNET_RESID_EPI_WARPS 16
 #endif
@@ -711,6 +712,8 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                 mbar_wait(bar_tfull + 8 * acc, (lt >> 1) & 1);
                 tc_fence_after();
                 const int row0 = MODE == CONV2_GATHER ? mt * args.units_per_tile * args.S * args.S : mt * kBM;
+                // conv1 dyn: a halo pixel outside the image stores 0 (R6)
+                const bool zrow = MODE == CONV1_DYN && mt * kBM + r < M && halo_pixel(args, mt * kBM + r, M) < 0;
 #pragma unroll 1
                 for (int p = 0; p < NP; ++p) {
                     const int qp = NP * lt + p;  // pass counter: the buffer's use
@@ -731,8 +734,9 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                             uint32_t pk[4];
 #pragma unroll
                             for (int e = 0; e < 4; ++e) {
-                                const float lo = fmaxf(__uint_as_float(v[8 * q + 2 * e]) + bb[2 * e], 0.f);
-                                const float hi = fmaxf(__uint_as_float(v[8 * q + 2 * e + 1]) + bb[2 * e + 1], 0.f);
+                                float lo = fmaxf(__uint_as_float(v[8 * q + 2 * e]) + bb[2 * e], 0.f);
+                                float hi = fmaxf(__uint_as_float(v[8 * q + 2 * e + 1]) + bb[2 * e + 1], 0.f);
+                                if (zrow) lo = hi = 0.f;
                                 pk[e] = pack_bf16x2(lo, hi);
                             }
                             asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(saddr), "r"(pk[0]), "r"(pk[1]),
