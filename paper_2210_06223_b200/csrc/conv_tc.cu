@@ -84,7 +84,7 @@ template <int MODE, int BN, bool PAIR = false> struct Cfg {
     // in flight per SM)
     static constexpr bool kHalfStage =
         (MODE == CONV2_GATHER || MODE == CONV1_DENSE || MODE == CONV1_DENSE_MASK || MODE == CONV1_DYN) && BN == 256 &&
-        !PAIR;
+        !PAIR;  // (PROJ_SC measured: 7^2 shortcut 64 -> 54 us, 28^2 96 -> 116 us: not taken)
 #ifndef LASNET_RESID_EPI_WARPS
 #define LASNET_RESID_EPI_WARPS 16
 #endif
@@ -705,66 +705,6 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
             const int n0 = (tile - mt * geo.n_tiles_n) * BN;
             const int acc = lt & 1, b = lt % NSTG;
             const uint32_t sbuf = staging + b * C::kStagingBytes;
-            if constexpr (C::kHalfStage) {
-                // BN / CP passes of CP columns through the one staging buffer: pass p stages columns
-                // [CP p, CP p + CP) (warp: its 32 rows x CP / 2 columns) and TMA-stores them
-                constexpr int CP = 64 * C::kStagingChunks, NP = BN / CP;
-                mbar_wait(bar_tfull + 8 * acc, (lt >> 1) & 1);
-                tc_fence_after();
-                const int row0 = MODE == CONV2_GATHER ? mt * args.units_per_tile * args.S * args.S : mt * kBM;
-                // conv1 dyn: a halo pixel outside the image stores 0 (R6)
-                const bool zrow = MODE == CONV1_DYN && mt * kBM + r < M && halo_pixel(args, mt * kBM + r, M) < 0;
-#pragma unroll 1
-                for (int p = 0; p < NP; ++p) {
-                    const int qp = NP * lt + p;  // pass counter: the buffer's use
-                    mbar_wait(bar_sempty, (qp & 1) ^ 1);
-#pragma unroll 1
-                    for (int cc = 0; cc < CP / 2; cc += 32) {
-                        const int c = CP * p + (warp >> 2) * (CP / 2) + cc, hc = c - CP * p;
-                        uint32_t v[32];
-                        tmem_ld32(tmem_base + lane_base + acc * BN + c, v);
-                        tmem_ld_wait();
-                        const uint32_t rowbase = staging + (hc >> 6) * kChunkBytes + r * 128;
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const uint32_t saddr = rowbase + ((((hc & 63) >> 3) + q) ^ (r & 7)) * 16;
-                            const float4 b0 = __ldg(reinterpret_cast<const float4 *>(args.bias + n0 + c + 8 * q));
-                            const float4 b1 = __ldg(reinterpret_cast<const float4 *>(args.bias + n0 + c + 8 * q + 4));
-                            const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-                            uint32_t pk[4];
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                float lo = fmaxf(__uint_as_float(v[8 * q + 2 * e]) + bb[2 * e], 0.f);
-                                float hi = fmaxf(__uint_as_float(v[8 * q + 2 * e + 1]) + bb[2 * e + 1], 0.f);
-                                if (zrow) lo = hi = 0.f;
-                                pk[e] = pack_bf16x2(lo, hi);
-                            }
-                            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(saddr), "r"(pk[0]), "r"(pk[1]),
-                                         "r"(pk[2]), "r"(pk[3])
-                                         : "memory");
-                        }
-                    }
-                    if (p == NP - 1) {  // every TMEM read of this tile is done
-                        tc_fence_before();
-                        mbar_arrive(bar_tempty + 8 * acc);
-                    }
-                    fence_proxy_async_smem();
-                    named_bar_sync(1, EPI);
-                    if (tid == 0) {
-                        for (int c2 = 0; c2 < C::kStagingChunks; ++c2) {
-                            if (MODE == CONV2_GATHER)
-                                tma_store_2d(&args.tmap_out, staging + c2 * kChunkBytes, n0 + CP * p + 64 * c2, row0);
-                            else  // conv1: h1 [c_mid/64][rows][64]
-                                tma_store_3d(&args.tmap_out, staging + c2 * kChunkBytes, 0, mt * kBM,
-                                             ((n0 + CP * p) >> 6) + c2);
-                        }
-                        bulk_commit();
-                        bulk_wait_read<0>();  // the buffer is free once this store has read it
-                        mbar_arrive(bar_sempty);
-                    }
-                }
-                continue;
-            }
             bool zero = false;  // conv1: halo pixel outside the image stores 0 (R6)
             if (MODE == CONV1_DYN) zero = mt * kBM + r < M && halo_pixel(args, mt * kBM + r, M) < 0;
             bool relu = !args.no_relu;
@@ -792,6 +732,70 @@ __global__ void __launch_bounds__(threads_of<MODE, BN>(), 1) conv_tc_kernel(cons
                     const int cell = (n * args.Gh + args.fd_S.div(yy)) * args.Gw + args.fd_S.div(xx);
                     relu = __ldg(args.relu_mask + cell) == 0;
                 }
+            }
+            if constexpr (C::kHalfStage) {
+                // BN / CP passes of CP columns through the one staging buffer: pass p stages columns
+                // [CP p, CP p + CP) (warp: its 32 rows x CP / 2 columns) and TMA-stores them
+                constexpr int CP = 64 * C::kStagingChunks, NP = BN / CP;
+                mbar_wait(bar_tfull + 8 * acc, (lt >> 1) & 1);
+                tc_fence_after();
+                const int row0 = MODE == CONV2_GATHER ? mt * args.units_per_tile * args.S * args.S : mt * kBM;
+#pragma unroll 1
+                for (int p = 0; p < NP; ++p) {
+                    const int qp = NP * lt + p;  // pass counter: the buffer's use
+                    mbar_wait(bar_sempty, (qp & 1) ^ 1);
+#pragma unroll 1
+                    for (int cc = 0; cc < CP / 2; cc += 32) {
+                        const int c = CP * p + (warp >> 2) * (CP / 2) + cc, hc = c - CP * p;
+                        uint32_t v[32];
+                        tmem_ld32(tmem_base + lane_base + acc * BN + c, v);
+                        tmem_ld_wait();
+                        const uint32_t rowbase = staging + (hc >> 6) * kChunkBytes + r * 128;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const uint32_t saddr = rowbase + ((((hc & 63) >> 3) + q) ^ (r & 7)) * 16;
+                            const float4 b0 = __ldg(reinterpret_cast<const float4 *>(args.bias + n0 + c + 8 * q));
+                            const float4 b1 = __ldg(reinterpret_cast<const float4 *>(args.bias + n0 + c + 8 * q + 4));
+                            const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                            uint32_t pk[4];
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                float lo = __uint_as_float(v[8 * q + 2 * e]) + bb[2 * e];
+                                float hi = __uint_as_float(v[8 * q + 2 * e + 1]) + bb[2 * e + 1];
+                                if (relu) lo = fmaxf(lo, 0.f), hi = fmaxf(hi, 0.f);
+                                if (zero) lo = hi = 0.f;
+                                pk[e] = pack_bf16x2(lo, hi);
+                            }
+                            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(saddr), "r"(pk[0]), "r"(pk[1]),
+                                         "r"(pk[2]), "r"(pk[3])
+                                         : "memory");
+                        }
+                    }
+                    if (p == NP - 1) {  // every TMEM read of this tile is done
+                        tc_fence_before();
+                        mbar_arrive(bar_tempty + 8 * acc);
+                    }
+                    fence_proxy_async_smem();
+                    named_bar_sync(1, EPI);
+                    if (tid == 0) {
+                        for (int c2 = 0; c2 < C::kStagingChunks; ++c2) {
+                            const uint32_t src = staging + c2 * kChunkBytes;
+                            if (MODE == CONV2_GATHER || ((MODE == PROJ_SC) && !args.view4)) {
+                                tma_store_2d(&args.tmap_out, src, n0 + CP * p + 64 * c2, row0);
+                            } else if ((MODE == PROJ_SC)) {  // the 4-D output view of the dense tile
+                                int d2n, d2y, d2x;
+                                dense_tile_origin(args, mt, d2n, d2y, d2x);
+                                tma_store_4d(&args.tmap_out, src, n0 + CP * p + 64 * c2, d2x, d2y, d2n);
+                            } else {  // conv1: h1 [c_mid/64][rows][64]
+                                tma_store_3d(&args.tmap_out, src, 0, mt * kBM, ((n0 + CP * p) >> 6) + c2);
+                            }
+                        }
+                        bulk_commit();
+                        bulk_wait_read<0>();  // the buffer is free once this store has read it
+                        mbar_arrive(bar_sempty);
+                    }
+                }
+                continue;
             }
             int cell_ahead = -2;
             if (kResid) {
