@@ -125,12 +125,15 @@ template <int MODE, int BN, bool PAIR = false> struct Cfg {
     // of once per 128-column N tile, and each UMMA moves 96 instead of 128 smem bytes
     // per clock; 3 stages of 48 KB + one 64 KB staging tile
     static_assert(BN != 256 || !kResid, "BN = 256 only without the residual epilogue");
-    static constexpr int kStaging = BN == 256 ? 1 : (kGather ? 1 : (kResid ? 3 : 2));
+    // dense conv1 at 128 columns: 5 stages and one staging tile (more bytes in flight)
+    static constexpr bool kDeep128 = (MODE == CONV1_DENSE || MODE == CONV1_DENSE_MASK) && BN == 128 && !PAIR;
+    static constexpr int kStaging = BN == 256 || kDeep128 ? 1 : (kGather ? 1 : (kResid ? 3 : 2));
     // pairs: stages of 32 KB (BN 256) / 24 KB (BN 128) -> deeper rings in the same smem
     // stem: resident weights, 16 KB A-only stages
     static constexpr int kStages =
         MODE == STEM ? 6
         : kHalfStage ? 4
+        : kDeep128 ? 5
         : PAIR ? (BN == 256 ? 4 : (kResid ? 4 : 6))
                : (BN == 256 ? 3 : (kGather ? (BN == 128 ? 6 : 8) : (kResid ? 3 : (BN == 128 ? 4 : 6))));
     static constexpr int kTmemCols = 2 * BN;
