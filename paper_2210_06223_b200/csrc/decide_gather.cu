@@ -111,6 +111,14 @@ __device__ double cell_exact(const DecideArgs &a, int n, int y0, int x0, int ch,
 // cell's pixel rows j, j+4, ... in fp64, the quad combines them (fixed order).
 constexpr int kDecCells = kDecThreads / 4;  // cells per CTA (a multiple of 32)
 
+// the partials were written by the previous kernel (conv1) while this grid may already be resident
+// (programmatic dependent launch): read them at L2, never through the non-coherent path
+__device__ __forceinline__ float4 ld_cg_f4(const float4 *p) {
+    float4 v;
+    asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+
 __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -152,7 +160,7 @@ __global__ void __launch_bounds__(kDecThreads) decide_kernel(const DecideArgs a)
                 float4 v[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
-                    v[i] = p0 + i < cw ? __ldg(row + p0 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    v[i] = p0 + i < cw ? ld_cg_f4(row + p0 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     z += (double)v[i].x + (double)v[i].z;
