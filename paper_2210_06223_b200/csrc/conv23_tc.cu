@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(c23::kThreads, 1) conv23_kernel(const __grid_c
             if (i >= ntl) return -1;
             int t0, nv;
             dt.range(tile_of(i), t0, nv);
-            return lane < nv ? __ldg(args.idx + t0 + lane) : -1;
+            return lane < nv ? __ldcg(args.idx + t0 + lane) : -1;  // (written by the previous kernel)
         };
         int next = ids_of(0);
         for (int i = 0; i < ntl; ++i) {

@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(256) compact_gather_kernel(const GatherArgs a)
 
 // Compaction only (the direct schedule, no gather): one warp per 32-cell group
 // writes the ids of its active cells at the group's prefix.
-__global__ void __launch_bounds__(256) compact_idx_kernel(const uint8_t *__restrict__ dec, const int32_t *__restrict__ gpre,
+__global__ void __launch_bounds__(256) compact_idx_kernel(const uint8_t *dec, const int32_t *gpre,
                                                           int32_t *__restrict__ idx, int ncells, int ngroups) {
     pdl_wait();
     pdl_trigger();

@@ -130,7 +130,7 @@ __device__ __forceinline__ void warp_items_s(const T *__restrict__ x, const floa
                     const uint4 *pix = base + qy * rowpitch + (long)qx * (C / PV);
 #pragma unroll
                     for (int sl = 0; sl < SLOTS; ++sl)  // a partial last slot (nvec % 32) loads zeros
-                        q[i * SLOTS + sl] = (!wide || sl * 32 + vlane < mg.nvec) ? __ldg(pix + sl * 32)
+                        q[i * SLOTS + sl] = (!wide || sl * 32 + vlane < mg.nvec) ? __ldca(pix + sl * 32)
                                                                                   : make_uint4(0u, 0u, 0u, 0u);
                     ++np;
                 }
@@ -350,7 +350,7 @@ __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned lon
     return v;
 }
 
-__global__ void __launch_bounds__(kCompactThreads) compact_kernel(const uint8_t *__restrict__ mask, int ncells,
+__global__ void __launch_bounds__(kCompactThreads) compact_kernel(const uint8_t *mask, int ncells,
                                                                   int32_t *__restrict__ idx,
                                                                   int32_t *__restrict__ count,
                                                                   unsigned long long *status) {

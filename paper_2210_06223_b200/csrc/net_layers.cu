@@ -43,7 +43,7 @@ __device__ __forceinline__ uint4 max8(uint4 a, uint4 b) {
     return r;
 }
 
-__global__ void __launch_bounds__(256) maxpool_kernel(const uint4 *__restrict__ x, uint4 *__restrict__ y, int n_img,
+__global__ void __launch_bounds__(256) maxpool_kernel(const uint4 *x, uint4 *__restrict__ y, int n_img,
                                                       int Ho, int Wo, int vpp) {
     pdl_wait();
     pdl_trigger();
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(256) maxpool_kernel(const uint4 *__restrict__ 
             for (int dx = 0; dx < 5; ++dx) {
                 const int xx = 2 * ox - 1 + dx;
                 const bool ok = yy >= 0 && yy < Hi && xx >= 0 && xx < Wi;
-                q[dx] = ok ? __ldg(x + (((long)n * Hi + yy) * Wi + xx) * vpp + v) : ninf;
+                q[dx] = ok ? __ldca(x + (((long)n * Hi + yy) * Wi + xx) * vpp + v) : ninf;  // coherent (PDL)
             }
             const uint4 h0 = max8(max8(q[0], q[1]), q[2]), h1 = max8(max8(q[2], q[3]), q[4]);
             if (dy <= 2) {
@@ -101,7 +101,7 @@ cudaError_t launch_maxpool(const void *x, void *y, int n_img, int Ho, int Wo, in
 // warp + 8, ... (fp32 sums in pixel order), and the 8 partials are added in warp order
 // (fixed order), then / hw.  16-B loads coalesced along the channels.
 constexpr int kPoolGroups = 8;
-__global__ void __launch_bounds__(32 * kPoolGroups) avgpool_kernel(const __nv_bfloat16 *__restrict__ x,
+__global__ void __launch_bounds__(32 * kPoolGroups) avgpool_kernel(const __nv_bfloat16 *x,
                                                                    float *__restrict__ pooled, int n_img, int hw,
                                                                    int c) {
     pdl_wait();
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(32 * kPoolGroups) avgpool_kernel(const __nv_bf
         const uint4 *src = reinterpret_cast<const uint4 *>(x + n * hw * c) + v;
 #pragma unroll 4
         for (int p = pg; p < hw; p += kPoolGroups) {
-            const uint4 q = __ldg(src + (long)p * cv);
+            const uint4 q = __ldca(src + (long)p * cv);  // coherent: the previous kernel wrote x
             const uint32_t u[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -166,7 +166,7 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-__global__ void __launch_bounds__(32 * kFcSlices) fc_kernel(const float *__restrict__ pooled,
+__global__ void __launch_bounds__(32 * kFcSlices) fc_kernel(const float *pooled,
                                                             const __nv_bfloat16 *__restrict__ w,
                                                             const float *__restrict__ b, float *__restrict__ logits,
                                                             int n_img, int c, int classes) {
@@ -189,10 +189,11 @@ __global__ void __launch_bounds__(32 * kFcSlices) fc_kernel(const float *__restr
     for (int kk = kbeg; kk < kend; kk += 16) {
         const int ka = kk + 2 * t, kb = ka + 8;  // (c % 8 == 0: kb < c unless c % 16 == 8 at the tail)
         const float2 z = make_float2(0.f, 0.f);
-        const float2 x00 = __ldg(reinterpret_cast<const float2 *>(pa0 + ka));
-        const float2 x10 = __ldg(reinterpret_cast<const float2 *>(pa1 + ka));
-        const float2 x01 = kb < c ? __ldg(reinterpret_cast<const float2 *>(pa0 + kb)) : z;
-        const float2 x11 = kb < c ? __ldg(reinterpret_cast<const float2 *>(pa1 + kb)) : z;
+        // (the pooled features come from the previous kernel: coherent loads, PDL)
+        const float2 x00 = __ldcg(reinterpret_cast<const float2 *>(pa0 + ka));
+        const float2 x10 = __ldcg(reinterpret_cast<const float2 *>(pa1 + ka));
+        const float2 x01 = kb < c ? __ldcg(reinterpret_cast<const float2 *>(pa0 + kb)) : z;
+        const float2 x11 = kb < c ? __ldcg(reinterpret_cast<const float2 *>(pa1 + kb)) : z;
         uint32_t bw[4][2];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {

@@ -12,7 +12,7 @@
 
 namespace lasnet {
 
-__global__ void __launch_bounds__(256) subsample_kernel(const uint4 *__restrict__ in, uint4 *__restrict__ out, int n_img,
+__global__ void __launch_bounds__(256) subsample_kernel(const uint4 *in, uint4 *__restrict__ out, int n_img,
                                                         int Ho, int Wo, int vpp, int stride) {
     pdl_wait();
     pdl_trigger();

@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(kGcThreads, 2) gconv_kernel(const GconvArgs a)
         in_rows = np * a.hs * a.hs;
         if (a.direct)  // window origin (image, y, x) of each patch of the tile, from its cell id
             for (int p = threadIdx.x; p < np; p += kGcThreads) {
-                const int c = __ldg(a.idx + t0 + p), n = c / a.G, g = c - n * a.G, gy = g / a.Gw;
+                const int c = __ldcg(a.idx + t0 + p), n = c / a.G, g = c - n * a.G, gy = g / a.Gw;
                 s_pn[p] = n;
                 s_py[p] = gy * a.S - 1;
                 s_px[p] = (g - gy * a.Gw) * a.S - 1;
@@ -242,12 +242,12 @@ __global__ void __launch_bounds__(kSeThreads) se_kernel(const SeArgs a) {
             for (int r = rs; r < nrows; r += RS) {
                 if (a.count) {  // clipped edge cells: only in-image pixels
                     const int t = t0 + r / ss, j = r - (r / ss) * ss;
-                    const int cell = __ldg(a.idx + t) - n * a.G;
+                    const int cell = __ldcg(a.idx + t) - n * a.G;
                     const int gy = cell / a.Gw, gx = cell - gy * a.Gw;
                     const int py = j / a.S, px = j - py * a.S;
                     if (gy * a.S + py >= a.H || gx * a.S + px >= a.W) continue;
                 }
-                const uint4 q = __ldg(reinterpret_cast<const uint4 *>(a.h2 + (row0 + r) * a.C) + vv);
+                const uint4 q = __ldca(reinterpret_cast<const uint4 *>(a.h2 + (row0 + r) * a.C) + vv);  // (PDL)
                 const uint32_t u[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(kSeThreads) se_kernel(const SeArgs a) {
 // out[n][j] = act(b[j] + sum_k in[n][k] w[j][k]), act = ReLU (W1) or sigmoid (W2);
 // one CTA per 32 images x 32 outputs, K staged in 64-wide chunks, fixed-order sums.
 // Images without active cells (a dynamic block) are skipped (their scale is unused).
-__global__ void __launch_bounds__(256) se_fc_kernel(const float *__restrict__ in, const float *__restrict__ w,
+__global__ void __launch_bounds__(256) se_fc_kernel(const float *in, const float *__restrict__ w,
                                                     const float *__restrict__ b, float *__restrict__ out, int n_img,
                                                     int K, int N, int sigmoid_act) {
     pdl_wait();
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(256) se_apply_kernel(__nv_bfloat16 *h2, const 
     const int64_t total = (int64_t)rows * cv;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int r = (int)(i / cv), v = (int)(i - (int64_t)r * cv);
-        const int n = count ? __ldg(idx + r / ss) / G : r / HW;
+        const int n = count ? __ldcg(idx + r / ss) / G : r / HW;
         uint4 *p = reinterpret_cast<uint4 *>(h2 + (int64_t)r * C) + v;
         uint4 q = *p;
         uint32_t u[4] = {q.x, q.y, q.z, q.w};

@@ -281,11 +281,13 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t m, uint32_t n) {
 }
 
 // ---------------------------------------------------------------- misc -----
-// Read-only global load the compiler may not move across other volatile asm
-// (used to issue index loads early, ahead of a cp.async loop).
+// Global load at L2 (.cg) the compiler may not move across other volatile asm (used to issue
+// index loads early, ahead of a cp.async loop).  Never the non-coherent path: with programmatic
+// dependent launch a kernel's lifetime overlaps its predecessor's, which may still be writing the
+// data (the ids), so the read-only premise of ld.global.nc does not hold.
 __device__ __forceinline__ int ld_nc_volatile(const int *p) {
     int v;
-    asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    asm volatile("ld.global.cg.b32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
 }
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
