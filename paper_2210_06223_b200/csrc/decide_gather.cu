@@ -125,86 +125,92 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
     return v;
 }
 
-// COOP (all CTAs co-resident; the direct schedule): after the decisions a grid
-// barrier, then every CTA sums the group counts before its own and writes the
-// ids of its active cells -- no last-CTA scan and no second launch.
+// COOP (all CTAs co-resident; the direct schedule): a CTA decides the 64-cell chunks
+// blockIdx.x, blockIdx.x + gridDim.x, ... (the grid is capped at the co-residency
+// capacity, so large maps take several chunks per CTA), then a grid barrier, then
+// for each of its chunks it sums the group counts before the chunk and writes the ids
+// of its active cells -- no last-CTA scan and no second launch.  !COOP: one chunk per
+// CTA, the last CTA to finish turns the group counts into prefixes (ids by a second launch).
 template <bool COOP>
 __global__ void __launch_bounds__(kDecThreads) decide_kernel(const DecideArgs a) {
     __shared__ int s_unc[kDecCells], s_nunc;
     __shared__ uint8_t s_dec[kDecCells];
     __shared__ int s_last;
+    __shared__ double s_red[kDecThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = a.Gh * a.Gw;
-    const int cell0 = blockIdx.x * kDecCells;
     const int lc = tid >> 2, q = tid & 3;  // local cell, lane in the quad
+    const int nchunks = (a.ncells + kDecCells - 1) / kDecCells;
     pdl_wait();
     pdl_trigger();
-    if (tid == 0) s_nunc = 0;
-    __syncthreads();
+    for (int chunk = blockIdx.x; chunk < (COOP ? nchunks : (int)blockIdx.x + 1); chunk += gridDim.x) {
+        const int cell0 = chunk * kDecCells;
+        if (tid == 0) s_nunc = 0;
+        __syncthreads();
 
-    // certified decision per cell from the fused conv1's partials
-    const int cell = cell0 + lc;
-    const bool valid = cell < a.ncells;
-    int n = 0, y0 = 0, x0 = 0, ch = 0, cw = 0;
-    double z = 0.0, m = 0.0;
-    if (valid) {
-        n = cell / G;
-        const int g = cell - n * G, gy = g / a.Gw, gx = g - gy * a.Gw;
-        y0 = gy * a.S;
-        x0 = gx * a.S;
-        ch = min(y0 + a.S, a.H) - y0;
-        cw = min(x0 + a.S, a.W) - x0;
-        for (int py = q; py < ch; py += 4) {  // rows q, q + 4, ...: a row's loads in flight first
-            const float4 *row = a.mpart + (size_t)(n * a.H + y0 + py) * a.W + x0;
-            for (int p0 = 0; p0 < cw; p0 += 8) {
-                float4 v[8];
+        // certified decision per cell from the fused conv1's partials
+        const int cell = cell0 + lc;
+        const bool valid = cell < a.ncells;
+        int n = 0, y0 = 0, x0 = 0, ch = 0, cw = 0;
+        double z = 0.0, m = 0.0;
+        if (valid) {
+            n = cell / G;
+            const int g = cell - n * G, gy = g / a.Gw, gx = g - gy * a.Gw;
+            y0 = gy * a.S;
+            x0 = gx * a.S;
+            ch = min(y0 + a.S, a.H) - y0;
+            cw = min(x0 + a.S, a.W) - x0;
+            for (int py = q; py < ch; py += 4) {  // rows q, q + 4, ...: a row's loads in flight first
+                const float4 *row = a.mpart + (size_t)(n * a.H + y0 + py) * a.W + x0;
+                for (int p0 = 0; p0 < cw; p0 += 8) {
+                    float4 v[8];
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    v[i] = p0 + i < cw ? ld_cg_f4(row + p0 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (int i = 0; i < 8; ++i)
+                        v[i] = p0 + i < cw ? ld_cg_f4(row + p0 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    z += (double)v[i].x + (double)v[i].z;
-                    m += (double)v[i].y + (double)v[i].w;
+                    for (int i = 0; i < 8; ++i) {
+                        z += (double)v[i].x + (double)v[i].z;
+                        m += (double)v[i].y + (double)v[i].w;
+                    }
                 }
             }
         }
-    }
-    z += __shfl_xor_sync(0xffffffffu, z, 1);
-    m += __shfl_xor_sync(0xffffffffu, m, 1);
-    z += __shfl_xor_sync(0xffffffffu, z, 2);
-    m += __shfl_xor_sync(0xffffffffu, m, 2);
-    int dec = 0;
-    if (valid && q == 0) {
-        const double u32 = 5.9604644775390625e-8, u64 = 1.1102230246251565e-16;  // 2^-24, 2^-53
-        const double n32 = (double)(a.c_in / 16 + 10), n64 = (double)(2 * ch * cw + 4);
-        const double gam = n32 * u32 / (1.0 - n32 * u32) + n64 * u64 / (1.0 - n64 * u64);
-        // m_p are fp32 sums (relative error <= c_in 2^-24 < 1e-3 for c_in < 16k): x1.01
-        const double err = m * 1.01 * gam + 1e-300;
-        z += (double)a.bm * (double)(ch * cw);
-        if (fabs(z) > err) dec = z > 0.0;
-        else s_unc[atomicAdd(&s_nunc, 1)] = lc;
-        s_dec[lc] = (uint8_t)dec;
-    }
-    __syncthreads();
-    // fp64 re-sum of the undecided cells (rare), each by the whole CTA: one
-    // load round trip per 1024 vectors instead of a warp's serial pixel loop
-    __shared__ double s_red[kDecThreads / 32];
-    for (int k = 0; k < s_nunc; ++k) {
-        const int t = s_unc[k], c = cell0 + t;
-        const int cn = c / G, g = c - cn * G, gy = g / a.Gw, gx = g - gy * a.Gw;
-        const int cy0 = gy * a.S, cx0 = gx * a.S;
-        const int cch = min(cy0 + a.S, a.H) - cy0, ccw = min(cx0 + a.S, a.W) - cx0;
-        const double sum = cell_exact(a, cn, cy0, cx0, cch, ccw, s_red);
-        if (tid == 0) s_dec[t] = (sum / (double)(cch * ccw) + (double)a.bm) > 0.0;
-    }
-    __syncthreads();
-    // decisions out, one count per 32-cell group (warps 0 .. kDecCells/32 - 1)
-    if (tid < kDecCells) {
-        const int c = cell0 + tid;
-        const int d = c < a.ncells ? s_dec[tid] : 0;
-        if (c < a.ncells) a.dec[c] = (uint8_t)d;
-        const unsigned bal = __ballot_sync(0xffffffffu, d);
-        if (lane == 0 && cell0 / 32 + warp < a.ngroups) a.gpre[cell0 / 32 + warp] = __popc(bal);
+        z += __shfl_xor_sync(0xffffffffu, z, 1);
+        m += __shfl_xor_sync(0xffffffffu, m, 1);
+        z += __shfl_xor_sync(0xffffffffu, z, 2);
+        m += __shfl_xor_sync(0xffffffffu, m, 2);
+        if (valid && q == 0) {
+            const double u32 = 5.9604644775390625e-8, u64 = 1.1102230246251565e-16;  // 2^-24, 2^-53
+            const double n32 = (double)(a.c_in / 16 + 10), n64 = (double)(2 * ch * cw + 4);
+            const double gam = n32 * u32 / (1.0 - n32 * u32) + n64 * u64 / (1.0 - n64 * u64);
+            // m_p are fp32 sums (relative error <= c_in 2^-24 < 1e-3 for c_in < 16k): x1.01
+            const double err = m * 1.01 * gam + 1e-300;
+            z += (double)a.bm * (double)(ch * cw);
+            int dec = 0;
+            if (fabs(z) > err) dec = z > 0.0;
+            else s_unc[atomicAdd(&s_nunc, 1)] = lc;
+            s_dec[lc] = (uint8_t)dec;
+        }
+        __syncthreads();
+        // fp64 re-sum of the undecided cells (rare), each by the whole CTA: one
+        // load round trip per 1024 vectors instead of a warp's serial pixel loop
+        for (int k = 0; k < s_nunc; ++k) {
+            const int t = s_unc[k], c = cell0 + t;
+            const int cn = c / G, g = c - cn * G, gy = g / a.Gw, gx = g - gy * a.Gw;
+            const int cy0 = gy * a.S, cx0 = gx * a.S;
+            const int cch = min(cy0 + a.S, a.H) - cy0, ccw = min(cx0 + a.S, a.W) - cx0;
+            const double sum = cell_exact(a, cn, cy0, cx0, cch, ccw, s_red);
+            if (tid == 0) s_dec[t] = (sum / (double)(cch * ccw) + (double)a.bm) > 0.0;
+        }
+        __syncthreads();
+        // decisions out, one count per 32-cell group (warps 0 .. kDecCells/32 - 1)
+        if (tid < kDecCells) {
+            const int c = cell0 + tid;
+            const int d = c < a.ncells ? s_dec[tid] : 0;
+            if (c < a.ncells) a.dec[c] = (uint8_t)d;
+            const unsigned bal = __ballot_sync(0xffffffffu, d);
+            if (lane == 0 && cell0 / 32 + warp < a.ngroups) a.gpre[cell0 / 32 + warp] = __popc(bal);
+        }
     }
 
     if constexpr (COOP) {
@@ -221,41 +227,44 @@ __global__ void __launch_bounds__(kDecThreads) decide_kernel(const DecideArgs a)
             }
         }
         __syncthreads();
-        // this CTA's base: the active cells of all groups before its first one
         __shared__ int s_part[kDecThreads / 32], s_wcnt[kDecCells / 32];
-        const int g0 = cell0 / 32;
-        int part = 0;
-        for (int g = tid; g < g0; g += kDecThreads) {
-            int v;
-            asm volatile("ld.global.cg.b32 %0, [%1];" : "=r"(v) : "l"(a.gpre + g));
-            part += v;
-        }
+        for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
+            // the chunk's base: the active cells of all groups before its first one
+            const int cell0 = chunk * kDecCells, g0 = cell0 / 32;
+            int part = 0;
+            for (int g = tid; g < g0; g += kDecThreads) {
+                int v;
+                asm volatile("ld.global.cg.b32 %0, [%1];" : "=r"(v) : "l"(a.gpre + g));
+                part += v;
+            }
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
-        if (lane == 0) s_part[warp] = part;
-        int d = 0;
-        unsigned bal = 0u;
-        if (tid < kDecCells) {
-            d = cell0 + tid < a.ncells ? s_dec[tid] : 0;
-            bal = __ballot_sync(0xffffffffu, d);
-            if (lane == 0) s_wcnt[warp] = __popc(bal);
-        }
-        __syncthreads();
-        int base = 0;
+            for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+            if (lane == 0) s_part[warp] = part;
+            int d = 0;
+            unsigned bal = 0u;
+            if (tid < kDecCells) {  // this CTA's own decisions of the chunk (written above)
+                d = cell0 + tid < a.ncells ? a.dec[cell0 + tid] : 0;
+                bal = __ballot_sync(0xffffffffu, d);
+                if (lane == 0) s_wcnt[warp] = __popc(bal);
+            }
+            __syncthreads();
+            int base = 0;
 #pragma unroll
-        for (int w = 0; w < kDecThreads / 32; ++w) base += s_part[w];
-        if (tid < kDecCells) {
-            int off = base;
-            for (int w = 0; w < warp; ++w) off += s_wcnt[w];
-            if (d) a.idx[off + __popc(bal & ((1u << lane) - 1u))] = cell0 + tid;
-            // exclusive group prefixes for the gather (a separate array: other CTAs may
-            // still be summing the counts)
-            if (lane == 0 && g0 + warp < a.ngroups) a.gpx[g0 + warp] = off;
-        }
-        if (tid == 0 && blockIdx.x == gridDim.x - 1) {
-            int tot = base;
-            for (int w = 0; w < kDecCells / 32; ++w) tot += s_wcnt[w];
-            *a.count = tot;
+            for (int w = 0; w < kDecThreads / 32; ++w) base += s_part[w];
+            if (tid < kDecCells) {
+                int off = base;
+                for (int w = 0; w < warp; ++w) off += s_wcnt[w];
+                if (d) a.idx[off + __popc(bal & ((1u << lane) - 1u))] = cell0 + tid;
+                // exclusive group prefixes for the gather (a separate array: other CTAs may
+                // still be summing the counts)
+                if (lane == 0 && g0 + warp < a.ngroups) a.gpx[g0 + warp] = off;
+            }
+            if (tid == 0 && chunk == nchunks - 1) {
+                int tot = base;
+                for (int w = 0; w < kDecCells / 32; ++w) tot += s_wcnt[w];
+                *a.count = tot;
+            }
+            __syncthreads();  // s_part / s_wcnt are reused by the next chunk
         }
         return;
     }
@@ -451,10 +460,11 @@ cudaError_t launch_decide_gather(const float4 *mpart, const void *x, const float
         coop_cap = coop_cap_dev[dev] > 0 ? coop_cap_dev[dev] : 0;
     }
     a.gpx = a.gpre + a.ngroups;
-    bool coop = h1d != nullptr && grid <= coop_cap;
+    // the cooperative grid is capped at the co-residency capacity (a CTA then takes several chunks)
+    bool coop = h1d != nullptr && coop_cap > 0;
     cudaError_t e = cudaErrorUnknown;
     if (coop) {
-        e = launch_k_coop(decide_kernel<true>, dim3(grid), dim3(kDecThreads), 0, st, a);
+        e = launch_k_coop(decide_kernel<true>, dim3(grid < coop_cap ? grid : coop_cap), dim3(kDecThreads), 0, st, a);
         if (e == cudaErrorCooperativeLaunchTooLarge) {  // not co-resident now: the two-launch form
             (void)cudaGetLastError();
             coop = false;
