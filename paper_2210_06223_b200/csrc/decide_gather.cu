@@ -7,7 +7,7 @@
 // (conv_tc.cu, CONV1_DENSE_MASK) leaves per pixel p, for the lower (h = 0) and the
 // upper (h = 1) 32 channels of every 64-channel K-block, the fp32 partials
 //   a_ph = sum_c wm_c x[p,c]   and   m_ph = sum_c |wm_c x[p,c]|,
-// and two launches finish steps 1-2 and the gather:
+// and one cooperative launch finishes steps 1-2 (a second one the gathered copy, when used):
 //   (a) decides each cell (P:109 avg-pool + 1x1 conv, P:562 sign form):
 //       z = sum_{p in Omega} (a_p0 + a_p1) + bm*|Omega| in fp64.  With gamma_n =
 //       n u/(1-n u) (Higham, recursive summation): every channel term of a_ph
@@ -19,9 +19,13 @@
 //       When |z| exceeds that bound the sign is the exact sign; otherwise (~1e-5
 //       of the cells) the cell is re-summed from x in fp64 (exact products) --
 //       the rule of the standalone masker (R20).
-//       decide_kernel, one thread per cell: writes the mask and the active count of
-//       every 32-cell group; the last CTA to finish (done counter) turns the
-//       group counts into exclusive prefixes and writes the total count.
+//       decide_kernel<true>, four lanes per cell, 64-cell chunks (a CTA takes several
+//       when the map has more chunks than the grid can hold co-resident): writes the
+//       mask and the active count of every 32-cell group, then after a software grid
+//       barrier (cooperative launch) each chunk sums the counts before it and writes
+//       its ids (ascending) and group prefixes; the last chunk writes the count.
+//       (decide_kernel<false>, the fallback: one chunk per CTA, the last CTA to finish
+//       turns the counts into prefixes; compact_idx_kernel writes the ids.)
 //   (b) compact_gather_kernel, one warp per (group, 64-channel chunk, halo row):
 //       the group's active cells get positions prefix + ballot rank (ascending
 //       cell ids, App. B: idx/count), and the warp copies that halo row
