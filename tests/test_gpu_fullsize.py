@@ -133,3 +133,19 @@ def test_stage3_wide_pairs_many_rounds():
         want = np.concatenate(list(ex.map(lambda i: oracle.static_block(xsd[i:i + 1], wd, rmode=oracle.ROUND_BF16),
                                           range(nd))))
     assert max_abs_rel(synth.to_f64(yd.cpu()), want) <= BF16_TOL
+
+
+def test_fused_decide_more_chunks_than_coresident_ctas():
+    """The cooperative decide caps its grid at the co-residency capacity (4 CTAs of 256
+    threads per SM: 592 on 148 SMs) and a CTA then decides several 64-cell chunks: the
+    LAS-R101 56^2 stage has 784 chunks.  N = 64 at 56x56, S = 2 (50 176 cells, 784
+    chunks) through the fused schedule: mask / idx / count bit-exact, every element vs
+    the oracle."""
+    n, h, w, c_in, c_mid, s = 64, 56, 56, 64, 64, 2
+    x, wts, wm = make_case(n, h, w, c_in, c_mid, s, seed=880)
+    xd = synth.to_f64(x)
+    _, l0 = oracle.masker(xd, synth.to_f64(wm), 0.0, s)
+    bm = margin_bias(l0, 0.5)
+    y, m, idx, count = L.block_forward(x.cuda(), to_dev(wts), wm.cuda(), bm, s, L.SCHED_FUSED)
+    assert (n * (h // s) * (w // s) + 63) // 64 > 4 * 148, "must exceed the co-resident grid"
+    _check_block(x, wts, wm, bm, s, y.cpu(), m.cpu().numpy(), idx.cpu().numpy(), int(count.item()))
