@@ -140,7 +140,8 @@ __global__ void __launch_bounds__(32 * kPoolGroups) avgpool_kernel(const __nv_bf
 // Head, pass 2: logits[n][k] = b[k] + sum_c pooled[n][c] w[k][c] on the tensor cores
 // (mma.sync m16n8k16, bf16 x bf16 -> fp32).  The fp32 pooled operand is split into three
 // bf16 terms, p = p0 + p1 + p2 (p0 = RNE_bf16(p), p1 = RNE_bf16(p - p0), p2 = RNE_bf16(p - p0 - p1):
-// 3 x 8 significand bits cover fp32's 24), and the bf16 x bf16 products are exact in fp32,
+// 3 x 8 significand bits cover fp32's 24: exact for |p| >= 2^-110, absolute error < 2^-133 below;
+// tests/test_head_split.py), and the bf16 x bf16 products are exact in fp32,
 // so the three MMAs over the same bf16 weights see the fp32 operand; only the fp32
 // accumulation order differs from a scalar loop.  CTA = 16 images x 32 classes, its four
 // warps take four K slices (each warp: 16 x 32 as four n8 blocks), and the slice partials
