@@ -210,24 +210,38 @@ __global__ void __launch_bounds__(kSeThreads) se_kernel(const SeArgs a) {
     const int n = blockIdx.x;
     int t0 = 0, t1 = 0;
     if (a.count) {
-        if (threadIdx.x == 0) {
-            const int cnt = *a.count;
-            int lo = 0, hi = cnt;  // first patch of image n
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (a.idx[mid] / a.G < n) lo = mid + 1; else hi = mid;
-            }
-            int lo2 = lo, hi2 = cnt;  // first patch of image n + 1
-            while (lo2 < hi2) {
-                const int mid = (lo2 + hi2) >> 1;
-                if (a.idx[mid] / a.G < n + 1) lo2 = mid + 1; else hi2 = mid;
-            }
-            range[0] = lo;
-            range[1] = lo2;
+        // the image's patches [t0, t1) in the ascending ids: the first id of image >= n and >= n + 1,
+        // found by the whole CTA in two probe rounds (256 evenly spaced positions, then every
+        // position between the two bracketing probes) instead of a one-thread binary search
+        // (~28 dependent L2 round trips)
+        __shared__ int s_lo[2], s_hi[2];
+        const int cnt = __ldcg(a.count);
+        if (threadIdx.x < 2) {
+            s_lo[threadIdx.x] = 0;
+            s_hi[threadIdx.x] = cnt;
         }
         __syncthreads();
-        t0 = range[0];
-        t1 = range[1];
+        {
+            const long p = (long)cnt * threadIdx.x / kSeThreads;  // round 1: evenly spaced probes
+            const int img = p < cnt ? __ldcg(a.idx + p) / a.G : 0x7fffffff;
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+                if (p < cnt && img < n + b) atomicMax(&s_lo[b], (int)p);  // last probe below the bound
+                if (p < cnt && img >= n + b) atomicMin(&s_hi[b], (int)p);  // first probe at or above it
+            }
+        }
+        __syncthreads();
+        __shared__ int s_first[2];
+        if (threadIdx.x < 2) s_first[threadIdx.x] = s_hi[threadIdx.x];
+        __syncthreads();
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {  // round 2: every position of the bracket (< cnt / 256 + 1 of them)
+            for (int p = s_lo[b] + (int)threadIdx.x; p < s_hi[b]; p += kSeThreads)
+                if (__ldcg(a.idx + p) / a.G >= n + b) atomicMin(&s_first[b], p);
+        }
+        __syncthreads();
+        t0 = s_first[0];
+        t1 = s_first[1];
         if (t0 == t1) return;  // no active cell: the block leaves the image untouched
     }
     const int ss = a.S * a.S;
@@ -239,22 +253,44 @@ __global__ void __launch_bounds__(kSeThreads) se_kernel(const SeArgs a) {
         for (int vv = v; vv < cv; vv += (RS == 1 ? kSeThreads : cv)) {
             float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
             int cntp = 0;
-            for (int r = rs; r < nrows; r += RS) {
-                if (a.count) {  // clipped edge cells: only in-image pixels
-                    const int t = t0 + r / ss, j = r - (r / ss) * ss;
-                    const int cell = __ldcg(a.idx + t) - n * a.G;
-                    const int gy = cell / a.Gw, gx = cell - gy * a.Gw;
-                    const int py = j / a.S, px = j - py * a.S;
-                    if (gy * a.S + py >= a.H || gx * a.S + px >= a.W) continue;
-                }
-                const uint4 q = __ldca(reinterpret_cast<const uint4 *>(a.h2 + (row0 + r) * a.C) + vv);  // (PDL)
-                const uint32_t u[4] = {q.x, q.y, q.z, q.w};
+            // the thread's rows r = rs, rs + RS, ... eight at a time: their id loads, then their
+            // h2 loads, are in flight together (one round trip each per 8 rows instead of per
+            // row); the sums still run in row order (bitwise the row-by-row loop)
+            constexpr int kU = 8;
+            for (int rb = rs; rb < nrows; rb += kU * RS) {
+                bool ok[kU];
+                int cellv[kU];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    acc[2 * e] += __uint_as_float(u[e] << 16);
-                    acc[2 * e + 1] += __uint_as_float(u[e] & 0xffff0000u);
+                for (int k = 0; k < kU; ++k) {
+                    const int r = rb + k * RS;
+                    ok[k] = r < nrows;
+                    cellv[k] = 0;
+                    if (a.count && ok[k]) cellv[k] = __ldcg(a.idx + t0 + r / ss);
                 }
-                ++cntp;
+                uint4 q[kU];
+#pragma unroll
+                for (int k = 0; k < kU; ++k) {
+                    const int r = rb + k * RS;
+                    if (a.count && ok[k]) {  // clipped edge cells: only in-image pixels
+                        const int j = r - (r / ss) * ss, cell = cellv[k] - n * a.G;
+                        const int gy = cell / a.Gw, gx = cell - gy * a.Gw;
+                        const int py = j / a.S, px = j - py * a.S;
+                        ok[k] = gy * a.S + py < a.H && gx * a.S + px < a.W;
+                    }
+                    q[k] = ok[k] ? __ldca(reinterpret_cast<const uint4 *>(a.h2 + (row0 + r) * a.C) + vv)  // (PDL)
+                                 : make_uint4(0u, 0u, 0u, 0u);
+                }
+#pragma unroll
+                for (int k = 0; k < kU; ++k) {
+                    if (!ok[k]) continue;
+                    const uint32_t u[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        acc[2 * e] += __uint_as_float(u[e] << 16);
+                        acc[2 * e + 1] += __uint_as_float(u[e] & 0xffff0000u);
+                    }
+                    ++cntp;
+                }
             }
 #pragma unroll
             for (int e = 0; e < 8; ++e) part[rs * a.C + 8 * vv + e] = acc[e];
