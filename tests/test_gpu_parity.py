@@ -781,3 +781,21 @@ def test_small_block_matches_oracle(n, h, w, c, c_mid, s, r):
     assert L.last_launch_count() == 1
     wdense = oracle.static_block(xd, synth.weights_f64(wts), rmode=oracle.ROUND_F32)
     assert max_abs_rel(synth.to_f64(yd.cpu()), wdense) <= 1e-5
+
+
+def test_maxpool_odd_output_and_head_ragged_shapes():
+    """The 2 x 2-block max pool at odd output sizes (a block's second row / column past the
+    edge), exact vs the oracle; the tensor-core head at ragged shapes (images not a multiple of
+    16, classes not a multiple of 32, c % 16 == 8: the last K-step half-empty) within 1e-4."""
+    g = torch.Generator().manual_seed(77)
+    for (n, ho, wo, c) in [(1, 7, 9, 64), (3, 5, 3, 16), (2, 1, 1, 8)]:
+        x = torch.randn((n, 2 * ho, 2 * wo, c), generator=g).to(torch.bfloat16)
+        got = synth.to_f64(L.maxpool(x.cuda()).cpu())
+        assert np.array_equal(got, oracle.maxpool(synth.to_f64(x))), (n, ho, wo, c)
+    for (n, hw, c, classes) in [(5, 9, 72, 37), (17, 4, 24, 100), (1, 1, 8, 1)]:
+        x = torch.randn((n, hw, 1, c), generator=g).abs().to(torch.bfloat16)
+        wf = (torch.randn((classes, c), generator=g) * 0.1).to(torch.bfloat16)
+        bf = (torch.randn((classes,), generator=g) * 0.1).float()
+        lg = L.head(x.cuda(), wf.cuda(), bf.cuda()).cpu().numpy()
+        want = oracle.head(synth.to_f64(x), synth.to_f64(wf), synth.to_f64(bf))
+        assert np.abs(lg - want).max() <= 1e-4 * max(1.0, np.abs(want).max()), (n, hw, c, classes)
